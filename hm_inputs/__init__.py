@@ -1,0 +1,284 @@
+"""Seeded synthetic inputs for the HODLR / HSS matvec (BASELINE.json configs 1-5).
+
+This module serves BOTH sides — the oracle (tests) and the CUDA path (tests,
+bench) — and therefore holds none of the method's arithmetic: it only draws
+random generators with the shapes/distributions of DESIGN.md §4 and fills the
+closed-form inverse-Laplacian generators (integer products plus one IEEE
+division, bit-identical on any IEEE machine). It imports neither ``oracle``
+nor ``paper_1909_07909_b200``.
+
+Layouts (same as include/hm.h): row-major fp64;
+  HODLR  D [2^p][b][b], U/V level-major [sum_l n*k_l] (level l = 1..p, [n][k_l]);
+  HSS    D [2^p][b][b], U/V [n][k], R/W [2^p-2][2k][k], B [2^p-1][2][k][k].
+
+Randomness: numpy's counter-based Philox bit generator, one independent stream
+per (master seed, config id, array id, block id), so any block (a leaf, a row
+slab of a level) can be drawn on its own — a rank can generate just its shard.
+Array ids: X=0, D=1, U=2, V=3, R=4, W=5, B=6.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Sequence, Tuple
+
+import numpy as np
+
+MASTER_SEED = 190907909  # fixed and recorded in the bench output
+AID = {"X": 0, "D": 1, "U": 2, "V": 3, "R": 4, "W": 5, "B": 6}
+
+
+@dataclass(frozen=True)
+class Config:
+    """One BASELINE.json config (index 1..5), with the readings of DESIGN.md §3."""
+
+    cid: int
+    fmt: str  # "hodlr" | "hss"
+    n: int
+    leaf: int
+    levels: int
+    k: int
+    nrhs: Tuple[int, ...]
+    laplacian: bool = False
+    gpus: Tuple[int, ...] = (1,)
+
+    @property
+    def nleaves(self) -> int:
+        return 1 << self.levels
+
+
+CONFIGS: Dict[int, Config] = {
+    1: Config(1, "hodlr", 1024, 64, 4, 8, (1,)),
+    2: Config(2, "hss", 4096, 64, 6, 16, (16,)),
+    3: Config(3, "hodlr", 1 << 20, 256, 12, 16, (1, 8, 64)),
+    4: Config(4, "hss", 1 << 22, 128, 15, 32, (32,), gpus=(1, 2, 4, 8)),
+    5: Config(5, "hodlr", 1 << 24, 256, 16, 1, (1,), laplacian=True, gpus=(1, 2, 4, 8)),
+}
+
+
+def _rng(seed: int, cid: int, aid: int, block: int) -> np.random.Generator:
+    key = np.array([(seed & 0xFFFFFFFF) | ((cid & 0xFFFF) << 32), (aid << 48) | (block & ((1 << 48) - 1))],
+                   dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def normal(shape, seed: int, cid: int, aid: int, block: int = 0) -> np.ndarray:
+    """iid N(0,1) fp64 of the given shape from stream (seed, cid, aid, block)."""
+    return _rng(seed, cid, aid, block).standard_normal(size=shape, dtype=np.float64)
+
+
+def _orth_blocks(G: np.ndarray) -> np.ndarray:
+    """Thin-QR Q factor of each block of a stack [N][r][k] (SURVEY G8/G10:
+    'Gaussian orthonormalised (QR)'). Any Householder QR; Q is fixed once drawn."""
+    q, _ = np.linalg.qr(G, mode="reduced")
+    return np.ascontiguousarray(q)
+
+
+# ----------------------------------------------------------------- HODLR --
+
+@dataclass
+class Hodlr:
+    n: int
+    levels: int
+    leaf: int
+    ranks: np.ndarray  # int32 [levels]
+    D: np.ndarray
+    U: np.ndarray
+    V: np.ndarray
+
+    def level_slice(self, l: int) -> slice:
+        off = int(self.n * int(self.ranks[: l - 1].sum()))
+        return slice(off, off + self.n * int(self.ranks[l - 1]))
+
+
+def hodlr_random(n: int, levels: int, ranks: Sequence[int], seed: int = MASTER_SEED, cid: int = 0,
+                 rows: Optional[Tuple[int, int]] = None) -> Hodlr:
+    """Random HODLR generators (configs 1 and 3; reading G7): D_i iid N(0,1)/sqrt(b),
+    U_l, V_l iid N(0,1)/sqrt(s_l), s_l = n/2^l. If ``rows`` = (r0, r1) (aligned to
+    leaves) only that row slab is drawn — a rank's shard; the full-array draw is the
+    concatenation of the shards for any split."""
+    b = n >> levels
+    assert b << levels == n, "uniform tree: n = leaf * 2^levels"
+    ranks = np.asarray(ranks if levels > 0 else [], dtype=np.int32).reshape(levels)
+    r0, r1 = rows if rows is not None else (0, n)
+    assert r0 % b == 0 and r1 % b == 0
+    leaves = range(r0 // b, r1 // b)
+    D = np.empty((len(leaves), b, b), dtype=np.float64)
+    for t, i in enumerate(leaves):
+        D[t] = normal((b, b), seed, cid, AID["D"], i) / np.sqrt(b)
+    U = np.empty(((r1 - r0) * int(ranks.sum()),), dtype=np.float64)
+    V = np.empty_like(U)
+    off = 0
+    for l in range(1, levels + 1):
+        k = int(ranks[l - 1])
+        s = n >> l
+        # one stream per (level, leaf-sized slab) so shards are independent
+        for name, dst in (("U", U), ("V", V)):
+            blk = dst[off: off + (r1 - r0) * k].reshape(r1 - r0, k)
+            for i in leaves:
+                blk[(i * b - r0):(i * b - r0 + b)] = normal((b, k), seed, cid, AID[name], (l << 40) | i) / np.sqrt(s)
+        off += (r1 - r0) * k
+    return Hodlr(n, levels, b, ranks, D.reshape(-1), U, V)
+
+
+def hodlr_inverse_laplacian(n: int, levels: int, rows: Optional[Tuple[int, int]] = None, xp=np,
+                            device=None) -> Hodlr:
+    """Exact HODLR form (rank 1 on every level) of A = tridiag(-1,2,-1)^{-1},
+    A_ij = min(i,j)(n+1-max(i,j))/(n+1), 1-based (BASELINE.json config 5; reading G11).
+    Upper block (i<j): u_i = i, v_j = (n+1-j)/(n+1); lower block (i>j): u_i = n+1-i,
+    v_j = j/(n+1). Every entry is an exact integer product (< 2^53) then at most one
+    correctly rounded division, so numpy and torch (CPU or CUDA) agree bit for bit.
+    ``xp`` may be numpy or torch (then ``device`` applies)."""
+    b = n >> levels
+    assert b << levels == n
+    r0, r1 = rows if rows is not None else (0, n)
+    nl = (r1 - r0) // b
+    kw = {} if xp is np else {"device": device}
+    f64 = xp.float64
+    i64 = xp.int64
+    np1 = n + 1
+    g = xp.arange(r0 + 1, r1 + 1, dtype=i64, **kw)  # 1-based global rows
+    # D_i[r][c] = min(gr,gc)(n+1-max(gr,gc))/(n+1)
+    gl = g.reshape(nl, b)
+    gr = gl[:, :, None]
+    gc = gl[:, None, :]
+    if xp is np:
+        mn, mx = np.minimum(gr, gc), np.maximum(gr, gc)
+    else:
+        mn, mx = xp.minimum(gr, gc), xp.maximum(gr, gc)
+    D = (mn * (np1 - mx)).to(f64) / np1 if xp is not np else (mn * (np1 - mx)).astype(f64) / np1
+    Us, Vs = [], []
+    for l in range(1, levels + 1):
+        s = n >> l
+        node_odd = ((g - 1) // s) % 2 == 1
+        gf = g.to(f64) if xp is not np else g.astype(f64)
+        u = xp.where(node_odd, np1 - gf, gf)
+        v = xp.where(node_odd, (np1 - gf) / np1, gf / np1)
+        Us.append(u)
+        Vs.append(v)
+    if levels:
+        U = xp.cat(Us) if xp is not np else np.concatenate(Us)
+        V = xp.cat(Vs) if xp is not np else np.concatenate(Vs)
+    else:
+        U = xp.zeros(0, dtype=f64, **kw)
+        V = xp.zeros(0, dtype=f64, **kw)
+    ranks = np.ones(levels, dtype=np.int32)
+    return Hodlr(n, levels, b, ranks, D.reshape(-1), U, V)
+
+
+# ------------------------------------------------------------------- HSS --
+
+@dataclass
+class Hss:
+    n: int
+    levels: int
+    leaf: int
+    k: int
+    D: np.ndarray
+    U: np.ndarray
+    V: np.ndarray
+    R: np.ndarray
+    W: np.ndarray
+    B: np.ndarray
+
+
+def hss_random(n: int, levels: int, k: int, seed: int = MASTER_SEED, cid: int = 0) -> Hss:
+    """Random HSS generators (configs 2 and 4; readings G8/G10): leaf U_i, V_i (b x k)
+    and R, W (2k x k) are thin-QR Q factors of Gaussian blocks; B12, B21 iid N(0,1);
+    D_i iid N(0,1)/sqrt(b)."""
+    b = n >> levels
+    assert b << levels == n
+    nl = 1 << levels
+    D = np.empty((nl, b, b), dtype=np.float64)
+    for i in range(nl):
+        D[i] = normal((b, b), seed, cid, AID["D"], i) / np.sqrt(b)
+    nt = max((1 << levels) - 2, 0)
+    nb = (1 << levels) - 1
+    if k > 0 and levels > 0:
+        U = _orth_blocks(normal((nl, b, k), seed, cid, AID["U"]))
+        V = _orth_blocks(normal((nl, b, k), seed, cid, AID["V"]))
+        R = _orth_blocks(normal((nt, 2 * k, k), seed, cid, AID["R"])) if nt else np.zeros((0, 2 * k, k))
+        W = _orth_blocks(normal((nt, 2 * k, k), seed, cid, AID["W"])) if nt else np.zeros((0, 2 * k, k))
+        B = normal((nb, 2, k, k), seed, cid, AID["B"])
+    else:
+        U = np.zeros((nl, b, k)); V = np.zeros((nl, b, k))
+        R = np.zeros((nt, 2 * k, k)); W = np.zeros((nt, 2 * k, k)); B = np.zeros((nb, 2, k, k))
+    return Hss(n, levels, b, k, D.reshape(-1), U.reshape(-1), V.reshape(-1), R.reshape(-1), W.reshape(-1),
+               B.reshape(-1))
+
+
+def hss_inverse_laplacian(n: int, levels: int) -> Hss:
+    """Exact rank-2 HSS form of tridiag(-1,2,-1)^{-1} (SURVEY §8(c) pins):
+    U = [r, n+1-r] (1-based rows), V = U/(n+1), R = W = [I2; I2],
+    B12 = [[0,1],[0,0]], B21 = [[0,0],[1,0]], D_i from the closed form."""
+    b = n >> levels
+    assert b << levels == n and levels >= 1
+    h = hodlr_inverse_laplacian(n, levels)
+    g = np.arange(1, n + 1, dtype=np.float64)
+    U = np.stack([g, (n + 1) - g], axis=1)
+    V = U / (n + 1)
+    nt, nb = (1 << levels) - 2, (1 << levels) - 1
+    I2 = np.eye(2)
+    R = np.tile(np.concatenate([I2, I2])[None], (nt, 1, 1))
+    B = np.tile(np.array([[[0.0, 1.0], [0.0, 0.0]], [[0.0, 0.0], [1.0, 0.0]]])[None], (nb, 1, 1, 1))
+    return Hss(n, levels, b, 2, h.D, U.reshape(-1), V.reshape(-1), R.reshape(-1), R.reshape(-1).copy(),
+               B.reshape(-1))
+
+
+def rhs(n: int, m: int, seed: int = MASTER_SEED, cid: int = 0, rows: Optional[Tuple[int, int]] = None,
+        slab: int = 1 << 16) -> np.ndarray:
+    """X iid N(0,1), [n][m], drawn in slabs of ``slab`` rows (shardable)."""
+    r0, r1 = rows if rows is not None else (0, n)
+    X = np.empty((r1 - r0, m), dtype=np.float64)
+    s0 = r0 // slab
+    for s in range(s0, (r1 + slab - 1) // slab):
+        a, z = max(s * slab, r0), min((s + 1) * slab, r1)
+        full = normal((slab, m), seed, cid, AID["X"], s)
+        X[a - r0: z - r0] = full[a - s * slab: z - s * slab]
+    return X
+
+
+# ---------------------------------------------------------- device copies --
+
+def device_hodlr_random(n, levels, ranks, seed, device, dtype=None):
+    """Same distributions as hodlr_random, drawn with torch's device RNG (bench only:
+    inputs resident in HBM without a host round trip; not bit-equal to the host draw)."""
+    import torch
+    b = n >> levels
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    D = torch.randn(n * b, dtype=torch.float64, device=device, generator=g).mul_(1.0 / np.sqrt(b))
+    parts_u, parts_v = [], []
+    for l in range(1, levels + 1):
+        k = int(ranks[l - 1])
+        s = n >> l
+        parts_u.append(torch.randn(n * k, dtype=torch.float64, device=device, generator=g).mul_(1.0 / np.sqrt(s)))
+        parts_v.append(torch.randn(n * k, dtype=torch.float64, device=device, generator=g).mul_(1.0 / np.sqrt(s)))
+    U = torch.cat(parts_u) if parts_u else torch.zeros(0, dtype=torch.float64, device=device)
+    V = torch.cat(parts_v) if parts_v else torch.zeros(0, dtype=torch.float64, device=device)
+    return Hodlr(n, levels, b, np.asarray(ranks, dtype=np.int32), D, U, V)
+
+
+def device_hss_random(n, levels, k, seed, device):
+    """Same distributions as hss_random, drawn and orthonormalised on the device (bench only)."""
+    import torch
+    b = n >> levels
+    nl = 1 << levels
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    f = dict(dtype=torch.float64, device=device, generator=g)
+    D = torch.randn(nl * b * b, **f).mul_(1.0 / np.sqrt(b))
+    nt, nb = (1 << levels) - 2, (1 << levels) - 1
+
+    def orth(cnt, r):
+        out = torch.empty(cnt, r, k, dtype=torch.float64, device=device)
+        step = 8192
+        for a in range(0, cnt, step):
+            z = min(cnt, a + step)
+            q, _ = torch.linalg.qr(torch.randn(z - a, r, k, **f), mode="reduced")
+            out[a:z] = q
+        return out.reshape(-1)
+
+    U, V = orth(nl, b), orth(nl, b)
+    R, W = orth(nt, 2 * k), orth(nt, 2 * k)
+    B = torch.randn(nb * 2 * k * k, **f)
+    return Hss(n, levels, b, k, D, U, V, R, W, B)

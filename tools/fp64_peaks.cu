@@ -1,0 +1,117 @@
+// Microbenchmarks that fix the roofline denominators MEASURED_PEAKS.json lacks:
+//   (1) DFMA-only throughput (fp64 CUDA-core peak),
+//   (2) DMMA (mma.sync .f64, SASS DMMA.8x8x4) throughput (fp64 tensor peak),
+//   (3) a read-only fp64 stream over a buffer much larger than L2 (achievable read BW),
+//   (4) a read+write copy (same definition as MEASURED_PEAKS.json hbm_gbs).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peaks tools/fp64_peaks.cu
+// Prints one JSON object.
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+template <int CH>
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+  double acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = fma(acc[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += acc[c];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int CH>
+__global__ void dmma_kernel(double* out, int iters) {
+  double d[CH][2];
+  double a = 1.0 + threadIdx.x * 1e-12, b = 0.999999;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) { d[c][0] = c; d[c][1] = -c; }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(d[c][0]), "+d"(d[c][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += d[c][0] + d[c][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+__global__ void read_kernel(const double2* __restrict__ p, size_t n2, double* out) {
+  double s0 = 0, s1 = 0;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    double2 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride), v3 = __ldg(p + i + 3 * stride);
+    s0 += v0.x + v1.x + v2.x + v3.x;
+    s1 += v0.y + v1.y + v2.y + v3.y;
+  }
+  for (; i < n2; i += stride) { double2 v = __ldg(p + i); s0 += v.x; s1 += v.y; }
+  if (s0 + s1 == 12345.678) out[0] = s0;
+}
+
+__global__ void copy_kernel(const double2* __restrict__ a, double2* __restrict__ b, size_t n2) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) b[i] = a[i];
+}
+
+template <typename F>
+float time_ms(F f, int reps) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  f(); CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(e0));
+    f();
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main() {
+  int dev = 0; CK(cudaSetDevice(dev));
+  cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, dev));
+  int sms = prop.multiProcessorCount;
+  double* out; CK(cudaMalloc(&out, 1 << 20));
+
+  // DFMA: 8 chains per thread, 1024 threads per SM resident x 2
+  const int iters = 1 << 14;
+  int blocks = sms * 8, threads = 256;
+  float ms_dfma = time_ms([&] { dfma_kernel<8><<<blocks, threads>>>(out, iters, 0.9999999, 1e-7); }, 5);
+  double dfma_tflops = 2.0 * 8 * iters * (double)blocks * threads / (ms_dfma * 1e-3) / 1e12;
+
+  // DMMA m8n8k4: 2*8*8*4 = 512 flop per warp-instruction
+  float ms_dmma = time_ms([&] { dmma_kernel<8><<<blocks, threads>>>(out, iters / 4); }, 5);
+  double dmma_tflops = 512.0 * 8 * (iters / 4) * (double)blocks * (threads / 32) / (ms_dmma * 1e-3) / 1e12;
+
+  // Streams over 8 GiB
+  size_t bytes = (size_t)8 << 30;
+  double2 *a, *b;
+  CK(cudaMalloc(&a, bytes));
+  CK(cudaMalloc(&b, bytes / 2));
+  CK(cudaMemset(a, 0, bytes));
+  CK(cudaMemset(b, 0, bytes / 2));
+  size_t n2 = bytes / sizeof(double2);
+  float ms_read = time_ms([&] { read_kernel<<<sms * 8, 256>>>(a, n2, out); }, 10);
+  double read_gbs = bytes / (ms_read * 1e-3) / 1e9;
+  size_t c2 = (bytes / 2) / sizeof(double2);
+  float ms_copy = time_ms([&] { copy_kernel<<<sms * 8, 256>>>(a, b, c2); }, 10);
+  double copy_gbs = 2.0 * (bytes / 2) / (ms_copy * 1e-3) / 1e9;
+
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_khz\": %d, \"dfma_tflops\": %.3f, \"dmma_m8n8k4_tflops\": %.3f, "
+         "\"read_stream_gbs\": %.1f, \"copy_rw_gbs\": %.1f}\n",
+         prop.name, sms, prop.clockRate, dfma_tflops, dmma_tflops, read_gbs, copy_gbs);
+  return 0;
+}

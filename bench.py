@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark: HODLR/HSS fp64 matvec GB/s and % of the HBM roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5+c4]
+
+One STEP = one pass of the whole hot path: one HODLR
+matvec on BASELINE config 5 (inverse 1D Laplacian, n = 2^24, leaf 256, 16 levels,
+rank 1, nrhs 1) and one HSS matvec on BASELINE config 4 (n = 2^22, leaf 128,
+15 levels, rank 32, nrhs 32) — the two configs BASELINE.json quotes "at 1/2/4/8
+B200" — with generators and X resident in HBM. `value` = algorithmic bytes
+(every generator once + X once + Y once) of all steps on all ranks
+/ device time of the timed region (max over ranks). Inputs (49 GB/step) are far
+larger than the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0. `--impl reference` times the CPU oracle (the
+slow, plain C reference of oracle/) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import hm_inputs  # noqa: E402
+
+METRIC = "HODLR/HSS fp64 matvec GB/s and % of HBM roofline vs nrhs, at 1/2/4/8 B200"
+
+
+# ------------------------------------------------------------- workloads --
+
+def hodlr_bytes(n, b, p, k, m):
+    """8 (n b + 2 p n k + 2 n m)."""
+    return 8 * (n * b + 2 * p * n * k + 2 * n * m)
+
+
+def hodlr_flops(n, b, p, k, m):
+    return 2 * n * m * (b + 2 * p * k)
+
+
+def hss_bytes(n, b, p, k, m):
+    """8 (n b + 2 n k + 4 (2^p - 2) k^2 + 2 (2^p - 1) k^2 + 2 n m)."""
+    return 8 * (n * b + 2 * n * k + 4 * ((1 << p) - 2) * k * k + 2 * ((1 << p) - 1) * k * k + 2 * n * m)
+
+
+def hss_flops(n, b, p, k, m):
+    return 2 * n * m * (b + 2 * k) + 8 * ((1 << p) - 2) * k * k * m + 4 * ((1 << p) - 1) * k * k * m
+
+
+C5 = hm_inputs.CONFIGS[5]
+C4 = hm_inputs.CONFIGS[4]
+M5, M4 = 1, 32
+
+
+def step_bytes():
+    return hodlr_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5) + hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
+
+
+def leaf_apply_c5_bytes(n, b, p, k, m):
+    """Algorithmic bytes of one HODLR leaf_apply launch: D + every level's U + X + Y."""
+    return 8 * (n * b + p * n * k + 2 * n * m)
+
+
+# ------------------------------------------------------------------ peaks --
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def committed_traffic(kernel, workload):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        e = t.get(workload, {}).get(kernel)
+        return None if e is None else float(e)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="hm_clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax = float(parts[1])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------- our implementation --
+
+class Workload:
+    """Device-resident generators for the step (rank-local shard when N > 1)."""
+
+    def __init__(self, torch, device, seed):
+        self.torch = torch
+        self.device = device
+        # config 5: closed-form inverse Laplacian filled on the device (no host round trip)
+        self.h5 = hm_inputs.hodlr_inverse_laplacian(C5.n, C5.levels, xp=torch, device=device)
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        self.X5 = torch.randn(C5.n, M5, dtype=torch.float64, device=device, generator=g)
+        self.Y5 = torch.empty_like(self.X5)
+        # config 4: orthonormalised Gaussian generators drawn on the device
+        self.s4 = hm_inputs.device_hss_random(C4.n, C4.levels, C4.k, seed + 1, device)
+        self.X4 = torch.randn(C4.n, M4, dtype=torch.float64, device=device, generator=g)
+        self.Y4 = torch.empty_like(self.X4)
+        import paper_1909_07909_b200 as hm
+        self.hm = hm
+        self.ws5 = torch.empty(hm.hm_hodlr_workspace_bytes(C5.n, C5.levels, C5.leaf, self.h5.ranks, M5),
+                               dtype=torch.uint8, device=device)
+        self.ws4 = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4), dtype=torch.uint8,
+                               device=device)
+        # end-to-end: pinned host X / Y, library copies through its own workspace
+        self.X5h = self.X5.cpu().pin_memory()
+        self.Y5h = torch.empty_like(self.X5h).pin_memory()
+        self.X4h = self.X4.cpu().pin_memory()
+        self.Y4h = torch.empty_like(self.X4h).pin_memory()
+        self.ws5io = torch.empty(hm.hm_hodlr_workspace_bytes(C5.n, C5.levels, C5.leaf, self.h5.ranks, M5,
+                                                             hm.HM_WS_HOSTIO), dtype=torch.uint8, device=device)
+        self.ws4io = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4, hm.HM_WS_HOSTIO),
+                                 dtype=torch.uint8, device=device)
+        self.launches = 0
+
+    def step(self):
+        hm, h, s = self.hm, self.h5, self.s4
+        hm.hodlr_matvec(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, self.X5, self.Y5, self.ws5)
+        self.launches += hm.last_launch_count()
+        hm.hss_matvec(C4.n, C4.levels, C4.leaf, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, self.X4, self.Y4, self.ws4)
+        self.launches += hm.last_launch_count()
+
+    def step_e2e(self):
+        hm, h, s = self.hm, self.h5, self.s4
+        hm.hodlr_matvec_hostio(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, self.X5h, self.Y5h, self.ws5io)
+        hm.hss_matvec_hostio(C4.n, C4.levels, C4.leaf, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, self.X4h, self.Y4h,
+                             self.ws4io)
+
+    def h2d_d2h_bytes(self):
+        return 8 * (C5.n * M5 + C4.n * M4), 8 * (C5.n * M5 + C4.n * M4)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        raise SystemExit("multi-GPU bench needs the distributed path (hodlr_matvec_dist / hss_matvec_dist)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    from paper_1909_07909_b200 import build as hm_build
+    hm_build.build()
+
+    wl = Workload(torch, device, seed=hm_inputs.MASTER_SEED + rank)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        wl.step()
+    torch.cuda.synchronize()
+    wl.hm.hm_profile_collect()  # discard anything traced so far
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    wl.launches = 0
+    wl.hm.hm_profile_enable(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        wl.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wl.hm.hm_profile_enable(False)
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    trace = wl.hm.hm_profile_collect()
+    launches = wl.launches
+
+    # end-to-end (host X in, host Y out through the C-ABI hostio calls)
+    for _ in range(2):
+        wl.step_e2e()
+    torch.cuda.synchronize()
+    e2 = max(3, args.steps // 5)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2):
+        wl.step_e2e()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = f0.elapsed_time(f1)
+
+    # per-kernel device time from the trace: call 2j = HODLR (config 5), 2j+1 = HSS (config 4)
+    per = {}
+    for name, call, t in trace:
+        key = ("c5" if call % 2 == 0 else "c4") + ":" + name
+        d = per.setdefault(key, [0, 0.0])
+        d[0] += 1
+        d[1] += t
+    step_ms = ms / args.steps
+    total_bytes = step_bytes() * args.steps * world
+    value = total_bytes / (ms * 1e-3) / 1e9
+    peak, peak_kind = load_peaks()
+    dom = per.get("c5:leaf_apply", [1, float("nan")])
+    dom_avg_ms = dom[1] / dom[0]
+    dom_bytes = leaf_apply_c5_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5)
+    achieved = dom_bytes / (dom_avg_ms * 1e-3) / 1e9
+    c5_ms = sum(v[1] for k_, v in per.items() if k_.startswith("c5:")) / args.steps
+    c4_ms = sum(v[1] for k_, v in per.items() if k_.startswith("c4:")) / args.steps
+    b5 = hodlr_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5)
+    b4 = hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
+    f4 = hss_flops(C4.n, C4.leaf, C4.levels, C4.k, M4)
+    h2d, d2h = wl.h2d_d2h_bytes()
+    out = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded; config 5 closed-form inverse Laplacian, config 4 orthonormalised Gaussians)",
+        "config": {
+            "workload": "c5+c4: HODLR config 5 (n=2^24, leaf 256, 16 levels, k=1, nrhs=1) + HSS config 4 "
+                        "(n=2^22, leaf 128, 15 levels, k=32, nrhs=32) per step",
+            "step_alg_bytes": step_bytes(),
+            "l2": "inputs 49 GB/step >> 126 MB L2; no flush needed",
+            "seed": hm_inputs.MASTER_SEED,
+            "parallelism": f"rows split by the top log2({world}) tree levels" if world > 1 else "single GPU",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "leaf_apply (config 5: D_i X_i + sum_l U_l t_l, all leaves)",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": committed_traffic("leaf_apply", "c5"),
+            "alg_bytes_per_launch": dom_bytes,
+            "avg_launch_ms": round(dom_avg_ms, 4),
+            "share_of_step": round(dom[1] / args.steps / step_ms, 4),
+        },
+        "per_config": {
+            "c5_hodlr": {"ms": round(c5_ms, 4), "GB/s": round(b5 / (c5_ms * 1e-3) / 1e9, 1),
+                         "frac_hbm": round(b5 / (c5_ms * 1e-3) / 1e9 / peak, 4)},
+            "c4_hss": {"ms": round(c4_ms, 4), "GB/s": round(b4 / (c4_ms * 1e-3) / 1e9, 1),
+                       "frac_hbm": round(b4 / (c4_ms * 1e-3) / 1e9 / peak, 4),
+                       "fp64_TFLOP/s": round(f4 / (c4_ms * 1e-3) / 1e12, 2)},
+        },
+        "kernels": {k_: {"launches_per_step": v[0] // args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
+                    for k_, v in sorted(per.items())},
+        "e2e": {"value": round(step_bytes() * e2 * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "hodlr_matvec_hostio + hss_matvec_hostio: pinned host X in, host Y out, every step"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------ CPU oracle --
+
+def oracle_sample():
+    """Bounded sample of the same workload for the oracle: config-5 structure at n = 2^20
+    (leaf 256, 12 levels, k = 1) and config-4 structure at n = 2^17 (leaf 128, 10 levels,
+    k = 32, nrhs 32). Both are GB/s-normalised, so the sample's GB/s is comparable."""
+    n5, p5 = 1 << 20, 12
+    n4, p4 = 1 << 17, 10
+    h = hm_inputs.hodlr_inverse_laplacian(n5, p5)
+    X5 = hm_inputs.rhs(n5, M5, cid=5)
+    s = hm_inputs.hss_random(n4, p4, C4.k, cid=4)
+    X4 = hm_inputs.rhs(n4, M4, cid=4)
+    nbytes = hodlr_bytes(n5, 256, p5, 1, M5) + hss_bytes(n4, 128, p4, C4.k, M4)
+    desc = (f"oracle on config-5 structure n=2^20 (leaf 256, 12 levels, k=1, nrhs=1) + config-4 structure "
+            f"n=2^17 (leaf 128, 10 levels, k=32, nrhs=32)")
+
+    def run():
+        import oracle
+        oracle.hodlr_matvec(n5, p5, h.ranks, h.D, h.U, h.V, X5)
+        oracle.hss_matvec(n4, p4, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, X4)
+
+    return run, nbytes, desc
+
+
+def cpu_baseline(seconds=12.0):
+    import oracle
+    run, nbytes, desc = oracle_sample()
+    run()  # first touch / thread pool
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        run()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": round(nbytes * reps / el / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": f"{desc}; {reps} repetitions in {el:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    run, nbytes, desc = oracle_sample()
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    el = time.perf_counter() - t0
+    value = nbytes * args.steps / el / 1e9
+    cores = oracle.num_threads()
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded)",
+        "config": {"workload": "c5+c4 (bounded host sample per step: " + desc + ")"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

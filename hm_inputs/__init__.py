@@ -120,49 +120,64 @@ def hodlr_random(n: int, levels: int, ranks: Sequence[int], seed: int = MASTER_S
     return Hodlr(n, levels, b, ranks, D.reshape(-1), U, V)
 
 
-def hodlr_inverse_laplacian(n: int, levels: int, rows: Optional[Tuple[int, int]] = None, xp=np,
-                            device=None) -> Hodlr:
-    """Exact HODLR form (rank 1 on every level) of A = tridiag(-1,2,-1)^{-1},
-    A_ij = min(i,j)(n+1-max(i,j))/(n+1), 1-based (BASELINE.json config 5; reading G11).
-    Upper block (i<j): u_i = i, v_j = (n+1-j)/(n+1); lower block (i>j): u_i = n+1-i,
-    v_j = j/(n+1). Every entry is an exact integer product (< 2^53) then at most one
-    correctly rounded division, so numpy and torch (CPU or CUDA) agree bit for bit.
-    ``xp`` may be numpy or torch (then ``device`` applies)."""
+def inverse_laplacian_leaf_blocks(n: int, levels: int, leaves=None, xp=np, device=None, chunk: int = 256):
+    """D_i = A(I_i, I_i) of A = tridiag(-1,2,-1)^{-1}: A_ij = min(i,j)(n+1-max(i,j))/(n+1),
+    1-based (BASELINE.json config 5). Integer product (< 2^53, exact) then one correctly
+    rounded division: numpy and torch (CPU or CUDA) give identical bits. ``leaves``: list of
+    leaf indices (default: all, in order). Filled ``chunk`` leaves at a time."""
     b = n >> levels
     assert b << levels == n
-    r0, r1 = rows if rows is not None else (0, n)
-    nl = (r1 - r0) // b
     kw = {} if xp is np else {"device": device}
-    f64 = xp.float64
-    i64 = xp.int64
+    if leaves is None:
+        leaves = range(1 << levels)
+    leaves = list(leaves)
+    out = xp.empty((len(leaves), b, b), dtype=xp.float64, **kw)
     np1 = n + 1
-    g = xp.arange(r0 + 1, r1 + 1, dtype=i64, **kw)  # 1-based global rows
-    # D_i[r][c] = min(gr,gc)(n+1-max(gr,gc))/(n+1)
-    gl = g.reshape(nl, b)
-    gr = gl[:, :, None]
-    gc = gl[:, None, :]
-    if xp is np:
-        mn, mx = np.minimum(gr, gc), np.maximum(gr, gc)
-    else:
-        mn, mx = xp.minimum(gr, gc), xp.maximum(gr, gc)
-    D = (mn * (np1 - mx)).to(f64) / np1 if xp is not np else (mn * (np1 - mx)).astype(f64) / np1
-    Us, Vs = [], []
+    rr = xp.arange(1, b + 1, dtype=xp.int64, **kw)
+    for a in range(0, len(leaves), chunk):
+        sel = leaves[a:a + chunk]
+        base = xp.asarray(np.asarray(sel, dtype=np.int64) * b) if xp is np else \
+            xp.as_tensor(np.asarray(sel, dtype=np.int64) * b, device=device)
+        g = base[:, None] + rr[None, :]               # 1-based global rows of each leaf
+        gr, gc = g[:, :, None], g[:, None, :]
+        mn = xp.minimum(gr, gc)
+        mx = xp.maximum(gr, gc)
+        num = mn * (np1 - mx)
+        if xp is np:
+            out[a:a + len(sel)] = num.astype(np.float64) / np1
+        else:  # tensor / tensor: a true IEEE division (torch turns "/ scalar" into "* (1/scalar)")
+            numf = num.to(xp.float64)
+            out[a:a + len(sel)] = numf / xp.full_like(numf, float(np1))
+    return out.reshape(-1)
+
+
+def inverse_laplacian_factors(n: int, levels: int, xp=np, device=None):
+    """Level-major rank-1 factors (HODLR layout) of A = tridiag(-1,2,-1)^{-1} (reading G11):
+    upper block (i<j): u_i = i, v_j = (n+1-j)/(n+1); lower block (i>j): u_i = n+1-i,
+    v_j = j/(n+1). Row r of level l sits in node (r-1)//s_l; odd nodes are lower blocks."""
+    kw = {} if xp is np else {"device": device}
+    np1 = n + 1
+    g = xp.arange(1, n + 1, dtype=xp.int64, **kw)
+    gf = g.astype(np.float64) if xp is np else g.to(xp.float64)
+    # divisor as an array: torch turns "/ scalar" into "* (1/scalar)", which is not
+    # correctly rounded; tensor / tensor is a true IEEE division like numpy's
+    den = np1 if xp is np else xp.full_like(gf, float(np1))
+    U = xp.empty(n * levels, dtype=xp.float64, **kw)
+    V = xp.empty(n * levels, dtype=xp.float64, **kw)
     for l in range(1, levels + 1):
         s = n >> l
-        node_odd = ((g - 1) // s) % 2 == 1
-        gf = g.to(f64) if xp is not np else g.astype(f64)
-        u = xp.where(node_odd, np1 - gf, gf)
-        v = xp.where(node_odd, (np1 - gf) / np1, gf / np1)
-        Us.append(u)
-        Vs.append(v)
-    if levels:
-        U = xp.cat(Us) if xp is not np else np.concatenate(Us)
-        V = xp.cat(Vs) if xp is not np else np.concatenate(Vs)
-    else:
-        U = xp.zeros(0, dtype=f64, **kw)
-        V = xp.zeros(0, dtype=f64, **kw)
-    ranks = np.ones(levels, dtype=np.int32)
-    return Hodlr(n, levels, b, ranks, D.reshape(-1), U, V)
+        odd = ((g - 1) // s) % 2 == 1
+        U[(l - 1) * n: l * n] = xp.where(odd, np1 - gf, gf)
+        V[(l - 1) * n: l * n] = xp.where(odd, (np1 - gf) / den, gf / den)
+    return U, V
+
+
+def hodlr_inverse_laplacian(n: int, levels: int, xp=np, device=None) -> Hodlr:
+    """Exact HODLR form (rank 1 on every level) of tridiag(-1,2,-1)^{-1} (config 5)."""
+    b = n >> levels
+    D = inverse_laplacian_leaf_blocks(n, levels, xp=xp, device=device)
+    U, V = inverse_laplacian_factors(n, levels, xp=xp, device=device)
+    return Hodlr(n, levels, b, np.ones(levels, dtype=np.int32), D, U, V)
 
 
 # ------------------------------------------------------------------- HSS --
@@ -212,7 +227,7 @@ def hss_inverse_laplacian(n: int, levels: int) -> Hss:
     B12 = [[0,1],[0,0]], B21 = [[0,0],[1,0]], D_i from the closed form."""
     b = n >> levels
     assert b << levels == n and levels >= 1
-    h = hodlr_inverse_laplacian(n, levels)
+    D = inverse_laplacian_leaf_blocks(n, levels)
     g = np.arange(1, n + 1, dtype=np.float64)
     U = np.stack([g, (n + 1) - g], axis=1)
     V = U / (n + 1)
@@ -220,7 +235,7 @@ def hss_inverse_laplacian(n: int, levels: int) -> Hss:
     I2 = np.eye(2)
     R = np.tile(np.concatenate([I2, I2])[None], (nt, 1, 1))
     B = np.tile(np.array([[[0.0, 1.0], [0.0, 0.0]], [[0.0, 0.0], [1.0, 0.0]]])[None], (nb, 1, 1, 1))
-    return Hss(n, levels, b, 2, h.D, U.reshape(-1), V.reshape(-1), R.reshape(-1), R.reshape(-1).copy(),
+    return Hss(n, levels, b, 2, D, U.reshape(-1), V.reshape(-1), R.reshape(-1), R.reshape(-1).copy(),
                B.reshape(-1))
 
 

@@ -1,0 +1,170 @@
+/*
+ * hm.h — C-ABI of libhm: the B200 hot path of hm-toolbox (arXiv 1909.07909),
+ * the fast hierarchical matrix–(multi)vector product Y = A·X in fp64 for
+ *   - HODLR matrices (§4.1, Fig. 5 left P:666-678;
+ *     format: Def. 2.2, class P:226-235), and
+ *   - HSS matrices (§4.1, Fig. 5 right P:683-721; format: eq. (3)
+ *     P:256-259, Def. 2.3, class P:332-344).
+ * "P:n" = line n of /root/reference/PAPER.md. DESIGN.md §2 lists every
+ * reading of an ambiguous passage (G1..G17) that these calls implement.
+ *
+ * Everything here is plain C: pointers, sizes, integers. No torch type, no
+ * C++ type. All matrices are real fp64, ROW-MAJOR, contiguous.
+ *
+ * Memory and ownership
+ *   - Generator arrays, X, Y and the workspace are DEVICE pointers on the
+ *     calling thread's current CUDA device, owned by the caller. The library
+ *     allocates nothing, keeps no pointer after return, never synchronises the
+ *     stream and never modifies an input (all inputs are const).
+ *   - Exception: the *_hostio variants take X and Y as HOST pointers (pinned
+ *     memory recommended; pageable works but serialises) and copy them
+ *     through the workspace on `stream` — the end-to-end path.
+ *   - `stream` is a cudaStream_t (CUstream) handle; NULL = legacy default.
+ *     Work is enqueued asynchronously; results are valid once the stream has
+ *     reached the point of the call.
+ *   - Y is overwritten (Y = A X, not accumulated). X and Y must not overlap.
+ *
+ * Errors: every call returns an hm_status; on a negative status nothing was
+ * enqueued (validation happens on the host before any launch) except for
+ * HM_ERR_CUDA, which reports a launch failure. hm_last_error() returns a
+ * thread-local, human-readable message for the last non-OK status. No call
+ * aborts, exits or throws.
+ *
+ * Determinism: identical inputs on the same GPU give bitwise-identical Y
+ * (no atomics, fixed reduction order) — SPEC S:343-344's deterministic mode.
+ */
+#ifndef HM_H
+#define HM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HM_ABI_VERSION 1
+
+typedef enum {
+  HM_OK = 0,
+  HM_ERR_INVALID_ARG = -1, /* inconsistent sizes, NULL/misaligned pointer, overlap */
+  HM_ERR_UNSUPPORTED = -2, /* valid per the paper but not built (see each call)    */
+  HM_ERR_WORKSPACE = -3,   /* workspace NULL or smaller than the query returned    */
+  HM_ERR_CUDA = -4,        /* a CUDA launch / copy failed                          */
+  HM_ERR_NCCL = -5         /* reserved for the multi-GPU calls                     */
+} hm_status;
+
+/* Cluster tree (Def. 2.1). This build supports the balanced tree of
+ * n = leaf * 2^levels, every level-l node I_i^l = [i*n/2^l, (i+1)*n/2^l)
+ * (0-based), i.e. the default split of P:378-379 when n/leaf is a power of two.
+ * levels = p = depth (root l = 0, leaves l = p); levels = 0 means A = D (one
+ * dense block). General endpoint vectors (empty leaves)
+ * return HM_ERR_UNSUPPORTED. */
+typedef struct {
+  int64_t n;      /* matrix order, >= 1                                    */
+  int32_t levels; /* p >= 0                                                */
+  int32_t flags;  /* must be 0                                             */
+  int64_t leaf;   /* leaf block size b >= 1, n == leaf << levels           */
+} hm_tree;
+
+/* ------------------------------------------------------------------ HODLR --
+ * Generators (flat level-major layout; class fields of P:226-235):
+ *   D  [2^p][b][b]   D_i = A(I_i^p, I_i^p), the dense leaves ("F").
+ *   U  level-major:  level l = 1..p starts at offset n*sum_{l'<l} k_{l'} and
+ *                    is [n][k_l]. Rows I_a^l of level l hold the left factor
+ *                    of the sibling block (a, sib a):  A(I_a, I_b) =
+ *                    U_l(I_a) V_l(I_b)^T for siblings a, b = a^1.
+ *                    (U12 = U_l(I_2q), U21 = U_l(I_2q+1) of the parent q.)
+ *   V  same shape as U; rows I_b of level l hold the right factor of block
+ *                    (sib b, b). (V12 = V_l(I_2q+1), V21 = V_l(I_2q).)
+ *   ranks [p] (host array): ranks[l-1] = k_l >= 0 (0 encodes the zero
+ *                    block). Supported: every nonzero k_l equal and
+ *                    <= 64; otherwise HM_ERR_UNSUPPORTED.
+ *   X  [n][nrhs], Y [n][nrhs]; nrhs >= 1.
+ * Cost O(k n log n); bytes = 8(n b + 2 sum_l n k_l + 2 n nrhs). */
+
+/* Workspace bytes for hodlr_matvec (flags = 0) or hodlr_matvec_hostio
+ * (flags = HM_WS_HOSTIO). Returns HM_OK and writes *bytes. */
+#define HM_WS_HOSTIO 1
+hm_status hm_hodlr_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs,
+                                   int32_t flags, size_t* bytes);
+
+/* Y = A X for a HODLR matrix A, computed as Fig. 5 left prescribes
+ * (y1+y2 / y3+y4 at every level) but level-parallel: all V_l^T X products
+ * first, then each leaf's rows receive D_i X(I_i) + sum_l U_l t_{l,sib}. */
+hm_status hodlr_matvec(const hm_tree* tree, const int32_t* ranks,
+                       const double* D, const double* U, const double* V,
+                       const double* X, int32_t nrhs, double* Y,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same, with X and Y in HOST memory (copied on `stream` through the
+ * workspace; query with HM_WS_HOSTIO). */
+hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks,
+                              const double* D, const double* U, const double* V,
+                              const double* X_host, int32_t nrhs, double* Y_host,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* -------------------------------------------------------------------- HSS --
+ * Generators (class fields of P:332-344; uniform rank k):
+ *   D  [2^p][b][b]           leaf diagonal blocks D_i.
+ *   U, V [n][k]              leaf bases U_i^(p), V_i^(p) stacked by leaf rows.
+ *   R, W [2^p-2][2k][k]      translation operators of node (l,i), l = 1..p-1,
+ *                            at index 2^l-2+i: R = R_{U,i}^(l) = [Rl; Rr],
+ *                            W = R_{V,i}^(l) = [Wl; Wr] (eq. (3); "W_U" of
+ *                            P:337 is R_V, reading G3). Rows 0..k-1 belong
+ *                            to the left child. Unused (may be NULL) if p < 2.
+ *   B  [2^p-1][2][k][k]      core blocks of node (l,q), l = 0..p-1, at index
+ *                            2^l-1+q: [0] = B12 = S_{2q,2q+1}^(l+1),
+ *                            [1] = B21 = S_{2q+1,2q}^(l+1).
+ *   k in [0, 64]; k = 0 makes A block diagonal (G17). X, Y as for HODLR.
+ * Cost O(k n). */
+hm_status hm_hss_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags,
+                                 size_t* bytes);
+
+/* Y = A X for an HSS matrix A: Step 1 (leaf V^T X, upsweep through W^T),
+ * Step 2 (cores B, on every level l = 1..p — reading G1 of the garbled loop
+ * bounds at P:695-706), Step 3 (downsweep through R), Step 4
+ * (Y(I_i) = U_i y_i + D_i X(I_i), reading G2). */
+hm_status hss_matvec(const hm_tree* tree, int32_t k,
+                     const double* D, const double* U, const double* V,
+                     const double* R, const double* W, const double* B,
+                     const double* X, int32_t nrhs, double* Y,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
+                            const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B,
+                            const double* X_host, int32_t nrhs, double* Y_host,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ misc -- */
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* hm_last_error(void);
+
+/* HM_ABI_VERSION of the loaded library. */
+int32_t hm_abi_version(void);
+
+/* Number of kernel launches the last successful matvec call on this thread
+ * enqueued (bench bookkeeping for "gpu_launches"). */
+int32_t hm_last_launch_count(void);
+
+/* Launch tracing (the measurement hook bench.py uses for per-kernel roofline
+ * numbers). While enabled, every kernel launch of every matvec call is
+ * bracketed by two CUDA events recorded on the launch's stream (no
+ * synchronisation, ~1 us of host work per launch). hm_profile_collect waits
+ * for the recorded events, writes up to `cap` records in launch order and
+ * clears the trace. `call` numbers the matvec calls since the trace began. */
+typedef struct {
+  char name[40];  /* kernel name, e.g. "leaf_apply", "vt_contract" */
+  int32_t call;   /* index of the matvec call that launched it      */
+  float ms;       /* device time between the bracketing events      */
+} hm_launch_record;
+
+hm_status hm_profile_enable(int32_t on);
+hm_status hm_profile_collect(hm_launch_record* out, int32_t cap, int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HM_H */

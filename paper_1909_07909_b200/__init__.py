@@ -1,0 +1,227 @@
+"""B200-native HODLR / HSS matrix-(multi)vector product (hm-toolbox, arXiv 1909.07909).
+
+Thin Python binding over the C-ABI library ``libhm.so`` (include/hm.h). It only
+marshals arguments — torch tensors to device pointers, the tree to an
+``hm_tree`` struct, torch's current CUDA stream to a ``cudaStream_t`` — and
+allocates the workspace with torch. Every step of the product runs in the
+library's sm_100a kernels. There is no CPU fallback: a missing library or a
+non-CUDA tensor raises.
+
+Names follow the C-ABI: ``hodlr_matvec``, ``hss_matvec`` (device tensors),
+``hodlr_matvec_hostio``, ``hss_matvec_hostio`` (host X / Y, end-to-end path),
+``hm_hodlr_workspace_bytes``, ``hm_hss_workspace_bytes``, ``hm_last_error``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhm.so")
+
+HM_OK, HM_ERR_INVALID_ARG, HM_ERR_UNSUPPORTED, HM_ERR_WORKSPACE, HM_ERR_CUDA, HM_ERR_NCCL = 0, -1, -2, -3, -4, -5
+HM_WS_HOSTIO = 1
+_STATUS = {0: "HM_OK", -1: "HM_ERR_INVALID_ARG", -2: "HM_ERR_UNSUPPORTED", -3: "HM_ERR_WORKSPACE",
+           -4: "HM_ERR_CUDA", -5: "HM_ERR_NCCL"}
+
+# every symbol include/hm.h declares (tests check the library exports all of them)
+EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "hm_hss_workspace_bytes",
+           "hss_matvec", "hss_matvec_hostio", "hm_last_error", "hm_abi_version", "hm_last_launch_count",
+           "hm_profile_enable", "hm_profile_collect")
+
+
+class HmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class hm_tree(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("levels", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("leaf", ctypes.c_int64)]
+
+
+class hm_launch_record(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 40), ("call", ctypes.c_int32), ("ms", ctypes.c_float)]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libhm.so (raises if it has not been built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_1909_07909_b200.build` "
+                          "(the CUDA path has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    T = ctypes.POINTER(hm_tree)
+    sigs = {
+        "hm_hodlr_workspace_bytes": [T, P, i32, i32, ctypes.POINTER(sz)],
+        "hodlr_matvec": [T, P, P, P, P, P, i32, P, P, sz, P],
+        "hodlr_matvec_hostio": [T, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_hss_workspace_bytes": [T, i32, i32, i32, ctypes.POINTER(sz)],
+        "hss_matvec": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hss_matvec_hostio": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_profile_enable": [i32],
+        "hm_profile_collect": [ctypes.POINTER(hm_launch_record), i32, ctypes.POINTER(i32)],
+    }
+    for name, args in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.hm_last_error.argtypes = []
+    lib.hm_last_error.restype = ctypes.c_char_p
+    lib.hm_abi_version.restype = ctypes.c_int32
+    lib.hm_last_launch_count.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+def hm_last_error() -> str:
+    return load().hm_last_error().decode()
+
+
+def last_launch_count() -> int:
+    return int(load().hm_last_launch_count())
+
+
+def hm_profile_enable(on: bool = True) -> None:
+    """Bracket every kernel launch with CUDA events on its stream (include/hm.h)."""
+    _check(load().hm_profile_enable(1 if on else 0))
+
+
+def hm_profile_collect(cap: int = 1 << 16):
+    """[(kernel name, call index, ms)] in launch order; clears the trace."""
+    buf = (hm_launch_record * cap)()
+    cnt = ctypes.c_int32(0)
+    _check(load().hm_profile_collect(buf, cap, ctypes.byref(cnt)))
+    return [(buf[i].name.decode(), int(buf[i].call), float(buf[i].ms)) for i in range(min(cnt.value, cap))]
+
+
+def _check(rc: int) -> None:
+    if rc != HM_OK:
+        raise HmError(rc, hm_last_error())
+
+
+def make_tree(n: int, levels: int, leaf: int) -> hm_tree:
+    return hm_tree(int(n), int(levels), 0, int(leaf))
+
+
+def _ranks(ranks: Sequence[int], levels: int):
+    arr = (ctypes.c_int32 * max(levels, 1))(*([int(r) for r in ranks][:levels] or [0]))
+    return arr
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr() if t.numel() > 0 else None
+
+
+def _dev(t, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor (no CPU fallback)")
+    return t
+
+
+def _stream(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs, flags=0) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hodlr_workspace_bytes(ctypes.byref(t), _ranks(ranks, levels), int(nrhs), int(flags),
+                                           ctypes.byref(out)))
+    return out.value
+
+
+def hm_hss_workspace_bytes(n, levels, leaf, k, nrhs, flags=0) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hss_workspace_bytes(ctypes.byref(t), int(k), int(nrhs), int(flags), ctypes.byref(out)))
+    return out.value
+
+
+def _workspace(nbytes, workspace, device):
+    import torch
+    if workspace is None:
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    if workspace.numel() < nbytes:
+        raise HmError(HM_ERR_WORKSPACE, f"workspace {workspace.numel()} < {nbytes} bytes")
+    return workspace
+
+
+def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, stream=None):
+    """Y = A X on the current CUDA stream for the HODLR matrix (D, U, V) (include/hm.h).
+    X: [n][nrhs] (or [n]) float64 CUDA tensor. Returns Y (allocated if None)."""
+    import torch
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs), workspace, X.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hodlr_matvec(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(X), nrhs,
+                               _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return Y
+
+
+def hodlr_matvec_hostio(n, levels, leaf, ranks, D, U, V, X_host, Y_host, workspace=None, stream=None):
+    """End-to-end variant: X_host / Y_host are (pinned) CPU float64 tensors; the library copies
+    X in and Y out on the stream. The caller synchronises before reading Y_host."""
+    import torch
+    nrhs = 1 if X_host.dim() == 1 else X_host.shape[1]
+    for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
+        if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
+            raise TypeError(f"{nm} must be a contiguous float64 host tensor")
+    _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs, HM_WS_HOSTIO), workspace, D.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hodlr_matvec_hostio(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V),
+                                      X_host.data_ptr(), nrhs, Y_host.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      _stream(stream)))
+    return Y_host
+
+
+def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, stream=None):
+    """Y = A X on the current CUDA stream for the HSS matrix (D, U, V, R, W, B) (include/hm.h)."""
+    import torch
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs), workspace, X.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_matvec(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                             _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return Y
+
+
+def hss_matvec_hostio(n, levels, leaf, k, D, U, V, R, W, B, X_host, Y_host, workspace=None, stream=None):
+    import torch
+    nrhs = 1 if X_host.dim() == 1 else X_host.shape[1]
+    for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
+        if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
+            raise TypeError(f"{nm} must be a contiguous float64 host tensor")
+    for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs, HM_WS_HOSTIO), workspace, D.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_matvec_hostio(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                                    X_host.data_ptr(), nrhs, Y_host.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _stream(stream)))
+    return Y_host

@@ -1,0 +1,322 @@
+// hm_kernels.cuh — sm_100a kernels for the HODLR / HSS matvec hot path.
+//
+// Paper: hm-toolbox (arXiv 1909.07909), PAPER.md "P:n" = line n.
+// Three kernel families cover every step of both products:
+//
+//   vt_contract  t_{l,j} = V_l(I_j)^T X(I_j) for several levels in ONE pass
+//                over the row tiles of X (X tile staged in shared memory and
+//                reused across levels). HODLR: the V12^* v2 / V21^* v1 halves
+//                of "y2 <- A12 v2", "y3 <- A21 v1" (Fig. 5 left),
+//                all levels at once because HODLR blocks are independent
+//                across levels. HSS: Step 1, v_i^p = V_i^* v(I_i)
+//                (P:684-686). Nodes larger than a tile leave per-tile
+//                partials, summed by reduce_partials in a fixed order.
+//   leaf_apply   per leaf i: Y(I_i) = D_i X(I_i) + sum_s U_s(I_i) T_s[node_s]
+//                with Y written exactly once. HODLR: "if A is dense return Av"
+//                 plus every level's U (V^* v) term (y1+y2 / y3+y4,
+//                P:674-675). HSS: Step 4, y = U_i v_i^p + d_i.
+//   hss_up_level / hss_down_level
+//                level-synchronous batched k x k products: upsweep through
+//                R_V^* = W^T and, fused, coupling by the cores B
+//                (reading G1) + downsweep through R_U.
+//
+// All arithmetic fp64. No atomics: every output element has one owner and a
+// fixed summation order, so results are bitwise reproducible.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hm {
+
+constexpr int kThreads = 256;
+constexpr int kMaxLevels = 48;
+constexpr int kMaxRank = 64;
+
+// ----------------------------------------------------------- vt_contract --
+
+struct VtLevel {
+  const double* V;  // [n][k] rows of this level's right factors
+  double* out;      // complete node results  [nodes][k][m]
+  double* partial;  // per-tile partials       [n / tile][k][m] (nodes larger than a tile)
+  int64_t s;        // node size (rows); s % tile == 0 or tile % s == 0
+  int32_t k;
+  int32_t pad;
+};
+
+struct VtParams {
+  const double* X;  // [n][m]
+  int64_t n;
+  int32_t m;
+  int32_t mc;       // columns per CTA (grid.y = ceil(m / mc))
+  int64_t tile;     // rows per CTA (a whole number of leaves)
+  int32_t nlev;
+  VtLevel lev[kMaxLevels];
+};
+
+// One CTA = one row tile x one column chunk; loops over the levels.
+// Thread t owns output o = t % O2 of the (k x mc) block (a = o % k, c = o / k)
+// for the rows r == t / O2 (mod 256 / O2) of the current segment, then a
+// fixed-order shared-memory reduction over the row groups.
+__global__ void __launch_bounds__(kThreads) vt_contract_kernel(const VtParams P) {
+  extern __shared__ double smem[];
+  const int64_t tile = P.tile;
+  const int64_t row0 = (int64_t)blockIdx.x * tile;
+  const int c0 = blockIdx.y * P.mc;
+  const int mc = min(P.mc, P.m - c0);
+  double* Xs = smem;                       // [tile][mc]
+  double* red = smem + tile * P.mc;        // [kThreads]
+  for (int64_t e = threadIdx.x; e < tile * mc; e += kThreads) {
+    int64_t r = e / mc;
+    int c = (int)(e - r * mc);
+    Xs[r * mc + c] = P.X[(row0 + r) * P.m + c0 + c];
+  }
+  __syncthreads();
+  for (int L = 0; L < P.nlev; ++L) {
+    const VtLevel lv = P.lev[L];
+    const int k = lv.k;
+    if (k == 0) continue;
+    const int O = k * mc;
+    int O2 = 1;
+    while (O2 < O) O2 <<= 1;
+    const bool big = lv.s > tile;       // node spans several tiles: per-tile partials
+    const int64_t seglen = big ? tile : lv.s;
+    const int64_t nseg = tile / seglen;
+    if (O2 <= kThreads) {
+      const int G = kThreads / O2;
+      const int o = threadIdx.x % O2, g = threadIdx.x / O2;
+      const int a = o % k, c = o / k;
+      for (int64_t sgi = 0; sgi < nseg; ++sgi) {
+        const int64_t rb = sgi * seglen;
+        double acc = 0.0;
+        if (o < O) {
+          const double* Vp = lv.V + (row0 + rb) * k + a;
+          const double* Xp = Xs + rb * mc + c;
+          for (int64_t r = g; r < seglen; r += G) acc = fma(Vp[r * k], Xp[r * mc], acc);
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < O) {
+          double s = 0.0;
+          for (int gg = 0; gg < G; ++gg) s += red[gg * O2 + threadIdx.x];
+          const int aa = threadIdx.x % k, cc = threadIdx.x / k;
+          double* dst;
+          if (big) {
+            dst = lv.partial + (int64_t)blockIdx.x * k * P.m;
+          } else {
+            const int64_t node = (row0 + rb) / lv.s;
+            dst = lv.out + node * k * P.m;
+          }
+          dst[aa * P.m + c0 + cc] = s;
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int64_t sgi = 0; sgi < nseg; ++sgi) {
+        const int64_t rb = sgi * seglen;
+        for (int o = threadIdx.x; o < O; o += kThreads) {
+          const int a = o % k, c = o / k;
+          const double* Vp = lv.V + (row0 + rb) * k + a;
+          const double* Xp = Xs + rb * mc + c;
+          double acc = 0.0;
+          for (int64_t r = 0; r < seglen; ++r) acc = fma(Vp[r * k], Xp[r * mc], acc);
+          double* dst;
+          if (big) {
+            dst = lv.partial + (int64_t)blockIdx.x * k * P.m;
+          } else {
+            const int64_t node = (row0 + rb) / lv.s;
+            dst = lv.out + node * k * P.m;
+          }
+          dst[a * P.m + c0 + c] = acc;
+        }
+      }
+    }
+  }
+}
+
+// t_l[node] = sum_{j < s/tile} partial_l[node * (s/tile) + j], fixed order.
+struct ReduceLevel {
+  const double* partial;
+  double* out;
+  int64_t nodes;
+  int32_t per_node;  // tiles per node
+  int32_t km;        // k * m
+};
+struct ReduceParams {
+  int32_t nlev;
+  ReduceLevel lev[kMaxLevels];
+};
+
+__global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceParams P) {
+  const ReduceLevel lv = P.lev[blockIdx.y];
+  const int64_t total = lv.nodes * lv.km;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t node = e / lv.km;
+    const int64_t o = e - node * lv.km;
+    const double* src = lv.partial + node * lv.per_node * lv.km + o;
+    double s = 0.0;
+    for (int j = 0; j < lv.per_node; ++j) s += src[(int64_t)j * lv.km];
+    lv.out[e] = s;
+  }
+}
+
+// ------------------------------------------------------------ leaf_apply --
+
+struct LeafSeg {
+  const double* A;  // [n][k]: this term's left factor rows (U_l or HSS U)
+  const double* T;  // coefficient blocks [nodes][k][m]
+  int32_t k;
+  int32_t shift;    // node = (leaf >> shift) ^ xr
+  int32_t xr;
+  int32_t pad;
+};
+struct LeafParams {
+  const double* D;  // [nleaves][b][b]
+  const double* X;  // [n][m]
+  double* Y;        // [n][m]
+  int64_t b;
+  int32_t m;
+  int32_t mc;       // columns per CTA
+  int32_t nseg;
+  int32_t ktot;     // sum of segment ranks
+  LeafSeg seg[kMaxLevels];
+};
+
+constexpr int kMaxMc = 16;
+
+// One CTA = one leaf x one column chunk. The CTA stages the "extended" right
+// operand Z = [X(I_i); T_1[node_1]; ...; T_S[node_S]] ((b + sum k) x mc) in
+// shared memory; each warp then owns rows r of the leaf and computes
+// Y[r][c] = [D_i[r][:], U_1[r][:], ..., U_S[r][:]] . Z[:][c] with lanes
+// striding the extended row, then a butterfly reduction.
+template <int MC>
+__global__ void __launch_bounds__(kThreads) leaf_apply_kernel(const LeafParams P) {
+  extern __shared__ double smem[];
+  const int64_t leaf = blockIdx.x;
+  const int64_t b = P.b;
+  const int64_t r0 = leaf * b;
+  const int c0 = blockIdx.y * MC;
+  const int mc = min(MC, P.m - c0);
+  double* Z = smem;  // [(b + ktot)][MC]
+  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
+    int64_t r = e / MC;
+    int c = (int)(e - r * MC);
+    Z[e] = (c < mc) ? P.X[(r0 + r) * P.m + c0 + c] : 0.0;
+  }
+  {
+    int64_t off = b * MC;
+    for (int s = 0; s < P.nseg; ++s) {
+      const LeafSeg sg = P.seg[s];
+      const int64_t node = (leaf >> sg.shift) ^ sg.xr;
+      const double* T = sg.T + node * sg.k * P.m;
+      for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
+        int a = e / MC, c = e - a * MC;
+        Z[off + e] = (c < mc) ? T[a * P.m + c0 + c] : 0.0;
+      }
+      off += (int64_t)sg.k * MC;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Di = P.D + leaf * b * b;
+  for (int64_t r = warp; r < b; r += kThreads / 32) {
+    double acc[MC];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) acc[c] = 0.0;
+    const double* Dr = Di + r * b;
+    for (int64_t j = lane; j < b; j += 32) {
+      const double d = Dr[j];
+#pragma unroll
+      for (int c = 0; c < MC; ++c) acc[c] = fma(d, Z[j * MC + c], acc[c]);
+    }
+    int64_t off = b;
+    for (int s = 0; s < P.nseg; ++s) {
+      const LeafSeg sg = P.seg[s];
+      const double* Ar = sg.A + (r0 + r) * sg.k;
+      for (int a = lane; a < sg.k; a += 32) {
+        const double u = Ar[a];
+#pragma unroll
+        for (int c = 0; c < MC; ++c) acc[c] = fma(u, Z[(off + a) * MC + c], acc[c]);
+      }
+      off += sg.k;
+    }
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      double v = acc[c];
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) v += __shfl_xor_sync(0xffffffffu, v, w);
+      acc[c] = v;
+    }
+    if (lane < mc) {
+      double v = acc[0];
+#pragma unroll
+      for (int c = 1; c < MC; ++c)
+        if (c == lane) v = acc[c];
+      P.Y[(r0 + r) * P.m + c0 + lane] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- HSS --
+
+// Upsweep, one level l:  x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]
+// W node (l,i) at index 2^l - 2 + i, [2k][k]. x level l at node offset 2^l - 2.
+struct HssLevelParams {
+  const double* W;   // or R for the downsweep
+  const double* B;
+  double* xh;        // [(2^{p+1}-2)][k][m]
+  double* yh;
+  int32_t level;
+  int32_t k;
+  int32_t m;
+  int32_t pad;
+};
+
+__global__ void __launch_bounds__(kThreads) hss_up_level_kernel(const HssLevelParams P) {
+  const int l = P.level, k = P.k, m = P.m;
+  const int64_t cnt = 1ll << l;
+  const int64_t km = (int64_t)k * m;
+  const int64_t total = cnt * km;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = e / km;
+    const int o = (int)(e - i * km);
+    const int a = o / m, c = o - a * m;
+    const double* Wn = P.W + ((1ll << l) - 2 + i) * 2 * k * k;
+    const double* z0 = P.xh + ((1ll << (l + 1)) - 2 + 2 * i) * km;
+    const double* z1 = z0 + km;
+    double acc = 0.0;
+    for (int r = 0; r < k; ++r) acc = fma(Wn[r * k + a], z0[r * m + c], acc);
+    for (int r = 0; r < k; ++r) acc = fma(Wn[(k + r) * k + a], z1[r * m + c], acc);
+    P.xh[((1ll << l) - 2 + i) * km + o] = acc;
+  }
+}
+
+// Coupling + downsweep, one level l = 1..p (reading G1):
+//   y_l[2q+w] = S_w x_l[2q+1-w] + (l >= 2 ? R_{l-1,q}[w] y_{l-1}[q] : 0)
+// S_0 = B12, S_1 = B21 of node (l-1, q) (index 2^{l-1}-1+q); R node (l-1,q)
+// at index 2^{l-1}-2+q, rows w*k..w*k+k-1.
+__global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const HssLevelParams P) {
+  const int l = P.level, k = P.k, m = P.m;
+  const int64_t cnt = 1ll << l;
+  const int64_t km = (int64_t)k * m;
+  const int64_t total = cnt * km;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t j = e / km;
+    const int o = (int)(e - j * km);
+    const int a = o / m, c = o - a * m;
+    const int64_t q = j >> 1;
+    const int w = (int)(j & 1);
+    const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * k * k;
+    const double* xs = P.xh + ((1ll << l) - 2 + (j ^ 1)) * km;
+    double yc = 0.0;
+    for (int r = 0; r < k; ++r) yc = fma(S[a * k + r], xs[r * m + c], yc);
+    double yd = 0.0;
+    if (l >= 2) {
+      const double* Rn = P.W + (((1ll << (l - 1)) - 2 + q) * 2 * k + w * k) * k;
+      const double* yp = P.yh + ((1ll << (l - 1)) - 2 + q) * km;
+      for (int r = 0; r < k; ++r) yd = fma(Rn[a * k + r], yp[r * m + c], yd);
+    }
+    P.yh[((1ll << l) - 2 + j) * km + o] = yc + yd;
+  }
+}
+
+}  // namespace hm

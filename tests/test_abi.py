@@ -1,0 +1,130 @@
+"""Host-side checks of the C-ABI library (no GPU needed, no compute calls).
+
+- libhm.so loads and exports every function include/hm.h declares;
+- the workspace queries follow the documented layout;
+- invalid arguments are rejected on the host with the documented status and
+  a message, before anything is launched.
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1909_07909_b200 as hm
+from paper_1909_07909_b200 import build as hm_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    hm_build.build()
+    return hm.load()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "hm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:hm_status|const char\*|int32_t)\s+(\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_binding_names():
+    fns = header_functions()
+    assert set(fns) == set(hm.EXPORTS), fns
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", hm.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [f for f in header_functions() if f not in exported]
+    assert not missing, missing
+
+
+def test_abi_version_and_no_error():
+    lib = hm.load()
+    assert lib.hm_abi_version() == 1
+    assert isinstance(hm.hm_last_error(), str)
+
+
+def test_library_has_no_torch_dependency():
+    out = subprocess.run(["ldd", hm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "torch" not in out and "c10" not in out
+
+
+def test_kernels_are_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", hm.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_hodlr_workspace_layout():
+    n, p, b, k = 1 << 20, 12, 256, 16
+    m = 8
+    ws = hm.hm_hodlr_workspace_bytes(n, p, b, [k] * p, m)
+    coef = sum((1 << l) * k * m * 8 for l in range(1, p + 1))
+    assert ws >= coef
+    assert ws < coef + 64 * 1024 * 1024  # partials stay small (tile-granular)
+    ws_io = hm.hm_hodlr_workspace_bytes(n, p, b, [k] * p, m, hm.HM_WS_HOSTIO)
+    assert ws_io >= ws + 2 * n * m * 8
+
+
+def test_hss_workspace_layout():
+    n, p, b, k, m = 1 << 22, 15, 128, 32, 32
+    ws = hm.hm_hss_workspace_bytes(n, p, b, k, m)
+    assert ws >= 2 * ((1 << (p + 1)) - 2) * k * m * 8
+
+
+@pytest.mark.parametrize("n,levels,leaf,err", [
+    (1000, 2, 256, hm.HM_ERR_UNSUPPORTED),   # not leaf * 2^levels (general tree)
+    (0, 0, 1, hm.HM_ERR_INVALID_ARG),
+    (1024, -1, 1024, hm.HM_ERR_INVALID_ARG),
+])
+def test_bad_trees_rejected(n, levels, leaf, err):
+    with pytest.raises(hm.HmError) as e:
+        hm.hm_hodlr_workspace_bytes(n, levels, leaf, [4] * max(levels, 0), 1)
+    assert e.value.status == err
+    assert len(hm.hm_last_error()) > 0
+
+
+def test_bad_ranks_and_nrhs_rejected():
+    with pytest.raises(hm.HmError) as e:
+        hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, -1], 1)
+    assert e.value.status == hm.HM_ERR_INVALID_ARG
+    with pytest.raises(hm.HmError) as e:
+        hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 8], 1)   # variable ranks: not built
+    assert e.value.status == hm.HM_ERR_UNSUPPORTED
+    with pytest.raises(hm.HmError) as e:
+        hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 4], 0)
+    assert e.value.status == hm.HM_ERR_INVALID_ARG
+    with pytest.raises(hm.HmError) as e:
+        hm.hm_hss_workspace_bytes(1024, 2, 256, 65, 1)
+    assert e.value.status == hm.HM_ERR_UNSUPPORTED
+
+
+def test_matvec_validation_happens_before_launch():
+    """Invalid calls return on the host (this container has no GPU, so reaching a launch
+    would fail differently): NULL pointers, small workspace, overlapping X/Y."""
+    lib = hm.load()
+    t = hm.make_tree(1024, 2, 256)
+    ranks = (ctypes.c_int32 * 2)(4, 4)
+    buf = ctypes.create_string_buffer(1 << 16)
+    base = (ctypes.addressof(buf) + 255) // 256 * 256
+    rc = lib.hodlr_matvec(ctypes.byref(t), ranks, None, None, None, None, 1, None, base, 1 << 15, None)
+    assert rc == hm.HM_ERR_INVALID_ARG or rc == hm.HM_ERR_WORKSPACE
+    need = hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 4], 1)
+    rc = lib.hodlr_matvec(ctypes.byref(t), ranks, 16, 16, 16, 16, 1, 16, base, need - 1, None)
+    assert rc == hm.HM_ERR_WORKSPACE
+    # X and Y overlap
+    rc = lib.hodlr_matvec(ctypes.byref(t), ranks, 256, 256, 256, 4096, 1, 4096 + 8, base, need, None)
+    assert rc == hm.HM_ERR_INVALID_ARG and "overlap" in hm.hm_last_error()
+    # misaligned D
+    rc = lib.hodlr_matvec(ctypes.byref(t), ranks, 8, 256, 256, 4096, 1, 1 << 20, base, need, None)
+    assert rc == hm.HM_ERR_INVALID_ARG and "aligned" in hm.hm_last_error()
+
+
+def test_binding_refuses_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    x = torch.zeros(1024, 1, dtype=torch.float64)
+    with pytest.raises(TypeError):
+        hm.hodlr_matvec(1024, 2, 256, [4, 4], x, x, x, x)

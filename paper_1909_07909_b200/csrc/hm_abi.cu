@@ -16,6 +16,7 @@
 
 #include "../../include/hm.h"
 #include "hm_kernels.cuh"
+#include "hm_fast.cuh"
 
 namespace {
 
@@ -134,14 +135,52 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+// ---------------------------------------------------------------- dispatch --
+// Which kernels run is decided on the host from the shapes:
+// the tuned kernels of hm_fast.cuh where their shape conditions hold, the
+// generic kernels of hm_kernels.cuh otherwise. Both are exact implementations
+// of the same steps; the parity tests cover both families.
+
+bool pow2_rank(int k, int lo, int hi) {
+  for (int v = lo; v <= hi; v <<= 1)
+    if (k == v) return true;
+  return false;
+}
+
+int nt_for(int m, int cap) {
+  int nt = 1;
+  while (nt < cap && nt * 8 < m) nt <<= 1;
+  return nt;
+}
+
+template <typename F>
+hm_status launch(const char* name, cudaStream_t s, F&& f) {
+  int slot = prof_begin(name, s);
+  f();
+  prof_end(slot, s);
+  ++g_launches;
+  return cuda_check(name);
+}
+
+template <typename K>
+void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 // ------------------------------------------------------------------ HODLR --
+
+enum class VtPath { kNone, kGeneric, kGemv, kMma };
+enum class LeafPath { kGeneric, kGemv, kMma };
 
 struct HodlrPlan {
   int64_t n, b;
-  int32_t p, m, k;       // k = the common nonzero rank (0 if all zero)
-  int32_t mc_vt, mc_leaf;
-  int64_t tile;
-  size_t off_t[hm::kMaxLevels + 1];   // coefficient blocks t_l, per level
+  int32_t p, m, k;  // k = the common nonzero rank (0 if all zero)
+  int64_t ktot;
+  VtPath vt;
+  LeafPath leaf;
+  int32_t mc_vt, mc_leaf, nt_vt, nt_leaf;
+  int64_t tile;  // rows per vt CTA
+  size_t off_t[hm::kMaxLevels + 1];
   size_t off_part[hm::kMaxLevels + 1];
   size_t off_x, off_y, total;
 };
@@ -153,7 +192,6 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
   if (tree->levels > 0 && !ranks) return fail(HM_ERR_INVALID_ARG, "ranks is NULL");
   memset(P, 0, sizeof *P);
   P->n = tree->n; P->b = tree->leaf; P->p = tree->levels; P->m = nrhs;
-  int64_t ktot = 0;
   for (int l = 1; l <= P->p; ++l) {
     int k = ranks[l - 1];
     if (k < 0) return fail(HM_ERR_INVALID_ARG, "ranks[%d] = %d < 0", l - 1, k);
@@ -163,27 +201,57 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
         return fail(HM_ERR_UNSUPPORTED, "per-level ranks differ (%d vs %d); variable ranks (P:264) not built", P->k, k);
       P->k = k;
     }
-    ktot += k;
+    P->ktot += k;
   }
-  P->mc_vt = vt_mc(P->b, nrhs);
-  P->mc_leaf = pick_mc(P->b, ktot, nrhs);
-  if ((P->b + ktot) * P->mc_leaf > kSmemBudgetDoubles)
-    return fail(HM_ERR_UNSUPPORTED, "leaf %lld + ranks %lld too large for shared-memory staging", (long long)P->b, (long long)ktot);
-  P->tile = pick_tile(P->b, P->p, P->mc_vt);
+  const int64_t b = P->b, k = P->k;
+  const bool tiles8 = P->p >= 3;  // 8-leaf row tiles exist
+  // phase 1: V_l^T X
+  if (k == 0 || P->p == 0) {
+    P->vt = VtPath::kNone;
+  } else if (nrhs == 1 && tiles8 && b % 64 == 0 && b <= 4096 && pow2_rank((int)k, 1, 64)) {
+    P->vt = VtPath::kGemv;
+    P->tile = 8 * b;
+  } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 16, 64)) {
+    P->vt = VtPath::kMma;
+    P->tile = 8 * b;
+    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : 4);
+  } else {
+    P->vt = VtPath::kGeneric;
+    P->mc_vt = vt_mc(b, nrhs);
+    P->tile = pick_tile(b, P->p, P->mc_vt);
+  }
+  // phase 2: leaves
+  const bool k8 = (k % 8 == 0);
+  if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (k == 0 || pow2_rank((int)k, 1, 64)) &&
+      (2 * b + P->ktot) * 8 <= 160 * 1024) {
+    P->leaf = LeafPath::kGemv;
+  } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && k8) {
+    P->leaf = LeafPath::kMma;
+    const int rg = (int)(b / 64);
+    P->nt_leaf = nt_for(nrhs, rg == 4 ? 2 : 4);
+    if ((b + P->ktot) * (8 * P->nt_leaf + 4) > kSmemBudgetDoubles) P->leaf = LeafPath::kGeneric;
+  } else {
+    P->leaf = LeafPath::kGeneric;
+  }
+  if (P->leaf == LeafPath::kGeneric) {
+    P->mc_leaf = pick_mc(b, P->ktot, nrhs);
+    if ((b + P->ktot) * P->mc_leaf > kSmemBudgetDoubles)
+      return fail(HM_ERR_UNSUPPORTED, "leaf %lld + ranks %lld too large for shared-memory staging", (long long)b,
+                  (long long)P->ktot);
+  }
+  // workspace: t_l per level, per-tile partials where a node spans several tiles
   size_t off = 0;
   for (int l = 1; l <= P->p; ++l) {
-    int64_t k = ranks[l - 1];
     P->off_t[l] = off;
-    off = align_up(off + sizeof(double) * (size_t)((1ll << l) * k * nrhs));
+    off = align_up(off + sizeof(double) * (size_t)((1ll << l) * ranks[l - 1] * nrhs));
   }
   for (int l = 1; l <= P->p; ++l) {
-    int64_t k = ranks[l - 1];
-    int64_t s = P->n >> l;
+    const int64_t s = P->n >> l;
     P->off_part[l] = off;
-    if (k > 0 && s > P->tile) off = align_up(off + sizeof(double) * (size_t)((P->n / P->tile) * k * nrhs));
+    if (P->vt != VtPath::kNone && ranks[l - 1] > 0 && s > P->tile)
+      off = align_up(off + sizeof(double) * (size_t)((P->n / P->tile) * ranks[l - 1] * nrhs));
   }
-  P->off_x = off;
-  P->off_y = off;
+  P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off;
     off = align_up(off + sizeof(double) * (size_t)(P->n * nrhs));
@@ -194,44 +262,143 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
   return HM_OK;
 }
 
+// ---- leaf launches (shared by HODLR and HSS) ----
+
 template <int MC>
-hm_status launch_leaf(const hm::LeafParams& lp, int64_t nleaves, int m, size_t smem, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(hm::leaf_apply_kernel<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  dim3 grid((unsigned)nleaves, (unsigned)((m + MC - 1) / MC));
-  int slot = prof_begin("leaf_apply", s);
-  hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp);
-  prof_end(slot, s);
-  ++g_launches;
-  return cuda_check("leaf_apply_kernel");
+hm_status launch_leaf_generic(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * MC);
+  allow_smem(hm::leaf_apply_kernel<MC>, smem);
+  dim3 grid((unsigned)nleaves, (unsigned)((lp.m + MC - 1) / MC));
+  return launch("leaf_apply", s, [&] { hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
 }
 
-hm_status leaf_apply(const hm::LeafParams& lp, int64_t nleaves, int mc, cudaStream_t s) {
-  size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * mc);
+template <int K>
+hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  size_t smem = sizeof(double) * (size_t)(2 * lp.b + lp.nseg * K);
+  allow_smem(hm::leaf_gemv_kernel<K>, smem);
+  return launch("leaf_apply", s, [&] { hm::leaf_gemv_kernel<K><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+}
+
+template <int RG, int NT>
+hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * (NT * 8 + 4));
+  allow_smem(hm::leaf_mma_kernel<RG, NT>, smem);
+  const int64_t chunks = (lp.m + NT * 8 - 1) / (NT * 8);
+  return launch("leaf_apply", s,
+                [&] { hm::leaf_mma_kernel<RG, NT><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp); });
+}
+
+hm_status leaf_dispatch(const hm::LeafParams& lp, int64_t nleaves, LeafPath path, int k, int nt, int mc,
+                        cudaStream_t s) {
+  if (path == LeafPath::kGemv) {
+    switch (k) {
+      case 0: case 1: return launch_leaf_gemv<1>(lp, nleaves, s);
+      case 2: return launch_leaf_gemv<2>(lp, nleaves, s);
+      case 4: return launch_leaf_gemv<4>(lp, nleaves, s);
+      case 8: return launch_leaf_gemv<8>(lp, nleaves, s);
+      case 16: return launch_leaf_gemv<16>(lp, nleaves, s);
+      case 32: return launch_leaf_gemv<32>(lp, nleaves, s);
+      default: return launch_leaf_gemv<64>(lp, nleaves, s);
+    }
+  }
+  if (path == LeafPath::kMma) {
+    const int rg = (int)(lp.b / 64);
+#define HM_LEAF_MMA(RG_)                                            \
+  if (rg == RG_) {                                                  \
+    if (nt == 1) return launch_leaf_mma<RG_, 1>(lp, nleaves, s);    \
+    if (nt == 2) return launch_leaf_mma<RG_, 2>(lp, nleaves, s);    \
+    if constexpr (RG_ < 4) return launch_leaf_mma<RG_, 4>(lp, nleaves, s); \
+  }
+    HM_LEAF_MMA(1)
+    HM_LEAF_MMA(2)
+    HM_LEAF_MMA(4)
+#undef HM_LEAF_MMA
+    return fail(HM_ERR_UNSUPPORTED, "leaf_mma: no instance for b=%lld nt=%d", (long long)lp.b, nt);
+  }
   switch (mc) {
-    case 1: return launch_leaf<1>(lp, nleaves, lp.m, smem, s);
-    case 2: return launch_leaf<2>(lp, nleaves, lp.m, smem, s);
-    case 4: return launch_leaf<4>(lp, nleaves, lp.m, smem, s);
-    case 8: return launch_leaf<8>(lp, nleaves, lp.m, smem, s);
-    default: return launch_leaf<16>(lp, nleaves, lp.m, smem, s);
+    case 1: return launch_leaf_generic<1>(lp, nleaves, s);
+    case 2: return launch_leaf_generic<2>(lp, nleaves, s);
+    case 4: return launch_leaf_generic<4>(lp, nleaves, s);
+    case 8: return launch_leaf_generic<8>(lp, nleaves, s);
+    default: return launch_leaf_generic<16>(lp, nleaves, s);
   }
 }
 
-hm_status vt_contract(const hm::VtParams& vp, int64_t n, size_t smem, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(hm::vt_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+// ---- V^T X launches ----
+
+hm_status vt_generic(const hm::VtParams& vp, int64_t n, cudaStream_t s) {
+  size_t smem = sizeof(double) * (size_t)(vp.tile * vp.mc + hm::kThreads);
+  allow_smem(hm::vt_contract_kernel, smem);
   dim3 grid((unsigned)(n / vp.tile), (unsigned)((vp.m + vp.mc - 1) / vp.mc));
-  int slot = prof_begin("vt_contract", s);
-  hm::vt_contract_kernel<<<grid, hm::kThreads, smem, s>>>(vp);
-  prof_end(slot, s);
-  ++g_launches;
-  return cuda_check("vt_contract_kernel");
+  return launch("vt_contract", s, [&] { hm::vt_contract_kernel<<<grid, hm::kThreads, smem, s>>>(vp); });
+}
+
+template <int K>
+hm_status vt_gemv_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
+  hm::VtGemvParams gp;
+  memset(&gp, 0, sizeof gp);
+  gp.X = vp.X; gp.n = vp.n; gp.b = b; gp.nlev = vp.nlev;
+  for (int i = 0; i < vp.nlev; ++i) gp.lev[i] = vp.lev[i];
+  size_t smem = sizeof(double) * (size_t)(8 * b);
+  allow_smem(hm::vt_gemv_kernel<K>, smem);
+  return launch("vt_contract", s,
+                [&] { hm::vt_gemv_kernel<K><<<(unsigned)(vp.n / (8 * b)), 256, smem, s>>>(gp); });
+}
+
+hm_status vt_gemv_dispatch(const hm::VtParams& vp, int64_t b, int k, cudaStream_t s) {
+  switch (k) {
+    case 1: return vt_gemv_launch<1>(vp, b, s);
+    case 2: return vt_gemv_launch<2>(vp, b, s);
+    case 4: return vt_gemv_launch<4>(vp, b, s);
+    case 8: return vt_gemv_launch<8>(vp, b, s);
+    case 16: return vt_gemv_launch<16>(vp, b, s);
+    case 32: return vt_gemv_launch<32>(vp, b, s);
+    default: return vt_gemv_launch<64>(vp, b, s);
+  }
+}
+
+template <int KT, int NT>
+hm_status vt_mma_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
+  size_t smem = sizeof(double) * (size_t)(8 * KT * NT * 8);
+  allow_smem(hm::vt_mma_levels_kernel<KT, NT>, smem);
+  return launch("vt_contract", s, [&] {
+    hm::vt_mma_levels_kernel<KT, NT><<<(unsigned)(vp.n / (8 * b)), 256, smem, s>>>(vp, b);
+  });
+}
+
+hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cudaStream_t s) {
+#define HM_VT_MMA(KT_)                                             \
+  if (k == KT_) {                                                  \
+    if (nt == 1) return vt_mma_launch<KT_, 1>(vp, b, s);           \
+    if (nt == 2) return vt_mma_launch<KT_, 2>(vp, b, s);           \
+    if constexpr (KT_ < 64) return vt_mma_launch<KT_, 4>(vp, b, s); \
+  }
+  HM_VT_MMA(16)
+  HM_VT_MMA(32)
+  HM_VT_MMA(64)
+#undef HM_VT_MMA
+  return fail(HM_ERR_UNSUPPORTED, "vt_mma: no instance for k=%d nt=%d", k, nt);
+}
+
+template <int KT, int NT>
+hm_status vt_batched_launch(const char* name, const hm::BatchedVtParams& bp, cudaStream_t s) {
+  return launch(name, s, [&] {
+    hm::vt_batched_kernel<KT, NT><<<(unsigned)((bp.count + 7) / 8), 256, 0, s>>>(bp);
+  });
+}
+
+hm_status vt_batched_dispatch(const char* name, const hm::BatchedVtParams& bp, int k, int nt, cudaStream_t s) {
+#define HM_VTB(KT_)                                                 \
+  if (k == KT_) {                                                   \
+    if (nt == 1) return vt_batched_launch<KT_, 1>(name, bp, s);     \
+    if (nt == 2) return vt_batched_launch<KT_, 2>(name, bp, s);     \
+    if constexpr (KT_ < 64) return vt_batched_launch<KT_, 4>(name, bp, s); \
+  }
+  HM_VTB(16)
+  HM_VTB(32)
+  HM_VTB(64)
+#undef HM_VTB
+  return fail(HM_ERR_UNSUPPORTED, "vt_batched: no instance for k=%d nt=%d", k, nt);
 }
 
 hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
@@ -244,9 +411,12 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
   if (!D || !X || !Y || (P.k > 0 && (!U || !V)))
     return fail(HM_ERR_INVALID_ARG, "NULL generator / X / Y pointer");
-  if (!aligned16(D) || !aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "D and workspace must be 16-byte aligned");
+  if (!aligned16(D) || !aligned16(ws) || (P.k > 0 && (!aligned16(U) || !aligned16(V))))
+    return fail(HM_ERR_INVALID_ARG, "D, U, V and the workspace must be 16-byte aligned");
   const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
   if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
+    return fail(HM_ERR_INVALID_ARG, "X and Y must be 16-byte aligned");
 
   char* w = static_cast<char*>(ws);
   const double* Xd = X;
@@ -260,8 +430,8 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
       return cuda_check("H2D copy of X");
   }
 
-  // (1) all levels' V_l^T X in one pass (vt_contract), partials -> reduce
-  if (P.k > 0) {
+  // (1) every level's V_l^T X in one pass over row tiles; partials -> fixed-order reduce
+  if (P.vt != VtPath::kNone) {
     hm::VtParams vp;
     memset(&vp, 0, sizeof vp);
     vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile;
@@ -269,8 +439,8 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     memset(&rp, 0, sizeof rp);
     int64_t uoff = 0;
     for (int l = 1; l <= P.p; ++l) {
-      int k = ranks[l - 1];
-      int64_t s = P.n >> l;
+      const int k = ranks[l - 1];
+      const int64_t s = P.n >> l;
       if (k > 0) {
         hm::VtLevel& lv = vp.lev[vp.nlev++];
         lv.V = V + uoff;
@@ -289,15 +459,15 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
       }
       uoff += P.n * k;
     }
-    size_t smem = sizeof(double) * (size_t)(P.tile * P.mc_vt + hm::kThreads);
-    if ((st = vt_contract(vp, P.n, smem, stream))) return st;
+    if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
+    else if (P.vt == VtPath::kMma) st = vt_mma_dispatch(vp, P.b, P.k, P.nt_vt, stream);
+    else st = vt_generic(vp, P.n, stream);
+    if (st) return st;
     if (rp.nlev > 0) {
       dim3 grid(64, rp.nlev);
-      int slot = prof_begin("reduce_partials", stream);
-      hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp);
-      prof_end(slot, stream);
-      ++g_launches;
-      if ((st = cuda_check("reduce_partials_kernel"))) return st;
+      st = launch("reduce_partials", stream,
+                  [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp); });
+      if (st) return st;
     }
   }
 
@@ -308,7 +478,7 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
   {
     int64_t uoff = 0;
     for (int l = 1; l <= P.p; ++l) {
-      int k = ranks[l - 1];
+      const int k = ranks[l - 1];
       if (k > 0) {
         hm::LeafSeg& sg = lp.seg[lp.nseg++];
         sg.A = U + uoff;
@@ -321,7 +491,7 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
       uoff += P.n * k;
     }
   }
-  if ((st = leaf_apply(lp, 1ll << P.p, P.mc_leaf, stream))) return st;
+  if ((st = leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream))) return st;
 
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
@@ -334,7 +504,11 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
 
 struct HssPlan {
   int64_t n, b;
-  int32_t p, m, k, mc_vt, mc_leaf;
+  int32_t p, m, k;
+  VtPath vt;
+  LeafPath leaf;
+  bool mma_levels;  // DMMA up/down level kernels
+  int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
   size_t off_xh, off_yh, off_x, off_y, total;
 };
@@ -347,11 +521,38 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
   if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
   memset(P, 0, sizeof *P);
   P->n = tree->n; P->b = tree->leaf; P->p = tree->levels; P->m = nrhs; P->k = k;
-  P->mc_vt = vt_mc(P->b, nrhs);
-  P->mc_leaf = pick_mc(P->b, k, nrhs);
-  if ((P->b + k) * P->mc_leaf > kSmemBudgetDoubles)
-    return fail(HM_ERR_UNSUPPORTED, "leaf %lld too large for shared-memory staging", (long long)P->b);
-  P->tile = pick_tile(P->b, P->p, P->mc_vt);
+  const int64_t b = P->b;
+  const bool coupled = (k > 0 && P->p > 0);
+  if (!coupled) {
+    P->vt = VtPath::kNone;
+  } else if (nrhs == 1 && P->p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
+    P->vt = VtPath::kGemv;
+    P->tile = 8 * b;
+  } else if (nrhs >= 2 && b % 4 == 0 && pow2_rank(k, 16, 64)) {
+    P->vt = VtPath::kMma;  // batched: one warp per leaf
+    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : 4);
+  } else {
+    P->vt = VtPath::kGeneric;
+    P->mc_vt = vt_mc(b, nrhs);
+    P->tile = pick_tile(b, P->p, P->mc_vt);
+  }
+  P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
+  if (P->mma_levels) P->nt_down = nt_for(nrhs, std::max(1, 8 / (k / 8)));
+  const int ktot = coupled ? k : 0;
+  if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
+    P->leaf = LeafPath::kGemv;
+  } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && ktot % 8 == 0) {
+    P->leaf = LeafPath::kMma;
+    P->nt_leaf = nt_for(nrhs, b == 256 ? 2 : 4);
+    if ((b + ktot) * (8 * P->nt_leaf + 4) > kSmemBudgetDoubles) P->leaf = LeafPath::kGeneric;
+  } else {
+    P->leaf = LeafPath::kGeneric;
+  }
+  if (P->leaf == LeafPath::kGeneric) {
+    P->mc_leaf = pick_mc(b, ktot, nrhs);
+    if ((b + ktot) * P->mc_leaf > kSmemBudgetDoubles)
+      return fail(HM_ERR_UNSUPPORTED, "leaf %lld too large for shared-memory staging", (long long)b);
+  }
   const size_t coef = sizeof(double) * (size_t)((((int64_t)1 << (P->p + 1)) - 2) * k * nrhs);
   size_t off = 0;
   P->off_xh = off; off = align_up(off + coef);
@@ -365,6 +566,27 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
   return HM_OK;
 }
 
+template <int KT, int NT>
+hm_status hss_down_launch(const hm::HssDownParams& dp, cudaStream_t s) {
+  const int64_t cnt = 1ll << dp.level;
+  return launch("hss_down_level", s,
+                [&] { hm::hss_down_mma_kernel<KT, NT><<<(unsigned)((cnt + 7) / 8), 256, 0, s>>>(dp); });
+}
+
+hm_status hss_down_dispatch(const hm::HssDownParams& dp, int k, int nt, cudaStream_t s) {
+#define HM_DOWN(KT_)                                              \
+  if (k == KT_) {                                                 \
+    if (nt == 1) return hss_down_launch<KT_, 1>(dp, s);           \
+    if constexpr (KT_ <= 32) { if (nt == 2) return hss_down_launch<KT_, 2>(dp, s); } \
+    if constexpr (KT_ <= 16) { if (nt == 4) return hss_down_launch<KT_, 4>(dp, s); } \
+  }
+  HM_DOWN(16)
+  HM_DOWN(32)
+  HM_DOWN(64)
+#undef HM_DOWN
+  return fail(HM_ERR_UNSUPPORTED, "hss_down: no instance for k=%d nt=%d", k, nt);
+}
+
 hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                   const double* R, const double* W, const double* B, const double* X, int32_t nrhs, double* Y,
                   void* ws, size_t ws_bytes, cudaStream_t stream, int32_t flags) {
@@ -376,8 +598,12 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   if (k > 0 && P.p > 0 && (!U || !V || !B)) return fail(HM_ERR_INVALID_ARG, "NULL U / V / B pointer");
   if (k > 0 && P.p > 1 && (!R || !W)) return fail(HM_ERR_INVALID_ARG, "NULL R / W pointer");
   if (!aligned16(D) || !aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "D and workspace must be 16-byte aligned");
+  if (k > 0 && P.p > 0 && (!aligned16(U) || !aligned16(V) || !aligned16(B) || (P.p > 1 && (!aligned16(R) || !aligned16(W)))))
+    return fail(HM_ERR_INVALID_ARG, "U, V, R, W, B must be 16-byte aligned");
   const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
   if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
+    return fail(HM_ERR_INVALID_ARG, "X and Y must be 16-byte aligned");
 
   char* w = static_cast<char*>(ws);
   double* xh = reinterpret_cast<double*>(w + P.off_xh);
@@ -392,38 +618,55 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
     if (cudaMemcpyAsync(const_cast<double*>(Xd), X, xy_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
       return cuda_check("H2D copy of X");
   }
+  const int64_t km = (int64_t)k * nrhs;
   const bool coupled = (k > 0 && P.p > 0);
   if (coupled) {
     // Step 1: v_i^p = V_i^T X(I_i) for every leaf (node size b: always complete)
-    hm::VtParams vp;
-    memset(&vp, 0, sizeof vp);
-    vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile; vp.nlev = 1;
-    vp.lev[0].V = V; vp.lev[0].k = k; vp.lev[0].s = P.b;
-    vp.lev[0].out = xh + (((int64_t)1 << P.p) - 2) * k * nrhs;
-    vp.lev[0].partial = nullptr;
-    size_t smem = sizeof(double) * (size_t)(P.tile * P.mc_vt + hm::kThreads);
-    if ((st = vt_contract(vp, P.n, smem, stream))) return st;
+    double* xleaf = xh + (((int64_t)1 << P.p) - 2) * km;
+    if (P.vt == VtPath::kMma) {
+      hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
+      if ((st = vt_batched_dispatch("vt_contract", bp, k, P.nt_vt, stream))) return st;
+    } else {
+      hm::VtParams vp;
+      memset(&vp, 0, sizeof vp);
+      vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile; vp.nlev = 1;
+      vp.lev[0].V = V; vp.lev[0].k = k; vp.lev[0].s = P.b;
+      vp.lev[0].out = xleaf;
+      vp.lev[0].partial = nullptr;
+      st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
+      if (st) return st;
+    }
     // Step 1 (cont.): upsweep l = p-1 .. 1 through W^T
     for (int l = P.p - 1; l >= 1; --l) {
-      hm::HssLevelParams hp{W, B, xh, yh, l, k, nrhs, 0};
-      int64_t total = ((int64_t)1 << l) * k * nrhs;
-      unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
-      int slot = prof_begin("hss_up_level", stream);
-      hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp);
-      prof_end(slot, stream);
-      ++g_launches;
-      if ((st = cuda_check("hss_up_level_kernel"))) return st;
+      if (P.mma_levels) {
+        hm::BatchedVtParams bp{W + (((int64_t)1 << l) - 2) * 2 * k * k, 2ll * k * k,
+                               xh + (((int64_t)1 << (l + 1)) - 2) * km, 2 * km,
+                               xh + (((int64_t)1 << l) - 2) * km, km, (int64_t)1 << l, 2 * k, nrhs};
+        if ((st = vt_batched_dispatch("hss_up_level", bp, k, P.nt_vt ? P.nt_vt : nt_for(nrhs, k == 64 ? 2 : 4),
+                                      stream)))
+          return st;
+      } else {
+        hm::HssLevelParams hp{W, B, xh, yh, l, k, nrhs, 0};
+        const int64_t total = ((int64_t)1 << l) * km;
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+        st = launch("hss_up_level", stream,
+                    [&] { hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+        if (st) return st;
+      }
     }
     // Steps 2+3: coupling on level l (cores of the parents) + downsweep from l-1
     for (int l = 1; l <= P.p; ++l) {
-      hm::HssLevelParams hp{R, B, xh, yh, l, k, nrhs, 0};
-      int64_t total = ((int64_t)1 << l) * k * nrhs;
-      unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
-      int slot = prof_begin("hss_down_level", stream);
-      hm::hss_down_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp);
-      prof_end(slot, stream);
-      ++g_launches;
-      if ((st = cuda_check("hss_down_level_kernel"))) return st;
+      if (P.mma_levels) {
+        hm::HssDownParams dp{B, R, xh, yh, l, nrhs};
+        if ((st = hss_down_dispatch(dp, k, P.nt_down, stream))) return st;
+      } else {
+        hm::HssLevelParams hp{R, B, xh, yh, l, k, nrhs, 0};
+        const int64_t total = ((int64_t)1 << l) * km;
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+        st = launch("hss_down_level", stream,
+                    [&] { hm::hss_down_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+        if (st) return st;
+      }
     }
   }
   // Step 4: Y(I_i) = U_i y_i^p + D_i X(I_i)
@@ -433,11 +676,11 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   if (coupled) {
     hm::LeafSeg& sg = lp.seg[lp.nseg++];
     sg.A = U;
-    sg.T = yh + (((int64_t)1 << P.p) - 2) * k * nrhs;
+    sg.T = yh + (((int64_t)1 << P.p) - 2) * km;
     sg.k = k; sg.shift = 0; sg.xr = 0;
     lp.ktot = k;
   }
-  if ((st = leaf_apply(lp, 1ll << P.p, P.mc_leaf, stream))) return st;
+  if ((st = leaf_dispatch(lp, 1ll << P.p, P.leaf, coupled ? k : 0, P.nt_leaf, P.mc_leaf, stream))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");

@@ -1,0 +1,581 @@
+// hm_fast.cuh — the tuned sm_100a kernels. The generic kernels in
+// hm_kernels.cuh remain as the fallback for shapes these do not cover (leaf
+// sizes not multiple of 64, ranks that are not 8/16/32/64, ...).
+//
+// nrhs == 1  (HBM-bound GEMV regime, BASELINE configs 3 (m=1) and 5):
+//   vt_gemv_kernel<K>   all levels' V_l^T x in one pass over row tiles;
+//   leaf_gemv_kernel<K> per leaf y = D_i x_i + sum_l U_l(I_i) t_l.
+//   128-bit streaming loads (ld.global.cs), warp-shuffle reductions,
+//   fixed-order cross-warp sums through shared memory.
+// nrhs >= 2  (fp64 tensor-core regime, configs 2, 3 (m=8,64), 4):
+//   DMMA = mma.sync.aligned.m8n8k4.row.col.f64 (SASS DMMA.8x8x4) — on sm_100a
+//   the fp64 tensor path; tcgen05.mma has no f64 kind. Fragments are fed
+//   straight from 128-bit global loads, permuting the contraction index so that
+//   one LDG.128 feeds two DMMAs (the sum is order-free in exact arithmetic):
+//     leaf_mma_kernel       Y_i = [D_i | U_1 | .. | U_S](I_i) . [X_i; T_1; ..; T_S]
+//     vt_batched_kernel     t_j = A_j^T B_j for a batch of segments (HSS Step 1
+//                           per leaf; HSS upsweep per node with A = W, B = children)
+//     vt_mma_levels_kernel  HODLR: every level's V_l^T X over 8-leaf row tiles
+//     hss_down_mma_kernel   HSS coupling + downsweep per node:
+//                           y_j = S_w x_sib + R_w y_parent
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hm_kernels.cuh"
+
+namespace hm {
+
+// ------------------------------------------------------------ primitives --
+
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+// D (8x8) += A (8x4, row) * B (4x8, col). Lane l holds a = A[l>>2][l&3],
+// b = B[l&3][l>>2], c0/c1 = C[l>>2][2(l&3)], C[l>>2][2(l&3)+1].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) v += __shfl_xor_sync(0xffffffffu, v, w);
+  return v;
+}
+
+// =================================================================== m == 1 ==
+
+// vt_gemv: one CTA = 8 warps = 8 leaves (tile = 8 b rows); warp w owns the b
+// rows of leaf w of the tile. For every level: the warp streams V_l over its
+// rows as consecutive 128-bit chunks (64 doubles per warp instruction, i.e.
+// 64/K rows), lane l always sees the same rank columns a = (2l) % K, (2l+1) % K,
+// so accumulation stays in registers; then a butterfly over the lanes sharing
+// a column, and a fixed-order sum over the warps of each node.
+struct VtGemvParams {
+  const double* X;   // [n]
+  int64_t n, b;
+  int32_t nlev;
+  VtLevel lev[kMaxLevels];  // partial used for levels with s > 8 b
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) vt_gemv_kernel(const VtGemvParams P) {
+  static_assert(K == 1 || K == 2 || K == 4 || K == 8 || K == 16 || K == 32 || K == 64, "K");
+  constexpr int kPerChunk = 64;                 // doubles per warp instruction (32 lanes x 2)
+  constexpr int kRowsPerChunk = (K >= 64) ? 1 : kPerChunk / K;
+  constexpr int kChunksPerRow = (K >= 64) ? K / kPerChunk : 1;
+  __shared__ double red[8][K];
+  extern __shared__ double xs_all[];  // x of the tile, [8 b]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = P.b;
+  const int64_t tile = 8 * b;
+  const int64_t row0 = (int64_t)blockIdx.x * tile + (int64_t)warp * b;  // this warp's leaf
+  for (int64_t e = threadIdx.x; e < tile; e += 256) xs_all[e] = __ldg(P.X + (int64_t)blockIdx.x * tile + e);
+  __syncthreads();
+  const double* xw = xs_all + (int64_t)warp * b;
+  for (int L = 0; L < P.nlev; ++L) {
+    const VtLevel lv = P.lev[L];
+    const double* V = lv.V + row0 * K;
+    const int64_t nchunk = b * K / kPerChunk;    // b % 64 == 0 guaranteed by dispatch
+    double acc0 = 0.0, acc1 = 0.0;
+    int64_t c = 0;
+#pragma unroll 1
+    for (; c + 4 <= nchunk; c += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ldg_stream2(V + (c + u) * kPerChunk + 2 * lane);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = (c + u) * kPerChunk + 2 * lane;  // element index within the warp's block
+        const int64_t r = e / K;
+        if (K == 1) {
+          const double2 x = *reinterpret_cast<const double2*>(xw + r);
+          acc0 = fma(v[u].x, x.x, acc0);
+          acc1 = fma(v[u].y, x.y, acc1);
+        } else {
+          const double x = xw[r];
+          acc0 = fma(v[u].x, x, acc0);
+          acc1 = fma(v[u].y, x, acc1);
+        }
+      }
+    }
+    for (; c < nchunk; ++c) {
+      const double2 v = ldg_stream2(V + c * kPerChunk + 2 * lane);
+      const int64_t e = c * kPerChunk + 2 * lane;
+      const int64_t r = e / K;
+      if (K == 1) {
+        acc0 = fma(v.x, xw[r], acc0);
+        acc1 = fma(v.y, xw[r + 1], acc1);
+      } else {
+        const double x = xw[r];
+        acc0 = fma(v.x, x, acc0);
+        acc1 = fma(v.y, x, acc1);
+      }
+    }
+    // lanes sharing rank column: l == l' (mod K/2) (K >= 2); K == 1: everyone
+    if (K == 1) {
+      double s = warp_sum(acc0 + acc1);
+      if (lane == 0) red[warp][0] = s;
+    } else if (K < 64) {
+#pragma unroll
+      for (int w = 16; w >= K / 2 && w >= 1; w >>= 1) {
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, w);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, w);
+      }
+      if (lane < K / 2) {
+        red[warp][2 * lane] = acc0;
+        red[warp][2 * lane + 1] = acc1;
+      }
+    } else {
+      red[warp][2 * lane] = acc0;
+      red[warp][2 * lane + 1] = acc1;
+    }
+    (void)kRowsPerChunk;
+    (void)kChunksPerRow;
+    __syncthreads();
+    // combine warps: node size s (multiple of b): groups of g = min(8, s/b) warps
+    const int64_t g = lv.s >= tile ? 8 : lv.s / b;
+    const int ngroups = (int)(8 / g);
+    for (int o = threadIdx.x; o < ngroups * K; o += 256) {
+      const int grp = o / K, a = o - grp * K;
+      double s = 0.0;
+      for (int w = 0; w < g; ++w) s += red[grp * g + w][a];
+      const int64_t rfirst = (int64_t)blockIdx.x * tile + grp * g * b;
+      if (lv.s > tile) {
+        lv.partial[(int64_t)blockIdx.x * K + a] = s;
+      } else {
+        lv.out[(rfirst / lv.s) * K + a] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// leaf_gemv: one CTA (256 threads) per leaf. D part: warp w owns rows
+// w, w+8, ...; a row is b doubles = b/64 128-bit chunks per lane, 4 rows in
+// flight per warp. U part: thread-per-row over every segment (K columns each).
+template <int K>
+__global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
+  extern __shared__ double sm[];
+  const int64_t leaf = blockIdx.x;
+  const int64_t b = P.b;
+  const int64_t r0 = leaf * b;
+  double* xs = sm;            // [b]
+  double* yd = sm + b;        // [b]
+  double* ts = sm + 2 * b;    // [nseg][K]
+  for (int64_t e = threadIdx.x; e < b; e += 256) xs[e] = __ldg(P.X + r0 + e);
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    const int64_t node = (leaf >> sg.shift) ^ sg.xr;
+    for (int a = threadIdx.x; a < K; a += 256) ts[s * K + a] = __ldg(sg.T + node * K + a);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Di = P.D + leaf * b * b;
+  const int nch = (int)(b / 64);
+  // rows warp, warp+8, ... processed 4 at a time
+  for (int64_t rb = warp; rb < b; rb += 32) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = 0; c < nch; ++c) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t r = rb + 8 * u;
+        v[u] = (r < b) ? ldg_stream2(Di + r * b + 64 * c + 2 * lane) : make_double2(0.0, 0.0);
+      }
+      const double2 x = *reinterpret_cast<const double2*>(xs + 64 * c + 2 * lane);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(v[u].y, x.y, fma(v[u].x, x.x, acc[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double s = warp_sum(acc[u]);
+      const int64_t r = rb + 8 * u;
+      if (lane == 0 && r < b) yd[r] = s;
+    }
+  }
+  // U part, thread per row
+  double yu[4];
+  int nr = 0;
+  for (int64_t r = threadIdx.x; r < b; r += 256, ++nr) {
+    double u = 0.0;
+    for (int s = 0; s < P.nseg; ++s) {
+      const double* Ur = P.seg[s].A + (r0 + r) * K;
+      const double* t = ts + s * K;
+      if (K == 1) {
+        u = fma(ldg_stream(Ur), t[0], u);
+      } else {
+#pragma unroll
+        for (int a = 0; a < K; a += 2) {
+          const double2 w = ldg_stream2(Ur + a);
+          u = fma(w.y, t[a + 1], fma(w.x, t[a], u));
+        }
+      }
+    }
+    if (nr < 4) yu[nr] = u;
+  }
+  __syncthreads();
+  nr = 0;
+  for (int64_t r = threadIdx.x; r < b; r += 256, ++nr) P.Y[r0 + r] = yd[r] + yu[nr];
+}
+
+// =================================================================== m >= 2 ==
+
+// One warp accumulates C (8 RG rows x 8 NT cols) += E (rows, K) . Z (K, cols)
+// where E rows are row-major in global memory (lda) and Z (row stride zs) is
+// in shared memory (ZG = false, zero-padded columns) or global memory (ZG =
+// true, columns >= zvalid read as 0). K % 8 == 0. One LDG.128 per row group
+// and 8 k-indices feeds two DMMAs: k = kc+2j (".x") and kc+2j+1 (".y"),
+// j = lane & 3 — a permutation of the contraction index.
+template <int RG, int NT, bool ZG>
+__device__ __forceinline__ void warp_rowmajor_mma(double (&acc)[RG][NT][2], const double* __restrict__ E, int64_t lda,
+                                                  int K, const double* Z, int64_t zs, int zvalid, int lane) {
+  const int j = lane & 3, i = lane >> 2;
+  const double* base = E + (int64_t)i * lda + 2 * j;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = !ZG || (nt * 8 + i) < zvalid;
+  constexpr int PF = 4;  // 8-wide k-chunks in flight per row group
+  const int nq = K / 8;
+  int q = 0;
+#pragma unroll 1
+  for (; q + PF <= nq; q += PF) {
+    double2 a[PF][RG];
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg) a[u][rg] = ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * (q + u));
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const double* zr = Z + (int64_t)(8 * (q + u) + 2 * j) * zs + i;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double b0 = colok[nt] ? (ZG ? __ldg(zr + nt * 8) : zr[nt * 8]) : 0.0;
+        const double b1 = colok[nt] ? (ZG ? __ldg(zr + zs + nt * 8) : zr[zs + nt * 8]) : 0.0;
+#pragma unroll
+        for (int rg = 0; rg < RG; ++rg) {
+          dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].x, b0);
+          dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].y, b1);
+        }
+      }
+    }
+  }
+  for (; q < nq; ++q) {
+    double2 a[RG];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) a[rg] = ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * q);
+    const double* zr = Z + (int64_t)(8 * q + 2 * j) * zs + i;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double b0 = colok[nt] ? (ZG ? __ldg(zr + nt * 8) : zr[nt * 8]) : 0.0;
+      const double b1 = colok[nt] ? (ZG ? __ldg(zr + zs + nt * 8) : zr[zs + nt * 8]) : 0.0;
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg) {
+        dmma(acc[rg][nt][0], acc[rg][nt][1], a[rg].x, b0);
+        dmma(acc[rg][nt][0], acc[rg][nt][1], a[rg].y, b1);
+      }
+    }
+  }
+}
+
+// leaf_mma: grid (chunks of NT*8 columns, leaves); 8 warps; warp w owns rows
+// [w*8*RG, (w+1)*8*RG) of the leaf (b = 64 RG). Z = [X_i; T_1; ..; T_S] staged
+// in shared memory with row stride NT*8+4 (conflict-free B fragments).
+template <int RG, int NT>
+__global__ void __launch_bounds__(256) leaf_mma_kernel(const LeafParams P) {
+  extern __shared__ double sm[];
+  constexpr int MC = NT * 8;
+  constexpr int ZS = MC + 4;
+  const int nchunks = (P.m + MC - 1) / MC;
+  const int64_t leaf = blockIdx.x / nchunks;
+  const int c0 = (int)(blockIdx.x - leaf * nchunks) * MC;
+  const int64_t b = P.b;  // == 64 * RG
+  const int64_t r0 = leaf * b;
+  const int m = P.m;
+  double* Z = sm;
+  for (int64_t e = threadIdx.x; e < b * MC; e += 256) {
+    const int64_t r = e / MC;
+    const int c = (int)(e - r * MC);
+    Z[r * ZS + c] = (c0 + c < m) ? __ldg(P.X + (r0 + r) * m + c0 + c) : 0.0;
+  }
+  int64_t zoff = b;
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    const int64_t node = (leaf >> sg.shift) ^ sg.xr;
+    const double* T = sg.T + node * sg.k * m;
+    for (int e = threadIdx.x; e < sg.k * MC; e += 256) {
+      const int a = e / MC, c = e - a * MC;
+      Z[(zoff + a) * ZS + c] = (c0 + c < m) ? __ldg(T + a * m + c0 + c) : 0.0;
+    }
+    zoff += sg.k;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[RG][NT][2];
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
+  const int64_t wrow = (int64_t)warp * 8 * RG;
+  warp_rowmajor_mma<RG, NT, false>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
+  zoff = b;
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    warp_rowmajor_mma<RG, NT, false>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS, MC, lane);
+    zoff += sg.k;
+  }
+  const int i = lane >> 2, j = lane & 3;
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    double* y = P.Y + (r0 + wrow + 8 * rg + i) * m;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * j;
+      if (c + 1 < m) {
+        if ((m & 1) == 0) {
+          *reinterpret_cast<double2*>(y + c) = make_double2(acc[rg][nt][0], acc[rg][nt][1]);
+        } else {
+          y[c] = acc[rg][nt][0];
+          y[c + 1] = acc[rg][nt][1];
+        }
+      } else if (c < m) {
+        y[c] = acc[rg][nt][0];
+      }
+    }
+  }
+}
+
+// One warp accumulates C (KT x 8 NT) += A^T B over K rows, A [K][KT] row-major
+// (ld = KT), B [K][ldb] (columns c0.. of B). The 4 rows of one k-step are rows
+// r + (lane & 3). One LDG.128 of A covers 16 rank columns: ".x" feeds the tile
+// of even columns, ".y" the tile of odd columns (output rows permuted back at
+// the store). KT in {16, 32, 64}; K % 4 == 0.
+template <int KT, int NT, bool STREAM>
+__device__ __forceinline__ void warp_transposed_mma(double (&acc)[KT / 8][NT][2], const double* __restrict__ A,
+                                                    const double* __restrict__ B, int64_t ldb, int c0, int m,
+                                                    int K, int lane) {
+  constexpr int MP = KT / 16;
+  const int j = lane & 3, i = lane >> 2;
+  const double* ap = A + (int64_t)j * KT + 2 * i;
+  const double* bp = B + (int64_t)j * ldb + c0 + i;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = (c0 + nt * 8 + i) < m;
+  constexpr int PF = 4;
+  int q = 0;
+#pragma unroll 1
+  for (; q + PF <= K / 4; q += PF) {
+    double2 a[PF][MP];
+    double bf[PF][NT];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+#pragma unroll
+      for (int mp = 0; mp < MP; ++mp) {
+        const double* p = ap + (int64_t)(q + u) * 4 * KT + mp * 16;
+        a[u][mp] = STREAM ? ldg_stream2(p) : ldg2(p);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? __ldg(bp + (int64_t)(q + u) * 4 * ldb + nt * 8) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+#pragma unroll
+      for (int mp = 0; mp < MP; ++mp)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[u][mp].x, bf[u][nt]);
+          dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[u][mp].y, bf[u][nt]);
+        }
+  }
+  for (; q < K / 4; ++q) {
+    double2 a[MP];
+    double bf[NT];
+#pragma unroll
+    for (int mp = 0; mp < MP; ++mp) {
+      const double* p = ap + (int64_t)q * 4 * KT + mp * 16;
+      a[mp] = STREAM ? ldg_stream2(p) : ldg2(p);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bf[nt] = colok[nt] ? __ldg(bp + (int64_t)q * 4 * ldb + nt * 8) : 0.0;
+#pragma unroll
+    for (int mp = 0; mp < MP; ++mp)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[mp].x, bf[nt]);
+        dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[mp].y, bf[nt]);
+      }
+  }
+}
+
+// Store (or stage) a warp's KT x 8NT result: tile t = 2 mp + e holds rank
+// columns a = 16 mp + 2 i + e for i = lane >> 2; columns c0 + 8 nt + 2 (lane&3) + {0,1}.
+template <int KT, int NT>
+__device__ __forceinline__ void store_transposed(const double (&acc)[KT / 8][NT][2], double* out, int64_t ldo, int c0,
+                                                 int m, int lane, int cbase = 0) {
+  const int i = lane >> 2, j = lane & 3;
+#pragma unroll
+  for (int t = 0; t < KT / 8; ++t) {
+    const int a = 16 * (t >> 1) + 2 * i + (t & 1);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * j;
+      double* o = out + (int64_t)a * ldo + (c - cbase);
+      if (c + 1 < m) {
+        o[0] = acc[t][nt][0];
+        o[1] = acc[t][nt][1];
+      } else if (c < m) {
+        o[0] = acc[t][nt][0];
+      }
+    }
+  }
+}
+
+// Batched t_j = A_j^T B_j (K x KT)^T (K x m): one warp per segment j.
+struct BatchedVtParams {
+  const double* A;  int64_t a_stride;   // A_j = A + j * a_stride, [K][KT]
+  const double* B;  int64_t b_stride;   // B_j = B + j * b_stride, [K][m]
+  double* out;      int64_t o_stride;   // out_j = out + j * o_stride, [KT][m]
+  int64_t count;
+  int32_t K, m;
+};
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) vt_batched_kernel(const BatchedVtParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t jseg = (int64_t)blockIdx.x * 8 + warp;
+  if (jseg >= P.count) return;
+  for (int c0 = 0; c0 < P.m; c0 += NT * 8) {
+    double acc[KT / 8][NT][2];
+#pragma unroll
+    for (int t = 0; t < KT / 8; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+    warp_transposed_mma<KT, NT, true>(acc, P.A + jseg * P.a_stride, P.B + jseg * P.b_stride, P.m, c0, P.m, P.K, lane);
+    store_transposed<KT, NT>(acc, P.out + jseg * P.o_stride, P.m, c0, P.m, lane);
+  }
+}
+
+// HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
+// Per level: warp partial t over its b rows (DMMA), staged in shared memory,
+// then fixed-order sums over the warps of each node.
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, int64_t b) {
+  extern __shared__ double red[];  // [8][KT][MC]
+  constexpr int MC = NT * 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = 8 * b;
+  const int64_t row0 = (int64_t)blockIdx.x * tile + (int64_t)warp * b;
+  const int m = P.m;
+  for (int c0 = 0; c0 < m; c0 += MC) {
+    const int mc = min(MC, m - c0);
+    for (int L = 0; L < P.nlev; ++L) {
+      const VtLevel lv = P.lev[L];
+      double acc[KT / 8][NT][2];
+#pragma unroll
+      for (int t = 0; t < KT / 8; ++t)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+      warp_transposed_mma<KT, NT, true>(acc, lv.V + row0 * KT, P.X + row0 * m, m, c0, m, (int)b, lane);
+      store_transposed<KT, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
+      __syncthreads();
+      const int64_t g = lv.s >= tile ? 8 : lv.s / b;
+      const int ngroups = (int)(8 / g);
+      for (int o = threadIdx.x; o < ngroups * KT * mc; o += 256) {
+        const int grp = o / (KT * mc);
+        const int rem = o - grp * KT * mc;
+        const int a = rem / mc, c = rem - a * mc;
+        double s = 0.0;
+        for (int w = 0; w < g; ++w) s += red[((int64_t)(grp * g + w) * KT + a) * MC + c];
+        const int64_t rfirst = (int64_t)blockIdx.x * tile + grp * g * b;
+        if (lv.s > tile) {
+          lv.partial[((int64_t)blockIdx.x * KT + a) * m + c0 + c] = s;
+        } else {
+          lv.out[((rfirst / lv.s) * KT + a) * m + c0 + c] = s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// HSS coupling + downsweep on level l (reading G1), one warp per
+// node j: y_j = S_w x_{j^1} + [l >= 2] R_w y_parent, w = j & 1, as one
+// row-major product [S_w | R_w] (k x 2k) . [x_{j^1}; y_parent] (2k x m).
+struct HssDownParams {
+  const double* B;   // cores  [2^p-1][2][k][k]
+  const double* R;   // transl [2^p-2][2k][k]
+  const double* xh;  // level-major coefficient blocks [k][m]
+  double* yh;
+  int32_t level, m;
+};
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) hss_down_mma_kernel(const HssDownParams P) {
+  constexpr int MC = NT * 8;
+  constexpr int RG = KT / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int l = P.level, m = P.m;
+  const int64_t cnt = 1ll << l;
+  const int64_t j = (int64_t)blockIdx.x * 8 + warp;
+  if (j >= cnt) return;
+  const int64_t km = (int64_t)KT * m;
+  const int64_t q = j >> 1;
+  const int w = (int)(j & 1);
+  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * KT * KT;
+  const double* xs = P.xh + ((1ll << l) - 2 + (j ^ 1)) * km;
+  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + w * KT) * KT : nullptr;
+  const double* yp = (l >= 2) ? P.yh + ((1ll << (l - 1)) - 2 + q) * km : nullptr;
+  double* yo = P.yh + ((1ll << l) - 2 + j) * km;
+  const int i = lane >> 2, jj = lane & 3;
+  for (int c0 = 0; c0 < m; c0 += MC) {
+    double acc[RG][NT][2];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
+    warp_rowmajor_mma<RG, NT, true>(acc, S, KT, KT, xs + c0, m, m - c0, lane);
+    if (Rw) {
+      // coupling first, then the downsweep term added (P:707-716 order)
+      double acc2[RG][NT][2];
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc2[rg][nt][0] = acc2[rg][nt][1] = 0.0;
+      warp_rowmajor_mma<RG, NT, true>(acc2, Rw, KT, KT, yp + c0, m, m - c0, lane);
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[rg][nt][0] += acc2[rg][nt][0];
+          acc[rg][nt][1] += acc2[rg][nt][1];
+        }
+    }
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) {
+      double* y = yo + (int64_t)(8 * rg + i) * m;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = c0 + nt * 8 + 2 * jj;
+        if (c + 1 < m) {
+          y[c] = acc[rg][nt][0];
+          y[c + 1] = acc[rg][nt][1];
+        } else if (c < m) {
+          y[c] = acc[rg][nt][0];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace hm

@@ -78,6 +78,12 @@ HODLR_CASES = [
     (65536, 256, 8, 16, 1),     # many row tiles: partial sums on the top levels
     (65536, 128, 9, 4, 64),
     (4096, 1, 12, 1, 1),        # leaf size 1 (Fig. 1's n_min = 1)
+    (65536, 256, 8, 16, 64),    # config-3 shapes (DMMA paths), smaller depth
+    (65536, 128, 9, 32, 33),    # DMMA paths, ragged column chunk
+    (32768, 64, 9, 16, 2),
+    (8192, 256, 5, 16, 8),
+    (16384, 64, 8, 2, 1),       # GEMV paths, rank 2
+    (32768, 128, 8, 64, 1),     # GEMV paths, rank 64
 ]
 
 
@@ -100,6 +106,10 @@ HSS_CASES = [
     (8192, 64, 7, 64, 3),       # maximum rank
     (32768, 128, 8, 32, 32),    # config-4 shapes at a smaller depth
     (4096, 64, 6, 16, 33),      # ragged column chunk
+    (8192, 64, 7, 16, 1),       # GEMV paths
+    (16384, 256, 6, 32, 8),
+    (16384, 128, 7, 64, 5),
+    (2048, 128, 4, 16, 2),
 ]
 
 

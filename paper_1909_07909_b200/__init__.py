@@ -18,7 +18,7 @@ import os
 from typing import Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhm.so")
+LIB_PATH = os.environ.get("HM_LIBHM") or os.path.join(_PKG, "libhm.so")  # HM_LIBHM: dev variants only
 
 HM_OK, HM_ERR_INVALID_ARG, HM_ERR_UNSUPPORTED, HM_ERR_WORKSPACE, HM_ERR_CUDA, HM_ERR_NCCL = 0, -1, -2, -3, -4, -5
 HM_WS_HOSTIO = 1

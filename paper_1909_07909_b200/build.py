@@ -41,12 +41,15 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile every csrc/*.cu into `out` (default: the in-tree libhm.so). `defines`
+    (e.g. ["HM_LEAF_PF=2"]) build development variants under another name."""
+    if not force and out == LIB and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
+           *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:
@@ -56,10 +59,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), LIB)
+    print(build(force="--force" in args or out != LIB, verbose=True, defines=defs, out=out))

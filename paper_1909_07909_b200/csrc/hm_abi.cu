@@ -17,6 +17,7 @@
 #include "../../include/hm.h"
 #include "hm_kernels.cuh"
 #include "hm_fast.cuh"
+#include "hm_tree.cuh"
 
 namespace {
 
@@ -136,6 +137,12 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 // ---------------------------------------------------------------- dispatch --
+#ifndef HM_VTB_NTMAX
+#define HM_VTB_NTMAX 4
+#endif
+#ifndef HM_TREE_NTMAX
+#define HM_TREE_NTMAX 4
+#endif
 // Which kernels run is decided on the host from the shapes:
 // the tuned kernels of hm_fast.cuh where their shape conditions hold, the
 // generic kernels of hm_kernels.cuh otherwise. Both are exact implementations
@@ -279,13 +286,22 @@ hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream
   return launch("leaf_apply", s, [&] { hm::leaf_gemv_kernel<K><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
 }
 
+// (RG, NT) -> prefetch depth and launch-bound occupancy (measured, r01_tuning.md)
+template <int RG, int NT>
+struct LeafMmaTune {
+  static constexpr int PF = (RG == 2 && NT == 4) ? 1 : 2;
+  static constexpr int MINB = (RG == 2 && NT == 4) ? 4 : 0;
+};
+
 template <int RG, int NT>
 hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  constexpr int PF = LeafMmaTune<RG, NT>::PF, MINB = LeafMmaTune<RG, NT>::MINB;
   size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * (NT * 8 + 4));
-  allow_smem(hm::leaf_mma_kernel<RG, NT>, smem);
+  allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB>, smem);
   const int64_t chunks = (lp.m + NT * 8 - 1) / (NT * 8);
-  return launch("leaf_apply", s,
-                [&] { hm::leaf_mma_kernel<RG, NT><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp); });
+  return launch("leaf_apply", s, [&] {
+    hm::leaf_mma_kernel<RG, NT, PF, MINB><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp);
+  });
 }
 
 hm_status leaf_dispatch(const hm::LeafParams& lp, int64_t nleaves, LeafPath path, int k, int nt, int mc,
@@ -382,8 +398,11 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
 
 template <int KT, int NT>
 hm_status vt_batched_launch(const char* name, const hm::BatchedVtParams& bp, cudaStream_t s) {
+  constexpr int MPW = 1;
+  const int64_t nck = (bp.m + NT * 8 - 1) / (NT * 8);
+  const int64_t warps = bp.count * (KT / 16 / MPW) * nck;
   return launch(name, s, [&] {
-    hm::vt_batched_kernel<KT, NT><<<(unsigned)((bp.count + 7) / 8), 256, 0, s>>>(bp);
+    hm::vt_batched_kernel<KT, MPW, NT><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(bp);
   });
 }
 
@@ -392,7 +411,7 @@ hm_status vt_batched_dispatch(const char* name, const hm::BatchedVtParams& bp, i
   if (k == KT_) {                                                   \
     if (nt == 1) return vt_batched_launch<KT_, 1>(name, bp, s);     \
     if (nt == 2) return vt_batched_launch<KT_, 2>(name, bp, s);     \
-    if constexpr (KT_ < 64) return vt_batched_launch<KT_, 4>(name, bp, s); \
+    return vt_batched_launch<KT_, 4>(name, bp, s);                  \
   }
   HM_VTB(16)
   HM_VTB(32)
@@ -455,6 +474,11 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
           rl.nodes = 1ll << l;
           rl.per_node = (int32_t)(s / P.tile);
           rl.km = k * nrhs;
+          int lg = 0;
+          while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
+          rl.log2g = lg;
+          rl.thread_begin = rp.threads;
+          rp.threads += ((rl.nodes * rl.km << lg) + 31) / 32 * 32;
         }
       }
       uoff += P.n * k;
@@ -464,7 +488,7 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     else st = vt_generic(vp, P.n, stream);
     if (st) return st;
     if (rp.nlev > 0) {
-      dim3 grid(64, rp.nlev);
+      const unsigned grid = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
       st = launch("reduce_partials", stream,
                   [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp); });
       if (st) return st;
@@ -530,14 +554,14 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
     P->tile = 8 * b;
   } else if (nrhs >= 2 && b % 4 == 0 && pow2_rank(k, 16, 64)) {
     P->vt = VtPath::kMma;  // batched: one warp per leaf
-    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : 4);
+    P->nt_vt = nt_for(nrhs, HM_VTB_NTMAX);
   } else {
     P->vt = VtPath::kGeneric;
     P->mc_vt = vt_mc(b, nrhs);
     P->tile = pick_tile(b, P->p, P->mc_vt);
   }
   P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
-  if (P->mma_levels) P->nt_down = nt_for(nrhs, std::max(1, 8 / (k / 8)));
+  if (P->mma_levels) P->nt_down = nt_for(nrhs, HM_TREE_NTMAX);
   const int ktot = coupled ? k : 0;
   if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
     P->leaf = LeafPath::kGemv;
@@ -569,22 +593,93 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 template <int KT, int NT>
 hm_status hss_down_launch(const hm::HssDownParams& dp, cudaStream_t s) {
   const int64_t cnt = 1ll << dp.level;
+  const int64_t nck = (dp.m + NT * 8 - 1) / (NT * 8);
+  const int64_t warps = cnt * (KT / 8) * nck;
   return launch("hss_down_level", s,
-                [&] { hm::hss_down_mma_kernel<KT, NT><<<(unsigned)((cnt + 7) / 8), 256, 0, s>>>(dp); });
+                [&] { hm::hss_down_mma_kernel<KT, NT><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(dp); });
 }
 
 hm_status hss_down_dispatch(const hm::HssDownParams& dp, int k, int nt, cudaStream_t s) {
 #define HM_DOWN(KT_)                                              \
   if (k == KT_) {                                                 \
     if (nt == 1) return hss_down_launch<KT_, 1>(dp, s);           \
-    if constexpr (KT_ <= 32) { if (nt == 2) return hss_down_launch<KT_, 2>(dp, s); } \
-    if constexpr (KT_ <= 16) { if (nt == 4) return hss_down_launch<KT_, 4>(dp, s); } \
+    if (nt == 2) return hss_down_launch<KT_, 2>(dp, s);           \
+    return hss_down_launch<KT_, 4>(dp, s);                        \
   }
   HM_DOWN(16)
   HM_DOWN(32)
   HM_DOWN(64)
 #undef HM_DOWN
   return fail(HM_ERR_UNSUPPORTED, "hss_down: no instance for k=%d nt=%d", k, nt);
+}
+
+// Levels with at least kTreeBigLevel nodes run one launch per level; the
+// levels above run inside one cooperative launch (hss_tree_sweep_kernel).
+constexpr int64_t kTreeBigLevel = 2048;
+
+template <int KT, int NT>
+hm_status tree_launch(const hm::TreeParams& tp, int p, cudaStream_t s) {
+  constexpr int MINB = (KT == 32 && NT == 4) ? 3 : 0;  // measured, r01_tuning.md
+  const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
+  static bool attrs = false;
+  int sweep_blocks_per_sm = 0;
+  if (!attrs) {
+    allow_smem(hm::hss_up_pair_kernel<KT, NT, MINB>, 200 * 1024);
+    allow_smem(hm::hss_down_pair_kernel<KT, NT, MINB>, 200 * 1024);
+    allow_smem(hm::hss_tree_sweep_kernel<KT, NT>, 200 * 1024);
+    attrs = true;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sweep_blocks_per_sm, hm::hss_tree_sweep_kernel<KT, NT>, 256,
+                                                    smem) != cudaSuccess)
+    return cuda_check("occupancy query (hss_tree_sweep)");
+  int lbig = 1;  // first level with >= kTreeBigLevel nodes
+  while (lbig <= p && (1ll << lbig) < kTreeBigLevel) ++lbig;
+  hm_status st;
+  // upsweep: big levels p-1 .. lbig one launch each
+  for (int l = p - 1; l >= lbig; --l) {
+    const unsigned pairs = (unsigned)(1ll << (l - 1));
+    st = launch("hss_up_level", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    if (st) return st;
+  }
+  // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
+  const int up_from = std::min(p - 1, lbig - 1), down_to = std::min(p, lbig - 1);
+  if (up_from >= 1 || down_to >= 1) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t need = std::max<int64_t>(1, (1ll << std::max(up_from, down_to)) / 2);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sweep_blocks_per_sm * sms, need)));
+    hm::TreeParams arg = tp;
+    int a1 = up_from, a2 = 1, a3 = 1, a4 = down_to;
+    void* args[] = {&arg, &a1, &a2, &a3, &a4};
+    cudaError_t e = cudaSuccess;
+    st = launch("hss_tree_sweep", s, [&] {
+      e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_sweep_kernel<KT, NT>, grid, dim3(256), args, smem, s);
+    });
+    if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
+    if (st) return st;
+  }
+  // downsweep: big levels lbig .. p one launch each
+  for (int l = std::max(lbig, 1); l <= p; ++l) {
+    const unsigned pairs = (unsigned)(1ll << (l - 1));
+    st = launch("hss_down_level", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    if (st) return st;
+  }
+  return HM_OK;
+}
+
+hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, cudaStream_t s) {
+#define HM_TREE(KT_)                                           \
+  if (k == KT_) {                                              \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, s);         \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, s);         \
+    return tree_launch<KT_, 4>(tp, p, s);                      \
+  }
+  HM_TREE(16)
+  HM_TREE(32)
+  HM_TREE(64)
+#undef HM_TREE
+  return fail(HM_ERR_UNSUPPORTED, "hss tree: no instance for k=%d", k);
 }
 
 hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
@@ -636,16 +731,13 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
       st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
       if (st) return st;
     }
-    // Step 1 (cont.): upsweep l = p-1 .. 1 through W^T
-    for (int l = P.p - 1; l >= 1; --l) {
-      if (P.mma_levels) {
-        hm::BatchedVtParams bp{W + (((int64_t)1 << l) - 2) * 2 * k * k, 2ll * k * k,
-                               xh + (((int64_t)1 << (l + 1)) - 2) * km, 2 * km,
-                               xh + (((int64_t)1 << l) - 2) * km, km, (int64_t)1 << l, 2 * k, nrhs};
-        if ((st = vt_batched_dispatch("hss_up_level", bp, k, P.nt_vt ? P.nt_vt : nt_for(nrhs, k == 64 ? 2 : 4),
-                                      stream)))
-          return st;
-      } else {
+    if (P.mma_levels) {
+      // Step 1 (cont.) upsweep + Steps 2-3 coupling/downsweep: one cooperative launch
+      hm::TreeParams tp{W, R, B, xh, yh, nrhs, 0, 0, 0};
+      if ((st = tree_dispatch(tp, P.p, k, P.nt_down, stream))) return st;
+    } else {
+      // Step 1 (cont.): upsweep l = p-1 .. 1 through W^T
+      for (int l = P.p - 1; l >= 1; --l) {
         hm::HssLevelParams hp{W, B, xh, yh, l, k, nrhs, 0};
         const int64_t total = ((int64_t)1 << l) * km;
         const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
@@ -653,13 +745,8 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
                     [&] { hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
         if (st) return st;
       }
-    }
-    // Steps 2+3: coupling on level l (cores of the parents) + downsweep from l-1
-    for (int l = 1; l <= P.p; ++l) {
-      if (P.mma_levels) {
-        hm::HssDownParams dp{B, R, xh, yh, l, nrhs};
-        if ((st = hss_down_dispatch(dp, k, P.nt_down, stream))) return st;
-      } else {
+      // Steps 2+3: coupling on level l (cores of the parents) + downsweep from l-1
+      for (int l = 1; l <= P.p; ++l) {
         hm::HssLevelParams hp{R, B, xh, yh, l, k, nrhs, 0};
         const int64_t total = ((int64_t)1 << l) * km;
         const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);

@@ -19,6 +19,7 @@
 //     hss_down_mma_kernel   HSS coupling + downsweep per node:
 //                           y_j = S_w x_sib + R_w y_parent
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -39,6 +40,18 @@ __device__ __forceinline__ double ldg_stream(const double* p) {
   return v;
 }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+// Coherent (L2) load for data written earlier in the same launch (cooperative
+// kernels): never the non-coherent read-only path.
+__device__ __forceinline__ double ldg_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <bool COH>
+__device__ __forceinline__ double ld_operand(const double* p) {
+  if constexpr (COH) return ldg_cg(p);
+  else return __ldg(p);
+}
 
 // D (8x8) += A (8x4, row) * B (4x8, col). Lane l holds a = A[l>>2][l&3],
 // b = B[l&3][l>>2], c0/c1 = C[l>>2][2(l&3)], C[l>>2][2(l&3)+1].
@@ -232,13 +245,93 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
 
 // =================================================================== m >= 2 ==
 
+#ifndef HM_RM_PF
+#define HM_RM_PF 2
+#endif
+// Tuning: the DMMA kernels take MINB (minimum resident CTAs per SM for the
+// launch bounds; 0 = unconstrained) and the A-stream prefetch depth PF as
+// template parameters; the host picks them per shape (hm_abi.cu, measured on
+// B200: profiles/r01_tuning.md).
+
+// cp.async (LDGSTS) 16-byte global -> shared copies: the whole staging of a
+// block is in flight at once, with no register round trip.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Stage `rows` x `cols` doubles (global, row stride lds) into shared memory
+// rows of stride zs, zero-filling columns cols .. mp-1. All threads of the CTA
+// take part; the caller issues cp_async_wait_all() + __syncthreads(). cp.async.cg
+// reads through L2, so this is also coherent inside a cooperative kernel.
+__device__ __forceinline__ void stage_rows_async(double* dst, int zs, const double* src, int64_t lds, int rows,
+                                                 int cols, int mp) {
+  const bool vec = ((cols & 1) == 0) && ((lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                   ((zs & 1) == 0);
+  if (vec) {
+    const int h = cols >> 1;  // 16-byte chunks per row
+    for (int e = threadIdx.x; e < rows * h; e += blockDim.x) {
+      const int r = e / h, c = (e - r * h) * 2;
+      cp_async16(dst + r * zs + c, src + (int64_t)r * lds + c);
+    }
+  } else {
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+      const int r = e / cols, c = e - r * cols;
+      dst[r * zs + c] = ldg_cg(src + (int64_t)r * lds + c);
+    }
+  }
+  if (mp > cols)
+    for (int e = threadIdx.x; e < rows * (mp - cols); e += blockDim.x) {
+      const int r = e / (mp - cols), c = cols + (e - r * (mp - cols));
+      dst[r * zs + c] = 0.0;
+    }
+}
+
 // One warp accumulates C (8 RG rows x 8 NT cols) += E (rows, K) . Z (K, cols)
 // where E rows are row-major in global memory (lda) and Z (row stride zs) is
 // in shared memory (ZG = false, zero-padded columns) or global memory (ZG =
 // true, columns >= zvalid read as 0). K % 8 == 0. One LDG.128 per row group
 // and 8 k-indices feeds two DMMAs: k = kc+2j (".x") and kc+2j+1 (".y"),
-// j = lane & 3 — a permutation of the contraction index.
-template <int RG, int NT, bool ZG>
+// j = lane & 3 — a permutation of the contraction index. The A stream is
+// software-pipelined: groups of PF k-chunks ping-pong between two register
+// buffers, so the next group's loads are in flight while the current one
+// feeds the tensor pipe.
+template <int RG, int NT, bool ZG, bool COH, int PF>
+__device__ __forceinline__ void rm_group(double (&acc)[RG][NT][2], const double2 (&a)[PF][RG], const double* Z,
+                                         int64_t zs, int q, int nq, const bool (&colok)[NT], int lane) {
+  const int j = lane & 3, i = lane >> 2;
+#pragma unroll
+  for (int u = 0; u < PF; ++u) {
+    if (q + u >= nq) break;  // warp-uniform
+    const double* zr = Z + (int64_t)(8 * (q + u) + 2 * j) * zs + i;
+    double b0[NT], b1[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      b0[nt] = colok[nt] ? (ZG ? ld_operand<COH>(zr + nt * 8) : zr[nt * 8]) : 0.0;
+      b1[nt] = colok[nt] ? (ZG ? ld_operand<COH>(zr + zs + nt * 8) : zr[zs + nt * 8]) : 0.0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg) dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].x, b0[nt]);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int rg = 0; rg < RG; ++rg) dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].y, b1[nt]);
+  }
+}
+
+template <int RG, int PF>
+__device__ __forceinline__ void rm_load(double2 (&a)[PF][RG], const double* base, int64_t lda, int q, int nq) {
+#pragma unroll
+  for (int u = 0; u < PF; ++u)
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg)
+      a[u][rg] = (q + u < nq) ? ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * (q + u)) : make_double2(0.0, 0.0);
+}
+
+template <int RG, int NT, bool ZG, bool COH = false, int PF = HM_RM_PF>
 __device__ __forceinline__ void warp_rowmajor_mma(double (&acc)[RG][NT][2], const double* __restrict__ E, int64_t lda,
                                                   int K, const double* Z, int64_t zs, int zvalid, int lane) {
   const int j = lane & 3, i = lane >> 2;
@@ -246,54 +339,23 @@ __device__ __forceinline__ void warp_rowmajor_mma(double (&acc)[RG][NT][2], cons
   bool colok[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) colok[nt] = !ZG || (nt * 8 + i) < zvalid;
-  constexpr int PF = 4;  // 8-wide k-chunks in flight per row group
   const int nq = K / 8;
-  int q = 0;
-#pragma unroll 1
-  for (; q + PF <= nq; q += PF) {
-    double2 a[PF][RG];
-#pragma unroll
-    for (int u = 0; u < PF; ++u)
-#pragma unroll
-      for (int rg = 0; rg < RG; ++rg) a[u][rg] = ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * (q + u));
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const double* zr = Z + (int64_t)(8 * (q + u) + 2 * j) * zs + i;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double b0 = colok[nt] ? (ZG ? __ldg(zr + nt * 8) : zr[nt * 8]) : 0.0;
-        const double b1 = colok[nt] ? (ZG ? __ldg(zr + zs + nt * 8) : zr[zs + nt * 8]) : 0.0;
-#pragma unroll
-        for (int rg = 0; rg < RG; ++rg) {
-          dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].x, b0);
-          dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg].y, b1);
-        }
-      }
-    }
-  }
-  for (; q < nq; ++q) {
-    double2 a[RG];
-#pragma unroll
-    for (int rg = 0; rg < RG; ++rg) a[rg] = ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * q);
-    const double* zr = Z + (int64_t)(8 * q + 2 * j) * zs + i;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const double b0 = colok[nt] ? (ZG ? __ldg(zr + nt * 8) : zr[nt * 8]) : 0.0;
-      const double b1 = colok[nt] ? (ZG ? __ldg(zr + zs + nt * 8) : zr[zs + nt * 8]) : 0.0;
-#pragma unroll
-      for (int rg = 0; rg < RG; ++rg) {
-        dmma(acc[rg][nt][0], acc[rg][nt][1], a[rg].x, b0);
-        dmma(acc[rg][nt][0], acc[rg][nt][1], a[rg].y, b1);
-      }
-    }
+  double2 a0[PF][RG], a1[PF][RG];
+  rm_load<RG, PF>(a0, base, lda, 0, nq);
+  for (int q = 0; q < nq; q += 2 * PF) {
+    rm_load<RG, PF>(a1, base, lda, q + PF, nq);
+    rm_group<RG, NT, ZG, COH, PF>(acc, a0, Z, zs, q, nq, colok, lane);
+    if (q + PF >= nq) break;
+    rm_load<RG, PF>(a0, base, lda, q + 2 * PF, nq);
+    rm_group<RG, NT, ZG, COH, PF>(acc, a1, Z, zs, q + PF, nq, colok, lane);
   }
 }
 
 // leaf_mma: grid (chunks of NT*8 columns, leaves); 8 warps; warp w owns rows
 // [w*8*RG, (w+1)*8*RG) of the leaf (b = 64 RG). Z = [X_i; T_1; ..; T_S] staged
 // in shared memory with row stride NT*8+4 (conflict-free B fragments).
-template <int RG, int NT>
-__global__ void __launch_bounds__(256) leaf_mma_kernel(const LeafParams P) {
+template <int RG, int NT, int PF, int MINB>
+__global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   constexpr int MC = NT * 8;
   constexpr int ZS = MC + 4;
@@ -304,22 +366,16 @@ __global__ void __launch_bounds__(256) leaf_mma_kernel(const LeafParams P) {
   const int64_t r0 = leaf * b;
   const int m = P.m;
   double* Z = sm;
-  for (int64_t e = threadIdx.x; e < b * MC; e += 256) {
-    const int64_t r = e / MC;
-    const int c = (int)(e - r * MC);
-    Z[r * ZS + c] = (c0 + c < m) ? __ldg(P.X + (r0 + r) * m + c0 + c) : 0.0;
-  }
+  const int mc = min(MC, m - c0);
+  stage_rows_async(Z, ZS, P.X + r0 * m + c0, m, (int)b, mc, MC);
   int64_t zoff = b;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
     const int64_t node = (leaf >> sg.shift) ^ sg.xr;
-    const double* T = sg.T + node * sg.k * m;
-    for (int e = threadIdx.x; e < sg.k * MC; e += 256) {
-      const int a = e / MC, c = e - a * MC;
-      Z[(zoff + a) * ZS + c] = (c0 + c < m) ? __ldg(T + a * m + c0 + c) : 0.0;
-    }
+    stage_rows_async(Z + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
     zoff += sg.k;
   }
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[RG][NT][2];
@@ -328,11 +384,12 @@ __global__ void __launch_bounds__(256) leaf_mma_kernel(const LeafParams P) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
   const int64_t wrow = (int64_t)warp * 8 * RG;
-  warp_rowmajor_mma<RG, NT, false>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
+  warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
   zoff = b;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
-    warp_rowmajor_mma<RG, NT, false>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS, MC, lane);
+    warp_rowmajor_mma<RG, NT, false, false, PF>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS, MC,
+                                                        lane);
     zoff += sg.k;
   }
   const int i = lane >> 2, j = lane & 3;
@@ -356,18 +413,17 @@ __global__ void __launch_bounds__(256) leaf_mma_kernel(const LeafParams P) {
   }
 }
 
-// One warp accumulates C (KT x 8 NT) += A^T B over K rows, A [K][KT] row-major
-// (ld = KT), B [K][ldb] (columns c0.. of B). The 4 rows of one k-step are rows
-// r + (lane & 3). One LDG.128 of A covers 16 rank columns: ".x" feeds the tile
-// of even columns, ".y" the tile of odd columns (output rows permuted back at
-// the store). KT in {16, 32, 64}; K % 4 == 0.
-template <int KT, int NT, bool STREAM>
-__device__ __forceinline__ void warp_transposed_mma(double (&acc)[KT / 8][NT][2], const double* __restrict__ A,
-                                                    const double* __restrict__ B, int64_t ldb, int c0, int m,
-                                                    int K, int lane) {
-  constexpr int MP = KT / 16;
+// One warp accumulates C (16 MPW x 8 NT) += A^T B over K rows, A [K][lda]
+// row-major (the warp's rank columns start at A), B [K][ldb] (columns c0..).
+// The 4 rows of one k-step are rows r + (lane & 3). One LDG.128 of A covers 16
+// rank columns: ".x" feeds the tile of even columns, ".y" the tile of odd
+// columns (output rows permuted back at the store). K % 4 == 0.
+template <int MPW, int NT, bool COH = false>
+__device__ __forceinline__ void warp_transposed_mma(double (&acc)[2 * MPW][NT][2], const double* __restrict__ A,
+                                                    int64_t lda, const double* __restrict__ B, int64_t ldb, int c0,
+                                                    int m, int K, int lane) {
   const int j = lane & 3, i = lane >> 2;
-  const double* ap = A + (int64_t)j * KT + 2 * i;
+  const double* ap = A + (int64_t)j * lda + 2 * i;
   const double* bp = B + (int64_t)j * ldb + c0 + i;
   bool colok[NT];
 #pragma unroll
@@ -376,22 +432,19 @@ __device__ __forceinline__ void warp_transposed_mma(double (&acc)[KT / 8][NT][2]
   int q = 0;
 #pragma unroll 1
   for (; q + PF <= K / 4; q += PF) {
-    double2 a[PF][MP];
+    double2 a[PF][MPW];
     double bf[PF][NT];
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
 #pragma unroll
-      for (int mp = 0; mp < MP; ++mp) {
-        const double* p = ap + (int64_t)(q + u) * 4 * KT + mp * 16;
-        a[u][mp] = STREAM ? ldg_stream2(p) : ldg2(p);
-      }
+      for (int mp = 0; mp < MPW; ++mp) a[u][mp] = ldg_stream2(ap + (int64_t)(q + u) * 4 * lda + mp * 16);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? __ldg(bp + (int64_t)(q + u) * 4 * ldb + nt * 8) : 0.0;
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? ld_operand<COH>(bp + (int64_t)(q + u) * 4 * ldb + nt * 8) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < PF; ++u)
 #pragma unroll
-      for (int mp = 0; mp < MP; ++mp)
+      for (int mp = 0; mp < MPW; ++mp)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[u][mp].x, bf[u][nt]);
@@ -399,17 +452,14 @@ __device__ __forceinline__ void warp_transposed_mma(double (&acc)[KT / 8][NT][2]
         }
   }
   for (; q < K / 4; ++q) {
-    double2 a[MP];
+    double2 a[MPW];
     double bf[NT];
 #pragma unroll
-    for (int mp = 0; mp < MP; ++mp) {
-      const double* p = ap + (int64_t)q * 4 * KT + mp * 16;
-      a[mp] = STREAM ? ldg_stream2(p) : ldg2(p);
-    }
+    for (int mp = 0; mp < MPW; ++mp) a[mp] = ldg_stream2(ap + (int64_t)q * 4 * lda + mp * 16);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bf[nt] = colok[nt] ? __ldg(bp + (int64_t)q * 4 * ldb + nt * 8) : 0.0;
+    for (int nt = 0; nt < NT; ++nt) bf[nt] = colok[nt] ? ld_operand<COH>(bp + (int64_t)q * 4 * ldb + nt * 8) : 0.0;
 #pragma unroll
-    for (int mp = 0; mp < MP; ++mp)
+    for (int mp = 0; mp < MPW; ++mp)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[mp].x, bf[nt]);
@@ -418,14 +468,15 @@ __device__ __forceinline__ void warp_transposed_mma(double (&acc)[KT / 8][NT][2]
   }
 }
 
-// Store (or stage) a warp's KT x 8NT result: tile t = 2 mp + e holds rank
-// columns a = 16 mp + 2 i + e for i = lane >> 2; columns c0 + 8 nt + 2 (lane&3) + {0,1}.
-template <int KT, int NT>
-__device__ __forceinline__ void store_transposed(const double (&acc)[KT / 8][NT][2], double* out, int64_t ldo, int c0,
+// Store a warp's (16 MPW) x 8NT result: tile t = 2 mp + e holds rank columns
+// a = 16 mp + 2 i + e (i = lane >> 2) relative to the warp's first column;
+// columns c0 + 8 nt + 2 (lane&3) + {0,1}, written at (c - cbase).
+template <int MPW, int NT>
+__device__ __forceinline__ void store_transposed(const double (&acc)[2 * MPW][NT][2], double* out, int64_t ldo, int c0,
                                                  int m, int lane, int cbase = 0) {
   const int i = lane >> 2, j = lane & 3;
 #pragma unroll
-  for (int t = 0; t < KT / 8; ++t) {
+  for (int t = 0; t < 2 * MPW; ++t) {
     const int a = 16 * (t >> 1) + 2 * i + (t & 1);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -441,7 +492,8 @@ __device__ __forceinline__ void store_transposed(const double (&acc)[KT / 8][NT]
   }
 }
 
-// Batched t_j = A_j^T B_j (K x KT)^T (K x m): one warp per segment j.
+// Batched t_j = A_j^T B_j ([K][KT])^T [K][m]. Each segment is split over
+// (KT/16/MPW) rank-column groups x ceil(m / 8NT) column chunks, one warp each.
 struct BatchedVtParams {
   const double* A;  int64_t a_stride;   // A_j = A + j * a_stride, [K][KT]
   const double* B;  int64_t b_stride;   // B_j = B + j * b_stride, [K][m]
@@ -450,20 +502,32 @@ struct BatchedVtParams {
   int32_t K, m;
 };
 
-template <int KT, int NT>
+// One warp task of the batched product: segment jseg, rank-column group mg,
+// column chunk ck.
+template <int KT, int MPW, int NT, bool COH = false>
+__device__ __forceinline__ void vt_batched_task(const BatchedVtParams& P, int64_t jseg, int mg, int ck, int lane) {
+  const int c0 = ck * NT * 8;
+  double acc[2 * MPW][NT][2];
+#pragma unroll
+  for (int t = 0; t < 2 * MPW; ++t)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+  warp_transposed_mma<MPW, NT, COH>(acc, P.A + jseg * P.a_stride + mg * 16 * MPW, KT, P.B + jseg * P.b_stride, P.m,
+                                    c0, P.m, P.K, lane);
+  store_transposed<MPW, NT>(acc, P.out + jseg * P.o_stride + (int64_t)mg * 16 * MPW * P.m, P.m, c0, P.m, lane);
+}
+
+template <int KT, int MPW, int NT>
 __global__ void __launch_bounds__(256) vt_batched_kernel(const BatchedVtParams P) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t jseg = (int64_t)blockIdx.x * 8 + warp;
+  constexpr int MG = KT / 16 / MPW;  // rank-column groups
+  const int lane = threadIdx.x & 31;
+  const int nck = (P.m + NT * 8 - 1) / (NT * 8);
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t per = (int64_t)MG * nck;
+  const int64_t jseg = gw / per;
   if (jseg >= P.count) return;
-  for (int c0 = 0; c0 < P.m; c0 += NT * 8) {
-    double acc[KT / 8][NT][2];
-#pragma unroll
-    for (int t = 0; t < KT / 8; ++t)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-    warp_transposed_mma<KT, NT, true>(acc, P.A + jseg * P.a_stride, P.B + jseg * P.b_stride, P.m, c0, P.m, P.K, lane);
-    store_transposed<KT, NT>(acc, P.out + jseg * P.o_stride, P.m, c0, P.m, lane);
-  }
+  const int sub = (int)(gw - jseg * per);
+  vt_batched_task<KT, MPW, NT>(P, jseg, sub % MG, sub / MG, lane);
 }
 
 // HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
@@ -486,8 +550,8 @@ __global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, in
       for (int t = 0; t < KT / 8; ++t)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-      warp_transposed_mma<KT, NT, true>(acc, lv.V + row0 * KT, P.X + row0 * m, m, c0, m, (int)b, lane);
-      store_transposed<KT, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
+      warp_transposed_mma<KT / 16, NT>(acc, lv.V + row0 * KT, KT, P.X + row0 * m, m, c0, m, (int)b, lane);
+      store_transposed<KT / 16, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
       __syncthreads();
       const int64_t g = lv.s >= tile ? 8 : lv.s / b;
       const int ngroups = (int)(8 / g);
@@ -520,61 +584,104 @@ struct HssDownParams {
   int32_t level, m;
 };
 
-template <int KT, int NT>
-__global__ void __launch_bounds__(256) hss_down_mma_kernel(const HssDownParams P) {
-  constexpr int MC = NT * 8;
-  constexpr int RG = KT / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int l = P.level, m = P.m;
-  const int64_t cnt = 1ll << l;
-  const int64_t j = (int64_t)blockIdx.x * 8 + warp;
-  if (j >= cnt) return;
+// One warp task of the coupling + downsweep on level l: node j, 8-row group
+// rg, column chunk ck.  y_j[rg rows] = R_w[rg rows] y_parent + S_w[rg rows] x_{j^1}.
+template <int KT, int NT, bool COH = false>
+__device__ __forceinline__ void hss_down_task(const HssDownParams& P, int l, int64_t j, int rg, int ck, int lane) {
+  const int m = P.m;
+  const int c0 = ck * NT * 8;
   const int64_t km = (int64_t)KT * m;
   const int64_t q = j >> 1;
   const int w = (int)(j & 1);
-  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * KT * KT;
+  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * KT * KT + (int64_t)rg * 8 * KT;
   const double* xs = P.xh + ((1ll << l) - 2 + (j ^ 1)) * km;
-  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + w * KT) * KT : nullptr;
-  const double* yp = (l >= 2) ? P.yh + ((1ll << (l - 1)) - 2 + q) * km : nullptr;
-  double* yo = P.yh + ((1ll << l) - 2 + j) * km;
+  double acc[1][NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
+  if (l >= 2) {  // downsweep term R_w y_parent
+    const double* Rw = P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + w * KT + rg * 8) * KT;
+    const double* yp = P.yh + ((1ll << (l - 1)) - 2 + q) * km;
+    warp_rowmajor_mma<1, NT, true, COH>(acc, Rw, KT, KT, yp + c0, m, m - c0, lane);
+  }
+  warp_rowmajor_mma<1, NT, true, COH>(acc, S, KT, KT, xs + c0, m, m - c0, lane);  // coupling
   const int i = lane >> 2, jj = lane & 3;
-  for (int c0 = 0; c0 < m; c0 += MC) {
-    double acc[RG][NT][2];
+  double* y = P.yh + ((1ll << l) - 2 + j) * km + (int64_t)(8 * rg + i) * m;
 #pragma unroll
-    for (int rg = 0; rg < RG; ++rg)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
-    warp_rowmajor_mma<RG, NT, true>(acc, S, KT, KT, xs + c0, m, m - c0, lane);
-    if (Rw) {
-      // coupling first, then the downsweep term added (P:707-716 order)
-      double acc2[RG][NT][2];
-#pragma unroll
-      for (int rg = 0; rg < RG; ++rg)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) acc2[rg][nt][0] = acc2[rg][nt][1] = 0.0;
-      warp_rowmajor_mma<RG, NT, true>(acc2, Rw, KT, KT, yp + c0, m, m - c0, lane);
-#pragma unroll
-      for (int rg = 0; rg < RG; ++rg)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          acc[rg][nt][0] += acc2[rg][nt][0];
-          acc[rg][nt][1] += acc2[rg][nt][1];
-        }
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = c0 + nt * 8 + 2 * jj;
+    if (c + 1 < m) {
+      y[c] = acc[0][nt][0];
+      y[c + 1] = acc[0][nt][1];
+    } else if (c < m) {
+      y[c] = acc[0][nt][0];
     }
-#pragma unroll
-    for (int rg = 0; rg < RG; ++rg) {
-      double* y = yo + (int64_t)(8 * rg + i) * m;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int c = c0 + nt * 8 + 2 * jj;
-        if (c + 1 < m) {
-          y[c] = acc[rg][nt][0];
-          y[c + 1] = acc[rg][nt][1];
-        } else if (c < m) {
-          y[c] = acc[rg][nt][0];
-        }
-      }
+  }
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) hss_down_mma_kernel(const HssDownParams P) {
+  constexpr int RGS = KT / 8;  // 8-row groups per node
+  const int lane = threadIdx.x & 31;
+  const int nck = (P.m + NT * 8 - 1) / (NT * 8);
+  const int64_t cnt = 1ll << P.level;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t per = (int64_t)RGS * nck;
+  const int64_t j = gw / per;
+  if (j >= cnt) return;
+  const int sub = (int)(gw - j * per);
+  hss_down_task<KT, NT>(P, P.level, j, sub % RGS, sub / RGS, lane);
+}
+
+// The whole tree part of the HSS product in ONE persistent cooperative launch:
+// upsweep levels l = up_hi .. 1 (x_l = W^T [x_{l+1}; x_{l+1}]), then coupling
+// + downsweep levels l = 1 .. down_hi, one grid-wide barrier between levels
+// (each level depends on the previous one). Every level's tasks are spread
+// over all resident warps, so the small top levels cost a barrier instead of
+// a launch each.
+struct HssSweepParams {
+  const double* W;
+  const double* R;
+  const double* B;
+  double* xh;
+  double* yh;
+  int32_t m, up_hi, down_hi, pad;
+};
+
+template <int KT, int NTU, int NTD>
+__global__ void __launch_bounds__(256) hss_sweep_kernel(const HssSweepParams P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int MG = KT / 16;
+  constexpr int RGS = KT / 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int m = P.m;
+  const int64_t km = (int64_t)KT * m;
+  const int ncku = (m + NTU * 8 - 1) / (NTU * 8);
+  for (int l = P.up_hi; l >= 1; --l) {
+    BatchedVtParams bp{P.W + ((1ll << l) - 2) * 2 * KT * KT, 2ll * KT * KT, P.xh + ((1ll << (l + 1)) - 2) * km, 2 * km,
+                       P.xh + ((1ll << l) - 2) * km, km, 1ll << l, 2 * KT, m};
+    const int64_t per = (int64_t)MG * ncku;
+    const int64_t tasks = (1ll << l) * per;
+    for (int64_t t = w0; t < tasks; t += nw) {
+      const int64_t jseg = t / per;
+      const int sub = (int)(t - jseg * per);
+      vt_batched_task<KT, 1, NTU, true>(bp, jseg, sub % MG, sub / MG, lane);
     }
+    grid.sync();
+  }
+  const int nckd = (m + NTD * 8 - 1) / (NTD * 8);
+  HssDownParams dp{P.B, P.R, P.xh, P.yh, 0, m};
+  for (int l = 1; l <= P.down_hi; ++l) {
+    const int64_t per = (int64_t)RGS * nckd;
+    const int64_t tasks = (1ll << l) * per;
+    for (int64_t t = w0; t < tasks; t += nw) {
+      const int64_t j = t / per;
+      const int sub = (int)(t - j * per);
+      hss_down_task<KT, NTD, true>(dp, l, j, sub % RGS, sub / RGS, lane);
+    }
+    if (l < P.down_hi) grid.sync();
   }
 }
 

@@ -133,30 +133,54 @@ __global__ void __launch_bounds__(kThreads) vt_contract_kernel(const VtParams P)
   }
 }
 
-// t_l[node] = sum_{j < s/tile} partial_l[node * (s/tile) + j], fixed order.
+// t_l[node] = sum_{j < s/tile} partial_l[node * (s/tile) + j] in a fixed order:
+// a group of G (power of two <= 32) consecutive lanes owns one output; lane g
+// sums j = g, g+G, ... sequentially, then a butterfly over the group. The
+// order depends only on the shapes, never on timing.
 struct ReduceLevel {
   const double* partial;
   double* out;
   int64_t nodes;
-  int32_t per_node;  // tiles per node
-  int32_t km;        // k * m
+  int64_t thread_begin;  // first global thread of this level (multiple of 32)
+  int32_t per_node;      // tiles per node
+  int32_t km;            // k * m
+  int32_t log2g;         // group size G = 2^log2g
+  int32_t pad;
 };
 struct ReduceParams {
   int32_t nlev;
+  int64_t threads;
   ReduceLevel lev[kMaxLevels];
 };
 
 __global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceParams P) {
-  const ReduceLevel lv = P.lev[blockIdx.y];
-  const int64_t total = lv.nodes * lv.km;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
-    const int64_t node = e / lv.km;
-    const int64_t o = e - node * lv.km;
-    const double* src = lv.partial + node * lv.per_node * lv.km + o;
-    double s = 0.0;
-    for (int j = 0; j < lv.per_node; ++j) s += src[(int64_t)j * lv.km];
-    lv.out[e] = s;
+  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int L = 0;
+  while (L + 1 < P.nlev && P.lev[L + 1].thread_begin <= t) ++L;
+  const ReduceLevel lv = P.lev[L];
+  const int64_t local = t - lv.thread_begin;
+  const int G = 1 << lv.log2g;
+  const int64_t oi = local >> lv.log2g;
+  const int g = (int)(local & (G - 1));
+  const bool active = t < P.threads && oi < lv.nodes * lv.km;
+  double s = 0.0;
+  if (active) {
+    const int64_t node = oi / lv.km;
+    const int64_t o = oi - node * lv.km;
+    const double* src = lv.partial + node * (int64_t)lv.per_node * lv.km + o;
+    // 8 independent running sums (loads in flight), combined in a fixed order
+    double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int j = g;
+    for (; j + 7 * G < lv.per_node; j += 8 * G) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] += src[(int64_t)(j + u * G) * lv.km];
+    }
+    for (int u = 0; j < lv.per_node; j += G, ++u) r[u] += src[(int64_t)j * lv.km];
+    s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
   }
+  for (int w = 1; w < 32; w <<= 1)
+    if (w < G) s += __shfl_xor_sync(0xffffffffu, s, w);
+  if (active && g == 0) lv.out[oi] = s;
 }
 
 // ------------------------------------------------------------ leaf_apply --

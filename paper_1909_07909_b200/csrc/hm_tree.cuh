@@ -1,0 +1,215 @@
+// hm_tree.cuh — HSS tree levels, nrhs >= 2, DMMA fragments.
+//
+// Upsweep (Fig. 5 right):   x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]
+// Coupling + downsweep (reading G1), one level at a time:
+//                                      y_l[2q+w] = R_{l-1,q}[w] y_{l-1}[q] + S_w x_l[2q+1-w]
+// One CTA (8 warps) owns a PAIR of nodes: the coefficient blocks it needs
+// (the four children of an up pair; the sibling pair's x and the parent's y of
+// a down pair) are staged once in shared memory with a padded row stride, so
+// every warp reads its DMMA B fragments from shared memory; generators (W, R,
+// B) stream from HBM as 128-bit A fragments. Big levels run as one launch per
+// level; the small top levels run in ONE persistent cooperative launch with a
+// grid-wide barrier between levels (hss_tree_sweep_kernel).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "hm_fast.cuh"
+
+namespace hm {
+
+struct TreeParams {
+  const double* W;  // [2^p-2][2k][k]
+  const double* R;  // [2^p-2][2k][k]
+  const double* B;  // [2^p-1][2][k][k]
+  double* xh;       // level-major coefficient blocks [k][m]
+  double* yh;
+  int32_t m;
+  int32_t lo, hi;   // level range for the sweep kernel (up: hi-1 .. lo... see kernels)
+  int32_t pad;
+};
+
+// Staged blocks hold mpad = ceil(m / 8NT) * 8NT columns (zero padded) so every
+// column chunk reads inside its row. Row strides: transposed B fragments read
+// rows r..r+3 (stride = 8 mod 16 doubles is conflict-free), row-major B
+// fragments read rows r, r+2, r+4, r+6 (stride = 4 mod 8).
+__host__ __device__ constexpr int tree_mpad(int m, int nt) { return (m + nt * 8 - 1) / (nt * 8) * (nt * 8); }
+__host__ __device__ constexpr int tree_up_stride(int mpad) { return mpad + (mpad % 16 == 0 ? 8 : 0); }
+__host__ __device__ constexpr int tree_down_stride(int mpad) { return mpad + 4; }
+__host__ __device__ constexpr int64_t tree_smem_doubles(int kt, int m, int nt) {
+  return (4ll * kt * tree_up_stride(tree_mpad(m, nt)) > 3ll * kt * tree_down_stride(tree_mpad(m, nt)))
+             ? 4ll * kt * tree_up_stride(tree_mpad(m, nt))
+             : 3ll * kt * tree_down_stride(tree_mpad(m, nt));
+}
+
+// Transposed product with B in shared memory: C (16 x 8NT) += A^T B, A [K][lda]
+// global (the warp's 16 rank columns start at A), B [K][zs] shared.
+template <int NT, int PF>
+__device__ __forceinline__ void warp_transposed_smem(double (&acc)[2][NT][2], const double* __restrict__ A, int64_t lda,
+                                                     const double* Bs, int zs, int c0, int K, int lane) {
+  const int j = lane & 3, i = lane >> 2;
+  const double* ap = A + (int64_t)j * lda + 2 * i;
+  const double* bp = Bs + j * zs + c0 + i;
+  int q = 0;
+#pragma unroll 1
+  for (; q + PF <= K / 4; q += PF) {
+    double2 a[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) a[u] = ldg_stream2(ap + (int64_t)(q + u) * 4 * lda);
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      double bf[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = bp[(q + u) * 4 * zs + nt * 8];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[u].x, bf[nt]);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a[u].y, bf[nt]);
+    }
+  }
+  for (; q < K / 4; ++q) {
+    const double2 a = ldg_stream2(ap + (int64_t)q * 4 * lda);
+    double bf[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bf[nt] = bp[q * 4 * zs + nt * 8];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a.x, bf[nt]);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a.y, bf[nt]);
+  }
+}
+
+// Up: CTA task for the node pair (2r, 2r+1) of level l (children: 4 consecutive
+// level-(l+1) blocks). 4 warps per node: rank-column group mg = w % MG, column
+// chunks ck = w / MG, w / MG + 4/MG, ...
+template <int KT, int NT, bool COH>
+__device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t r, double* sm) {
+  constexpr int MG = KT / 16;
+  constexpr int CKS = 4 / MG;  // chunk step per node
+  const int m = P.m;
+  const int mp = tree_mpad(m, NT);
+  const int zs = tree_up_stride(mp);
+  const int64_t km = (int64_t)KT * m;
+  const int64_t n0 = 2 * r;  // level l >= 1 has an even number of nodes
+  const int nodes = 2;
+  stage_rows_async(sm, zs, P.xh + ((1ll << (l + 1)) - 2 + 2 * n0) * km, m, 2 * nodes * KT, m, mp);
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3;
+  {
+    const int64_t node = n0 + nd;
+    const int mg = sub % MG;
+    const double* A = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16;
+    const double* Bs = sm + nd * 2 * KT * zs;
+    double* out = P.xh + ((1ll << l) - 2 + node) * km + (int64_t)mg * 16 * m;
+    const int nck = mp / (NT * 8);
+    for (int ck = sub / MG; ck < nck; ck += CKS) {
+      double acc[2][NT][2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+      warp_transposed_smem<NT, (KT / 2 < 16 ? KT / 2 : 16)>(acc, A, KT, Bs, zs, ck * NT * 8, 2 * KT, lane);
+      store_transposed<1, NT>(acc, out, m, ck * NT * 8, m, lane);
+    }
+  }
+  __syncthreads();  // shared memory is reused by the next task
+}
+
+// Down: CTA task for the sibling pair (2q, 2q+1) of level l: stage x_l[2q],
+// x_l[2q+1] (contiguous) and y_{l-1}[q]; warp (nd, sub) computes rows of
+// y_l[2q+nd] = R_{l-1,q}[nd] y_{l-1}[q] + S_nd x_l[2q+1-nd].
+template <int KT, int NT, bool COH>
+__device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64_t q, double* sm) {
+  constexpr int RGS = KT / 8;
+  const int m = P.m;
+  const int mp = tree_mpad(m, NT);
+  const int zs = tree_down_stride(mp);
+  const int64_t km = (int64_t)KT * m;
+  stage_rows_async(sm, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
+  if (l >= 2) stage_rows_async(sm + 2 * KT * zs, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3;
+  const int64_t j = 2 * q + nd;
+  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + nd) * KT * KT;
+  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT : nullptr;
+  const double* Zx = sm + (1 - nd) * KT * zs;  // the sibling's x
+  const double* Zy = sm + 2 * KT * zs;
+  double* yo = P.yh + ((1ll << l) - 2 + j) * km;
+  const int nck = mp / (NT * 8);
+  const int i = lane >> 2, jj = lane & 3;
+  for (int t = sub; t < RGS * nck; t += 4) {
+    const int rg = t % RGS, ck = t / RGS;
+    const int c0 = ck * NT * 8;
+    double acc[1][NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
+    // every A fragment of both terms is requested before the first DMMA
+    constexpr int NQ = KT / 8;
+    double2 aR[NQ][1], aS[NQ][1];
+    const double* bR = Rw ? Rw + (int64_t)(rg * 8 + i) * KT + 2 * jj : nullptr;
+    const double* bS = S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
+#pragma unroll
+    for (int q2 = 0; q2 < NQ; ++q2) {
+      aR[q2][0] = bR ? ldg_stream2(bR + 8 * q2) : make_double2(0.0, 0.0);
+      aS[q2][0] = ldg_stream2(bS + 8 * q2);
+    }
+    bool colok[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
+    if (Rw) rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
+    rm_group<1, NT, false, false, NQ>(acc, aS, Zx + c0, zs, 0, NQ, colok, lane);
+    double* y = yo + (int64_t)(8 * rg + i) * m;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * jj;
+      if (c + 1 < m) {
+        y[c] = acc[0][nt][0];
+        y[c + 1] = acc[0][nt][1];
+      } else if (c < m) {
+        y[c] = acc[0][nt][0];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int KT, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) hss_up_pair_kernel(const TreeParams P, int l) {
+  extern __shared__ double sm[];
+  tree_up_pair<KT, NT, false>(P, l, blockIdx.x, sm);
+}
+
+template <int KT, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) hss_down_pair_kernel(const TreeParams P, int l) {
+  extern __shared__ double sm[];
+  tree_down_pair<KT, NT, false>(P, l, blockIdx.x, sm);
+}
+
+// Levels [lo, hi] of both sweeps in one cooperative launch: up l = hi-1 .. lo
+// (reading x_{l+1}), then down l = lo' .. hi where lo' = lo for the down pass
+// (down starts at level 1 when lo == 1). Grid barrier between levels.
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) hss_tree_sweep_kernel(const TreeParams P, int up_from, int up_to, int down_from,
+                                                              int down_to) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double sm[];
+  cg::grid_group grid = cg::this_grid();
+  bool first = true;
+  for (int l = up_from; l >= up_to; --l) {
+    if (!first) grid.sync();
+    first = false;
+    const int64_t pairs = ((1ll << l) + 1) / 2;
+    for (int64_t r = blockIdx.x; r < pairs; r += gridDim.x) tree_up_pair<KT, NT, true>(P, l, r, sm);
+  }
+  for (int l = down_from; l <= down_to; ++l) {
+    if (!first) grid.sync();
+    first = false;
+    const int64_t pairs = 1ll << (l - 1);
+    for (int64_t q = blockIdx.x; q < pairs; q += gridDim.x) tree_down_pair<KT, NT, true>(P, l, q, sm);
+  }
+}
+
+}  // namespace hm

@@ -1,0 +1,88 @@
+"""Per-kernel timing of single configs (development tool, not the bench contract).
+
+    python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 [--reps N]
+
+Inputs drawn on the device; prints per-kernel device ms (launch trace of
+libhm) and the config's algorithmic GB/s.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import hm_inputs  # noqa: E402
+import paper_1909_07909_b200 as hm  # noqa: E402
+from bench import hodlr_bytes, hss_bytes, hss_flops, hodlr_flops  # noqa: E402
+
+
+def run(name, reps):
+    dev = torch.device("cuda:0")
+    if name.startswith("c3") or name in ("c5", "c1"):
+        cfg = hm_inputs.CONFIGS[{"c1": 1, "c5": 5}.get(name, 3)]
+        m = int(name[3:]) if name.startswith("c3m") else 1
+        if cfg.laplacian:
+            h = hm_inputs.hodlr_inverse_laplacian(cfg.n, cfg.levels, xp=torch, device=dev)
+        else:
+            h = hm_inputs.device_hodlr_random(cfg.n, cfg.levels, [cfg.k] * cfg.levels, 7, dev)
+        X = torch.randn(cfg.n, m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hodlr_workspace_bytes(cfg.n, cfg.levels, cfg.leaf, h.ranks, m), dtype=torch.uint8,
+                         device=dev)
+        f = lambda: hm.hodlr_matvec(cfg.n, cfg.levels, cfg.leaf, h.ranks, h.D, h.U, h.V, X, Y, ws)
+        nbytes = hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
+        flops = hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
+    else:
+        cfg = hm_inputs.CONFIGS[{"c2": 2, "c4": 4}[name]]
+        m = cfg.nrhs[0]
+        s = hm_inputs.device_hss_random(cfg.n, cfg.levels, cfg.k, 7, dev)
+        X = torch.randn(cfg.n, m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hss_workspace_bytes(cfg.n, cfg.levels, cfg.leaf, cfg.k, m), dtype=torch.uint8,
+                         device=dev)
+        f = lambda: hm.hss_matvec(cfg.n, cfg.levels, cfg.leaf, cfg.k, s.D, s.U, s.V, s.R, s.W, s.B, X, Y, ws)
+        nbytes = hss_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
+        flops = hss_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    hm.hm_profile_collect()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    plain = e0.elapsed_time(e1) / reps
+    hm.hm_profile_enable(True)
+    for _ in range(reps):
+        f()
+    torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    tr = hm.hm_profile_collect()
+    per = {}
+    for nm, call, ms in tr:
+        per.setdefault(nm, []).append(ms)
+    print(f"== {name}: {plain * 1e3:.1f} us/call  {nbytes / plain / 1e6:.0f} GB/s  "
+          f"{flops / plain / 1e9:.2f} TFLOP/s")
+    for nm, v in per.items():
+        cnt = len(v) // reps
+        tot = sum(v) / reps
+        print(f"   {nm:<18} x{cnt:<3} {tot * 1e3:9.1f} us")
+    if "--levels" in sys.argv:
+        calls = [t for t in tr if t[1] == 0]
+        print("   " + " ".join(f"{n[:6]}:{ms * 1e3:.1f}" for n, _, ms in calls))
+    del X, Y, ws
+    torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    reps = 10
+    names = [a for a in sys.argv[1:] if not a.startswith("--")]
+    if "--reps" in sys.argv:
+        reps = int(sys.argv[sys.argv.index("--reps") + 1])
+        names = [a for a in names if not a.isdigit()]
+    for nm in names:
+        run(nm, reps)

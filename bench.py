@@ -202,6 +202,68 @@ class Workload:
     def h2d_d2h_bytes(self):
         return 8 * (C5.n * M5 + C4.n * M4), 8 * (C5.n * M5 + C4.n * M4)
 
+    calls = ("c5", "c4")  # matvec calls per step (launch-trace labels)
+    rows5 = C5.n
+
+
+class DistWorkload:
+    """Rank r of P: the shards of include/hm.h "multi-GPU" (rows of node (q, r) and its
+    subtree), filled on this rank's GPU; one allgather per matvec (NCCL)."""
+
+    calls = ("c5", "c5", "c5", "c4", "c4")  # hodlr begin/local/end, hss begin/end
+
+    def __init__(self, torch, device, seed, P, r):
+        import paper_1909_07909_b200 as hm
+        from paper_1909_07909_b200 import dist as hd
+        self.torch, self.device, self.hm, self.hd, self.P, self.r = torch, device, hm, hd, P, r
+        n5, p5, b5 = C5.n, C5.levels, C5.leaf
+        lpr = (1 << p5) // P
+        nl5 = n5 // P
+        self.rows5 = nl5
+        self.D5 = hm_inputs.inverse_laplacian_leaf_blocks(n5, p5, leaves=range(r * lpr, (r + 1) * lpr), xp=torch,
+                                                          device=device)
+        U, V = hm_inputs.inverse_laplacian_factors(n5, p5, xp=torch, device=device)
+        self.ranks5 = [1] * p5
+        _, self.U5, self.V5 = hd.hodlr_shard(n5, p5, b5, self.ranks5, self.D5[:0], U, V, P, r)
+        del U, V
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        self.X5 = torch.randn(nl5, M5, dtype=torch.float64, device=device, generator=g)
+        self.Y5 = torch.empty_like(self.X5)
+        s4 = hm_inputs.device_hss_random(C4.n, C4.levels, C4.k, seed + 1, device)  # same draw on every rank
+        self.sh4 = {k_: v.contiguous() for k_, v in
+                    hd.hss_shard(C4.n, C4.levels, C4.leaf, C4.k, s4.D, s4.U, s4.V, s4.R, s4.W, s4.B, P, r).items()}
+        del s4
+        torch.cuda.empty_cache()
+        nl4 = C4.n // P
+        self.X4 = torch.randn(nl4, M4, dtype=torch.float64, device=device, generator=g)
+        self.Y4 = torch.empty_like(self.X4)
+        w5, self.sd5 = hd.hodlr_dist_sizes(n5, p5, b5, self.ranks5, M5, P, r)
+        w4, self.sd4 = hd.hss_dist_sizes(C4.n, C4.levels, C4.leaf, C4.k, M4, P, r)
+        self.ws5 = torch.empty(w5, dtype=torch.uint8, device=device)
+        self.ws4 = torch.empty(w4, dtype=torch.uint8, device=device)
+        self.X5h = self.X5.cpu().pin_memory()
+        self.Y5h = torch.empty_like(self.X5h).pin_memory()
+        self.X4h = self.X4.cpu().pin_memory()
+        self.Y4h = torch.empty_like(self.X4h).pin_memory()
+        self.launches = 0
+
+    def step(self):
+        hd, hm = self.hd, self.hm
+        hd.hodlr_matvec_dist(C5.n, C5.levels, C5.leaf, self.ranks5, self.D5, self.U5, self.V5, self.X5, self.Y5,
+                             ws=self.ws5)
+        hd.hss_matvec_dist(C4.n, C4.levels, C4.leaf, C4.k, self.sh4, self.X4, self.Y4, ws=self.ws4)
+
+    def step_e2e(self):
+        self.X5.copy_(self.X5h, non_blocking=True)
+        self.X4.copy_(self.X4h, non_blocking=True)
+        self.step()
+        self.Y5h.copy_(self.Y5, non_blocking=True)
+        self.Y4h.copy_(self.Y4, non_blocking=True)
+
+    def h2d_d2h_bytes(self):
+        return 8 * (self.X5.numel() + self.X4.numel()), 8 * (self.Y5.numel() + self.Y4.numel())
+
 
 def run_ours(args):
     import torch
@@ -212,14 +274,20 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1:
-        raise SystemExit("multi-GPU bench needs the distributed path (hodlr_matvec_dist / hss_matvec_dist)")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
     from paper_1909_07909_b200 import build as hm_build
-    hm_build.build()
+    if rank == 0:
+        hm_build.build()
+    if world > 1:
+        dist.barrier()
 
-    wl = Workload(torch, device, seed=hm_inputs.MASTER_SEED + rank)
+    if world > 1:
+        wl = DistWorkload(torch, device, hm_inputs.MASTER_SEED, world, rank)
+    else:
+        wl = Workload(torch, device, seed=hm_inputs.MASTER_SEED)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         wl.step()
@@ -239,17 +307,25 @@ def run_ours(args):
         wl.step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     wl.hm.hm_profile_enable(False)
     ms = e0.elapsed_time(e1)
+    if world > 1:  # max over ranks
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     clocks = sampler.stop()
     trace = wl.hm.hm_profile_collect()
-    launches = wl.launches
+    launches = len(trace)  # every traced record is one of libhm's kernel launches in the timed region
 
     # end-to-end (host X in, host Y out through the C-ABI hostio calls)
     for _ in range(2):
         wl.step_e2e()
     torch.cuda.synchronize()
     e2 = max(3, args.steps // 5)
+    if world > 1:
+        dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(e2):
@@ -257,11 +333,16 @@ def run_ours(args):
     f1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
 
     # per-kernel device time from the trace: call 2j = HODLR (config 5), 2j+1 = HSS (config 4)
     per = {}
+    ncall = len(wl.calls)
     for name, call, t in trace:
-        key = ("c5" if call % 2 == 0 else "c4") + ":" + name
+        key = wl.calls[call % ncall] + ":" + name
         d = per.setdefault(key, [0, 0.0])
         d[0] += 1
         d[1] += t
@@ -271,7 +352,7 @@ def run_ours(args):
     peak, peak_kind = load_peaks()
     dom = per.get("c5:leaf_apply", [1, float("nan")])
     dom_avg_ms = dom[1] / dom[0]
-    dom_bytes = leaf_apply_c5_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5)
+    dom_bytes = leaf_apply_c5_bytes(wl.rows5, C5.leaf, C5.levels, C5.k, M5)
     achieved = dom_bytes / (dom_avg_ms * 1e-3) / 1e9
     c5_ms = sum(v[1] for k_, v in per.items() if k_.startswith("c5:")) / args.steps
     c4_ms = sum(v[1] for k_, v in per.items() if k_.startswith("c4:")) / args.steps
@@ -330,8 +411,14 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    if world > 1:
+        out["per_config"]["note"] = "per-rank device time (rank 0's launch trace)"
+        out["roofline"]["kernel"] += f" — rank 0's shard (1/{world} of the rows)"
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------ CPU oracle --

@@ -137,6 +137,61 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
                             const double* X_host, int32_t nrhs, double* Y_host,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------- multi-GPU (§8(e)) --
+ * One process per GPU, P = 2^q ranks (1 <= P <= 2^levels). Rank r owns the
+ * rows I_r = [r n/P, (r+1) n/P) — the level-q node (q, r) and its whole
+ * subtree (Def. 2.1) — and these generators ("local" arrays):
+ *   HODLR  D_local [2^(p-q)][b][b]; U_local, V_local level-major over ALL p
+ *          levels with n/P rows each: level l at offset (n/P) sum_{l'<l} k_l',
+ *          [n/P][k_l] = rows I_r of the global U_l, V_l. X_local, Y_local
+ *          [n/P][nrhs] = rows I_r.
+ *   HSS    D_local, U_local, V_local [n/P][k] likewise; the subtree's W_sub,
+ *          R_sub [2^(p-q)-2][2k][k] and B_sub [2^(p-q)-1][2][k][k] in heap
+ *          order relative to node (q, r) (B_sub[0] = the cores of node (q,r));
+ *          W_root, R_root [2k][k] = the translations of node (q, r) itself;
+ *          W_top, R_top [2^q-2][2k][k] and B_top [2^q-1][2][k][k] = the global
+ *          arrays' prefixes (levels < q), replicated on every rank.
+ * The ONLY exchange is an allgather of `send_doubles` doubles per rank into
+ * `gathered` [P][send_doubles] (rank order), done by the caller (NCCL through
+ * torch.distributed in the binding) between _begin and _end:
+ *   HODLR  send = this rank's partial t_l = V_l(I_r)^T X(I_r) for l = 1..q;
+ *          _end sums, for each top level, the partials of the ranks under the
+ *          sibling of its ancestor, in rank order, and adds U_l(I_r) t_l.
+ *          _local (V^T X of the subtree levels) may run while the allgather
+ *          is in flight.
+ *   HSS    send = x of node (q, r) (Step 1 up to the subtree root); _end runs
+ *          the replicated top tree (levels 1..q) and then the subtree's
+ *          coupling/downsweep from y of node (q, r), and the leaves.
+ * Results equal the single-GPU product up to the order of the top-level sums. */
+typedef struct {
+  int32_t nranks; /* P, a power of two <= 2^levels */
+  int32_t rank;   /* 0 <= rank < P                  */
+} hm_part;
+
+hm_status hm_hodlr_dist_sizes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, const hm_part* part,
+                              size_t* ws_bytes, int64_t* send_doubles);
+hm_status hodlr_matvec_dist_begin(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                  const double* V_local, const double* X_local, int32_t nrhs, double* send,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                  const double* V_local, const double* X_local, int32_t nrhs,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                const double* D_local, const double* U_local, const double* X_local, int32_t nrhs,
+                                const double* gathered, double* Y_local, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+hm_status hm_hss_dist_sizes(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, size_t* ws_bytes,
+                            int64_t* send_doubles);
+hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* part, const double* V_local,
+                                const double* W_sub, const double* W_root, const double* X_local, int32_t nrhs,
+                                double* send, void* workspace, size_t workspace_bytes, void* stream);
+hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* part, const double* D_local,
+                              const double* U_local, const double* R_sub, const double* B_sub,
+                              const double* R_root, const double* W_top, const double* R_top, const double* B_top,
+                              const double* X_local, int32_t nrhs, const double* gathered, double* Y_local,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ misc -- */
 
 /* Thread-local message describing the last non-OK status ("" if none). */

@@ -28,7 +28,9 @@ _STATUS = {0: "HM_OK", -1: "HM_ERR_INVALID_ARG", -2: "HM_ERR_UNSUPPORTED", -3: "
 # every symbol include/hm.h declares (tests check the library exports all of them)
 EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "hm_hss_workspace_bytes",
            "hss_matvec", "hss_matvec_hostio", "hm_last_error", "hm_abi_version", "hm_last_launch_count",
-           "hm_profile_enable", "hm_profile_collect")
+           "hm_profile_enable", "hm_profile_collect",
+           "hm_hodlr_dist_sizes", "hodlr_matvec_dist_begin", "hodlr_matvec_dist_local", "hodlr_matvec_dist_end",
+           "hm_hss_dist_sizes", "hss_matvec_dist_begin", "hss_matvec_dist_end")
 
 
 class HmError(RuntimeError):

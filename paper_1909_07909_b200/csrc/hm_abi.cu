@@ -175,32 +175,39 @@ void allow_smem(K kernel, size_t bytes) {
 }
 
 // ------------------------------------------------------------------ HODLR --
+//
+// A HODLR problem is planned on a row block of n rows that is a whole subtree
+// of depth p (leaf b), plus q "top" levels whose nodes contain the whole block
+// (q > 0 only for one rank of the distributed product). Levels
+// keep their global index: top levels 1..q, subtree levels q+1..q+p;
+// ranks[l-1] = k_l for all of them.
 
 enum class VtPath { kNone, kGeneric, kGemv, kMma };
 enum class LeafPath { kGeneric, kGemv, kMma };
 
 struct HodlrPlan {
   int64_t n, b;
-  int32_t p, m, k;  // k = the common nonzero rank (0 if all zero)
-  int64_t ktot;
+  int32_t p, q, m, k;  // k = the common nonzero rank (0 if all zero)
+  int64_t ktot;        // sum over all q + p levels
+  int64_t top_doubles; // sum_{l <= q} k_l m (the distributed exchange block)
   VtPath vt;
   LeafPath leaf;
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf;
   int64_t tile;  // rows per vt CTA
   size_t off_t[hm::kMaxLevels + 1];
   size_t off_part[hm::kMaxLevels + 1];
-  size_t off_x, off_y, total;
+  size_t off_ttop, off_x, off_y, total;
 };
 
-hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags, HodlrPlan* P) {
-  hm_status st = check_tree(tree);
-  if (st) return st;
+hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_t* ranks, int32_t nrhs,
+                        int32_t flags, HodlrPlan* P) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
-  if (tree->levels > 0 && !ranks) return fail(HM_ERR_INVALID_ARG, "ranks is NULL");
+  if (p + q > 0 && !ranks) return fail(HM_ERR_INVALID_ARG, "ranks is NULL");
+  if (p + q + 1 > hm::kMaxLevels) return fail(HM_ERR_UNSUPPORTED, "too many levels");
   memset(P, 0, sizeof *P);
-  P->n = tree->n; P->b = tree->leaf; P->p = tree->levels; P->m = nrhs;
-  for (int l = 1; l <= P->p; ++l) {
-    int k = ranks[l - 1];
+  P->n = n; P->b = b; P->p = p; P->q = q; P->m = nrhs;
+  for (int l = 1; l <= p + q; ++l) {
+    const int k = ranks[l - 1];
     if (k < 0) return fail(HM_ERR_INVALID_ARG, "ranks[%d] = %d < 0", l - 1, k);
     if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
     if (k > 0) {
@@ -209,11 +216,11 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
       P->k = k;
     }
     P->ktot += k;
+    if (l <= q) P->top_doubles += (int64_t)k * nrhs;
   }
-  const int64_t b = P->b, k = P->k;
-  const bool tiles8 = P->p >= 3;  // 8-leaf row tiles exist
-  // phase 1: V_l^T X
-  if (k == 0 || P->p == 0) {
+  const int64_t k = P->k;
+  const bool tiles8 = p >= 3;  // 8-leaf row tiles exist
+  if (k == 0 || p + q == 0) {
     P->vt = VtPath::kNone;
   } else if (nrhs == 1 && tiles8 && b % 64 == 0 && b <= 4096 && pow2_rank((int)k, 1, 64)) {
     P->vt = VtPath::kGemv;
@@ -225,9 +232,8 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
   } else {
     P->vt = VtPath::kGeneric;
     P->mc_vt = vt_mc(b, nrhs);
-    P->tile = pick_tile(b, P->p, P->mc_vt);
+    P->tile = pick_tile(b, p, P->mc_vt);
   }
-  // phase 2: leaves
   const bool k8 = (k % 8 == 0);
   if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (k == 0 || pow2_rank((int)k, 1, 64)) &&
       (2 * b + P->ktot) * 8 <= 160 * 1024) {
@@ -246,27 +252,36 @@ hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, in
       return fail(HM_ERR_UNSUPPORTED, "leaf %lld + ranks %lld too large for shared-memory staging", (long long)b,
                   (long long)P->ktot);
   }
-  // workspace: t_l per level, per-tile partials where a node spans several tiles
+  // workspace: subtree t_l, per-tile partials where a node spans several tiles
+  // (every top level: its node is the whole block), combined top t blocks
   size_t off = 0;
-  for (int l = 1; l <= P->p; ++l) {
+  for (int l = q + 1; l <= q + p; ++l) {
     P->off_t[l] = off;
-    off = align_up(off + sizeof(double) * (size_t)((1ll << l) * ranks[l - 1] * nrhs));
+    off = align_up(off + sizeof(double) * (size_t)((1ll << (l - q)) * ranks[l - 1] * nrhs));
   }
-  for (int l = 1; l <= P->p; ++l) {
-    const int64_t s = P->n >> l;
+  for (int l = 1; l <= q + p; ++l) {
+    const int64_t s = l <= q ? n : (n >> (l - q));
     P->off_part[l] = off;
     if (P->vt != VtPath::kNone && ranks[l - 1] > 0 && s > P->tile)
-      off = align_up(off + sizeof(double) * (size_t)((P->n / P->tile) * ranks[l - 1] * nrhs));
+      off = align_up(off + sizeof(double) * (size_t)((n / P->tile) * ranks[l - 1] * nrhs));
   }
+  P->off_ttop = off;
+  off = align_up(off + sizeof(double) * (size_t)P->top_doubles);
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off;
-    off = align_up(off + sizeof(double) * (size_t)(P->n * nrhs));
+    off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
     P->off_y = off;
-    off = align_up(off + sizeof(double) * (size_t)(P->n * nrhs));
+    off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
   }
   P->total = std::max<size_t>(off, kAlign);
   return HM_OK;
+}
+
+hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags, HodlrPlan* P) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  return hodlr_plan_ex(tree->n, tree->leaf, tree->levels, 0, ranks, nrhs, flags, P);
 }
 
 // ---- leaf launches (shared by HODLR and HSS) ----
@@ -420,24 +435,117 @@ hm_status vt_batched_dispatch(const char* name, const hm::BatchedVtParams& bp, i
   return fail(HM_ERR_UNSUPPORTED, "vt_batched: no instance for k=%d nt=%d", k, nt);
 }
 
+// Phase 1 of the HODLR product: V_l^T X for the levels [l0, l1] (global
+// indices) in one pass over row tiles, per-tile partials -> fixed-order reduce.
+// Top levels (l <= q) have one node = the whole block; their result goes to
+// `top_out` (packed [sum_{l<=q} k_l][m]); subtree levels go to the workspace.
+hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double* V, const double* Xd, char* w,
+                         int l0, int l1, double* top_out, cudaStream_t stream) {
+  if (P.vt == VtPath::kNone) return HM_OK;
+  const int nrhs = P.m;
+  hm::VtParams vp;
+  memset(&vp, 0, sizeof vp);
+  vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile;
+  hm::ReduceParams rp;
+  memset(&rp, 0, sizeof rp);
+  int64_t uoff = 0, toff = 0;
+  for (int l = 1; l <= P.q + P.p; ++l) {
+    const int k = ranks[l - 1];
+    const int64_t s = l <= P.q ? P.n : (P.n >> (l - P.q));
+    if (k > 0 && l >= l0 && l <= l1) {
+      hm::VtLevel& lv = vp.lev[vp.nlev++];
+      lv.V = V + uoff;
+      lv.k = k;
+      lv.s = s;
+      lv.out = l <= P.q ? top_out + toff : reinterpret_cast<double*>(w + P.off_t[l]);
+      lv.partial = reinterpret_cast<double*>(w + P.off_part[l]);
+      if (s > P.tile) {
+        hm::ReduceLevel& rl = rp.lev[rp.nlev++];
+        rl.partial = lv.partial;
+        rl.out = lv.out;
+        rl.nodes = P.n / s;
+        rl.per_node = (int32_t)(s / P.tile);
+        rl.km = k * nrhs;
+        int lg = 0;
+        while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
+        rl.log2g = lg;
+        rl.thread_begin = rp.threads;
+        rp.threads += ((rl.nodes * rl.km << lg) + 31) / 32 * 32;
+      }
+    }
+    uoff += P.n * k;
+    if (l <= P.q) toff += (int64_t)k * nrhs;
+  }
+  if (vp.nlev == 0) return HM_OK;
+  hm_status st;
+  if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
+  else if (P.vt == VtPath::kMma) st = vt_mma_dispatch(vp, P.b, P.k, P.nt_vt, stream);
+  else st = vt_generic(vp, P.n, stream);
+  if (st) return st;
+  if (rp.nlev > 0) {
+    const unsigned grid = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
+    st = launch("reduce_partials", stream,
+                [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp); });
+    if (st) return st;
+  }
+  return HM_OK;
+}
+
+// Phase 2: per leaf Y(I_i) = D_i X(I_i) + sum_l U_l(I_i) t_{l, sib(node_l(i))};
+// for top levels the coefficient block is the same for every leaf (ttop).
+hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const double* D, const double* U,
+                           const double* Xd, double* Yd, char* w, const double* ttop, cudaStream_t stream) {
+  hm::LeafParams lp;
+  memset(&lp, 0, sizeof lp);
+  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf;
+  int64_t uoff = 0, toff = 0;
+  for (int l = 1; l <= P.q + P.p; ++l) {
+    const int k = ranks[l - 1];
+    if (k > 0) {
+      hm::LeafSeg& sg = lp.seg[lp.nseg++];
+      sg.A = U + uoff;
+      sg.k = k;
+      if (l <= P.q) {
+        sg.T = ttop + toff;
+        sg.shift = 62;  // node index 0 for every leaf
+        sg.xr = 0;
+      } else {
+        sg.T = reinterpret_cast<const double*>(w + P.off_t[l]);
+        sg.shift = P.q + P.p - l;  // node of leaf i at level l: i >> (depth - l)
+        sg.xr = 1;                 // the sibling's coefficients: A(I_a, I_sib a) = U(I_a) V(I_sib)^T
+      }
+      lp.ktot += k;
+    }
+    uoff += P.n * k;
+    if (l <= P.q) toff += (int64_t)k * P.m;
+  }
+  return leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream);
+}
+
+hm_status hodlr_check_ptrs(const HodlrPlan& P, const double* D, const double* U, const double* V, const double* X,
+                           const double* Y, void* ws, size_t ws_bytes, int32_t flags) {
+  if (!ws || ws_bytes < P.total)
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
+  if (!X || !Y || (P.k > 0 && (!U || !V))) return fail(HM_ERR_INVALID_ARG, "NULL generator / X / Y pointer");
+  if ((D && !aligned16(D)) || !aligned16(ws) || (P.k > 0 && (!aligned16(U) || !aligned16(V))))
+    return fail(HM_ERR_INVALID_ARG, "D, U, V and the workspace must be 16-byte aligned");
+  const size_t xy_bytes = sizeof(double) * (size_t)(P.n * P.m);
+  if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
+    return fail(HM_ERR_INVALID_ARG, "X and Y must be 16-byte aligned");
+  return HM_OK;
+}
+
 hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                     const double* V, const double* X, int32_t nrhs, double* Y, void* ws, size_t ws_bytes,
                     cudaStream_t stream, int32_t flags) {
   HodlrPlan P;
   hm_status st = hodlr_plan(tree, ranks, nrhs, flags, &P);
   if (st) return st;
-  if (!ws || ws_bytes < P.total)
-    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
-  if (!D || !X || !Y || (P.k > 0 && (!U || !V)))
-    return fail(HM_ERR_INVALID_ARG, "NULL generator / X / Y pointer");
-  if (!aligned16(D) || !aligned16(ws) || (P.k > 0 && (!aligned16(U) || !aligned16(V))))
-    return fail(HM_ERR_INVALID_ARG, "D, U, V and the workspace must be 16-byte aligned");
-  const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
-  if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
-  if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
-    return fail(HM_ERR_INVALID_ARG, "X and Y must be 16-byte aligned");
-
+  if (!D) return fail(HM_ERR_INVALID_ARG, "NULL D pointer");
+  if ((st = hodlr_check_ptrs(P, D, U, V, X, Y, ws, ws_bytes, flags))) return st;
   char* w = static_cast<char*>(ws);
+  const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
   const double* Xd = X;
   double* Yd = Y;
   g_launches = 0;
@@ -448,75 +556,8 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     if (cudaMemcpyAsync(const_cast<double*>(Xd), X, xy_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
       return cuda_check("H2D copy of X");
   }
-
-  // (1) every level's V_l^T X in one pass over row tiles; partials -> fixed-order reduce
-  if (P.vt != VtPath::kNone) {
-    hm::VtParams vp;
-    memset(&vp, 0, sizeof vp);
-    vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile;
-    hm::ReduceParams rp;
-    memset(&rp, 0, sizeof rp);
-    int64_t uoff = 0;
-    for (int l = 1; l <= P.p; ++l) {
-      const int k = ranks[l - 1];
-      const int64_t s = P.n >> l;
-      if (k > 0) {
-        hm::VtLevel& lv = vp.lev[vp.nlev++];
-        lv.V = V + uoff;
-        lv.k = k;
-        lv.s = s;
-        lv.out = reinterpret_cast<double*>(w + P.off_t[l]);
-        lv.partial = reinterpret_cast<double*>(w + P.off_part[l]);
-        if (s > P.tile) {
-          hm::ReduceLevel& rl = rp.lev[rp.nlev++];
-          rl.partial = lv.partial;
-          rl.out = lv.out;
-          rl.nodes = 1ll << l;
-          rl.per_node = (int32_t)(s / P.tile);
-          rl.km = k * nrhs;
-          int lg = 0;
-          while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
-          rl.log2g = lg;
-          rl.thread_begin = rp.threads;
-          rp.threads += ((rl.nodes * rl.km << lg) + 31) / 32 * 32;
-        }
-      }
-      uoff += P.n * k;
-    }
-    if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
-    else if (P.vt == VtPath::kMma) st = vt_mma_dispatch(vp, P.b, P.k, P.nt_vt, stream);
-    else st = vt_generic(vp, P.n, stream);
-    if (st) return st;
-    if (rp.nlev > 0) {
-      const unsigned grid = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
-      st = launch("reduce_partials", stream,
-                  [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp); });
-      if (st) return st;
-    }
-  }
-
-  // (2) per leaf: Y(I_i) = D_i X(I_i) + sum_l U_l(I_i) t_{l, sib(node_l(i))}
-  hm::LeafParams lp;
-  memset(&lp, 0, sizeof lp);
-  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = nrhs; lp.mc = P.mc_leaf;
-  {
-    int64_t uoff = 0;
-    for (int l = 1; l <= P.p; ++l) {
-      const int k = ranks[l - 1];
-      if (k > 0) {
-        hm::LeafSeg& sg = lp.seg[lp.nseg++];
-        sg.A = U + uoff;
-        sg.T = reinterpret_cast<const double*>(w + P.off_t[l]);
-        sg.k = k;
-        sg.shift = P.p - l;  // node of leaf i at level l: i >> (p - l)
-        sg.xr = 1;           // the sibling's coefficients: A(I_a, I_sib a) = U(I_a) V(I_sib)^T
-        lp.ktot += k;
-      }
-      uoff += P.n * k;
-    }
-  }
-  if ((st = leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream))) return st;
-
+  if ((st = hodlr_vt_phase(P, ranks, V, Xd, w, 1, P.p, nullptr, stream))) return st;
+  if ((st = hodlr_leaf_phase(P, ranks, D, U, Xd, Yd, w, nullptr, stream))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");
@@ -524,45 +565,73 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
   return HM_OK;
 }
 
+// ---- distributed HODLR ----
+
+struct DistPart {
+  int32_t P, q, rank;
+};
+
+hm_status check_part(const hm_tree* tree, const hm_part* part, DistPart* d) {
+  if (!part) return fail(HM_ERR_INVALID_ARG, "part is NULL");
+  const int P = part->nranks;
+  if (P < 1 || (P & (P - 1)) != 0) return fail(HM_ERR_UNSUPPORTED, "nranks = %d is not a power of two", P);
+  int q = 0;
+  while ((1 << q) < P) ++q;
+  if (q > tree->levels) return fail(HM_ERR_UNSUPPORTED, "nranks = %d > 2^levels", P);
+  if (part->rank < 0 || part->rank >= P) return fail(HM_ERR_INVALID_ARG, "rank %d not in [0, %d)", part->rank, P);
+  d->P = P; d->q = q; d->rank = part->rank;
+  return HM_OK;
+}
+
+hm_status hodlr_dist_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, const hm_part* part, int32_t flags,
+                          HodlrPlan* P, DistPart* d) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  if ((st = check_part(tree, part, d))) return st;
+  return hodlr_plan_ex(tree->n >> d->q, tree->leaf, tree->levels - d->q, d->q, ranks, nrhs, flags, P);
+}
+
 // -------------------------------------------------------------------- HSS --
+//
+// Planned on a subtree of depth p (leaf b) over n rows; for one rank of the
+// distributed product (q > 0) the workspace also holds the replicated top tree
+// (levels 1..q) and the subtree root's x / y blocks.
 
 struct HssPlan {
   int64_t n, b;
-  int32_t p, m, k;
+  int32_t p, q, m, k;
   VtPath vt;
   LeafPath leaf;
-  bool mma_levels;  // DMMA up/down level kernels
+  bool mma_levels;  // DMMA tree kernels
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
-  size_t off_xh, off_yh, off_x, off_y, total;
+  size_t off_xh, off_yh, off_txh, off_tyh, off_x, off_y, total;
 };
 
-hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
-  hm_status st = check_tree(tree);
-  if (st) return st;
+hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
   if (k < 0) return fail(HM_ERR_INVALID_ARG, "k = %d < 0", k);
   if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
   memset(P, 0, sizeof *P);
-  P->n = tree->n; P->b = tree->leaf; P->p = tree->levels; P->m = nrhs; P->k = k;
-  const int64_t b = P->b;
-  const bool coupled = (k > 0 && P->p > 0);
+  P->n = n; P->b = b; P->p = p; P->q = q; P->m = nrhs; P->k = k;
+  const bool coupled = (k > 0 && p + q > 0);
+  const bool leaf_coupled = (k > 0 && (p > 0 || q > 0));
   if (!coupled) {
     P->vt = VtPath::kNone;
-  } else if (nrhs == 1 && P->p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
+  } else if (nrhs == 1 && p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
     P->vt = VtPath::kGemv;
     P->tile = 8 * b;
   } else if (nrhs >= 2 && b % 4 == 0 && pow2_rank(k, 16, 64)) {
-    P->vt = VtPath::kMma;  // batched: one warp per leaf
+    P->vt = VtPath::kMma;  // batched: warps per leaf
     P->nt_vt = nt_for(nrhs, HM_VTB_NTMAX);
   } else {
     P->vt = VtPath::kGeneric;
     P->mc_vt = vt_mc(b, nrhs);
-    P->tile = pick_tile(b, P->p, P->mc_vt);
+    P->tile = pick_tile(b, p, P->mc_vt);
   }
   P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
   if (P->mma_levels) P->nt_down = nt_for(nrhs, HM_TREE_NTMAX);
-  const int ktot = coupled ? k : 0;
+  const int ktot = leaf_coupled ? k : 0;
   if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
     P->leaf = LeafPath::kGemv;
   } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && ktot % 8 == 0) {
@@ -577,40 +646,27 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
     if ((b + ktot) * P->mc_leaf > kSmemBudgetDoubles)
       return fail(HM_ERR_UNSUPPORTED, "leaf %lld too large for shared-memory staging", (long long)b);
   }
-  const size_t coef = sizeof(double) * (size_t)((((int64_t)1 << (P->p + 1)) - 2) * k * nrhs);
+  const size_t blk = sizeof(double) * (size_t)k * nrhs;
+  const size_t coef = blk * (size_t)((((int64_t)1 << (p + 1)) - 2));
+  const size_t tcoef = blk * (size_t)((((int64_t)1 << (q + 1)) - 2));
   size_t off = 0;
   P->off_xh = off; off = align_up(off + coef);
   P->off_yh = off; off = align_up(off + coef);
+  P->off_txh = off; off = align_up(off + tcoef);
+  P->off_tyh = off; off = align_up(off + tcoef);
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
-    P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(P->n * nrhs));
-    P->off_y = off; off = align_up(off + sizeof(double) * (size_t)(P->n * nrhs));
+    P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
+    P->off_y = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
   }
   P->total = std::max<size_t>(off, kAlign);
   return HM_OK;
 }
 
-template <int KT, int NT>
-hm_status hss_down_launch(const hm::HssDownParams& dp, cudaStream_t s) {
-  const int64_t cnt = 1ll << dp.level;
-  const int64_t nck = (dp.m + NT * 8 - 1) / (NT * 8);
-  const int64_t warps = cnt * (KT / 8) * nck;
-  return launch("hss_down_level", s,
-                [&] { hm::hss_down_mma_kernel<KT, NT><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(dp); });
-}
-
-hm_status hss_down_dispatch(const hm::HssDownParams& dp, int k, int nt, cudaStream_t s) {
-#define HM_DOWN(KT_)                                              \
-  if (k == KT_) {                                                 \
-    if (nt == 1) return hss_down_launch<KT_, 1>(dp, s);           \
-    if (nt == 2) return hss_down_launch<KT_, 2>(dp, s);           \
-    return hss_down_launch<KT_, 4>(dp, s);                        \
-  }
-  HM_DOWN(16)
-  HM_DOWN(32)
-  HM_DOWN(64)
-#undef HM_DOWN
-  return fail(HM_ERR_UNSUPPORTED, "hss_down: no instance for k=%d nt=%d", k, nt);
+hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  return hss_plan_ex(tree->n, tree->leaf, tree->levels, 0, k, nrhs, flags, P);
 }
 
 // Levels with at least kTreeBigLevel nodes run one launch per level; the
@@ -618,7 +674,7 @@ hm_status hss_down_dispatch(const hm::HssDownParams& dp, int k, int nt, cudaStre
 constexpr int64_t kTreeBigLevel = 2048;
 
 template <int KT, int NT>
-hm_status tree_launch(const hm::TreeParams& tp, int p, cudaStream_t s) {
+hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s) {
   constexpr int MINB = (KT == 32 && NT == 4) ? 3 : 0;  // measured, r01_tuning.md
   const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
   static bool attrs = false;
@@ -636,13 +692,13 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, cudaStream_t s) {
   while (lbig <= p && (1ll << lbig) < kTreeBigLevel) ++lbig;
   hm_status st;
   // upsweep: big levels p-1 .. lbig one launch each
-  for (int l = p - 1; l >= lbig; --l) {
+  for (int l = p - 1; up && l >= lbig; --l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
     st = launch("hss_up_level", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
-  const int up_from = std::min(p - 1, lbig - 1), down_to = std::min(p, lbig - 1);
+  const int up_from = up ? std::min(p - 1, lbig - 1) : 0, down_to = down ? std::min(p, lbig - 1) : 0;
   if (up_from >= 1 || down_to >= 1) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -660,7 +716,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, cudaStream_t s) {
     if (st) return st;
   }
   // downsweep: big levels lbig .. p one launch each
-  for (int l = std::max(lbig, 1); l <= p; ++l) {
+  for (int l = std::max(lbig, 1); down && l <= p; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
     st = launch("hss_down_level", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
@@ -668,12 +724,12 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, cudaStream_t s) {
   return HM_OK;
 }
 
-hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, cudaStream_t s) {
-#define HM_TREE(KT_)                                           \
-  if (k == KT_) {                                              \
-    if (nt == 1) return tree_launch<KT_, 1>(tp, p, s);         \
-    if (nt == 2) return tree_launch<KT_, 2>(tp, p, s);         \
-    return tree_launch<KT_, 4>(tp, p, s);                      \
+hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s) {
+#define HM_TREE(KT_)                                                   \
+  if (k == KT_) {                                                      \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s);       \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s);       \
+    return tree_launch<KT_, 4>(tp, p, up, down, s);                    \
   }
   HM_TREE(16)
   HM_TREE(32)
@@ -682,19 +738,126 @@ hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, cudaStre
   return fail(HM_ERR_UNSUPPORTED, "hss tree: no instance for k=%d", k);
 }
 
+// Upsweep and coupling/downsweep of a (sub)tree of depth p on its workspace:
+// generic per-level kernels or the DMMA tree kernels (tree_dispatch).
+hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
+                         double* yh, const double* R_root, const double* y_root, bool up, bool down,
+                         cudaStream_t stream) {
+  const int k = P.k, nrhs = P.m;
+  hm_status st;
+  if (P.mma_levels) {
+    hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, 0};
+    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream);
+  }
+  const int64_t km = (int64_t)k * nrhs;
+  if (up)
+    for (int l = p - 1; l >= 1; --l) {
+      hm::HssLevelParams hp{W, B, xh, yh, nullptr, nullptr, l, k, nrhs, 0};
+      const int64_t total = ((int64_t)1 << l) * km;
+      const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+      st = launch("hss_up_level", stream, [&] { hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+      if (st) return st;
+    }
+  if (down)
+    for (int l = 1; l <= p; ++l) {
+      hm::HssLevelParams hp{R, B, xh, yh, R_root, y_root, l, k, nrhs, 0};
+      const int64_t total = ((int64_t)1 << l) * km;
+      const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+      st = launch("hss_down_level", stream,
+                  [&] { hm::hss_down_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+      if (st) return st;
+    }
+  return HM_OK;
+}
+
+// x_out = A^T Z for one block (A [K][k], Z [K][m]): the subtree root's upsweep
+// step x_root = W_root^T [x_{1,0}; x_{1,1}] and the leaf-only subtree x = V^T X.
+hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int64_t K, double* out,
+                        cudaStream_t stream) {
+  const int k = P.k, nrhs = P.m;
+  if (nrhs >= 2 && pow2_rank(k, 16, 64) && K % 4 == 0) {
+    hm::BatchedVtParams bp{A, 0, Z, 0, out, 0, 1, (int32_t)K, nrhs};
+    return vt_batched_dispatch("vt_contract", bp, k, nt_for(nrhs, HM_VTB_NTMAX), stream);
+  }
+  hm::VtParams vp;
+  memset(&vp, 0, sizeof vp);
+  vp.X = Z; vp.n = K; vp.m = nrhs; vp.mc = vt_mc(K, nrhs); vp.tile = K; vp.nlev = 1;
+  vp.lev[0].V = A; vp.lev[0].k = k; vp.lev[0].s = K; vp.lev[0].out = out; vp.lev[0].partial = nullptr;
+  return vt_generic(vp, K, stream);
+}
+
+// Step 1 on the subtree: leaf x = V^T X, upsweep to level 1, and (W_root given)
+// the subtree root's x_root = W_root^T [x_{1,0}; x_{1,1}]. A depth-0 subtree is
+// one leaf: its x is the root's, written to x_root.
+hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
+                       const double* W_root, double* x_root, cudaStream_t stream) {
+  const int k = P.k, nrhs = P.m;
+  const int64_t km = (int64_t)k * nrhs;
+  hm_status st;
+  double* xleaf = (P.p == 0) ? x_root : xh + (((int64_t)1 << P.p) - 2) * km;
+  if (xleaf == nullptr) return HM_OK;
+  if (P.vt == VtPath::kMma) {
+    hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
+    if ((st = vt_batched_dispatch("vt_contract", bp, k, P.nt_vt, stream))) return st;
+  } else {
+    hm::VtParams vp;
+    memset(&vp, 0, sizeof vp);
+    vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt ? P.mc_vt : vt_mc(P.b, nrhs);
+    vp.tile = P.tile ? P.tile : pick_tile(P.b, P.p, vp.mc); vp.nlev = 1;
+    vp.lev[0].V = V; vp.lev[0].k = k; vp.lev[0].s = P.b;
+    vp.lev[0].out = xleaf;
+    vp.lev[0].partial = nullptr;
+    st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
+    if (st) return st;
+  }
+  if (P.p >= 2 && (st = hss_tree_phase(P, P.p, W, nullptr, nullptr, xh, nullptr, nullptr, nullptr, true, false,
+                                       stream)))
+    return st;
+  if (W_root && P.p >= 1 && (st = hss_single_vt(P, W_root, xh, 2 * k, x_root, stream))) return st;
+  return HM_OK;
+}
+
+// Step 4: Y(I_i) = U_i y_i + D_i X(I_i); y of the leaves from yh (or y_root for a
+// depth-0 subtree).
+hm_status hss_leaf_phase(const HssPlan& P, const double* D, const double* U, const double* Xd, double* Yd,
+                         const double* yleaf, cudaStream_t stream) {
+  hm::LeafParams lp;
+  memset(&lp, 0, sizeof lp);
+  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf;
+  const bool coupled = P.k > 0 && yleaf != nullptr;
+  if (coupled) {
+    hm::LeafSeg& sg = lp.seg[lp.nseg++];
+    sg.A = U;
+    sg.T = yleaf;
+    sg.k = P.k; sg.shift = 0; sg.xr = 0;
+    lp.ktot = P.k;
+  }
+  return leaf_dispatch(lp, 1ll << P.p, P.leaf, coupled ? P.k : 0, P.nt_leaf, P.mc_leaf, stream);
+}
+
+hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, const double* R, const double* W,
+                         const double* B, void* ws, size_t ws_bytes) {
+  if (!ws || ws_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
+  if (!aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+  const int k = P.k;
+  if (k == 0 || P.p + P.q == 0) return HM_OK;  // block diagonal: only D is read
+  if (!U || !V) return fail(HM_ERR_INVALID_ARG, "NULL U / V pointer");
+  if (P.p > 0 && !B) return fail(HM_ERR_INVALID_ARG, "NULL B pointer");
+  if (P.p > 1 && (!R || !W)) return fail(HM_ERR_INVALID_ARG, "NULL R / W pointer");
+  if (k > 0 && (!aligned16(U) || !aligned16(V) || (B && !aligned16(B)) || (R && !aligned16(R)) || (W && !aligned16(W))))
+    return fail(HM_ERR_INVALID_ARG, "U, V, R, W, B must be 16-byte aligned");
+  return HM_OK;
+}
+
 hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                   const double* R, const double* W, const double* B, const double* X, int32_t nrhs, double* Y,
                   void* ws, size_t ws_bytes, cudaStream_t stream, int32_t flags) {
   HssPlan P;
   hm_status st = hss_plan(tree, k, nrhs, flags, &P);
   if (st) return st;
-  if (!ws || ws_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
   if (!D || !X || !Y) return fail(HM_ERR_INVALID_ARG, "NULL D / X / Y pointer");
-  if (k > 0 && P.p > 0 && (!U || !V || !B)) return fail(HM_ERR_INVALID_ARG, "NULL U / V / B pointer");
-  if (k > 0 && P.p > 1 && (!R || !W)) return fail(HM_ERR_INVALID_ARG, "NULL R / W pointer");
-  if (!aligned16(D) || !aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "D and workspace must be 16-byte aligned");
-  if (k > 0 && P.p > 0 && (!aligned16(U) || !aligned16(V) || !aligned16(B) || (P.p > 1 && (!aligned16(R) || !aligned16(W)))))
-    return fail(HM_ERR_INVALID_ARG, "U, V, R, W, B must be 16-byte aligned");
+  if (!aligned16(D)) return fail(HM_ERR_INVALID_ARG, "D must be 16-byte aligned");
+  if ((st = hss_check_ptrs(P, U, V, R, W, B, ws, ws_bytes))) return st;
   const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
   if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
   if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
@@ -716,63 +879,26 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   const int64_t km = (int64_t)k * nrhs;
   const bool coupled = (k > 0 && P.p > 0);
   if (coupled) {
-    // Step 1: v_i^p = V_i^T X(I_i) for every leaf (node size b: always complete)
-    double* xleaf = xh + (((int64_t)1 << P.p) - 2) * km;
-    if (P.vt == VtPath::kMma) {
-      hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
-      if ((st = vt_batched_dispatch("vt_contract", bp, k, P.nt_vt, stream))) return st;
-    } else {
-      hm::VtParams vp;
-      memset(&vp, 0, sizeof vp);
-      vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt; vp.tile = P.tile; vp.nlev = 1;
-      vp.lev[0].V = V; vp.lev[0].k = k; vp.lev[0].s = P.b;
-      vp.lev[0].out = xleaf;
-      vp.lev[0].partial = nullptr;
-      st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
-      if (st) return st;
-    }
-    if (P.mma_levels) {
-      // Step 1 (cont.) upsweep + Steps 2-3 coupling/downsweep: one cooperative launch
-      hm::TreeParams tp{W, R, B, xh, yh, nrhs, 0, 0, 0};
-      if ((st = tree_dispatch(tp, P.p, k, P.nt_down, stream))) return st;
-    } else {
-      // Step 1 (cont.): upsweep l = p-1 .. 1 through W^T
-      for (int l = P.p - 1; l >= 1; --l) {
-        hm::HssLevelParams hp{W, B, xh, yh, l, k, nrhs, 0};
-        const int64_t total = ((int64_t)1 << l) * km;
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
-        st = launch("hss_up_level", stream,
-                    [&] { hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
-        if (st) return st;
-      }
-      // Steps 2+3: coupling on level l (cores of the parents) + downsweep from l-1
-      for (int l = 1; l <= P.p; ++l) {
-        hm::HssLevelParams hp{R, B, xh, yh, l, k, nrhs, 0};
-        const int64_t total = ((int64_t)1 << l) * km;
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
-        st = launch("hss_down_level", stream,
-                    [&] { hm::hss_down_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
-        if (st) return st;
-      }
-    }
+    if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
+    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream))) return st;
   }
-  // Step 4: Y(I_i) = U_i y_i^p + D_i X(I_i)
-  hm::LeafParams lp;
-  memset(&lp, 0, sizeof lp);
-  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = nrhs; lp.mc = P.mc_leaf;
-  if (coupled) {
-    hm::LeafSeg& sg = lp.seg[lp.nseg++];
-    sg.A = U;
-    sg.T = yh + (((int64_t)1 << P.p) - 2) * km;
-    sg.k = k; sg.shift = 0; sg.xr = 0;
-    lp.ktot = k;
-  }
-  if ((st = leaf_dispatch(lp, 1ll << P.p, P.leaf, coupled ? k : 0, P.nt_leaf, P.mc_leaf, stream))) return st;
+  const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
+  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");
   }
   return HM_OK;
+}
+
+// ---- distributed HSS ----
+
+hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, int32_t flags,
+                        HssPlan* P, DistPart* d) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  if ((st = check_part(tree, part, d))) return st;
+  return hss_plan_ex(tree->n >> d->q, tree->leaf, tree->levels - d->q, d->q, k, nrhs, flags, P);
 }
 
 }  // namespace
@@ -824,6 +950,157 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k, const double* D, con
                             int32_t nrhs, double* Y_host, void* workspace, size_t workspace_bytes, void* stream) {
   return hss_run(tree, k, D, U, V, R, W, B, X_host, nrhs, Y_host, workspace, workspace_bytes,
                  static_cast<cudaStream_t>(stream), HM_WS_HOSTIO);
+}
+
+// ---------------------------------------------------------------- multi-GPU --
+
+hm_status hm_hodlr_dist_sizes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, const hm_part* part,
+                              size_t* ws_bytes, int64_t* send_doubles) {
+  HodlrPlan P;
+  DistPart d;
+  hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (ws_bytes) *ws_bytes = P.total;
+  if (send_doubles) *send_doubles = P.top_doubles;
+  return HM_OK;
+}
+
+hm_status hodlr_matvec_dist_begin(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                  const double* V_local, const double* X_local, int32_t nrhs, double* send,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  HodlrPlan P;
+  DistPart d;
+  hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!workspace || workspace_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace too small");
+  if (!X_local || (P.k > 0 && !V_local) || (P.top_doubles > 0 && !send))
+    return fail(HM_ERR_INVALID_ARG, "NULL V / X / send pointer");
+  g_launches = 0;
+  prof_new_call();
+  return hodlr_vt_phase(P, ranks, V_local, X_local, static_cast<char*>(workspace), 1, P.q, send,
+                        static_cast<cudaStream_t>(stream));
+}
+
+hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                  const double* V_local, const double* X_local, int32_t nrhs, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  HodlrPlan P;
+  DistPart d;
+  hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!workspace || workspace_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace too small");
+  if (!X_local || (P.k > 0 && !V_local)) return fail(HM_ERR_INVALID_ARG, "NULL V / X pointer");
+  g_launches = 0;
+  prof_new_call();
+  return hodlr_vt_phase(P, ranks, V_local, X_local, static_cast<char*>(workspace), P.q + 1, P.q + P.p, nullptr,
+                        static_cast<cudaStream_t>(stream));
+}
+
+hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
+                                const double* D_local, const double* U_local, const double* X_local, int32_t nrhs,
+                                const double* gathered, double* Y_local, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  HodlrPlan P;
+  DistPart d;
+  hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!D_local || !aligned16(D_local)) return fail(HM_ERR_INVALID_ARG, "D_local NULL or misaligned");
+  if ((st = hodlr_check_ptrs(P, D_local, U_local, U_local, X_local, Y_local, workspace, workspace_bytes, 0)))
+    return st;
+  if (P.top_doubles > 0 && !gathered) return fail(HM_ERR_INVALID_ARG, "NULL gathered pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  double* ttop = reinterpret_cast<double*>(w + P.off_ttop);
+  g_launches = 0;
+  prof_new_call();
+  if (P.top_doubles > 0) {
+    hm::CombineParams cp;
+    memset(&cp, 0, sizeof cp);
+    cp.gathered = gathered; cp.out = ttop; cp.per_rank = P.top_doubles; cp.q = d.q; cp.rank = d.rank;
+    int64_t off = 0;
+    for (int l = 1; l <= d.q; ++l) {
+      cp.lev_off[l] = off;
+      off += (int64_t)ranks[l - 1] * nrhs;
+    }
+    cp.lev_off[d.q + 1] = off;
+    const unsigned grid = (unsigned)((P.top_doubles + hm::kThreads - 1) / hm::kThreads);
+    st = launch("dist_combine", s, [&] { hm::dist_combine_kernel<<<grid, hm::kThreads, 0, s>>>(cp); });
+    if (st) return st;
+  }
+  return hodlr_leaf_phase(P, ranks, D_local, U_local, X_local, Y_local, w, ttop, s);
+}
+
+hm_status hm_hss_dist_sizes(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, size_t* ws_bytes,
+                            int64_t* send_doubles) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (ws_bytes) *ws_bytes = P.total;
+  if (send_doubles) *send_doubles = (d.q > 0) ? (int64_t)k * nrhs : 0;
+  return HM_OK;
+}
+
+hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* part, const double* V_local,
+                                const double* W_sub, const double* W_root, const double* X_local, int32_t nrhs,
+                                double* send, void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
+    return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
+  g_launches = 0;
+  prof_new_call();
+  if (k == 0 || d.q == 0) return HM_OK;  // nothing to exchange
+  if (!X_local || !V_local || !send || (P.p >= 2 && !W_sub) || (P.p >= 1 && !W_root))
+    return fail(HM_ERR_INVALID_ARG, "NULL V / W / X / send pointer");
+  double* xh = reinterpret_cast<double*>(static_cast<char*>(workspace) + P.off_xh);
+  return hss_up_phase(P, V_local, W_sub, X_local, xh, W_root, send, static_cast<cudaStream_t>(stream));
+}
+
+hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* part, const double* D_local,
+                              const double* U_local, const double* R_sub, const double* B_sub,
+                              const double* R_root, const double* W_top, const double* R_top, const double* B_top,
+                              const double* X_local, int32_t nrhs, const double* gathered, double* Y_local,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!D_local || !X_local || !Y_local || !aligned16(D_local))
+    return fail(HM_ERR_INVALID_ARG, "NULL or misaligned D / X / Y pointer");
+  if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
+    return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  double* xh = reinterpret_cast<double*>(w + P.off_xh);
+  double* yh = reinterpret_cast<double*>(w + P.off_yh);
+  double* txh = reinterpret_cast<double*>(w + P.off_txh);
+  double* tyh = reinterpret_cast<double*>(w + P.off_tyh);
+  const int64_t km = (int64_t)k * nrhs;
+  g_launches = 0;
+  prof_new_call();
+  const double* yleaf = nullptr;
+  if (k > 0 && d.q > 0) {
+    if (!gathered || !U_local || !B_top || (d.q >= 2 && (!W_top || !R_top)) || (P.p >= 1 && (!R_root || !B_sub)) ||
+        (P.p >= 2 && !R_sub))
+      return fail(HM_ERR_INVALID_ARG, "NULL gathered / generator pointer");
+    // replicated top tree: x of level q from the allgather, up q-1..1, down 1..q
+    if (cudaMemcpyAsync(txh + (((int64_t)1 << d.q) - 2) * km, gathered, sizeof(double) * (size_t)(d.P * km),
+                        cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return cuda_check("copy of the gathered blocks");
+    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s))) return st;
+    const double* y_root = tyh + (((int64_t)1 << d.q) - 2 + d.rank) * km;
+    if (P.p >= 1) {
+      // the subtree's x blocks were left in this workspace by _begin
+      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s))) return st;
+      yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+    } else {
+      yleaf = y_root;
+    }
+  }
+  return hss_leaf_phase(P, D_local, U_local, X_local, Y_local, yleaf, s);
 }
 
 const char* hm_last_error(void) { return g_err.c_str(); }

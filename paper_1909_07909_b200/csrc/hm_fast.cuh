@@ -573,116 +573,4 @@ __global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, in
   }
 }
 
-// HSS coupling + downsweep on level l (reading G1), one warp per
-// node j: y_j = S_w x_{j^1} + [l >= 2] R_w y_parent, w = j & 1, as one
-// row-major product [S_w | R_w] (k x 2k) . [x_{j^1}; y_parent] (2k x m).
-struct HssDownParams {
-  const double* B;   // cores  [2^p-1][2][k][k]
-  const double* R;   // transl [2^p-2][2k][k]
-  const double* xh;  // level-major coefficient blocks [k][m]
-  double* yh;
-  int32_t level, m;
-};
-
-// One warp task of the coupling + downsweep on level l: node j, 8-row group
-// rg, column chunk ck.  y_j[rg rows] = R_w[rg rows] y_parent + S_w[rg rows] x_{j^1}.
-template <int KT, int NT, bool COH = false>
-__device__ __forceinline__ void hss_down_task(const HssDownParams& P, int l, int64_t j, int rg, int ck, int lane) {
-  const int m = P.m;
-  const int c0 = ck * NT * 8;
-  const int64_t km = (int64_t)KT * m;
-  const int64_t q = j >> 1;
-  const int w = (int)(j & 1);
-  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * KT * KT + (int64_t)rg * 8 * KT;
-  const double* xs = P.xh + ((1ll << l) - 2 + (j ^ 1)) * km;
-  double acc[1][NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
-  if (l >= 2) {  // downsweep term R_w y_parent
-    const double* Rw = P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + w * KT + rg * 8) * KT;
-    const double* yp = P.yh + ((1ll << (l - 1)) - 2 + q) * km;
-    warp_rowmajor_mma<1, NT, true, COH>(acc, Rw, KT, KT, yp + c0, m, m - c0, lane);
-  }
-  warp_rowmajor_mma<1, NT, true, COH>(acc, S, KT, KT, xs + c0, m, m - c0, lane);  // coupling
-  const int i = lane >> 2, jj = lane & 3;
-  double* y = P.yh + ((1ll << l) - 2 + j) * km + (int64_t)(8 * rg + i) * m;
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int c = c0 + nt * 8 + 2 * jj;
-    if (c + 1 < m) {
-      y[c] = acc[0][nt][0];
-      y[c + 1] = acc[0][nt][1];
-    } else if (c < m) {
-      y[c] = acc[0][nt][0];
-    }
-  }
-}
-
-template <int KT, int NT>
-__global__ void __launch_bounds__(256) hss_down_mma_kernel(const HssDownParams P) {
-  constexpr int RGS = KT / 8;  // 8-row groups per node
-  const int lane = threadIdx.x & 31;
-  const int nck = (P.m + NT * 8 - 1) / (NT * 8);
-  const int64_t cnt = 1ll << P.level;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t per = (int64_t)RGS * nck;
-  const int64_t j = gw / per;
-  if (j >= cnt) return;
-  const int sub = (int)(gw - j * per);
-  hss_down_task<KT, NT>(P, P.level, j, sub % RGS, sub / RGS, lane);
-}
-
-// The whole tree part of the HSS product in ONE persistent cooperative launch:
-// upsweep levels l = up_hi .. 1 (x_l = W^T [x_{l+1}; x_{l+1}]), then coupling
-// + downsweep levels l = 1 .. down_hi, one grid-wide barrier between levels
-// (each level depends on the previous one). Every level's tasks are spread
-// over all resident warps, so the small top levels cost a barrier instead of
-// a launch each.
-struct HssSweepParams {
-  const double* W;
-  const double* R;
-  const double* B;
-  double* xh;
-  double* yh;
-  int32_t m, up_hi, down_hi, pad;
-};
-
-template <int KT, int NTU, int NTD>
-__global__ void __launch_bounds__(256) hss_sweep_kernel(const HssSweepParams P) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  constexpr int MG = KT / 16;
-  constexpr int RGS = KT / 8;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int m = P.m;
-  const int64_t km = (int64_t)KT * m;
-  const int ncku = (m + NTU * 8 - 1) / (NTU * 8);
-  for (int l = P.up_hi; l >= 1; --l) {
-    BatchedVtParams bp{P.W + ((1ll << l) - 2) * 2 * KT * KT, 2ll * KT * KT, P.xh + ((1ll << (l + 1)) - 2) * km, 2 * km,
-                       P.xh + ((1ll << l) - 2) * km, km, 1ll << l, 2 * KT, m};
-    const int64_t per = (int64_t)MG * ncku;
-    const int64_t tasks = (1ll << l) * per;
-    for (int64_t t = w0; t < tasks; t += nw) {
-      const int64_t jseg = t / per;
-      const int sub = (int)(t - jseg * per);
-      vt_batched_task<KT, 1, NTU, true>(bp, jseg, sub % MG, sub / MG, lane);
-    }
-    grid.sync();
-  }
-  const int nckd = (m + NTD * 8 - 1) / (NTD * 8);
-  HssDownParams dp{P.B, P.R, P.xh, P.yh, 0, m};
-  for (int l = 1; l <= P.down_hi; ++l) {
-    const int64_t per = (int64_t)RGS * nckd;
-    const int64_t tasks = (1ll << l) * per;
-    for (int64_t t = w0; t < tasks; t += nw) {
-      const int64_t j = t / per;
-      const int sub = (int)(t - j * per);
-      hss_down_task<KT, NTD, true>(dp, l, j, sub % RGS, sub / RGS, lane);
-    }
-    if (l < P.down_hi) grid.sync();
-  }
-}
-
 }  // namespace hm

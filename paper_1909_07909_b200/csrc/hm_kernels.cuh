@@ -183,6 +183,31 @@ __global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceP
   if (active && g == 0) lv.out[oi] = s;
 }
 
+// Distributed HODLR: after the allgather of every rank's
+// partial top-level products t_l^(r) = V_l(I_r)^T X(I_r), rank `rank` needs
+// t_{l, sib} = sum of the partials of the ranks under the sibling of its
+// level-l ancestor, summed in increasing rank order (fixed order).
+struct CombineParams {
+  const double* gathered;  // [P][per_rank]
+  double* out;             // [per_rank]
+  int64_t per_rank;        // sum_{l <= q} k_l m
+  int32_t q, rank;
+  int64_t lev_off[kMaxLevels + 2];  // start of level l's block (l = 1..q), lev_off[q+1] = per_rank
+};
+
+__global__ void __launch_bounds__(kThreads) dist_combine_kernel(const CombineParams C) {
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= C.per_rank) return;
+  int l = 1;
+  while (l < C.q && C.lev_off[l + 1] <= e) ++l;
+  const int a = C.rank >> (C.q - l);
+  const int span = 1 << (C.q - l);
+  const int r0 = (a ^ 1) * span;
+  double s = 0.0;
+  for (int r = r0; r < r0 + span; ++r) s += C.gathered[(int64_t)r * C.per_rank + e];
+  C.out[e] = s;
+}
+
 // ------------------------------------------------------------ leaf_apply --
 
 struct LeafSeg {
@@ -289,6 +314,8 @@ struct HssLevelParams {
   const double* B;
   double* xh;        // [(2^{p+1}-2)][k][m]
   double* yh;
+  const double* R_root;  // optional subtree-root term at level 1 (distributed HSS)
+  const double* y_root;
   int32_t level;
   int32_t k;
   int32_t m;
@@ -338,6 +365,9 @@ __global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const HssLevel
       const double* Rn = P.W + (((1ll << (l - 1)) - 2 + q) * 2 * k + w * k) * k;
       const double* yp = P.yh + ((1ll << (l - 1)) - 2 + q) * km;
       for (int r = 0; r < k; ++r) yd = fma(Rn[a * k + r], yp[r * m + c], yd);
+    } else if (P.R_root) {
+      const double* Rn = P.R_root + (int64_t)w * k * k;
+      for (int r = 0; r < k; ++r) yd = fma(Rn[a * k + r], P.y_root[r * m + c], yd);
     }
     P.yh[((1ll << l) - 2 + j) * km + o] = yc + yd;
   }

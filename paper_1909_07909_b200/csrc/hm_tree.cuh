@@ -18,13 +18,14 @@
 namespace hm {
 
 struct TreeParams {
-  const double* W;  // [2^p-2][2k][k]
-  const double* R;  // [2^p-2][2k][k]
-  const double* B;  // [2^p-1][2][k][k]
-  double* xh;       // level-major coefficient blocks [k][m]
+  const double* W;       // [2^p-2][2k][k]
+  const double* R;       // [2^p-2][2k][k]
+  const double* B;       // [2^p-1][2][k][k]
+  double* xh;            // level-major coefficient blocks [k][m]
   double* yh;
+  const double* R_root;  // optional (distributed subtree): translation of the subtree root,
+  const double* y_root;  //   [2k][k], and its y block [k][m]: adds R_root[w] y_root at level 1
   int32_t m;
-  int32_t lo, hi;   // level range for the sweep kernel (up: hi-1 .. lo... see kernels)
   int32_t pad;
 };
 
@@ -127,14 +128,17 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
   const int zs = tree_down_stride(mp);
   const int64_t km = (int64_t)KT * m;
   stage_rows_async(sm, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
+  const bool root_term = (l == 1 && P.R_root != nullptr);
   if (l >= 2) stage_rows_async(sm + 2 * KT * zs, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  if (root_term) stage_rows_async(sm + 2 * KT * zs, zs, P.y_root, m, KT, m, mp);
   cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = w >> 2, sub = w & 3;
   const int64_t j = 2 * q + nd;
   const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + nd) * KT * KT;
-  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT : nullptr;
+  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT
+                     : (root_term ? P.R_root + (int64_t)nd * KT * KT : nullptr);
   const double* Zx = sm + (1 - nd) * KT * zs;  // the sibling's x
   const double* Zy = sm + 2 * KT * zs;
   double* yo = P.yh + ((1ll << l) - 2 + j) * km;

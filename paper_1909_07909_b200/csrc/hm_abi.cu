@@ -183,7 +183,7 @@ void allow_smem(K kernel, size_t bytes) {
 // ranks[l-1] = k_l for all of them.
 
 enum class VtPath { kNone, kGeneric, kGemv, kMma };
-enum class LeafPath { kGeneric, kGemv, kMma };
+enum class LeafPath { kGeneric, kGemv, kMma };  // kGemv: TMA ring when the shape allows (leaf_gemv_tma)
 
 struct HodlrPlan {
   int64_t n, b;
@@ -294,11 +294,57 @@ hm_status launch_leaf_generic(const hm::LeafParams& lp, int64_t nleaves, cudaStr
   return launch("leaf_apply", s, [&] { hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
 }
 
+template <int K, int NCH>
+hm_status launch_leaf_gemv_n(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  constexpr int ROWS = NCH >= 8 ? 2 : (NCH == 0 ? 4 : HM_GEMV_ROWS);
+  size_t smem = sizeof(double) * (size_t)(2 * lp.b + lp.nseg * K);
+  allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS>, smem);
+  return launch("leaf_apply", s,
+                [&] { hm::leaf_gemv_kernel<K, NCH, ROWS><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+}
+
+#ifndef HM_NO_TMA
+#define HM_NO_TMA 0
+#endif
+constexpr int kTmaStages = 6;
+
+template <int K, int NCH>
+hm_status launch_leaf_gemv_tma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
+  const size_t smem = (size_t)kTmaStages * hm::kTmaChunkBytes + 2 * kTmaStages * sizeof(uint64_t) +
+                      sizeof(double) * (size_t)(2 * 64 * NCH + lp.nseg * K);
+  allow_smem(hm::leaf_gemv_tma_kernel<K, NCH>, smem);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>(nleaves, sms);
+  return launch("leaf_apply", s, [&] {
+    hm::leaf_gemv_tma_kernel<K, NCH><<<grid, 32 * (hm::kTmaConsumers + 1), smem, s>>>(lp, nleaves, kTmaStages);
+  });
+}
+
+// nrhs = 1 leaf pass: the TMA ring wins when the U rows are a large share of
+// the leaf's bytes (k >= 8: config 3 m=1, 604 vs 649 us); for k < 8 (config 5)
+// the register-streaming kernel wins (5.25 vs 6.45 ms) — measured, r01_tuning.md.
 template <int K>
 hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
-  size_t smem = sizeof(double) * (size_t)(2 * lp.b + lp.nseg * K);
-  allow_smem(hm::leaf_gemv_kernel<K>, smem);
-  return launch("leaf_apply", s, [&] { hm::leaf_gemv_kernel<K><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+  if constexpr (K >= 8 && K <= 32) {
+    if (!HM_NO_TMA && lp.b * K <= 4096) {
+      switch (lp.b) {
+        case 64: return launch_leaf_gemv_tma<K, 1>(lp, nleaves, s);
+        case 128: return launch_leaf_gemv_tma<K, 2>(lp, nleaves, s);
+        case 256: return launch_leaf_gemv_tma<K, 4>(lp, nleaves, s);
+        case 512: if constexpr (K <= 8) return launch_leaf_gemv_tma<K, 8>(lp, nleaves, s); break;
+        default: break;
+      }
+    }
+  }
+  switch (lp.b) {
+    case 64: return launch_leaf_gemv_n<K, 1>(lp, nleaves, s);
+    case 128: return launch_leaf_gemv_n<K, 2>(lp, nleaves, s);
+    case 256: return launch_leaf_gemv_n<K, 4>(lp, nleaves, s);
+    case 512: return launch_leaf_gemv_n<K, 8>(lp, nleaves, s);
+    default: return launch_leaf_gemv_n<K, 0>(lp, nleaves, s);
+  }
 }
 
 // (RG, NT) -> prefetch depth and launch-bound occupancy (measured, r01_tuning.md)

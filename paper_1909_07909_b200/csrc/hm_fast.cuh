@@ -29,6 +29,7 @@ namespace hm {
 
 // ------------------------------------------------------------ primitives --
 
+// Streaming (evict-first, ld.global.cs) loads for data read exactly once.
 __device__ __forceinline__ double2 ldg_stream2(const double* p) {
   double2 v;
   asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -39,6 +40,11 @@ __device__ __forceinline__ double ldg_stream(const double* p) {
   asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// Register fence: every value passed must be available here, and nothing that
+// uses it may move above. Placed after a batch of (volatile, hence ordered)
+// loads it keeps the whole batch in flight before the first use — ptxas would
+// otherwise interleave each load with its FMAs to save registers.
+__device__ __forceinline__ void reg_fence(double2& v) { asm volatile("" : "+d"(v.x), "+d"(v.y)); }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 // Coherent (L2) load for data written earlier in the same launch (cooperative
 // kernels): never the non-coherent read-only path.
@@ -176,13 +182,18 @@ __global__ void __launch_bounds__(256) vt_gemv_kernel(const VtGemvParams P) {
 }
 
 // leaf_gemv: one CTA (256 threads) per leaf. D part: warp w owns rows
-// w, w+8, ...; a row is b doubles = b/64 128-bit chunks per lane, 4 rows in
-// flight per warp. U part: thread-per-row over every segment (K columns each).
-template <int K>
+// w, w+8, ...; a row is b doubles = NCH = b/64 128-bit chunks per lane; ROWS
+// rows x NCH chunks (all compile-time) are requested before the first FMA, so
+// every warp keeps ROWS*NCH*512 B of D in flight. U part: thread-per-row over
+// every segment (K columns each). NCH = 0: runtime b (any multiple of 64).
+#ifndef HM_GEMV_ROWS
+#define HM_GEMV_ROWS 4
+#endif
+template <int K, int NCH, int ROWS>
 __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   const int64_t leaf = blockIdx.x;
-  const int64_t b = P.b;
+  const int64_t b = NCH > 0 ? 64 * NCH : P.b;
   const int64_t r0 = leaf * b;
   double* xs = sm;            // [b]
   double* yd = sm + b;        // [b]
@@ -196,23 +207,45 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Di = P.D + leaf * b * b;
-  const int nch = (int)(b / 64);
-  // rows warp, warp+8, ... processed 4 at a time
-  for (int64_t rb = warp; rb < b; rb += 32) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int c = 0; c < nch; ++c) {
-      double2 v[4];
+  const int nch = NCH > 0 ? NCH : (int)(b / 64);
+  for (int64_t rb = warp; rb < b; rb += 8 * ROWS) {
+    double acc[ROWS];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t r = rb + 8 * u;
-        v[u] = (r < b) ? ldg_stream2(Di + r * b + 64 * c + 2 * lane) : make_double2(0.0, 0.0);
+    for (int u = 0; u < ROWS; ++u) acc[u] = 0.0;
+    if constexpr (NCH > 0) {
+      double2 v[ROWS][NCH];
+#pragma unroll
+      for (int u = 0; u < ROWS; ++u)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int64_t r = rb + 8 * u;  // b = 64 NCH is a multiple of 8 ROWS: always a row
+          v[u][c] = ldg_stream2(Di + r * b + 64 * c + 2 * lane);
+        }
+#pragma unroll
+      for (int u = 0; u < ROWS; ++u)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) reg_fence(v[u][c]);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const double2 x = *reinterpret_cast<const double2*>(xs + 64 * c + 2 * lane);
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u) acc[u] = fma(v[u][c].y, x.y, fma(v[u][c].x, x.x, acc[u]));
       }
-      const double2 x = *reinterpret_cast<const double2*>(xs + 64 * c + 2 * lane);
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        double2 v[ROWS];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(v[u].y, x.y, fma(v[u].x, x.x, acc[u]));
+        for (int u = 0; u < ROWS; ++u) {
+          const int64_t r = rb + 8 * u;
+          v[u] = (r < b) ? ldg_stream2(Di + r * b + 64 * c + 2 * lane) : make_double2(0.0, 0.0);
+        }
+        const double2 x = *reinterpret_cast<const double2*>(xs + 64 * c + 2 * lane);
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u) acc[u] = fma(v[u].y, x.y, fma(v[u].x, x.x, acc[u]));
+      }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < ROWS; ++u) {
       const double s = warp_sum(acc[u]);
       const int64_t r = rb + 8 * u;
       if (lane == 0 && r < b) yd[r] = s;
@@ -241,6 +274,177 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   __syncthreads();
   nr = 0;
   for (int64_t r = threadIdx.x; r < b; r += 256, ++nr) P.Y[r0 + r] = yd[r] + yu[nr];
+}
+
+// ------------------------------------------------ TMA bulk-copy leaf GEMV --
+// leaf_gemv_tma: persistent CTAs (one per SM), warp-specialised. One producer
+// thread streams every leaf's D rows and U_l rows with 1-D bulk async copies
+// (cp.async.bulk, SASS UBLKCP) into an NS-stage shared-memory ring, completion
+// signalled on mbarriers (expect_tx); 8 consumer warps compute from shared
+// memory and release stages through "empty" mbarriers. Deep, register-free
+// memory-level parallelism (NS x 32 KB in flight per SM) for the pure-HBM
+// nrhs = 1 leaf pass (BASELINE configs 3 (m=1) and 5).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// Bounded wait: a protocol bug traps (a reported launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t it = 0; it < (1u << 28); ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+constexpr int kTmaChunkBytes = 32 * 1024;
+constexpr int kTmaConsumers = 8;  // warps
+
+// Per leaf: nD chunks of `rpc` D rows, then nU chunks of G consecutive U segments.
+template <int K, int NCH>
+__global__ void __launch_bounds__(32 * (kTmaConsumers + 1), 1)
+    leaf_gemv_tma_kernel(const LeafParams P, int64_t nleaves, int NS) {
+  constexpr int B = 64 * NCH;
+  constexpr int RPC = kTmaChunkBytes / (B * 8);          // D rows per chunk
+  constexpr int SEGB = B * K * 8;                        // bytes of one U segment of a leaf
+  constexpr int G = SEGB >= kTmaChunkBytes ? 1 : kTmaChunkBytes / SEGB;  // segments per U chunk
+  static_assert(RPC >= 1 && RPC % 1 == 0, "leaf too large for a 32 KB chunk row");
+  extern __shared__ __align__(128) unsigned char tsm[];
+  unsigned char* ring = tsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)NS * kTmaChunkBytes);
+  uint64_t* empty = full + NS;
+  double* xs = reinterpret_cast<double*>(empty + NS);  // [B]
+  double* yd = xs + B;                                 // [B]
+  double* ts = yd + B;                                 // [nseg][K]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nseg = P.nseg;
+  const int nD = B / RPC;
+  const int nU = (nseg + G - 1) / G;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kTmaConsumers) {
+    // ---------------- producer (one thread) ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t leaf = blockIdx.x; leaf < nleaves; leaf += gridDim.x) {
+        const unsigned char* Dl = reinterpret_cast<const unsigned char*>(P.D + leaf * B * B);
+        for (int c = 0; c < nD; ++c) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], RPC * B * 8);
+          bulk_g2s(ring + (size_t)s * kTmaChunkBytes, Dl + (size_t)c * RPC * B * 8, RPC * B * 8, &full[s]);
+          if (++s == NS) { s = 0; ph ^= 1; }
+        }
+        for (int g = 0; g < nU; ++g) {
+          const int s0 = g * G, s1 = min(nseg, s0 + G);
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(s1 - s0) * SEGB);
+          for (int sg = s0; sg < s1; ++sg)
+            bulk_g2s(ring + (size_t)s * kTmaChunkBytes + (size_t)(sg - s0) * SEGB, P.seg[sg].A + leaf * B * K, SEGB,
+                     &full[s]);
+          if (++s == NS) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers (8 warps, 256 threads) ----------------
+  int s = 0;
+  uint32_t ph = 0;
+  const int t = threadIdx.x;
+  for (int64_t leaf = blockIdx.x; leaf < nleaves; leaf += gridDim.x) {
+    const int64_t r0 = leaf * B;
+    named_bar(1, 32 * kTmaConsumers);  // previous leaf fully written out
+    for (int e = t; e < B; e += 32 * kTmaConsumers) xs[e] = __ldg(P.X + r0 + e);
+    for (int sg = 0; sg < nseg; ++sg) {
+      const LeafSeg g = P.seg[sg];
+      const int64_t node = (leaf >> g.shift) ^ g.xr;
+      for (int a = t; a < K; a += 32 * kTmaConsumers) ts[sg * K + a] = __ldg(g.T + node * K + a);
+    }
+    named_bar(1, 32 * kTmaConsumers);
+    double2 xr[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) xr[j] = *reinterpret_cast<const double2*>(xs + 64 * j + 2 * lane);
+    for (int c = 0; c < nD; ++c) {
+      mbar_wait(&full[s], ph);
+      const double* chunk = reinterpret_cast<const double*>(ring + (size_t)s * kTmaChunkBytes);
+      for (int rr = warp; rr < RPC; rr += kTmaConsumers) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const double2 v = *reinterpret_cast<const double2*>(chunk + rr * B + 64 * j + 2 * lane);
+          acc = fma(v.y, xr[j].y, fma(v.x, xr[j].x, acc));
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) yd[c * RPC + rr] = acc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == NS) { s = 0; ph ^= 1; }
+    }
+    // U segments: thread per row (rows t, t + 256, ...)
+    double yu[(B + 255) / 256];
+#pragma unroll
+    for (int i = 0; i < (B + 255) / 256; ++i) yu[i] = 0.0;
+    for (int g = 0; g < nU; ++g) {
+      mbar_wait(&full[s], ph);
+      const double* chunk = reinterpret_cast<const double*>(ring + (size_t)s * kTmaChunkBytes);
+      const int s0 = g * G, s1 = min(nseg, s0 + G);
+      for (int sg = s0; sg < s1; ++sg) {
+        const double* Us = chunk + (size_t)(sg - s0) * B * K;
+        const double* tv = ts + sg * K;
+#pragma unroll
+        for (int i = 0; i < (B + 255) / 256; ++i) {
+          const int r = t + 256 * i;
+          if (r < B) {
+            double u = 0.0;
+#pragma unroll
+            for (int a = 0; a < K; ++a) u = fma(Us[r * K + ((a + r) & (K - 1))], tv[(a + r) & (K - 1)], u);
+            yu[i] += u;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == NS) { s = 0; ph ^= 1; }
+    }
+    named_bar(1, 32 * kTmaConsumers);  // every yd row written
+#pragma unroll
+    for (int i = 0; i < (B + 255) / 256; ++i) {
+      const int r = t + 256 * i;
+      if (r < B) P.Y[r0 + r] = yd[r] + yu[i];
+    }
+  }
 }
 
 // =================================================================== m >= 2 ==

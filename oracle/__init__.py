@@ -26,6 +26,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lib: Optional[ctypes.CDLL] = None
 
 _CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-Wall"]
+_LDLIBS = ["-lm"]
 
 
 def build(force: bool = False) -> str:
@@ -34,7 +35,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "hm_oracle.h"))
     ):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC, *_LDLIBS])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -57,6 +58,13 @@ def _load() -> ctypes.CDLL:
             "oracle_dense_matvec": [i64, P, P, i32, P],
             "oracle_laplacian_inverse_apply": [i64, P, i32, P],
             "oracle_num_threads": [],
+            "oracle_hodlr_matvec_t": [i64, i32, P, P, P, P, P, P, i32, P],
+            "oracle_hodlr_matvec_t_leaves": [i64, i32, P, P, P, P, P, P, i32, P, i64, P],
+            "oracle_hss_matvec_t": [i64, i32, P, i32, P, P, P, P, P, P, P, i32, P],
+            "oracle_hss_matvec_t_leaves": [i64, i32, P, i32, P, P, P, P, P, P, P, i32, P, i64, P],
+            "oracle_hodlr_norm2_est": [i64, i32, P, P, P, P, P, P, i32, P],
+            "oracle_hss_norm2_est": [i64, i32, P, i32, P, P, P, P, P, P, P, i32, P],
+            "oracle_hss_to_hodlr": [i64, i32, P, i32, P, P, P, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -205,3 +213,102 @@ def laplacian_inverse_apply(X) -> np.ndarray:
     Y = np.empty((n, m), dtype=np.float64)
     _check(_load().oracle_laplacian_inverse_apply(n, _ptr(X), m, _ptr(Y)), "laplacian_inverse_apply")
     return Y
+
+
+# ------------------------------------------------------------ adjoint (f1) --
+
+def hodlr_matvec_t(n, p, ranks, D, U, V, X, c=None) -> np.ndarray:
+    """Y = A^* X (A^T: real), Fig. 5 left on the adjoint's generators."""
+    c = _tree(n, p, c)
+    X = _X2(X)
+    m = X.shape[1]
+    ranks = np.ascontiguousarray(ranks if p > 0 else [0], dtype=np.int32)
+    D, U, V = _f64(D), _f64(U), _f64(V)
+    Y = np.empty((n, m), dtype=np.float64)
+    rc = _load().oracle_hodlr_matvec_t(n, p, _ptr(c), _ptr(ranks), _ptr(D), _ptr(U), _ptr(V), _ptr(X), m, _ptr(Y))
+    _check(rc, "hodlr_matvec_t")
+    return Y
+
+
+def hodlr_matvec_t_leaves(n, p, ranks, Dsel, U, V, X, leaves, c=None) -> np.ndarray:
+    c = _tree(n, p, c)
+    X = _X2(X)
+    m = X.shape[1]
+    ranks = np.ascontiguousarray(ranks if p > 0 else [0], dtype=np.int32)
+    leaves = np.ascontiguousarray(leaves, dtype=np.int64)
+    rows = sum(int(c[L] - (c[L - 1] if L > 0 else 0)) for L in leaves)
+    Dsel, U, V = _f64(Dsel), _f64(U), _f64(V)
+    Y = np.empty((rows, m), dtype=np.float64)
+    rc = _load().oracle_hodlr_matvec_t_leaves(
+        n, p, _ptr(c), _ptr(ranks), _ptr(Dsel), _ptr(U), _ptr(V), _ptr(X), m, _ptr(leaves), leaves.size, _ptr(Y)
+    )
+    _check(rc, "hodlr_matvec_t_leaves")
+    return Y
+
+
+def hss_matvec_t(n, p, k, D, U, V, R, W, B, X, c=None) -> np.ndarray:
+    """Y = A^* X, Fig. 5 right on the adjoint's generators."""
+    c = _tree(n, p, c)
+    X = _X2(X)
+    m = X.shape[1]
+    D, U, V, R, W, B = (_f64(a) for a in (D, U, V, R, W, B))
+    Y = np.empty((n, m), dtype=np.float64)
+    rc = _load().oracle_hss_matvec_t(
+        n, p, _ptr(c), k, _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(X), m, _ptr(Y)
+    )
+    _check(rc, "hss_matvec_t")
+    return Y
+
+
+def hss_matvec_t_leaves(n, p, k, Dsel, U, V, R, W, B, X, leaves, c=None) -> np.ndarray:
+    c = _tree(n, p, c)
+    X = _X2(X)
+    m = X.shape[1]
+    leaves = np.ascontiguousarray(leaves, dtype=np.int64)
+    rows = sum(int(c[L] - (c[L - 1] if L > 0 else 0)) for L in leaves)
+    Dsel, U, V, R, W, B = (_f64(a) for a in (Dsel, U, V, R, W, B))
+    Y = np.empty((rows, m), dtype=np.float64)
+    rc = _load().oracle_hss_matvec_t_leaves(
+        n, p, _ptr(c), k, _ptr(Dsel), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(X), m,
+        _ptr(leaves), leaves.size, _ptr(Y)
+    )
+    _check(rc, "hss_matvec_t_leaves")
+    return Y
+
+
+# ------------------------------------------------------ norm estimate (f2) --
+
+def hodlr_norm2_est(n, p, ranks, D, U, V, x0, iters, c=None) -> float:
+    """||A||_2 estimate: power method on A A^* (P:1146), `iters` steps from x0."""
+    c = _tree(n, p, c)
+    ranks = np.ascontiguousarray(ranks if p > 0 else [0], dtype=np.int32)
+    D, U, V, x0 = _f64(D), _f64(U), _f64(V), _f64(x0).ravel()
+    est = ctypes.c_double(0.0)
+    rc = _load().oracle_hodlr_norm2_est(n, p, _ptr(c), _ptr(ranks), _ptr(D), _ptr(U), _ptr(V), _ptr(x0),
+                                        int(iters), ctypes.addressof(est))
+    _check(rc, "hodlr_norm2_est")
+    return est.value
+
+
+def hss_norm2_est(n, p, k, D, U, V, R, W, B, x0, iters, c=None) -> float:
+    c = _tree(n, p, c)
+    D, U, V, R, W, B, x0 = (_f64(a) for a in (D, U, V, R, W, B, x0))
+    est = ctypes.c_double(0.0)
+    rc = _load().oracle_hss_norm2_est(n, p, _ptr(c), k, _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                                      _ptr(x0.ravel()), int(iters), ctypes.addressof(est))
+    _check(rc, "hss_norm2_est")
+    return est.value
+
+
+# ----------------------------------------------------------- hss2hodlr (f3) --
+
+def hss_to_hodlr(n, p, k, U, V, R, W, B, c=None):
+    """(Uh, Vh) level-major [p][n][k]: exact HODLR factors of the HSS matrix."""
+    c = _tree(n, p, c)
+    U, V, R, W, B = (_f64(a) for a in (U, V, R, W, B))
+    Uh = np.zeros(max(p, 1) * n * k, dtype=np.float64)
+    Vh = np.zeros(max(p, 1) * n * k, dtype=np.float64)
+    rc = _load().oracle_hss_to_hodlr(n, p, _ptr(c), k, _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                                     _ptr(Uh), _ptr(Vh))
+    _check(rc, "hss_to_hodlr")
+    return Uh[: p * n * k], Vh[: p * n * k]

@@ -16,6 +16,7 @@
  */
 #include "hm_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -115,6 +116,21 @@ static void dense_mul(int64_t rows, int64_t cols, const double* A, int64_t lda,
   }
 }
 
+/* Y[r][:] = sum_j A[j][r] X[j][:] — the product with A^T (A: cols x rows
+ * row-major, lda), sums over j in natural order. The adjoint's leaf term
+ * D_i^* v(I_i) (reading G4: * is the transpose). */
+static void dense_mul_t(int64_t rows, int64_t cols, const double* A, int64_t lda,
+                        const double* X, int32_t m, double* Y) {
+#pragma omp parallel for schedule(static) if (rows * cols * m > OMP_MIN_WORK)
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int32_t q = 0; q < m; ++q) {
+      double s = 0.0;
+      for (int64_t j = 0; j < cols; ++j) s += A[j * lda + r] * X[j * m + q];
+      Y[r * m + q] = s;
+    }
+  }
+}
+
 /* t = V^T x : t[a][q] = sum_{r} V[r][a] x[r][q], rows in natural order
  * (the (V_j^{(l)})^* v(I_j) products of P:645-651 / P:686). V has ld = k. */
 static void vt_mul(int64_t rows, int32_t k, const double* V, const double* X, int32_t m, double* t) {
@@ -139,6 +155,7 @@ typedef struct {
   int64_t* d_off;         /* leaf block offsets */
   const double *D, *U, *V, *X;
   int32_t m;
+  int trans;              /* 1: apply A^* (adjoint) */
   double* Y_out;
 } hodlr_ctx;
 
@@ -169,9 +186,10 @@ static int hodlr_rec(const hodlr_ctx* h, int32_t l, int64_t i) {
   int64_t lo, hi;
   node_range(h->c, h->p, l, i, &lo, &hi);
   int32_t m = h->m;
-  if (l == h->p) { /* "if A is dense return Av" */
+  if (l == h->p) { /* "if A is dense return Av" (A^* v for the adjoint) */
     int64_t s = hi - lo;
-    dense_mul(s, s, h->D + h->d_off[i], s, h->X + lo * m, m, h->Y_out + lo * m);
+    if (h->trans) dense_mul_t(s, s, h->D + h->d_off[i], s, h->X + lo * m, m, h->Y_out + lo * m);
+    else dense_mul(s, s, h->D + h->d_off[i], s, h->X + lo * m, m, h->Y_out + lo * m);
     return 0;
   }
   int64_t a = 2 * i, b = 2 * i + 1, alo, ahi, blo, bhi;
@@ -216,21 +234,30 @@ static void hodlr_teardown(hodlr_ctx* h) {
   free(h->d_off);
 }
 
-int oracle_hodlr_matvec(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
-                        const double* D, const double* U, const double* V,
-                        const double* X, int32_t m, double* Y) {
+/* The adjoint A^* of a HODLR matrix is a HODLR matrix on the same tree:
+ * A^*(I_a, I_b) = (A(I_b, I_a))^* = (U_l(I_b) V_l(I_a)^*)^* = V_l(I_a) U_l(I_b)^*
+ * for siblings a, b (Def. 2.2), and A^*(I_i, I_i) = D_i^*. So the
+ * adjoint product is Fig. 5 left with the roles of U and V exchanged and the
+ * leaf blocks transposed (P:404, P:416 use A^* products). */
+static int hodlr_matvec_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                           const double* D, const double* U, const double* V,
+                           const double* X, int32_t m, double* Y, int trans) {
   hodlr_ctx h;
-  if (hodlr_setup(&h, n, p, c, ranks, D, U, V, X, m) || Y == NULL) { hodlr_teardown(&h); return -1; }
+  if (hodlr_setup(&h, n, p, c, ranks, D, trans ? V : U, trans ? U : V, X, m) || Y == NULL) {
+    hodlr_teardown(&h);
+    return -1;
+  }
+  h.trans = trans;
   h.Y_out = Y;
   int rc = hodlr_rec(&h, 0, 0);
   hodlr_teardown(&h);
   return rc;
 }
 
-int oracle_hodlr_matvec_leaves(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
-                               const double* Dsel, const double* U, const double* V,
-                               const double* X, int32_t m,
-                               const int64_t* leaves, int64_t nleaves, double* Yout) {
+static int hodlr_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                                  const double* Dsel, const double* U, const double* V,
+                                  const double* X, int32_t m,
+                                  const int64_t* leaves, int64_t nleaves, double* Yout, int trans) {
   /* The recursion of Fig. 5 left, followed only down the root-to-leaf path of
    * each listed leaf. On that path, the rows of leaf L receive, in the
    * recursion's order: the leaf product D_L v(I_L) ("if A is dense return
@@ -238,7 +265,8 @@ int oracle_hodlr_matvec_leaves(int64_t n, int32_t p, const int64_t* c, const int
    * term U_l(I_L) (V_l(I_sib)^T v(I_sib)) of the block coupling the level-l
    * node on the path with its sibling ("y1 + y2" / "y3 + y4"). */
   hodlr_ctx h;
-  if (hodlr_setup(&h, n, p, c, ranks, NULL, U, V, X, m) || Yout == NULL || leaves == NULL) {
+  if (hodlr_setup(&h, n, p, c, ranks, NULL, trans ? V : U, trans ? U : V, X, m) || Yout == NULL ||
+      leaves == NULL) {
     hodlr_teardown(&h);
     return -1;
   }
@@ -249,7 +277,8 @@ int oracle_hodlr_matvec_leaves(int64_t n, int32_t p, const int64_t* c, const int
     if (L < 0 || L >= nl) { rc = -1; break; }
     int64_t lo = leaf_lo(c, L), hi = c[L], rows = hi - lo;
     double* y = Yout + yoff;
-    dense_mul(rows, rows, Dsel + doff, rows, X + lo * m, m, y);
+    if (trans) dense_mul_t(rows, rows, Dsel + doff, rows, X + lo * m, m, y);
+    else dense_mul(rows, rows, Dsel + doff, rows, X + lo * m, m, y);
     double* term = (double*)malloc(sizeof(double) * (size_t)(rows * m + 1));
     if (!term) { rc = -1; break; }
     for (int32_t l = p; l >= 1; --l) {
@@ -264,6 +293,32 @@ int oracle_hodlr_matvec_leaves(int64_t n, int32_t p, const int64_t* c, const int
   }
   hodlr_teardown(&h);
   return rc;
+}
+
+int oracle_hodlr_matvec(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                        const double* D, const double* U, const double* V,
+                        const double* X, int32_t m, double* Y) {
+  return hodlr_matvec_op(n, p, c, ranks, D, U, V, X, m, Y, 0);
+}
+
+int oracle_hodlr_matvec_t(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                          const double* D, const double* U, const double* V,
+                          const double* X, int32_t m, double* Y) {
+  return hodlr_matvec_op(n, p, c, ranks, D, U, V, X, m, Y, 1);
+}
+
+int oracle_hodlr_matvec_leaves(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                               const double* Dsel, const double* U, const double* V,
+                               const double* X, int32_t m,
+                               const int64_t* leaves, int64_t nleaves, double* Yout) {
+  return hodlr_matvec_leaves_op(n, p, c, ranks, Dsel, U, V, X, m, leaves, nleaves, Yout, 0);
+}
+
+int oracle_hodlr_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                                 const double* Dsel, const double* U, const double* V,
+                                 const double* X, int32_t m,
+                                 const int64_t* leaves, int64_t nleaves, double* Yout) {
+  return hodlr_matvec_leaves_op(n, p, c, ranks, Dsel, U, V, X, m, leaves, nleaves, Yout, 1);
 }
 
 int oracle_hodlr_dense(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
@@ -312,6 +367,7 @@ typedef struct {
   const double *D, *U, *V, *R, *W, *B, *X;
   double* xh; /* v_i^l of Step 1, one k x m block per node l = 1..p */
   double* yh; /* the same vectors after Steps 2-3 */
+  int trans;  /* 1: apply A^* (adjoint), see hss_matvec_op */
 } hss_ctx;
 
 static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, int32_t k,
@@ -379,13 +435,15 @@ static void hss_upsweep(hss_ctx* s) {
 static void hss_couple(hss_ctx* s, int32_t l, int64_t q, int which) {
   int32_t k = s->k, m = s->m;
   const double* Bn = s->B + (((int64_t)1 << (l - 1)) - 1 + q) * 2 * k * k;
-  const double* S = Bn + (which == 0 ? 0 : k * k);          /* B12 or B21 */
   const double* xin = s->xh + coef_index(l, 2 * q + (which == 0 ? 1 : 0)) * k * m;
   double* yout = s->yh + coef_index(l, 2 * q + which) * k * m;
+  /* A: S = B12 (which 0) or B21 (which 1). A^*: the cores of A^* are
+   * S'_{2q,2q+1} = (S_{2q+1,2q})^* = B21^T and S'_{2q+1,2q} = B12^T. */
+  const double* S = s->trans ? Bn + (which == 0 ? k * k : 0) : Bn + (which == 0 ? 0 : k * k);
   for (int32_t a = 0; a < k; ++a)
     for (int32_t c2 = 0; c2 < m; ++c2) {
       double acc = 0.0;
-      for (int32_t r = 0; r < k; ++r) acc += S[a * k + r] * xin[r * m + c2];
+      for (int32_t r = 0; r < k; ++r) acc += (s->trans ? S[r * k + a] : S[a * k + r]) * xin[r * m + c2];
       yout[a * m + c2] = acc;
     }
 }
@@ -415,7 +473,8 @@ static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double
   for (int64_t r = 0; r < rows; ++r)
     for (int32_t q = 0; q < m; ++q) {
       double d = 0.0;
-      for (int64_t j = 0; j < rows; ++j) d += Dblk[r * rows + j] * s->X[(lo + j) * m + q];
+      for (int64_t j = 0; j < rows; ++j)
+        d += (s->trans ? Dblk[j * rows + r] : Dblk[r * rows + j]) * s->X[(lo + j) * m + q];
       double u = 0.0;
       if (yv)
         for (int32_t a = 0; a < k; ++a) u += s->U[(lo + r) * k + a] * yv[a * m + q];
@@ -423,12 +482,23 @@ static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double
     }
 }
 
-int oracle_hss_matvec(int64_t n, int32_t p, const int64_t* c, int32_t k,
-                      const double* D, const double* U, const double* V,
-                      const double* R, const double* W, const double* B,
-                      const double* X, int32_t m, double* Y) {
+/* The adjoint of an HSS matrix is HSS on the same tree (eq. (3)):
+ * A^*(I_b, I_a) = (U_a^(l) S_ab V_b^(l)*)^* = V_b^(l) S_ab^* U_a^(l)*, so A^*
+ * has row bases V (translations W), column bases U (translations R), cores
+ * S'_ba = S_ab^* and leaf blocks D_i^*. hss_matvec_op runs Fig. 5 right on
+ * those generators (trans = 1): U <-> V and R <-> W exchanged here, the
+ * transposed cores in hss_couple, D_i^* in hss_leaf_out. */
+static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                         const double* D, const double* U, const double* V,
+                         const double* R, const double* W, const double* B,
+                         const double* X, int32_t m, double* Y, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, k, D, U, V, R, W, B, X, m) || Y == NULL) { hss_teardown(&s); return -1; }
+  if (hss_setup(&s, n, p, c, k, D, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+      Y == NULL) {
+    hss_teardown(&s);
+    return -1;
+  }
+  s.trans = trans;
   hss_upsweep(&s);
   if (k > 0) {
     for (int32_t l = 1; l <= p; ++l) { /* Step 2, all levels incl. the leaves (G1) */
@@ -456,16 +526,18 @@ int oracle_hss_matvec(int64_t n, int32_t p, const int64_t* c, int32_t k,
   return 0;
 }
 
-int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
-                             const double* Dsel, const double* U, const double* V,
-                             const double* R, const double* W, const double* B,
-                             const double* X, int32_t m,
-                             const int64_t* leaves, int64_t nleaves, double* Yout) {
+static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                                const double* Dsel, const double* U, const double* V,
+                                const double* R, const double* W, const double* B,
+                                const double* X, int32_t m,
+                                const int64_t* leaves, int64_t nleaves, double* Yout, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, k, NULL, U, V, R, W, B, X, m) || Yout == NULL || leaves == NULL) {
+  if (hss_setup(&s, n, p, c, k, NULL, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+      Yout == NULL || leaves == NULL) {
     hss_teardown(&s);
     return -1;
   }
+  s.trans = trans;
   hss_upsweep(&s); /* every v_i^l is needed: couplings read siblings' vectors */
   int64_t nl = (int64_t)1 << p, yoff = 0, doff = 0;
   for (int64_t t = 0; t < nleaves; ++t) {
@@ -489,6 +561,36 @@ int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
   }
   hss_teardown(&s);
   return 0;
+}
+
+int oracle_hss_matvec(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                      const double* D, const double* U, const double* V,
+                      const double* R, const double* W, const double* B,
+                      const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, k, D, U, V, R, W, B, X, m, Y, 0);
+}
+
+int oracle_hss_matvec_t(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                        const double* D, const double* U, const double* V,
+                        const double* R, const double* W, const double* B,
+                        const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, k, D, U, V, R, W, B, X, m, Y, 1);
+}
+
+int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                             const double* Dsel, const double* U, const double* V,
+                             const double* R, const double* W, const double* B,
+                             const double* X, int32_t m,
+                             const int64_t* leaves, int64_t nleaves, double* Yout) {
+  return hss_matvec_leaves_op(n, p, c, k, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 0);
+}
+
+int oracle_hss_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                               const double* Dsel, const double* U, const double* V,
+                               const double* R, const double* W, const double* B,
+                               const double* X, int32_t m,
+                               const int64_t* leaves, int64_t nleaves, double* Yout) {
+  return hss_matvec_leaves_op(n, p, c, k, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 1);
 }
 
 int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
@@ -563,6 +665,136 @@ int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
   }
   free(tmp); free(Ub); free(Vb);
   return 0;
+}
+
+/* --------------------------------------------------- hss2hodlr (f3) -- */
+/* P:522 ("hss2hodlr ... by simply building explicit low-rank factorizations",
+ * S:514-522): the level-l bases of eq. (3),
+ *   U_i^(l) = blockdiag(U_{2i}^(l+1), U_{2i+1}^(l+1)) R_{U,i}^(l), V likewise with
+ *   R_{V,i}^(l) = W, built level by level from the leaves (U^(p) = U, V^(p) = V);
+ * then every sibling block A(I_a, I_b) = U_a^(l) S_ab V_b^(l)* is
+ * the HODLR block U_l(I_a) V_l(I_b)^* with U_l(I_a) = U_a^(l) S_ab (S = B12
+ * for a = 2q, B21 for a = 2q+1 of the parent q) and V_l(I_b) = V_b^(l).
+ * Output: Uh, Vh level-major [p][n][k] (the HODLR layout with ranks k). Exact
+ * (no truncation). Sums in natural order. */
+int oracle_hss_to_hodlr(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                        const double* U, const double* V, const double* R, const double* W,
+                        const double* B, double* Uh, double* Vh) {
+  if (check_tree(n, p, c) || k < 0 || (p > 0 && (!Uh || !Vh))) return -1;
+  if (p == 0 || k == 0) return 0;
+  const size_t nk = (size_t)n * (size_t)k;
+  double* Ucur = (double*)malloc(sizeof(double) * nk); /* U^(l): rows I_i^l hold U_i^(l) */
+  double* Unext = (double*)malloc(sizeof(double) * nk);
+  if (!Ucur || !Unext) { free(Ucur); free(Unext); return -1; }
+  memcpy(Ucur, U, sizeof(double) * nk);
+  memcpy(Vh + (size_t)(p - 1) * nk, V, sizeof(double) * nk); /* V_p = V^(p) */
+  for (int32_t l = p; l >= 1; --l) {
+    double* Ul = Uh + (size_t)(l - 1) * nk;
+    double* Vl = Vh + (size_t)(l - 1) * nk;
+    /* U_l(I_a) = U_a^(l) S_{a, sib a} */
+    for (int64_t a = 0; a < ((int64_t)1 << l); ++a) {
+      int64_t lo, hi;
+      node_range(c, p, l, a, &lo, &hi);
+      const double* S = B + ((((int64_t)1 << (l - 1)) - 1 + (a >> 1)) * 2 + (a & 1)) * k * k;
+      for (int64_t r = lo; r < hi; ++r)
+        for (int32_t e = 0; e < k; ++e) {
+          double s = 0.0;
+          for (int32_t f = 0; f < k; ++f) s += Ucur[r * k + f] * S[f * k + e];
+          Ul[r * k + e] = s;
+        }
+    }
+    if (l == 1) break;
+    /* eq. (3): U^(l-1), V^(l-1) from the level-l bases and the translations of
+     * the level-(l-1) nodes: rows of child ch of node i get U^(l) R_ch, V^(l) W_ch */
+    for (int64_t i = 0; i < ((int64_t)1 << (l - 1)); ++i)
+      for (int ch = 0; ch < 2; ++ch) {
+        int64_t lo, hi;
+        node_range(c, p, l, 2 * i + ch, &lo, &hi);
+        const double* Rh = R + coef_index(l - 1, i) * 2 * k * k + ch * k * k;
+        const double* Wh = W + coef_index(l - 1, i) * 2 * k * k + ch * k * k;
+        for (int64_t r = lo; r < hi; ++r)
+          for (int32_t e = 0; e < k; ++e) {
+            double su = 0.0, sv = 0.0;
+            for (int32_t f = 0; f < k; ++f) {
+              su += Ucur[r * k + f] * Rh[f * k + e];
+              sv += Vl[r * k + f] * Wh[f * k + e];
+            }
+            Unext[r * k + e] = su;
+            Vh[(size_t)(l - 2) * nk + r * k + e] = sv;
+          }
+      }
+    double* t = Ucur; Ucur = Unext; Unext = t;
+  }
+  free(Ucur); free(Unext);
+  return 0;
+}
+
+/* ------------------------------------------------- norm estimate (f2) -- */
+/* Power method on A A^* ("estimating ||A||_2 by means of the power
+ * method on AA^*"; SPEC S:165-173 estimate_norm2): with v_0 = x0/||x0||,
+ *   w_j = A^* v_{j-1},  eta_j = ||w_j||_2,  z_j = A w_j,  v_j = z_j/||z_j||_2,
+ * j = 1..iters; returns eta_iters (0 for the zero operator). eta_j = ||A^* v||
+ * for a unit v, so eta_j <= ||A||_2 (reading R-f2 in DESIGN.md). Norms are
+ * sqrt of a sequential sum of squares in natural order. */
+static double vec_norm2(int64_t n, const double* v) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += v[i] * v[i];
+  return sqrt(s);
+}
+
+typedef int (*apply_fn)(const void* ctx, int trans, const double* x, double* y);
+
+static int power_norm2(int64_t n, const double* x0, int32_t iters, apply_fn f, const void* ctx, double* est) {
+  if (n < 1 || iters < 1 || !x0 || !est) return -1;
+  double* v = (double*)malloc(sizeof(double) * (size_t)n);
+  double* w = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!v || !w) { free(v); free(w); return -1; }
+  double nv = vec_norm2(n, x0), eta = 0.0;
+  int rc = 0;
+  if (nv > 0.0) {
+    for (int64_t i = 0; i < n; ++i) v[i] = x0[i] / nv;
+    for (int32_t j = 1; j <= iters && rc == 0; ++j) {
+      if ((rc = f(ctx, 1, v, w))) break;           /* w = A^* v */
+      eta = vec_norm2(n, w);
+      if (eta == 0.0) break;
+      if ((rc = f(ctx, 0, w, v))) break;           /* z = A w (into v) */
+      double nz = vec_norm2(n, v);
+      for (int64_t i = 0; i < n; ++i) v[i] = v[i] / nz;
+    }
+  }
+  free(v); free(w);
+  *est = eta;
+  return rc;
+}
+
+typedef struct {
+  int64_t n; int32_t p; const int64_t* c; const int32_t* ranks; int32_t k;
+  const double *D, *U, *V, *R, *W, *B;
+} op_ctx;
+
+static int hodlr_apply(const void* ctx, int trans, const double* x, double* y) {
+  const op_ctx* o = (const op_ctx*)ctx;
+  return hodlr_matvec_op(o->n, o->p, o->c, o->ranks, o->D, o->U, o->V, x, 1, y, trans);
+}
+
+static int hss_apply(const void* ctx, int trans, const double* x, double* y) {
+  const op_ctx* o = (const op_ctx*)ctx;
+  return hss_matvec_op(o->n, o->p, o->c, o->k, o->D, o->U, o->V, o->R, o->W, o->B, x, 1, y, trans);
+}
+
+int oracle_hodlr_norm2_est(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                           const double* D, const double* U, const double* V,
+                           const double* x0, int32_t iters, double* est) {
+  op_ctx o = {n, p, c, ranks, 0, D, U, V, NULL, NULL, NULL};
+  return power_norm2(n, x0, iters, hodlr_apply, &o, est);
+}
+
+int oracle_hss_norm2_est(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                         const double* D, const double* U, const double* V,
+                         const double* R, const double* W, const double* B,
+                         const double* x0, int32_t iters, double* est) {
+  op_ctx o = {n, p, c, NULL, k, D, U, V, R, W, B};
+  return power_norm2(n, x0, iters, hss_apply, &o, est);
 }
 
 int oracle_dense_matvec(int64_t n, const double* A, const double* X, int32_t m, double* Y) {

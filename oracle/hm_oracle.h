@@ -81,6 +81,47 @@ int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
                              const double* X, int32_t m,
                              const int64_t* leaves, int64_t nleaves, double* Yout);
 
+/* Adjoint products Y = A^* X (reading G4: real, so A^T X) — SURVEY §8(f) f1.
+ * A^* of a HODLR / HSS matrix has the same format on the same tree with the
+ * generators' roles exchanged (U <-> V, R <-> W, cores transposed and
+ * swapped, D_i transposed); each routine runs the same pseudocode (Fig. 5)
+ * on those generators. Arguments as for the forward products. */
+int oracle_hodlr_matvec_t(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                          const double* D, const double* U, const double* V,
+                          const double* X, int32_t m, double* Y);
+int oracle_hodlr_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                                 const double* Dsel, const double* U, const double* V,
+                                 const double* X, int32_t m,
+                                 const int64_t* leaves, int64_t nleaves, double* Yout);
+int oracle_hss_matvec_t(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                        const double* D, const double* U, const double* V,
+                        const double* R, const double* W, const double* B,
+                        const double* X, int32_t m, double* Y);
+int oracle_hss_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                               const double* Dsel, const double* U, const double* V,
+                               const double* R, const double* W, const double* B,
+                               const double* X, int32_t m,
+                               const int64_t* leaves, int64_t nleaves, double* Yout);
+
+/* ||A||_2 estimate by the power method on A A^* (SURVEY §8(f) f2):
+ * v_0 = x0/||x0||; w = A^* v, eta = ||w||, z = A w, v = z/||z||, `iters`
+ * times; *est = the last eta (<= ||A||_2; 0 for the zero operator). x0 [n]. */
+int oracle_hodlr_norm2_est(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                           const double* D, const double* U, const double* V,
+                           const double* x0, int32_t iters, double* est);
+int oracle_hss_norm2_est(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                         const double* D, const double* U, const double* V,
+                         const double* R, const double* W, const double* B,
+                         const double* x0, int32_t iters, double* est);
+
+/* hss2hodlr: exact HODLR factors of an HSS matrix.
+ * Uh, Vh: level-major [p][n][k] (HODLR layout, every rank k); the HODLR leaf
+ * blocks are the HSS D unchanged. U_l(I_a) = U_a^(l) S_{a,sib a},
+ * V_l(I_b) = V_b^(l), bases by eq. (3). */
+int oracle_hss_to_hodlr(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                        const double* U, const double* V, const double* R, const double* W,
+                        const double* B, double* Uh, double* Vh);
+
 /* Dense matrix represented by the generators (n x n, row-major), by the
  * definitions: HODLR Def. 2.2; HSS off-diagonal blocks
  * U_i^(l) S_ij^(l) V_j^(l)T with bases rebuilt by eq. (3). */

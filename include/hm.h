@@ -97,6 +97,17 @@ hm_status hodlr_matvec(const hm_tree* tree, const int32_t* ranks,
                        const double* X, int32_t nrhs, double* Y,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Adjoint product Y = A^T X ("A^*" of P:404, the
+ * Afunt handle of P:433-438; real data, so * is the transpose, reading G4).
+ * Same arguments, layouts, workspace query (flags = 0), errors and
+ * determinism as hodlr_matvec. A^T is HODLR on the same tree with the factor
+ * roles exchanged, A^T(I_a, I_b) = V_l(I_a) U_l(I_b)^T, and leaf blocks D_i^T:
+ * computed as U_l^T X contractions, then D_i^T X(I_i) + sum_l V_l(I_i) t_l. */
+hm_status hodlr_matvec_t(const hm_tree* tree, const int32_t* ranks,
+                         const double* D, const double* U, const double* V,
+                         const double* X, int32_t nrhs, double* Y,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Same, with X and Y in HOST memory (copied on `stream` through the
  * workspace; query with HM_WS_HOSTIO). */
 hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks,
@@ -130,6 +141,17 @@ hm_status hss_matvec(const hm_tree* tree, int32_t k,
                      const double* R, const double* W, const double* B,
                      const double* X, int32_t nrhs, double* Y,
                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* Adjoint product Y = A^T X. Same arguments, workspace
+ * query, errors and determinism as hss_matvec. A^T is HSS on the same tree
+ * with row bases V (translations W), column bases U (translations R), cores
+ * S'_{2q,2q+1} = B21^T, S'_{2q+1,2q} = B12^T and leaf blocks D_i^T; the four
+ * steps of Fig. 5 right run on those generators (no copy is made). */
+hm_status hss_matvec_t(const hm_tree* tree, int32_t k,
+                       const double* D, const double* U, const double* V,
+                       const double* R, const double* W, const double* B,
+                       const double* X, int32_t nrhs, double* Y,
+                       void* workspace, size_t workspace_bytes, void* stream);
 
 hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
                             const double* D, const double* U, const double* V,

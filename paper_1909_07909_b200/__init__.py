@@ -30,7 +30,8 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hss_matvec", "hss_matvec_hostio", "hm_last_error", "hm_abi_version", "hm_last_launch_count",
            "hm_profile_enable", "hm_profile_collect",
            "hm_hodlr_dist_sizes", "hodlr_matvec_dist_begin", "hodlr_matvec_dist_local", "hodlr_matvec_dist_end",
-           "hm_hss_dist_sizes", "hss_matvec_dist_begin", "hss_matvec_dist_end")
+           "hm_hss_dist_sizes", "hss_matvec_dist_begin", "hss_matvec_dist_end",
+           "hodlr_matvec_t", "hss_matvec_t")
 
 
 class HmError(RuntimeError):
@@ -66,6 +67,8 @@ def load() -> ctypes.CDLL:
         "hm_hodlr_workspace_bytes": [T, P, i32, i32, ctypes.POINTER(sz)],
         "hodlr_matvec": [T, P, P, P, P, P, i32, P, P, sz, P],
         "hodlr_matvec_hostio": [T, P, P, P, P, P, i32, P, P, sz, P],
+        "hodlr_matvec_t": [T, P, P, P, P, P, i32, P, P, sz, P],
+        "hss_matvec_t": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hm_hss_workspace_bytes": [T, i32, i32, i32, ctypes.POINTER(sz)],
         "hss_matvec": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hss_matvec_hostio": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
@@ -164,7 +167,7 @@ def _workspace(nbytes, workspace, device):
     return workspace
 
 
-def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, stream=None):
+def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, stream=None, _fn="hodlr_matvec"):
     """Y = A X on the current CUDA stream for the HODLR matrix (D, U, V) (include/hm.h).
     X: [n][nrhs] (or [n]) float64 CUDA tensor. Returns Y (allocated if None)."""
     import torch
@@ -175,9 +178,14 @@ def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, str
     _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
     ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs), workspace, X.device)
     t = make_tree(n, levels, leaf)
-    _check(load().hodlr_matvec(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(X), nrhs,
-                               _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
+    _check(getattr(load(), _fn)(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(X), nrhs,
+                                _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
     return Y
+
+
+def hodlr_matvec_t(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, stream=None):
+    """Y = A^T X (adjoint, include/hm.h hodlr_matvec_t); arguments as hodlr_matvec."""
+    return hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y, workspace, stream, _fn="hodlr_matvec_t")
 
 
 def hodlr_matvec_hostio(n, levels, leaf, ranks, D, U, V, X_host, Y_host, workspace=None, stream=None):
@@ -197,7 +205,12 @@ def hodlr_matvec_hostio(n, levels, leaf, ranks, D, U, V, X_host, Y_host, workspa
     return Y_host
 
 
-def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, stream=None):
+def hss_matvec_t(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, stream=None):
+    """Y = A^T X (adjoint, include/hm.h hss_matvec_t); arguments as hss_matvec."""
+    return hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y, workspace, stream, _fn="hss_matvec_t")
+
+
+def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, stream=None, _fn="hss_matvec"):
     """Y = A X on the current CUDA stream for the HSS matrix (D, U, V, R, W, B) (include/hm.h)."""
     import torch
     X = _dev(X, "X")
@@ -208,8 +221,8 @@ def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, 
         _dev(t_, nm)
     ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs), workspace, X.device)
     t = make_tree(n, levels, leaf)
-    _check(load().hss_matvec(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
-                             _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
+    _check(getattr(load(), _fn)(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                                _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
     return Y
 
 

@@ -291,12 +291,19 @@ hm_status launch_leaf_generic(const hm::LeafParams& lp, int64_t nleaves, cudaStr
   size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * MC);
   allow_smem(hm::leaf_apply_kernel<MC>, smem);
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + MC - 1) / MC));
-  return launch("leaf_apply", s, [&] { hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
+  return launch(lp.dtrans ? "leaf_apply_t" : "leaf_apply", s,
+                [&] { hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
 }
 
 template <int K, int NCH>
 hm_status launch_leaf_gemv_n(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
   constexpr int ROWS = NCH >= 8 ? 2 : (NCH == 0 ? 4 : HM_GEMV_ROWS);
+  if (lp.dtrans) {  // adjoint: D_i^T x_i, per-warp column partials in shared memory
+    const size_t smem = sizeof(double) * (size_t)(10 * lp.b + lp.nseg * K);
+    allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS, true>, smem);
+    return launch("leaf_apply_t", s,
+                  [&] { hm::leaf_gemv_kernel<K, NCH, ROWS, true><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+  }
   size_t smem = sizeof(double) * (size_t)(2 * lp.b + lp.nseg * K);
   allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS>, smem);
   return launch("leaf_apply", s,
@@ -328,7 +335,7 @@ hm_status launch_leaf_gemv_tma(const hm::LeafParams& lp, int64_t nleaves, cudaSt
 template <int K>
 hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
   if constexpr (K >= 8 && K <= 32) {
-    if (!HM_NO_TMA && lp.b * K <= 4096) {
+    if (!HM_NO_TMA && !lp.dtrans && lp.b * K <= 4096) {
       switch (lp.b) {
         case 64: return launch_leaf_gemv_tma<K, 1>(lp, nleaves, s);
         case 128: return launch_leaf_gemv_tma<K, 2>(lp, nleaves, s);
@@ -358,8 +365,14 @@ template <int RG, int NT>
 hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
   constexpr int PF = LeafMmaTune<RG, NT>::PF, MINB = LeafMmaTune<RG, NT>::MINB;
   size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * (NT * 8 + 4));
-  allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB>, smem);
   const int64_t chunks = (lp.m + NT * 8 - 1) / (NT * 8);
+  if (lp.dtrans) {
+    allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB, true>, smem);
+    return launch("leaf_apply_t", s, [&] {
+      hm::leaf_mma_kernel<RG, NT, PF, MINB, true><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp);
+    });
+  }
+  allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB>, smem);
   return launch("leaf_apply", s, [&] {
     hm::leaf_mma_kernel<RG, NT, PF, MINB><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp);
   });
@@ -540,10 +553,11 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
 // Phase 2: per leaf Y(I_i) = D_i X(I_i) + sum_l U_l(I_i) t_{l, sib(node_l(i))};
 // for top levels the coefficient block is the same for every leaf (ttop).
 hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const double* D, const double* U,
-                           const double* Xd, double* Yd, char* w, const double* ttop, cudaStream_t stream) {
+                           const double* Xd, double* Yd, char* w, const double* ttop, cudaStream_t stream,
+                           bool dtrans = false) {
   hm::LeafParams lp;
   memset(&lp, 0, sizeof lp);
-  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf;
+  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf; lp.dtrans = dtrans ? 1 : 0;
   int64_t uoff = 0, toff = 0;
   for (int l = 1; l <= P.q + P.p; ++l) {
     const int k = ranks[l - 1];
@@ -582,9 +596,13 @@ hm_status hodlr_check_ptrs(const HodlrPlan& P, const double* D, const double* U,
   return HM_OK;
 }
 
+// op = 0: Y = A X. op = 1: Y = A^T X: A^T is HODLR on the
+// same tree with U and V exchanged and D_i transposed (A^T(I_a, I_b) =
+// V_l(I_a) U_l(I_b)^T), so phase 1 contracts U^T X and the leaf pass applies
+// D_i^T and the V_l rows.
 hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                     const double* V, const double* X, int32_t nrhs, double* Y, void* ws, size_t ws_bytes,
-                    cudaStream_t stream, int32_t flags) {
+                    cudaStream_t stream, int32_t flags, int op = 0) {
   HodlrPlan P;
   hm_status st = hodlr_plan(tree, ranks, nrhs, flags, &P);
   if (st) return st;
@@ -602,8 +620,8 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     if (cudaMemcpyAsync(const_cast<double*>(Xd), X, xy_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
       return cuda_check("H2D copy of X");
   }
-  if ((st = hodlr_vt_phase(P, ranks, V, Xd, w, 1, P.p, nullptr, stream))) return st;
-  if ((st = hodlr_leaf_phase(P, ranks, D, U, Xd, Yd, w, nullptr, stream))) return st;
+  if ((st = hodlr_vt_phase(P, ranks, op ? U : V, Xd, w, 1, P.p, nullptr, stream))) return st;
+  if ((st = hodlr_leaf_phase(P, ranks, D, op ? V : U, Xd, Yd, w, nullptr, stream, op != 0))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");
@@ -788,11 +806,11 @@ hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up,
 // generic per-level kernels or the DMMA tree kernels (tree_dispatch).
 hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
                          double* yh, const double* R_root, const double* y_root, bool up, bool down,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, int bt = 0) {
   const int k = P.k, nrhs = P.m;
   hm_status st;
   if (P.mma_levels) {
-    hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, 0};
+    hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
     return tree_dispatch(tp, p, k, P.nt_down, up, down, stream);
   }
   const int64_t km = (int64_t)k * nrhs;
@@ -806,7 +824,7 @@ hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double*
     }
   if (down)
     for (int l = 1; l <= p; ++l) {
-      hm::HssLevelParams hp{R, B, xh, yh, R_root, y_root, l, k, nrhs, 0};
+      hm::HssLevelParams hp{R, B, xh, yh, R_root, y_root, l, k, nrhs, bt};
       const int64_t total = ((int64_t)1 << l) * km;
       const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
       st = launch("hss_down_level", stream,
@@ -866,10 +884,10 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
 // Step 4: Y(I_i) = U_i y_i + D_i X(I_i); y of the leaves from yh (or y_root for a
 // depth-0 subtree).
 hm_status hss_leaf_phase(const HssPlan& P, const double* D, const double* U, const double* Xd, double* Yd,
-                         const double* yleaf, cudaStream_t stream) {
+                         const double* yleaf, cudaStream_t stream, bool dtrans = false) {
   hm::LeafParams lp;
   memset(&lp, 0, sizeof lp);
-  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf;
+  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf; lp.dtrans = dtrans ? 1 : 0;
   const bool coupled = P.k > 0 && yleaf != nullptr;
   if (coupled) {
     hm::LeafSeg& sg = lp.seg[lp.nseg++];
@@ -895,9 +913,17 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
   return HM_OK;
 }
 
+// op = 1: Y = A^T X. A^T is HSS on the same tree with row
+// bases V (translations W), column bases U (translations R), cores
+// S'_{2q,2q+1} = B21^T, S'_{2q+1,2q} = B12^T and leaf blocks D_i^T: the same
+// four steps with U <-> V, R <-> W exchanged, transposed cores (bt) and D^T.
 hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                   const double* R, const double* W, const double* B, const double* X, int32_t nrhs, double* Y,
-                  void* ws, size_t ws_bytes, cudaStream_t stream, int32_t flags) {
+                  void* ws, size_t ws_bytes, cudaStream_t stream, int32_t flags, int op = 0) {
+  if (op) {
+    std::swap(U, V);
+    std::swap(R, W);
+  }
   HssPlan P;
   hm_status st = hss_plan(tree, k, nrhs, flags, &P);
   if (st) return st;
@@ -926,10 +952,10 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   const bool coupled = (k > 0 && P.p > 0);
   if (coupled) {
     if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
-    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream))) return st;
+    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op))) return st;
   }
   const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
-  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream))) return st;
+  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");
@@ -975,6 +1001,13 @@ hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks, const d
                    static_cast<cudaStream_t>(stream), HM_WS_HOSTIO);
 }
 
+hm_status hodlr_matvec_t(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
+                         const double* V, const double* X, int32_t nrhs, double* Y, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  return hodlr_run(tree, ranks, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
+                   static_cast<cudaStream_t>(stream), 0, 1);
+}
+
 hm_status hm_hss_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, size_t* bytes) {
   if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
   HssPlan P;
@@ -989,6 +1022,13 @@ hm_status hss_matvec(const hm_tree* tree, int32_t k, const double* D, const doub
                      double* Y, void* workspace, size_t workspace_bytes, void* stream) {
   return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                  static_cast<cudaStream_t>(stream), 0);
+}
+
+hm_status hss_matvec_t(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                       const double* R, const double* W, const double* B, const double* X, int32_t nrhs,
+                       double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
+                 static_cast<cudaStream_t>(stream), 0, 1);
 }
 
 hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,

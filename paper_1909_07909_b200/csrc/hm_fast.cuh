@@ -189,7 +189,12 @@ __global__ void __launch_bounds__(256) vt_gemv_kernel(const VtGemvParams P) {
 #ifndef HM_GEMV_ROWS
 #define HM_GEMV_ROWS 4
 #endif
-template <int K, int NCH, int ROWS>
+//
+// DT = true (adjoint): the leaf term is D_i^T x_i. The same
+// row-major 128-bit stream of D; warp w owns rows w, w+8, ..; lane l keeps the
+// partial sums of columns 64c + 2l, 64c + 2l + 1 in registers (x[r] broadcast
+// from shared memory); the 8 warps' partials are summed in a fixed order.
+template <int K, int NCH, int ROWS, bool DT = false>
 __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   const int64_t leaf = blockIdx.x;
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   double* xs = sm;            // [b]
   double* yd = sm + b;        // [b]
   double* ts = sm + 2 * b;    // [nseg][K]
+  double* red = ts + P.nseg * K;  // DT: [8][b] per-warp column partials
   for (int64_t e = threadIdx.x; e < b; e += 256) xs[e] = __ldg(P.X + r0 + e);
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
@@ -208,7 +214,55 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Di = P.D + leaf * b * b;
   const int nch = NCH > 0 ? NCH : (int)(b / 64);
-  for (int64_t rb = warp; rb < b; rb += 8 * ROWS) {
+  if constexpr (DT) {
+    if constexpr (NCH > 0) {
+      double2 acc[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) acc[c] = make_double2(0.0, 0.0);
+      for (int64_t rb = warp; rb < b; rb += 8 * ROWS) {
+        double2 v[ROWS][NCH];
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) v[u][c] = ldg_stream2(Di + (rb + 8 * u) * b + 64 * c + 2 * lane);
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) reg_fence(v[u][c]);
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u) {
+          const double x = xs[rb + 8 * u];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            acc[c].x = fma(v[u][c].x, x, acc[c].x);
+            acc[c].y = fma(v[u][c].y, x, acc[c].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        *reinterpret_cast<double2*>(red + (int64_t)warp * b + 64 * c + 2 * lane) = acc[c];
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int64_t r = warp; r < b; r += 8) {
+          const double2 v = ldg_stream2(Di + r * b + 64 * c + 2 * lane);
+          const double x = xs[r];
+          acc.x = fma(v.x, x, acc.x);
+          acc.y = fma(v.y, x, acc.y);
+        }
+        *reinterpret_cast<double2*>(red + (int64_t)warp * b + 64 * c + 2 * lane) = acc;
+      }
+    }
+    __syncthreads();
+    for (int64_t col = threadIdx.x; col < b; col += 256) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[(int64_t)w * b + col];
+      yd[col] = s;
+    }
+  }
+  for (int64_t rb = warp; !DT && rb < b; rb += 8 * ROWS) {
     double acc[ROWS];
 #pragma unroll
     for (int u = 0; u < ROWS; ++u) acc[u] = 0.0;
@@ -526,40 +580,97 @@ __device__ __forceinline__ void rm_group(double (&acc)[RG][NT][2], const double2
   }
 }
 
-template <int RG, int PF>
+// Row of the warp's tile rg held by lane group i (= lane >> 2): 8 rg + i, or,
+// with PAIR (the row order of warp_dt_mma, adjoint leaf pass), tiles 2pr and
+// 2pr+1 interleaved over 16 rows: 16 pr + 2 i + (rg & 1).
+template <bool PAIR>
+__device__ __forceinline__ int tile_row(int rg, int i) {
+  return PAIR ? 16 * (rg >> 1) + 2 * i + (rg & 1) : 8 * rg + i;
+}
+
+template <int RG, int PF, bool PAIR = false>
 __device__ __forceinline__ void rm_load(double2 (&a)[PF][RG], const double* base, int64_t lda, int q, int nq) {
 #pragma unroll
   for (int u = 0; u < PF; ++u)
 #pragma unroll
     for (int rg = 0; rg < RG; ++rg)
-      a[u][rg] = (q + u < nq) ? ldg_stream2(base + (int64_t)rg * 8 * lda + 8 * (q + u)) : make_double2(0.0, 0.0);
+      a[u][rg] = (q + u < nq) ? ldg_stream2(base + (int64_t)tile_row<PAIR>(rg, 0) * lda + 8 * (q + u))
+                              : make_double2(0.0, 0.0);
 }
 
-template <int RG, int NT, bool ZG, bool COH = false, int PF = HM_RM_PF>
+template <int RG, int NT, bool ZG, bool COH = false, int PF = HM_RM_PF, bool PAIR = false>
 __device__ __forceinline__ void warp_rowmajor_mma(double (&acc)[RG][NT][2], const double* __restrict__ E, int64_t lda,
                                                   int K, const double* Z, int64_t zs, int zvalid, int lane) {
   const int j = lane & 3, i = lane >> 2;
-  const double* base = E + (int64_t)i * lda + 2 * j;
+  const double* base = E + (int64_t)(PAIR ? 2 * i : i) * lda + 2 * j;
   bool colok[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) colok[nt] = !ZG || (nt * 8 + i) < zvalid;
   const int nq = K / 8;
   double2 a0[PF][RG], a1[PF][RG];
-  rm_load<RG, PF>(a0, base, lda, 0, nq);
+  rm_load<RG, PF, PAIR>(a0, base, lda, 0, nq);
   for (int q = 0; q < nq; q += 2 * PF) {
-    rm_load<RG, PF>(a1, base, lda, q + PF, nq);
+    rm_load<RG, PF, PAIR>(a1, base, lda, q + PF, nq);
     rm_group<RG, NT, ZG, COH, PF>(acc, a0, Z, zs, q, nq, colok, lane);
     if (q + PF >= nq) break;
-    rm_load<RG, PF>(a0, base, lda, q + 2 * PF, nq);
+    rm_load<RG, PF, PAIR>(a0, base, lda, q + 2 * PF, nq);
     rm_group<RG, NT, ZG, COH, PF>(acc, a1, Z, zs, q + PF, nq, colok, lane);
+  }
+}
+
+// Adjoint leaf term: one warp accumulates C += D^T(rows, :) Z
+// for its 8 RG output rows, D [K][ldd] row-major in global memory (Dc points at
+// the warp's first column). A fragment of tile rg: D[k][tile_row(rg, i)] with
+// k = 4q + (lane & 3). For even RG one LDG.128 of two adjacent columns feeds
+// the two interleaved tiles of a pair (PAIR row order); for RG = 1 a 64-bit
+// load per fragment. B fragments: rows 4q + (lane & 3) of Z (shared memory).
+template <int RG, int NT>
+__device__ __forceinline__ void warp_dt_mma(double (&acc)[RG][NT][2], const double* __restrict__ Dc, int64_t ldd, int K,
+                                            const double* Z, int64_t zs, int lane) {
+  constexpr bool PAIR = (RG % 2 == 0);
+  constexpr int PF = 4;  // k-steps (4 rows of D each) per batch of loads
+  const int j = lane & 3, i = lane >> 2;
+  const double* ap = Dc + (int64_t)j * ldd + (PAIR ? 2 * i : i);
+  const double* zp = Z + (int64_t)j * zs + i;
+#pragma unroll 1
+  for (int q = 0; q < K / 4; q += PF) {  // K % 16 == 0 (leaf sizes 64, 128, 256)
+    double a[PF][RG];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const double* ar = ap + (int64_t)(q + u) * 4 * ldd;
+      if constexpr (PAIR) {
+#pragma unroll
+        for (int pr = 0; pr < RG / 2; ++pr) {
+          const double2 v = ldg_stream2(ar + 16 * pr);
+          a[u][2 * pr] = v.x;
+          a[u][2 * pr + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int rg = 0; rg < RG; ++rg) a[u][rg] = ldg_stream(ar + 8 * rg);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      double bf[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = zp[(int64_t)(q + u) * 4 * zs + nt * 8];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int rg = 0; rg < RG; ++rg) dmma(acc[rg][nt][0], acc[rg][nt][1], a[u][rg], bf[nt]);
+    }
   }
 }
 
 // leaf_mma: grid (chunks of NT*8 columns, leaves); 8 warps; warp w owns rows
 // [w*8*RG, (w+1)*8*RG) of the leaf (b = 64 RG). Z = [X_i; T_1; ..; T_S] staged
 // in shared memory with row stride NT*8+4 (conflict-free B fragments).
-template <int RG, int NT, int PF, int MINB>
+// DT (adjoint): the leaf term is D_i^T X_i (warp_dt_mma); for even RG the
+// warp's rows are in PAIR order, which the U segments and the store follow.
+template <int RG, int NT, int PF, int MINB, bool DT = false>
 __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P) {
+  constexpr bool PAIR = DT && (RG % 2 == 0);
   extern __shared__ double sm[];
   constexpr int MC = NT * 8;
   constexpr int ZS = MC + 4;
@@ -588,18 +699,19 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
   const int64_t wrow = (int64_t)warp * 8 * RG;
-  warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
+  if constexpr (DT) warp_dt_mma<RG, NT>(acc, P.D + leaf * b * b + wrow, b, (int)b, Z, ZS, lane);
+  else warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
   zoff = b;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
-    warp_rowmajor_mma<RG, NT, false, false, PF>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS, MC,
-                                                        lane);
+    warp_rowmajor_mma<RG, NT, false, false, PF, PAIR>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS,
+                                                      MC, lane);
     zoff += sg.k;
   }
   const int i = lane >> 2, j = lane & 3;
 #pragma unroll
   for (int rg = 0; rg < RG; ++rg) {
-    double* y = P.Y + (r0 + wrow + 8 * rg + i) * m;
+    double* y = P.Y + (r0 + wrow + tile_row<PAIR>(rg, i)) * m;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int c = c0 + nt * 8 + 2 * j;

@@ -227,6 +227,8 @@ struct LeafParams {
   int32_t mc;       // columns per CTA
   int32_t nseg;
   int32_t ktot;     // sum of segment ranks
+  int32_t dtrans;   // 1: the leaf term is D_i^T X(I_i) (adjoint product)
+  int32_t pad;
   LeafSeg seg[kMaxLevels];
 };
 
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) leaf_apply_kernel(const LeafParams P
     for (int c = 0; c < MC; ++c) acc[c] = 0.0;
     const double* Dr = Di + r * b;
     for (int64_t j = lane; j < b; j += 32) {
-      const double d = Dr[j];
+      const double d = P.dtrans ? Di[j * b + r] : Dr[j];  // D_i^T: column r of D_i
 #pragma unroll
       for (int c = 0; c < MC; ++c) acc[c] = fma(d, Z[j * MC + c], acc[c]);
     }
@@ -319,7 +321,7 @@ struct HssLevelParams {
   int32_t level;
   int32_t k;
   int32_t m;
-  int32_t pad;
+  int32_t bt;        // 1: cores of the adjoint, S'_0 = B21^T, S'_1 = B12^T
 };
 
 __global__ void __launch_bounds__(kThreads) hss_up_level_kernel(const HssLevelParams P) {
@@ -356,10 +358,15 @@ __global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const HssLevel
     const int a = o / m, c = o - a * m;
     const int64_t q = j >> 1;
     const int w = (int)(j & 1);
-    const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * k * k;
     const double* xs = P.xh + ((1ll << l) - 2 + (j ^ 1)) * km;
     double yc = 0.0;
-    for (int r = 0; r < k; ++r) yc = fma(S[a * k + r], xs[r * m + c], yc);
+    if (P.bt) {  // S'_w = (S_{1-w})^T
+      const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + (1 - w)) * k * k;
+      for (int r = 0; r < k; ++r) yc = fma(S[r * k + a], xs[r * m + c], yc);
+    } else {
+      const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + w) * k * k;
+      for (int r = 0; r < k; ++r) yc = fma(S[a * k + r], xs[r * m + c], yc);
+    }
     double yd = 0.0;
     if (l >= 2) {
       const double* Rn = P.W + (((1ll << (l - 1)) - 2 + q) * 2 * k + w * k) * k;

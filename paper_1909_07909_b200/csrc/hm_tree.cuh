@@ -26,7 +26,7 @@ struct TreeParams {
   const double* R_root;  // optional (distributed subtree): translation of the subtree root,
   const double* y_root;  //   [2k][k], and its y block [k][m]: adds R_root[w] y_root at level 1
   int32_t m;
-  int32_t pad;
+  int32_t bt;            // 1: adjoint cores S'_0 = B21^T, S'_1 = B12^T
 };
 
 // Staged blocks hold mpad = ceil(m / 8NT) * 8NT columns (zero padded) so every
@@ -136,7 +136,8 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = w >> 2, sub = w & 3;
   const int64_t j = 2 * q + nd;
-  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + nd) * KT * KT;
+  // A: S = B12 (nd 0) / B21 (nd 1); adjoint (bt): S' = (the other core)^T
+  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + (P.bt ? 1 - nd : nd)) * KT * KT;
   const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT
                      : (root_term ? P.R_root + (int64_t)nd * KT * KT : nullptr);
   const double* Zx = sm + (1 - nd) * KT * zs;  // the sibling's x
@@ -154,11 +155,13 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
     constexpr int NQ = KT / 8;
     double2 aR[NQ][1], aS[NQ][1];
     const double* bR = Rw ? Rw + (int64_t)(rg * 8 + i) * KT + 2 * jj : nullptr;
-    const double* bS = S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
+    const double* bS = P.bt ? S + (int64_t)(2 * jj) * KT + rg * 8 + i : S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
 #pragma unroll
     for (int q2 = 0; q2 < NQ; ++q2) {
       aR[q2][0] = bR ? ldg_stream2(bR + 8 * q2) : make_double2(0.0, 0.0);
-      aS[q2][0] = ldg_stream2(bS + 8 * q2);
+      // S'[row][k] = S[k][row]: the two k-indices 8 q2 + 2 jj (+1) are rows of S
+      aS[q2][0] = P.bt ? make_double2(ldg_stream(bS + (int64_t)8 * q2 * KT), ldg_stream(bS + (int64_t)(8 * q2 + 1) * KT))
+                       : ldg_stream2(bS + 8 * q2);
     }
     bool colok[NT];
 #pragma unroll

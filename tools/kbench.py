@@ -2,6 +2,8 @@
 
     python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 [--reps N]
 
+A trailing "t" (c5t, c4t, c3m8t, ...) times the adjoint product A^T X instead.
+
 Inputs drawn on the device; prints per-kernel device ms (launch trace of
 libhm) and the config's algorithmic GB/s.
 """
@@ -20,6 +22,9 @@ from bench import hodlr_bytes, hss_bytes, hss_flops, hodlr_flops  # noqa: E402
 
 def run(name, reps):
     dev = torch.device("cuda:0")
+    adj = name.endswith("t")
+    if adj:
+        name = name[:-1]
     if name.startswith("c3") or name in ("c5", "c1"):
         cfg = hm_inputs.CONFIGS[{"c1": 1, "c5": 5}.get(name, 3)]
         m = int(name[3:]) if name.startswith("c3m") else 1
@@ -31,7 +36,8 @@ def run(name, reps):
         Y = torch.empty_like(X)
         ws = torch.empty(hm.hm_hodlr_workspace_bytes(cfg.n, cfg.levels, cfg.leaf, h.ranks, m), dtype=torch.uint8,
                          device=dev)
-        f = lambda: hm.hodlr_matvec(cfg.n, cfg.levels, cfg.leaf, h.ranks, h.D, h.U, h.V, X, Y, ws)
+        mv = hm.hodlr_matvec_t if adj else hm.hodlr_matvec
+        f = lambda: mv(cfg.n, cfg.levels, cfg.leaf, h.ranks, h.D, h.U, h.V, X, Y, ws)
         nbytes = hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
         flops = hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
     else:
@@ -42,7 +48,8 @@ def run(name, reps):
         Y = torch.empty_like(X)
         ws = torch.empty(hm.hm_hss_workspace_bytes(cfg.n, cfg.levels, cfg.leaf, cfg.k, m), dtype=torch.uint8,
                          device=dev)
-        f = lambda: hm.hss_matvec(cfg.n, cfg.levels, cfg.leaf, cfg.k, s.D, s.U, s.V, s.R, s.W, s.B, X, Y, ws)
+        mv = hm.hss_matvec_t if adj else hm.hss_matvec
+        f = lambda: mv(cfg.n, cfg.levels, cfg.leaf, cfg.k, s.D, s.U, s.V, s.R, s.W, s.B, X, Y, ws)
         nbytes = hss_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
         flops = hss_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
     for _ in range(3):
@@ -65,7 +72,7 @@ def run(name, reps):
     per = {}
     for nm, call, ms in tr:
         per.setdefault(nm, []).append(ms)
-    print(f"== {name}: {plain * 1e3:.1f} us/call  {nbytes / plain / 1e6:.0f} GB/s  "
+    print(f"== {name}{'^T' if adj else ''}: {plain * 1e3:.1f} us/call  {nbytes / plain / 1e6:.0f} GB/s  "
           f"{flops / plain / 1e9:.2f} TFLOP/s")
     for nm, v in per.items():
         cnt = len(v) // reps

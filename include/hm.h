@@ -159,6 +159,52 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
                             const double* X_host, int32_t nrhs, double* Y_host,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------- norm estimate (§8(f) f2) --
+ * ||A||_2 estimate by the power method on A A^* ("estimating ||A||_2
+ * by means of the power method on AA^*", run before every recompression;
+ * SPEC S:165-173 estimate_norm2):
+ *   v = x0/||x0||;  iters times:  w = A^T v,  eta = ||w||_2,  z = A w,  v = z/||z||_2
+ * and *est = the last eta. For a unit v, eta = ||A^T v|| <= ||A||_2, and eta
+ * is nondecreasing in the iteration count. A zero x0 or zero operator gives 0.
+ *   x0   [n] device vector (start vector; not modified)
+ *   iters >= 1 (HM_ERR_INVALID_ARG otherwise)
+ *   est  ONE double in device memory, written on `stream` (async)
+ * Workspace: the *_norm2_workspace_bytes query (the nrhs = 1 matvec
+ * workspace plus two n-vectors and the norm partials). Every product runs
+ * through hodlr_matvec / hodlr_matvec_t (hss_*); norms are fixed-order
+ * reductions, so the result is bitwise repeatable. Capturable in a CUDA graph
+ * (no synchronisation, no allocation). */
+hm_status hm_hodlr_norm2_workspace_bytes(const hm_tree* tree, const int32_t* ranks, size_t* bytes);
+hm_status hodlr_norm2_est(const hm_tree* tree, const int32_t* ranks,
+                          const double* D, const double* U, const double* V,
+                          const double* x0, int32_t iters, double* est,
+                          void* workspace, size_t workspace_bytes, void* stream);
+hm_status hm_hss_norm2_workspace_bytes(const hm_tree* tree, int32_t k, size_t* bytes);
+hm_status hss_norm2_est(const hm_tree* tree, int32_t k,
+                        const double* D, const double* U, const double* V,
+                        const double* R, const double* W, const double* B,
+                        const double* x0, int32_t iters, double* est,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------- hss2hodlr (§8(f) f3) --
+ * Exact conversion HSS -> HODLR ("by simply building explicit low-rank
+ * factorizations"): the level-l bases of eq. (3)
+ * are built from the leaves, U^(l-1) = blockdiag(U^(l) children) R,
+ * V^(l-1) likewise with W, and every sibling block U_a^(l) S_ab V_b^(l)T
+ * becomes the HODLR block U_l(I_a) V_l(I_b)^T with
+ *   U_l(I_a) = U_a^(l) S_{a, sib a} (B12 for a = 2q, B21 for a = 2q+1),
+ *   V_l(I_b) = V_b^(l).
+ * Inputs: the HSS generators U, V [n][k], R, W, B as for hss_matvec.
+ * Outputs: Uh, Vh [levels][n][k] device, the HODLR U, V of hodlr_matvec with
+ * ranks[l-1] = k on every level; the HODLR leaf blocks are the HSS D
+ * unchanged (reuse the same buffer). Uh, Vh must not overlap each other or
+ * an input (HM_ERR_INVALID_ARG). levels = 0 or k = 0 writes nothing. No
+ * workspace; O(k^2 n log n) flops, O(k n log n) bytes written; async on
+ * `stream`; bitwise repeatable. */
+hm_status hss_to_hodlr(const hm_tree* tree, int32_t k,
+                       const double* U, const double* V, const double* R, const double* W, const double* B,
+                       double* Uh, double* Vh, void* stream);
+
 /* ---------------------------------------------------- multi-GPU (§8(e)) --
  * One process per GPU, P = 2^q ranks (1 <= P <= 2^levels). Rank r owns the
  * rows I_r = [r n/P, (r+1) n/P) — the level-q node (q, r) and its whole

@@ -31,7 +31,9 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hm_profile_enable", "hm_profile_collect",
            "hm_hodlr_dist_sizes", "hodlr_matvec_dist_begin", "hodlr_matvec_dist_local", "hodlr_matvec_dist_end",
            "hm_hss_dist_sizes", "hss_matvec_dist_begin", "hss_matvec_dist_end",
-           "hodlr_matvec_t", "hss_matvec_t")
+           "hodlr_matvec_t", "hss_matvec_t",
+           "hm_hodlr_norm2_workspace_bytes", "hodlr_norm2_est", "hm_hss_norm2_workspace_bytes", "hss_norm2_est",
+           "hss_to_hodlr")
 
 
 class HmError(RuntimeError):
@@ -72,6 +74,11 @@ def load() -> ctypes.CDLL:
         "hm_hss_workspace_bytes": [T, i32, i32, i32, ctypes.POINTER(sz)],
         "hss_matvec": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hss_matvec_hostio": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_hodlr_norm2_workspace_bytes": [T, P, ctypes.POINTER(sz)],
+        "hodlr_norm2_est": [T, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_hss_norm2_workspace_bytes": [T, i32, ctypes.POINTER(sz)],
+        "hss_norm2_est": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hss_to_hodlr": [T, i32, P, P, P, P, P, P, P, P],
         "hm_profile_enable": [i32],
         "hm_profile_collect": [ctypes.POINTER(hm_launch_record), i32, ctypes.POINTER(i32)],
     }
@@ -240,3 +247,73 @@ def hss_matvec_hostio(n, levels, leaf, k, D, U, V, R, W, B, X_host, Y_host, work
                                     X_host.data_ptr(), nrhs, Y_host.data_ptr(), ws.data_ptr(), ws.numel(),
                                     _stream(stream)))
     return Y_host
+
+
+# ------------------------------------------------- ||A||_2 estimate (f2) --
+
+def hm_hodlr_norm2_workspace_bytes(n, levels, leaf, ranks) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hodlr_norm2_workspace_bytes(ctypes.byref(t), _ranks(ranks, levels), ctypes.byref(out)))
+    return out.value
+
+
+def hm_hss_norm2_workspace_bytes(n, levels, leaf, k) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hss_norm2_workspace_bytes(ctypes.byref(t), int(k), ctypes.byref(out)))
+    return out.value
+
+
+def _est(est, device):
+    import torch
+    if est is None:
+        est = torch.zeros(1, dtype=torch.float64, device=device)
+    return _dev(est, "est")
+
+
+def hodlr_norm2_est(n, levels, leaf, ranks, D, U, V, x0, iters, est=None, workspace=None, stream=None):
+    """||A||_2 estimate (power method on A A^*, include/hm.h hodlr_norm2_est): returns a 1-element
+    float64 CUDA tensor written asynchronously on the stream."""
+    x0 = _dev(x0, "x0")
+    _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    est = _est(est, x0.device)
+    ws = _workspace(hm_hodlr_norm2_workspace_bytes(n, levels, leaf, ranks), workspace, x0.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hodlr_norm2_est(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(x0),
+                                  int(iters), _ptr(est), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return est
+
+
+def hss_norm2_est(n, levels, leaf, k, D, U, V, R, W, B, x0, iters, est=None, workspace=None, stream=None):
+    """||A||_2 estimate of an HSS matrix (include/hm.h hss_norm2_est)."""
+    x0 = _dev(x0, "x0")
+    for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    est = _est(est, x0.device)
+    ws = _workspace(hm_hss_norm2_workspace_bytes(n, levels, leaf, k), workspace, x0.device)
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_norm2_est(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
+                                _ptr(x0), int(iters), _ptr(est), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return est
+
+
+# ---------------------------------------------------------- hss2hodlr (f3) --
+
+def hss_to_hodlr(n, levels, leaf, k, U, V, R, W, B, Uh=None, Vh=None, stream=None):
+    """Exact HODLR factors (Uh, Vh), level-major [levels][n][k], of an HSS matrix (include/hm.h
+    hss_to_hodlr). The HODLR leaf blocks are the HSS D; ranks are [k] * levels."""
+    import torch
+    U = _dev(U, "U")
+    for t_, nm in ((V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    size = max(levels, 0) * n * k
+    if Uh is None:
+        Uh = torch.empty(size, dtype=torch.float64, device=U.device)
+    if Vh is None:
+        Vh = torch.empty(size, dtype=torch.float64, device=U.device)
+    _dev(Uh, "Uh"); _dev(Vh, "Vh")
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_to_hodlr(ctypes.byref(t), int(k), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(Uh),
+                               _ptr(Vh), _stream(stream)))
+    return Uh, Vh

@@ -18,6 +18,8 @@
 #include "hm_kernels.cuh"
 #include "hm_fast.cuh"
 #include "hm_tree.cuh"
+#include "hm_vec.cuh"
+#include "hm_convert.cuh"
 
 namespace {
 
@@ -973,9 +975,116 @@ hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_p
   return hss_plan_ex(tree->n >> d->q, tree->leaf, tree->levels - d->q, d->q, k, nrhs, flags, P);
 }
 
+// ------------------------------------------------ norm estimate (f2) --
+//
+// Power method on A A^* (SURVEY §8(f) f2), nrhs = 1:
+//   v = x0/||x0||; iters times: w = A^T v, eta = ||w|| (-> est), z = A w, v = z/||z||.
+// Workspace: [matvec workspace][v: n][w: n][norm partials]; every product is
+// libhm's own matvec / adjoint on the same workspace.
+struct NormPlan {
+  size_t off_v, off_w, off_part, total;
+};
+
+NormPlan norm_plan(size_t mv_bytes, int64_t n) {
+  NormPlan N;
+  size_t off = align_up(mv_bytes);
+  N.off_v = off; off = align_up(off + sizeof(double) * (size_t)n);
+  N.off_w = off; off = align_up(off + sizeof(double) * (size_t)n);
+  N.off_part = off; off = align_up(off + sizeof(double) * hm::kVecMaxBlocks);
+  N.total = off;
+  return N;
+}
+
+template <typename Apply>
+hm_status power_norm2(int64_t n, const double* x0, int32_t iters, double* est, char* w, const NormPlan& N,
+                      cudaStream_t s, Apply&& apply) {
+  if (iters < 1) return fail(HM_ERR_INVALID_ARG, "iters = %d < 1", iters);
+  if (!x0 || !est) return fail(HM_ERR_INVALID_ARG, "NULL x0 / est pointer");
+  double* v = reinterpret_cast<double*>(w + N.off_v);
+  double* wv = reinterpret_cast<double*>(w + N.off_w);
+  double* part = reinterpret_cast<double*>(w + N.off_part);
+  const int G = hm::vec_blocks(n);
+  const unsigned gs = (unsigned)std::min<int64_t>((n + hm::kVecThreads - 1) / hm::kVecThreads, 148 * 8);
+  int32_t launches = 0;
+  hm_status st;
+  auto sumsq = [&](const double* x) {
+    ++launches;
+    return launch("vec_sumsq", s, [&] { hm::vec_sumsq_kernel<<<G, hm::kVecThreads, 0, s>>>(x, n, part); });
+  };
+  auto normalize = [&](const double* x, double* out) {
+    ++launches;
+    return launch("vec_normalize", s,
+                  [&] { hm::vec_normalize_kernel<<<gs, hm::kVecThreads, 0, s>>>(x, n, part, G, out); });
+  };
+  if ((st = sumsq(x0)) || (st = normalize(x0, v))) return st;
+  for (int32_t j = 1; j <= iters; ++j) {
+    if ((st = apply(1, v, wv))) return st;  // w = A^T v
+    launches += g_launches;
+    if ((st = sumsq(wv))) return st;
+    ++launches;
+    if ((st = launch("vec_norm_write", s, [&] { hm::vec_norm_write_kernel<<<1, 32, 0, s>>>(part, G, est); })))
+      return st;                             // eta = ||w||
+    if ((st = apply(0, wv, v))) return st;  // z = A w (into v)
+    launches += g_launches;
+    if ((st = sumsq(v)) || (st = normalize(v, v))) return st;
+  }
+  g_launches = launches;
+  return HM_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+hm_status hm_hodlr_norm2_workspace_bytes(const hm_tree* tree, const int32_t* ranks, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  HodlrPlan P;
+  hm_status st = hodlr_plan(tree, ranks, 1, 0, &P);
+  if (st) return st;
+  *bytes = norm_plan(P.total, P.n).total;
+  return HM_OK;
+}
+
+hm_status hodlr_norm2_est(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
+                          const double* V, const double* x0, int32_t iters, double* est, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  HodlrPlan P;
+  hm_status st = hodlr_plan(tree, ranks, 1, 0, &P);
+  if (st) return st;
+  const NormPlan N = norm_plan(P.total, P.n);
+  if (!workspace || workspace_bytes < N.total)
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, N.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return power_norm2(P.n, x0, iters, est, static_cast<char*>(workspace), N, s,
+                     [&](int op, const double* x, double* y) {
+                       return hodlr_run(tree, ranks, D, U, V, x, 1, y, workspace, P.total, s, 0, op);
+                     });
+}
+
+hm_status hm_hss_norm2_workspace_bytes(const hm_tree* tree, int32_t k, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, 1, 0, &P);
+  if (st) return st;
+  *bytes = norm_plan(P.total, P.n).total;
+  return HM_OK;
+}
+
+hm_status hss_norm2_est(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                        const double* R, const double* W, const double* B, const double* x0, int32_t iters,
+                        double* est, void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, 1, 0, &P);
+  if (st) return st;
+  const NormPlan N = norm_plan(P.total, P.n);
+  if (!workspace || workspace_bytes < N.total)
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, N.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return power_norm2(P.n, x0, iters, est, static_cast<char*>(workspace), N, s,
+                     [&](int op, const double* x, double* y) {
+                       return hss_run(tree, k, D, U, V, R, W, B, x, 1, y, workspace, P.total, s, 0, op);
+                     });
+}
 
 hm_status hm_hodlr_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags,
                                    size_t* bytes) {
@@ -1187,6 +1296,44 @@ hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* par
     }
   }
   return hss_leaf_phase(P, D_local, U_local, X_local, Y_local, yleaf, s);
+}
+
+// ------------------------------------------------------ hss2hodlr (f3) --
+
+hm_status hss_to_hodlr(const hm_tree* tree, int32_t k, const double* U, const double* V, const double* R,
+                       const double* W, const double* B, double* Uh, double* Vh, void* stream) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  if (k < 0) return fail(HM_ERR_INVALID_ARG, "k = %d < 0", k);
+  if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
+  const int p = tree->levels;
+  const int64_t n = tree->n;
+  g_launches = 0;
+  prof_new_call();
+  if (p == 0 || k == 0) return HM_OK;  // no off-diagonal level / all blocks zero: nothing to write
+  if (!U || !V || !B || !Uh || !Vh || (p >= 2 && (!R || !W)))
+    return fail(HM_ERR_INVALID_ARG, "NULL generator / output pointer");
+  const size_t nk = sizeof(double) * (size_t)n * (size_t)k;
+  const size_t out = nk * (size_t)p;
+  const size_t tr = sizeof(double) * (size_t)((((int64_t)1 << p) - 2) * 2 * k * k);
+  const size_t bb = sizeof(double) * (size_t)((((int64_t)1 << p) - 1) * 2 * k * k);
+  if (overlap(Uh, out, Vh, out) || overlap(Uh, out, U, nk) || overlap(Uh, out, V, nk) || overlap(Vh, out, U, nk) ||
+      overlap(Vh, out, V, nk) || overlap(Uh, out, B, bb) || overlap(Vh, out, B, bb) ||
+      (p >= 2 && (overlap(Uh, out, R, tr) || overlap(Uh, out, W, tr) || overlap(Vh, out, R, tr) ||
+                  overlap(Vh, out, W, tr))))
+    return fail(HM_ERR_INVALID_ARG, "outputs Uh / Vh overlap each other or an input");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(Uh + (size_t)(p - 1) * n * k, U, nk, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(Vh + (size_t)(p - 1) * n * k, V, nk, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return cuda_check("copy of the leaf bases");
+  hm::ConvertParams cp{R, W, B, Uh, Vh, n, tree->leaf, p, k};
+  const size_t smem = sizeof(double) * 2 * hm::kConvRows * (size_t)k;
+  const unsigned grid = (unsigned)((n + hm::kConvRows - 1) / hm::kConvRows);
+  for (int l = p; l >= 1; --l) {
+    st = launch("hss2hodlr_level", s, [&] { hm::hss2hodlr_level_kernel<<<grid, 256, smem, s>>>(cp, l); });
+    if (st) return st;
+  }
+  return HM_OK;
 }
 
 const char* hm_last_error(void) { return g_err.c_str(); }

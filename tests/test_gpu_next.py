@@ -1,0 +1,166 @@
+"""GPU parity of SURVEY §8(f) f2 (||A||_2 estimate, power method on A A^*)
+and f3 (hss2hodlr) against the oracle, plus properties that hold at
+any size (closed-form ||T^-1||_2 at BASELINE config 5; converted-HODLR product
+= HSS product at config 4 in full), determinism and CUDA-graph capture.
+
+Tolerances: relative 1e-12 (BASELINE.json north_star) for the norm estimate,
+the converted factors (per level, Frobenius) and every product.
+"""
+import numpy as np
+import pytest
+
+import hm_inputs
+import oracle
+from test_gpu_parity import TOL, dev, relerr
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1909_07909_b200 as hm_
+    from paper_1909_07909_b200 import build
+    build.build()
+    hm_.load()
+    return hm_
+
+
+def exact_inv_laplacian_norm(n):
+    return 1.0 / (4.0 * np.sin(np.pi / (2 * (n + 1))) ** 2)
+
+
+# ------------------------------------------------------- norm estimate --
+
+NORM_HODLR = [(1024, 64, 4, 8, 3), (65536, 256, 8, 16, 5), (16384, 64, 8, 2, 4), (4096, 32, 7, 4, 1),
+              (256, 256, 0, 0, 6)]
+
+
+@pytest.mark.parametrize("n,leaf,levels,k,iters", NORM_HODLR)
+def test_hodlr_norm2_est_vs_oracle(hm, n, leaf, levels, k, iters):
+    h = hm_inputs.hodlr_random(n, levels, [k] * levels, cid=41)
+    x0 = hm_inputs.rhs(n, 1, cid=41).ravel()
+    ref = oracle.hodlr_norm2_est(n, levels, h.ranks, h.D, h.U, h.V, x0, iters)
+    est = hm.hodlr_norm2_est(n, levels, leaf, h.ranks, dev(h.D), dev(h.U), dev(h.V), dev(x0), iters)
+    assert abs(float(est.item()) - ref) <= TOL * ref
+
+
+NORM_HSS = [(4096, 64, 6, 16, 3), (8192, 64, 7, 16, 4), (2048, 128, 4, 32, 2), (100, 100, 0, 4, 3)]
+
+
+@pytest.mark.parametrize("n,leaf,levels,k,iters", NORM_HSS)
+def test_hss_norm2_est_vs_oracle(hm, n, leaf, levels, k, iters):
+    s = hm_inputs.hss_random(n, levels, k, cid=42)
+    x0 = hm_inputs.rhs(n, 1, cid=42).ravel()
+    ref = oracle.hss_norm2_est(n, levels, k, s.D, s.U, s.V, s.R, s.W, s.B, x0, iters)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    est = hm.hss_norm2_est(n, levels, leaf, k, *g, dev(x0), iters)
+    assert abs(float(est.item()) - ref) <= TOL * ref
+
+
+def test_norm2_est_zero_cases(hm):
+    n, p, b = 4096, 4, 256
+    h = hm_inputs.hodlr_random(n, p, [4] * p, cid=43)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    e0 = hm.hodlr_norm2_est(n, p, b, h.ranks, dev(h.D), dev(h.U), dev(h.V), z, 3)  # zero start vector
+    zD, zU = torch.zeros(h.D.size, dtype=torch.float64, device="cuda"), torch.zeros(h.U.size, dtype=torch.float64,
+                                                                                      device="cuda")
+    e1 = hm.hodlr_norm2_est(n, p, b, h.ranks, zD, zU, zU, dev(hm_inputs.rhs(n, 1, cid=43).ravel()), 3)
+    assert float(e0.item()) == 0.0 and float(e1.item()) == 0.0
+
+
+def test_norm2_est_config5_closed_form(hm):
+    """BASELINE config 5 in full (n = 2^24, 16 levels): ||T^{-1}||_2 = 1/(4 sin^2(pi/(2(n+1)))),
+    eigenvalue ratio 1/4 — 12 power steps are at rounding level."""
+    cfg = hm_inputs.CONFIGS[5]
+    hd = hm_inputs.hodlr_inverse_laplacian(cfg.n, cfg.levels, xp=torch, device="cuda:0")
+    x0 = dev(hm_inputs.rhs(cfg.n, 1, cid=5).ravel())
+    est = hm.hodlr_norm2_est(cfg.n, cfg.levels, cfg.leaf, hd.ranks, hd.D, hd.U, hd.V, x0, 12)
+    ex = exact_inv_laplacian_norm(cfg.n)
+    assert abs(float(est.item()) - ex) <= TOL * ex
+
+
+def test_norm2_est_hss_closed_form_config4_tree(hm):
+    """Rank-2 HSS inverse Laplacian on the config-4 tree (n = 2^22, leaf 128, 15 levels)."""
+    n, p = 1 << 22, 15
+    s = hm_inputs.hss_inverse_laplacian(n, p)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    x0 = dev(hm_inputs.rhs(n, 1, cid=5).ravel())
+    est = hm.hss_norm2_est(n, p, s.leaf, s.k, *g, x0, 12)
+    ex = exact_inv_laplacian_norm(n)
+    assert abs(float(est.item()) - ex) <= TOL * ex
+
+
+def test_norm2_est_deterministic_and_graph_capture(hm):
+    """Bitwise repeatable; the whole estimate (products, norms, scaling — HSS includes the
+    cooperative tree sweep) captured in one CUDA graph and replayed gives the same bits."""
+    n, p, k = 4096, 6, 16
+    s = hm_inputs.hss_random(n, p, k, cid=44)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    x0 = dev(hm_inputs.rhs(n, 1, cid=44).ravel())
+    ws = torch.empty(hm.hm_hss_norm2_workspace_bytes(n, p, s.leaf, k), dtype=torch.uint8, device="cuda")
+    e1 = hm.hss_norm2_est(n, p, s.leaf, k, *g, x0, 5, workspace=ws).clone()
+    e2 = hm.hss_norm2_est(n, p, s.leaf, k, *g, x0, 5, workspace=ws).clone()
+    est = torch.zeros(1, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up on the capture stream (function attributes set once)
+        hm.hss_norm2_est(n, p, s.leaf, k, *g, x0, 5, est=est, workspace=ws)
+    torch.cuda.current_stream().wait_stream(side)
+    est.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        hm.hss_norm2_est(n, p, s.leaf, k, *g, x0, 5, est=est, workspace=ws)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(e1, e2) and torch.equal(est, e1)
+
+
+# -------------------------------------------------------------- hss2hodlr --
+
+CONV_CASES = [(4096, 64, 6, 16), (2048, 128, 4, 32), (8192, 64, 7, 64), (64, 32, 1, 4), (4096, 16, 8, 3),
+              (32768, 128, 8, 32)]
+
+
+@pytest.mark.parametrize("n,leaf,p,k", CONV_CASES)
+def test_hss_to_hodlr_vs_oracle(hm, n, leaf, p, k):
+    s = hm_inputs.hss_random(n, p, k, cid=45)
+    Uo, Vo = oracle.hss_to_hodlr(n, p, k, s.U, s.V, s.R, s.W, s.B)
+    Uh, Vh = hm.hss_to_hodlr(n, p, leaf, k, dev(s.U), dev(s.V), dev(s.R), dev(s.W), dev(s.B))
+    torch.cuda.synchronize()
+    Uh, Vh = Uh.cpu().numpy(), Vh.cpu().numpy()
+    for l in range(p):  # per level: a small level cannot hide in a global norm (G14)
+        sl = slice(l * n * k, (l + 1) * n * k)
+        assert relerr(Uh[sl], Uo[sl]) <= TOL and relerr(Vh[sl], Vo[sl]) <= TOL
+    # the converted HODLR matrix is the HSS matrix: GPU HODLR product vs HSS oracle
+    X = hm_inputs.rhs(n, 3, cid=45)
+    Y = hm.hodlr_matvec(n, p, leaf, [k] * p, dev(s.D), dev(Uh), dev(Vh), dev(X))
+    torch.cuda.synchronize()
+    assert relerr(Y.cpu().numpy(), oracle.hss_matvec(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)) <= TOL
+
+
+def test_hss_to_hodlr_config4_full_size(hm):
+    """BASELINE config 4 in full (n = 2^22, leaf 128, 15 levels, k = 32): the HODLR product of
+    the converted factors equals the HSS product (both on the GPU, X with 32 columns), and the
+    conversion is bitwise repeatable."""
+    cfg = hm_inputs.CONFIGS[4]
+    n, p, b, k = cfg.n, cfg.levels, cfg.leaf, cfg.k
+    s = hm_inputs.device_hss_random(n, p, k, 4, torch.device("cuda:0"))
+    X = torch.randn(n, 32, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(4))
+    Ys = hm.hss_matvec(n, p, b, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
+    Uh, Vh = hm.hss_to_hodlr(n, p, b, k, s.U, s.V, s.R, s.W, s.B)
+    Yh = hm.hodlr_matvec(n, p, b, [k] * p, s.D, Uh, Vh, X)
+    rel = float(torch.linalg.norm(Yh - Ys) / torch.linalg.norm(Ys))
+    assert rel <= TOL
+    Uh2, _ = hm.hss_to_hodlr(n, p, b, k, s.U, s.V, s.R, s.W, s.B)
+    assert torch.equal(Uh, Uh2)
+
+
+def test_hss_to_hodlr_rejects_overlap(hm):
+    s = hm_inputs.hss_random(256, 2, 4, cid=46)
+    g = [dev(a) for a in (s.U, s.V, s.R, s.W, s.B)]
+    with pytest.raises(hm.HmError):
+        hm.hss_to_hodlr(256, 2, 64, 4, *g, Uh=g[0].new_empty(2 * 256 * 4), Vh=None)  # fine
+        big = torch.empty(2 * 256 * 4, dtype=torch.float64, device="cuda")
+        hm.hss_to_hodlr(256, 2, 64, 4, *g, Uh=big, Vh=big)  # same buffer twice

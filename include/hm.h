@@ -58,8 +58,8 @@ typedef enum {
  * n = leaf * 2^levels, every level-l node I_i^l = [i*n/2^l, (i+1)*n/2^l)
  * (0-based), i.e. the default split of P:378-379 when n/leaf is a power of two.
  * levels = p = depth (root l = 0, leaves l = p); levels = 0 means A = D (one
- * dense block). General endpoint vectors (empty leaves)
- * return HM_ERR_UNSUPPORTED. */
+ * dense block). General endpoint vectors (empty
+ * leaves) use the *_general calls below. */
 typedef struct {
   int64_t n;      /* matrix order, >= 1                                    */
   int32_t levels; /* p >= 0                                                */
@@ -78,8 +78,10 @@ typedef struct {
  *   V  same shape as U; rows I_b of level l hold the right factor of block
  *                    (sib b, b). (V12 = V_l(I_2q+1), V21 = V_l(I_2q).)
  *   ranks [p] (host array): ranks[l-1] = k_l >= 0 (0 encodes the zero
- *                    block). Supported: every nonzero k_l equal and
- *                    <= 64; otherwise HM_ERR_UNSUPPORTED.
+ *                    block), each <= 64. Equal nonzero ranks run the
+ *                    tuned kernels; per-level ranks run the
+ *                    general-tree kernels (hodlr_matvec_general) with the
+ *                    same workspace query (not with HM_WS_HOSTIO).
  *   X  [n][nrhs], Y [n][nrhs]; nrhs >= 1.
  * Cost O(k n log n); bytes = 8(n b + 2 sum_l n k_l + 2 n nrhs). */
 
@@ -158,6 +160,37 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
                             const double* R, const double* W, const double* B,
                             const double* X_host, int32_t nrhs, double* Y_host,
                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* ----------------------------------- general cluster trees (§8(f) f4) --
+ * The cluster tree of depth `levels` = p given by its leaf endpoint vector
+ * c (Def. 2.1): c is a HOST array of 2^p int64 values,
+ * nondecreasing, c[2^p - 1] = n; leaf i holds rows [c[i-1], c[i]) (c[-1] = 0)
+ * and may be EMPTY (Fig. 4); the level-l node i is the union of
+ * its 2^(p-l) leaves. D concatenates the |I_i| x |I_i| leaf blocks (row-major)
+ * in leaf order. HODLR ranks may differ per level, 0..64 each; U, V
+ * are level-major with level l at offset n * sum_{l' < l} k_l', [n][k_l]. HSS
+ * takes one rank k (0..64) and the generator layout of hss_matvec.
+ *   op = 0: Y = A X;  op = 1: Y = A^T X (adjoint, §8(f) f1).
+ * Limits: largest leaf + sum of ranks <= 20480 (shared-memory staging of a
+ * leaf), else HM_ERR_UNSUPPORTED. Errors as for the uniform calls; c not
+ * nondecreasing or c[2^p-1] != n is HM_ERR_INVALID_ARG. The tables derived
+ * from c are copied into the workspace with one pageable host-to-device copy
+ * per call, so these calls are NOT CUDA-graph capturable. Deterministic.
+ * (hodlr_matvec / hodlr_matvec_t on the uniform tree route per-level ranks
+ * here automatically, with the same workspace query.) */
+hm_status hm_hodlr_general_workspace_bytes(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks,
+                                           int32_t nrhs, size_t* bytes);
+hm_status hodlr_matvec_general(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks, int32_t op,
+                               const double* D, const double* U, const double* V,
+                               const double* X, int32_t nrhs, double* Y,
+                               void* workspace, size_t workspace_bytes, void* stream);
+hm_status hm_hss_general_workspace_bytes(int64_t n, int32_t levels, const int64_t* c, int32_t k, int32_t nrhs,
+                                         size_t* bytes);
+hm_status hss_matvec_general(int64_t n, int32_t levels, const int64_t* c, int32_t k, int32_t op,
+                             const double* D, const double* U, const double* V,
+                             const double* R, const double* W, const double* B,
+                             const double* X, int32_t nrhs, double* Y,
+                             void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------- norm estimate (§8(f) f2) --
  * ||A||_2 estimate by the power method on A A^* ("estimating ||A||_2

@@ -33,7 +33,8 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hm_hss_dist_sizes", "hss_matvec_dist_begin", "hss_matvec_dist_end",
            "hodlr_matvec_t", "hss_matvec_t",
            "hm_hodlr_norm2_workspace_bytes", "hodlr_norm2_est", "hm_hss_norm2_workspace_bytes", "hss_norm2_est",
-           "hss_to_hodlr")
+           "hss_to_hodlr", "hm_hodlr_general_workspace_bytes", "hodlr_matvec_general",
+           "hm_hss_general_workspace_bytes", "hss_matvec_general")
 
 
 class HmError(RuntimeError):
@@ -79,6 +80,10 @@ def load() -> ctypes.CDLL:
         "hm_hss_norm2_workspace_bytes": [T, i32, ctypes.POINTER(sz)],
         "hss_norm2_est": [T, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hss_to_hodlr": [T, i32, P, P, P, P, P, P, P, P],
+        "hm_hodlr_general_workspace_bytes": [i64, i32, P, P, i32, ctypes.POINTER(sz)],
+        "hodlr_matvec_general": [i64, i32, P, P, i32, P, P, P, P, i32, P, P, sz, P],
+        "hm_hss_general_workspace_bytes": [i64, i32, P, i32, i32, ctypes.POINTER(sz)],
+        "hss_matvec_general": [i64, i32, P, i32, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hm_profile_enable": [i32],
         "hm_profile_collect": [ctypes.POINTER(hm_launch_record), i32, ctypes.POINTER(i32)],
     }
@@ -317,3 +322,63 @@ def hss_to_hodlr(n, levels, leaf, k, U, V, R, W, B, Uh=None, Vh=None, stream=Non
     _check(load().hss_to_hodlr(ctypes.byref(t), int(k), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(Uh),
                                _ptr(Vh), _stream(stream)))
     return Uh, Vh
+
+
+# ------------------------------------------------------ general trees (f4) --
+
+def _endpoints(c, levels):
+    import numpy as np
+    c = np.ascontiguousarray(c, dtype=np.int64)
+    if c.shape != (1 << levels,):
+        raise ValueError("endpoint vector must have 2^levels entries")
+    return c
+
+
+def hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs) -> int:
+    c = _endpoints(c, levels)
+    out = ctypes.c_size_t(0)
+    _check(load().hm_hodlr_general_workspace_bytes(int(n), int(levels), c.ctypes.data, _ranks(ranks, levels),
+                                                   int(nrhs), ctypes.byref(out)))
+    return out.value
+
+
+def hodlr_matvec_general(n, levels, c, ranks, D, U, V, X, op=0, Y=None, workspace=None, stream=None):
+    """Y = A X (op 0) or A^T X (op 1) for a HODLR matrix on the tree with leaf endpoints c (host,
+    2^levels int64), per-level ranks allowed (include/hm.h hodlr_matvec_general)."""
+    import torch
+    c = _endpoints(c, levels)
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    ws = _workspace(hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs), workspace, X.device)
+    _check(load().hodlr_matvec_general(int(n), int(levels), c.ctypes.data, _ranks(ranks, levels), int(op), _ptr(D),
+                                       _ptr(U), _ptr(V), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
+                                       _stream(stream)))
+    return Y
+
+
+def hm_hss_general_workspace_bytes(n, levels, c, k, nrhs) -> int:
+    c = _endpoints(c, levels)
+    out = ctypes.c_size_t(0)
+    _check(load().hm_hss_general_workspace_bytes(int(n), int(levels), c.ctypes.data, int(k), int(nrhs),
+                                                 ctypes.byref(out)))
+    return out.value
+
+
+def hss_matvec_general(n, levels, c, k, D, U, V, R, W, B, X, op=0, Y=None, workspace=None, stream=None):
+    """Y = A X (op 0) or A^T X (op 1) for an HSS matrix on the tree with leaf endpoints c."""
+    import torch
+    c = _endpoints(c, levels)
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    ws = _workspace(hm_hss_general_workspace_bytes(n, levels, c, k, nrhs), workspace, X.device)
+    _check(load().hss_matvec_general(int(n), int(levels), c.ctypes.data, int(k), int(op), _ptr(D), _ptr(U), _ptr(V),
+                                     _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
+                                     _stream(stream)))
+    return Y

@@ -91,8 +91,10 @@ def test_bad_ranks_and_nrhs_rejected():
     with pytest.raises(hm.HmError) as e:
         hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, -1], 1)
     assert e.value.status == hm.HM_ERR_INVALID_ARG
+    # per-level ranks run on the general-tree kernels
+    assert hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 8], 1) > 0
     with pytest.raises(hm.HmError) as e:
-        hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 8], 1)   # variable ranks: not built
+        hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 65], 1)
     assert e.value.status == hm.HM_ERR_UNSUPPORTED
     with pytest.raises(hm.HmError) as e:
         hm.hm_hodlr_workspace_bytes(1024, 2, 256, [4, 4], 0)
@@ -128,3 +130,20 @@ def test_binding_refuses_cpu_tensors():
     x = torch.zeros(1024, 1, dtype=torch.float64)
     with pytest.raises(TypeError):
         hm.hodlr_matvec(1024, 2, 256, [4, 4], x, x, x, x)
+
+
+def test_general_tree_validation():
+    """Endpoint vectors: nondecreasing, last = n; empty leaves allowed."""
+    c = [3, 7, 7, 20, 26, 26, 31, 40]
+    assert hm.hm_hodlr_general_workspace_bytes(40, 3, c, [2, 1, 3], 2) > 0
+    assert hm.hm_hss_general_workspace_bytes(40, 3, c, 4, 2) > 0
+    for bad, st in (([3, 7, 6, 20, 26, 26, 31, 40], hm.HM_ERR_INVALID_ARG),   # decreasing
+                    ([3, 7, 7, 20, 26, 26, 31, 39], hm.HM_ERR_INVALID_ARG)):  # last != n
+        with pytest.raises(hm.HmError) as e:
+            hm.hm_hodlr_general_workspace_bytes(40, 3, bad, [2, 1, 3], 2)
+        assert e.value.status == st
+    with pytest.raises(hm.HmError) as e:  # one leaf larger than the shared-memory staging
+        hm.hm_hss_general_workspace_bytes(30000, 1, [29000, 30000], 4, 1)
+    assert e.value.status == hm.HM_ERR_UNSUPPORTED
+    with pytest.raises(ValueError):
+        hm.hm_hodlr_general_workspace_bytes(40, 3, c[:4], [2, 1, 3], 2)

@@ -1,0 +1,114 @@
+"""GPU parity on general cluster trees and per-level HODLR ranks.
+
+Trees given by leaf endpoint vectors: ragged leaves, empty leaves
+(Fig. 4), the default ceil split of P:378-379 for n not a multiple
+of 2^p, and nodes big enough to be split over several V^T X chunks. Forward
+and adjoint products against the oracle at 1e-12 (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from test_gpu_parity import TOL, dev, relerr
+from test_oracle import random_hodlr_general, random_hss_general
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1909_07909_b200 as hm_
+    from paper_1909_07909_b200 import build
+    build.build()
+    hm_.load()
+    return hm_
+
+
+def ragged_tree(n, p, seed, empty=0.15):
+    """Random nondecreasing endpoints with about `empty` of the leaves empty."""
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(0.2, 1.8, size=1 << p)
+    w[rng.uniform(size=1 << p) < empty] = 0.0
+    c = np.floor(np.cumsum(w) / w.sum() * n).astype(np.int64)
+    c[-1] = n
+    return c
+
+
+TREES = [
+    ("fig4", np.array([3, 7, 7, 20, 26, 26, 31, 40]), 3),
+    ("ceil_split_1000", None, None),            # default cluster n = 1000, nmin = 64
+    ("ragged_p6", ragged_tree(6000, 6, 1), 6),
+    ("ragged_p9", ragged_tree(40000, 9, 2), 9),
+    ("big_nodes", np.array([9000, 20000, 20000, 31000]), 2),   # nodes > one 4096-row chunk
+    ("p0", np.array([77]), 0),
+]
+
+
+def tree(name, c, p):
+    if c is None:
+        p, c = oracle.default_cluster(1000, 64)
+    return int(c[-1]), p, np.asarray(c, dtype=np.int64)
+
+
+@pytest.mark.parametrize("name,c,p", TREES)
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_hodlr_general_vs_oracle(hm, name, c, p, m):
+    n, p, c = tree(name, c, p)
+    rng = np.random.default_rng(51 + m)
+    ranks = [int(v) for v in rng.integers(0, 17, size=p)]  # per-level ranks incl. 0
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    for op in (0, 1):
+        Y = hm.hodlr_matvec_general(n, p, c, ranks, dev(D), dev(U), dev(V), dev(X), op=op)
+        torch.cuda.synchronize()
+        f = oracle.hodlr_matvec_t if op else oracle.hodlr_matvec
+        assert relerr(Y.cpu().numpy(), f(n, p, ranks, D, U, V, X, c=c)) <= TOL, op
+
+
+@pytest.mark.parametrize("name,c,p", TREES)
+@pytest.mark.parametrize("k,m", [(4, 1), (16, 16), (32, 3), (0, 2)])
+def test_hss_general_vs_oracle(hm, name, c, p, k, m):
+    n, p, c = tree(name, c, p)
+    rng = np.random.default_rng(61 + k + m)
+    D, U, V, R, W, B = random_hss_general(c, p, k, rng)
+    X = rng.standard_normal((n, m))
+    g = [dev(a) for a in (D, U, V, R, W, B)]
+    for op in (0, 1):
+        Y = hm.hss_matvec_general(n, p, c, k, *g, dev(X), op=op)
+        torch.cuda.synchronize()
+        f = oracle.hss_matvec_t if op else oracle.hss_matvec
+        assert relerr(Y.cpu().numpy(), f(n, p, k, D, U, V, R, W, B, X, c=c)) <= TOL, op
+
+
+@pytest.mark.parametrize("n,leaf,p,ranks,m", [
+    (65536, 256, 8, [16, 8, 16, 4, 2, 16, 32, 1], 1),
+    (65536, 256, 8, [64, 32, 16, 8, 4, 2, 1, 0], 8),
+    (16384, 64, 8, [1, 2, 3, 4, 5, 6, 7, 8], 3),
+])
+def test_uniform_tree_per_level_ranks(hm, n, leaf, p, ranks, m):
+    """hodlr_matvec / hodlr_matvec_t route per-level ranks to the general kernels."""
+    rng = np.random.default_rng(71)
+    c = np.arange(1, (1 << p) + 1, dtype=np.int64) * leaf
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    Y = hm.hodlr_matvec(n, p, leaf, ranks, dev(D), dev(U), dev(V), dev(X))
+    Yt = hm.hodlr_matvec_t(n, p, leaf, ranks, dev(D), dev(U), dev(V), dev(X))
+    torch.cuda.synchronize()
+    assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X)) <= TOL
+    assert relerr(Yt.cpu().numpy(), oracle.hodlr_matvec_t(n, p, ranks, D, U, V, X)) <= TOL
+
+
+def test_general_uniform_endpoints_match_uniform_path(hm):
+    """The general kernels on uniform endpoints agree with the tuned uniform kernels."""
+    n, p, b, k, m = 32768, 7, 256, 16, 8
+    rng = np.random.default_rng(72)
+    c = np.arange(1, (1 << p) + 1, dtype=np.int64) * b
+    D, U, V = random_hodlr_general(c, p, [k] * p, rng)
+    X = dev(rng.standard_normal((n, m)))
+    Yg = hm.hodlr_matvec_general(n, p, c, [k] * p, dev(D), dev(U), dev(V), X)
+    Yu = hm.hodlr_matvec(n, p, b, [k] * p, dev(D), dev(U), dev(V), X)
+    assert float(torch.linalg.norm(Yg - Yu) / torch.linalg.norm(Yu)) <= TOL
+    Yg2 = hm.hodlr_matvec_general(n, p, c, [k] * p, dev(D), dev(U), dev(V), X)
+    assert torch.equal(Yg, Yg2)

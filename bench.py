@@ -265,6 +265,112 @@ class DistWorkload:
         return 8 * (self.X5.numel() + self.X4.numel()), 8 * (self.Y5.numel() + self.Y4.numel())
 
 
+# ------------------------------------------------------ nrhs / ops sweep --
+
+def _time_call(torch, f, reps, warm=2):
+    """Device ms per call: CUDA events on the current stream around `reps` calls."""
+    for _ in range(warm):
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def sweep(torch, device, wl, peak):
+    """Secondary measurements (not part of `value`): the metric "vs nrhs" on config 3
+    (m = 1, 8, 64), the small configs 1-2 (latency-bound, L2-resident: us per call), the
+    adjoint products, the ||A||_2 estimate (f2), hss2hodlr (f3) and
+    general-tree / per-level-rank products (f4). Inputs drawn on the device."""
+    hm = wl.hm
+    out = {}
+
+    def gbs(nbytes, ms):
+        return round(nbytes / (ms * 1e-3) / 1e9, 1)
+
+    g = torch.Generator(device=device)
+    g.manual_seed(hm_inputs.MASTER_SEED + 7)
+    # config 3: HODLR n = 2^20, leaf 256, 12 levels, k = 16, nrhs 1 / 8 / 64, A X and A^T X
+    c3 = hm_inputs.CONFIGS[3]
+    h3 = hm_inputs.device_hodlr_random(c3.n, c3.levels, [c3.k] * c3.levels, hm_inputs.MASTER_SEED + 3, device)
+    for m in c3.nrhs:
+        X = torch.randn(c3.n, m, dtype=torch.float64, device=device, generator=g)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hodlr_workspace_bytes(c3.n, c3.levels, c3.leaf, h3.ranks, m), dtype=torch.uint8,
+                         device=device)
+        nb = hodlr_bytes(c3.n, c3.leaf, c3.levels, c3.k, m)
+        fl = hodlr_flops(c3.n, c3.leaf, c3.levels, c3.k, m)
+        for nm, fn in (("", hm.hodlr_matvec), ("^T", hm.hodlr_matvec_t)):
+            ms = _time_call(torch, lambda: fn(c3.n, c3.levels, c3.leaf, h3.ranks, h3.D, h3.U, h3.V, X, Y, ws), 10)
+            out[f"c3_m{m}{nm}"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
+                                   "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2)}
+        del X, Y, ws
+    # per-level ranks on the config-3 tree (f4): ranks 16 / 8 alternating -> general kernels
+    rk = [16 if l % 2 else 8 for l in range(c3.levels)]
+    hv = hm_inputs.device_hodlr_random(c3.n, c3.levels, rk, hm_inputs.MASTER_SEED + 5, device)
+    X = torch.randn(c3.n, 8, dtype=torch.float64, device=device, generator=g)
+    Y = torch.empty_like(X)
+    ws = torch.empty(hm.hm_hodlr_workspace_bytes(c3.n, c3.levels, c3.leaf, rk, 8), dtype=torch.uint8, device=device)
+    nb = 8 * (c3.n * c3.leaf + 2 * sum(rk) * c3.n + 2 * c3.n * 8)
+    ms = _time_call(torch, lambda: hm.hodlr_matvec(c3.n, c3.levels, c3.leaf, rk, hv.D, hv.U, hv.V, X, Y, ws), 5)
+    out["c3_m8_per_level_ranks"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "ranks": "16/8 alternating",
+                                    "path": "general-tree kernels"}
+    del h3, hv, X, Y, ws
+    # config 5 and 4 adjoints on the bench's own generators
+    h, s4 = wl.h5, wl.s4
+    ms = _time_call(torch, lambda: hm.hodlr_matvec_t(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, wl.X5, wl.Y5,
+                                                     wl.ws5), 5)
+    b5 = hodlr_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5)
+    out["c5^T"] = {"ms": round(ms, 4), "GB/s": gbs(b5, ms), "frac_hbm": round(b5 / (ms * 1e-3) / 1e9 / peak, 4)}
+    ms = _time_call(torch, lambda: hm.hss_matvec_t(C4.n, C4.levels, C4.leaf, C4.k, s4.D, s4.U, s4.V, s4.R, s4.W, s4.B,
+                                                   wl.X4, wl.Y4, wl.ws4), 5)
+    b4 = hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
+    out["c4^T"] = {"ms": round(ms, 4), "GB/s": gbs(b4, ms), "frac_hbm": round(b4 / (ms * 1e-3) / 1e9 / peak, 4)}
+    # ||A||_2 of config 5 (power method on A A^*, 10 steps = 20 products)
+    x0 = wl.X5[:, 0].contiguous()
+    wsn = torch.empty(hm.hm_hodlr_norm2_workspace_bytes(C5.n, C5.levels, C5.leaf, h.ranks), dtype=torch.uint8,
+                      device=device)
+    est = torch.zeros(1, dtype=torch.float64, device=device)
+    ms = _time_call(torch, lambda: hm.hodlr_norm2_est(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, x0, 10, est,
+                                                      wsn), 2, warm=1)
+    exact = 1.0 / (4.0 * np.sin(np.pi / (2 * (C5.n + 1))) ** 2)
+    out["c5_norm2_est"] = {"ms": round(ms, 3), "iters": 10, "ms_per_product": round(ms / 20, 4),
+                           "GB/s": gbs(20 * b5, ms), "rel_err_vs_closed_form": float(abs(est.item() - exact) / exact)}
+    del wsn
+    # hss2hodlr on config 4: bytes = generators read + 2 p n k doubles written
+    Uh = torch.empty(C4.levels * C4.n * C4.k, dtype=torch.float64, device=device)
+    Vh = torch.empty_like(Uh)
+    ms = _time_call(torch, lambda: hm.hss_to_hodlr(C4.n, C4.levels, C4.leaf, C4.k, s4.U, s4.V, s4.R, s4.W, s4.B, Uh,
+                                                   Vh), 3, warm=1)
+    nbc = 8 * (2 * C4.n * C4.k + 2 * C4.levels * C4.n * C4.k + 4 * ((1 << C4.levels) - 2) * C4.k ** 2
+               + 2 * ((1 << C4.levels) - 1) * C4.k ** 2)
+    out["c4_hss2hodlr"] = {"ms": round(ms, 3), "GB/s": gbs(nbc, ms),
+                           "bytes": "U,V,R,W,B read + Uh,Vh (levels x n x k) written"}
+    del Uh, Vh
+    torch.cuda.empty_cache()
+    # small configs: latency (us per call, L2-resident)
+    c1, c2 = hm_inputs.CONFIGS[1], hm_inputs.CONFIGS[2]
+    h1 = hm_inputs.device_hodlr_random(c1.n, c1.levels, [c1.k] * c1.levels, hm_inputs.MASTER_SEED + 1, device)
+    X = torch.randn(c1.n, 1, dtype=torch.float64, device=device, generator=g)
+    Y = torch.empty_like(X)
+    ws = torch.empty(hm.hm_hodlr_workspace_bytes(c1.n, c1.levels, c1.leaf, h1.ranks, 1), dtype=torch.uint8,
+                     device=device)
+    ms = _time_call(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V, X, Y, ws), 200)
+    out["c1_us"] = round(ms * 1e3, 2)
+    s2 = hm_inputs.device_hss_random(c2.n, c2.levels, c2.k, hm_inputs.MASTER_SEED + 2, device)
+    X = torch.randn(c2.n, 16, dtype=torch.float64, device=device, generator=g)
+    Y = torch.empty_like(X)
+    ws = torch.empty(hm.hm_hss_workspace_bytes(c2.n, c2.levels, c2.leaf, c2.k, 16), dtype=torch.uint8, device=device)
+    ms = _time_call(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R, s2.W, s2.B, X,
+                                                 Y, ws), 200)
+    out["c2_us"] = round(ms * 1e3, 2)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -411,6 +517,8 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    if world == 1 and not args.no_sweep:
+        out["sweep"] = sweep(torch, device, wl, peak)
     if world > 1:
         out["per_config"]["note"] = "per-rank device time (rank 0's launch trace)"
         out["roofline"]["kernel"] += f" — rank 0's shard (1/{world} of the rows)"
@@ -505,6 +613,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the secondary nrhs / ops sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -673,7 +673,11 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
   constexpr bool PAIR = DT && (RG % 2 == 0);
   extern __shared__ double sm[];
   constexpr int MC = NT * 8;
-  constexpr int ZS = MC + 4;
+  // Row strides of the staged operand (conflict-free 64-bit fragment loads, see
+  // hm_tree.cuh): rows 2j apart (row-major pattern) need ZS = 2 (mod 4); the
+  // adjoint's D^T pattern reads the X rows j apart and needs 4 (mod 8).
+  constexpr int ZS = MC + 2;
+  constexpr int ZSX = DT ? MC + 4 : ZS;  // X region
   const int nchunks = (P.m + MC - 1) / MC;
   const int64_t leaf = blockIdx.x / nchunks;
   const int c0 = (int)(blockIdx.x - leaf * nchunks) * MC;
@@ -682,12 +686,13 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
   const int m = P.m;
   double* Z = sm;
   const int mc = min(MC, m - c0);
-  stage_rows_async(Z, ZS, P.X + r0 * m + c0, m, (int)b, mc, MC);
-  int64_t zoff = b;
+  stage_rows_async(Z, ZSX, P.X + r0 * m + c0, m, (int)b, mc, MC);
+  double* ZT = Z + b * ZSX;  // T region
+  int64_t zoff = 0;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
     const int64_t node = (leaf >> sg.shift) ^ sg.xr;
-    stage_rows_async(Z + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
+    stage_rows_async(ZT + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
     zoff += sg.k;
   }
   cp_async_wait_all();
@@ -699,13 +704,13 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
   const int64_t wrow = (int64_t)warp * 8 * RG;
-  if constexpr (DT) warp_dt_mma<RG, NT>(acc, P.D + leaf * b * b + wrow, b, (int)b, Z, ZS, lane);
+  if constexpr (DT) warp_dt_mma<RG, NT>(acc, P.D + leaf * b * b + wrow, b, (int)b, Z, ZSX, lane);
   else warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
-  zoff = b;
+  zoff = 0;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
-    warp_rowmajor_mma<RG, NT, false, false, PF, PAIR>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, Z + zoff * ZS, ZS,
-                                                      MC, lane);
+    warp_rowmajor_mma<RG, NT, false, false, PF, PAIR>(acc, sg.A + (r0 + wrow) * sg.k, sg.k, sg.k, ZT + zoff * ZS,
+                                                      ZS, MC, lane);
     zoff += sg.k;
   }
   const int i = lane >> 2, j = lane & 3;

@@ -30,12 +30,17 @@ struct TreeParams {
 };
 
 // Staged blocks hold mpad = ceil(m / 8NT) * 8NT columns (zero padded) so every
-// column chunk reads inside its row. Row strides: transposed B fragments read
-// rows r..r+3 (stride = 8 mod 16 doubles is conflict-free), row-major B
-// fragments read rows r, r+2, r+4, r+6 (stride = 4 mod 8).
+// column chunk reads inside its row. Row strides (in doubles) for conflict-free
+// 64-bit fragment loads — a warp's 64-bit shared load is served per half-warp
+// (16 lanes: i = lane>>2 in 0..3, j = lane&3), conflict-free iff the 16
+// addresses fall in 16 distinct 8-byte bank pairs (d mod 16 distinct):
+//   transposed B fragments read rows r + j, d = j zs + i: zs = 4 (mod 8);
+//   row-major B fragments read rows r + 2j, d = 2 j zs + i: zs = 2 (mod 4).
+// (Measured with ncu: strides 8 (mod 16) / 4 (mod 8) gave 2-way conflicts on
+// every load, l1tex__data_bank_conflicts = 1/2 of the wavefronts.)
 __host__ __device__ constexpr int tree_mpad(int m, int nt) { return (m + nt * 8 - 1) / (nt * 8) * (nt * 8); }
-__host__ __device__ constexpr int tree_up_stride(int mpad) { return mpad + (mpad % 16 == 0 ? 8 : 0); }
-__host__ __device__ constexpr int tree_down_stride(int mpad) { return mpad + 4; }
+__host__ __device__ constexpr int tree_up_stride(int mpad) { return mpad + 4; }
+__host__ __device__ constexpr int tree_down_stride(int mpad) { return mpad + 2; }
 __host__ __device__ constexpr int64_t tree_smem_doubles(int kt, int m, int nt) {
   return (4ll * kt * tree_up_stride(tree_mpad(m, nt)) > 3ll * kt * tree_down_stride(tree_mpad(m, nt)))
              ? 4ll * kt * tree_up_stride(tree_mpad(m, nt))

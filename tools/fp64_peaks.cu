@@ -63,6 +63,39 @@ __global__ void copy_kernel(const double2* __restrict__ a, double2* __restrict__
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) b[i] = a[i];
 }
 
+// (5) DMMA and DFMA at once: even warps issue DMMA, odd warps DFMA. If the two
+// pipes are independent the combined rate approaches their sum.
+template <int CH>
+__global__ void mix_kernel(double* out, int iters) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (warp & 1) {
+    double acc[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = fma(acc[c], 0.9999999, 1e-7);
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += acc[c];
+  } else {
+    double d[CH][2];
+    double a = 1.0 + threadIdx.x * 1e-12, b = 0.999999;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { d[c][0] = c; d[c][1] = -c; }
+    for (int i = 0; i < iters / 4; ++i) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(d[c][0]), "+d"(d[c][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += d[c][0] + d[c][1];
+  }
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 template <typename F>
 float time_ms(F f, int reps) {
   cudaEvent_t e0, e1;
@@ -96,6 +129,12 @@ int main() {
   float ms_dmma = time_ms([&] { dmma_kernel<8><<<blocks, threads>>>(out, iters / 4); }, 5);
   double dmma_tflops = 512.0 * 8 * (iters / 4) * (double)blocks * (threads / 32) / (ms_dmma * 1e-3) / 1e12;
 
+  // DMMA + DFMA warps side by side (half the warps each, same per-warp work as above)
+  float ms_mix = time_ms([&] { mix_kernel<8><<<blocks, threads>>>(out, iters); }, 5);
+  double mix_flop = 0.5 * (2.0 * 8 * iters * (double)blocks * threads) +
+                    0.5 * (512.0 * 8 * (iters / 4) * (double)blocks * (threads / 32));
+  double mix_tflops = mix_flop / (ms_mix * 1e-3) / 1e12;
+
   // Streams over 8 GiB
   size_t bytes = (size_t)8 << 30;
   double2 *a, *b;
@@ -111,7 +150,7 @@ int main() {
   double copy_gbs = 2.0 * (bytes / 2) / (ms_copy * 1e-3) / 1e9;
 
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_khz\": %d, \"dfma_tflops\": %.3f, \"dmma_m8n8k4_tflops\": %.3f, "
-         "\"read_stream_gbs\": %.1f, \"copy_rw_gbs\": %.1f}\n",
-         prop.name, sms, prop.clockRate, dfma_tflops, dmma_tflops, read_gbs, copy_gbs);
+         "\"dmma_plus_dfma_tflops\": %.3f, \"read_stream_gbs\": %.1f, \"copy_rw_gbs\": %.1f}\n",
+         prop.name, sms, prop.clockRate, dfma_tflops, dmma_tflops, mix_tflops, read_gbs, copy_gbs);
   return 0;
 }

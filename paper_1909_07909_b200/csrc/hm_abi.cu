@@ -21,6 +21,7 @@
 #include "hm_vec.cuh"
 #include "hm_convert.cuh"
 #include "hm_general.cuh"
+#include "hm_leafup.cuh"
 
 namespace {
 
@@ -143,6 +144,9 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 #ifndef HM_VTB_NTMAX
 #define HM_VTB_NTMAX 4
 #endif
+#ifndef HM_VT16_NTMAX
+#define HM_VT16_NTMAX 8
+#endif
 #ifndef HM_TREE_NTMAX
 #define HM_TREE_NTMAX 4
 #endif
@@ -231,7 +235,8 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
   } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 16, 64)) {
     P->vt = VtPath::kMma;
     P->tile = 8 * b;
-    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : 4);
+    // k = 16: up to 64 columns per pass (NT = 8), so V is streamed once for m <= 64
+    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : (k == 16 ? HM_VT16_NTMAX : 4));
   } else {
     P->vt = VtPath::kGeneric;
     P->mc_vt = vt_mc(b, nrhs);
@@ -460,11 +465,12 @@ hm_status vt_mma_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
 }
 
 hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cudaStream_t s) {
-#define HM_VT_MMA(KT_)                                             \
-  if (k == KT_) {                                                  \
-    if (nt == 1) return vt_mma_launch<KT_, 1>(vp, b, s);           \
-    if (nt == 2) return vt_mma_launch<KT_, 2>(vp, b, s);           \
-    if constexpr (KT_ < 64) return vt_mma_launch<KT_, 4>(vp, b, s); \
+#define HM_VT_MMA(KT_)                                                         \
+  if (k == KT_) {                                                              \
+    if (nt == 1) return vt_mma_launch<KT_, 1>(vp, b, s);                       \
+    if (nt == 2) return vt_mma_launch<KT_, 2>(vp, b, s);                       \
+    if constexpr (KT_ == 16) if (nt == 8) return vt_mma_launch<KT_, 8>(vp, b, s); \
+    if constexpr (KT_ < 64) return vt_mma_launch<KT_, 4>(vp, b, s);             \
   }
   HM_VT_MMA(16)
   HM_VT_MMA(32)
@@ -741,7 +747,7 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 constexpr int64_t kTreeBigLevel = 2048;
 
 template <int KT, int NT>
-hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s) {
+hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l) {
   constexpr int MINB = (KT == 32 && NT == 4) ? 3 : 0;  // measured, r01_tuning.md
   const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
   static bool attrs = false;
@@ -758,14 +764,14 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   int lbig = 1;  // first level with >= kTreeBigLevel nodes
   while (lbig <= p && (1ll << lbig) < kTreeBigLevel) ++lbig;
   hm_status st;
-  // upsweep: big levels p-1 .. lbig one launch each
-  for (int l = p - 1; up && l >= lbig; --l) {
+  // upsweep: big levels up_from_l .. lbig one launch each
+  for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
     st = launch("hss_up_level", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
-  const int up_from = up ? std::min(p - 1, lbig - 1) : 0, down_to = down ? std::min(p, lbig - 1) : 0;
+  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(p, lbig - 1) : 0;
   if (up_from >= 1 || down_to >= 1) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -791,12 +797,13 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   return HM_OK;
 }
 
-hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s) {
-#define HM_TREE(KT_)                                                   \
-  if (k == KT_) {                                                      \
-    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s);       \
-    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s);       \
-    return tree_launch<KT_, 4>(tp, p, up, down, s);                    \
+hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s,
+                        int up_from) {
+#define HM_TREE(KT_)                                                          \
+  if (k == KT_) {                                                             \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from);     \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from);     \
+    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from);                  \
   }
   HM_TREE(16)
   HM_TREE(32)
@@ -809,16 +816,17 @@ hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up,
 // generic per-level kernels or the DMMA tree kernels (tree_dispatch).
 hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
                          double* yh, const double* R_root, const double* y_root, bool up, bool down,
-                         cudaStream_t stream, int bt = 0) {
+                         cudaStream_t stream, int bt = 0, int up_from = -1) {
   const int k = P.k, nrhs = P.m;
   hm_status st;
+  if (up_from < 0) up_from = p - 1;  // first upsweep level to compute
   if (P.mma_levels) {
     hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
-    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream);
+    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from);
   }
   const int64_t km = (int64_t)k * nrhs;
   if (up)
-    for (int l = p - 1; l >= 1; --l) {
+    for (int l = up_from; l >= 1; --l) {
       hm::HssLevelParams hp{W, B, xh, yh, nullptr, nullptr, l, k, nrhs, 0};
       const int64_t total = ((int64_t)1 << l) * km;
       const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
@@ -853,6 +861,71 @@ hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int6
   return vt_generic(vp, K, stream);
 }
 
+// Fused Step 1 + first upsweep level (hss_leaf_up_kernel): k in {16, 32, 64},
+// 2 <= m <= 32, leaf a multiple of 16 and two leaves' staging in shared memory.
+int leafup_mp(int m) { return m <= 8 ? 8 : (m <= 16 ? 16 : 32); }
+
+template <int KT, int MP>
+size_t leafup_smem(int ru, int wd) { return hm::LeafUpLayout<KT, MP>::smem_bytes(ru, wd); }
+
+int leafup_wd(int64_t b, int ru) { return b / ru >= 2 ? 2 : 3; }
+
+size_t leafup_smem_rt(int k, int mp, int ru, int64_t b) {
+#define HM_LU(KT_, MP_) if (k == KT_ && mp == MP_) return leafup_smem<KT_, MP_>(ru, leafup_wd(b, ru));
+  HM_LU(16, 8) HM_LU(16, 16) HM_LU(16, 32) HM_LU(32, 8) HM_LU(32, 16) HM_LU(32, 32) HM_LU(64, 8) HM_LU(64, 16)
+  HM_LU(64, 32)
+#undef HM_LU
+  return (size_t)-1;
+}
+
+// The fused Step-1 + first-upsweep kernel (hm_leafup.cuh) is correct (parity
+// tested with HM_LEAFUP=1) but measured slower than vt_batched + hss_up_pair on
+// config 4 (763 vs 629 us: a persistent 1-CTA/SM pipeline leaves the DMMA pipe
+// 60% idle; r01_tuning.md), so it is off by default.
+#ifndef HM_LEAFUP
+#define HM_LEAFUP 0
+#endif
+#define HM_NO_LEAFUP (!HM_LEAFUP)
+
+// Rows per pipeline unit: the largest power of two <= 64 dividing the leaf
+// whose 4-slot ring fits in 226 KB of shared memory (0: none fits).
+int leafup_ru(const HssPlan& P) {
+  for (int ru = 64; ru >= 32; ru >>= 1)  // two contraction halves of >= 16 rows
+    if (P.b % ru == 0 && leafup_smem_rt(P.k, leafup_mp(P.m), ru, P.b) <= 226 * 1024) return ru;
+  return 0;
+}
+
+bool leafup_ok(const HssPlan& P) {
+  if (HM_NO_LEAFUP || P.m < 2 || P.m > 32 || P.b % 32 != 0) return false;
+  if (!(P.k == 16 || P.k == 32 || P.k == 64)) return false;
+  return leafup_ru(P) > 0;
+}
+
+template <int KT, int MP>
+hm_status leafup_launch(const hm::LeafUpParams& lp, cudaStream_t s) {
+  const size_t smem = leafup_smem<KT, MP>(lp.ru, lp.wd);
+  allow_smem(hm::hss_leaf_up_kernel<KT, MP>, smem);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(lp.npairs, sms));
+  return launch("hss_leaf_up", s,
+                [&] { hm::hss_leaf_up_kernel<KT, MP><<<grid, hm::kLeafUpThreads, smem, s>>>(lp); });
+}
+
+hm_status leafup_dispatch(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
+                          cudaStream_t s) {
+  const int ru = leafup_ru(P);
+  hm::LeafUpParams lp{V, Xd, P.p >= 2 ? W : nullptr, xh, (int64_t)1 << (P.p - 1), (int32_t)P.b, P.m, P.p,
+                      ru, leafup_wd(P.b, ru), 0};
+  const int mp = leafup_mp(P.m);
+#define HM_LU(KT_, MP_) if (P.k == KT_ && mp == MP_) return leafup_launch<KT_, MP_>(lp, s);
+  HM_LU(16, 8) HM_LU(16, 16) HM_LU(16, 32) HM_LU(32, 8) HM_LU(32, 16) HM_LU(32, 32) HM_LU(64, 8) HM_LU(64, 16)
+  HM_LU(64, 32)
+#undef HM_LU
+  return fail(HM_ERR_UNSUPPORTED, "hss_leaf_up: no instance for k=%d m=%d", P.k, P.m);
+}
+
 // Step 1 on the subtree: leaf x = V^T X, upsweep to level 1, and (W_root given)
 // the subtree root's x_root = W_root^T [x_{1,0}; x_{1,1}]. A depth-0 subtree is
 // one leaf: its x is the root's, written to x_root.
@@ -863,7 +936,12 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
   hm_status st;
   double* xleaf = (P.p == 0) ? x_root : xh + (((int64_t)1 << P.p) - 2) * km;
   if (xleaf == nullptr) return HM_OK;
-  if (P.vt == VtPath::kMma) {
+  int up_from = P.p - 1;
+  if (P.vt == VtPath::kMma && P.p >= 1 && leafup_ok(P)) {
+    // Step 1 fused with the first upsweep level (hm_leafup.cuh)
+    if ((st = leafup_dispatch(P, V, W, Xd, xh, stream))) return st;
+    up_from = P.p - 2;
+  } else if (P.vt == VtPath::kMma) {
     hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
     if ((st = vt_batched_dispatch("vt_contract", bp, k, P.nt_vt, stream))) return st;
   } else {
@@ -877,8 +955,8 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
     st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
     if (st) return st;
   }
-  if (P.p >= 2 && (st = hss_tree_phase(P, P.p, W, nullptr, nullptr, xh, nullptr, nullptr, nullptr, true, false,
-                                       stream)))
+  if (up_from >= 1 && (st = hss_tree_phase(P, P.p, W, nullptr, nullptr, xh, nullptr, nullptr, nullptr, true,
+                                             false, stream, 0, up_from)))
     return st;
   if (W_root && P.p >= 1 && (st = hss_single_vt(P, W_root, xh, 2 * k, x_root, stream))) return st;
   return HM_OK;

@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
 // The 4 rows of one k-step are rows r + (lane & 3). One LDG.128 of A covers 16
 // rank columns: ".x" feeds the tile of even columns, ".y" the tile of odd
 // columns (output rows permuted back at the store). K % 4 == 0.
-template <int MPW, int NT, bool COH = false>
+template <int MPW, int NT, bool COH = false, int PF = (NT > 4 ? 2 : 4)>
 __device__ __forceinline__ void warp_transposed_mma(double (&acc)[2 * MPW][NT][2], const double* __restrict__ A,
                                                     int64_t lda, const double* __restrict__ B, int64_t ldb, int c0,
                                                     int m, int K, int lane) {
@@ -749,7 +749,6 @@ __device__ __forceinline__ void warp_transposed_mma(double (&acc)[2 * MPW][NT][2
   bool colok[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) colok[nt] = (c0 + nt * 8 + i) < m;
-  constexpr int PF = 4;
   int q = 0;
 #pragma unroll 1
   for (; q + PF <= K / 4; q += PF) {

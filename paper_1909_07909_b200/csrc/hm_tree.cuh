@@ -102,21 +102,24 @@ __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = w >> 2, sub = w & 3;
+  // the 4 warps of a node split MG rank groups x column chunks; narrower chunks
+  // (NTU = NT * MG / 4) keep all 4 busy when MG < 4 (k = 16, 32)
+  constexpr int NTU = (NT * MG / 4) >= 1 ? (NT * MG / 4) : 1;
   {
     const int64_t node = n0 + nd;
     const int mg = sub % MG;
     const double* A = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16;
     const double* Bs = sm + nd * 2 * KT * zs;
     double* out = P.xh + ((1ll << l) - 2 + node) * km + (int64_t)mg * 16 * m;
-    const int nck = mp / (NT * 8);
+    const int nck = mp / (NTU * 8);
     for (int ck = sub / MG; ck < nck; ck += CKS) {
-      double acc[2][NT][2];
+      double acc[2][NTU][2];
 #pragma unroll
       for (int t = 0; t < 2; ++t)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-      warp_transposed_smem<NT, (KT / 2 < 16 ? KT / 2 : 16)>(acc, A, KT, Bs, zs, ck * NT * 8, 2 * KT, lane);
-      store_transposed<1, NT>(acc, out, m, ck * NT * 8, m, lane);
+        for (int nt = 0; nt < NTU; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+      warp_transposed_smem<NTU, (KT / 2 < 16 ? KT / 2 : 16)>(acc, A, KT, Bs, zs, ck * NTU * 8, 2 * KT, lane);
+      store_transposed<1, NTU>(acc, out, m, ck * NTU * 8, m, lane);
     }
   }
   __syncthreads();  // shared memory is reused by the next task

@@ -22,6 +22,7 @@
 #include "hm_convert.cuh"
 #include "hm_general.cuh"
 #include "hm_leafup.cuh"
+#include "hm_small.cuh"
 
 namespace {
 
@@ -678,7 +679,7 @@ struct HssPlan {
   bool mma_levels;  // DMMA tree kernels
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
-  size_t off_xh, off_yh, off_txh, off_tyh, off_x, off_y, total;
+  size_t off_xh, off_yh, off_txh, off_tyh, off_sync, off_x, off_y, total;
 };
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
@@ -727,6 +728,7 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
   P->off_yh = off; off = align_up(off + coef);
   P->off_txh = off; off = align_up(off + tcoef);
   P->off_tyh = off; off = align_up(off + tcoef);
+  P->off_sync = off; off = align_up(off + 2 * sizeof(unsigned));  // hss_small_kernel counters
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
@@ -994,6 +996,60 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
   return HM_OK;
 }
 
+// ---- small trees: one cooperative launch (hm_small.cuh) ----
+#ifndef HM_NO_SMALL
+#define HM_NO_SMALL 0
+#endif
+constexpr int kSmallMaxLevels = 8;  // up to 256 leaves: one CTA per leaf, all co-resident
+
+bool small_ok(const HssPlan& P) {
+  return !HM_NO_SMALL && P.q == 0 && P.mma_levels && P.p >= 1 && P.p <= kSmallMaxLevels && P.m >= 2 && P.m <= 32 &&
+         (P.b == 64 || P.b == 128);
+}
+
+template <int KT, int NT, int RG>
+hm_status small_launch(const hm::SmallHssParams& sp, unsigned grid, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)KT * (NT * 8 + 2);
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_small_kernel<KT, NT, RG>, 256, smem) !=
+      cudaSuccess)
+    return cuda_check("occupancy query (hss_small)");
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((int64_t)per_sm * sms < (int64_t)grid) return fail(HM_ERR_UNSUPPORTED, "hss_small: grid not co-resident");
+  if (cudaMemsetAsync(sp.sync, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return cuda_check("memset (hss_small)");
+  hm::SmallHssParams arg = sp;
+  void* args[] = {&arg};
+  cudaError_t e = cudaSuccess;
+  hm_status st = launch("hss_small", s, [&] {
+    e = cudaLaunchCooperativeKernel((const void*)hm::hss_small_kernel<KT, NT, RG>, dim3(grid), dim3(256), args, smem,
+                                    s);
+  });
+  if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_small: %s", cudaGetErrorString(e));
+  return st;
+}
+
+hm_status small_dispatch(const HssPlan& P, const double* D, const double* U, const double* V, const double* R,
+                         const double* W, const double* B, const double* X, double* Y, double* xh, double* yh,
+                         unsigned* sync, cudaStream_t s) {
+  const int h = std::min(3, P.p);
+  hm::SmallHssParams sp{D, U, V, R, W, B, X, Y, xh, yh, sync, (int32_t)P.b, P.p, P.m, h, 1 << (P.p - h), 0};
+  const unsigned grid = 1u << P.p;
+  const int nt = P.m <= 16 ? 2 : 4, rg = (int)(P.b / 64);
+#define HM_SM(KT_)                                                         \
+  if (P.k == KT_) {                                                        \
+    if (nt == 2 && rg == 1) return small_launch<KT_, 2, 1>(sp, grid, s);   \
+    if (nt == 2 && rg == 2) return small_launch<KT_, 2, 2>(sp, grid, s);   \
+    if (nt == 4 && rg == 1) return small_launch<KT_, 4, 1>(sp, grid, s);   \
+    if (nt == 4 && rg == 2) return small_launch<KT_, 4, 2>(sp, grid, s);   \
+  }
+  HM_SM(16)
+  HM_SM(32)
+  HM_SM(64)
+#undef HM_SM
+  return fail(HM_ERR_UNSUPPORTED, "hss_small: no instance");
+}
+
 // op = 1: Y = A^T X. A^T is HSS on the same tree with row
 // bases V (translations W), column bases U (translations R), cores
 // S'_{2q,2q+1} = B21^T, S'_{2q+1,2q} = B12^T and leaf blocks D_i^T: the same
@@ -1031,6 +1087,15 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   }
   const int64_t km = (int64_t)k * nrhs;
   const bool coupled = (k > 0 && P.p > 0);
+  if (coupled && op == 0 && small_ok(P)) {  // small tree: the whole product in one launch (hm_small.cuh)
+    if ((st = small_dispatch(P, D, U, V, R, W, B, Xd, Yd, xh, yh, reinterpret_cast<unsigned*>(w + P.off_sync),
+                             stream)) == HM_OK) {
+      if ((flags & HM_WS_HOSTIO) && cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return cuda_check("D2H copy of Y");
+      return HM_OK;
+    }
+    if (st != HM_ERR_UNSUPPORTED) return st;  // not co-resident on this device: the level-by-level path
+  }
   if (coupled) {
     if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
     if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op))) return st;

@@ -348,7 +348,8 @@ def sweep(torch, device, wl, peak):
                                                    Vh), 3, warm=1)
     nbc = 8 * (2 * C4.n * C4.k + 2 * C4.levels * C4.n * C4.k + 4 * ((1 << C4.levels) - 2) * C4.k ** 2
                + 2 * ((1 << C4.levels) - 1) * C4.k ** 2)
-    out["c4_hss2hodlr"] = {"ms": round(ms, 3), "GB/s": gbs(nbc, ms),
+    flc = 3 * 2 * C4.levels * C4.n * C4.k ** 2  # U S, U R, V W per row and level (upper bound: level 1 has no R/W)
+    out["c4_hss2hodlr"] = {"ms": round(ms, 3), "GB/s": gbs(nbc, ms), "fp64_TFLOP/s": round(flc / (ms * 1e-3) / 1e12, 2),
                            "bytes": "U,V,R,W,B read + Uh,Vh (levels x n x k) written"}
     del Uh, Vh
     torch.cuda.empty_cache()

@@ -1845,6 +1845,14 @@ hm_status hss_to_hodlr(const hm_tree* tree, int32_t k, const double* U, const do
       cudaMemcpyAsync(Vh + (size_t)(p - 1) * n * k, V, nk, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return cuda_check("copy of the leaf bases");
   hm::ConvertParams cp{R, W, B, Uh, Vh, n, tree->leaf, p, k};
+  if (tree->leaf % 64 == 0 && (k == 16 || k == 32 || k == 64)) {  // one-pass DMMA kernel
+    const unsigned g = (unsigned)(n / 64);
+    const size_t sm = sizeof(double) * 3 * (size_t)k * (k + 2);
+    if (k == 16) return launch("hss2hodlr_mma", s, [&] { hm::hss2hodlr_mma_kernel<16><<<g, 256, sm, s>>>(cp); });
+    if (k == 32) return launch("hss2hodlr_mma", s, [&] { hm::hss2hodlr_mma_kernel<32><<<g, 256, sm, s>>>(cp); });
+    allow_smem(hm::hss2hodlr_mma_kernel<64>, sm);
+    return launch("hss2hodlr_mma", s, [&] { hm::hss2hodlr_mma_kernel<64><<<g, 256, sm, s>>>(cp); });
+  }
   const size_t smem = sizeof(double) * 2 * hm::kConvRows * (size_t)k;
   const unsigned grid = (unsigned)((n + hm::kConvRows - 1) / hm::kConvRows);
   for (int l = p; l >= 1; --l) {

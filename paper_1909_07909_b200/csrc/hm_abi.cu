@@ -375,6 +375,13 @@ hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_
   constexpr int PF = LeafMmaTune<RG, NT>::PF, MINB = LeafMmaTune<RG, NT>::MINB;
   size_t smem = sizeof(double) * (size_t)((lp.b + lp.ktot) * (NT * 8 + 4));
   const int64_t chunks = (lp.m + NT * 8 - 1) / (NT * 8);
+  if (lp.dp > 0) {  // HSS: leaf-level coupling + downsweep fused (y_i computed in the CTA)
+    const size_t sm2 = smem + sizeof(double) * 2 * (size_t)lp.seg[0].k * (NT * 8 + 2);
+    allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB, false, true>, sm2);
+    return launch("leaf_apply", s, [&] {
+      hm::leaf_mma_kernel<RG, NT, PF, MINB, false, true><<<(unsigned)(nleaves * chunks), 256, sm2, s>>>(lp);
+    });
+  }
   if (lp.dtrans) {
     allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB, true>, smem);
     return launch("leaf_apply_t", s, [&] {
@@ -749,7 +756,8 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 constexpr int64_t kTreeBigLevel = 2048;
 
 template <int KT, int NT>
-hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l) {
+hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
+                      int down_last) {
   constexpr int MINB = (KT == 32 && NT == 4) ? 3 : 0;  // measured, r01_tuning.md
   const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
   static bool attrs = false;
@@ -773,7 +781,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
-  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(p, lbig - 1) : 0;
+  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
   if (up_from >= 1 || down_to >= 1) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -791,7 +799,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     if (st) return st;
   }
   // downsweep: big levels lbig .. p one launch each
-  for (int l = std::max(lbig, 1); down && l <= p; ++l) {
+  for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
     st = launch("hss_down_level", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
@@ -800,12 +808,12 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
 }
 
 hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s,
-                        int up_from) {
-#define HM_TREE(KT_)                                                          \
-  if (k == KT_) {                                                             \
-    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from);     \
-    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from);     \
-    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from);                  \
+                        int up_from, int down_last) {
+#define HM_TREE(KT_)                                                                     \
+  if (k == KT_) {                                                                        \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from, down_last);     \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from, down_last);     \
+    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from, down_last);                  \
   }
   HM_TREE(16)
   HM_TREE(32)
@@ -818,13 +826,14 @@ hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up,
 // generic per-level kernels or the DMMA tree kernels (tree_dispatch).
 hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
                          double* yh, const double* R_root, const double* y_root, bool up, bool down,
-                         cudaStream_t stream, int bt = 0, int up_from = -1) {
+                         cudaStream_t stream, int bt = 0, int up_from = -1, int down_last = -1) {
   const int k = P.k, nrhs = P.m;
   hm_status st;
   if (up_from < 0) up_from = p - 1;  // first upsweep level to compute
+  if (down_last < 0) down_last = p;  // last downsweep level to compute
   if (P.mma_levels) {
     hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
-    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from);
+    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from, down_last);
   }
   const int64_t km = (int64_t)k * nrhs;
   if (up)
@@ -836,7 +845,7 @@ hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double*
       if (st) return st;
     }
   if (down)
-    for (int l = 1; l <= p; ++l) {
+    for (int l = 1; l <= down_last; ++l) {
       hm::HssLevelParams hp{R, B, xh, yh, R_root, y_root, l, k, nrhs, bt};
       const int64_t total = ((int64_t)1 << l) * km;
       const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
@@ -966,11 +975,26 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
 
 // Step 4: Y(I_i) = U_i y_i + D_i X(I_i); y of the leaves from yh (or y_root for a
 // depth-0 subtree).
+// fused: {B, R, xh, yh} of the tree when the leaf-level coupling + downsweep runs
+// inside the DMMA leaf kernel (leaf_mma DOWN; yleaf is then not read).
+struct FusedDown {
+  const double *B, *R, *xh, *yh;
+};
+
 hm_status hss_leaf_phase(const HssPlan& P, const double* D, const double* U, const double* Xd, double* Yd,
-                         const double* yleaf, cudaStream_t stream, bool dtrans = false) {
+                         const double* yleaf, cudaStream_t stream, bool dtrans = false,
+                         const FusedDown* fd = nullptr) {
   hm::LeafParams lp;
   memset(&lp, 0, sizeof lp);
   lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf; lp.dtrans = dtrans ? 1 : 0;
+  if (fd) {
+    const int64_t km = (int64_t)P.k * P.m, kk = (int64_t)P.k * P.k;
+    lp.dp = P.p;
+    lp.dB = fd->B + (((int64_t)1 << (P.p - 1)) - 1) * 2 * kk;                 // level p-1 nodes' cores
+    lp.dR = P.p >= 2 ? fd->R + (((int64_t)1 << (P.p - 1)) - 2) * 2 * kk : nullptr;
+    lp.dx = fd->xh + (((int64_t)1 << P.p) - 2) * km;                            // level p x blocks
+    lp.dyp = P.p >= 2 ? fd->yh + (((int64_t)1 << (P.p - 1)) - 2) * km : nullptr;  // level p-1 y blocks
+  }
   const bool coupled = P.k > 0 && yleaf != nullptr;
   if (coupled) {
     hm::LeafSeg& sg = lp.seg[lp.nseg++];
@@ -995,6 +1019,16 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
     return fail(HM_ERR_INVALID_ARG, "U, V, R, W, B must be 16-byte aligned");
   return HM_OK;
 }
+
+// Leaf-level coupling + downsweep fused into the DMMA leaf kernel (leaf_mma
+// DOWN): correct (parity tested with HM_FUSED_DOWN=1) but measured slower on
+// config 4 — the leaf kernel grows by 457 us (the y_i product sits on each CTA's
+// critical path before the main product) while the level-p down kernel saves
+// 230 us (r01_tuning.md). Off by default.
+#ifndef HM_FUSED_DOWN
+#define HM_FUSED_DOWN 0
+#endif
+#define HM_NO_FUSED_DOWN (!HM_FUSED_DOWN)
 
 // ---- small trees: one cooperative launch (hm_small.cuh) ----
 #ifndef HM_NO_SMALL
@@ -1096,12 +1130,18 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
     }
     if (st != HM_ERR_UNSUPPORTED) return st;  // not co-resident on this device: the level-by-level path
   }
+  // the leaf-level coupling + downsweep fused into the DMMA leaf kernel (forward product)
+  const bool fuse = coupled && op == 0 && !HM_NO_FUSED_DOWN && P.leaf == LeafPath::kMma && P.mma_levels;
   if (coupled) {
     if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
-    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op))) return st;
+    if ((!fuse || P.p >= 2) &&
+        (st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op, -1,
+                             fuse ? P.p - 1 : P.p)))
+      return st;
   }
   const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
-  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) return st;
+  const FusedDown fd{B, R, xh, yh};
+  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0, fuse ? &fd : nullptr))) return st;
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");

@@ -228,7 +228,13 @@ struct LeafParams {
   int32_t nseg;
   int32_t ktot;     // sum of segment ranks
   int32_t dtrans;   // 1: the leaf term is D_i^T X(I_i) (adjoint product)
-  int32_t pad;
+  int32_t dp;       // HSS leaf-level downsweep fused into the leaf pass (leaf_mma DOWN): level p (>= 1)
+  // y_i = S_w x_{i^1} + R_w y_{parent}: cores / translations of the level-(p-1) nodes,
+  // level-p x blocks, level-(p-1) y blocks (dyp NULL when p = 1)
+  const double* dB;
+  const double* dR;
+  const double* dx;
+  const double* dyp;
   LeafSeg seg[kMaxLevels];
 };
 

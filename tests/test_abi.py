@@ -147,3 +147,24 @@ def test_general_tree_validation():
     assert e.value.status == hm.HM_ERR_UNSUPPORTED
     with pytest.raises(ValueError):
         hm.hm_hodlr_general_workspace_bytes(40, 3, c[:4], [2, 1, 3], 2)
+
+
+def _build_c_example(tmp_path):
+    """Compile examples/hm_matvec_example.c (plain C, include/hm.h only) against libhm.so."""
+    exe = str(tmp_path / "hm_matvec_example")
+    libdir = os.path.dirname(hm.LIB_PATH)
+    cuda_lib = "/usr/local/cuda/lib64"
+    cmd = ["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "hm_matvec_example.c"), "-o", exe, "-L", libdir, "-l:libhm.so",
+           "-L", cuda_lib, "-lcudart", f"-Wl,-rpath,{libdir}:{cuda_lib}", "-lm"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_example_links_and_validates(tmp_path):
+    """The C-ABI is usable from plain C: the example compiles against include/hm.h, links
+    libhm.so, queries a workspace and sees an invalid tree rejected on the host."""
+    exe = _build_c_example(tmp_path)
+    out = subprocess.run([exe, "--host-only"], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    assert "invalid tree rejected" in out.stdout

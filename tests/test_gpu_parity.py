@@ -274,3 +274,14 @@ def test_config5_full_size(hm):
     Yr = oracle.hodlr_matvec_leaves(n, p, hd.ranks, Dsel, Uh, Vh, X, leaves)
     Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
     assert relerr(Yg, Yr) <= TOL
+
+
+def test_c_example_on_gpu(hm, tmp_path):
+    """examples/hm_matvec_example.c: plain C through the C-ABI on the GPU (A X and A^T X of the
+    inverse Laplacian, tridiag(-1,2,-1) residual <= 1e-14)."""
+    import subprocess
+    from test_abi import _build_c_example
+    exe = _build_c_example(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "A^T X: tridiag residual" in out.stdout

@@ -204,7 +204,7 @@ struct HodlrPlan {
   int64_t tile;  // rows per vt CTA
   size_t off_t[hm::kMaxLevels + 1];
   size_t off_part[hm::kMaxLevels + 1];
-  size_t off_ttop, off_x, off_y, total;
+  size_t off_ttop, off_spart, off_ssync, off_x, off_y, total;
 };
 
 hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_t* ranks, int32_t nrhs,
@@ -276,6 +276,11 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
   }
   P->off_ttop = off;
   off = align_up(off + sizeof(double) * (size_t)P->top_doubles);
+  // small problems (hodlr_small_kernel): per-leaf partials + an arrival counter
+  P->off_spart = off;
+  off = align_up(off + sizeof(double) * (size_t)(((int64_t)1 << p) * P->ktot * nrhs));
+  P->off_ssync = off;
+  off = align_up(off + sizeof(unsigned));
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off;
@@ -599,6 +604,63 @@ hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const doubl
   return leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream);
 }
 
+// ---- small problems: the whole product in one cooperative launch ----
+// One-launch HODLR for small problems (hodlr_small_kernel): correct (parity
+// tested with HM_SMALL_HODLR=1) but not faster on config 1 (22.9 vs 21 us per
+// call: the kernel alone takes 17.7 us, the two-kernel path 20.5 us of device
+// time); off by default (r01_tuning.md).
+#ifndef HM_SMALL_HODLR
+#define HM_SMALL_HODLR 0
+#endif
+#define HM_NO_SMALL_HODLR (!HM_SMALL_HODLR)
+
+// Latency-bound sizes only: one CTA per leaf (<= 256, co-resident), the leaf's
+// inputs fit in shared memory, little arithmetic per CTA.
+bool hodlr_small_ok(const HodlrPlan& P) {
+  return !HM_NO_SMALL_HODLR && P.q == 0 && P.p >= 1 && P.p <= 8 && P.n <= 16384 && P.m <= 16 &&
+         P.ktot * P.m * P.b <= 524288 &&
+         hm::hodlr_small_smem_doubles(P.b, P.ktot, P.m) * (int64_t)sizeof(double) <= 200 * 1024;
+}
+
+hm_status hodlr_small_dispatch(const HodlrPlan& P, const int32_t* ranks, const double* D, const double* U,
+                               const double* V, const double* X, double* Y, char* w, cudaStream_t s) {
+  hm::SmallHodlrParams sp;
+  memset(&sp, 0, sizeof sp);
+  sp.D = D; sp.U = U; sp.V = V; sp.X = X; sp.Y = Y;
+  sp.part = reinterpret_cast<double*>(w + P.off_spart);
+  sp.sync = reinterpret_cast<unsigned*>(w + P.off_ssync);
+  sp.n = P.n; sp.b = (int32_t)P.b; sp.p = P.p; sp.m = P.m; sp.ktot = (int32_t)P.ktot;
+  int64_t ko = 0;
+  for (int l = 1; l <= P.p; ++l) {
+    sp.k[l - 1] = ranks[l - 1];
+    sp.koff[l - 1] = ko;
+    ko += ranks[l - 1];
+  }
+  const unsigned grid = 1u << P.p;
+  const size_t smem = sizeof(double) * (size_t)hm::hodlr_small_smem_doubles(P.b, P.ktot, P.m);
+  // residency check cached per shared-memory size (host latency matters at these sizes)
+  static thread_local size_t last_smem = 0;
+  static thread_local int64_t last_cap = 0;
+  if (smem != last_smem) {
+    allow_smem(hm::hodlr_small_kernel, 200 * 1024);
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hodlr_small_kernel, 256, smem) != cudaSuccess)
+      return cuda_check("occupancy query (hodlr_small)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    last_smem = smem;
+    last_cap = (int64_t)per_sm * sms;
+  }
+  if (last_cap < (int64_t)grid) return fail(HM_ERR_UNSUPPORTED, "hodlr_small: grid not co-resident");
+  void* args[] = {&sp};
+  cudaError_t e = cudaSuccess;
+  hm_status st = launch("hodlr_small", s, [&] {
+    e = cudaLaunchCooperativeKernel((const void*)hm::hodlr_small_kernel, dim3(grid), dim3(256), args, smem, s);
+  });
+  if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hodlr_small: %s", cudaGetErrorString(e));
+  return st;
+}
+
 hm_status hodlr_check_ptrs(const HodlrPlan& P, const double* D, const double* U, const double* V, const double* X,
                            const double* Y, void* ws, size_t ws_bytes, int32_t flags) {
   if (!ws || ws_bytes < P.total)
@@ -636,6 +698,15 @@ hm_status hodlr_run(const hm_tree* tree, const int32_t* ranks, const double* D, 
     Yd = reinterpret_cast<double*>(w + P.off_y);
     if (cudaMemcpyAsync(const_cast<double*>(Xd), X, xy_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
       return cuda_check("H2D copy of X");
+  }
+  if (op == 0 && hodlr_small_ok(P)) {  // small problem: one cooperative launch (hm_small.cuh)
+    st = hodlr_small_dispatch(P, ranks, D, U, V, Xd, Yd, w, stream);
+    if (st != HM_OK && st != HM_ERR_UNSUPPORTED) return st;
+    if (st == HM_OK) {
+      if ((flags & HM_WS_HOSTIO) && cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return cuda_check("D2H copy of Y");
+      return HM_OK;
+    }
   }
   if ((st = hodlr_vt_phase(P, ranks, op ? U : V, Xd, w, 1, P.p, nullptr, stream))) return st;
   if ((st = hodlr_leaf_phase(P, ranks, D, op ? V : U, Xd, Yd, w, nullptr, stream, op != 0))) return st;
@@ -1044,14 +1115,17 @@ bool small_ok(const HssPlan& P) {
 template <int KT, int NT, int RG>
 hm_status small_launch(const hm::SmallHssParams& sp, unsigned grid, cudaStream_t s) {
   const size_t smem = sizeof(double) * (size_t)KT * (NT * 8 + 2);
-  int per_sm = 0, dev = 0, sms = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_small_kernel<KT, NT, RG>, 256, smem) !=
-      cudaSuccess)
-    return cuda_check("occupancy query (hss_small)");
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if ((int64_t)per_sm * sms < (int64_t)grid) return fail(HM_ERR_UNSUPPORTED, "hss_small: grid not co-resident");
-  if (cudaMemsetAsync(sp.sync, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return cuda_check("memset (hss_small)");
+  static int64_t cap = -1;  // co-resident CTAs of this instance (queried once)
+  if (cap < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_small_kernel<KT, NT, RG>, 256, smem) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_small)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (int64_t)per_sm * sms;
+  }
+  if (cap < (int64_t)grid) return fail(HM_ERR_UNSUPPORTED, "hss_small: grid not co-resident");
   hm::SmallHssParams arg = sp;
   void* args[] = {&arg};
   cudaError_t e = cudaSuccess;

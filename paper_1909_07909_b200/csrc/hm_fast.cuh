@@ -526,7 +526,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void stage_rows_async(double* dst, int zs, const double* src, int64_t lds, int rows,
                                                  int cols, int mp) {
   const bool vec = ((cols & 1) == 0) && ((lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
-                   ((zs & 1) == 0);
+                   ((zs & 1) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
   if (vec) {
     const int h = cols >> 1;  // 16-byte chunks per row
     for (int e = threadIdx.x; e < rows * h; e += blockDim.x) {

@@ -175,15 +175,22 @@ class Workload:
                                dtype=torch.uint8, device=device)
         self.ws4 = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4), dtype=torch.uint8,
                                device=device)
-        # end-to-end: pinned host X / Y, library copies through its own workspace
-        self.X5h = self.X5.cpu().pin_memory()
-        self.Y5h = torch.empty_like(self.X5h).pin_memory()
-        self.X4h = self.X4.cpu().pin_memory()
-        self.Y4h = torch.empty_like(self.X4h).pin_memory()
-        self.ws5io = torch.empty(hm.hm_hodlr_workspace_bytes(C5.n, C5.levels, C5.leaf, self.h5.ranks, M5,
-                                                             hm.HM_WS_HOSTIO), dtype=torch.uint8, device=device)
-        self.ws4io = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4, hm.HM_WS_HOSTIO),
-                                 dtype=torch.uint8, device=device)
+        # end-to-end: pinned host X / Y, the library copies them through its own
+        # workspace. Three lanes (stream + workspaces + host buffers) so that step
+        # i+1's host-to-device copies overlap step i's kernels and device-to-host
+        # copies (separate copy engines) — every step still moves its own X in
+        # and its own Y out.
+        self.lanes = []
+        for _ in range(int(os.environ.get("HM_E2E_LANES", "3"))):
+            ln = {"stream": torch.cuda.Stream(device=device),
+                  "X5h": self.X5.cpu().pin_memory(), "X4h": self.X4.cpu().pin_memory()}
+            ln["Y5h"] = torch.empty_like(ln["X5h"]).pin_memory()
+            ln["Y4h"] = torch.empty_like(ln["X4h"]).pin_memory()
+            ln["ws5"] = torch.empty(hm.hm_hodlr_workspace_bytes(C5.n, C5.levels, C5.leaf, self.h5.ranks, M5,
+                                                                hm.HM_WS_HOSTIO), dtype=torch.uint8, device=device)
+            ln["ws4"] = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4, hm.HM_WS_HOSTIO),
+                                    dtype=torch.uint8, device=device)
+            self.lanes.append(ln)
         self.launches = 0
 
     def step(self):
@@ -193,11 +200,23 @@ class Workload:
         hm.hss_matvec(C4.n, C4.levels, C4.leaf, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, self.X4, self.Y4, self.ws4)
         self.launches += hm.last_launch_count()
 
-    def step_e2e(self):
+    def step_e2e(self, i=0):
         hm, h, s = self.hm, self.h5, self.s4
-        hm.hodlr_matvec_hostio(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, self.X5h, self.Y5h, self.ws5io)
-        hm.hss_matvec_hostio(C4.n, C4.levels, C4.leaf, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, self.X4h, self.Y4h,
-                             self.ws4io)
+        ln = self.lanes[i % len(self.lanes)]
+        st = ln["stream"]
+        hm.hodlr_matvec_hostio(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, ln["X5h"], ln["Y5h"], ln["ws5"],
+                               stream=st)
+        hm.hss_matvec_hostio(C4.n, C4.levels, C4.leaf, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, ln["X4h"], ln["Y4h"],
+                             ln["ws4"], stream=st)
+
+    def e2e_begin(self, ev):
+        for ln in self.lanes:
+            ln["stream"].wait_event(ev)
+
+    def e2e_end(self, torch):
+        cur = torch.cuda.current_stream()
+        for ln in self.lanes:
+            cur.wait_stream(ln["stream"])
 
     def h2d_d2h_bytes(self):
         return 8 * (C5.n * M5 + C4.n * M4), 8 * (C5.n * M5 + C4.n * M4)
@@ -254,7 +273,13 @@ class DistWorkload:
                              ws=self.ws5)
         hd.hss_matvec_dist(C4.n, C4.levels, C4.leaf, C4.k, self.sh4, self.X4, self.Y4, ws=self.ws4)
 
-    def step_e2e(self):
+    def e2e_begin(self, ev):
+        pass
+
+    def e2e_end(self, torch):
+        pass
+
+    def step_e2e(self, i=0):
         self.X5.copy_(self.X5h, non_blocking=True)
         self.X4.copy_(self.X4h, non_blocking=True)
         self.step()
@@ -427,16 +452,18 @@ def run_ours(args):
     launches = len(trace)  # every traced record is one of libhm's kernel launches in the timed region
 
     # end-to-end (host X in, host Y out through the C-ABI hostio calls)
-    for _ in range(2):
-        wl.step_e2e()
+    for i in range(2):
+        wl.step_e2e(i)
     torch.cuda.synchronize()
     e2 = max(3, args.steps // 5)
     if world > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(e2):
-        wl.step_e2e()
+    wl.e2e_begin(f0)
+    for i in range(e2):
+        wl.step_e2e(i)
+    wl.e2e_end(torch)
     f1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = f0.elapsed_time(f1)
@@ -512,7 +539,8 @@ def run_ours(args):
                     for k_, v in sorted(per.items())},
         "e2e": {"value": round(step_bytes() * e2 * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "hodlr_matvec_hostio + hss_matvec_hostio: pinned host X in, host Y out, every step"},
+                "note": "hodlr_matvec_hostio + hss_matvec_hostio: pinned host X in, host Y out, every step; "
+                        "consecutive steps rotate over 3 streams so copies overlap kernels"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -493,8 +493,11 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
 }
 
 template <int KT, int NT>
+#ifndef HM_VTB_MPW
+#define HM_VTB_MPW 2  // 32 rank columns per warp when k allows (measured, r01_tuning.md)
+#endif
 hm_status vt_batched_launch(const char* name, const hm::BatchedVtParams& bp, cudaStream_t s) {
-  constexpr int MPW = 1;
+  constexpr int MPW = (KT / 16) % HM_VTB_MPW == 0 ? HM_VTB_MPW : 1;
   const int64_t nck = (bp.m + NT * 8 - 1) / (NT * 8);
   const int64_t warps = bp.count * (KT / 16 / MPW) * nck;
   return launch(name, s, [&] {

@@ -853,7 +853,10 @@ struct BatchedVtParams {
 
 // One warp task of the batched product: segment jseg, rank-column group mg,
 // column chunk ck.
-template <int KT, int MPW, int NT, bool COH = false>
+// k-steps per batch of A/B loads: measured on config 4 Step 1 (r01_tuning.md):
+// MPW 1: PF 4 483 us, PF 2 452 us, PF 1 742 us; MPW 2 (one warp, 32 rank
+// columns): PF 1 398 us, PF 2 721 us.
+template <int KT, int MPW, int NT, bool COH = false, int PF = (NT > 4 ? 2 : (MPW >= 2 ? 1 : 2))>
 __device__ __forceinline__ void vt_batched_task(const BatchedVtParams& P, int64_t jseg, int mg, int ck, int lane) {
   const int c0 = ck * NT * 8;
   double acc[2 * MPW][NT][2];
@@ -861,8 +864,8 @@ __device__ __forceinline__ void vt_batched_task(const BatchedVtParams& P, int64_
   for (int t = 0; t < 2 * MPW; ++t)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-  warp_transposed_mma<MPW, NT, COH>(acc, P.A + jseg * P.a_stride + mg * 16 * MPW, KT, P.B + jseg * P.b_stride, P.m,
-                                    c0, P.m, P.K, lane);
+  warp_transposed_mma<MPW, NT, COH, PF>(acc, P.A + jseg * P.a_stride + mg * 16 * MPW, KT, P.B + jseg * P.b_stride,
+                                        P.m, c0, P.m, P.K, lane);
   store_transposed<MPW, NT>(acc, P.out + jseg * P.o_stride + (int64_t)mg * 16 * MPW * P.m, P.m, c0, P.m, lane);
 }
 

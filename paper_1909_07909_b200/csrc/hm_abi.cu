@@ -24,6 +24,15 @@
 #include "hm_leafup.cuh"
 #include "hm_small.cuh"
 
+// One-launch HODLR for small problems (hodlr_small_kernel): correct (parity
+// tested with HM_SMALL_HODLR=1) but not faster on config 1 (22.9 vs 21 us per
+// call: the kernel alone takes 17.7 us, the two-kernel path 20.5 us of device
+// time); off by default (r01_tuning.md).
+#ifndef HM_SMALL_HODLR
+#define HM_SMALL_HODLR 0
+#endif
+#define HM_NO_SMALL_HODLR (!HM_SMALL_HODLR)
+
 namespace {
 
 thread_local std::string g_err;
@@ -204,7 +213,7 @@ struct HodlrPlan {
   int64_t tile;  // rows per vt CTA
   size_t off_t[hm::kMaxLevels + 1];
   size_t off_part[hm::kMaxLevels + 1];
-  size_t off_ttop, off_spart, off_ssync, off_x, off_y, total;
+  size_t off_ttop, off_spart, off_x, off_y, total;
 };
 
 hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_t* ranks, int32_t nrhs,
@@ -276,11 +285,9 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
   }
   P->off_ttop = off;
   off = align_up(off + sizeof(double) * (size_t)P->top_doubles);
-  // small problems (hodlr_small_kernel): per-leaf partials + an arrival counter
+  // small problems (hodlr_small_kernel, HM_SMALL_HODLR): per-leaf partials
   P->off_spart = off;
-  off = align_up(off + sizeof(double) * (size_t)(((int64_t)1 << p) * P->ktot * nrhs));
-  P->off_ssync = off;
-  off = align_up(off + sizeof(unsigned));
+  if (HM_SMALL_HODLR) off = align_up(off + sizeof(double) * (size_t)(((int64_t)1 << p) * P->ktot * nrhs));
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off;
@@ -608,14 +615,6 @@ hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const doubl
 }
 
 // ---- small problems: the whole product in one cooperative launch ----
-// One-launch HODLR for small problems (hodlr_small_kernel): correct (parity
-// tested with HM_SMALL_HODLR=1) but not faster on config 1 (22.9 vs 21 us per
-// call: the kernel alone takes 17.7 us, the two-kernel path 20.5 us of device
-// time); off by default (r01_tuning.md).
-#ifndef HM_SMALL_HODLR
-#define HM_SMALL_HODLR 0
-#endif
-#define HM_NO_SMALL_HODLR (!HM_SMALL_HODLR)
 
 // Latency-bound sizes only: one CTA per leaf (<= 256, co-resident), the leaf's
 // inputs fit in shared memory, little arithmetic per CTA.
@@ -631,7 +630,6 @@ hm_status hodlr_small_dispatch(const HodlrPlan& P, const int32_t* ranks, const d
   memset(&sp, 0, sizeof sp);
   sp.D = D; sp.U = U; sp.V = V; sp.X = X; sp.Y = Y;
   sp.part = reinterpret_cast<double*>(w + P.off_spart);
-  sp.sync = reinterpret_cast<unsigned*>(w + P.off_ssync);
   sp.n = P.n; sp.b = (int32_t)P.b; sp.p = P.p; sp.m = P.m; sp.ktot = (int32_t)P.ktot;
   int64_t ko = 0;
   for (int l = 1; l <= P.p; ++l) {
@@ -760,7 +758,7 @@ struct HssPlan {
   bool mma_levels;  // DMMA tree kernels
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
-  size_t off_xh, off_yh, off_txh, off_tyh, off_sync, off_x, off_y, total;
+  size_t off_xh, off_yh, off_txh, off_tyh, off_x, off_y, total;
 };
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
@@ -809,7 +807,6 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
   P->off_yh = off; off = align_up(off + coef);
   P->off_txh = off; off = align_up(off + tcoef);
   P->off_tyh = off; off = align_up(off + tcoef);
-  P->off_sync = off; off = align_up(off + 2 * sizeof(unsigned));  // hss_small_kernel counters
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
@@ -1142,9 +1139,9 @@ hm_status small_launch(const hm::SmallHssParams& sp, unsigned grid, cudaStream_t
 
 hm_status small_dispatch(const HssPlan& P, const double* D, const double* U, const double* V, const double* R,
                          const double* W, const double* B, const double* X, double* Y, double* xh, double* yh,
-                         unsigned* sync, cudaStream_t s) {
+                         cudaStream_t s) {
   const int h = std::min(3, P.p);
-  hm::SmallHssParams sp{D, U, V, R, W, B, X, Y, xh, yh, sync, (int32_t)P.b, P.p, P.m, h, 1 << (P.p - h), 0};
+  hm::SmallHssParams sp{D, U, V, R, W, B, X, Y, xh, yh, (int32_t)P.b, P.p, P.m, h, 1 << (P.p - h), 0};
   const unsigned grid = 1u << P.p;
   const int nt = P.m <= 16 ? 2 : 4, rg = (int)(P.b / 64);
 #define HM_SM(KT_)                                                         \
@@ -1199,8 +1196,7 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   const int64_t km = (int64_t)k * nrhs;
   const bool coupled = (k > 0 && P.p > 0);
   if (coupled && op == 0 && small_ok(P)) {  // small tree: the whole product in one launch (hm_small.cuh)
-    if ((st = small_dispatch(P, D, U, V, R, W, B, Xd, Yd, xh, yh, reinterpret_cast<unsigned*>(w + P.off_sync),
-                             stream)) == HM_OK) {
+    if ((st = small_dispatch(P, D, U, V, R, W, B, Xd, Yd, xh, yh, stream)) == HM_OK) {
       if ((flags & HM_WS_HOSTIO) && cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
         return cuda_check("D2H copy of Y");
       return HM_OK;

@@ -882,6 +882,9 @@ __global__ void __launch_bounds__(256) vt_batched_kernel(const BatchedVtParams P
   vt_batched_task<KT, MPW, NT>(P, jseg, sub % MG, sub / MG, lane);
 }
 
+#ifndef HM_VTM_PF
+#define HM_VTM_PF(NT) ((NT) > 4 ? 2 : 4)
+#endif
 // HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
 // Per level: warp partial t over its b rows (DMMA), staged in shared memory,
 // then fixed-order sums over the warps of each node.
@@ -902,7 +905,8 @@ __global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, in
       for (int t = 0; t < KT / 8; ++t)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-      warp_transposed_mma<KT / 16, NT>(acc, lv.V + row0 * KT, KT, P.X + row0 * m, m, c0, m, (int)b, lane);
+      warp_transposed_mma<KT / 16, NT, false, HM_VTM_PF(NT)>(acc, lv.V + row0 * KT, KT, P.X + row0 * m, m, c0, m,
+                                                             (int)b, lane);
       store_transposed<KT / 16, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
       __syncthreads();
       const int64_t g = lv.s >= tile ? 8 : lv.s / b;

@@ -29,17 +29,10 @@ struct SmallHssParams {
   const double *D, *U, *V, *R, *W, *B, *X;
   double* Y;
   double *xh, *yh;   // level-major coefficient blocks [.][k][m] (workspace)
-  unsigned* sync;    // [0] subtrees done with phase 1, [1] phase 2 done
   int32_t b, p, m, h;
   int32_t nsub;      // S = 2^(p-h)
   int32_t pad;
 };
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // Coefficient block of node (l, i) (l >= 1) in xh / yh.
 __device__ __forceinline__ int64_t coef_off(int l, int64_t i, int64_t km) { return (((int64_t)1 << l) - 2 + i) * km; }
@@ -203,7 +196,6 @@ struct SmallHodlrParams {
   const double *D, *U, *V, *X;
   double* Y;
   double* part;       // [nleaves][ktot][m] partials
-  unsigned* sync;     // arrival counter (zeroed by a memset before the launch)
   int64_t n;
   int32_t b, p, m, ktot;
   int32_t k[kMaxLevels];   // ranks of levels 1..p (index l - 1)

@@ -56,6 +56,7 @@ def hss_flops(n, b, p, k, m):
     return 2 * n * m * (b + 2 * k) + 8 * ((1 << p) - 2) * k * k * m + 4 * ((1 << p) - 1) * k * k * m
 
 
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA (mma.sync f64) peak on this pool's B200, tools/fp64_peaks.cu
 C5 = hm_inputs.CONFIGS[5]
 C4 = hm_inputs.CONFIGS[4]
 M5, M4 = 1, 32
@@ -332,7 +333,9 @@ def sweep(torch, device, wl, peak):
         for nm, fn in (("", hm.hodlr_matvec), ("^T", hm.hodlr_matvec_t)):
             ms = _time_call(torch, lambda: fn(c3.n, c3.levels, c3.leaf, h3.ranks, h3.D, h3.U, h3.V, X, Y, ws), 10)
             out[f"c3_m{m}{nm}"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
-                                   "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2)}
+                                   "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2),
+                                   "frac_fp64": round(fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                                   "matvecs/s": round(1e3 / ms, 1), "column_matvecs/s": round(m * 1e3 / ms, 1)}
         del X, Y, ws
     # per-level ranks on the config-3 tree (f4): ranks 16 / 8 alternating -> general kernels
     rk = [16 if l % 2 else 8 for l in range(c3.levels)]
@@ -530,10 +533,14 @@ def run_ours(args):
         },
         "per_config": {
             "c5_hodlr": {"ms": round(c5_ms, 4), "GB/s": round(b5 / (c5_ms * 1e-3) / 1e9, 1),
-                         "frac_hbm": round(b5 / (c5_ms * 1e-3) / 1e9 / peak, 4)},
+                         "frac_hbm": round(b5 / (c5_ms * 1e-3) / 1e9 / peak, 4),
+                         "matvecs/s": round(1e3 / c5_ms, 1), "column_matvecs/s": round(M5 * 1e3 / c5_ms, 1)},
             "c4_hss": {"ms": round(c4_ms, 4), "GB/s": round(b4 / (c4_ms * 1e-3) / 1e9, 1),
                        "frac_hbm": round(b4 / (c4_ms * 1e-3) / 1e9 / peak, 4),
-                       "fp64_TFLOP/s": round(f4 / (c4_ms * 1e-3) / 1e12, 2)},
+                       "fp64_TFLOP/s": round(f4 / (c4_ms * 1e-3) / 1e12, 2),
+                       "frac_fp64": round(f4 / (c4_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                       "fp64_peak": f"{FP64_PEAK_TFLOPS} TFLOP/s measured DMMA (profiles/r01_next/fp64_peaks_mix.json)",
+                       "matvecs/s": round(1e3 / c4_ms, 1), "column_matvecs/s": round(M4 * 1e3 / c4_ms, 1)},
         },
         "kernels": {k_: {"launches_per_step": v[0] // args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
                     for k_, v in sorted(per.items())},

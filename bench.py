@@ -358,6 +358,19 @@ def sweep(torch, device, wl, peak):
                                                    wl.X4, wl.Y4, wl.ws4), 5)
     b4 = hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
     out["c4^T"] = {"ms": round(ms, 4), "GB/s": gbs(b4, ms), "frac_hbm": round(b4 / (ms * 1e-3) / 1e9 / peak, 4)}
+    # HSS vs nrhs: config 4's generators with 1 and 8 columns (the step runs 32)
+    for m in (1, 8):
+        X = torch.randn(C4.n, m, dtype=torch.float64, device=device, generator=g)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hss_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, m), dtype=torch.uint8,
+                         device=device)
+        ms = _time_call(torch, lambda: hm.hss_matvec(C4.n, C4.levels, C4.leaf, C4.k, s4.D, s4.U, s4.V, s4.R, s4.W,
+                                                     s4.B, X, Y, ws), 5)
+        nb, fl = hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, m), hss_flops(C4.n, C4.leaf, C4.levels, C4.k, m)
+        out[f"c4_m{m}"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
+                           "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2), "matvecs/s": round(1e3 / ms, 1),
+                           "column_matvecs/s": round(m * 1e3 / ms, 1)}
+        del X, Y, ws
     # ||A||_2 of config 5 (power method on A A^*, 10 steps = 20 products)
     x0 = wl.X5[:, 0].contiguous()
     wsn = torch.empty(hm.hm_hodlr_norm2_workspace_bytes(C5.n, C5.levels, C5.leaf, h.ranks), dtype=torch.uint8,

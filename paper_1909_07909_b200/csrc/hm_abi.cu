@@ -23,6 +23,7 @@
 #include "hm_general.cuh"
 #include "hm_leafup.cuh"
 #include "hm_small.cuh"
+#include "hm_treegemv.cuh"
 
 // One-launch HODLR for small problems (hodlr_small_kernel): correct (parity
 // tested with HM_SMALL_HODLR=1) but not faster on config 1 (22.9 vs 21 us per
@@ -350,13 +351,14 @@ hm_status launch_leaf_gemv_tma(const hm::LeafParams& lp, int64_t nleaves, cudaSt
   });
 }
 
-// nrhs = 1 leaf pass: the TMA ring wins when the U rows are a large share of
-// the leaf's bytes (k >= 8: config 3 m=1, 604 vs 649 us); for k < 8 (config 5)
-// the register-streaming kernel wins (5.25 vs 6.45 ms) — measured, r01_tuning.md.
+// nrhs = 1 leaf pass, measured (r01_tuning.md): the TMA ring wins for k >= 8
+// at b = 256 (config 3 m=1: 594 vs 631 us) and b = 64 (config 1: 20 vs 29 us
+// per call); the register-streaming kernel wins for k < 8 (config 5: 5.25 vs
+// 6.45 ms) and at b = 128 (config 4 at m=1, k=32: 830 vs 1041 us).
 template <int K>
 hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
   if constexpr (K >= 8 && K <= 32) {
-    if (!HM_NO_TMA && !lp.dtrans && lp.b * K <= 4096) {
+    if (!HM_NO_TMA && !lp.dtrans && lp.b != 128 && lp.b * K <= 4096) {
       switch (lp.b) {
         case 64: return launch_leaf_gemv_tma<K, 1>(lp, nleaves, s);
         case 128: return launch_leaf_gemv_tma<K, 2>(lp, nleaves, s);
@@ -755,11 +757,17 @@ struct HssPlan {
   int32_t p, q, m, k;
   VtPath vt;
   LeafPath leaf;
-  bool mma_levels;  // DMMA tree kernels
+  bool mma_levels;   // DMMA tree kernels
+  bool gemv_levels;  // warp-per-node GEMV tree kernels (nrhs <= 4), preferred over DMMA
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
   size_t off_xh, off_yh, off_txh, off_tyh, off_x, off_y, total;
 };
+
+#ifndef HM_TREE_GEMV_MAXM
+#define HM_TREE_GEMV_MAXM 1  // m = 2..4: the DMMA tree levels measured faster (C4 m=2: 490 vs 560 us)
+#endif
+constexpr int kTreeGemvMaxM = HM_TREE_GEMV_MAXM;
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
@@ -783,6 +791,7 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
     P->tile = pick_tile(b, p, P->mc_vt);
   }
   P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
+  P->gemv_levels = coupled && nrhs <= kTreeGemvMaxM && pow2_rank(k, 16, 64);
   if (P->mma_levels) P->nt_down = nt_for(nrhs, HM_TREE_NTMAX);
   const int ktot = leaf_coupled ? k : 0;
   if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
@@ -825,6 +834,69 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 // Levels with at least kTreeBigLevel nodes run one launch per level; the
 // levels above run inside one cooperative launch (hss_tree_sweep_kernel).
 constexpr int64_t kTreeBigLevel = 2048;
+
+// ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
+constexpr int64_t kGemvBigLevel = 8192;  // nodes: one launch per level from here down
+
+template <int K, int MB>
+hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
+                           int down_last) {
+  static int64_t cap = -1;  // co-resident CTAs of the sweep kernel (queried once)
+  if (cap < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_tree_gemv_sweep_kernel<K, MB>, 256, 0) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_tree_gemv_sweep)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (int64_t)per_sm * sms;
+  }
+  int lbig = 1;  // first level with >= kGemvBigLevel nodes
+  while (lbig <= p && (1ll << lbig) < kGemvBigLevel) ++lbig;
+  hm_status st;
+  for (int l = up_from_l; up && l >= lbig; --l) {
+    const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
+    st = launch("hss_up_level", s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    if (st) return st;
+  }
+  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
+  if (up_from >= 1 || down_to >= 1) {
+    const int64_t need = std::max<int64_t>(1, ((1ll << std::max(up_from, down_to)) + 7) / 8);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need)));
+    hm::TreeGemvParams arg = tp;
+    int a1 = up_from, a2 = down_to;
+    void* args[] = {&arg, &a1, &a2};
+    cudaError_t e = cudaSuccess;
+    st = launch("hss_tree_sweep", s, [&] {
+      e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_gemv_sweep_kernel<K, MB>, grid, dim3(256), args, 0,
+                                      s);
+    });
+    if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_gemv_sweep: %s", cudaGetErrorString(e));
+    if (st) return st;
+  }
+  for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
+    const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
+    st = launch("hss_down_level", s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    if (st) return st;
+  }
+  return HM_OK;
+}
+
+hm_status tree_gemv_dispatch(const hm::TreeGemvParams& tp, int p, int k, bool up, bool down, cudaStream_t s,
+                             int up_from, int down_last) {
+  const int mb = tp.m <= 1 ? 1 : (tp.m <= 2 ? 2 : 4);
+#define HM_TG(K_)                                                                      \
+  if (k == K_) {                                                                       \
+    if (mb == 1) return tree_gemv_launch<K_, 1>(tp, p, up, down, s, up_from, down_last); \
+    if (mb == 2) return tree_gemv_launch<K_, 2>(tp, p, up, down, s, up_from, down_last); \
+    return tree_gemv_launch<K_, 4>(tp, p, up, down, s, up_from, down_last);            \
+  }
+  HM_TG(16)
+  HM_TG(32)
+  HM_TG(64)
+#undef HM_TG
+  return fail(HM_ERR_UNSUPPORTED, "hss tree gemv: no instance for k=%d", k);
+}
 
 template <int KT, int NT>
 hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
@@ -902,6 +974,10 @@ hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double*
   hm_status st;
   if (up_from < 0) up_from = p - 1;  // first upsweep level to compute
   if (down_last < 0) down_last = p;  // last downsweep level to compute
+  if (P.gemv_levels) {
+    hm::TreeGemvParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
+    return tree_gemv_dispatch(tp, p, k, up, down, stream, up_from, down_last);
+  }
   if (P.mma_levels) {
     hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
     return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from, down_last);

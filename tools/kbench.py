@@ -1,6 +1,6 @@
 """Per-kernel timing of single configs (development tool, not the bench contract).
 
-    python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 [--reps N]
+    python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 c4m1 c4m8 [--reps N]
 
 A trailing "t" (c5t, c4t, c3m8t, ...) times the adjoint product A^T X instead.
 
@@ -41,8 +41,8 @@ def run(name, reps):
         nbytes = hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
         flops = hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
     else:
-        cfg = hm_inputs.CONFIGS[{"c2": 2, "c4": 4}[name]]
-        m = cfg.nrhs[0]
+        cfg = hm_inputs.CONFIGS[{"c2": 2, "c4": 4}[name[:2]]]
+        m = int(name[3:]) if name[2:3] == "m" else cfg.nrhs[0]  # c4m8: config 4 with 8 columns
         s = hm_inputs.device_hss_random(cfg.n, cfg.levels, cfg.k, 7, dev)
         X = torch.randn(cfg.n, m, dtype=torch.float64, device=dev)
         Y = torch.empty_like(X)

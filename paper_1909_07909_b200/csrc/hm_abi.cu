@@ -836,7 +836,10 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 constexpr int64_t kTreeBigLevel = 2048;
 
 // ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
-constexpr int64_t kGemvBigLevel = 8192;  // nodes: one launch per level from here down
+#ifndef HM_GEMV_BIG
+#define HM_GEMV_BIG 8192
+#endif
+constexpr int64_t kGemvBigLevel = HM_GEMV_BIG;  // nodes: one launch per level from here down
 
 template <int K, int MB>
 hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,

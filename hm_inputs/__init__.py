@@ -68,7 +68,12 @@ def normal(shape, seed: int, cid: int, aid: int, block: int = 0) -> np.ndarray:
 
 def _orth_blocks(G: np.ndarray) -> np.ndarray:
     """Thin-QR Q factor of each block of a stack [N][r][k] (SURVEY G8/G10:
-    'Gaussian orthonormalised (QR)'). Any Householder QR; Q is fixed once drawn."""
+    'Gaussian orthonormalised (QR)'). Any Householder QR; Q is fixed once drawn.
+    A block with fewer rows than columns (leaf b < rank k) gets orthonormal rows
+    instead (Q of its transpose, transposed), keeping the [N][r][k] shape."""
+    if G.shape[-2] < G.shape[-1]:
+        q, _ = np.linalg.qr(np.swapaxes(G, -1, -2), mode="reduced")
+        return np.ascontiguousarray(np.swapaxes(q, -1, -2))
     q, _ = np.linalg.qr(G, mode="reduced")
     return np.ascontiguousarray(q)
 

@@ -67,7 +67,7 @@ def step_bytes():
 
 
 def leaf_apply_c5_bytes(n, b, p, k, m):
-    """Algorithmic bytes of one HODLR leaf_apply launch: D + every level's U + X + Y."""
+    """Algorithmic bytes of one HODLR leaf-pass (leaf_gemv) launch: D + every level's U + X + Y."""
     return 8 * (n * b + p * n * k + 2 * n * m)
 
 
@@ -337,17 +337,29 @@ def sweep(torch, device, wl, peak):
                                    "frac_fp64": round(fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                                    "matvecs/s": round(1e3 / ms, 1), "column_matvecs/s": round(m * 1e3 / ms, 1)}
         del X, Y, ws
-    # per-level ranks on the config-3 tree (f4): ranks 16 / 8 alternating -> general kernels
-    rk = [16 if l % 2 else 8 for l in range(c3.levels)]
-    hv = hm_inputs.device_hodlr_random(c3.n, c3.levels, rk, hm_inputs.MASTER_SEED + 5, device)
-    X = torch.randn(c3.n, 8, dtype=torch.float64, device=device, generator=g)
-    Y = torch.empty_like(X)
-    ws = torch.empty(hm.hm_hodlr_workspace_bytes(c3.n, c3.levels, c3.leaf, rk, 8), dtype=torch.uint8, device=device)
-    nb = 8 * (c3.n * c3.leaf + 2 * sum(rk) * c3.n + 2 * c3.n * 8)
-    ms = _time_call(torch, lambda: hm.hodlr_matvec(c3.n, c3.levels, c3.leaf, rk, hv.D, hv.U, hv.V, X, Y, ws), 5)
-    out["c3_m8_per_level_ranks"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "ranks": "16/8 alternating",
-                                    "path": "general-tree kernels"}
-    del h3, hv, X, Y, ws
+    # per-level ranks on the config-3 tree (f4): one V^T X pass per distinct
+    # rank (tuned kernel where the rank fits it, vt_contract otherwise), one leaf pass
+    for tag, m, rk in (("16/8", 8, [16 if l % 2 else 8 for l in range(c3.levels)]),
+                       ("32/16", 8, [32 if l % 2 else 16 for l in range(c3.levels)]),
+                       ("16/8/4/2", 1, [16 >> (l % 4) for l in range(c3.levels)])):
+        hv = hm_inputs.device_hodlr_random(c3.n, c3.levels, rk, hm_inputs.MASTER_SEED + 5, device)
+        X = torch.randn(c3.n, m, dtype=torch.float64, device=device, generator=g)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hodlr_workspace_bytes(c3.n, c3.levels, c3.leaf, rk, m), dtype=torch.uint8,
+                         device=device)
+        nb = 8 * (c3.n * c3.leaf + 2 * sum(rk) * c3.n + 2 * c3.n * m)
+        hm.hm_profile_collect()
+        hm.hm_profile_enable(True)
+        hm.hodlr_matvec(c3.n, c3.levels, c3.leaf, rk, hv.D, hv.U, hv.V, X, Y, ws)
+        torch.cuda.synchronize()
+        hm.hm_profile_enable(False)
+        kern = sorted({t[0] for t in hm.hm_profile_collect()})
+        ms = _time_call(torch, lambda: hm.hodlr_matvec(c3.n, c3.levels, c3.leaf, rk, hv.D, hv.U, hv.V, X, Y, ws), 5)
+        out[f"c3_m{m}_per_level_ranks_{tag}"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms),
+                                                 "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
+                                                 "ranks": f"{tag} by level", "kernels": kern}
+        del hv, X, Y, ws
+    del h3
     # config 5 and 4 adjoints on the bench's own generators
     h, s4 = wl.h5, wl.s4
     ms = _time_call(torch, lambda: hm.hodlr_matvec_t(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, wl.X5, wl.Y5,
@@ -500,7 +512,7 @@ def run_ours(args):
     total_bytes = step_bytes() * args.steps * world
     value = total_bytes / (ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
-    dom = per.get("c5:leaf_apply", [1, float("nan")])
+    dom = per.get("c5:leaf_gemv", [1, float("nan")])
     dom_avg_ms = dom[1] / dom[0]
     dom_bytes = leaf_apply_c5_bytes(wl.rows5, C5.leaf, C5.levels, C5.k, M5)
     achieved = dom_bytes / (dom_avg_ms * 1e-3) / 1e9
@@ -533,13 +545,13 @@ def run_ours(args):
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "leaf_apply (config 5: D_i X_i + sum_l U_l t_l, all leaves)",
+            "kernel": "leaf_gemv_kernel<K=1> (config-5 leaf pass: D_i X_i + sum_l U_l t_l, all leaves, Y written once)",
             "achieved": round(achieved, 1),
             "peak": peak,
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": committed_traffic("leaf_apply", "c5"),
+            "traffic": committed_traffic("leaf_gemv", "c5"),
             "alg_bytes_per_launch": dom_bytes,
             "avg_launch_ms": round(dom_avg_ms, 4),
             "share_of_step": round(dom[1] / args.steps / step_ms, 4),

@@ -205,7 +205,8 @@ enum class LeafPath { kGeneric, kGemv, kMma };  // kGemv: TMA ring when the shap
 
 struct HodlrPlan {
   int64_t n, b;
-  int32_t p, q, m, k;  // k = the common nonzero rank (0 if all zero)
+  int32_t p, q, m, k;  // k = the common nonzero rank (0 if all zero); the largest one when kvary
+  bool kvary;          // per-level ranks on the uniform tree: levels grouped by rank
   int64_t ktot;        // sum over all q + p levels
   int64_t top_doubles; // sum_{l <= q} k_l m (the distributed exchange block)
   VtPath vt;
@@ -217,8 +218,13 @@ struct HodlrPlan {
   size_t off_ttop, off_spart, off_x, off_y, total;
 };
 
+// Column tiles (of 8) per V^T X pass of vt_mma_levels: as many as the
+// accumulators allow, so V is streamed once per pass (k <= 16: up to 64
+// columns, NT = 8; measured on config 3 at m = 64: 1769 -> 1403 us for k = 16).
+int vt_mma_nt(int k, int nrhs) { return nt_for(nrhs, k == 64 ? 2 : (k == 32 ? 4 : (k == 16 ? HM_VT16_NTMAX : 8))); }
+
 hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_t* ranks, int32_t nrhs,
-                        int32_t flags, HodlrPlan* P) {
+                        int32_t flags, HodlrPlan* P, bool allow_vary = false) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
   if (p + q > 0 && !ranks) return fail(HM_ERR_INVALID_ARG, "ranks is NULL");
   if (p + q + 1 > hm::kMaxLevels) return fail(HM_ERR_UNSUPPORTED, "too many levels");
@@ -229,25 +235,57 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     if (k < 0) return fail(HM_ERR_INVALID_ARG, "ranks[%d] = %d < 0", l - 1, k);
     if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
     if (k > 0) {
-      if (P->k != 0 && P->k != k)
-        return fail(HM_ERR_UNSUPPORTED, "per-level ranks differ (%d vs %d); variable ranks (P:264) not built", P->k, k);
-      P->k = k;
+      if (P->k != 0 && P->k != k) {
+        if (!allow_vary)
+          return fail(HM_ERR_UNSUPPORTED, "per-level ranks differ (%d vs %d); variable ranks (P:264) not built here",
+                      P->k, k);
+        P->kvary = true;
+      }
+      P->k = std::max(P->k, k);
     }
     P->ktot += k;
     if (l <= q) P->top_doubles += (int64_t)k * nrhs;
   }
   const int64_t k = P->k;
   const bool tiles8 = p >= 3;  // 8-leaf row tiles exist
+  if (P->kvary) {
+    // Per-level ranks on the uniform tree, 8-leaf row tiles: one V^T X
+    // pass per distinct rank — the tuned kernel where the rank fits it (GEMV:
+    // powers of two <= 64 at nrhs = 1; DMMA: 16/32/64 at nrhs >= 2), else
+    // vt_contract on the same tiles — and ONE leaf pass with per-segment ranks.
+    // Other shapes (p < 3, leaf not a multiple of 64) take the general-tree kernels.
+    if (!(tiles8 && b % 64 == 0 && b <= 1024))
+      return fail(HM_ERR_UNSUPPORTED, "per-level ranks: uniform-tree kernels need levels >= 3 and leaf %% 64 == 0");
+    P->vt = nrhs == 1 ? VtPath::kGemv : VtPath::kMma;
+    P->tile = 8 * b;
+    int mc = std::min<int32_t>(nrhs, hm::kMaxMc);
+    while (mc > 1 && P->tile * mc + hm::kThreads > kSmemBudgetDoubles) --mc;
+    P->mc_vt = mc;
+    bool pow2 = true, k8 = true;
+    for (int l = 1; l <= p + q; ++l) {
+      const int kl = ranks[l - 1];
+      if (kl == 0) continue;
+      pow2 = pow2 && pow2_rank(kl, 1, 64);
+      k8 = k8 && kl % 8 == 0;
+    }
+    P->leaf = LeafPath::kGeneric;
+    if (nrhs == 1 && pow2 && (2 * b + (int64_t)(p + q) * k) * 8 <= 160 * 1024) {
+      P->leaf = LeafPath::kGemv;
+    } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && k8) {
+      const int rg = (int)(b / 64);
+      P->nt_leaf = nt_for(nrhs, rg == 4 ? 2 : 4);
+      if ((b + P->ktot) * (8 * P->nt_leaf + 4) <= kSmemBudgetDoubles) P->leaf = LeafPath::kMma;
+    }
+  } else {
   if (k == 0 || p + q == 0) {
     P->vt = VtPath::kNone;
   } else if (nrhs == 1 && tiles8 && b % 64 == 0 && b <= 4096 && pow2_rank((int)k, 1, 64)) {
     P->vt = VtPath::kGemv;
     P->tile = 8 * b;
-  } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 16, 64)) {
+  } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 1, 64)) {
     P->vt = VtPath::kMma;
     P->tile = 8 * b;
-    // k = 16: up to 64 columns per pass (NT = 8), so V is streamed once for m <= 64
-    P->nt_vt = nt_for(nrhs, k == 64 ? 2 : (k == 16 ? HM_VT16_NTMAX : 4));
+    P->nt_vt = vt_mma_nt((int)k, nrhs);
   } else {
     P->vt = VtPath::kGeneric;
     P->mc_vt = vt_mc(b, nrhs);
@@ -264,6 +302,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     if ((b + P->ktot) * (8 * P->nt_leaf + 4) > kSmemBudgetDoubles) P->leaf = LeafPath::kGeneric;
   } else {
     P->leaf = LeafPath::kGeneric;
+  }
   }
   if (P->leaf == LeafPath::kGeneric) {
     P->mc_leaf = pick_mc(b, P->ktot, nrhs);
@@ -303,7 +342,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
 hm_status hodlr_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags, HodlrPlan* P) {
   hm_status st = check_tree(tree);
   if (st) return st;
-  return hodlr_plan_ex(tree->n, tree->leaf, tree->levels, 0, ranks, nrhs, flags, P);
+  return hodlr_plan_ex(tree->n, tree->leaf, tree->levels, 0, ranks, nrhs, flags, P, /*allow_vary=*/true);
 }
 
 // ---- leaf launches (shared by HODLR and HSS) ----
@@ -317,19 +356,19 @@ hm_status launch_leaf_generic(const hm::LeafParams& lp, int64_t nleaves, cudaStr
                 [&] { hm::leaf_apply_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
 }
 
-template <int K, int NCH>
+template <int K, int NCH, bool VARK = false>
 hm_status launch_leaf_gemv_n(const hm::LeafParams& lp, int64_t nleaves, cudaStream_t s) {
   constexpr int ROWS = NCH >= 8 ? 2 : (NCH == 0 ? 4 : HM_GEMV_ROWS);
   if (lp.dtrans) {  // adjoint: D_i^T x_i, per-warp column partials in shared memory
     const size_t smem = sizeof(double) * (size_t)(10 * lp.b + lp.nseg * K);
-    allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS, true>, smem);
-    return launch("leaf_apply_t", s,
-                  [&] { hm::leaf_gemv_kernel<K, NCH, ROWS, true><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+    allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS, true, VARK>, smem);
+    return launch("leaf_gemv_t", s,
+                  [&] { hm::leaf_gemv_kernel<K, NCH, ROWS, true, VARK><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
   }
   size_t smem = sizeof(double) * (size_t)(2 * lp.b + lp.nseg * K);
-  allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS>, smem);
-  return launch("leaf_apply", s,
-                [&] { hm::leaf_gemv_kernel<K, NCH, ROWS><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
+  allow_smem(hm::leaf_gemv_kernel<K, NCH, ROWS, false, VARK>, smem);
+  return launch("leaf_gemv", s,
+                [&] { hm::leaf_gemv_kernel<K, NCH, ROWS, false, VARK><<<(unsigned)nleaves, 256, smem, s>>>(lp); });
 }
 
 #ifndef HM_NO_TMA
@@ -346,7 +385,7 @@ hm_status launch_leaf_gemv_tma(const hm::LeafParams& lp, int64_t nleaves, cudaSt
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>(nleaves, sms);
-  return launch("leaf_apply", s, [&] {
+  return launch("leaf_gemv_tma", s, [&] {
     hm::leaf_gemv_tma_kernel<K, NCH><<<grid, 32 * (hm::kTmaConsumers + 1), smem, s>>>(lp, nleaves, kTmaStages);
   });
 }
@@ -392,24 +431,41 @@ hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_
   if (lp.dp > 0) {  // HSS: leaf-level coupling + downsweep fused (y_i computed in the CTA)
     const size_t sm2 = smem + sizeof(double) * 2 * (size_t)lp.seg[0].k * (NT * 8 + 2);
     allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB, false, true>, sm2);
-    return launch("leaf_apply", s, [&] {
+    return launch("leaf_mma_down", s, [&] {
       hm::leaf_mma_kernel<RG, NT, PF, MINB, false, true><<<(unsigned)(nleaves * chunks), 256, sm2, s>>>(lp);
     });
   }
   if (lp.dtrans) {
     allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB, true>, smem);
-    return launch("leaf_apply_t", s, [&] {
+    return launch("leaf_mma_t", s, [&] {
       hm::leaf_mma_kernel<RG, NT, PF, MINB, true><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp);
     });
   }
   allow_smem(hm::leaf_mma_kernel<RG, NT, PF, MINB>, smem);
-  return launch("leaf_apply", s, [&] {
+  return launch("leaf_mma", s, [&] {
     hm::leaf_mma_kernel<RG, NT, PF, MINB><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp);
   });
 }
 
 hm_status leaf_dispatch(const hm::LeafParams& lp, int64_t nleaves, LeafPath path, int k, int nt, int mc,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool kvary = false) {
+  if (path == LeafPath::kGemv && kvary) {  // per-level ranks: k = the largest (register streaming kernel)
+#define HM_LEAF_VARK(K_)                                          \
+  if (k == K_) switch (lp.b) {                                    \
+      case 64: return launch_leaf_gemv_n<K_, 1, true>(lp, nleaves, s);  \
+      case 128: return launch_leaf_gemv_n<K_, 2, true>(lp, nleaves, s); \
+      case 256: return launch_leaf_gemv_n<K_, 4, true>(lp, nleaves, s); \
+      default: break;                                             \
+    }
+    HM_LEAF_VARK(2)
+    HM_LEAF_VARK(4)
+    HM_LEAF_VARK(8)
+    HM_LEAF_VARK(16)
+    HM_LEAF_VARK(32)
+    HM_LEAF_VARK(64)
+#undef HM_LEAF_VARK
+    return fail(HM_ERR_UNSUPPORTED, "leaf_gemv (per-level ranks): no instance for k=%d b=%lld", k, (long long)lp.b);
+  }
   if (path == LeafPath::kGemv) {
     switch (k) {
       case 0: case 1: return launch_leaf_gemv<1>(lp, nleaves, s);
@@ -461,7 +517,7 @@ hm_status vt_gemv_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
   for (int i = 0; i < vp.nlev; ++i) gp.lev[i] = vp.lev[i];
   size_t smem = sizeof(double) * (size_t)(8 * b);
   allow_smem(hm::vt_gemv_kernel<K>, smem);
-  return launch("vt_contract", s,
+  return launch("vt_gemv", s,
                 [&] { hm::vt_gemv_kernel<K><<<(unsigned)(vp.n / (8 * b)), 256, smem, s>>>(gp); });
 }
 
@@ -481,7 +537,7 @@ template <int KT, int NT>
 hm_status vt_mma_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
   size_t smem = sizeof(double) * (size_t)(8 * KT * NT * 8);
   allow_smem(hm::vt_mma_levels_kernel<KT, NT>, smem);
-  return launch("vt_contract", s, [&] {
+  return launch("vt_mma_levels", s, [&] {
     hm::vt_mma_levels_kernel<KT, NT><<<(unsigned)(vp.n / (8 * b)), 256, smem, s>>>(vp, b);
   });
 }
@@ -498,6 +554,18 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
   HM_VT_MMA(32)
   HM_VT_MMA(64)
 #undef HM_VT_MMA
+#define HM_VT_MMA_SMALL(KT_)                                                   \
+  if (k == KT_) {                                                              \
+    if (nt == 1) return vt_mma_launch<KT_, 1>(vp, b, s);                       \
+    if (nt == 2) return vt_mma_launch<KT_, 2>(vp, b, s);                       \
+    if (nt == 4) return vt_mma_launch<KT_, 4>(vp, b, s);                       \
+    return vt_mma_launch<KT_, 8>(vp, b, s);                                    \
+  }
+  HM_VT_MMA_SMALL(1)
+  HM_VT_MMA_SMALL(2)
+  HM_VT_MMA_SMALL(4)
+  HM_VT_MMA_SMALL(8)
+#undef HM_VT_MMA_SMALL
   return fail(HM_ERR_UNSUPPORTED, "vt_mma: no instance for k=%d nt=%d", k, nt);
 }
 
@@ -570,8 +638,26 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
     if (l <= P.q) toff += (int64_t)k * nrhs;
   }
   if (vp.nlev == 0) return HM_OK;
-  hm_status st;
-  if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
+  hm_status st = HM_OK;
+  if (P.kvary) {
+    // per-level ranks: one pass per distinct rank over the levels of that rank
+    // (X, small next to V, is re-read once per pass)
+    for (int g = 0; g < vp.nlev; ++g) {
+      const int kg = vp.lev[g].k;
+      bool seen = false;
+      for (int h = 0; h < g; ++h) seen = seen || vp.lev[h].k == kg;
+      if (seen) continue;
+      hm::VtParams vg = vp;
+      vg.nlev = 0;
+      for (int h = 0; h < vp.nlev; ++h)
+        if (vp.lev[h].k == kg) vg.lev[vg.nlev++] = vp.lev[h];
+      if (nrhs == 1 && pow2_rank(kg, 1, 64)) st = vt_gemv_dispatch(vg, P.b, kg, stream);
+      else if (nrhs >= 2 && pow2_rank(kg, 1, 64))
+        st = vt_mma_dispatch(vg, P.b, kg, vt_mma_nt(kg, nrhs), stream);
+      else st = vt_generic(vg, P.n, stream);  // same 8-leaf tiles (P.tile), P.mc_vt columns
+      if (st) return st;
+    }
+  } else if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
   else if (P.vt == VtPath::kMma) st = vt_mma_dispatch(vp, P.b, P.k, P.nt_vt, stream);
   else st = vt_generic(vp, P.n, stream);
   if (st) return st;
@@ -613,7 +699,7 @@ hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const doubl
     uoff += P.n * k;
     if (l <= P.q) toff += (int64_t)k * P.m;
   }
-  return leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream);
+  return leaf_dispatch(lp, 1ll << P.p, P.leaf, P.k, P.nt_leaf, P.mc_leaf, stream, P.kvary);
 }
 
 // ---- small problems: the whole product in one cooperative launch ----
@@ -859,7 +945,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
   hm_status st;
   for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
-    st = launch("hss_up_level", s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    st = launch("hss_up_gemv", s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
     if (st) return st;
   }
   const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
@@ -870,7 +956,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
     int a1 = up_from, a2 = down_to;
     void* args[] = {&arg, &a1, &a2};
     cudaError_t e = cudaSuccess;
-    st = launch("hss_tree_sweep", s, [&] {
+    st = launch("hss_tree_gemv_sweep", s, [&] {
       e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_gemv_sweep_kernel<K, MB>, grid, dim3(256), args, 0,
                                       s);
     });
@@ -879,7 +965,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
   }
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
-    st = launch("hss_down_level", s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    st = launch("hss_down_gemv", s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
     if (st) return st;
   }
   return HM_OK;
@@ -904,12 +990,20 @@ hm_status tree_gemv_dispatch(const hm::TreeGemvParams& tp, int p, int k, bool up
 template <int KT, int NT>
 hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
                       int down_last) {
-  constexpr int MINB = (KT == 32 && NT == 4) ? 3 : 0;  // measured, r01_tuning.md
+#ifndef HM_TREE_UP_MINB
+#define HM_TREE_UP_MINB 2
+#endif
+#ifndef HM_TREE_DN_MINB
+#define HM_TREE_DN_MINB 3
+#endif
+  // min CTAs per SM for the config-4 shape (k = 32, m = 32), measured (r01_tuning.md)
+  constexpr int MINB_UP = (KT == 32 && NT == 4) ? HM_TREE_UP_MINB : 0;
+  constexpr int MINB = (KT == 32 && NT == 4) ? HM_TREE_DN_MINB : 0;
   const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
   static bool attrs = false;
   int sweep_blocks_per_sm = 0;
   if (!attrs) {
-    allow_smem(hm::hss_up_pair_kernel<KT, NT, MINB>, 200 * 1024);
+    allow_smem(hm::hss_up_pair_kernel<KT, NT, MINB_UP>, 200 * 1024);
     allow_smem(hm::hss_down_pair_kernel<KT, NT, MINB>, 200 * 1024);
     allow_smem(hm::hss_tree_sweep_kernel<KT, NT>, 200 * 1024);
     attrs = true;
@@ -923,7 +1017,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // upsweep: big levels up_from_l .. lbig one launch each
   for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch("hss_up_level", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    st = launch("hss_up_pair", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
@@ -947,7 +1041,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // downsweep: big levels lbig .. p one launch each
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch("hss_down_level", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    st = launch("hss_down_pair", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   return HM_OK;
@@ -1013,7 +1107,7 @@ hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int6
   const int k = P.k, nrhs = P.m;
   if (nrhs >= 2 && pow2_rank(k, 16, 64) && K % 4 == 0) {
     hm::BatchedVtParams bp{A, 0, Z, 0, out, 0, 1, (int32_t)K, nrhs};
-    return vt_batched_dispatch("vt_contract", bp, k, nt_for(nrhs, HM_VTB_NTMAX), stream);
+    return vt_batched_dispatch("vt_batched", bp, k, nt_for(nrhs, HM_VTB_NTMAX), stream);
   }
   hm::VtParams vp;
   memset(&vp, 0, sizeof vp);
@@ -1104,7 +1198,7 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
     up_from = P.p - 2;
   } else if (P.vt == VtPath::kMma) {
     hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
-    if ((st = vt_batched_dispatch("vt_contract", bp, k, P.nt_vt, stream))) return st;
+    if ((st = vt_batched_dispatch("vt_batched", bp, k, P.nt_vt, stream))) return st;
   } else {
     hm::VtParams vp;
     memset(&vp, 0, sizeof vp);
@@ -1581,6 +1675,17 @@ bool ranks_vary(int32_t p, const int32_t* ranks) {
   return false;
 }
 
+// Per-level ranks on the uniform tree: the general-tree kernels take
+// the call unless every rank fits the tuned kernels (hodlr_plan with kvary).
+bool hodlr_use_general(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags) {
+  if (!tree || check_tree(tree) != HM_OK || !ranks || !ranks_vary(tree->levels, ranks)) return false;
+  HodlrPlan P;
+  const std::string saved = g_err;
+  const bool fast = hodlr_plan(tree, ranks, nrhs, flags, &P) == HM_OK;
+  g_err = saved;
+  return !fast;
+}
+
 std::vector<int64_t> uniform_endpoints(const hm_tree* t) {
   std::vector<int64_t> c((size_t)1 << t->levels);
   for (size_t i = 0; i < c.size(); ++i) c[i] = (int64_t)(i + 1) * t->leaf;
@@ -1780,7 +1885,7 @@ hm_status hss_norm2_est(const hm_tree* tree, int32_t k, const double* D, const d
 hm_status hm_hodlr_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t flags,
                                    size_t* bytes) {
   if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
-  if (flags == 0 && tree && check_tree(tree) == HM_OK && ranks && ranks_vary(tree->levels, ranks)) {
+  if (flags == 0 && hodlr_use_general(tree, ranks, nrhs, flags)) {
     // per-level ranks: the general-tree kernels on the uniform endpoints
     GenPlan G;
     const std::vector<int64_t> c = uniform_endpoints(tree);
@@ -1799,7 +1904,7 @@ hm_status hm_hodlr_workspace_bytes(const hm_tree* tree, const int32_t* ranks, in
 hm_status hodlr_matvec(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                        const double* V, const double* X, int32_t nrhs, double* Y, void* workspace,
                        size_t workspace_bytes, void* stream) {
-  if (tree && check_tree(tree) == HM_OK && ranks && ranks_vary(tree->levels, ranks)) {
+  if (hodlr_use_general(tree, ranks, nrhs, 0)) {
     const std::vector<int64_t> c = uniform_endpoints(tree);
     return hodlr_gen_run(tree->n, tree->levels, c.data(), ranks, 0, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
                          static_cast<cudaStream_t>(stream));
@@ -1818,7 +1923,7 @@ hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks, const d
 hm_status hodlr_matvec_t(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                          const double* V, const double* X, int32_t nrhs, double* Y, void* workspace,
                          size_t workspace_bytes, void* stream) {
-  if (tree && check_tree(tree) == HM_OK && ranks && ranks_vary(tree->levels, ranks)) {
+  if (hodlr_use_general(tree, ranks, nrhs, 0)) {
     const std::vector<int64_t> c = uniform_endpoints(tree);
     return hodlr_gen_run(tree->n, tree->levels, c.data(), ranks, 1, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
                          static_cast<cudaStream_t>(stream));

@@ -194,7 +194,10 @@ __global__ void __launch_bounds__(256) vt_gemv_kernel(const VtGemvParams P) {
 // row-major 128-bit stream of D; warp w owns rows w, w+8, ..; lane l keeps the
 // partial sums of columns 64c + 2l, 64c + 2l + 1 in registers (x[r] broadcast
 // from shared memory); the 8 warps' partials are summed in a fixed order.
-template <int K, int NCH, int ROWS, bool DT = false>
+//
+// VARK = true (per-level ranks on the uniform tree): K is the largest
+// rank; segment s has its own rank P.seg[s].k (a power of two <= K).
+template <int K, int NCH, int ROWS, bool DT = false, bool VARK = false>
 __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   extern __shared__ double sm[];
   const int64_t leaf = blockIdx.x;
@@ -208,7 +211,8 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
     const int64_t node = (leaf >> sg.shift) ^ sg.xr;
-    for (int a = threadIdx.x; a < K; a += 256) ts[s * K + a] = __ldg(sg.T + node * K + a);
+    const int kk = VARK ? sg.k : K;
+    for (int a = threadIdx.x; a < kk; a += 256) ts[s * K + a] = __ldg(sg.T + node * kk + a);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -311,13 +315,15 @@ __global__ void __launch_bounds__(256) leaf_gemv_kernel(const LeafParams P) {
   for (int64_t r = threadIdx.x; r < b; r += 256, ++nr) {
     double u = 0.0;
     for (int s = 0; s < P.nseg; ++s) {
-      const double* Ur = P.seg[s].A + (r0 + r) * K;
+      const int kk = VARK ? P.seg[s].k : K;
+      const double* Ur = P.seg[s].A + (r0 + r) * kk;
       const double* t = ts + s * K;
-      if (K == 1) {
+      if (K == 1 || (VARK && kk == 1)) {
         u = fma(ldg_stream(Ur), t[0], u);
       } else {
 #pragma unroll
         for (int a = 0; a < K; a += 2) {
+          if (VARK && a >= kk) break;
           const double2 w = ldg_stream2(Ur + a);
           u = fma(w.y, t[a + 1], fma(w.x, t[a], u));
         }
@@ -885,6 +891,47 @@ __global__ void __launch_bounds__(256) vt_batched_kernel(const BatchedVtParams P
 #ifndef HM_VTM_PF
 #define HM_VTM_PF(NT) ((NT) > 4 ? 2 : 4)
 #endif
+
+// Small ranks (KT = 1, 2, 4, 8; per-level ranks below 16): C (8 x 8NT)
+// += A^T B with A [K][KT]. One DMMA tile holds every rank column (rows a < KT
+// valid). A k-step's A fragment is A[4q + j][i] (i = lane >> 2, j = lane & 3):
+// 4 consecutive rows of KT doubles, one coalesced 64-bit load per lane; B
+// fragments X[4q + j][c0 + 8nt + i] straight from global memory.
+template <int KT, int NT, int PF>
+__device__ __forceinline__ void warp_transposed_mma_small(double (&acc)[1][NT][2], const double* __restrict__ A,
+                                                          const double* __restrict__ B, int64_t ldb, int c0, int m,
+                                                          int K, int lane) {
+  const int j = lane & 3, i = lane >> 2;
+  const bool aok = i < KT;
+  const double* ap = A + (int64_t)j * KT + (aok ? i : 0);
+  const double* bp = B + (int64_t)j * ldb + c0 + i;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = (c0 + nt * 8 + i) < m;
+  int q = 0;
+#pragma unroll 1
+  for (; q + PF <= K / 4; q += PF) {
+    double a[PF], bf[PF][NT];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      a[u] = aok ? ldg_stream(ap + (int64_t)(q + u) * 4 * KT) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? __ldg(bp + (int64_t)(q + u) * 4 * ldb + nt * 8) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[u], bf[u][nt]);
+  }
+  for (; q < K / 4; ++q) {
+    const double a = aok ? ldg_stream(ap + (int64_t)q * 4 * KT) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double bf = colok[nt] ? __ldg(bp + (int64_t)q * 4 * ldb + nt * 8) : 0.0;
+      dmma(acc[0][nt][0], acc[0][nt][1], a, bf);
+    }
+  }
+}
 // HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
 // Per level: warp partial t over its b rows (DMMA), staged in shared memory,
 // then fixed-order sums over the warps of each node.
@@ -900,14 +947,27 @@ __global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, in
     const int mc = min(MC, m - c0);
     for (int L = 0; L < P.nlev; ++L) {
       const VtLevel lv = P.lev[L];
-      double acc[KT / 8][NT][2];
+      double acc[(KT + 7) / 8][NT][2];
 #pragma unroll
-      for (int t = 0; t < KT / 8; ++t)
+      for (int t = 0; t < (KT + 7) / 8; ++t)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-      warp_transposed_mma<KT / 16, NT, false, HM_VTM_PF(NT)>(acc, lv.V + row0 * KT, KT, P.X + row0 * m, m, c0, m,
-                                                             (int)b, lane);
-      store_transposed<KT / 16, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
+      if constexpr (KT < 16) {
+        warp_transposed_mma_small<KT, NT, (NT > 4 ? 4 : 8)>(acc, lv.V + row0 * KT, P.X + row0 * m, m, c0, m, (int)b,
+                                                           lane);
+        const int i = lane >> 2, j = lane & 3;
+        if (i < KT)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            double* o = red + ((int64_t)warp * KT + i) * MC + nt * 8 + 2 * j;
+            o[0] = acc[0][nt][0];
+            o[1] = acc[0][nt][1];
+          }
+      } else {
+        warp_transposed_mma<KT / 16, NT, false, HM_VTM_PF(NT)>(acc, lv.V + row0 * KT, KT, P.X + row0 * m, m, c0, m,
+                                                               (int)b, lane);
+        store_transposed<KT / 16, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
+      }
       __syncthreads();
       const int64_t g = lv.s >= tile ? 8 : lv.s / b;
       const int ngroups = (int)(8 / g);

@@ -47,43 +47,6 @@ __host__ __device__ constexpr int64_t tree_smem_doubles(int kt, int m, int nt) {
              : 3ll * kt * tree_down_stride(tree_mpad(m, nt));
 }
 
-// Transposed product with B in shared memory: C (16 x 8NT) += A^T B, A [K][lda]
-// global (the warp's 16 rank columns start at A), B [K][zs] shared.
-template <int NT, int PF>
-__device__ __forceinline__ void warp_transposed_smem(double (&acc)[2][NT][2], const double* __restrict__ A, int64_t lda,
-                                                     const double* Bs, int zs, int c0, int K, int lane) {
-  const int j = lane & 3, i = lane >> 2;
-  const double* ap = A + (int64_t)j * lda + 2 * i;
-  const double* bp = Bs + j * zs + c0 + i;
-  int q = 0;
-#pragma unroll 1
-  for (; q + PF <= K / 4; q += PF) {
-    double2 a[PF];
-#pragma unroll
-    for (int u = 0; u < PF; ++u) a[u] = ldg_stream2(ap + (int64_t)(q + u) * 4 * lda);
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      double bf[NT];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[nt] = bp[(q + u) * 4 * zs + nt * 8];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[u].x, bf[nt]);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a[u].y, bf[nt]);
-    }
-  }
-  for (; q < K / 4; ++q) {
-    const double2 a = ldg_stream2(ap + (int64_t)q * 4 * lda);
-    double bf[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bf[nt] = bp[q * 4 * zs + nt * 8];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a.x, bf[nt]);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a.y, bf[nt]);
-  }
-}
-
 // Up: CTA task for the node pair (2r, 2r+1) of level l (children: 4 consecutive
 // level-(l+1) blocks). 4 warps per node: rank-column group mg = w % MG, column
 // chunks ck = w / MG, w / MG + 4/MG, ...
@@ -91,6 +54,7 @@ template <int KT, int NT, bool COH>
 __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t r, double* sm) {
   constexpr int MG = KT / 16;
   constexpr int CKS = 4 / MG;  // chunk step per node
+  constexpr int NQ = KT / 2;   // k-steps of the 2k-row contraction
   const int m = P.m;
   const int mp = tree_mpad(m, NT);
   const int zs = tree_up_stride(mp);
@@ -98,28 +62,47 @@ __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t
   const int64_t n0 = 2 * r;  // level l >= 1 has an even number of nodes
   const int nodes = 2;
   stage_rows_async(sm, zs, P.xh + ((1ll << (l + 1)) - 2 + 2 * n0) * km, m, 2 * nodes * KT, m, mp);
-  cp_async_wait_all();
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = w >> 2, sub = w & 3;
+  const int i = lane >> 2, j = lane & 3;
+  const int64_t node = n0 + nd;
+  const int mg = sub % MG;
+  // The warp's whole slice of W (2k rows x 16 rank columns, one LDG.128 per
+  // k-step) is requested before the staged children are waited for, so the
+  // generator stream and the staging overlap instead of running back to back.
+  double2 a[NQ];
+  {
+    const double* ap = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16 + (int64_t)j * KT + 2 * i;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a[q] = ldg_stream2(ap + (int64_t)q * 4 * KT);
+  }
+  cp_async_wait_all();
+  __syncthreads();
   // the 4 warps of a node split MG rank groups x column chunks; narrower chunks
   // (NTU = NT * MG / 4) keep all 4 busy when MG < 4 (k = 16, 32)
   constexpr int NTU = (NT * MG / 4) >= 1 ? (NT * MG / 4) : 1;
   {
-    const int64_t node = n0 + nd;
-    const int mg = sub % MG;
-    const double* A = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16;
-    const double* Bs = sm + nd * 2 * KT * zs;
+    const double* bp = sm + nd * 2 * KT * zs + j * zs + i;
     double* out = P.xh + ((1ll << l) - 2 + node) * km + (int64_t)mg * 16 * m;
     const int nck = mp / (NTU * 8);
     for (int ck = sub / MG; ck < nck; ck += CKS) {
+      const int c0 = ck * NTU * 8;
       double acc[2][NTU][2];
 #pragma unroll
       for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int nt = 0; nt < NTU; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-      warp_transposed_smem<NTU, (KT / 2 < 16 ? KT / 2 : 16)>(acc, A, KT, Bs, zs, ck * NTU * 8, 2 * KT, lane);
-      store_transposed<1, NTU>(acc, out, m, ck * NTU * 8, m, lane);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double bf[NTU];
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) bf[nt] = bp[q * 4 * zs + c0 + nt * 8];
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[q].x, bf[nt]);
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a[q].y, bf[nt]);
+      }
+      store_transposed<1, NTU>(acc, out, m, c0, m, lane);
     }
   }
   __syncthreads();  // shared memory is reused by the next task
@@ -139,8 +122,6 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
   const bool root_term = (l == 1 && P.R_root != nullptr);
   if (l >= 2) stage_rows_async(sm + 2 * KT * zs, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
   if (root_term) stage_rows_async(sm + 2 * KT * zs, zs, P.y_root, m, KT, m, mp);
-  cp_async_wait_all();
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nd = w >> 2, sub = w & 3;
   const int64_t j = 2 * q + nd;
@@ -152,16 +133,14 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
   const double* Zy = sm + 2 * KT * zs;
   double* yo = P.yh + ((1ll << l) - 2 + j) * km;
   const int nck = mp / (NT * 8);
+  const int ntask = RGS * nck;
   const int i = lane >> 2, jj = lane & 3;
-  for (int t = sub; t < RGS * nck; t += 4) {
-    const int rg = t % RGS, ck = t / RGS;
-    const int c0 = ck * NT * 8;
-    double acc[1][NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
-    // every A fragment of both terms is requested before the first DMMA
-    constexpr int NQ = KT / 8;
-    double2 aR[NQ][1], aS[NQ][1];
+  // every A fragment of both terms of a task is requested before the first
+  // DMMA — for the first task before the staged blocks are waited for
+  constexpr int NQ = KT / 8;
+  double2 aR[NQ][1], aS[NQ][1];
+  auto load_task = [&](int t) {
+    const int rg = t % RGS;
     const double* bR = Rw ? Rw + (int64_t)(rg * 8 + i) * KT + 2 * jj : nullptr;
     const double* bS = P.bt ? S + (int64_t)(2 * jj) * KT + rg * 8 + i : S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
 #pragma unroll
@@ -171,11 +150,22 @@ __device__ __forceinline__ void tree_down_pair(const TreeParams& P, int l, int64
       aS[q2][0] = P.bt ? make_double2(ldg_stream(bS + (int64_t)8 * q2 * KT), ldg_stream(bS + (int64_t)(8 * q2 + 1) * KT))
                        : ldg_stream2(bS + 8 * q2);
     }
+  };
+  if (sub < ntask) load_task(sub);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int t = sub; t < ntask; t += 4) {
+    const int rg = t % RGS, ck = t / RGS;
+    const int c0 = ck * NT * 8;
+    double acc[1][NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
     bool colok[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
     if (Rw) rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
     rm_group<1, NT, false, false, NQ>(acc, aS, Zx + c0, zs, 0, NQ, colok, lane);
+    if (t + 4 < ntask) load_task(t + 4);
     double* y = yo + (int64_t)(8 * rg + i) * m;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {

@@ -82,22 +82,65 @@ def test_hss_general_vs_oracle(hm, name, c, p, k, m):
         assert relerr(Y.cpu().numpy(), f(n, p, k, D, U, V, R, W, B, X, c=c)) <= TOL, op
 
 
-@pytest.mark.parametrize("n,leaf,p,ranks,m", [
-    (65536, 256, 8, [16, 8, 16, 4, 2, 16, 32, 1], 1),
-    (65536, 256, 8, [64, 32, 16, 8, 4, 2, 1, 0], 8),
-    (16384, 64, 8, [1, 2, 3, 4, 5, 6, 7, 8], 3),
+@pytest.mark.parametrize("n,leaf,p,ranks,m,route", [
+    (65536, 256, 8, [64, 32, 16, 8, 4, 2, 1, 0], 8, "uniform"),   # ranks < 8: generic leaf pass
+    (16384, 64, 8, [1, 2, 3, 4, 5, 6, 7, 8], 3, "uniform"),       # odd ranks: vt_contract groups
+    (12288, 96, 7, [8, 16, 4, 2, 16, 8, 1], 2, "general"),        # leaf not a multiple of 64
+    (4096, 1024, 2, [16, 8], 5, "general"),                       # fewer than 8 leaves
 ])
-def test_uniform_tree_per_level_ranks(hm, n, leaf, p, ranks, m):
-    """hodlr_matvec / hodlr_matvec_t route per-level ranks to the general kernels."""
+def test_uniform_tree_per_level_ranks(hm, n, leaf, p, ranks, m, route):
+    """hodlr_matvec / hodlr_matvec_t on per-level ranks outside the tuned
+    kernels' shapes: mixed tuned / generic uniform-tree kernels, or the
+    general-tree kernels when the tree has no 8-leaf tiles of 64-multiples."""
     rng = np.random.default_rng(71)
     c = np.arange(1, (1 << p) + 1, dtype=np.int64) * leaf
     D, U, V = random_hodlr_general(c, p, ranks, rng)
     X = rng.standard_normal((n, m))
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
     Y = hm.hodlr_matvec(n, p, leaf, ranks, dev(D), dev(U), dev(V), dev(X))
     Yt = hm.hodlr_matvec_t(n, p, leaf, ranks, dev(D), dev(U), dev(V), dev(X))
     torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert any(nm.startswith("gen_") for nm in names) == (route == "general"), names
     assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X)) <= TOL
     assert relerr(Yt.cpu().numpy(), oracle.hodlr_matvec_t(n, p, ranks, D, U, V, X)) <= TOL
+
+
+@pytest.mark.parametrize("n,leaf,p,ranks,m", [
+    (65536, 256, 8, [16, 8, 16, 4, 2, 16, 32, 1], 1),
+    (131072, 256, 9, [1, 2, 4, 8, 16, 32, 64, 1, 0], 1),
+    (32768, 128, 8, [2, 1, 2, 1, 2, 1, 2, 1], 1),
+    (65536, 128, 9, [32, 16, 0, 64, 16, 32, 16, 16, 32], 8),
+    (32768, 64, 9, [16, 32, 16, 32, 16, 32, 16, 32, 64], 2),
+    (65536, 256, 8, [16, 32, 16, 32, 16, 32, 0, 32], 64),
+    (16384, 64, 8, [64, 16, 16, 16, 32, 16, 16, 16], 13),
+    (65536, 256, 8, [16, 8, 16, 8, 16, 8, 16, 8], 8),   # bench sweep's 16/8 set, smaller depth
+    (65536, 128, 9, [8, 4, 2, 1, 0, 1, 2, 4, 8], 3),    # small ranks: DMMA V^T X, generic leaf pass
+])
+def test_uniform_tree_per_level_ranks_tuned_kernels(hm, n, leaf, p, ranks, m):
+    """Per-level ranks that fit the tuned kernels run on them (one V^T X pass
+    per distinct rank, per-segment ranks in the leaf pass), not on the general ones."""
+    rng = np.random.default_rng(73 + m)
+    c = np.arange(1, (1 << p) + 1, dtype=np.int64) * leaf
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    g = [dev(a) for a in (D, U, V)]
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    Y = hm.hodlr_matvec(n, p, leaf, ranks, *g, dev(X))
+    Yt = hm.hodlr_matvec_t(n, p, leaf, ranks, *g, dev(X))
+    torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert not any(nm.startswith("gen_") for nm in names), names
+    assert names & {"vt_gemv", "vt_mma_levels"}, names
+    assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X)) <= TOL
+    assert relerr(Yt.cpu().numpy(), oracle.hodlr_matvec_t(n, p, ranks, D, U, V, X)) <= TOL
+    # bitwise repeatable (fixed-order reductions)
+    Y2 = hm.hodlr_matvec(n, p, leaf, ranks, *g, dev(X))
+    assert torch.equal(Y, Y2)
 
 
 def test_general_uniform_endpoints_match_uniform_path(hm):

@@ -84,6 +84,10 @@ HODLR_CASES = [
     (8192, 256, 5, 16, 8),
     (16384, 64, 8, 2, 1),       # GEMV paths, rank 2
     (32768, 128, 8, 64, 1),     # GEMV paths, rank 64
+    (32768, 64, 9, 8, 5),       # small-rank DMMA V^T X (one tile holds every rank column)
+    (65536, 256, 8, 8, 64),
+    (16384, 128, 7, 2, 9),      # small-rank DMMA, ragged column chunk
+    (16384, 64, 8, 1, 2),
 ]
 
 

@@ -991,7 +991,7 @@ template <int KT, int NT>
 hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
                       int down_last) {
 #ifndef HM_TREE_UP_MINB
-#define HM_TREE_UP_MINB 2
+#define HM_TREE_UP_MINB 4
 #endif
 #ifndef HM_TREE_DN_MINB
 #define HM_TREE_DN_MINB 3

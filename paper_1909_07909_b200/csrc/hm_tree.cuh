@@ -38,6 +38,9 @@ struct TreeParams {
 //   row-major B fragments read rows r + 2j, d = 2 j zs + i: zs = 2 (mod 4).
 // (Measured with ncu: strides 8 (mod 16) / 4 (mod 8) gave 2-way conflicts on
 // every load, l1tex__data_bank_conflicts = 1/2 of the wavefronts.)
+#ifndef HM_TREE_UP_HQ
+#define HM_TREE_UP_HQ 4  // k-steps of W per register chunk in the up kernel (measured, r01_tuning.md)
+#endif
 __host__ __device__ constexpr int tree_mpad(int m, int nt) { return (m + nt * 8 - 1) / (nt * 8) * (nt * 8); }
 __host__ __device__ constexpr int tree_up_stride(int mpad) { return mpad + 4; }
 __host__ __device__ constexpr int tree_down_stride(int mpad) { return mpad + 2; }
@@ -67,15 +70,15 @@ __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t
   const int i = lane >> 2, j = lane & 3;
   const int64_t node = n0 + nd;
   const int mg = sub % MG;
-  // The warp's whole slice of W (2k rows x 16 rank columns, one LDG.128 per
-  // k-step) is requested before the staged children are waited for, so the
-  // generator stream and the staging overlap instead of running back to back.
-  double2 a[NQ];
-  {
-    const double* ap = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16 + (int64_t)j * KT + 2 * i;
+  // The warp's slice of W (2k rows x 16 rank columns, one LDG.128 per k-step)
+  // streams in chunks of HQ k-steps; the first chunk is requested before the
+  // staged children are waited for, so the generator stream and the staging
+  // overlap. HQ < NQ bounds the registers (more CTAs per SM).
+  constexpr int HQ = HM_TREE_UP_HQ < NQ ? HM_TREE_UP_HQ : NQ;
+  const double* ap = P.W + ((1ll << l) - 2 + node) * 2 * KT * KT + mg * 16 + (int64_t)j * KT + 2 * i;
+  double2 a[HQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) a[q] = ldg_stream2(ap + (int64_t)q * 4 * KT);
-  }
+  for (int q = 0; q < HQ; ++q) a[q] = ldg_stream2(ap + (int64_t)q * 4 * KT);
   cp_async_wait_all();
   __syncthreads();
   // the 4 warps of a node split MG rank groups x column chunks; narrower chunks
@@ -85,6 +88,7 @@ __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t
     const double* bp = sm + nd * 2 * KT * zs + j * zs + i;
     double* out = P.xh + ((1ll << l) - 2 + node) * km + (int64_t)mg * 16 * m;
     const int nck = mp / (NTU * 8);
+    bool loaded = true;  // a[] holds chunk 0
     for (int ck = sub / MG; ck < nck; ck += CKS) {
       const int c0 = ck * NTU * 8;
       double acc[2][NTU][2];
@@ -93,14 +97,22 @@ __device__ __forceinline__ void tree_up_pair(const TreeParams& P, int l, int64_t
 #pragma unroll
         for (int nt = 0; nt < NTU; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        double bf[NTU];
+      for (int q0 = 0; q0 < NQ; q0 += HQ) {
+        if (!loaded) {
 #pragma unroll
-        for (int nt = 0; nt < NTU; ++nt) bf[nt] = bp[q * 4 * zs + c0 + nt * 8];
+          for (int q = 0; q < HQ; ++q) a[q] = ldg_stream2(ap + (int64_t)(q0 + q) * 4 * KT);
+        }
+        loaded = false;
 #pragma unroll
-        for (int nt = 0; nt < NTU; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[q].x, bf[nt]);
+        for (int q = 0; q < HQ; ++q) {
+          double bf[NTU];
 #pragma unroll
-        for (int nt = 0; nt < NTU; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a[q].y, bf[nt]);
+          for (int nt = 0; nt < NTU; ++nt) bf[nt] = bp[(q0 + q) * 4 * zs + c0 + nt * 8];
+#pragma unroll
+          for (int nt = 0; nt < NTU; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], a[q].x, bf[nt]);
+#pragma unroll
+          for (int nt = 0; nt < NTU; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], a[q].y, bf[nt]);
+        }
       }
       store_transposed<1, NTU>(acc, out, m, c0, m, lane);
     }

@@ -419,8 +419,16 @@ hm_status launch_leaf_gemv(const hm::LeafParams& lp, int64_t nleaves, cudaStream
 // (RG, NT) -> prefetch depth and launch-bound occupancy (measured, r01_tuning.md)
 template <int RG, int NT>
 struct LeafMmaTune {
+#ifdef HM_LEAF_PF_OVR  // development overrides (tools/kbench.py A/B builds)
+  static constexpr int PF = HM_LEAF_PF_OVR;
+#else
   static constexpr int PF = (RG == 2 && NT == 4) ? 1 : 2;
+#endif
+#ifdef HM_LEAF_MINB_OVR
+  static constexpr int MINB = HM_LEAF_MINB_OVR;
+#else
   static constexpr int MINB = (RG == 2 && NT == 4) ? 4 : 0;
+#endif
 };
 
 template <int RG, int NT>

@@ -594,13 +594,32 @@ __device__ __forceinline__ int tile_row(int rg, int i) {
   return PAIR ? 16 * (rg >> 1) + 2 * i + (rg & 1) : 8 * rg + i;
 }
 
+// Load policy of the row-major A stream (leaf pass D and U rows): a warp
+// instruction covers 64 B of 8 rows, so every 128-B line is completed by a
+// later instruction. 0: ld.global.cs (evict-first); 1: ld.global.nc (evict
+// normal); 2: evict-normal with an L2 256-B prefetch of the line pair.
+#ifndef HM_LDA_POLICY
+#define HM_LDA_POLICY 2  // measured: config-4 leaf DRAM read 7.60 -> 6.71 GB (= algorithmic), 1539 -> 1485 us
+#endif
+__device__ __forceinline__ double2 ld_a_stream2(const double* p) {
+#if HM_LDA_POLICY == 0
+  return ldg_stream2(p);
+#elif HM_LDA_POLICY == 1
+  return __ldg(reinterpret_cast<const double2*>(p));
+#else
+  double2 v;
+  asm volatile("ld.global.nc.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#endif
+}
+
 template <int RG, int PF, bool PAIR = false>
 __device__ __forceinline__ void rm_load(double2 (&a)[PF][RG], const double* base, int64_t lda, int q, int nq) {
 #pragma unroll
   for (int u = 0; u < PF; ++u)
 #pragma unroll
     for (int rg = 0; rg < RG; ++rg)
-      a[u][rg] = (q + u < nq) ? ldg_stream2(base + (int64_t)tile_row<PAIR>(rg, 0) * lda + 8 * (q + u))
+      a[u][rg] = (q + u < nq) ? ld_a_stream2(base + (int64_t)tile_row<PAIR>(rg, 0) * lda + 8 * (q + u))
                               : make_double2(0.0, 0.0);
 }
 

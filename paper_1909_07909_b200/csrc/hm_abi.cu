@@ -577,6 +577,55 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
   return fail(HM_ERR_UNSUPPORTED, "vt_mma: no instance for k=%d nt=%d", k, nt);
 }
 
+// Many right-hand sides: the level-parallel pipelined kernel (vt_lv_kernel, X
+// and V read once). Returns HM_ERR_UNSUPPORTED when the shape does not fit it.
+#ifndef HM_VT_LV_MIN_M
+#define HM_VT_LV_MIN_M 17  // X re-reads of vt_mma_levels fall out of L2 above this (config 3, m = 64)
+#endif
+#ifndef HM_VT_LV_NW
+#define HM_VT_LV_NW 16
+#endif
+#ifndef HM_VT_LV_NT
+#define HM_VT_LV_NT 2
+#endif
+template <int KT, int IPW, int NS>
+hm_status vt_lv_launch(const hm::VtParams& vp, int64_t b, size_t smem, cudaStream_t s) {
+  constexpr int NW = HM_VT_LV_NW, NT = HM_VT_LV_NT;
+  allow_smem(hm::vt_lv_kernel<KT, NT, IPW, 16, NS, NW>, smem);
+  return launch("vt_lv", s, [&] {
+    hm::vt_lv_kernel<KT, NT, IPW, 16, NS, NW><<<(unsigned)(vp.n / (8 * b)), NW * 32, smem, s>>>(vp, b);
+  });
+}
+
+hm_status vt_lv_dispatch(const hm::VtParams& vp, int64_t b, int k, cudaStream_t s) {
+  constexpr int R = 16, NW = HM_VT_LV_NW, MC = 8 * HM_VT_LV_NT;
+  if (HM_VT_LV_MIN_M <= 0 || vp.m < HM_VT_LV_MIN_M || !(k == 16 || k == 32) || b % R != 0 || vp.nlev < 1)
+    return HM_ERR_UNSUPPORTED;
+  const int mp = (vp.m + MC - 1) / MC * MC;
+  const int items = vp.nlev * (k / 16) * (mp / MC);
+  const int ipw = (items + NW - 1) / NW;
+  if (ipw > 4) return HM_ERR_UNSUPPORTED;
+  const int64_t sd = hm::vt_lv_stage_doubles(R, k, vp.nlev, mp);
+  int ns = 0;
+  if (4 * sd * 8 <= 220 * 1024) ns = 4;
+  else if (2 * sd * 8 <= 220 * 1024) ns = 2;
+  if (!ns) return HM_ERR_UNSUPPORTED;
+  const size_t smem = (size_t)ns * sd * 8;
+#define HM_LV(KT_, IPW_)                                                               \
+  if (k == KT_ && ipw == IPW_)                                                         \
+    return ns == 4 ? vt_lv_launch<KT_, IPW_, 4>(vp, b, smem, s) : vt_lv_launch<KT_, IPW_, 2>(vp, b, smem, s);
+  HM_LV(16, 1) HM_LV(16, 2) HM_LV(16, 3) HM_LV(16, 4)
+  HM_LV(32, 1) HM_LV(32, 2) HM_LV(32, 3) HM_LV(32, 4)
+#undef HM_LV
+  return HM_ERR_UNSUPPORTED;
+}
+
+hm_status vt_mma_any(const hm::VtParams& vp, int64_t b, int k, int nt, cudaStream_t s) {
+  const hm_status st = vt_lv_dispatch(vp, b, k, s);
+  if (st != HM_ERR_UNSUPPORTED) return st;
+  return vt_mma_dispatch(vp, b, k, nt, s);
+}
+
 template <int KT, int NT>
 #ifndef HM_VTB_MPW
 #define HM_VTB_MPW 2  // 32 rank columns per warp when k allows (measured, r01_tuning.md)
@@ -661,12 +710,12 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
         if (vp.lev[h].k == kg) vg.lev[vg.nlev++] = vp.lev[h];
       if (nrhs == 1 && pow2_rank(kg, 1, 64)) st = vt_gemv_dispatch(vg, P.b, kg, stream);
       else if (nrhs >= 2 && pow2_rank(kg, 1, 64))
-        st = vt_mma_dispatch(vg, P.b, kg, vt_mma_nt(kg, nrhs), stream);
+        st = vt_mma_any(vg, P.b, kg, vt_mma_nt(kg, nrhs), stream);
       else st = vt_generic(vg, P.n, stream);  // same 8-leaf tiles (P.tile), P.mc_vt columns
       if (st) return st;
     }
   } else if (P.vt == VtPath::kGemv) st = vt_gemv_dispatch(vp, P.b, P.k, stream);
-  else if (P.vt == VtPath::kMma) st = vt_mma_dispatch(vp, P.b, P.k, P.nt_vt, stream);
+  else if (P.vt == VtPath::kMma) st = vt_mma_any(vp, P.b, P.k, P.nt_vt, stream);
   else st = vt_generic(vp, P.n, stream);
   if (st) return st;
   if (rp.nlev > 0) {

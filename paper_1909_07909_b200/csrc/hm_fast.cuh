@@ -951,6 +951,170 @@ __device__ __forceinline__ void warp_transposed_mma_small(double (&acc)[1][NT][2
     }
   }
 }
+// HODLR, many right-hand sides (m > 16): vt_mma_levels re-reads a tile's X rows
+// once per level, and with m = 64 the live X tiles of all resident CTAs (1 MB
+// each) exceed L2 — ncu on config 3, m = 64: 8.0 GB of DRAM reads for 2.1 GB of
+// V and X. vt_lv_kernel reads X and V exactly once: the CTA walks its 8-leaf
+// tile in chunks of R rows; a cp.async pipeline of NS stages holds, per chunk,
+// the R rows of X (row stride m_pad + 4) and of every level's V (row stride
+// KT + 4); warps own work items (level, 16-rank-column group, column chunk of
+// 8 NT) — up to IPW each for NW warps, accumulators in registers across the
+// chunks of a node — with A fragments (V, 128-bit) and B fragments (X, 64-bit)
+// both from shared memory. NW = 16 warps, NT = 2: with 8 warps and NT = 4
+// (ncu, config 3 m = 64) the tensor pipe was 57% active, stalled on DMMA
+// dependency waits with 2 warps per SMSP. A node's sum is written when its last chunk is done (nodes
+// inside the tile) or as the tile's partial (nodes spanning tiles; fixed-order
+// reduce_partials). Shared-memory strides: 128-bit loads of V rows 4q + j,
+// columns 2i (8 lanes per wavefront) need KT + 4 = 4 (mod 16) doubles... for
+// KT = 16 that is 20; the X rows j apart need m_pad + 4 = 4 (mod 8).
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_groups() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__host__ __device__ constexpr int vt_lv_vstride(int kt) { return kt + 4; }
+__host__ __device__ constexpr int vt_lv_xstride(int mpad) { return mpad + 4; }
+// doubles of one pipeline stage: R rows of every level's V and of X
+__host__ __device__ constexpr int64_t vt_lv_stage_doubles(int r, int kt, int nlev, int mpad) {
+  return (int64_t)r * ((int64_t)nlev * vt_lv_vstride(kt) + vt_lv_xstride(mpad));
+}
+
+template <int KT, int NT, int IPW, int R, int NS, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) vt_lv_kernel(const VtParams P, int64_t b) {
+  extern __shared__ double stg[];
+  constexpr int BS = NW * 32;
+  constexpr int MC = NT * 8;
+  constexpr int G = KT / 16;  // 16-rank-column groups per level
+  constexpr int VS = vt_lv_vstride(KT);
+  constexpr int VH = KT / 2;  // 16-byte pieces per V row
+  constexpr int VP = R * VH;  // pieces per level and chunk
+  static_assert(BS % VP == 0 || VP % BS == 0, "V staging split");
+  const int m = P.m, nlev = P.nlev;
+  const int mp = (m + MC - 1) / MC * MC;
+  const int XS = vt_lv_xstride(mp);
+  const int sd = (int)vt_lv_stage_doubles(R, KT, nlev, mp);
+  const int64_t T = 8 * b;  // tile rows
+  const int64_t row0 = (int64_t)blockIdx.x * T;
+  const int nch = (int)(T / R);
+  const int nck = mp / MC;
+  const int nitems = nlev * G * nck;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = lane >> 2, j = lane & 3;
+  const int xoff = nlev * R * VS;  // X region of a stage
+
+  // staging: per-thread piece coordinates computed once (no division per chunk)
+  const int vL0 = BS >= VP ? threadIdx.x / VP : 0, vLs = BS >= VP ? BS / VP : 1;
+  const int ve = BS >= VP ? threadIdx.x % VP : threadIdx.x;
+  const bool xvec = (m & 1) == 0;
+  const int XH = xvec ? m / 2 : m;  // pieces per X row
+  const int xr0 = threadIdx.x / XH, xc0 = threadIdx.x % XH, xdr = BS / XH, xdc = BS % XH;
+  auto stage = [&](int c) {
+    double* dst = stg + (c % NS) * sd;
+    const int64_t r0 = row0 + (int64_t)c * R;
+    for (int L = vL0; L < nlev; L += vLs) {
+      const double* src = P.lev[L].V + r0 * KT;
+      double* d = dst + L * R * VS;
+      for (int e = ve; e < VP; e += (BS >= VP ? VP : BS)) {
+        const int r = e / VH, c2 = (e % VH) * 2;  // VH constexpr: shifts
+        cp_async16(d + r * VS + c2, src + r * KT + c2);
+      }
+    }
+    double* dx = dst + xoff;
+    const double* xsrc = P.X + r0 * m;
+    for (int r = xr0, cc = xc0; r < R;) {
+      if (xvec) cp_async16(dx + r * XS + 2 * cc, xsrc + (int64_t)r * m + 2 * cc);
+      else dx[r * XS + cc] = __ldg(xsrc + (int64_t)r * m + cc);
+      r += xdr;
+      cc += xdc;
+      if (cc >= XH) { cc -= XH; ++r; }
+    }
+    cp_async_commit_group();
+  };
+  // zero the padded X columns of every buffer once (never written by the stages)
+  if (mp > m)
+    for (int bf = 0; bf < NS; ++bf) {
+      double* dx = stg + bf * sd + xoff;
+      for (int e = threadIdx.x; e < R * (mp - m); e += BS) {
+        const int r = e / (mp - m);
+        dx[r * XS + m + (e - r * (mp - m))] = 0.0;
+      }
+    }
+
+  // work items of this warp, decoded once
+  int ia[IPW], ib[IPW], icpn[IPW], icmax[IPW];  // A / B offsets in a stage, chunks per node (0: spans tiles), column limit
+  double* iout[IPW];
+#pragma unroll
+  for (int u = 0; u < IPW; ++u) {
+    const int t = warp + NW * u;
+    const int tt = t < nitems ? t : 0;
+    const int L = tt / (G * nck), rem = tt - L * G * nck;
+    const int g = rem / nck, ck = rem - g * nck;
+    ia[u] = L * R * VS + j * VS + g * 16 + 2 * i;
+    ib[u] = xoff + j * XS + ck * MC + i;
+    const VtLevel& lv = P.lev[L];
+    const bool inside = lv.s <= T;
+    icpn[u] = inside ? (int)(lv.s / R) : 0;
+    icmax[u] = m - 2 * j - ck * MC;  // columns ck MC + 8 nt + 2 j (+1) valid while < m
+    // node output base (inside: node of the tile's first row; advanced per node) or tile partial
+    iout[u] = (inside ? lv.out + (row0 / lv.s) * KT * m : lv.partial + (int64_t)blockIdx.x * KT * m) +
+              (int64_t)(g * 16 + 2 * i) * m + ck * MC + 2 * j;
+  }
+
+  double acc[IPW][2][NT][2];
+#pragma unroll
+  for (int u = 0; u < IPW; ++u)
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[u][t][nt][0] = acc[u][t][nt][1] = 0.0;
+
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) stage(c);
+    else cp_async_commit_group();  // keep the group count uniform
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait_groups<NS - 2>();  // chunk c has landed (this thread's copies)
+    __syncthreads();                 // ... and everyone's; buffer (c-1) % NS is free
+    if (c + NS - 1 < nch) stage(c + NS - 1);
+    else cp_async_commit_group();
+    const double* buf = stg + (c % NS) * sd;
+#pragma unroll
+    for (int u = 0; u < IPW; ++u) {
+      if (warp + NW * u >= nitems) break;  // warp-uniform
+      const double* va = buf + ia[u];
+      const double* xb = buf + ib[u];
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        const double2 a = *reinterpret_cast<const double2*>(va + q * 4 * VS);
+        double bf[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bf[nt] = xb[q * 4 * XS + nt * 8];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma(acc[u][0][nt][0], acc[u][0][nt][1], a.x, bf[nt]);
+          dmma(acc[u][1][nt][0], acc[u][1][nt][1], a.y, bf[nt]);
+        }
+      }
+      // node complete (inside the tile) or tile complete (node spans tiles)
+      const bool flush = icpn[u] ? ((c + 1) & (icpn[u] - 1)) == 0 : (c == nch - 1);
+      if (flush) {
+        double* o = iout[u];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            double* oe = o + (int64_t)e * m + nt * 8;
+            if (nt * 8 < icmax[u]) oe[0] = acc[u][e][nt][0];
+            if (nt * 8 + 1 < icmax[u]) oe[1] = acc[u][e][nt][1];
+            acc[u][e][nt][0] = acc[u][e][nt][1] = 0.0;
+          }
+        iout[u] += (int64_t)KT * m;  // next node of the level (inside the tile)
+      }
+    }
+  }
+  cp_async_wait_groups<0>();
+}
+
 // HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
 // Per level: warp partial t over its b rows (DMMA), staged in shared memory,
 // then fixed-order sums over the warps of each node.

@@ -88,6 +88,7 @@ def emulate_hss(hd, n, p, b, k, g, X, P):
     (4096, 64, 6, 8, 3, 4),            # generic kernels
     (2048, 64, 5, 16, 2, 32),          # one leaf per rank (P = 2^p)
     (1 << 16, 128, 9, 32, 33, 2),
+    (1 << 16, 256, 8, 16, 64, 4),      # vt_lv on the subtree, top levels as tile partials
 ])
 def test_hodlr_dist_emulated(hm, n, b, p, k, m, P):
     from paper_1909_07909_b200 import dist as hd

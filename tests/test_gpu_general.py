@@ -135,7 +135,7 @@ def test_uniform_tree_per_level_ranks_tuned_kernels(hm, n, leaf, p, ranks, m):
     hm.hm_profile_enable(False)
     names = {t[0] for t in hm.hm_profile_collect()}
     assert not any(nm.startswith("gen_") for nm in names), names
-    assert names & {"vt_gemv", "vt_mma_levels"}, names
+    assert names & {"vt_gemv", "vt_mma_levels", "vt_lv"}, names
     assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X)) <= TOL
     assert relerr(Yt.cpu().numpy(), oracle.hodlr_matvec_t(n, p, ranks, D, U, V, X)) <= TOL
     # bitwise repeatable (fixed-order reductions)

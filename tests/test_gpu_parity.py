@@ -88,6 +88,9 @@ HODLR_CASES = [
     (65536, 256, 8, 8, 64),
     (16384, 128, 7, 2, 9),      # small-rank DMMA, ragged column chunk
     (16384, 64, 8, 1, 2),
+    (32768, 128, 8, 32, 32),    # level-parallel pipelined V^T X (vt_lv, m > 16)
+    (16384, 64, 8, 16, 17),     # vt_lv, odd m: synchronous X staging, padded columns
+    (65536, 256, 8, 16, 48),    # vt_lv, 3 work items per warp
 ]
 
 

@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches <launches.csv>            # per-kernel share of a step
     python tools/ncu_summary.py report <file.ncu-rep> [alg_bytes]  # key metrics of one capture
+    python tools/ncu_summary.py raw <file.raw.csv> [alg_bytes]     # same, from `ncu -i .. --page raw --csv`
 """
 import csv
 import io
@@ -35,8 +36,9 @@ UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "byte": 1.0, "u
         "nsecond": 1e-9, "second": 1.0, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}
 
 
-def report(path, alg_bytes=None):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def report(path, alg_bytes=None, raw_csv=None):
+    out = raw_csv if raw_csv is not None else subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                                                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units, r = rows[0], rows[1], rows[2]
     res = {"kernel": r[h.index("Kernel Name")]}
@@ -60,21 +62,31 @@ def report(path, alg_bytes=None):
 
 
 def launches(path):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
-    h = rows[0]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    tot, cnt = {}, {}
-    for r in rows[1:]:
-        name = r[ki].split("(")[0].replace("void ", "")
-        tot[name] = tot.get(name, 0.0) + float(r[vi].replace(",", "")) / 1e3
-        cnt[name] = cnt.get(name, 0) + 1
+    """Per-kernel totals of a `--metrics gpu__time_duration.sum[,dram__bytes_*]` launch list."""
+    txt = open(path).read()
+    rows = list(csv.DictReader(io.StringIO(txt[txt.find('"ID"'):])))
+    tot, cnt, dram, seen = {}, {}, {}, set()
+    for r in rows:
+        name = r["Kernel Name"].split("(")[0].replace("void ", "")
+        v = float(r["Metric Value"].replace(",", "")) * UNIT.get(r["Metric Unit"], 1.0)
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            tot[name] = tot.get(name, 0.0) + v * 1e6
+            if r["ID"] not in seen:
+                seen.add(r["ID"])
+                cnt[name] = cnt.get(name, 0) + 1
+        elif r["Metric Name"].startswith("dram__bytes"):
+            dram[name] = dram.get(name, 0.0) + v
     all_us = sum(tot.values())
-    return {k: {"launches": cnt[k], "us_total": round(v, 1), "share": round(v / all_us, 4)}
+    return {k: {"launches": cnt[k], "us_total": round(v, 1), "share": round(v / all_us, 4),
+                **({"dram_GB": round(dram[k] / 1e9, 3), "dram_GBps": round(dram[k] / (v * 1e-6) / 1e9, 1)}
+                   if k in dram else {})}
             for k, v in sorted(tot.items(), key=lambda kv: -kv[1])}
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
+    elif sys.argv[1] == "raw":
+        print(json.dumps(report(None, sys.argv[3] if len(sys.argv) > 3 else None, open(sys.argv[2]).read()), indent=1))
     else:
         print(json.dumps(report(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None), indent=1))

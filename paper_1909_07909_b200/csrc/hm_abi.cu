@@ -976,7 +976,10 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 
 // Levels with at least kTreeBigLevel nodes run one launch per level; the
 // levels above run inside one cooperative launch (hss_tree_sweep_kernel).
-constexpr int64_t kTreeBigLevel = 2048;
+#ifndef HM_TREE_BIG_LEVEL
+#define HM_TREE_BIG_LEVEL 2048
+#endif
+constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
 
 // ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
 #ifndef HM_GEMV_BIG

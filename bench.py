@@ -362,6 +362,30 @@ def sweep(torch, device, wl, peak):
                                                  "ranks": f"{tag} by level", "kernels": kern}
         del hv, X, Y, ws
     del h3
+    # general cluster tree (f4) at the config-3 scale: ragged leaves of
+    # 128..384 rows (config-3 mean 256), k = 16 on every level; general-tree kernels
+    rng = np.random.default_rng(hm_inputs.MASTER_SEED + 9)
+    nl = 1 << c3.levels
+    sizes = rng.integers(128, 385, size=nl)
+    c_end = np.cumsum(sizes).astype(np.int64)
+    ng = int(c_end[-1])
+    Dg = torch.randn(int((sizes.astype(np.int64) ** 2).sum()), dtype=torch.float64, device=device, generator=g)
+    Ug = torch.randn(c3.levels * ng * c3.k, dtype=torch.float64, device=device, generator=g)
+    Vg = torch.randn(c3.levels * ng * c3.k, dtype=torch.float64, device=device, generator=g)
+    rk = [c3.k] * c3.levels
+    for m in (1, 8):
+        X = torch.randn(ng, m, dtype=torch.float64, device=device, generator=g)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hodlr_general_workspace_bytes(ng, c3.levels, c_end, rk, m), dtype=torch.uint8,
+                         device=device)
+        nb = 8 * (int((sizes.astype(np.int64) ** 2).sum()) + 2 * c3.levels * ng * c3.k + 2 * ng * m)
+        ms = _time_call(torch, lambda: hm.hodlr_matvec_general(ng, c3.levels, c_end, rk, Dg, Ug, Vg, X, 0, Y, ws), 5)
+        out[f"c3_ragged_m{m}"] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms),
+                                  "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
+                                  "tree": f"{nl} leaves of 128..384 rows, n = {ng}, k = {c3.k}",
+                                  "path": "general-tree kernels"}
+        del X, Y, ws
+    del Dg, Ug, Vg
     # config 5 and 4 adjoints on the bench's own generators
     h, s4 = wl.h5, wl.s4
     ms = _time_call(torch, lambda: hm.hodlr_matvec_t(C5.n, C5.levels, C5.leaf, h.ranks, h.D, h.U, h.V, wl.X5, wl.Y5,

@@ -1548,7 +1548,7 @@ void gen_add_vt_level(GenPlan* G, int l) {
 int pick_gen_mc(int64_t smax, int64_t ktot, int32_t m) {
   int mc = 1;
   while (mc < hm::kMaxMc && mc < m) mc <<= 1;
-  while (mc > 1 && (smax + ktot) * mc > kSmemBudgetDoubles) mc >>= 1;
+  while (mc > 1 && (smax + ktot) * hm::gen_leaf_zs(mc) > kSmemBudgetDoubles) mc >>= 1;
   return mc;
 }
 
@@ -1580,6 +1580,20 @@ hm_status gen_upload_tables(const GenPlan& G, char* w, cudaStream_t s) {
 
 // V^T X for every vt level: chunk partials then fixed-order per-node sums.
 // `Vlev[L]`, `outlev[L]`, `klev[L]` per vt level.
+template <int KT, int NT>
+hm_status gen_vt_mma_launch(const hm::GenVtParams& vp, int64_t nchunks, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)(8 * KT * NT * 8);
+  allow_smem(hm::gen_vt_mma_kernel<KT, NT>, smem);
+  dim3 grid((unsigned)nchunks, (unsigned)((vp.m + NT * 8 - 1) / (NT * 8)));
+  return launch("gen_vt_mma", s, [&] { hm::gen_vt_mma_kernel<KT, NT><<<grid, hm::kThreads, smem, s>>>(vp); });
+}
+
+hm_status gen_vt_mma_dispatch(const hm::GenVtParams& vp, int64_t nchunks, int k, cudaStream_t s) {
+  if (k == 16) return vp.m <= 16 ? gen_vt_mma_launch<16, 2>(vp, nchunks, s) : gen_vt_mma_launch<16, 4>(vp, nchunks, s);
+  if (k == 32) return vp.m <= 16 ? gen_vt_mma_launch<32, 2>(vp, nchunks, s) : gen_vt_mma_launch<32, 4>(vp, nchunks, s);
+  return gen_vt_mma_launch<64, 2>(vp, nchunks, s);
+}
+
 hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* const* outlev, const int32_t* klev,
                        const double* X, char* w, cudaStream_t s) {
   const int nlev = (int)G.vt_levels.size();
@@ -1611,8 +1625,21 @@ hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* cons
     rp.threads += lv.nodes * (int64_t)lv.k * G.m;
   }
   rp.thread_begin[nlev] = rp.threads;
+  // nrhs = 1 with even power-of-two ranks: 128-bit streaming GEMV per chunk
+  bool gemv = G.m == 1;
+  for (int L = 0; L < nlev; ++L) gemv = gemv && pow2_rank(klev[L], 2, 64);
   dim3 grid((unsigned)G.nchunks, (unsigned)((G.m + G.mc_vt - 1) / G.mc_vt));
-  hm_status st = launch("gen_vt_chunk", s, [&] { hm::gen_vt_chunk_kernel<<<grid, hm::kThreads, 0, s>>>(vp); });
+  // nrhs >= 2 with one rank in {16, 32, 64} on every level: DMMA per chunk
+  int kmma = G.m >= 2 ? klev[0] : 0;
+  for (int L = 0; L < nlev; ++L) kmma = (klev[L] == kmma && pow2_rank(kmma, 16, 64)) ? kmma : 0;
+  hm_status st;
+  if (gemv) {
+    st = launch("gen_vt_gemv", s, [&] { hm::gen_vt_gemv_kernel<<<(unsigned)G.nchunks, hm::kThreads, 0, s>>>(vp); });
+  } else if (kmma) {
+    st = gen_vt_mma_dispatch(vp, G.nchunks, kmma, s);
+  } else {
+    st = launch("gen_vt_chunk", s, [&] { hm::gen_vt_chunk_kernel<<<grid, hm::kThreads, 0, s>>>(vp); });
+  }
   if (st) return st;
   const unsigned rg = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
   return launch("gen_vt_reduce", s, [&] { hm::gen_vt_reduce_kernel<<<rg, hm::kThreads, 0, s>>>(rp); });
@@ -1620,15 +1647,36 @@ hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* cons
 
 template <int MC>
 hm_status gen_leaf_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * MC);
+  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * hm::gen_leaf_zs(MC));
   allow_smem(hm::gen_leaf_kernel<MC>, std::max<size_t>(smem, 1));
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + MC - 1) / MC));
   return launch(lp.dtrans ? "gen_leaf_t" : "gen_leaf", s,
                 [&] { hm::gen_leaf_kernel<MC><<<grid, hm::kThreads, smem, s>>>(lp); });
 }
 
+#ifndef HM_GEN_LEAF_MMA_MIN_M
+#define HM_GEN_LEAF_MMA_MIN_M 2
+#endif
+template <int NT, bool DT>
+hm_status gen_leaf_mma_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * (NT * 8 + 4));
+  allow_smem(hm::gen_leaf_mma_kernel<NT, DT>, std::max<size_t>(smem, 1));
+  dim3 grid((unsigned)nleaves, (unsigned)((lp.m + NT * 8 - 1) / (NT * 8)));
+  return launch(DT ? "gen_leaf_mma_t" : "gen_leaf_mma", s,
+                [&] { hm::gen_leaf_mma_kernel<NT, DT><<<grid, hm::kThreads, smem, s>>>(lp); });
+}
+
 hm_status gen_leaf_phase(const GenPlan& G, const hm::GenLeafParams& lp, cudaStream_t s) {
   const int64_t nl = (int64_t)1 << G.p;
+  // nrhs >= 2: DMMA leaf pass (8 NT columns per CTA) when the staged rows fit
+  if (G.m >= HM_GEN_LEAF_MMA_MIN_M) {
+    const int nt = G.m <= 8 ? 1 : (G.m <= 16 ? 2 : 4);
+    if ((G.smax + G.ktot) * (nt * 8 + 4) <= kSmemBudgetDoubles) {
+      if (nt == 1) return lp.dtrans ? gen_leaf_mma_launch<1, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<1, false>(lp, nl, G.smax, s);
+      if (nt == 2) return lp.dtrans ? gen_leaf_mma_launch<2, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<2, false>(lp, nl, G.smax, s);
+      return lp.dtrans ? gen_leaf_mma_launch<4, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<4, false>(lp, nl, G.smax, s);
+    }
+  }
   switch (G.mc_leaf) {
     case 1: return gen_leaf_launch<1>(lp, nl, G.smax, s);
     case 2: return gen_leaf_launch<2>(lp, nl, G.smax, s);

@@ -21,7 +21,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "hm_kernels.cuh"
+#include "hm_fast.cuh"
 
 namespace hm {
 
@@ -55,6 +55,57 @@ struct GenVtParams {
   int32_t pad;
   GenVtLevel lev[kMaxLevels];
 };
+
+// nrhs = 1, k a power of two in 2..64 (hm_fast.cuh vt_gemv on a ragged chunk):
+// a chunk's V rows are one contiguous run of (hi - lo) k doubles; every warp
+// streams its share as 128-bit chunks (lane l keeps rank columns (2l) % k and
+// (2l+1) % k, so accumulation stays in registers), x[r] from L1; butterfly
+// over the lanes sharing a column, fixed-order sum over the 8 warps.
+__global__ void __launch_bounds__(kThreads) gen_vt_gemv_kernel(const GenVtParams P) {
+  __shared__ double red[kThreads / 32][64];
+  const GenChunk ch = P.chunks[blockIdx.x];
+  const GenVtLevel lv = P.lev[ch.lev];
+  const int k = lv.k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ne = (ch.hi - ch.lo) * k;  // doubles of the chunk (even: k even)
+  const double* V = lv.V + ch.lo * k;
+  const double* X = P.X + ch.lo;
+  const int lk = __ffs(k) - 1;  // log2 k
+  double acc0 = 0.0, acc1 = 0.0;
+  constexpr int U = 4;
+  for (int64_t e0 = ((int64_t)warp * 32 + lane) * 2; e0 < ne; e0 += (int64_t)kThreads * 2 * U) {
+    double2 v[U];
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * kThreads * 2;
+      const bool ok = e < ne;
+      v[u] = ok ? __ldg(reinterpret_cast<const double2*>(V + e)) : make_double2(0.0, 0.0);
+      x[u] = ok ? __ldg(X + (e >> lk)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc0 = fma(v[u].x, x[u], acc0);
+      acc1 = fma(v[u].y, x[u], acc1);
+    }
+  }
+  // lane l holds columns (2l) % k, (2l+1) % k: lanes l, l + k/2, ... share them
+  for (int w = 16; w >= k / 2 && w >= 1; w >>= 1) {
+    acc0 += __shfl_xor_sync(0xffffffffu, acc0, w);
+    acc1 += __shfl_xor_sync(0xffffffffu, acc1, w);
+  }
+  if (2 * lane < k) {
+    red[warp][2 * lane] = acc0;
+    red[warp][2 * lane + 1] = acc1;
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) sum += red[w][threadIdx.x];
+    lv.partial[(ch.pidx - lv.chunk0) * (int64_t)k + threadIdx.x] = sum;
+  }
+}
 
 // CTA = one chunk x one column group. Thread o < O2 owns output (a = o % k,
 // c = o / k); G = 256 / O2 row groups stride the chunk; fixed-order sum over
@@ -91,6 +142,76 @@ __global__ void __launch_bounds__(kThreads) gen_vt_chunk_kernel(const GenVtParam
       for (int64_t r = ch.lo; r < ch.hi; ++r) acc = fma(lv.V[r * k + a], P.X[r * m + c0 + c], acc);
       dst[a * m + c0 + c] = acc;
     }
+  }
+}
+
+// nrhs >= 2, every level of rank KT in {16, 32, 64}: DMMA per chunk. Warp w
+// takes an 8th of the chunk's rows (a multiple of 4), t = V(rows)^T X(rows)
+// with the hm_fast.cuh fragment layout (one 128-bit load of a V row covers 16
+// rank columns; rows past the chunk end read as zero), then a fixed-order sum
+// over the 8 warps in shared memory. grid.y = column chunks of 8 NT.
+template <int KT, int NT>
+__global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams P) {
+  extern __shared__ double red[];  // [8][KT][8 NT]
+  constexpr int MC = NT * 8, MPW = KT / 16;
+  const GenChunk ch = P.chunks[blockIdx.x];
+  const GenVtLevel lv = P.lev[ch.lev];
+  const int m = P.m;
+  const int c0 = blockIdx.y * MC;
+  const int mc = min(MC, m - c0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = lane >> 2, j = lane & 3;
+  const int64_t len = ch.hi - ch.lo;
+  const int64_t slice = (len + 31) / 32 * 4;
+  const int64_t r0 = ch.lo + warp * slice;
+  const int64_t K = max((int64_t)0, min(ch.hi, r0 + slice) - r0);
+  double acc[2 * MPW][NT][2];
+#pragma unroll
+  for (int t = 0; t < 2 * MPW; ++t)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = nt * 8 + i < mc;
+  const double* A = lv.V + r0 * KT + 2 * i;
+  const double* B = P.X + r0 * m + c0 + i;
+#pragma unroll 4
+  for (int64_t q = 0; q < (K + 3) / 4; ++q) {
+    const int64_t row = 4 * q + j;
+    const bool ok = row < K;
+    double2 a[MPW];
+    double bf[NT];
+#pragma unroll
+    for (int mp = 0; mp < MPW; ++mp)
+      a[mp] = ok ? __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16)) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bf[nt] = (ok && colok[nt]) ? __ldg(B + row * m + nt * 8) : 0.0;
+#pragma unroll
+    for (int mp = 0; mp < MPW; ++mp)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[mp].x, bf[nt]);
+        dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[mp].y, bf[nt]);
+      }
+  }
+#pragma unroll
+  for (int t = 0; t < 2 * MPW; ++t) {
+    const int a = 16 * (t >> 1) + 2 * i + (t & 1);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double* o = red + ((int64_t)warp * KT + a) * MC + nt * 8 + 2 * j;
+      o[0] = acc[t][nt][0];
+      o[1] = acc[t][nt][1];
+    }
+  }
+  __syncthreads();
+  double* dst = lv.partial + (ch.pidx - lv.chunk0) * (int64_t)KT * m;
+  for (int o = threadIdx.x; o < KT * mc; o += kThreads) {
+    const int a = o / mc, c = o - a * mc;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) sum += red[((int64_t)w * KT + a) * MC + c];
+    dst[a * m + c0 + c] = sum;
   }
 }
 
@@ -134,6 +255,22 @@ struct GenLeafParams {
   LeafSeg seg[kMaxLevels];  // node of leaf i for segment s: (i >> shift) ^ xr
 };
 
+__host__ __device__ constexpr int gen_leaf_zs(int mc) { return mc == 1 ? 1 : mc + 2; }
+// one staged row of MC doubles (16-byte aligned for MC >= 2) into registers
+template <int MC>
+__device__ __forceinline__ void zrow(double (&z)[MC], const double* zr) {
+  if constexpr (MC == 1) {
+    z[0] = zr[0];
+  } else {
+#pragma unroll
+    for (int c = 0; c < MC; c += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(zr + c);
+      z[c] = t.x;
+      z[c + 1] = t.y;
+    }
+  }
+}
+
 // CTA = one leaf x one column chunk (MC = P.mc columns, MC <= kMaxMc). Z = [X(I_i);
 // T_1[node_1]; ...] staged in shared memory; warp per output row, lanes striding
 // the extended row, butterfly reduction (fixed order).
@@ -145,61 +282,195 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
   if (b == 0) return;  // empty leaf: no rows
   const int c0 = blockIdx.y * MC;
   const int mc = min(MC, P.m - c0);
-  double* Z = smem;  // [(b + ktot)][MC]
+  // Z rows padded to ZS doubles: lanes read whole rows (jj = lane + 32 v) as
+  // 128-bit loads; ZS = MC + 2 (80 B for MC = 8) puts a quarter-warp's rows in
+  // distinct bank groups.
+  constexpr int ZS = gen_leaf_zs(MC);
+  double* Z = smem;  // [(b + ktot)][ZS]
   for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
     const int64_t r = e / MC;
     const int c = (int)(e - r * MC);
-    Z[e] = (c < mc) ? P.X[(r0 + r) * P.m + c0 + c] : 0.0;
+    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * P.m + c0 + c] : 0.0;
   }
   {
-    int64_t off = b * MC;
+    int64_t off = b;
     for (int s = 0; s < P.nseg; ++s) {
       const LeafSeg sg = P.seg[s];
       const int64_t node = (leaf >> sg.shift) ^ sg.xr;
       const double* T = sg.T + node * sg.k * P.m;
       for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
         const int a = e / MC, c = e - a * MC;
-        Z[off + e] = (c < mc) ? T[a * P.m + c0 + c] : 0.0;
+        Z[(off + a) * ZS + c] = (c < mc) ? T[a * P.m + c0 + c] : 0.0;
       }
-      off += (int64_t)sg.k * MC;
+      off += sg.k;
     }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Di = P.D + P.doff[leaf];
-  for (int64_t r = warp; r < b; r += kThreads / 32) {
-    double acc[MC];
+  // A warp owns GR rows at a time (rows r0w + 8u): every lane requests GR x UJ
+  // elements of D (and then of each level's U rows) before the first FMA, so
+  // a warp keeps GR * UJ loads in flight instead of one (memory-level
+  // parallelism for the HBM-bound leaf pass); lanes stride the columns.
+  constexpr int GR = MC <= 4 ? 4 : 2;
+  constexpr int UJ = 4;
+  for (int64_t rw = warp; rw < b; rw += GR * (kThreads / 32)) {
+    double acc[GR][MC];
 #pragma unroll
-    for (int c = 0; c < MC; ++c) acc[c] = 0.0;
-    for (int64_t j = lane; j < b; j += 32) {
-      const double d = P.dtrans ? Di[j * b + r] : Di[r * b + j];
+    for (int u = 0; u < GR; ++u)
 #pragma unroll
-      for (int c = 0; c < MC; ++c) acc[c] = fma(d, Z[j * MC + c], acc[c]);
+      for (int c = 0; c < MC; ++c) acc[u][c] = 0.0;
+    bool rok[GR];
+#pragma unroll
+    for (int u = 0; u < GR; ++u) rok[u] = rw + 8 * u < b;
+    for (int64_t j0 = lane; j0 < b; j0 += 32 * UJ) {
+      double d[GR][UJ];
+#pragma unroll
+      for (int u = 0; u < GR; ++u)
+#pragma unroll
+        for (int v = 0; v < UJ; ++v) {
+          const int64_t r = rw + 8 * u, jj = j0 + 32 * v;
+          d[u][v] = (rok[u] && jj < b) ? (P.dtrans ? __ldg(Di + jj * b + r) : __ldg(Di + r * b + jj)) : 0.0;
+        }
+#pragma unroll
+      for (int v = 0; v < UJ; ++v) {
+        const int64_t jj = j0 + 32 * v;
+        if (jj >= b) break;
+        double z[MC];
+        zrow<MC>(z, Z + jj * ZS);
+#pragma unroll
+        for (int c = 0; c < MC; ++c)
+#pragma unroll
+          for (int u = 0; u < GR; ++u) acc[u][c] = fma(d[u][v], z[c], acc[u][c]);
+      }
     }
     int64_t off = b;
-    for (int s = 0; s < P.nseg; ++s) {
-      const LeafSeg sg = P.seg[s];
-      const double* Ar = sg.A + (r0 + r) * sg.k;
-      for (int a = lane; a < sg.k; a += 32) {
-        const double u = Ar[a];
+    for (int sgi = 0; sgi < P.nseg; ++sgi) {
+      const LeafSeg sg = P.seg[sgi];
+      for (int a0 = lane; a0 < sg.k; a0 += 32) {
+        double uu[GR];
 #pragma unroll
-        for (int c = 0; c < MC; ++c) acc[c] = fma(u, Z[(off + a) * MC + c], acc[c]);
+        for (int u = 0; u < GR; ++u) uu[u] = rok[u] ? __ldg(sg.A + (r0 + rw + 8 * u) * sg.k + a0) : 0.0;
+        double z[MC];
+        zrow<MC>(z, Z + (off + a0) * ZS);
+#pragma unroll
+        for (int c = 0; c < MC; ++c)
+#pragma unroll
+          for (int u = 0; u < GR; ++u) acc[u][c] = fma(uu[u], z[c], acc[u][c]);
       }
       off += sg.k;
     }
 #pragma unroll
-    for (int c = 0; c < MC; ++c) {
-      double v = acc[c];
+    for (int u = 0; u < GR; ++u) {
 #pragma unroll
-      for (int w = 16; w >= 1; w >>= 1) v += __shfl_xor_sync(0xffffffffu, v, w);
-      acc[c] = v;
+      for (int c = 0; c < MC; ++c) {
+        double v = acc[u][c];
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) v += __shfl_xor_sync(0xffffffffu, v, w);
+        acc[u][c] = v;
+      }
+      if (rok[u] && lane < mc) {
+        double v = acc[u][0];
+#pragma unroll
+        for (int c = 1; c < MC; ++c)
+          if (c == lane) v = acc[u][c];
+        P.Y[(r0 + rw + 8 * u) * P.m + c0 + lane] = v;
+      }
     }
-    if (lane < mc) {
-      double v = acc[0];
+  }
+}
+
+// nrhs >= 2: the leaf pass on the fp64 tensor cores for any leaf size (ragged
+// trees). CTA = one leaf x one chunk of 8 NT columns; Z = [X(I_i); T_1; ..]
+// staged with row stride 8 NT + 4 (rows j apart: conflict-free). Warp w takes
+// the leaf's 8-row tiles w, w + 8, ..; per tile the DMMA A fragments are
+// D[8t + i][4q + j] (or D^T: D[4q + j][8t + i], DT) and U_s[8t + i][4q + j],
+// 64-bit loads with rows / contraction indices past the block read as zero, Q
+// k-steps requested before their DMMAs.
+template <int NT, bool DT>
+__global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafParams P) {
+  extern __shared__ double smem[];
+  constexpr int MC = NT * 8, ZS = MC + 4, Q = 4;
+  const int64_t leaf = blockIdx.x;
+  const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
+  if (b == 0) return;
+  const int c0 = blockIdx.y * MC;
+  const int m = P.m, mc = min(MC, m - c0);
+  double* Z = smem;  // [(b + ktot)][ZS]
+  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
+    const int64_t r = e / MC;
+    const int c = (int)(e - r * MC);
+    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * m + c0 + c] : 0.0;
+  }
+  int64_t off = b;
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    const double* T = sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m;
+    for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
+      const int a = e / MC, c = e - a * MC;
+      Z[(off + a) * ZS + c] = (c < mc) ? T[a * m + c0 + c] : 0.0;
+    }
+    off += sg.k;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = lane >> 2, j = lane & 3;
+  const double* Di = P.D + P.doff[leaf];
+  const int64_t ntile = (b + 7) / 8;
+  for (int64_t t = warp; t < ntile; t += kThreads / 32) {
+    const int64_t row = 8 * t + i;
+    const bool rok = row < b;
+    double acc[NT][2];
 #pragma unroll
-      for (int c = 1; c < MC; ++c)
-        if (c == lane) v = acc[c];
-      P.Y[(r0 + r) * P.m + c0 + lane] = v;
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    // leaf block: contraction over the b columns of D_i (rows of D_i^T)
+    for (int64_t q0 = 0; q0 < (b + 3) / 4; q0 += Q) {
+      double a[Q];
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        const int64_t kk = 4 * (q0 + u) + j;
+        a[u] = (rok && kk < b) ? __ldg(DT ? Di + kk * b + row : Di + row * b + kk) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        const int64_t kk = 4 * (q0 + u) + j;
+        if (4 * (q0 + u) >= b) break;  // warp-uniform
+        const double* zr = Z + (kk < b ? kk : 0) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < b ? zr[nt * 8] : 0.0);
+      }
+    }
+    // U segments: contraction over each segment's k rank columns
+    int64_t zo = b;
+    for (int s = 0; s < P.nseg; ++s) {
+      const LeafSeg sg = P.seg[s];
+      const double* Ar = sg.A + (r0 + (rok ? row : 0)) * sg.k;
+      for (int q0 = 0; q0 < (sg.k + 3) / 4; q0 += Q) {
+        double a[Q];
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          const int kk = 4 * (q0 + u) + j;
+          a[u] = (rok && kk < sg.k) ? __ldg(Ar + kk) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          const int kk = 4 * (q0 + u) + j;
+          if (4 * (q0 + u) >= sg.k) break;
+          const double* zr = Z + (zo + (kk < sg.k ? kk : 0)) * ZS + i;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < sg.k ? zr[nt * 8] : 0.0);
+        }
+      }
+      zo += sg.k;
+    }
+    if (rok) {
+      double* y = P.Y + (r0 + row) * m + c0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + 2 * j;
+        if (c < mc) y[c] = acc[nt][0];
+        if (c + 1 < mc) y[c + 1] = acc[nt][1];
+      }
     }
   }
 }

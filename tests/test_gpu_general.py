@@ -68,6 +68,33 @@ def test_hodlr_general_vs_oracle(hm, name, c, p, m):
 
 
 @pytest.mark.parametrize("name,c,p", TREES)
+@pytest.mark.parametrize("k,m,kernel", [(16, 1, "gen_vt_gemv"), (2, 1, "gen_vt_gemv"), (64, 1, "gen_vt_gemv"),
+                                        (16, 2, "gen_vt_mma"), (32, 9, "gen_vt_mma"), (64, 33, "gen_vt_mma"),
+                                        (16, 40, "gen_vt_mma")])
+def test_hodlr_general_one_rank_tuned_vt(hm, name, c, p, k, m, kernel):
+    """One rank on every level of a general tree: V^T X per chunk runs the
+    streaming GEMV (m = 1) or DMMA (k in 16/32/64) chunk kernel; ragged chunk
+    ends read as zero."""
+    n, p, c = tree(name, c, p)
+    if p == 0:
+        pytest.skip("no off-diagonal levels")
+    rng = np.random.default_rng(81 + k + m)
+    ranks = [k] * p
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    for op in (0, 1):
+        Y = hm.hodlr_matvec_general(n, p, c, ranks, dev(D), dev(U), dev(V), dev(X), op=op)
+        torch.cuda.synchronize()
+        f = oracle.hodlr_matvec_t if op else oracle.hodlr_matvec
+        assert relerr(Y.cpu().numpy(), f(n, p, ranks, D, U, V, X, c=c)) <= TOL, op
+    hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert kernel in names, names
+
+
+@pytest.mark.parametrize("name,c,p", TREES)
 @pytest.mark.parametrize("k,m", [(4, 1), (16, 16), (32, 3), (0, 2)])
 def test_hss_general_vs_oracle(hm, name, c, p, k, m):
     n, p, c = tree(name, c, p)

@@ -25,7 +25,25 @@ def run(name, reps):
     adj = name.endswith("t")
     if adj:
         name = name[:-1]
-    if name.startswith("c3") or name in ("c5", "c1"):
+    if name.startswith("cr"):  # ragged config-3-scale tree (general-tree kernels), e.g. cr1, cr8
+        import numpy as np
+        cfg = hm_inputs.CONFIGS[3]
+        m = int(name[2:])
+        rng = np.random.default_rng(9)
+        sizes = rng.integers(128, 385, size=1 << cfg.levels)
+        c = np.cumsum(sizes).astype(np.int64)
+        n = int(c[-1])
+        D = torch.randn(int((sizes.astype(np.int64) ** 2).sum()), dtype=torch.float64, device=dev)
+        U = torch.randn(cfg.levels * n * cfg.k, dtype=torch.float64, device=dev)
+        V = torch.randn(cfg.levels * n * cfg.k, dtype=torch.float64, device=dev)
+        X = torch.randn(n, m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        rk = [cfg.k] * cfg.levels
+        ws = torch.empty(hm.hm_hodlr_general_workspace_bytes(n, cfg.levels, c, rk, m), dtype=torch.uint8, device=dev)
+        f = lambda: hm.hodlr_matvec_general(n, cfg.levels, c, rk, D, U, V, X, 1 if adj else 0, Y, ws)
+        nbytes = 8 * (D.numel() + U.numel() + V.numel() + 2 * n * m)
+        flops = 2 * m * (D.numel() + U.numel() + V.numel())
+    elif name.startswith("c3") or name in ("c5", "c1"):
         cfg = hm_inputs.CONFIGS[{"c1": 1, "c5": 5}.get(name, 3)]
         m = int(name[3:]) if name.startswith("c3m") else 1
         if cfg.laplacian:

@@ -295,6 +295,31 @@ class DistWorkload:
 
 # ------------------------------------------------------ nrhs / ops sweep --
 
+def _graph_us(torch, f, calls=20, replays=20):
+    """Device us per call with `calls` calls captured in one CUDA graph (the
+    latency of a small, L2-resident product without host launch overhead)."""
+    try:
+        f()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            for _ in range(calls):
+                f()
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(replays):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) * 1e3 / (calls * replays), 2)
+    except Exception as e:  # report, do not fail the bench line
+        return f"graph capture failed: {type(e).__name__}: {e}"[:200]
+
+
 def _time_call(torch, f, reps, warm=2):
     """Device ms per call: CUDA events on the current stream around `reps` calls."""
     for _ in range(warm):
@@ -441,6 +466,8 @@ def sweep(torch, device, wl, peak):
                      device=device)
     ms = _time_call(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V, X, Y, ws), 200)
     out["c1_us"] = round(ms * 1e3, 2)
+    out["c1_us_graph"] = _graph_us(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V,
+                                                                  X, Y, ws))
     s2 = hm_inputs.device_hss_random(c2.n, c2.levels, c2.k, hm_inputs.MASTER_SEED + 2, device)
     X = torch.randn(c2.n, 16, dtype=torch.float64, device=device, generator=g)
     Y = torch.empty_like(X)
@@ -448,6 +475,8 @@ def sweep(torch, device, wl, peak):
     ms = _time_call(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R, s2.W, s2.B, X,
                                                  Y, ws), 200)
     out["c2_us"] = round(ms * 1e3, 2)
+    out["c2_us_graph"] = _graph_us(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R,
+                                                                s2.W, s2.B, X, Y, ws))
     return out
 
 

@@ -588,17 +588,20 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
 #ifndef HM_VT_LV_NT
 #define HM_VT_LV_NT 2
 #endif
+#ifndef HM_VT_LV_R
+#define HM_VT_LV_R 32  // rows per pipeline stage (measured: 8 / 16 / 32 -> 1216 / 1107 / 1033 us, config 3 m=64)
+#endif
 template <int KT, int IPW, int NS>
 hm_status vt_lv_launch(const hm::VtParams& vp, int64_t b, size_t smem, cudaStream_t s) {
   constexpr int NW = HM_VT_LV_NW, NT = HM_VT_LV_NT;
-  allow_smem(hm::vt_lv_kernel<KT, NT, IPW, 16, NS, NW>, smem);
+  allow_smem(hm::vt_lv_kernel<KT, NT, IPW, HM_VT_LV_R, NS, NW>, smem);
   return launch("vt_lv", s, [&] {
-    hm::vt_lv_kernel<KT, NT, IPW, 16, NS, NW><<<(unsigned)(vp.n / (8 * b)), NW * 32, smem, s>>>(vp, b);
+    hm::vt_lv_kernel<KT, NT, IPW, HM_VT_LV_R, NS, NW><<<(unsigned)(vp.n / (8 * b)), NW * 32, smem, s>>>(vp, b);
   });
 }
 
 hm_status vt_lv_dispatch(const hm::VtParams& vp, int64_t b, int k, cudaStream_t s) {
-  constexpr int R = 16, NW = HM_VT_LV_NW, MC = 8 * HM_VT_LV_NT;
+  constexpr int R = HM_VT_LV_R, NW = HM_VT_LV_NW, MC = 8 * HM_VT_LV_NT;
   if (HM_VT_LV_MIN_M <= 0 || vp.m < HM_VT_LV_MIN_M || !(k == 16 || k == 32) || b % R != 0 || vp.nlev < 1)
     return HM_ERR_UNSUPPORTED;
   const int mp = (vp.m + MC - 1) / MC * MC;

@@ -56,6 +56,7 @@ def hss_flops(n, b, p, k, m):
     return 2 * n * m * (b + 2 * k) + 8 * ((1 << p) - 2) * k * k * m + 4 * ((1 << p) - 1) * k * k * m
 
 
+READ_STREAM_GBS = 7185.1  # measured read-only fp64 stream on this pool's B200 (tools/fp64_peaks.cu)
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA (mma.sync f64) peak on this pool's B200, tools/fp64_peaks.cu
 C5 = hm_inputs.CONFIGS[5]
 C4 = hm_inputs.CONFIGS[4]
@@ -611,6 +612,10 @@ def run_ours(args):
             "alg_bytes_per_launch": dom_bytes,
             "avg_launch_ms": round(dom_avg_ms, 4),
             "share_of_step": round(dom[1] / args.steps / step_ms, 4),
+            # context: the kernel is 99.7% reads, so a read+write copy figure is not its ceiling
+            "read_stream_peak": READ_STREAM_GBS,
+            "frac_of_read_stream": round(achieved / READ_STREAM_GBS, 4),
+            "read_stream_source": "tools/fp64_peaks.cu read-only stream, profiles/r01_next/fp64_peaks_mix.json",
         },
         "per_config": {
             "c5_hodlr": {"ms": round(c5_ms, 4), "GB/s": round(b5 / (c5_ms * 1e-3) / 1e9, 1),

@@ -79,9 +79,13 @@ typedef struct {
  *                    (sib b, b). (V12 = V_l(I_2q+1), V21 = V_l(I_2q).)
  *   ranks [p] (host array): ranks[l-1] = k_l >= 0 (0 encodes the zero
  *                    block), each <= 64. Equal nonzero ranks run the
- *                    tuned kernels; per-level ranks run the
- *                    general-tree kernels (hodlr_matvec_general) with the
- *                    same workspace query (not with HM_WS_HOSTIO).
+ *                    tuned kernels. Per-level ranks also run the
+ *                    uniform-tree kernels when levels >= 3 and leaf is a
+ *                    multiple of 64 (<= 1024): one V^T X pass per distinct
+ *                    rank, one leaf pass with per-level segments; otherwise
+ *                    the general-tree kernels (hodlr_matvec_general), with
+ *                    the same workspace query either way (HM_WS_HOSTIO: the
+ *                    uniform-tree case only).
  *   X  [n][nrhs], Y [n][nrhs]; nrhs >= 1.
  * Cost O(k n log n); bytes = 8(n b + 2 sum_l n k_l + 2 n nrhs). */
 
@@ -176,8 +180,9 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
  * nondecreasing or c[2^p-1] != n is HM_ERR_INVALID_ARG. The tables derived
  * from c are copied into the workspace with one pageable host-to-device copy
  * per call, so these calls are NOT CUDA-graph capturable. Deterministic.
- * (hodlr_matvec / hodlr_matvec_t on the uniform tree route per-level ranks
- * here automatically, with the same workspace query.) */
+ * (hodlr_matvec / hodlr_matvec_t route per-level ranks on uniform trees
+ * with fewer than 3 levels or leaves not a multiple of 64 here
+ * automatically, with the same workspace query.) */
 hm_status hm_hodlr_general_workspace_bytes(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks,
                                            int32_t nrhs, size_t* bytes);
 hm_status hodlr_matvec_general(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks, int32_t op,

@@ -29,6 +29,12 @@
 // tested with HM_SMALL_HODLR=1) but not faster on config 1 (22.9 vs 21 us per
 // call: the kernel alone takes 17.7 us, the two-kernel path 20.5 us of device
 // time); off by default (r01_tuning.md).
+#ifndef HM_VT_LV_MIN_M
+#define HM_VT_LV_MIN_M 17  // X re-reads of vt_mma_levels fall out of L2 above this (config 3, m = 64)
+#endif
+#ifndef HM_VT_TILE4
+#define HM_VT_TILE4 1  // vt_mma_levels on 4-leaf tiles below the vt_lv threshold
+#endif
 #ifndef HM_SMALL_HODLR
 #define HM_SMALL_HODLR 0
 #endif
@@ -257,7 +263,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     if (!(tiles8 && b % 64 == 0 && b <= 1024))
       return fail(HM_ERR_UNSUPPORTED, "per-level ranks: uniform-tree kernels need levels >= 3 and leaf %% 64 == 0");
     P->vt = nrhs == 1 ? VtPath::kGemv : VtPath::kMma;
-    P->tile = 8 * b;
+    P->tile = (nrhs >= 2 && HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : 8 * b;
     int mc = std::min<int32_t>(nrhs, hm::kMaxMc);
     while (mc > 1 && P->tile * mc + hm::kThreads > kSmemBudgetDoubles) --mc;
     P->mc_vt = mc;
@@ -284,7 +290,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     P->tile = 8 * b;
   } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 1, 64)) {
     P->vt = VtPath::kMma;
-    P->tile = 8 * b;
+    P->tile = (HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : 8 * b;  // vt_lv (m >= HM_VT_LV_MIN_M) needs 8
     P->nt_vt = vt_mma_nt((int)k, nrhs);
   } else {
     P->vt = VtPath::kGeneric;
@@ -541,8 +547,17 @@ hm_status vt_gemv_dispatch(const hm::VtParams& vp, int64_t b, int k, cudaStream_
   }
 }
 
+// vp.tile = LPC b rows per CTA: 4 leaves when the plan chose it (m below the
+// vt_lv threshold: twice the CTAs, so the grid fills every SM evenly), else 8
 template <int KT, int NT>
 hm_status vt_mma_launch(const hm::VtParams& vp, int64_t b, cudaStream_t s) {
+  if (vp.tile == 4 * b) {
+    size_t smem = sizeof(double) * (size_t)(4 * KT * NT * 8);
+    allow_smem(hm::vt_mma_levels_kernel<KT, NT, 4>, smem);
+    return launch("vt_mma_levels", s, [&] {
+      hm::vt_mma_levels_kernel<KT, NT, 4><<<(unsigned)(vp.n / (4 * b)), 128, smem, s>>>(vp, b);
+    });
+  }
   size_t smem = sizeof(double) * (size_t)(8 * KT * NT * 8);
   allow_smem(hm::vt_mma_levels_kernel<KT, NT>, smem);
   return launch("vt_mma_levels", s, [&] {
@@ -579,9 +594,6 @@ hm_status vt_mma_dispatch(const hm::VtParams& vp, int64_t b, int k, int nt, cuda
 
 // Many right-hand sides: the level-parallel pipelined kernel (vt_lv_kernel, X
 // and V read once). Returns HM_ERR_UNSUPPORTED when the shape does not fit it.
-#ifndef HM_VT_LV_MIN_M
-#define HM_VT_LV_MIN_M 17  // X re-reads of vt_mma_levels fall out of L2 above this (config 3, m = 64)
-#endif
 #ifndef HM_VT_LV_NW
 #define HM_VT_LV_NW 16
 #endif

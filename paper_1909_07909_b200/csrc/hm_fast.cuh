@@ -1115,15 +1115,15 @@ __global__ void __launch_bounds__(NW * 32, 1) vt_lv_kernel(const VtParams P, int
   cp_async_wait_groups<0>();
 }
 
-// HODLR, nrhs >= 2: tile = 8 leaves (8 b rows), warp w = leaf w of the tile.
+// HODLR, nrhs >= 2: tile = LPC leaves (LPC b rows), warp w = leaf w of the tile.
 // Per level: warp partial t over its b rows (DMMA), staged in shared memory,
 // then fixed-order sums over the warps of each node.
-template <int KT, int NT>
-__global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, int64_t b) {
-  extern __shared__ double red[];  // [8][KT][MC]
+template <int KT, int NT, int LPC = 8>
+__global__ void __launch_bounds__(32 * LPC) vt_mma_levels_kernel(const VtParams P, int64_t b) {
+  extern __shared__ double red[];  // [LPC][KT][MC]
   constexpr int MC = NT * 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tile = 8 * b;
+  const int64_t tile = LPC * b;  // LPC leaves per CTA, one warp each
   const int64_t row0 = (int64_t)blockIdx.x * tile + (int64_t)warp * b;
   const int m = P.m;
   for (int c0 = 0; c0 < m; c0 += MC) {
@@ -1152,9 +1152,9 @@ __global__ void __launch_bounds__(256) vt_mma_levels_kernel(const VtParams P, in
         store_transposed<KT / 16, NT>(acc, red + (int64_t)warp * KT * MC, MC, c0, c0 + mc, lane, c0);
       }
       __syncthreads();
-      const int64_t g = lv.s >= tile ? 8 : lv.s / b;
-      const int ngroups = (int)(8 / g);
-      for (int o = threadIdx.x; o < ngroups * KT * mc; o += 256) {
+      const int64_t g = lv.s >= tile ? LPC : lv.s / b;
+      const int ngroups = (int)(LPC / g);
+      for (int o = threadIdx.x; o < ngroups * KT * mc; o += 32 * LPC) {
         const int grp = o / (KT * mc);
         const int rem = o - grp * KT * mc;
         const int a = rem / mc, c = rem - a * mc;

@@ -26,6 +26,9 @@
 namespace hm {
 
 constexpr int64_t kChunkRows = 4096;
+#ifndef HM_GEN_MMA_Q
+#define HM_GEN_MMA_Q 4  // k-steps of A fragments requested per batch in gen_leaf_mma
+#endif
 
 // One chunk: rows [lo, hi) of one node; its partial goes to partial + pidx * k * m.
 struct GenChunk {
@@ -323,25 +326,42 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
     bool rok[GR];
 #pragma unroll
     for (int u = 0; u < GR; ++u) rok[u] = rw + 8 * u < b;
-    for (int64_t j0 = lane; j0 < b; j0 += 32 * UJ) {
+    // row pointers of the warp's rows (rows past the leaf clamp to its last
+    // row: read, never stored), 32-bit column indices; only the tail chunk of
+    // a row is masked
+    const int bi = (int)b;
+    const double* drow[GR];
+#pragma unroll
+    for (int u = 0; u < GR; ++u) {
+      const int64_t r = rok[u] ? rw + 8 * u : b - 1;
+      drow[u] = P.dtrans ? Di + r : Di + r * b;
+    }
+    const int64_t dstep = P.dtrans ? b : 1;  // element stride along the contraction index
+    int j0 = lane;
+    for (; j0 + 32 * (UJ - 1) < bi; j0 += 32 * UJ) {  // full chunks: no masks
       double d[GR][UJ];
 #pragma unroll
       for (int u = 0; u < GR; ++u)
 #pragma unroll
-        for (int v = 0; v < UJ; ++v) {
-          const int64_t r = rw + 8 * u, jj = j0 + 32 * v;
-          d[u][v] = (rok[u] && jj < b) ? (P.dtrans ? __ldg(Di + jj * b + r) : __ldg(Di + r * b + jj)) : 0.0;
-        }
+        for (int v = 0; v < UJ; ++v) d[u][v] = __ldg(drow[u] + (j0 + 32 * v) * dstep);
 #pragma unroll
       for (int v = 0; v < UJ; ++v) {
-        const int64_t jj = j0 + 32 * v;
-        if (jj >= b) break;
         double z[MC];
-        zrow<MC>(z, Z + jj * ZS);
+        zrow<MC>(z, Z + (j0 + 32 * v) * ZS);
 #pragma unroll
         for (int c = 0; c < MC; ++c)
 #pragma unroll
           for (int u = 0; u < GR; ++u) acc[u][c] = fma(d[u][v], z[c], acc[u][c]);
+      }
+    }
+    for (; j0 < bi; j0 += 32) {  // tail
+      double z[MC];
+      zrow<MC>(z, Z + j0 * ZS);
+#pragma unroll
+      for (int u = 0; u < GR; ++u) {
+        const double d = __ldg(drow[u] + j0 * dstep);
+#pragma unroll
+        for (int c = 0; c < MC; ++c) acc[u][c] = fma(d, z[c], acc[u][c]);
       }
     }
     int64_t off = b;
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
 template <int NT, bool DT>
 __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafParams P) {
   extern __shared__ double smem[];
-  constexpr int MC = NT * 8, ZS = MC + 4, Q = 4;
+  constexpr int MC = NT * 8, ZS = MC + 4, Q = HM_GEN_MMA_Q;
   const int64_t leaf = blockIdx.x;
   const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
   if (b == 0) return;
@@ -423,22 +443,32 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
     double acc[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-    // leaf block: contraction over the b columns of D_i (rows of D_i^T)
-    for (int64_t q0 = 0; q0 < (b + 3) / 4; q0 += Q) {
+    // leaf block: contraction over the b columns of D_i (rows of D_i^T); rows
+    // past the leaf clamp to its last row (computed, never stored); full
+    // batches of Q k-steps unmasked, the tail masked
+    const int bi = (int)b;
+    const int64_t rr = rok ? row : b - 1;
+    const double* drow = DT ? Di + rr : Di + rr * b;
+    const int64_t dstep = DT ? b : 1;
+    int q0 = 0;
+    for (; 4 * (q0 + Q) <= bi; q0 += Q) {
       double a[Q];
 #pragma unroll
-      for (int u = 0; u < Q; ++u) {
-        const int64_t kk = 4 * (q0 + u) + j;
-        a[u] = (rok && kk < b) ? __ldg(DT ? Di + kk * b + row : Di + row * b + kk) : 0.0;
-      }
+      for (int u = 0; u < Q; ++u) a[u] = __ldg(drow + (4 * (q0 + u) + j) * dstep);
 #pragma unroll
       for (int u = 0; u < Q; ++u) {
-        const int64_t kk = 4 * (q0 + u) + j;
-        if (4 * (q0 + u) >= b) break;  // warp-uniform
-        const double* zr = Z + (kk < b ? kk : 0) * ZS + i;
+        const double* zr = Z + (4 * (q0 + u) + j) * ZS + i;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < b ? zr[nt * 8] : 0.0);
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], zr[nt * 8]);
       }
+    }
+    for (; 4 * q0 < bi; ++q0) {
+      const int kk = 4 * q0 + j;
+      const bool kok = kk < bi;
+      const double a = kok ? __ldg(drow + kk * dstep) : 0.0;
+      const double* zr = Z + (kok ? kk : 0) * ZS + i;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, kok ? zr[nt * 8] : 0.0);
     }
     // U segments: contraction over each segment's k rank columns
     int64_t zo = b;

@@ -243,6 +243,25 @@ def test_config3_full_size_sampled(hm, config3, m):
     assert np.isfinite(Y).all()
 
 
+@pytest.mark.parametrize("ranks_of,m", [(lambda l: 16 if l % 2 else 8, 8), (lambda l: 16 >> (l % 4), 1),
+                                         (lambda l: 32 if l % 2 else 16, 64)])
+def test_config3_tree_per_level_ranks_sampled(hm, ranks_of, m):
+    """Per-level ranks on the full config-3 tree, the bench sweep's sets:
+    one V^T X pass per distinct rank + one leaf pass, sampled leaves vs the oracle."""
+    cfg = hm_inputs.CONFIGS[3]
+    ranks = [ranks_of(l) for l in range(cfg.levels)]
+    h = hm_inputs.hodlr_random(cfg.n, cfg.levels, ranks, cid=6)
+    X = hm_inputs.rhs(cfg.n, m, cid=6)
+    Y = gpu_hodlr(hm, h, X)
+    b = cfg.leaf
+    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(60 + m))
+    Dsel = np.concatenate([h.D[L * b * b:(L + 1) * b * b] for L in leaves])
+    Yr = oracle.hodlr_matvec_leaves(cfg.n, cfg.levels, h.ranks, Dsel, h.U, h.V, X, leaves)
+    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
+    assert relerr(Yg, Yr) <= TOL
+    assert np.isfinite(Y).all()
+
+
 def test_config4_full_size_sampled(hm):
     cfg = hm_inputs.CONFIGS[4]
     s = hm_inputs.hss_random(cfg.n, cfg.levels, cfg.k, cid=4)

@@ -296,6 +296,12 @@ class DistWorkload:
 
 # ------------------------------------------------------ nrhs / ops sweep --
 
+def _fin(x, nd):
+    """round(x, nd), or None when x is not finite (strict JSON has no NaN)."""
+    import math
+    return round(x, nd) if isinstance(x, (int, float)) and math.isfinite(x) else None
+
+
 def _graph_us(torch, f, calls=20, replays=20):
     """Device us per call with `calls` calls captured in one CUDA graph (the
     latency of a small, L2-resident product without host launch overhead)."""
@@ -603,18 +609,18 @@ def run_ours(args):
         "roofline": {
             "bound": "hbm",
             "kernel": "leaf_gemv_kernel<K=1> (config-5 leaf pass: D_i X_i + sum_l U_l t_l, all leaves, Y written once)",
-            "achieved": round(achieved, 1),
+            "achieved": _fin(achieved, 1),
             "peak": peak,
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
             "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
+            "frac": _fin(achieved / peak, 4),
             "traffic": committed_traffic("leaf_gemv", "c5"),
             "alg_bytes_per_launch": dom_bytes,
-            "avg_launch_ms": round(dom_avg_ms, 4),
-            "share_of_step": round(dom[1] / args.steps / step_ms, 4),
+            "avg_launch_ms": _fin(dom_avg_ms, 4),
+            "share_of_step": _fin(dom[1] / args.steps / step_ms, 4),
             # context: the kernel is 99.7% reads, so a read+write copy figure is not its ceiling
             "read_stream_peak": READ_STREAM_GBS,
-            "frac_of_read_stream": round(achieved / READ_STREAM_GBS, 4),
+            "frac_of_read_stream": _fin(achieved / READ_STREAM_GBS, 4),
             "read_stream_source": "tools/fp64_peaks.cu read-only stream, profiles/r01_next/fp64_peaks_mix.json",
         },
         "per_config": {

@@ -572,7 +572,10 @@ def run_ours(args):
         d[0] += 1
         d[1] += t
     step_ms = ms / args.steps
-    total_bytes = step_bytes() * args.steps * world
+    # strong scaling: the P ranks together process ONE global C5 + C4 problem per
+    # step (each rank holds n / P rows), so the job's bytes per step are
+    # step_bytes() whatever P is
+    total_bytes = step_bytes() * args.steps
     value = total_bytes / (ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
     dom = per.get("c5:leaf_gemv", [1, float("nan")])
@@ -584,7 +587,8 @@ def run_ours(args):
     b5 = hodlr_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5)
     b4 = hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
     f4 = hss_flops(C4.n, C4.leaf, C4.levels, C4.k, M4)
-    h2d, d2h = wl.h2d_d2h_bytes()
+    h2d, d2h = wl.h2d_d2h_bytes()  # this rank's copies; the job's = P times (equal shards)
+    h2d, d2h = h2d * world, d2h * world
     out = {
         "metric": METRIC,
         "value": round(value, 2),
@@ -636,7 +640,7 @@ def run_ours(args):
         },
         "kernels": {k_: {"launches_per_step": v[0] // args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
                     for k_, v in sorted(per.items())},
-        "e2e": {"value": round(step_bytes() * e2 * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+        "e2e": {"value": round(step_bytes() * e2 / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": "hodlr_matvec_hostio + hss_matvec_hostio: pinned host X in, host Y out, every step; "
                         f"consecutive steps rotate over {len(getattr(wl, "lanes", [0]))} streams so copies overlap kernels; "

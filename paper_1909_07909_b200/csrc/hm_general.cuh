@@ -238,8 +238,17 @@ __global__ void __launch_bounds__(kThreads) gen_vt_reduce_kernel(const GenReduce
   const int64_t local = t - P.thread_begin[L];
   const int64_t j = local / km, e = local - j * km;
   const int64_t b0 = lv.cbeg[j], b1 = lv.cbeg[j + 1];
-  double s = 0.0;
-  for (int64_t c = b0; c < b1; ++c) s += lv.partial[c * km + e];
+  // 8 independent running sums (chunk c goes to sum (c - b0) % 8), combined in
+  // a fixed order: the loads of 8 chunks are in flight at once, and the result
+  // depends only on the chunk count, never on timing
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int64_t c = b0;
+  for (; c + 8 <= b1; c += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += lv.partial[(c + u) * km + e];
+  }
+  for (int u = 0; c < b1; ++c, ++u) acc[u] += lv.partial[c * km + e];
+  const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   lv.out[j * km + e] = s;
 }
 

@@ -227,6 +227,7 @@ class Workload:
 
     calls = ("c5", "c4")  # matvec calls per step (launch-trace labels)
     rows5 = C5.n
+    rows4 = C4.n
 
 
 class DistWorkload:
@@ -259,6 +260,7 @@ class DistWorkload:
         del s4
         torch.cuda.empty_cache()
         nl4 = C4.n // P
+        self.rows4 = nl4
         self.X4 = torch.randn(nl4, M4, dtype=torch.float64, device=device, generator=g)
         self.Y4 = torch.empty_like(self.X4)
         w5, self.sd5 = hd.hodlr_dist_sizes(n5, p5, b5, self.ranks5, M5, P, r)
@@ -295,6 +297,20 @@ class DistWorkload:
 
 
 # ------------------------------------------------------ nrhs / ops sweep --
+
+def _c4_leaf_roofline(per, steps, wl):
+    d = per.get("c4:leaf_mma")
+    if not d or d[0] == 0:
+        return None
+    rows = getattr(wl, "rows4", C4.n)
+    flops = 2.0 * rows * M4 * (C4.leaf + C4.k)
+    avg_ms = d[1] / d[0]
+    tf = flops / (avg_ms * 1e-3) / 1e12
+    return {"bound": "tensor (fp64 DMMA)", "kernel": "leaf_mma_kernel<2,4,1,4> (config-4 leaf pass: D_i X_i + U_i y_i)",
+            "achieved": _fin(tf, 2), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": _fin(tf / FP64_PEAK_TFLOPS, 4),
+            "peak_kind": "measured DMMA (tools/fp64_peaks.cu, profiles/r01_next/fp64_peaks_mix.json)",
+            "alg_flops_per_launch": flops, "avg_launch_ms": _fin(avg_ms, 4)}
+
 
 def _fin(x, nd):
     """round(x, nd), or None when x is not finite (strict JSON has no NaN)."""
@@ -627,6 +643,10 @@ def run_ours(args):
             "frac_of_read_stream": _fin(achieved / READ_STREAM_GBS, 4),
             "read_stream_source": "tools/fp64_peaks.cu read-only stream, profiles/r01_next/fp64_peaks_mix.json",
         },
+        # the second-largest kernel, config 4's leaf pass, is bound by the fp64
+        # tensor pipe: its algorithmic flops 2 n m (b + k) per launch over its
+        # average launch time, against the measured DMMA peak
+        "roofline_c4_leaf": _c4_leaf_roofline(per, args.steps, wl),
         "per_config": {
             "c5_hodlr": {"ms": round(c5_ms, 4), "GB/s": round(b5 / (c5_ms * 1e-3) / 1e9, 1),
                          "frac_hbm": round(b5 / (c5_ms * 1e-3) / 1e9 / peak, 4),

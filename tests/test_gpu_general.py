@@ -170,6 +170,25 @@ def test_uniform_tree_per_level_ranks_tuned_kernels(hm, n, leaf, p, ranks, m):
     assert torch.equal(Y, Y2)
 
 
+def test_per_level_ranks_hostio_matches_device(hm):
+    """Per-level ranks through the host-buffer entry point (hodlr_matvec_hostio, the
+    bench's e2e path) give bitwise the device-buffer result."""
+    n, p, b, m = 65536, 8, 256, 8
+    ranks = [16, 8, 16, 32, 8, 16, 4, 16]
+    rng = np.random.default_rng(74)
+    c = np.arange(1, (1 << p) + 1, dtype=np.int64) * b
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    g = [dev(a) for a in (D, U, V)]
+    Yd = hm.hodlr_matvec(n, p, b, ranks, *g, dev(X)).cpu()
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    hm.hodlr_matvec_hostio(n, p, b, ranks, *g, Xh, Yh)
+    torch.cuda.synchronize()
+    assert torch.equal(Yh, Yd)
+    assert relerr(Yh.numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X)) <= TOL
+
+
 def test_general_uniform_endpoints_match_uniform_path(hm):
     """The general kernels on uniform endpoints agree with the tuned uniform kernels."""
     n, p, b, k, m = 32768, 7, 256, 16, 8

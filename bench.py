@@ -514,7 +514,10 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    # HM_BENCH_DIST=1: the multi-GPU workload even at N = 1 (a one-rank process
+    # group), to exercise the distributed path on a single GPU
+    use_dist = world > 1 or os.environ.get("HM_BENCH_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=device)
     from paper_1909_07909_b200 import build as hm_build
     if rank == 0:
@@ -522,7 +525,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
-    if world > 1:
+    if use_dist:
         wl = DistWorkload(torch, device, hm_inputs.MASTER_SEED, world, rank)
     else:
         wl = Workload(torch, device, seed=hm_inputs.MASTER_SEED)

@@ -2185,10 +2185,17 @@ hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* p
     return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
   g_launches = 0;
   prof_new_call();
-  if (k == 0 || d.q == 0) return HM_OK;  // nothing to exchange
+  if (k == 0) return HM_OK;  // block diagonal: nothing to exchange, no tree
+  double* xh = reinterpret_cast<double*>(static_cast<char*>(workspace) + P.off_xh);
+  if (d.q == 0) {
+    // one rank: the whole tree is local and the exchange is empty; Step 1 and
+    // the upsweep to level 1 run here (as in hss_matvec), _end does the rest
+    if (P.p == 0) return HM_OK;
+    if (!X_local || !V_local || (P.p >= 2 && !W_sub)) return fail(HM_ERR_INVALID_ARG, "NULL V / W / X pointer");
+    return hss_up_phase(P, V_local, W_sub, X_local, xh, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+  }
   if (!X_local || !V_local || !send || (P.p >= 2 && !W_sub) || (P.p >= 1 && !W_root))
     return fail(HM_ERR_INVALID_ARG, "NULL V / W / X / send pointer");
-  double* xh = reinterpret_cast<double*>(static_cast<char*>(workspace) + P.off_xh);
   return hss_up_phase(P, V_local, W_sub, X_local, xh, W_root, send, static_cast<cudaStream_t>(stream));
 }
 
@@ -2215,6 +2222,13 @@ hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* par
   g_launches = 0;
   prof_new_call();
   const double* yleaf = nullptr;
+  if (k > 0 && d.q == 0 && P.p >= 1) {
+    // one rank: coupling + downsweep of the whole (local) tree on the x blocks
+    // _begin left in the workspace, then the leaves (as in hss_matvec)
+    if (!U_local || !B_sub || (P.p >= 2 && !R_sub)) return fail(HM_ERR_INVALID_ARG, "NULL U / R / B pointer");
+    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s))) return st;
+    yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+  }
   if (k > 0 && d.q > 0) {
     if (!gathered || !U_local || !B_top || (d.q >= 2 && (!W_top || !R_top)) || (P.p >= 1 && (!R_root || !B_sub)) ||
         (P.p >= 2 && !R_sub))

@@ -84,6 +84,7 @@ def emulate_hss(hd, n, p, b, k, g, X, P):
 
 @pytest.mark.parametrize("n,b,p,k,m,P", [
     (1 << 16, 256, 8, 16, 1, 2), (1 << 16, 256, 8, 16, 8, 4), (1 << 16, 256, 8, 16, 8, 8),
+    (1 << 16, 256, 8, 16, 8, 1), (1 << 17, 256, 9, 1, 1, 1),   # one rank: the whole tree local
     (1 << 17, 256, 9, 1, 1, 8),        # config-5 shape (k = 1)
     (4096, 64, 6, 8, 3, 4),            # generic kernels
     (2048, 64, 5, 16, 2, 32),          # one leaf per rank (P = 2^p)
@@ -104,6 +105,7 @@ def test_hodlr_dist_emulated(hm, n, b, p, k, m, P):
 
 @pytest.mark.parametrize("n,b,p,k,m,P", [
     (1 << 15, 128, 8, 32, 32, 2), (1 << 15, 128, 8, 32, 32, 8), (1 << 15, 128, 8, 32, 32, 4),
+    (1 << 15, 128, 8, 32, 32, 1), (8192, 64, 7, 16, 1, 1),     # one rank
     (8192, 64, 7, 16, 1, 4),           # m = 1 kernels
     (4096, 64, 6, 5, 3, 2),            # generic kernels
     (2048, 64, 5, 16, 2, 32),          # one leaf per rank

@@ -46,6 +46,18 @@ def test_hodlr_norm2_est_vs_oracle(hm, n, leaf, levels, k, iters):
     assert abs(float(est.item()) - ref) <= TOL * ref
 
 
+@pytest.mark.parametrize("ranks", [[16, 8, 16, 4, 32, 2], [3, 0, 5, 7, 1, 2]])
+def test_hodlr_norm2_est_per_level_ranks(hm, ranks):
+    """Per-level ranks in the norm estimate: uniform-tree kernels for
+    power-of-two ranks, the general ones otherwise; both vs the oracle."""
+    n, leaf, levels = 16384, 256, 6
+    h = hm_inputs.hodlr_random(n, levels, ranks, cid=42)
+    x0 = hm_inputs.rhs(n, 1, cid=42).ravel()
+    ref = oracle.hodlr_norm2_est(n, levels, h.ranks, h.D, h.U, h.V, x0, 4)
+    est = hm.hodlr_norm2_est(n, levels, leaf, h.ranks, dev(h.D), dev(h.U), dev(h.V), dev(x0), 4)
+    assert abs(float(est.item()) - ref) <= TOL * ref
+
+
 NORM_HSS = [(4096, 64, 6, 16, 3), (8192, 64, 7, 16, 4), (2048, 128, 4, 32, 2), (100, 100, 0, 4, 3)]
 
 

@@ -50,7 +50,10 @@ def test_abi_version_and_no_error():
 
 def test_library_has_no_torch_dependency():
     out = subprocess.run(["ldd", hm.LIB_PATH], capture_output=True, text=True).stdout
-    assert "torch" not in out and "c10" not in out
+    # library names only: the load addresses ldd prints are random hex and can
+    # contain "c10" (a flaky match before)
+    names = [line.split()[0] for line in out.splitlines() if line.strip()]
+    assert not [nm for nm in names if re.search(r"torch|c10", nm)], names
 
 
 def test_kernels_are_sm100a():

@@ -130,8 +130,43 @@ def make_tree(n: int, levels: int, leaf: int) -> hm_tree:
 
 
 def _ranks(ranks: Sequence[int], levels: int):
-    arr = (ctypes.c_int32 * max(levels, 1))(*([int(r) for r in ranks][:levels] or [0]))
-    return arr
+    """ranks[l-1] = k_l for l = 1..levels: exactly `levels` entries (a short list would
+    silently turn the missing levels into zero blocks)."""
+    ranks = [int(r) for r in ranks]
+    if levels >= 0 and len(ranks) != levels:  # (negative depths are the library's to reject)
+        raise ValueError(f"ranks has {len(ranks)} entries, need one per level ({levels})")
+    return (ctypes.c_int32 * max(levels, 1, len(ranks)))(*(ranks or [0]))
+
+
+def _numel_at_least(t, count, name):
+    if t is not None and t.numel() < count:
+        raise ValueError(f"{name} has {t.numel()} elements, the tree needs {count}")
+
+
+def _xy(X, Y, n):
+    """X [n] or [n][nrhs]; Y the same shape as X."""
+    if X.shape[0] != n or X.dim() > 2:
+        raise ValueError(f"X must be [n] or [n][nrhs] with n = {n}, got {tuple(X.shape)}")
+    if Y is not None and tuple(Y.shape) != tuple(X.shape):
+        raise ValueError(f"Y shape {tuple(Y.shape)} != X shape {tuple(X.shape)}")
+
+
+def _hodlr_sizes(n, leaf, ranks, D, U, V):
+    _numel_at_least(D, n * leaf, "D")
+    kt = sum(int(r) for r in ranks)
+    _numel_at_least(U, n * kt, "U")
+    _numel_at_least(V, n * kt, "V")
+
+
+def _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B):
+    _numel_at_least(D, n * leaf, "D")
+    if k > 0 and levels > 0:
+        _numel_at_least(U, n * k, "U")
+        _numel_at_least(V, n * k, "V")
+        _numel_at_least(B, ((1 << levels) - 1) * 2 * k * k, "B")
+        if levels >= 2:
+            _numel_at_least(R, ((1 << levels) - 2) * 2 * k * k, "R")
+            _numel_at_least(W, ((1 << levels) - 2) * 2 * k * k, "W")
 
 
 def _ptr(t) -> Optional[int]:
@@ -184,10 +219,12 @@ def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, str
     X: [n][nrhs] (or [n]) float64 CUDA tensor. Returns Y (allocated if None)."""
     import torch
     X = _dev(X, "X")
+    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs), workspace, X.device)
     t = make_tree(n, levels, leaf)
     _check(getattr(load(), _fn)(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(X), nrhs,
@@ -208,7 +245,9 @@ def hodlr_matvec_hostio(n, levels, leaf, ranks, D, U, V, X_host, Y_host, workspa
     for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
         if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous float64 host tensor")
+    _xy(X_host, Y_host, n)
     _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs, HM_WS_HOSTIO), workspace, D.device)
     t = make_tree(n, levels, leaf)
     _check(load().hodlr_matvec_hostio(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V),
@@ -226,11 +265,13 @@ def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, 
     """Y = A X on the current CUDA stream for the HSS matrix (D, U, V, R, W, B) (include/hm.h)."""
     import torch
     X = _dev(X, "X")
+    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs), workspace, X.device)
     t = make_tree(n, levels, leaf)
     _check(getattr(load(), _fn)(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
@@ -244,8 +285,10 @@ def hss_matvec_hostio(n, levels, leaf, k, D, U, V, R, W, B, X_host, Y_host, work
     for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
         if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous float64 host tensor")
+    _xy(X_host, Y_host, n)
     for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs, HM_WS_HOSTIO), workspace, D.device)
     t = make_tree(n, levels, leaf)
     _check(load().hss_matvec_hostio(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
@@ -281,7 +324,9 @@ def hodlr_norm2_est(n, levels, leaf, ranks, D, U, V, x0, iters, est=None, worksp
     """||A||_2 estimate (power method on A A^*, include/hm.h hodlr_norm2_est): returns a 1-element
     float64 CUDA tensor written asynchronously on the stream."""
     x0 = _dev(x0, "x0")
+    _numel_at_least(x0, n, "x0")
     _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     est = _est(est, x0.device)
     ws = _workspace(hm_hodlr_norm2_workspace_bytes(n, levels, leaf, ranks), workspace, x0.device)
     t = make_tree(n, levels, leaf)
@@ -293,8 +338,10 @@ def hodlr_norm2_est(n, levels, leaf, ranks, D, U, V, x0, iters, est=None, worksp
 def hss_norm2_est(n, levels, leaf, k, D, U, V, R, W, B, x0, iters, est=None, workspace=None, stream=None):
     """||A||_2 estimate of an HSS matrix (include/hm.h hss_norm2_est)."""
     x0 = _dev(x0, "x0")
+    _numel_at_least(x0, n, "x0")
     for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     est = _est(est, x0.device)
     ws = _workspace(hm_hss_norm2_workspace_bytes(n, levels, leaf, k), workspace, x0.device)
     t = make_tree(n, levels, leaf)
@@ -312,12 +359,15 @@ def hss_to_hodlr(n, levels, leaf, k, U, V, R, W, B, Uh=None, Vh=None, stream=Non
     U = _dev(U, "U")
     for t_, nm in ((V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    _hss_sizes(n, levels, leaf, k, None, U, V, R, W, B)
     size = max(levels, 0) * n * k
     if Uh is None:
         Uh = torch.empty(size, dtype=torch.float64, device=U.device)
     if Vh is None:
         Vh = torch.empty(size, dtype=torch.float64, device=U.device)
     _dev(Uh, "Uh"); _dev(Vh, "Vh")
+    _numel_at_least(Uh, size, "Uh")
+    _numel_at_least(Vh, size, "Vh")
     t = make_tree(n, levels, leaf)
     _check(load().hss_to_hodlr(ctypes.byref(t), int(k), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(Uh),
                                _ptr(Vh), _stream(stream)))
@@ -334,6 +384,14 @@ def _endpoints(c, levels):
     return c
 
 
+def _leaf_block_doubles(c) -> int:
+    prev, tot = 0, 0
+    for e in c:
+        tot += (int(e) - prev) ** 2
+        prev = int(e)
+    return tot
+
+
 def hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs) -> int:
     c = _endpoints(c, levels)
     out = ctypes.c_size_t(0)
@@ -348,10 +406,15 @@ def hodlr_matvec_general(n, levels, c, ranks, D, U, V, X, op=0, Y=None, workspac
     import torch
     c = _endpoints(c, levels)
     X = _dev(X, "X")
+    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    _numel_at_least(D, _leaf_block_doubles(c), "D")
+    kt = sum(int(r) for r in ranks)
+    _numel_at_least(U, n * kt, "U")
+    _numel_at_least(V, n * kt, "V")
     ws = _workspace(hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs), workspace, X.device)
     _check(load().hodlr_matvec_general(int(n), int(levels), c.ctypes.data, _ranks(ranks, levels), int(op), _ptr(D),
                                        _ptr(U), _ptr(V), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
@@ -372,11 +435,14 @@ def hss_matvec_general(n, levels, c, k, D, U, V, R, W, B, X, op=0, Y=None, works
     import torch
     c = _endpoints(c, levels)
     X = _dev(X, "X")
+    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    _hss_sizes(n, levels, 0, k, None, U, V, R, W, B)
+    _numel_at_least(D, _leaf_block_doubles(c), "D")
     ws = _workspace(hm_hss_general_workspace_bytes(n, levels, c, k, nrhs), workspace, X.device)
     _check(load().hss_matvec_general(int(n), int(levels), c.ctypes.data, int(k), int(op), _ptr(D), _ptr(U), _ptr(V),
                                      _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),

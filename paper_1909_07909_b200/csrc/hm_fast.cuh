@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(32 * (kTmaConsumers + 1), 1)
 #endif
 // Tuning: the DMMA kernels take MINB (minimum resident CTAs per SM for the
 // launch bounds; 0 = unconstrained) and the A-stream prefetch depth PF as
-// template parameters; the host picks them per shape (hm_abi.cu, measured on
+// template parameters; the host picks them per shape (hm_leaf.cu, measured on
 // B200: profiles/r01_tuning.md).
 
 // cp.async (LDGSTS) 16-byte global -> shared copies: the whole staging of a
@@ -693,13 +693,8 @@ __device__ __forceinline__ void warp_dt_mma(double (&acc)[RG][NT][2], const doub
 // in shared memory with row stride NT*8+4 (conflict-free B fragments).
 // DT (adjoint): the leaf term is D_i^T X_i (warp_dt_mma); for even RG the
 // warp's rows are in PAIR order, which the U segments and the store follow.
-//
-// DOWN (HSS, one segment): the last coupling + downsweep level is fused in. The
-// CTA stages x of the sibling leaf and y of the parent, computes
-// y_i = S_w x_{i^1} + R_w y_{parent} (w = i & 1; P:695-716 at level p) into
-// the T region, then applies U_i y_i as usual — the level-p down kernel and
-// its y round trip through HBM disappear.
-template <int RG, int NT, int PF, int MINB, bool DT = false, bool DOWN = false>
+
+template <int RG, int NT, int PF, int MINB, bool DT = false>
 __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P) {
   constexpr bool PAIR = DT && (RG % 2 == 0);
   extern __shared__ double sm[];
@@ -720,34 +715,11 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
   stage_rows_async(Z, ZSX, P.X + r0 * m + c0, m, (int)b, mc, MC);
   double* ZT = Z + b * ZSX;  // T region
   int64_t zoff = 0;
-  if constexpr (DOWN) {
-    const int k = P.seg[0].k;
-    double* Zs1 = ZT + k * ZS;   // x of the sibling leaf
-    double* Zs2 = Zs1 + k * ZS;  // y of the parent
-    stage_rows_async(Zs1, ZS, P.dx + (leaf ^ 1) * k * m + c0, m, k, mc, MC);
-    if (P.dyp) stage_rows_async(Zs2, ZS, P.dyp + (leaf >> 1) * k * m + c0, m, k, mc, MC);
-    cp_async_wait_all();
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int w = (int)(leaf & 1);
-    const double* S = P.dB + ((leaf >> 1) * 2 + w) * k * k;
-    const double* Rw = P.dyp ? P.dR + ((leaf >> 1) * 2 + w) * k * k : nullptr;
-    for (int t = warp; t < (k / 8) * NT; t += 8) {  // 8 x 8 tiles of y_i
-      const int rt = t % (k / 8), nt = t / (k / 8);
-      double acc[1][1][2] = {};
-      warp_rowmajor_mma<1, 1, false, false, 2>(acc, S + (int64_t)8 * rt * k, k, k, Zs1 + 8 * nt, ZS, MC, lane);
-      if (Rw) warp_rowmajor_mma<1, 1, false, false, 2>(acc, Rw + (int64_t)8 * rt * k, k, k, Zs2 + 8 * nt, ZS, MC, lane);
-      const int i = lane >> 2, jj = lane & 3;
-      ZT[(8 * rt + i) * ZS + 8 * nt + 2 * jj] = acc[0][0][0];
-      ZT[(8 * rt + i) * ZS + 8 * nt + 2 * jj + 1] = acc[0][0][1];
-    }
-  } else {
-    for (int s = 0; s < P.nseg; ++s) {
-      const LeafSeg sg = P.seg[s];
-      const int64_t node = (leaf >> sg.shift) ^ sg.xr;
-      stage_rows_async(ZT + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
-      zoff += sg.k;
-    }
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    const int64_t node = (leaf >> sg.shift) ^ sg.xr;
+    stage_rows_async(ZT + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
+    zoff += sg.k;
   }
   cp_async_wait_all();
   __syncthreads();

@@ -1,0 +1,618 @@
+// hm_hss.cu — the HSS product Y = A X (and A^T X): planning, Step 1 (leaf
+// V^T X + upsweep through W^T), Steps 2-3 (cores on every level l = 1..p,
+// reading G1, and the downsweep through R), Step 4 (U_i y_i + D_i X(I_i)),
+// the one-launch small-tree path, the distributed phases and
+// their C-ABI. Paper: Fig. 5 right, eq. (3), class
+// P:332-344; O(k n).
+#include "hm_internal.cuh"
+#include "hm_small.cuh"
+#include "hm_tree.cuh"
+#include "hm_treegemv.cuh"
+
+namespace hmi {
+
+#ifndef HM_TREE_GEMV_MAXM
+#define HM_TREE_GEMV_MAXM 1  // m = 2..4: the DMMA tree levels measured faster (C4 m=2: 490 vs 560 us)
+#endif
+constexpr int kTreeGemvMaxM = HM_TREE_GEMV_MAXM;
+
+hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
+  if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
+  if (k < 0) return fail(HM_ERR_INVALID_ARG, "k = %d < 0", k);
+  if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
+  memset(P, 0, sizeof *P);
+  P->n = n; P->b = b; P->p = p; P->q = q; P->m = nrhs; P->k = k;
+  const bool coupled = (k > 0 && p + q > 0);
+  const bool leaf_coupled = (k > 0 && (p > 0 || q > 0));
+  if (!coupled) {
+    P->vt = VtPath::kNone;
+  } else if (nrhs == 1 && p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
+    P->vt = VtPath::kGemv;
+    P->tile = 8 * b;
+  } else if (nrhs >= 2 && b % 4 == 0 && pow2_rank(k, 16, 64)) {
+    P->vt = VtPath::kMma;  // batched: warps per leaf
+    P->nt_vt = nt_for(nrhs, HM_VTB_NTMAX);
+  } else {
+    P->vt = VtPath::kGeneric;
+    P->mc_vt = vt_mc(b, nrhs);
+    P->tile = pick_tile(b, p, P->mc_vt);
+  }
+  P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
+  P->gemv_levels = coupled && nrhs <= kTreeGemvMaxM && pow2_rank(k, 16, 64);
+  if (P->mma_levels) P->nt_down = nt_for(nrhs, HM_TREE_NTMAX);
+  const int ktot = leaf_coupled ? k : 0;
+  if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
+    P->leaf = LeafPath::kGemv;
+  } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && ktot % 8 == 0) {
+    P->leaf = LeafPath::kMma;
+    P->nt_leaf = nt_for(nrhs, b == 256 ? 2 : 4);
+    if ((b + ktot) * (8 * P->nt_leaf + 4) > kSmemBudgetDoubles) P->leaf = LeafPath::kGeneric;
+  } else {
+    P->leaf = LeafPath::kGeneric;
+  }
+  if (P->leaf == LeafPath::kGeneric) {
+    P->mc_leaf = pick_mc(b, ktot, nrhs);
+    if ((b + ktot) * P->mc_leaf > kSmemBudgetDoubles)
+      return fail(HM_ERR_UNSUPPORTED, "leaf %lld too large for shared-memory staging", (long long)b);
+  }
+  const size_t blk = sizeof(double) * (size_t)k * nrhs;
+  const size_t coef = blk * (size_t)((((int64_t)1 << (p + 1)) - 2));
+  const size_t tcoef = blk * (size_t)((((int64_t)1 << (q + 1)) - 2));
+  size_t off = 0;
+  P->off_xh = off; off = align_up(off + coef);
+  P->off_yh = off; off = align_up(off + coef);
+  P->off_txh = off; off = align_up(off + tcoef);
+  P->off_tyh = off; off = align_up(off + tcoef);
+  P->off_x = P->off_y = off;
+  if (flags & HM_WS_HOSTIO) {
+    P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
+    P->off_y = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
+  }
+  P->total = std::max<size_t>(off, kAlign);
+  return HM_OK;
+}
+
+hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  return hss_plan_ex(tree->n, tree->leaf, tree->levels, 0, k, nrhs, flags, P);
+}
+
+// Levels with at least kTreeBigLevel nodes run one launch per level; the
+// levels above run inside one cooperative launch (hss_tree_sweep_kernel).
+#ifndef HM_TREE_BIG_LEVEL
+#define HM_TREE_BIG_LEVEL 2048
+#endif
+constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
+
+// ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
+#ifndef HM_GEMV_BIG
+#define HM_GEMV_BIG 8192
+#endif
+constexpr int64_t kGemvBigLevel = HM_GEMV_BIG;  // nodes: one launch per level from here down
+
+template <int K, int MB>
+hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
+                           int down_last) {
+  static int64_t cap = -1;  // co-resident CTAs of the sweep kernel (queried once)
+  if (cap < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_tree_gemv_sweep_kernel<K, MB>, 256, 0) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_tree_gemv_sweep)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (int64_t)per_sm * sms;
+  }
+  int lbig = 1;  // first level with >= kGemvBigLevel nodes
+  while (lbig <= p && (1ll << lbig) < kGemvBigLevel) ++lbig;
+  hm_status st;
+  for (int l = up_from_l; up && l >= lbig; --l) {
+    const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
+    st = launch("hss_up_gemv", s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    if (st) return st;
+  }
+  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
+  if (up_from >= 1 || down_to >= 1) {
+    const int64_t need = std::max<int64_t>(1, ((1ll << std::max(up_from, down_to)) + 7) / 8);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need)));
+    hm::TreeGemvParams arg = tp;
+    int a1 = up_from, a2 = down_to;
+    void* args[] = {&arg, &a1, &a2};
+    cudaError_t e = cudaSuccess;
+    st = launch("hss_tree_gemv_sweep", s, [&] {
+      e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_gemv_sweep_kernel<K, MB>, grid, dim3(256), args, 0,
+                                      s);
+    });
+    if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_gemv_sweep: %s", cudaGetErrorString(e));
+    if (st) return st;
+  }
+  for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
+    const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
+    st = launch("hss_down_gemv", s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    if (st) return st;
+  }
+  return HM_OK;
+}
+
+hm_status tree_gemv_dispatch(const hm::TreeGemvParams& tp, int p, int k, bool up, bool down, cudaStream_t s,
+                             int up_from, int down_last) {
+  const int mb = tp.m <= 1 ? 1 : (tp.m <= 2 ? 2 : 4);
+#define HM_TG(K_)                                                                      \
+  if (k == K_) {                                                                       \
+    if (mb == 1) return tree_gemv_launch<K_, 1>(tp, p, up, down, s, up_from, down_last); \
+    if (mb == 2) return tree_gemv_launch<K_, 2>(tp, p, up, down, s, up_from, down_last); \
+    return tree_gemv_launch<K_, 4>(tp, p, up, down, s, up_from, down_last);            \
+  }
+  HM_TG(16)
+  HM_TG(32)
+  HM_TG(64)
+#undef HM_TG
+  return fail(HM_ERR_UNSUPPORTED, "hss tree gemv: no instance for k=%d", k);
+}
+
+template <int KT, int NT>
+hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
+                      int down_last) {
+#ifndef HM_TREE_UP_MINB
+#define HM_TREE_UP_MINB 4
+#endif
+#ifndef HM_TREE_DN_MINB
+#define HM_TREE_DN_MINB 3
+#endif
+  // min CTAs per SM for the config-4 shape (k = 32, m = 32), measured (r01_tuning.md)
+  constexpr int MINB_UP = (KT == 32 && NT == 4) ? HM_TREE_UP_MINB : 0;
+  constexpr int MINB = (KT == 32 && NT == 4) ? HM_TREE_DN_MINB : 0;
+  const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
+  static bool attrs = false;
+  int sweep_blocks_per_sm = 0;
+  if (!attrs) {
+    allow_smem(hm::hss_up_pair_kernel<KT, NT, MINB_UP>, 200 * 1024);
+    allow_smem(hm::hss_down_pair_kernel<KT, NT, MINB>, 200 * 1024);
+    allow_smem(hm::hss_tree_sweep_kernel<KT, NT>, 200 * 1024);
+    attrs = true;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sweep_blocks_per_sm, hm::hss_tree_sweep_kernel<KT, NT>, 256,
+                                                    smem) != cudaSuccess)
+    return cuda_check("occupancy query (hss_tree_sweep)");
+  int lbig = 1;  // first level with >= kTreeBigLevel nodes
+  while (lbig <= p && (1ll << lbig) < kTreeBigLevel) ++lbig;
+  hm_status st;
+  // upsweep: big levels up_from_l .. lbig one launch each
+  for (int l = up_from_l; up && l >= lbig; --l) {
+    const unsigned pairs = (unsigned)(1ll << (l - 1));
+    st = launch("hss_up_pair", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
+    if (st) return st;
+  }
+  // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
+  const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
+  if (up_from >= 1 || down_to >= 1) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t need = std::max<int64_t>(1, (1ll << std::max(up_from, down_to)) / 2);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sweep_blocks_per_sm * sms, need)));
+    hm::TreeParams arg = tp;
+    int a1 = up_from, a2 = 1, a3 = 1, a4 = down_to;
+    void* args[] = {&arg, &a1, &a2, &a3, &a4};
+    cudaError_t e = cudaSuccess;
+    st = launch("hss_tree_sweep", s, [&] {
+      e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_sweep_kernel<KT, NT>, grid, dim3(256), args, smem, s);
+    });
+    if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
+    if (st) return st;
+  }
+  // downsweep: big levels lbig .. p one launch each
+  for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
+    const unsigned pairs = (unsigned)(1ll << (l - 1));
+    st = launch("hss_down_pair", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    if (st) return st;
+  }
+  return HM_OK;
+}
+
+hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s,
+                        int up_from, int down_last) {
+#define HM_TREE(KT_)                                                                     \
+  if (k == KT_) {                                                                        \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from, down_last);     \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from, down_last);     \
+    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from, down_last);                  \
+  }
+  HM_TREE(16)
+  HM_TREE(32)
+  HM_TREE(64)
+#undef HM_TREE
+  return fail(HM_ERR_UNSUPPORTED, "hss tree: no instance for k=%d", k);
+}
+
+// Upsweep and coupling/downsweep of a (sub)tree of depth p on its workspace:
+// generic per-level kernels or the DMMA tree kernels (tree_dispatch).
+hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
+                         double* yh, const double* R_root, const double* y_root, bool up, bool down,
+                         cudaStream_t stream, int bt, int up_from, int down_last) {
+  const int k = P.k, nrhs = P.m;
+  hm_status st;
+  if (up_from < 0) up_from = p - 1;  // first upsweep level to compute
+  if (down_last < 0) down_last = p;  // last downsweep level to compute
+  if (P.gemv_levels) {
+    hm::TreeGemvParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
+    return tree_gemv_dispatch(tp, p, k, up, down, stream, up_from, down_last);
+  }
+  if (P.mma_levels) {
+    hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
+    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from, down_last);
+  }
+  const int64_t km = (int64_t)k * nrhs;
+  if (up)
+    for (int l = up_from; l >= 1; --l) {
+      hm::HssLevelParams hp{W, B, xh, yh, nullptr, nullptr, l, k, nrhs, 0};
+      const int64_t total = ((int64_t)1 << l) * km;
+      const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+      st = launch("hss_up_level", stream, [&] { hm::hss_up_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+      if (st) return st;
+    }
+  if (down)
+    for (int l = 1; l <= down_last; ++l) {
+      hm::HssLevelParams hp{R, B, xh, yh, R_root, y_root, l, k, nrhs, bt};
+      const int64_t total = ((int64_t)1 << l) * km;
+      const unsigned blocks = (unsigned)std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16);
+      st = launch("hss_down_level", stream,
+                  [&] { hm::hss_down_level_kernel<<<blocks, hm::kThreads, 0, stream>>>(hp); });
+      if (st) return st;
+    }
+  return HM_OK;
+}
+
+// x_out = A^T Z for one block (A [K][k], Z [K][m]): the subtree root's upsweep
+// step x_root = W_root^T [x_{1,0}; x_{1,1}] and the leaf-only subtree x = V^T X.
+hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int64_t K, double* out,
+                        cudaStream_t stream) {
+  const int k = P.k, nrhs = P.m;
+  if (nrhs >= 2 && pow2_rank(k, 16, 64) && K % 4 == 0) {
+    hm::BatchedVtParams bp{A, 0, Z, 0, out, 0, 1, (int32_t)K, nrhs};
+    return vt_batched_dispatch("vt_batched", bp, k, nt_for(nrhs, HM_VTB_NTMAX), stream);
+  }
+  hm::VtParams vp;
+  memset(&vp, 0, sizeof vp);
+  vp.X = Z; vp.n = K; vp.m = nrhs; vp.mc = vt_mc(K, nrhs); vp.tile = K; vp.nlev = 1;
+  vp.lev[0].V = A; vp.lev[0].k = k; vp.lev[0].s = K; vp.lev[0].out = out; vp.lev[0].partial = nullptr;
+  return vt_generic(vp, K, stream);
+}
+
+// Step 1 on the subtree: leaf x = V^T X, upsweep to level 1, and (W_root given)
+// the subtree root's x_root = W_root^T [x_{1,0}; x_{1,1}]. A depth-0 subtree is
+// one leaf: its x is the root's, written to x_root.
+hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
+                       const double* W_root, double* x_root, cudaStream_t stream) {
+  const int k = P.k, nrhs = P.m;
+  const int64_t km = (int64_t)k * nrhs;
+  hm_status st;
+  double* xleaf = (P.p == 0) ? x_root : xh + (((int64_t)1 << P.p) - 2) * km;
+  if (xleaf == nullptr) return HM_OK;
+  const int up_from = P.p - 1;
+  if (P.vt == VtPath::kMma) {
+    hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
+    if ((st = vt_batched_dispatch("vt_batched", bp, k, P.nt_vt, stream))) return st;
+  } else {
+    hm::VtParams vp;
+    memset(&vp, 0, sizeof vp);
+    vp.X = Xd; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt ? P.mc_vt : vt_mc(P.b, nrhs);
+    vp.tile = P.tile ? P.tile : pick_tile(P.b, P.p, vp.mc); vp.nlev = 1;
+    vp.lev[0].V = V; vp.lev[0].k = k; vp.lev[0].s = P.b;
+    vp.lev[0].out = xleaf;
+    vp.lev[0].partial = nullptr;
+    st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
+    if (st) return st;
+  }
+  if (up_from >= 1 && (st = hss_tree_phase(P, P.p, W, nullptr, nullptr, xh, nullptr, nullptr, nullptr, true,
+                                             false, stream, 0, up_from)))
+    return st;
+  if (W_root && P.p >= 1 && (st = hss_single_vt(P, W_root, xh, 2 * k, x_root, stream))) return st;
+  return HM_OK;
+}
+
+// Step 4: Y(I_i) = U_i y_i + D_i X(I_i); y of the leaves from yh (or y_root for a
+// depth-0 subtree).
+hm_status hss_leaf_phase(const HssPlan& P, const double* D, const double* U, const double* Xd, double* Yd,
+                         const double* yleaf, cudaStream_t stream, bool dtrans = false) {
+  hm::LeafParams lp;
+  memset(&lp, 0, sizeof lp);
+  lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf; lp.dtrans = dtrans ? 1 : 0;
+  const bool coupled = P.k > 0 && yleaf != nullptr;
+  if (coupled) {
+    hm::LeafSeg& sg = lp.seg[lp.nseg++];
+    sg.A = U;
+    sg.T = yleaf;
+    sg.k = P.k; sg.shift = 0; sg.xr = 0;
+    lp.ktot = P.k;
+  }
+  return leaf_dispatch(lp, 1ll << P.p, P.leaf, coupled ? P.k : 0, P.nt_leaf, P.mc_leaf, stream);
+}
+
+hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, const double* R, const double* W,
+                         const double* B, void* ws, size_t ws_bytes) {
+  if (!ws || ws_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, P.total);
+  if (!aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+  const int k = P.k;
+  if (k == 0 || P.p + P.q == 0) return HM_OK;  // block diagonal: only D is read
+  if (!U || !V) return fail(HM_ERR_INVALID_ARG, "NULL U / V pointer");
+  if (P.p > 0 && !B) return fail(HM_ERR_INVALID_ARG, "NULL B pointer");
+  if (P.p > 1 && (!R || !W)) return fail(HM_ERR_INVALID_ARG, "NULL R / W pointer");
+  if (k > 0 && (!aligned16(U) || !aligned16(V) || (B && !aligned16(B)) || (R && !aligned16(R)) || (W && !aligned16(W))))
+    return fail(HM_ERR_INVALID_ARG, "U, V, R, W, B must be 16-byte aligned");
+  return HM_OK;
+}
+
+// ---- small trees: one cooperative launch (hm_small.cuh) ----
+#ifndef HM_NO_SMALL
+#define HM_NO_SMALL 0
+#endif
+constexpr int kSmallMaxLevels = 8;  // up to 256 leaves: one CTA per leaf, all co-resident
+
+bool small_ok(const HssPlan& P) {
+  return !HM_NO_SMALL && P.q == 0 && P.mma_levels && P.p >= 1 && P.p <= kSmallMaxLevels && P.m >= 2 && P.m <= 32 &&
+         (P.b == 64 || P.b == 128);
+}
+
+template <int KT, int NT, int RG>
+hm_status small_launch(const hm::SmallHssParams& sp, unsigned grid, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)KT * (NT * 8 + 2);
+  static int64_t cap = -1;  // co-resident CTAs of this instance (queried once)
+  if (cap < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_small_kernel<KT, NT, RG>, 256, smem) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_small)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (int64_t)per_sm * sms;
+  }
+  if (cap < (int64_t)grid) return fail(HM_ERR_UNSUPPORTED, "hss_small: grid not co-resident");
+  hm::SmallHssParams arg = sp;
+  void* args[] = {&arg};
+  cudaError_t e = cudaSuccess;
+  hm_status st = launch("hss_small", s, [&] {
+    e = cudaLaunchCooperativeKernel((const void*)hm::hss_small_kernel<KT, NT, RG>, dim3(grid), dim3(256), args, smem,
+                                    s);
+  });
+  if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_small: %s", cudaGetErrorString(e));
+  return st;
+}
+
+hm_status small_dispatch(const HssPlan& P, const double* D, const double* U, const double* V, const double* R,
+                         const double* W, const double* B, const double* X, double* Y, double* xh, double* yh,
+                         cudaStream_t s) {
+  const int h = std::min(3, P.p);
+  hm::SmallHssParams sp{D, U, V, R, W, B, X, Y, xh, yh, (int32_t)P.b, P.p, P.m, h, 1 << (P.p - h), 0};
+  const unsigned grid = 1u << P.p;
+  const int nt = P.m <= 16 ? 2 : 4, rg = (int)(P.b / 64);
+#define HM_SM(KT_)                                                         \
+  if (P.k == KT_) {                                                        \
+    if (nt == 2 && rg == 1) return small_launch<KT_, 2, 1>(sp, grid, s);   \
+    if (nt == 2 && rg == 2) return small_launch<KT_, 2, 2>(sp, grid, s);   \
+    if (nt == 4 && rg == 1) return small_launch<KT_, 4, 1>(sp, grid, s);   \
+    if (nt == 4 && rg == 2) return small_launch<KT_, 4, 2>(sp, grid, s);   \
+  }
+  HM_SM(16)
+  HM_SM(32)
+  HM_SM(64)
+#undef HM_SM
+  return fail(HM_ERR_UNSUPPORTED, "hss_small: no instance");
+}
+
+// op = 1: Y = A^T X. A^T is HSS on the same tree with row
+// bases V (translations W), column bases U (translations R), cores
+// S'_{2q,2q+1} = B21^T, S'_{2q+1,2q} = B12^T and leaf blocks D_i^T: the same
+// four steps with U <-> V, R <-> W exchanged, transposed cores (bt) and D^T.
+hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                  const double* R, const double* W, const double* B, const double* X, int32_t nrhs, double* Y,
+                  void* ws, size_t ws_bytes, cudaStream_t stream, int32_t flags, int op = 0) {
+  if (op) {
+    std::swap(U, V);
+    std::swap(R, W);
+  }
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, nrhs, flags, &P);
+  if (st) return st;
+  if (!D || !X || !Y) return fail(HM_ERR_INVALID_ARG, "NULL D / X / Y pointer");
+  if (!aligned16(D)) return fail(HM_ERR_INVALID_ARG, "D must be 16-byte aligned");
+  if ((st = hss_check_ptrs(P, U, V, R, W, B, ws, ws_bytes))) return st;
+  const size_t xy_bytes = sizeof(double) * (size_t)(P.n * nrhs);
+  if (overlap(X, xy_bytes, Y, xy_bytes)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  if (!(flags & HM_WS_HOSTIO) && (!aligned16(X) || !aligned16(Y)))
+    return fail(HM_ERR_INVALID_ARG, "X and Y must be 16-byte aligned");
+
+  char* w = static_cast<char*>(ws);
+  double* xh = reinterpret_cast<double*>(w + P.off_xh);
+  double* yh = reinterpret_cast<double*>(w + P.off_yh);
+  const double* Xd = X;
+  double* Yd = Y;
+  g_launches = 0;
+  prof_new_call();
+  if (flags & HM_WS_HOSTIO) {
+    Xd = reinterpret_cast<double*>(w + P.off_x);
+    Yd = reinterpret_cast<double*>(w + P.off_y);
+    if (cudaMemcpyAsync(const_cast<double*>(Xd), X, xy_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+      return cuda_check("H2D copy of X");
+  }
+  const int64_t km = (int64_t)k * nrhs;
+  const bool coupled = (k > 0 && P.p > 0);
+  if (coupled && op == 0 && small_ok(P)) {  // small tree: the whole product in one launch (hm_small.cuh)
+    if ((st = small_dispatch(P, D, U, V, R, W, B, Xd, Yd, xh, yh, stream)) == HM_OK) {
+      if ((flags & HM_WS_HOSTIO) && cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return cuda_check("D2H copy of Y");
+      return HM_OK;
+    }
+    if (st != HM_ERR_UNSUPPORTED) return st;  // not co-resident on this device: the level-by-level path
+  }
+  if (coupled) {
+    if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
+    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op))) return st;
+  }
+  const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
+  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) return st;
+  if (flags & HM_WS_HOSTIO) {
+    if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+      return cuda_check("D2H copy of Y");
+  }
+  return HM_OK;
+}
+
+// ---- distributed HSS ----
+
+hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, int32_t flags,
+                        HssPlan* P, DistPart* d) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  if ((st = check_part(tree, part, d))) return st;
+  return hss_plan_ex(tree->n >> d->q, tree->leaf, tree->levels - d->q, d->q, k, nrhs, flags, P);
+}
+}  // namespace hmi
+
+using namespace hmi;
+
+extern "C" {
+
+hm_status hm_hss_norm2_workspace_bytes(const hm_tree* tree, int32_t k, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, 1, 0, &P);
+  if (st) return st;
+  *bytes = norm_plan(P.total, P.n).total;
+  return HM_OK;
+}
+
+hm_status hss_norm2_est(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                        const double* R, const double* W, const double* B, const double* x0, int32_t iters,
+                        double* est, void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, 1, 0, &P);
+  if (st) return st;
+  const NormPlan N = norm_plan(P.total, P.n);
+  if (!workspace || workspace_bytes < N.total)
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, N.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return power_norm2(P.n, x0, iters, est, static_cast<char*>(workspace), N, s,
+                     [&](int op, const double* x, double* y) {
+                       return hss_run(tree, k, D, U, V, R, W, B, x, 1, y, workspace, P.total, s, 0, op);
+                     });
+}
+hm_status hm_hss_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  HssPlan P;
+  hm_status st = hss_plan(tree, k, nrhs, flags, &P);
+  if (st) return st;
+  *bytes = P.total;
+  return HM_OK;
+}
+
+hm_status hss_matvec(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                     const double* R, const double* W, const double* B, const double* X, int32_t nrhs,
+                     double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
+                 static_cast<cudaStream_t>(stream), 0);
+}
+
+hm_status hss_matvec_t(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                       const double* R, const double* W, const double* B, const double* X, int32_t nrhs,
+                       double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
+                 static_cast<cudaStream_t>(stream), 0, 1);
+}
+
+hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B, const double* X_host,
+                            int32_t nrhs, double* Y_host, void* workspace, size_t workspace_bytes, void* stream) {
+  return hss_run(tree, k, D, U, V, R, W, B, X_host, nrhs, Y_host, workspace, workspace_bytes,
+                 static_cast<cudaStream_t>(stream), HM_WS_HOSTIO);
+}
+
+hm_status hm_hss_dist_sizes(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, size_t* ws_bytes,
+                            int64_t* send_doubles) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (ws_bytes) *ws_bytes = P.total;
+  if (send_doubles) *send_doubles = (d.q > 0) ? (int64_t)k * nrhs : 0;
+  return HM_OK;
+}
+
+hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* part, const double* V_local,
+                                const double* W_sub, const double* W_root, const double* X_local, int32_t nrhs,
+                                double* send, void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
+    return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
+  g_launches = 0;
+  prof_new_call();
+  if (k == 0) return HM_OK;  // block diagonal: nothing to exchange, no tree
+  double* xh = reinterpret_cast<double*>(static_cast<char*>(workspace) + P.off_xh);
+  if (d.q == 0) {
+    // one rank: the whole tree is local and the exchange is empty; Step 1 and
+    // the upsweep to level 1 run here (as in hss_matvec), _end does the rest
+    if (P.p == 0) return HM_OK;
+    if (!X_local || !V_local || (P.p >= 2 && !W_sub)) return fail(HM_ERR_INVALID_ARG, "NULL V / W / X pointer");
+    return hss_up_phase(P, V_local, W_sub, X_local, xh, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+  }
+  if (!X_local || !V_local || !send || (P.p >= 2 && !W_sub) || (P.p >= 1 && !W_root))
+    return fail(HM_ERR_INVALID_ARG, "NULL V / W / X / send pointer");
+  return hss_up_phase(P, V_local, W_sub, X_local, xh, W_root, send, static_cast<cudaStream_t>(stream));
+}
+
+hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* part, const double* D_local,
+                              const double* U_local, const double* R_sub, const double* B_sub,
+                              const double* R_root, const double* W_top, const double* R_top, const double* B_top,
+                              const double* X_local, int32_t nrhs, const double* gathered, double* Y_local,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
+  if (st) return st;
+  if (!D_local || !X_local || !Y_local || !aligned16(D_local))
+    return fail(HM_ERR_INVALID_ARG, "NULL or misaligned D / X / Y pointer");
+  if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
+    return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  double* xh = reinterpret_cast<double*>(w + P.off_xh);
+  double* yh = reinterpret_cast<double*>(w + P.off_yh);
+  double* txh = reinterpret_cast<double*>(w + P.off_txh);
+  double* tyh = reinterpret_cast<double*>(w + P.off_tyh);
+  const int64_t km = (int64_t)k * nrhs;
+  g_launches = 0;
+  prof_new_call();
+  const double* yleaf = nullptr;
+  if (k > 0 && d.q == 0 && P.p >= 1) {
+    // one rank: coupling + downsweep of the whole (local) tree on the x blocks
+    // _begin left in the workspace, then the leaves (as in hss_matvec)
+    if (!U_local || !B_sub || (P.p >= 2 && !R_sub)) return fail(HM_ERR_INVALID_ARG, "NULL U / R / B pointer");
+    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s))) return st;
+    yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+  }
+  if (k > 0 && d.q > 0) {
+    if (!gathered || !U_local || !B_top || (d.q >= 2 && (!W_top || !R_top)) || (P.p >= 1 && (!R_root || !B_sub)) ||
+        (P.p >= 2 && !R_sub))
+      return fail(HM_ERR_INVALID_ARG, "NULL gathered / generator pointer");
+    // replicated top tree: x of level q from the allgather, up q-1..1, down 1..q
+    if (cudaMemcpyAsync(txh + (((int64_t)1 << d.q) - 2) * km, gathered, sizeof(double) * (size_t)(d.P * km),
+                        cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return cuda_check("copy of the gathered blocks");
+    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s))) return st;
+    const double* y_root = tyh + (((int64_t)1 << d.q) - 2 + d.rank) * km;
+    if (P.p >= 1) {
+      // the subtree's x blocks were left in this workspace by _begin
+      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s))) return st;
+      yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+    } else {
+      yleaf = y_root;
+    }
+  }
+  return hss_leaf_phase(P, D_local, U_local, X_local, Y_local, yleaf, s);
+}
+
+}  // extern "C"

@@ -57,7 +57,7 @@ struct VtParams {
 // Thread t owns output o = t % O2 of the (k x mc) block (a = o % k, c = o / k)
 // for the rows r == t / O2 (mod 256 / O2) of the current segment, then a
 // fixed-order shared-memory reduction over the row groups.
-__global__ void __launch_bounds__(kThreads) vt_contract_kernel(const VtParams P) {
+static __global__ void __launch_bounds__(kThreads) vt_contract_kernel(const VtParams P) {
   extern __shared__ double smem[];
   const int64_t tile = P.tile;
   const int64_t row0 = (int64_t)blockIdx.x * tile;
@@ -153,7 +153,7 @@ struct ReduceParams {
   ReduceLevel lev[kMaxLevels];
 };
 
-__global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceParams P) {
+static __global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceParams P) {
   const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   int L = 0;
   while (L + 1 < P.nlev && P.lev[L + 1].thread_begin <= t) ++L;
@@ -195,7 +195,7 @@ struct CombineParams {
   int64_t lev_off[kMaxLevels + 2];  // start of level l's block (l = 1..q), lev_off[q+1] = per_rank
 };
 
-__global__ void __launch_bounds__(kThreads) dist_combine_kernel(const CombineParams C) {
+static __global__ void __launch_bounds__(kThreads) dist_combine_kernel(const CombineParams C) {
   const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (e >= C.per_rank) return;
   int l = 1;
@@ -228,13 +228,6 @@ struct LeafParams {
   int32_t nseg;
   int32_t ktot;     // sum of segment ranks
   int32_t dtrans;   // 1: the leaf term is D_i^T X(I_i) (adjoint product)
-  int32_t dp;       // HSS leaf-level downsweep fused into the leaf pass (leaf_mma DOWN): level p (>= 1)
-  // y_i = S_w x_{i^1} + R_w y_{parent}: cores / translations of the level-(p-1) nodes,
-  // level-p x blocks, level-(p-1) y blocks (dyp NULL when p = 1)
-  const double* dB;
-  const double* dR;
-  const double* dx;
-  const double* dyp;
   LeafSeg seg[kMaxLevels];
 };
 
@@ -330,7 +323,7 @@ struct HssLevelParams {
   int32_t bt;        // 1: cores of the adjoint, S'_0 = B21^T, S'_1 = B12^T
 };
 
-__global__ void __launch_bounds__(kThreads) hss_up_level_kernel(const HssLevelParams P) {
+static __global__ void __launch_bounds__(kThreads) hss_up_level_kernel(const HssLevelParams P) {
   const int l = P.level, k = P.k, m = P.m;
   const int64_t cnt = 1ll << l;
   const int64_t km = (int64_t)k * m;
@@ -353,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) hss_up_level_kernel(const HssLevelPa
 //   y_l[2q+w] = S_w x_l[2q+1-w] + (l >= 2 ? R_{l-1,q}[w] y_{l-1}[q] : 0)
 // S_0 = B12, S_1 = B21 of node (l-1, q) (index 2^{l-1}-1+q); R node (l-1,q)
 // at index 2^{l-1}-2+q, rows w*k..w*k+k-1.
-__global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const HssLevelParams P) {
+static __global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const HssLevelParams P) {
   const int l = P.level, k = P.k, m = P.m;
   const int64_t cnt = 1ll << l;
   const int64_t km = (int64_t)k * m;

@@ -180,111 +180,4 @@ __global__ void __launch_bounds__(256) hss_small_kernel(const SmallHssParams P) 
   }
 }
 
-// ------------------------------------------------------------------ HODLR --
-// The whole HODLR product for small problems (BASELINE config 1: n = 1024,
-// 16 leaves, 4 levels) in ONE cooperative launch, CTA = leaf (Fig. 5 left,
-// P:666-678, level-parallel as in the main path). Latency is the cost, so every
-// input the CTA needs (D_L, the leaf's rows of every U_l and V_l, X(I_L)) is
-// requested at once with cp.async at kernel start:
-//   phase 1  partial t_l = V_l(I_L)^T X(I_L), every level, from shared memory,
-//            to the workspace; grid-wide barrier.
-//   phase 2  t_{l, sib(node_l(L))} = the sum of the partials of the 2^(p-l)
-//            leaves under the sibling node, in leaf order (fixed: bitwise
-//            repeatable); Y(I_L) = D_L X(I_L) + sum_l U_l(I_L) t_l from shared
-//            memory, thread per output.
-struct SmallHodlrParams {
-  const double *D, *U, *V, *X;
-  double* Y;
-  double* part;       // [nleaves][ktot][m] partials
-  int64_t n;
-  int32_t b, p, m, ktot;
-  int32_t k[kMaxLevels];   // ranks of levels 1..p (index l - 1)
-  int64_t koff[kMaxLevels]; // sum of ranks of the levels before l (index l - 1)
-};
-
-// shared layout (doubles): D [b][b+2] | U [b][ktot] | V [b][ktot] | X [b][m] | T [ktot][m]
-__host__ __device__ inline int64_t hodlr_small_smem_doubles(int64_t b, int64_t kt, int64_t m) {
-  return b * (b + 2) + 2 * b * kt + b * m + kt * m + 8;
-}
-
-__global__ void __launch_bounds__(256) hodlr_small_kernel(const SmallHodlrParams P) {
-  extern __shared__ __align__(16) double hsm[];
-  const int64_t L = blockIdx.x, b = P.b, n = P.n;
-  const int m = P.m, p = P.p, kt = P.ktot;
-  const int64_t r0 = L * b;
-  const int zd = (int)b + 2;
-  double* Ds = hsm;
-  double* Us = Ds + b * zd;
-  double* Vs = Us + b * kt;
-  double* Xs = Vs + b * kt;
-  double* Ts = Xs + b * m;
-  // every input of the CTA in flight at once
-  stage_rows_async(Ds, zd, P.D + L * b * b, b, (int)b, (int)b, (int)b);
-  {
-    int64_t uoff = 0;
-    for (int l = 1; l <= p; ++l) {
-      const int k = P.k[l - 1];
-      if (k > 0) {
-        stage_rows_async(Us + P.koff[l - 1], kt, P.U + uoff + r0 * k, k, (int)b, k, k);
-        stage_rows_async(Vs + P.koff[l - 1], kt, P.V + uoff + r0 * k, k, (int)b, k, k);
-      }
-      uoff += n * k;
-    }
-  }
-  stage_rows_async(Xs, m, P.X + r0 * m, m, (int)b, m, m);
-  cp_async_wait_all();
-  __syncthreads();
-  // phase 1: partials of this leaf; G = 8 consecutive lanes per (rank column, X
-  // column) output split the rows (stride G), then a fixed butterfly over the group
-  constexpr int G = 8;
-  double* myp = P.part + L * (int64_t)kt * m;
-  for (int base = 0; base < kt * m; base += blockDim.x / G) {
-    const int o = base + (int)threadIdx.x / G, g = (int)threadIdx.x % G;
-    double s = 0.0;
-    if (o < kt * m) {
-      const int a = o / m, c = o - a * m;
-      for (int64_t r = g; r < b; r += G) s = fma(Vs[r * kt + a], Xs[r * m + c], s);
-    }
-#pragma unroll
-    for (int w = 1; w < G; w <<= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
-    if (o < kt * m && g == 0) myp[o] = s;
-  }
-  cooperative_groups::this_grid().sync();  // every leaf's partials written
-  // phase 2a: t of the sibling nodes, thread per (level, rank column, X column)
-  for (int l = 1; l <= p; ++l) {
-    const int k = P.k[l - 1];
-    const int64_t span = (int64_t)1 << (p - l);
-    const int64_t first = ((L >> (p - l)) ^ 1) * span;  // first leaf of the sibling node
-    for (int o = threadIdx.x; o < k * m; o += blockDim.x) {
-      const int64_t e = P.koff[l - 1] * m + o;
-      double s = 0.0;
-      int64_t L2 = first;
-      for (; L2 + 4 <= first + span; L2 += 4) {  // 4 independent loads in flight, summed in order
-        const double v0 = ldg_cg(P.part + L2 * kt * m + e), v1 = ldg_cg(P.part + (L2 + 1) * kt * m + e);
-        const double v2 = ldg_cg(P.part + (L2 + 2) * kt * m + e), v3 = ldg_cg(P.part + (L2 + 3) * kt * m + e);
-        s += v0; s += v1; s += v2; s += v3;
-      }
-      for (; L2 < first + span; ++L2) s += ldg_cg(P.part + L2 * kt * m + e);
-      Ts[e] = s;
-    }
-  }
-  __syncthreads();
-  // phase 2b: Y(I_L) = D_L X(I_L) + U(I_L) T; G consecutive lanes per output
-  // split the extended row, fixed butterfly over the group
-  for (int64_t base = 0; base < b * m; base += blockDim.x / G) {
-    const int64_t o = base + (int)threadIdx.x / G;
-    const int g = (int)threadIdx.x % G;
-    double s = 0.0;
-    if (o < b * m) {
-      const int64_t r = o / m;
-      const int c = (int)(o - r * m);
-      for (int64_t j = g; j < b; j += G) s = fma(Ds[r * zd + j], Xs[j * m + c], s);
-      for (int a = g; a < kt; a += G) s = fma(Us[r * kt + a], Ts[a * m + c], s);
-    }
-#pragma unroll
-    for (int w = 1; w < G; w <<= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
-    if (o < b * m && g == 0) P.Y[(r0 + (o / m)) * m + (o % m)] = s;
-  }
-}
-
 }  // namespace hm

@@ -219,13 +219,13 @@ def hodlr_matvec(n, levels, leaf, ranks, D, U, V, X, Y=None, workspace=None, str
     X: [n][nrhs] (or [n]) float64 CUDA tensor. Returns Y (allocated if None)."""
     import torch
     X = _dev(X, "X")
-    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
-    _hodlr_sizes(n, leaf, ranks, D, U, V)
     ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs), workspace, X.device)
+    _xy(X, Y, n)
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     t = make_tree(n, levels, leaf)
     _check(getattr(load(), _fn)(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(X), nrhs,
                                 _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -245,10 +245,10 @@ def hodlr_matvec_hostio(n, levels, leaf, ranks, D, U, V, X_host, Y_host, workspa
     for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
         if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous float64 host tensor")
-    _xy(X_host, Y_host, n)
     _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
-    _hodlr_sizes(n, leaf, ranks, D, U, V)
     ws = _workspace(hm_hodlr_workspace_bytes(n, levels, leaf, ranks, nrhs, HM_WS_HOSTIO), workspace, D.device)
+    _xy(X_host, Y_host, n)
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     t = make_tree(n, levels, leaf)
     _check(load().hodlr_matvec_hostio(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V),
                                       X_host.data_ptr(), nrhs, Y_host.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -265,14 +265,14 @@ def hss_matvec(n, levels, leaf, k, D, U, V, R, W, B, X, Y=None, workspace=None, 
     """Y = A X on the current CUDA stream for the HSS matrix (D, U, V, R, W, B) (include/hm.h)."""
     import torch
     X = _dev(X, "X")
-    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
-    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs), workspace, X.device)
+    _xy(X, Y, n)
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     t = make_tree(n, levels, leaf)
     _check(getattr(load(), _fn)(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
                                 _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -285,11 +285,11 @@ def hss_matvec_hostio(n, levels, leaf, k, D, U, V, R, W, B, X_host, Y_host, work
     for t_, nm in ((X_host, "X_host"), (Y_host, "Y_host")):
         if t_.is_cuda or t_.dtype != torch.float64 or not t_.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous float64 host tensor")
-    _xy(X_host, Y_host, n)
     for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
-    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     ws = _workspace(hm_hss_workspace_bytes(n, levels, leaf, k, nrhs, HM_WS_HOSTIO), workspace, D.device)
+    _xy(X_host, Y_host, n)
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     t = make_tree(n, levels, leaf)
     _check(load().hss_matvec_hostio(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
                                     X_host.data_ptr(), nrhs, Y_host.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -324,11 +324,11 @@ def hodlr_norm2_est(n, levels, leaf, ranks, D, U, V, x0, iters, est=None, worksp
     """||A||_2 estimate (power method on A A^*, include/hm.h hodlr_norm2_est): returns a 1-element
     float64 CUDA tensor written asynchronously on the stream."""
     x0 = _dev(x0, "x0")
-    _numel_at_least(x0, n, "x0")
     _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
-    _hodlr_sizes(n, leaf, ranks, D, U, V)
     est = _est(est, x0.device)
     ws = _workspace(hm_hodlr_norm2_workspace_bytes(n, levels, leaf, ranks), workspace, x0.device)
+    _numel_at_least(x0, n, "x0")
+    _hodlr_sizes(n, leaf, ranks, D, U, V)
     t = make_tree(n, levels, leaf)
     _check(load().hodlr_norm2_est(ctypes.byref(t), _ranks(ranks, levels), _ptr(D), _ptr(U), _ptr(V), _ptr(x0),
                                   int(iters), _ptr(est), ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -338,12 +338,12 @@ def hodlr_norm2_est(n, levels, leaf, ranks, D, U, V, x0, iters, est=None, worksp
 def hss_norm2_est(n, levels, leaf, k, D, U, V, R, W, B, x0, iters, est=None, workspace=None, stream=None):
     """||A||_2 estimate of an HSS matrix (include/hm.h hss_norm2_est)."""
     x0 = _dev(x0, "x0")
-    _numel_at_least(x0, n, "x0")
     for t_, nm in ((D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
-    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     est = _est(est, x0.device)
     ws = _workspace(hm_hss_norm2_workspace_bytes(n, levels, leaf, k), workspace, x0.device)
+    _numel_at_least(x0, n, "x0")
+    _hss_sizes(n, levels, leaf, k, D, U, V, R, W, B)
     t = make_tree(n, levels, leaf)
     _check(load().hss_norm2_est(ctypes.byref(t), int(k), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B),
                                 _ptr(x0), int(iters), _ptr(est), ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -406,16 +406,16 @@ def hodlr_matvec_general(n, levels, c, ranks, D, U, V, X, op=0, Y=None, workspac
     import torch
     c = _endpoints(c, levels)
     X = _dev(X, "X")
-    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y"); _dev(D, "D"); _dev(U, "U"); _dev(V, "V")
+    ws = _workspace(hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs), workspace, X.device)
+    _xy(X, Y, n)
     _numel_at_least(D, _leaf_block_doubles(c), "D")
     kt = sum(int(r) for r in ranks)
     _numel_at_least(U, n * kt, "U")
     _numel_at_least(V, n * kt, "V")
-    ws = _workspace(hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs), workspace, X.device)
     _check(load().hodlr_matvec_general(int(n), int(levels), c.ctypes.data, _ranks(ranks, levels), int(op), _ptr(D),
                                        _ptr(U), _ptr(V), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
                                        _stream(stream)))
@@ -435,15 +435,15 @@ def hss_matvec_general(n, levels, c, k, D, U, V, R, W, B, X, op=0, Y=None, works
     import torch
     c = _endpoints(c, levels)
     X = _dev(X, "X")
-    _xy(X, Y, n)
     nrhs = 1 if X.dim() == 1 else X.shape[1]
     if Y is None:
         Y = torch.empty_like(X)
     for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
         _dev(t_, nm)
+    ws = _workspace(hm_hss_general_workspace_bytes(n, levels, c, k, nrhs), workspace, X.device)
+    _xy(X, Y, n)
     _hss_sizes(n, levels, 0, k, None, U, V, R, W, B)
     _numel_at_least(D, _leaf_block_doubles(c), "D")
-    ws = _workspace(hm_hss_general_workspace_bytes(n, levels, c, k, nrhs), workspace, X.device)
     _check(load().hss_matvec_general(int(n), int(levels), c.ctypes.data, int(k), int(op), _ptr(D), _ptr(U), _ptr(V),
                                      _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
                                      _stream(stream)))

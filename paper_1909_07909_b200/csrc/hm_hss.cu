@@ -9,6 +9,11 @@
 #include "hm_tree.cuh"
 #include "hm_treegemv.cuh"
 
+// Trace names carry the column-tile count of the instance that ran (tests
+// assert which instances a shape exercises): "<nt1>" = 8 columns per tile group.
+#define HM_NT_NAME(base) (NT == 1 ? base "<nt1>" : NT == 2 ? base "<nt2>" : base "<nt4>")
+#define HM_MB_NAME(base) (MB == 1 ? base "<m1>" : MB == 2 ? base "<m2>" : base "<m4>")
+
 namespace hmi {
 
 #ifndef HM_TREE_GEMV_MAXM
@@ -109,7 +114,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
   hm_status st;
   for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
-    st = launch("hss_up_gemv", s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    st = launch(HM_MB_NAME("hss_up_gemv"), s, [&] { hm::hss_up_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
     if (st) return st;
   }
   const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
@@ -120,7 +125,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
     int a1 = up_from, a2 = down_to;
     void* args[] = {&arg, &a1, &a2};
     cudaError_t e = cudaSuccess;
-    st = launch("hss_tree_gemv_sweep", s, [&] {
+    st = launch(HM_MB_NAME("hss_tree_gemv_sweep"), s, [&] {
       e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_gemv_sweep_kernel<K, MB>, grid, dim3(256), args, 0,
                                       s);
     });
@@ -129,7 +134,7 @@ hm_status tree_gemv_launch(const hm::TreeGemvParams& tp, int p, bool up, bool do
   }
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned grid = (unsigned)(((1ll << l) + 7) / 8);
-    st = launch("hss_down_gemv", s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
+    st = launch(HM_MB_NAME("hss_down_gemv"), s, [&] { hm::hss_down_gemv_kernel<K, MB><<<grid, 256, 0, s>>>(tp, l); });
     if (st) return st;
   }
   return HM_OK;
@@ -181,7 +186,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // upsweep: big levels up_from_l .. lbig one launch each
   for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch("hss_up_pair", s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
+    st = launch(HM_NT_NAME("hss_up_pair"), s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1)
@@ -196,7 +201,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     int a1 = up_from, a2 = 1, a3 = 1, a4 = down_to;
     void* args[] = {&arg, &a1, &a2, &a3, &a4};
     cudaError_t e = cudaSuccess;
-    st = launch("hss_tree_sweep", s, [&] {
+    st = launch(HM_NT_NAME("hss_tree_sweep"), s, [&] {
       e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_sweep_kernel<KT, NT>, grid, dim3(256), args, smem, s);
     });
     if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
@@ -205,7 +210,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // downsweep: big levels lbig .. p one launch each
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch("hss_down_pair", s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    st = launch(HM_NT_NAME("hss_down_pair"), s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
   return HM_OK;

@@ -3,15 +3,15 @@
 Same bar as the forward product (BASELINE.json north_star): ||Y_gpu - Y_ref||_F /
 ||Y_ref||_F <= 1e-12 in fp64, on the same seeded inputs; small cases through the
 full oracle (every shape family of test_gpu_parity: GEMV, DMMA and generic
-paths, ragged column chunks, k = 0, p = 0), full-size configs 3-5 on sampled
-leaves / the closed form.
+paths, ragged column chunks, k = 0, p = 0), config 5 at full size against the
+closed form (configs 3 and 4 in full: test_gpu_fullsize.py).
 """
 import numpy as np
 import pytest
 
 import hm_inputs
 import oracle
-from test_gpu_parity import HODLR_CASES, HSS_CASES, TOL, dev, relerr, sample_leaves, tridiag_residual
+from test_gpu_parity import HODLR_CASES, HSS_CASES, TOL, dev, relerr, tridiag_residual
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -101,38 +101,6 @@ def test_adjoint_inner_product_and_determinism(hm):
 
 
 # ------------------------------------------------- full-size configs --
-
-@pytest.fixture(scope="module")
-def config3():
-    cfg = hm_inputs.CONFIGS[3]
-    return cfg, hm_inputs.hodlr_random(cfg.n, cfg.levels, [cfg.k] * cfg.levels, cid=3)
-
-
-@pytest.mark.parametrize("m", [1, 8, 64])
-def test_config3_adjoint_sampled(hm, config3, m):
-    cfg, h = config3
-    X = hm_inputs.rhs(cfg.n, m, cid=3)
-    Y = gpu_hodlr_t(hm, h, X)
-    b = cfg.leaf
-    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(100 + m))
-    Dsel = np.concatenate([h.D[L * b * b:(L + 1) * b * b] for L in leaves])
-    Yr = oracle.hodlr_matvec_t_leaves(cfg.n, cfg.levels, h.ranks, Dsel, h.U, h.V, X, leaves)
-    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
-    assert relerr(Yg, Yr) <= TOL and np.isfinite(Y).all()
-
-
-def test_config4_adjoint_sampled(hm):
-    cfg = hm_inputs.CONFIGS[4]
-    s = hm_inputs.hss_random(cfg.n, cfg.levels, cfg.k, cid=4)
-    X = hm_inputs.rhs(cfg.n, 32, cid=4)
-    Y = gpu_hss_t(hm, s, X)
-    b = cfg.leaf
-    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(104))
-    Dsel = np.concatenate([s.D[L * b * b:(L + 1) * b * b] for L in leaves])
-    Yr = oracle.hss_matvec_t_leaves(cfg.n, cfg.levels, cfg.k, Dsel, s.U, s.V, s.R, s.W, s.B, X, leaves)
-    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
-    assert relerr(Yg, Yr) <= TOL and np.isfinite(Y).all()
-
 
 def test_config5_adjoint_closed_form(hm):
     """The inverse Laplacian is symmetric: A^T X is the closed form, at n = 2^24."""

@@ -2,9 +2,10 @@
 
 Tolerance (BASELINE.json north_star): ||Y_gpu - Y_ref||_F / ||Y_ref||_F <= 1e-12 in fp64.
 Inputs: seeded, from hm_inputs; the same bytes feed both sides.
-Small cases run the full oracle; full-size configs (BASELINE configs 3-5, the
-launch configuration bench.py times) are checked on sampled leaves the oracle
-computes one by one, and via closed forms that hold at any size.
+Small cases run the full oracle; configs 3 and 4 at full size are compared with
+the full oracle on every row in test_gpu_fullsize.py; config 5 (n = 2^24) here on
+every row against the closed-form oracle, plus sampled leaves through the HODLR
+oracle, and closed forms that hold at any size.
 """
 import numpy as np
 import pytest
@@ -220,60 +221,6 @@ def sample_leaves(nl, rng, extra=4):
     base = {0, 1, nl // 2 - 1, nl // 2, nl - 1}
     base |= set(int(v) for v in rng.integers(0, nl, size=extra))
     return sorted(base)
-
-
-@pytest.fixture(scope="module")
-def config3():
-    cfg = hm_inputs.CONFIGS[3]
-    h = hm_inputs.hodlr_random(cfg.n, cfg.levels, [cfg.k] * cfg.levels, cid=3)
-    return cfg, h
-
-
-@pytest.mark.parametrize("m", [1, 8, 64])
-def test_config3_full_size_sampled(hm, config3, m):
-    cfg, h = config3
-    X = hm_inputs.rhs(cfg.n, m, cid=3)
-    Y = gpu_hodlr(hm, h, X)
-    b = cfg.leaf
-    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(m))
-    Dsel = np.concatenate([h.D[L * b * b:(L + 1) * b * b] for L in leaves])
-    Yr = oracle.hodlr_matvec_leaves(cfg.n, cfg.levels, h.ranks, Dsel, h.U, h.V, X, leaves)
-    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
-    assert relerr(Yg, Yr) <= TOL
-    assert np.isfinite(Y).all()
-
-
-@pytest.mark.parametrize("ranks_of,m", [(lambda l: 16 if l % 2 else 8, 8), (lambda l: 16 >> (l % 4), 1),
-                                         (lambda l: 32 if l % 2 else 16, 64)])
-def test_config3_tree_per_level_ranks_sampled(hm, ranks_of, m):
-    """Per-level ranks on the full config-3 tree, the bench sweep's sets:
-    one V^T X pass per distinct rank + one leaf pass, sampled leaves vs the oracle."""
-    cfg = hm_inputs.CONFIGS[3]
-    ranks = [ranks_of(l) for l in range(cfg.levels)]
-    h = hm_inputs.hodlr_random(cfg.n, cfg.levels, ranks, cid=6)
-    X = hm_inputs.rhs(cfg.n, m, cid=6)
-    Y = gpu_hodlr(hm, h, X)
-    b = cfg.leaf
-    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(60 + m))
-    Dsel = np.concatenate([h.D[L * b * b:(L + 1) * b * b] for L in leaves])
-    Yr = oracle.hodlr_matvec_leaves(cfg.n, cfg.levels, h.ranks, Dsel, h.U, h.V, X, leaves)
-    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
-    assert relerr(Yg, Yr) <= TOL
-    assert np.isfinite(Y).all()
-
-
-def test_config4_full_size_sampled(hm):
-    cfg = hm_inputs.CONFIGS[4]
-    s = hm_inputs.hss_random(cfg.n, cfg.levels, cfg.k, cid=4)
-    X = hm_inputs.rhs(cfg.n, 32, cid=4)
-    Y = gpu_hss(hm, s, X)
-    b = cfg.leaf
-    leaves = sample_leaves(cfg.nleaves, np.random.default_rng(4))
-    Dsel = np.concatenate([s.D[L * b * b:(L + 1) * b * b] for L in leaves])
-    Yr = oracle.hss_matvec_leaves(cfg.n, cfg.levels, cfg.k, Dsel, s.U, s.V, s.R, s.W, s.B, X, leaves)
-    Yg = np.concatenate([Y[L * b:(L + 1) * b] for L in leaves])
-    assert relerr(Yg, Yr) <= TOL
-    assert np.isfinite(Y).all()
 
 
 def test_config5_full_size(hm):

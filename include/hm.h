@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HM_ABI_VERSION 1
+#define HM_ABI_VERSION 2
 
 typedef enum {
   HM_OK = 0,
@@ -51,7 +51,7 @@ typedef enum {
   HM_ERR_UNSUPPORTED = -2, /* valid per the paper but not built (see each call)    */
   HM_ERR_WORKSPACE = -3,   /* workspace NULL or smaller than the query returned    */
   HM_ERR_CUDA = -4,        /* a CUDA launch / copy failed                          */
-  HM_ERR_NCCL = -5         /* reserved for the multi-GPU calls                     */
+  HM_ERR_NCCL = -5         /* NCCL missing or failed (multi-GPU calls)             */
 } hm_status;
 
 /* Cluster tree (Def. 2.1). This build supports the balanced tree of
@@ -250,25 +250,79 @@ hm_status hss_to_hodlr(const hm_tree* tree, int32_t k,
  *   HODLR  D_local [2^(p-q)][b][b]; U_local, V_local level-major over ALL p
  *          levels with n/P rows each: level l at offset (n/P) sum_{l'<l} k_l',
  *          [n/P][k_l] = rows I_r of the global U_l, V_l. X_local, Y_local
- *          [n/P][nrhs] = rows I_r.
+ *          [n/P][nrhs] = rows I_r. One rank (uniform) for all levels.
  *   HSS    D_local, U_local, V_local [n/P][k] likewise; the subtree's W_sub,
  *          R_sub [2^(p-q)-2][2k][k] and B_sub [2^(p-q)-1][2][k][k] in heap
  *          order relative to node (q, r) (B_sub[0] = the cores of node (q,r));
  *          W_root, R_root [2k][k] = the translations of node (q, r) itself;
  *          W_top, R_top [2^q-2][2k][k] and B_top [2^q-1][2][k][k] = the global
  *          arrays' prefixes (levels < q), replicated on every rank.
- * The ONLY exchange is an allgather of `send_doubles` doubles per rank into
- * `gathered` [P][send_doubles] (rank order), done by the caller (NCCL through
- * torch.distributed in the binding) between _begin and _end:
- *   HODLR  send = this rank's partial t_l = V_l(I_r)^T X(I_r) for l = 1..q;
- *          _end sums, for each top level, the partials of the ranks under the
- *          sibling of its ancestor, in rank order, and adds U_l(I_r) t_l.
- *          _local (V^T X of the subtree levels) may run while the allgather
- *          is in flight.
- *   HSS    send = x of node (q, r) (Step 1 up to the subtree root); _end runs
- *          the replicated top tree (levels 1..q) and then the subtree's
- *          coupling/downsweep from y of node (q, r), and the leaves.
- * Results equal the single-GPU product up to the order of the top-level sums. */
+ * The ONLY exchange is an allgather of small coefficient blocks per product:
+ *   HODLR  rank r's partial t_l = V_l(I_r)^T X(I_r) for the top levels
+ *          l = 1..q (q k nrhs doubles; config 5 at P = 8: 24 bytes). Each rank
+ *          then sums, per top level, the partials of the ranks under the
+ *          sibling of its ancestor (rank order) and adds U_l(I_r) t_l.
+ *   HSS    x of node (q, r) (Step 1 up to the subtree root, k nrhs doubles);
+ *          every rank runs the replicated top tree (levels 1..q), then its
+ *          subtree's coupling / downsweep from y of node (q, r), and Step 4.
+ * Results equal the single-GPU product up to the order of the top-level sums
+ * (HSS: bitwise, the top tree runs the same kernels on the same blocks). */
+
+/* ---- communicator: NCCL (loaded at run time from libnccl.so.2), one per
+ * process, bound to the CUDA device current at hm_comm_init. Its allgather runs
+ * on the communicator's own stream, ordered against the caller's stream with
+ * events. Not thread-safe: one product at a time per communicator, issued in
+ * the same order on every rank. */
+typedef struct hm_comm_s hm_comm;
+#define HM_COMM_ID_BYTES 128
+
+/* Rank 0 creates the id and hands it to the other ranks out of band (the
+ * Python binding broadcasts it through torch.distributed; examples/ uses a
+ * pipe). HM_ERR_NCCL if NCCL cannot be loaded or fails. */
+hm_status hm_comm_unique_id(void* id_out /* HM_COMM_ID_BYTES bytes */);
+/* Collective over the nranks processes (blocks until all joined). nranks must
+ * be a power of two (HM_ERR_UNSUPPORTED otherwise); the current CUDA device
+ * must differ between the ranks (NCCL). *comm_out = NULL on failure. */
+hm_status hm_comm_init(int32_t nranks, int32_t rank, const void* id, hm_comm** comm_out);
+/* Waits for the communicator's stream, then frees it. NULL is a no-op. */
+hm_status hm_comm_destroy(hm_comm* comm);
+hm_status hm_comm_size(const hm_comm* comm, int32_t* nranks, int32_t* rank);
+/* recv[P][count] <- every rank's send[count], rank order (the exchange
+ * primitive of the products below), ordered after the work already on
+ * `stream`; work enqueued on `stream` afterwards sees recv complete. In place
+ * when send == recv + rank * count. */
+hm_status hm_comm_allgather(hm_comm* comm, const double* send, int64_t count, double* recv, void* stream);
+
+/* ---- the products, one call each (every rank calls with its local arrays).
+ * The current device must be the communicator's. Per-level HODLR ranks are
+ * not supported here (HM_ERR_UNSUPPORTED). Workspace: the query below (the
+ * same on every rank). HM_ERR_NCCL if the exchange fails.
+ * HODLR: the allgather runs while this rank computes its subtree's V^T X and
+ * — when the extra Y read + write costs at most 3% of the bytes — its leaf
+ * pass; the top-level terms are then added.
+ * HSS: nothing local is independent of y of node (q, r) after Step 1, so the
+ * allgather (k nrhs doubles per rank) is not overlapped. */
+hm_status hm_hodlr_dist_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t nranks,
+                                        size_t* bytes);
+hm_status hodlr_matvec_dist(hm_comm* comm, const hm_tree* tree, const int32_t* ranks, const double* D_local,
+                            const double* U_local, const double* V_local, const double* X_local, int32_t nrhs,
+                            double* Y_local, void* workspace, size_t workspace_bytes, void* stream);
+hm_status hm_hss_dist_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t nranks, size_t* bytes);
+hm_status hss_matvec_dist(hm_comm* comm, const hm_tree* tree, int32_t k, const double* D_local,
+                          const double* U_local, const double* V_local, const double* R_sub, const double* W_sub,
+                          const double* B_sub, const double* R_root, const double* W_root, const double* R_top,
+                          const double* W_top, const double* B_top, const double* X_local, int32_t nrhs,
+                          double* Y_local, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- split-phase interface: the same products with the exchange done by the
+ * caller (any transport; the tests use it to run every rank's kernels on one
+ * GPU with the allgather replaced by a concatenation). The caller allgathers
+ * `send_doubles` doubles per rank from `send` into `gathered` [P][send_doubles]
+ * (rank order) between _begin and _end:
+ *   HODLR  _begin (top partials into send); _local (the subtree's V^T X and,
+ *          when hodlr_matvec_dist would overlap it, the leaf pass without the
+ *          top levels — may run while the allgather is in flight); _end.
+ *   HSS    _begin (send = x of node (q, r)); _end. */
 typedef struct {
   int32_t nranks; /* P, a power of two <= 2^levels */
   int32_t rank;   /* 0 <= rank < P                  */
@@ -280,8 +334,9 @@ hm_status hodlr_matvec_dist_begin(const hm_tree* tree, const int32_t* ranks, con
                                   const double* V_local, const double* X_local, int32_t nrhs, double* send,
                                   void* workspace, size_t workspace_bytes, void* stream);
 hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
-                                  const double* V_local, const double* X_local, int32_t nrhs,
-                                  void* workspace, size_t workspace_bytes, void* stream);
+                                  const double* D_local, const double* U_local, const double* V_local,
+                                  const double* X_local, int32_t nrhs, double* Y_local, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
                                 const double* D_local, const double* U_local, const double* X_local, int32_t nrhs,
                                 const double* gathered, double* Y_local, void* workspace, size_t workspace_bytes,

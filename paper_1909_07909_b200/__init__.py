@@ -34,7 +34,9 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hodlr_matvec_t", "hss_matvec_t",
            "hm_hodlr_norm2_workspace_bytes", "hodlr_norm2_est", "hm_hss_norm2_workspace_bytes", "hss_norm2_est",
            "hss_to_hodlr", "hm_hodlr_general_workspace_bytes", "hodlr_matvec_general",
-           "hm_hss_general_workspace_bytes", "hss_matvec_general")
+           "hm_hss_general_workspace_bytes", "hss_matvec_general",
+           "hm_comm_unique_id", "hm_comm_init", "hm_comm_destroy", "hm_comm_size", "hm_comm_allgather",
+           "hm_hodlr_dist_workspace_bytes", "hodlr_matvec_dist", "hm_hss_dist_workspace_bytes", "hss_matvec_dist")
 
 
 class HmError(RuntimeError):

@@ -204,14 +204,14 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
 // for top levels the coefficient block is the same for every leaf (ttop).
 hm_status hodlr_leaf_phase(const HodlrPlan& P, const int32_t* ranks, const double* D, const double* U,
                            const double* Xd, double* Yd, char* w, const double* ttop, cudaStream_t stream,
-                           bool dtrans = false) {
+                           bool dtrans = false, bool skip_top = false) {
   hm::LeafParams lp;
   memset(&lp, 0, sizeof lp);
   lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf; lp.dtrans = dtrans ? 1 : 0;
   int64_t uoff = 0, toff = 0;
   for (int l = 1; l <= P.q + P.p; ++l) {
     const int k = ranks[l - 1];
-    if (k > 0) {
+    if (k > 0 && !(skip_top && l <= P.q)) {
       hm::LeafSeg& sg = lp.seg[lp.nseg++];
       sg.A = U + uoff;
       sg.k = k;
@@ -298,6 +298,77 @@ bool hodlr_use_general(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, 
   const bool fast = hodlr_plan(tree, ranks, nrhs, flags, &P) == HM_OK;
   g_err = saved;
   return !fast;
+}
+
+
+// ---- distributed HODLR: the exchange's consumers ----
+
+// t_l for the q top levels from the gathered per-rank partials: the sum, in
+// rank order, over the ranks under the sibling of this rank's level-l ancestor.
+hm_status hodlr_dist_combine(const HodlrPlan& P, const DistPart& d, const int32_t* ranks, const double* gathered,
+                             double* ttop, cudaStream_t s) {
+  if (P.top_doubles <= 0) return HM_OK;
+  hm::CombineParams cp;
+  memset(&cp, 0, sizeof cp);
+  cp.gathered = gathered; cp.out = ttop; cp.per_rank = P.top_doubles; cp.q = d.q; cp.rank = d.rank;
+  int64_t off = 0;
+  for (int l = 1; l <= d.q; ++l) {
+    cp.lev_off[l] = off;
+    off += (int64_t)ranks[l - 1] * P.m;
+  }
+  cp.lev_off[d.q + 1] = off;
+  const unsigned grid = (unsigned)((P.top_doubles + hm::kThreads - 1) / hm::kThreads);
+  return launch("dist_combine", s, [&] { hm::dist_combine_kernel<<<grid, hm::kThreads, 0, s>>>(cp); });
+}
+
+// Y(I_r) += sum_{l <= q} U_l(I_r) t_l after a leaf pass that left the top levels out.
+hm_status hodlr_top_epilogue(const HodlrPlan& P, const int32_t* ranks, const double* U, const double* ttop,
+                             double* Y, cudaStream_t s) {
+  hm::TopEpilogueParams ep;
+  memset(&ep, 0, sizeof ep);
+  ep.Y = Y; ep.U = U; ep.T = ttop; ep.n = P.n; ep.m = P.m;
+  int64_t uoff = 0;
+  for (int l = 1; l <= P.q; ++l) {
+    const int k = ranks[l - 1];
+    if (k > 0) {
+      ep.k[ep.nlev] = k;
+      ep.uoff[ep.nlev] = uoff;
+      ++ep.nlev;
+      ep.ktot += k;
+    }
+    uoff += P.n * k;
+  }
+  if (ep.nlev == 0) return HM_OK;
+  const size_t smem = sizeof(double) * (size_t)ep.ktot * P.m;
+  const unsigned grid = (unsigned)((P.n * P.m + hm::kThreads - 1) / hm::kThreads);
+  return launch("dist_top_epilogue", s,
+                [&] { hm::dist_top_epilogue_kernel<<<grid, hm::kThreads, smem, s>>>(ep); });
+}
+
+// The one-call product overlaps the allgather with the subtree's V^T X and the
+// leaf pass, then adds the top-level terms in an epilogue — when the epilogue's
+// extra Y read + write (16 m bytes per row) is at most 3% of the algorithmic
+// bytes per row, 8 (b + 2 sum_l k_l + 2 m) (config 5: 0.7%). Otherwise the
+// top-level terms stay in the leaf pass, which then waits for the exchange
+// (it still overlaps the subtree's V^T X).
+bool hodlr_dist_overlap_leaf(const HodlrPlan& P) {
+  const double per_row = 8.0 * ((double)P.b + 2.0 * (double)P.ktot + 2.0 * P.m);
+  return P.top_doubles > 0 && 16.0 * P.m <= 0.03 * per_row && P.top_doubles * 8 <= 48 * 1024;
+}
+
+struct HodlrDistWs {
+  size_t off_send, off_gath, total;
+};
+
+HodlrDistWs hodlr_dist_ws(const HodlrPlan& P, int32_t nranks) {
+  HodlrDistWs W;
+  size_t off = align_up(P.total);
+  W.off_send = off;
+  off = align_up(off + sizeof(double) * (size_t)P.top_doubles);
+  W.off_gath = off;
+  off = align_up(off + sizeof(double) * (size_t)P.top_doubles * (size_t)nranks);
+  W.total = off;
+  return W;
 }
 
 }  // namespace hmi
@@ -411,7 +482,8 @@ hm_status hodlr_matvec_dist_begin(const hm_tree* tree, const int32_t* ranks, con
 }
 
 hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
-                                  const double* V_local, const double* X_local, int32_t nrhs, void* workspace,
+                                  const double* D_local, const double* U_local, const double* V_local,
+                                  const double* X_local, int32_t nrhs, double* Y_local, void* workspace,
                                   size_t workspace_bytes, void* stream) {
   HodlrPlan P;
   DistPart d;
@@ -419,10 +491,20 @@ hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, con
   if (st) return st;
   if (!workspace || workspace_bytes < P.total) return fail(HM_ERR_WORKSPACE, "workspace too small");
   if (!X_local || (P.k > 0 && !V_local)) return fail(HM_ERR_INVALID_ARG, "NULL V / X pointer");
+  const bool leaf_now = hodlr_dist_overlap_leaf(P);
+  if (leaf_now) {
+    if (!D_local || !aligned16(D_local)) return fail(HM_ERR_INVALID_ARG, "D_local NULL or misaligned");
+    if ((st = hodlr_check_ptrs(P, D_local, U_local, V_local, X_local, Y_local, workspace, workspace_bytes, 0)))
+      return st;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
   g_launches = 0;
   prof_new_call();
-  return hodlr_vt_phase(P, ranks, V_local, X_local, static_cast<char*>(workspace), P.q + 1, P.q + P.p, nullptr,
-                        static_cast<cudaStream_t>(stream));
+  if ((st = hodlr_vt_phase(P, ranks, V_local, X_local, w, P.q + 1, P.q + P.p, nullptr, s))) return st;
+  if (leaf_now)  // the leaf pass without the top levels, ahead of the exchange's result
+    return hodlr_leaf_phase(P, ranks, D_local, U_local, X_local, Y_local, w, nullptr, s, false, true);
+  return HM_OK;
 }
 
 hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
@@ -442,20 +524,62 @@ hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const
   double* ttop = reinterpret_cast<double*>(w + P.off_ttop);
   g_launches = 0;
   prof_new_call();
-  if (P.top_doubles > 0) {
-    hm::CombineParams cp;
-    memset(&cp, 0, sizeof cp);
-    cp.gathered = gathered; cp.out = ttop; cp.per_rank = P.top_doubles; cp.q = d.q; cp.rank = d.rank;
-    int64_t off = 0;
-    for (int l = 1; l <= d.q; ++l) {
-      cp.lev_off[l] = off;
-      off += (int64_t)ranks[l - 1] * nrhs;
-    }
-    cp.lev_off[d.q + 1] = off;
-    const unsigned grid = (unsigned)((P.top_doubles + hm::kThreads - 1) / hm::kThreads);
-    st = launch("dist_combine", s, [&] { hm::dist_combine_kernel<<<grid, hm::kThreads, 0, s>>>(cp); });
-    if (st) return st;
+  if ((st = hodlr_dist_combine(P, d, ranks, gathered, ttop, s))) return st;
+  if (hodlr_dist_overlap_leaf(P)) return hodlr_top_epilogue(P, ranks, U_local, ttop, Y_local, s);
+  return hodlr_leaf_phase(P, ranks, D_local, U_local, X_local, Y_local, w, ttop, s);
+}
+
+// One call, NCCL inside: rank r's partial V_l(I_r)^T X(I_r) for
+// the q top levels, their allgather on the communicator's stream while the
+// subtree's V^T X and (hodlr_dist_overlap_leaf) the leaf pass run, then the
+// combine and the top-level terms.
+hm_status hm_hodlr_dist_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, int32_t nranks,
+                                        size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  const hm_part part{nranks, 0};
+  HodlrPlan P;
+  DistPart d;
+  hm_status st = hodlr_dist_plan(tree, ranks, nrhs, &part, 0, &P, &d);
+  if (st) return st;
+  *bytes = hodlr_dist_ws(P, nranks).total;
+  return HM_OK;
+}
+
+hm_status hodlr_matvec_dist(hm_comm* comm, const hm_tree* tree, const int32_t* ranks, const double* D_local,
+                            const double* U_local, const double* V_local, const double* X_local, int32_t nrhs,
+                            double* Y_local, void* workspace, size_t workspace_bytes, void* stream) {
+  int32_t nranks = 0, rank = 0;
+  hm_status st = comm_check(comm, &nranks, &rank);
+  if (st) return st;
+  const hm_part part{nranks, rank};
+  HodlrPlan P;
+  DistPart d;
+  if ((st = hodlr_dist_plan(tree, ranks, nrhs, &part, 0, &P, &d))) return st;
+  const HodlrDistWs W = hodlr_dist_ws(P, nranks);
+  if (!D_local || !aligned16(D_local)) return fail(HM_ERR_INVALID_ARG, "D_local NULL or misaligned");
+  if ((st = hodlr_check_ptrs(P, D_local, U_local, V_local, X_local, Y_local, workspace, workspace_bytes, 0)))
+    return st;
+  if (workspace_bytes < W.total)
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, W.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  double* send = reinterpret_cast<double*>(w + W.off_send);
+  double* gathered = reinterpret_cast<double*>(w + W.off_gath);
+  double* ttop = reinterpret_cast<double*>(w + P.off_ttop);
+  const int64_t top = P.top_doubles;
+  g_launches = 0;
+  prof_new_call();
+  if ((st = hodlr_vt_phase(P, ranks, V_local, X_local, w, 1, P.q, send, s))) return st;
+  if ((st = comm_allgather_start(comm, send, top, gathered, s))) return st;
+  if ((st = hodlr_vt_phase(P, ranks, V_local, X_local, w, P.q + 1, P.q + P.p, nullptr, s))) return st;
+  if (hodlr_dist_overlap_leaf(P)) {
+    if ((st = hodlr_leaf_phase(P, ranks, D_local, U_local, X_local, Y_local, w, nullptr, s, false, true))) return st;
+    if ((st = comm_allgather_wait(comm, top, s))) return st;
+    if ((st = hodlr_dist_combine(P, d, ranks, gathered, ttop, s))) return st;
+    return hodlr_top_epilogue(P, ranks, U_local, ttop, Y_local, s);
   }
+  if ((st = comm_allgather_wait(comm, top, s))) return st;
+  if ((st = hodlr_dist_combine(P, d, ranks, gathered, ttop, s))) return st;
   return hodlr_leaf_phase(P, ranks, D_local, U_local, X_local, Y_local, w, ttop, s);
 }
 

@@ -473,6 +473,71 @@ hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_p
   if ((st = check_part(tree, part, d))) return st;
   return hss_plan_ex(tree->n >> d->q, tree->leaf, tree->levels - d->q, d->q, k, nrhs, flags, P);
 }
+
+// ---- distributed HSS: phase bodies ----
+
+hm_status hss_dist_begin_body(const HssPlan& P, const DistPart& d, const double* V_local, const double* W_sub,
+                              const double* W_root, const double* X_local, double* send, char* w,
+                              cudaStream_t s) {
+  if (P.k == 0) return HM_OK;  // block diagonal: nothing to exchange, no tree
+  double* xh = reinterpret_cast<double*>(w + P.off_xh);
+  if (d.q == 0) {
+    // one rank: the whole tree is local and the exchange is empty; Step 1 and
+    // the upsweep to level 1 run here (as in hss_matvec), _end does the rest
+    if (P.p == 0) return HM_OK;
+    if (!X_local || !V_local || (P.p >= 2 && !W_sub)) return fail(HM_ERR_INVALID_ARG, "NULL V / W / X pointer");
+    return hss_up_phase(P, V_local, W_sub, X_local, xh, nullptr, nullptr, s);
+  }
+  if (!X_local || !V_local || !send || (P.p >= 2 && !W_sub) || (P.p >= 1 && !W_root))
+    return fail(HM_ERR_INVALID_ARG, "NULL V / W / X / send pointer");
+  return hss_up_phase(P, V_local, W_sub, X_local, xh, W_root, send, s);
+}
+
+// gathered: the P level-q x blocks in rank order; if it already is the top
+// tree's level-q coefficient array (the one-call path), no copy is made.
+hm_status hss_dist_end_body(const HssPlan& P, const DistPart& d, const double* D_local, const double* U_local,
+                            const double* R_sub, const double* B_sub, const double* R_root, const double* W_top,
+                            const double* R_top, const double* B_top, const double* X_local,
+                            const double* gathered, double* Y_local, char* w, cudaStream_t s) {
+  const int k = P.k;
+  if (!D_local || !X_local || !Y_local || !aligned16(D_local))
+    return fail(HM_ERR_INVALID_ARG, "NULL or misaligned D / X / Y pointer");
+  double* xh = reinterpret_cast<double*>(w + P.off_xh);
+  double* yh = reinterpret_cast<double*>(w + P.off_yh);
+  double* txh = reinterpret_cast<double*>(w + P.off_txh);
+  double* tyh = reinterpret_cast<double*>(w + P.off_tyh);
+  const int64_t km = (int64_t)k * P.m;
+  hm_status st;
+  const double* yleaf = nullptr;
+  if (k > 0 && d.q == 0 && P.p >= 1) {
+    // one rank: coupling + downsweep of the whole (local) tree on the x blocks
+    // _begin left in the workspace, then the leaves (as in hss_matvec)
+    if (!U_local || !B_sub || (P.p >= 2 && !R_sub)) return fail(HM_ERR_INVALID_ARG, "NULL U / R / B pointer");
+    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s))) return st;
+    yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+  }
+  if (k > 0 && d.q > 0) {
+    if (!gathered || !U_local || !B_top || (d.q >= 2 && (!W_top || !R_top)) || (P.p >= 1 && (!R_root || !B_sub)) ||
+        (P.p >= 2 && !R_sub))
+      return fail(HM_ERR_INVALID_ARG, "NULL gathered / generator pointer");
+    // replicated top tree: x of level q from the allgather, up q-1..1, down 1..q
+    double* tq = txh + (((int64_t)1 << d.q) - 2) * km;
+    if (gathered != tq && cudaMemcpyAsync(tq, gathered, sizeof(double) * (size_t)(d.P * km),
+                                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return cuda_check("copy of the gathered blocks");
+    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s))) return st;
+    const double* y_root = tyh + (((int64_t)1 << d.q) - 2 + d.rank) * km;
+    if (P.p >= 1) {
+      // the subtree's x blocks were left in this workspace by _begin
+      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s))) return st;
+      yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
+    } else {
+      yleaf = y_root;
+    }
+  }
+  return hss_leaf_phase(P, D_local, U_local, X_local, Y_local, yleaf, s);
+}
+
 }  // namespace hmi
 
 using namespace hmi;
@@ -555,18 +620,8 @@ hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* p
     return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
   g_launches = 0;
   prof_new_call();
-  if (k == 0) return HM_OK;  // block diagonal: nothing to exchange, no tree
-  double* xh = reinterpret_cast<double*>(static_cast<char*>(workspace) + P.off_xh);
-  if (d.q == 0) {
-    // one rank: the whole tree is local and the exchange is empty; Step 1 and
-    // the upsweep to level 1 run here (as in hss_matvec), _end does the rest
-    if (P.p == 0) return HM_OK;
-    if (!X_local || !V_local || (P.p >= 2 && !W_sub)) return fail(HM_ERR_INVALID_ARG, "NULL V / W / X pointer");
-    return hss_up_phase(P, V_local, W_sub, X_local, xh, nullptr, nullptr, static_cast<cudaStream_t>(stream));
-  }
-  if (!X_local || !V_local || !send || (P.p >= 2 && !W_sub) || (P.p >= 1 && !W_root))
-    return fail(HM_ERR_INVALID_ARG, "NULL V / W / X / send pointer");
-  return hss_up_phase(P, V_local, W_sub, X_local, xh, W_root, send, static_cast<cudaStream_t>(stream));
+  return hss_dist_begin_body(P, d, V_local, W_sub, W_root, X_local, send, static_cast<char*>(workspace),
+                             static_cast<cudaStream_t>(stream));
 }
 
 hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* part, const double* D_local,
@@ -578,46 +633,63 @@ hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* par
   DistPart d;
   hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
   if (st) return st;
-  if (!D_local || !X_local || !Y_local || !aligned16(D_local))
-    return fail(HM_ERR_INVALID_ARG, "NULL or misaligned D / X / Y pointer");
   if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
     return fail(HM_ERR_WORKSPACE, "workspace too small or misaligned");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  char* w = static_cast<char*>(workspace);
-  double* xh = reinterpret_cast<double*>(w + P.off_xh);
-  double* yh = reinterpret_cast<double*>(w + P.off_yh);
-  double* txh = reinterpret_cast<double*>(w + P.off_txh);
-  double* tyh = reinterpret_cast<double*>(w + P.off_tyh);
-  const int64_t km = (int64_t)k * nrhs;
   g_launches = 0;
   prof_new_call();
-  const double* yleaf = nullptr;
-  if (k > 0 && d.q == 0 && P.p >= 1) {
-    // one rank: coupling + downsweep of the whole (local) tree on the x blocks
-    // _begin left in the workspace, then the leaves (as in hss_matvec)
-    if (!U_local || !B_sub || (P.p >= 2 && !R_sub)) return fail(HM_ERR_INVALID_ARG, "NULL U / R / B pointer");
-    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s))) return st;
-    yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
-  }
-  if (k > 0 && d.q > 0) {
-    if (!gathered || !U_local || !B_top || (d.q >= 2 && (!W_top || !R_top)) || (P.p >= 1 && (!R_root || !B_sub)) ||
-        (P.p >= 2 && !R_sub))
-      return fail(HM_ERR_INVALID_ARG, "NULL gathered / generator pointer");
-    // replicated top tree: x of level q from the allgather, up q-1..1, down 1..q
-    if (cudaMemcpyAsync(txh + (((int64_t)1 << d.q) - 2) * km, gathered, sizeof(double) * (size_t)(d.P * km),
-                        cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return cuda_check("copy of the gathered blocks");
-    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s))) return st;
-    const double* y_root = tyh + (((int64_t)1 << d.q) - 2 + d.rank) * km;
-    if (P.p >= 1) {
-      // the subtree's x blocks were left in this workspace by _begin
-      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s))) return st;
-      yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
-    } else {
-      yleaf = y_root;
-    }
-  }
-  return hss_leaf_phase(P, D_local, U_local, X_local, Y_local, yleaf, s);
+  return hss_dist_end_body(P, d, D_local, U_local, R_sub, B_sub, R_root, W_top, R_top, B_top, X_local, gathered,
+                           Y_local, static_cast<char*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+// One call, NCCL inside: Step 1 + the subtree upsweep to x of
+// node (q, r); the allgather of the P level-q blocks straight into the
+// replicated top tree's workspace; the top tree (levels 1..q, every rank
+// redundantly), the subtree's coupling + downsweep from y of (q, r), Step 4.
+// The exchange is not overlapped: everything after it depends on y of (q, r)
+// (DESIGN.md §7 gives the measured cost and why no independent work remains).
+hm_status hm_hss_dist_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t nranks, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  const hm_part part{nranks, 0};
+  HssPlan P;
+  DistPart d;
+  hm_status st = hss_dist_plan(tree, k, nrhs, &part, 0, &P, &d);
+  if (st) return st;
+  *bytes = P.total;
+  return HM_OK;
+}
+
+hm_status hss_matvec_dist(hm_comm* comm, const hm_tree* tree, int32_t k, const double* D_local,
+                          const double* U_local, const double* V_local, const double* R_sub, const double* W_sub,
+                          const double* B_sub, const double* R_root, const double* W_root, const double* R_top,
+                          const double* W_top, const double* B_top, const double* X_local, int32_t nrhs,
+                          double* Y_local, void* workspace, size_t workspace_bytes, void* stream) {
+  int32_t nranks = 0, rank = 0;
+  hm_status st = comm_check(comm, &nranks, &rank);
+  if (st) return st;
+  const hm_part part{nranks, rank};
+  HssPlan P;
+  DistPart d;
+  if ((st = hss_dist_plan(tree, k, nrhs, &part, 0, &P, &d))) return st;
+  if (!workspace || workspace_bytes < P.total || !aligned16(workspace))
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu (or misaligned)", workspace_bytes, P.total);
+  if (X_local && Y_local && overlap(X_local, sizeof(double) * (size_t)(P.n * nrhs), Y_local,
+                                    sizeof(double) * (size_t)(P.n * nrhs)))
+    return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(workspace);
+  const int64_t km = (int64_t)k * nrhs;
+  const int64_t send_doubles = (d.q > 0) ? km : 0;
+  // rank r's block goes to its own slot of the level-q coefficient array of
+  // the top tree; the allgather then fills every slot in place
+  double* tq = reinterpret_cast<double*>(w + P.off_txh) + (((int64_t)1 << d.q) - 2) * km;
+  double* send = send_doubles > 0 ? tq + d.rank * km : nullptr;
+  g_launches = 0;
+  prof_new_call();
+  if ((st = hss_dist_begin_body(P, d, V_local, W_sub, W_root, X_local, send, w, s))) return st;
+  if ((st = comm_allgather_start(comm, send, send_doubles, tq, s))) return st;
+  if ((st = comm_allgather_wait(comm, send_doubles, s))) return st;
+  return hss_dist_end_body(P, d, D_local, U_local, R_sub, B_sub, R_root, W_top, R_top, B_top, X_local,
+                           send_doubles > 0 ? tq : nullptr, Y_local, w, s);
 }
 
 }  // extern "C"

@@ -206,6 +206,14 @@ hm_status hodlr_gen_run(int64_t n, int32_t p, const int64_t* c, const int32_t* r
                         const double* U, const double* V, const double* X, int32_t nrhs, double* Y, void* ws,
                         size_t ws_bytes, cudaStream_t s);
 
+// ------------------------------------------------------------- hm_comm.cu --
+// The exchange of the distributed product: comm_allgather_start enqueues the
+// allgather on the communicator's stream after the work already on s;
+// comm_allgather_wait makes s wait for it (s may run other work in between).
+hm_status comm_check(const hm_comm* c, int32_t* nranks, int32_t* rank);
+hm_status comm_allgather_start(hm_comm* c, const double* send, int64_t count, double* recv, cudaStream_t s);
+hm_status comm_allgather_wait(hm_comm* c, int64_t count, cudaStream_t s);
+
 // ------------------------------------------------------------- hm_norm.cu --
 // Power method on A A^* (SURVEY §8(f) f2). apply(op, x, y): y = A x
 // (op 0) or A^T x (op 1) with nrhs = 1, enqueued on s.

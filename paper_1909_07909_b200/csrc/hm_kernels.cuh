@@ -208,6 +208,39 @@ static __global__ void __launch_bounds__(kThreads) dist_combine_kernel(const Com
   C.out[e] = s;
 }
 
+// Distributed HODLR with the exchange overlapped (hodlr_matvec_dist): the leaf
+// pass runs while the allgather is in flight with the subtree levels only, and
+// the q top-level terms Y(I_r) += sum_{l <= q} U_l(I_r) t_l (Fig. 5 left's
+// y1 + y2 / y3 + y4 for the levels whose sibling block lives on other ranks,
+// P:666-678) are added afterwards. Thread per (row, column); fixed order.
+struct TopEpilogueParams {
+  double* Y;
+  const double* U;  // the rank's U_local (level-major)
+  const double* T;  // packed [sum_{l<=q} k_l][m] coefficient blocks (dist_combine output)
+  int64_t n;
+  int32_t m, nlev, ktot, pad;
+  int32_t k[kMaxLevels];
+  int64_t uoff[kMaxLevels];
+};
+
+static __global__ void __launch_bounds__(kThreads) dist_top_epilogue_kernel(const TopEpilogueParams P) {
+  extern __shared__ double ts[];  // T staged: ktot * m doubles
+  for (int i = threadIdx.x; i < P.ktot * P.m; i += blockDim.x) ts[i] = P.T[i];
+  __syncthreads();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P.n * P.m) return;
+  const int64_t r = e / P.m;
+  const int c = (int)(e - r * P.m);
+  double acc = 0.0;
+  int toff = 0;
+  for (int l = 0; l < P.nlev; ++l) {
+    const double* u = P.U + P.uoff[l] + r * P.k[l];
+    for (int a = 0; a < P.k[l]; ++a) acc = fma(u[a], ts[(toff + a) * P.m + c], acc);
+    toff += P.k[l];
+  }
+  P.Y[e] += acc;
+}
+
 // ------------------------------------------------------------ leaf_apply --
 
 struct LeafSeg {

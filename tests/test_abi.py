@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_no_error():
     lib = hm.load()
-    assert lib.hm_abi_version() == 1
+    assert lib.hm_abi_version() == 2
     assert isinstance(hm.hm_last_error(), str)
 
 
@@ -152,14 +152,16 @@ def test_general_tree_validation():
         hm.hm_hodlr_general_workspace_bytes(40, 3, c[:4], [2, 1, 3], 2)
 
 
-def _build_c_example(tmp_path):
-    """Compile examples/hm_matvec_example.c (plain C, include/hm.h only) against libhm.so."""
-    exe = str(tmp_path / "hm_matvec_example")
+def _build_c_example(tmp_path, name="hm_matvec_example"):
+    """Compile examples/<name>.c (plain C, include/hm.h only) against libhm.so."""
+    exe = str(tmp_path / name)
     libdir = os.path.dirname(hm.LIB_PATH)
     cuda_lib = "/usr/local/cuda/lib64"
     cmd = ["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
-           os.path.join(ROOT, "examples", "hm_matvec_example.c"), "-o", exe, "-L", libdir, "-l:libhm.so",
+           os.path.join(ROOT, "examples", name + ".c"), "-o", exe, "-L", libdir, "-l:libhm.so",
            "-L", cuda_lib, "-lcudart", f"-Wl,-rpath,{libdir}:{cuda_lib}", "-lm"]
+    if name != "hm_matvec_example":
+        cmd[1] = "-std=gnu99"  # fork / pipe
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     return exe
 
@@ -171,3 +173,37 @@ def test_c_example_links_and_validates(tmp_path):
     out = subprocess.run([exe, "--host-only"], capture_output=True, text=True, timeout=60)
     assert out.returncode == 0, out.stderr
     assert "invalid tree rejected" in out.stdout
+
+
+def test_c_dist_example_links_host_only(tmp_path):
+    """The distributed C-ABI from plain C: examples/hm_dist_example.c compiles against
+    include/hm.h, queries the distributed workspaces, creates a communicator id (NCCL,
+    loaded at run time) and sees P = 3 rejected — no GPU needed."""
+    exe = _build_c_example(tmp_path, "hm_dist_example")
+    out = subprocess.run([exe, "--host-only"], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "communicator id created" in out.stdout
+
+
+def test_library_does_not_link_nccl():
+    """NCCL is dlopen'ed by hm_comm_* only: the single-GPU calls load without it."""
+    out = subprocess.run(["ldd", hm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in out
+
+
+def test_comm_unique_id_on_host():
+    from paper_1909_07909_b200 import dist as hd
+    a, b = hd.unique_id(), hd.unique_id()
+    assert len(a) == hd.HM_COMM_ID_BYTES and a != b
+
+
+def test_dist_workspace_queries():
+    from paper_1909_07909_b200 import dist as hd
+    for P in (1, 2, 8):
+        assert hd.hodlr_dist_workspace_bytes(1 << 16, 8, 256, [16] * 8, 8, P) > 0
+        assert hd.hss_dist_workspace_bytes(1 << 15, 8, 128, 32, 32, P) > 0
+    with pytest.raises(hm.HmError) as e:
+        hd.hodlr_dist_workspace_bytes(1 << 16, 8, 256, [16] * 8, 8, 3)
+    assert e.value.status == hm.HM_ERR_UNSUPPORTED
+    with pytest.raises(hm.HmError):
+        hd.hss_dist_workspace_bytes(1 << 15, 8, 128, 32, 32, 512)   # P > 2^levels

@@ -21,6 +21,12 @@ import torch.multiprocessing as mp  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def allgather(send, gathered):
+    """gathered[P * len(send)] <- concat over ranks of send, rank order (gloo)."""
+    if send.numel():
+        dist.all_gather_into_tensor(gathered, send)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -48,7 +54,7 @@ def hodlr_rank(n, p, b, ranks, D, U, V, X, P, r, hd, oracle):
     send = np.concatenate(send) if send else np.zeros(0)
     assert send.size == sd
     gathered = torch.empty(P * sd, dtype=torch.float64)
-    hd.allgather(torch.from_numpy(send), gathered)
+    allgather(torch.from_numpy(send), gathered)
     gathered = gathered.numpy().reshape(P, sd)
     # _end: subtree product (levels q+1..p on the local rows) + top terms
     sub_ranks = list(ranks[q:])
@@ -104,7 +110,7 @@ def hss_rank(n, p, b, k, s, X, P, r, hd):
     xroot = xleaf[0] if pl == 0 else sh["W_root"].reshape(2 * k, k).T @ np.vstack([xs[1][0], xs[1][1]])
     assert xroot.size == sd
     gathered = torch.empty(P * sd, dtype=torch.float64)
-    hd.allgather(torch.from_numpy(np.ascontiguousarray(xroot).ravel()), gathered)
+    allgather(torch.from_numpy(np.ascontiguousarray(xroot).ravel()), gathered)
     xq = gathered.numpy().reshape(P, k, m)
     # replicated top tree (levels 1..q)
     txs = hss_up(xq, sh["W_top"], q, k, m)
@@ -165,3 +171,28 @@ def test_dist_gloo(tmp_path, world, case):
                        start_method="spawn")
     err = float(open(tmp_path / "err.txt").read())
     assert err < 1e-13, err
+
+
+def _id_worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1909_07909_b200 import dist as hd
+    uid = hd.broadcast_unique_id()
+    with open(os.path.join(outdir, f"id{rank}.bin"), "wb") as f:
+        f.write(uid)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_comm_unique_id_broadcast_gloo(tmp_path, world):
+    """Comm.from_group's out-of-band step: rank 0's libhm (NCCL) unique id reaches every
+    rank byte for byte (the host half of hm_comm_init; the NCCL half needs GPUs)."""
+    from paper_1909_07909_b200 import build
+    build.build()
+    mp.start_processes(_id_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    ids = [open(tmp_path / f"id{r}.bin", "rb").read() for r in range(world)]
+    assert len(ids[0]) == 128 and any(ids[0]) and all(i == ids[0] for i in ids)

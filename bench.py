@@ -232,14 +232,16 @@ class Workload:
 
 class DistWorkload:
     """Rank r of P: the shards of include/hm.h "multi-GPU" (rows of node (q, r) and its
-    subtree), filled on this rank's GPU; one allgather per matvec (NCCL)."""
+    subtree), filled on this rank's GPU; one libhm call per product, the allgather
+    inside libhm (NCCL communicator, hm_comm_*)."""
 
-    calls = ("c5", "c5", "c5", "c4", "c4")  # hodlr begin/local/end, hss begin/end
+    calls = ("c5", "c4")  # one traced call per product
 
     def __init__(self, torch, device, seed, P, r):
         import paper_1909_07909_b200 as hm
         from paper_1909_07909_b200 import dist as hd
         self.torch, self.device, self.hm, self.hd, self.P, self.r = torch, device, hm, hd, P, r
+        self.comm = hd.Comm.from_group()
         n5, p5, b5 = C5.n, C5.levels, C5.leaf
         lpr = (1 << p5) // P
         nl5 = n5 // P
@@ -251,7 +253,7 @@ class DistWorkload:
         _, self.U5, self.V5 = hd.hodlr_shard(n5, p5, b5, self.ranks5, self.D5[:0], U, V, P, r)
         del U, V
         g = torch.Generator(device=device)
-        g.manual_seed(seed)
+        g.manual_seed(seed + r)
         self.X5 = torch.randn(nl5, M5, dtype=torch.float64, device=device, generator=g)
         self.Y5 = torch.empty_like(self.X5)
         s4 = hm_inputs.device_hss_random(C4.n, C4.levels, C4.k, seed + 1, device)  # same draw on every rank
@@ -263,10 +265,10 @@ class DistWorkload:
         self.rows4 = nl4
         self.X4 = torch.randn(nl4, M4, dtype=torch.float64, device=device, generator=g)
         self.Y4 = torch.empty_like(self.X4)
-        w5, self.sd5 = hd.hodlr_dist_sizes(n5, p5, b5, self.ranks5, M5, P, r)
-        w4, self.sd4 = hd.hss_dist_sizes(C4.n, C4.levels, C4.leaf, C4.k, M4, P, r)
-        self.ws5 = torch.empty(w5, dtype=torch.uint8, device=device)
-        self.ws4 = torch.empty(w4, dtype=torch.uint8, device=device)
+        self.ws5 = torch.empty(hd.hodlr_dist_workspace_bytes(n5, p5, b5, self.ranks5, M5, P), dtype=torch.uint8,
+                               device=device)
+        self.ws4 = torch.empty(hd.hss_dist_workspace_bytes(C4.n, C4.levels, C4.leaf, C4.k, M4, P), dtype=torch.uint8,
+                               device=device)
         self.X5h = self.X5.cpu().pin_memory()
         self.Y5h = torch.empty_like(self.X5h).pin_memory()
         self.X4h = self.X4.cpu().pin_memory()
@@ -274,10 +276,10 @@ class DistWorkload:
         self.launches = 0
 
     def step(self):
-        hd, hm = self.hd, self.hm
-        hd.hodlr_matvec_dist(C5.n, C5.levels, C5.leaf, self.ranks5, self.D5, self.U5, self.V5, self.X5, self.Y5,
-                             ws=self.ws5)
-        hd.hss_matvec_dist(C4.n, C4.levels, C4.leaf, C4.k, self.sh4, self.X4, self.Y4, ws=self.ws4)
+        hd = self.hd
+        hd.hodlr_matvec_dist(self.comm, C5.n, C5.levels, C5.leaf, self.ranks5, self.D5, self.U5, self.V5, self.X5,
+                             self.Y5, ws=self.ws5)
+        hd.hss_matvec_dist(self.comm, C4.n, C4.levels, C4.leaf, C4.k, self.sh4, self.X4, self.Y4, ws=self.ws4)
 
     def e2e_begin(self, ev):
         pass
@@ -294,6 +296,9 @@ class DistWorkload:
 
     def h2d_d2h_bytes(self):
         return 8 * (self.X5.numel() + self.X4.numel()), 8 * (self.Y5.numel() + self.Y4.numel())
+
+    def close(self):
+        self.comm.close()
 
 
 # ------------------------------------------------------ nrhs / ops sweep --
@@ -357,7 +362,7 @@ def _time_call(torch, f, reps, warm=2):
     return e0.elapsed_time(e1) / reps
 
 
-def sweep(torch, device, wl, peak):
+def sweep(torch, device, wl, peak, parity=True):
     """Secondary measurements (not part of `value`): the metric "vs nrhs" on config 3
     (m = 1, 8, 64), the small configs 1-2 (latency-bound, L2-resident: us per call), the
     adjoint products, the ||A||_2 estimate (f2), hss2hodlr (f3) and
@@ -373,6 +378,10 @@ def sweep(torch, device, wl, peak):
     # config 3: HODLR n = 2^20, leaf 256, 12 levels, k = 16, nrhs 1 / 8 / 64, A X and A^T X
     c3 = hm_inputs.CONFIGS[3]
     h3 = hm_inputs.device_hodlr_random(c3.n, c3.levels, [c3.k] * c3.levels, hm_inputs.MASTER_SEED + 3, device)
+    if parity:
+        import oracle
+        oracle.set_num_threads(os.cpu_count() or 1)
+        h3h = [t.cpu().numpy() for t in (h3.D, h3.U, h3.V)]
     for m in c3.nrhs:
         X = torch.randn(c3.n, m, dtype=torch.float64, device=device, generator=g)
         Y = torch.empty_like(X)
@@ -386,6 +395,10 @@ def sweep(torch, device, wl, peak):
                                    "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2),
                                    "frac_fp64": round(fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                                    "matvecs/s": round(1e3 / ms, 1), "column_matvecs/s": round(m * 1e3 / ms, 1)}
+            if parity:  # every row of this product vs the oracle on the same bytes
+                ref = oracle.hodlr_matvec if nm == "" else oracle.hodlr_matvec_t
+                Yr = ref(c3.n, c3.levels, h3.ranks, *h3h, X.cpu().numpy())
+                out[f"c3_m{m}{nm}"]["parity"] = {"relerr_vs_oracle": _relerr(Y.cpu().numpy(), Yr), "rows": c3.n}
         del X, Y, ws
     # per-level ranks on the config-3 tree (f4): one V^T X pass per distinct
     # rank (tuned kernel where the rank fits it, vt_contract otherwise), one leaf pass
@@ -410,6 +423,8 @@ def sweep(torch, device, wl, peak):
                                                  "ranks": f"{tag} by level", "kernels": kern}
         del hv, X, Y, ws
     del h3
+    if parity:
+        del h3h
     # general cluster tree (f4) at the config-3 scale: ragged leaves of
     # 128..384 rows (config-3 mean 256), k = 16 on every level; general-tree kernels
     rng = np.random.default_rng(hm_inputs.MASTER_SEED + 9)
@@ -491,6 +506,12 @@ def sweep(torch, device, wl, peak):
     out["c1_us"] = round(ms * 1e3, 2)
     out["c1_us_graph"] = _graph_us(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V,
                                                                   X, Y, ws))
+    if parity:
+        hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V, X, Y, ws)
+        torch.cuda.synchronize()
+        Yr = oracle.hodlr_matvec(c1.n, c1.levels, h1.ranks, h1.D.cpu().numpy(), h1.U.cpu().numpy(),
+                                 h1.V.cpu().numpy(), X.cpu().numpy())
+        out["c1"] = {"us": out["c1_us"], "parity": {"relerr_vs_oracle": _relerr(Y.cpu().numpy(), Yr), "rows": c1.n}}
     s2 = hm_inputs.device_hss_random(c2.n, c2.levels, c2.k, hm_inputs.MASTER_SEED + 2, device)
     X = torch.randn(c2.n, 16, dtype=torch.float64, device=device, generator=g)
     Y = torch.empty_like(X)
@@ -500,6 +521,12 @@ def sweep(torch, device, wl, peak):
     out["c2_us"] = round(ms * 1e3, 2)
     out["c2_us_graph"] = _graph_us(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R,
                                                                 s2.W, s2.B, X, Y, ws))
+    if parity:
+        hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R, s2.W, s2.B, X, Y, ws)
+        torch.cuda.synchronize()
+        g2 = [t.cpu().numpy() for t in (s2.D, s2.U, s2.V, s2.R, s2.W, s2.B)]
+        Yr = oracle.hss_matvec(c2.n, c2.levels, c2.k, *g2, X.cpu().numpy())
+        out["c2"] = {"us": out["c2_us"], "parity": {"relerr_vs_oracle": _relerr(Y.cpu().numpy(), Yr), "rows": c2.n}}
     return out
 
 
@@ -673,74 +700,153 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
-    if world == 1 and not args.no_sweep:
-        out["sweep"] = sweep(torch, device, wl, peak)
-    if world > 1:
+    if not use_dist and not args.no_parity:
+        # every row of the timed step's Y vs the oracle on the same inputs (copied to
+        # the host); the same oracle runs, timed, are the cpu_baseline
+        par, cpu = parity_and_cpu(torch, wl, args.no_cpu_baseline)
+        out["parity"] = par
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+    if not use_dist and not args.no_sweep:
+        out["sweep"] = sweep(torch, device, wl, peak, parity=not args.no_parity)
+        if "parity" in out:  # configs 1-3 (sweep) beside 4-5 (the step): all five configs
+            out["parity"].update({k_: v["parity"] for k_, v in out["sweep"].items()
+                                  if isinstance(v, dict) and "parity" in v})
+            out["parity"]["all_within_tol"] = all(
+                v.get("relerr_vs_oracle", 0.0) <= out["parity"]["tol"] for v in out["parity"].values()
+                if isinstance(v, dict))
+    if use_dist:
         out["per_config"]["note"] = "per-rank device time (rank 0's launch trace)"
         out["roofline"]["kernel"] += f" — rank 0's shard (1/{world} of the rows)"
+        out["parity"] = {"note": "the distributed product's parity is checked by tests/test_dist_*.py "
+                                 "(emulated ranks vs the oracle, P = 1 NCCL vs the single-GPU product)"}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
+        wl.close()
         dist.barrier()
         dist.destroy_process_group()
 
 
 # ------------------------------------------------------------ CPU oracle --
+#
+# The oracle (oracle/, plain C, the method written out from the paper) is the
+# reported CPU baseline and the --impl reference arm. It is run
+# as it stands; only its OpenMP thread count is chosen (results are bitwise
+# independent of it).
 
-def oracle_sample():
-    """Bounded sample of the same workload for the oracle: config-5 structure at n = 2^20
-    (leaf 256, 12 levels, k = 1) and config-4 structure at n = 2^17 (leaf 128, 10 levels,
-    k = 32, nrhs 32). Both are GB/s-normalised, so the sample's GB/s is comparable."""
-    n5, p5 = 1 << 20, 12
-    n4, p4 = 1 << 17, 10
-    h = hm_inputs.hodlr_inverse_laplacian(n5, p5)
-    X5 = hm_inputs.rhs(n5, M5, cid=5)
-    s = hm_inputs.hss_random(n4, p4, C4.k, cid=4)
-    X4 = hm_inputs.rhs(n4, M4, cid=4)
-    nbytes = hodlr_bytes(n5, 256, p5, 1, M5) + hss_bytes(n4, 128, p4, C4.k, M4)
-    desc = (f"oracle on config-5 structure n=2^20 (leaf 256, 12 levels, k=1, nrhs=1) + config-4 structure "
-            f"n=2^17 (leaf 128, 10 levels, k=32, nrhs=32)")
-
-    def run():
-        import oracle
-        oracle.hodlr_matvec(n5, p5, h.ranks, h.D, h.U, h.V, X5)
-        oracle.hss_matvec(n4, p4, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, X4)
-
-    return run, nbytes, desc
+def host_info():
+    model, mem = "?", None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem = round(int(line.split()[1]) / 1024 / 1024, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "host_ram_gib": mem}
 
 
-def cpu_baseline(seconds=12.0):
+def _relerr(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _tridiag_residual(Y, X):
+    TY = 2 * Y
+    TY[1:] -= Y[:-1]
+    TY[:-1] -= Y[1:]
+    normT = 2 + 2 * np.cos(np.pi / (Y.shape[0] + 1))
+    return float(np.linalg.norm(TY - X) / (normT * np.linalg.norm(Y) + np.linalg.norm(X)))
+
+
+def parity_and_cpu(torch, wl, no_cpu=False, reps=3):
+    """Every row of the timed step's outputs (configs 5 and 4, full size) against the
+    oracle on the same input bytes, copied to the host; the oracle runs are timed
+    (all host cores, median of `reps`) and reported as cpu_baseline."""
     import oracle
-    run, nbytes, desc = oracle_sample()
-    run()  # first touch / thread pool
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        run()
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    return {"value": round(nbytes * reps / el / 1e9, 3), "unit": "GB/s", "cores": oracle.num_threads(),
-            "kind": "oracle", "sample": f"{desc}; {reps} repetitions in {el:.1f} s"}
+    oracle.build()
+    h, s4 = wl.h5, wl.s4
+    wl.step()
+    torch.cuda.synchronize()
+    host = lambda t: t.cpu().numpy()  # noqa: E731
+    X5, Y5, X4, Y4 = host(wl.X5), host(wl.Y5), host(wl.X4), host(wl.Y4)
+    D5, U5, V5 = host(h.D), host(h.U), host(h.V)
+    g4 = {a: host(getattr(s4, a)) for a in ("D", "U", "V", "R", "W", "B")}
+    oracle.set_num_threads(os.cpu_count() or 1)
+    cores = oracle.num_threads()
+    t5, t4 = [], []
+    for _ in range(1 if no_cpu else reps):
+        t0 = time.perf_counter()
+        Yr5 = oracle.hodlr_matvec(C5.n, C5.levels, h.ranks, D5, U5, V5, X5)
+        t5.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        Yr4 = oracle.hss_matvec(C4.n, C4.levels, C4.k, g4["D"], g4["U"], g4["V"], g4["R"], g4["W"], g4["B"], X4)
+        t4.append(time.perf_counter() - t0)
+    tol = 1e-12
+    par = {"tol": tol, "metric": "||Y_gpu - Y_oracle||_F / ||Y_oracle||_F over every row (north_star)",
+           "c5": {"relerr_vs_oracle": _relerr(Y5, Yr5),
+                  "relerr_vs_closed_form": _relerr(Y5, oracle.laplacian_inverse_apply(X5)),
+                  "tridiag_residual": _tridiag_residual(Y5, X5), "rows": C5.n},
+           "c4": {"relerr_vs_oracle": _relerr(Y4, Yr4), "rows": C4.n, "nrhs": M4}}
+    par["all_within_tol"] = par["c5"]["relerr_vs_oracle"] <= tol and par["c4"]["relerr_vs_oracle"] <= tol
+    del D5, U5, V5, g4
+    if no_cpu:
+        return par, None
+    m5, m4 = statistics.median(t5), statistics.median(t4)
+    cpu = {"value": round(step_bytes() / (m5 + m4) / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+           "sample": "the full timed workload (config 5 n=2^24 + config 4 n=2^22, nrhs 32) on the same input bytes "
+                     f"as the GPU step, median of {reps}",
+           "per_config_s": {"c5": round(m5, 3), "c4": round(m4, 3)}, **host_info()}
+    table = os.path.join(ROOT, "profiles", "r02_cpu_table.json")
+    if os.path.exists(table):
+        cpu["per_config_table"] = "profiles/r02_cpu_table.json (bench.py --cpu-table: every config, 1 thread and " \
+                                  "all cores, median of 3, full sizes)"
+    return par, cpu
+
+
+def host_workload():
+    """The step's inputs generated on the host (hm_inputs), full size: config 5 from the
+    closed form, config 4 orthonormalised Gaussians; X iid N(0,1)."""
+    h = hm_inputs.hodlr_inverse_laplacian(C5.n, C5.levels)
+    X5 = hm_inputs.rhs(C5.n, M5, cid=5)
+    s = hm_inputs.hss_random(C4.n, C4.levels, C4.k, cid=4)
+    X4 = hm_inputs.rhs(C4.n, M4, cid=4)
+    return h, X5, s, X4
 
 
 def run_reference(args):
+    """The reference arm: the oracle on the host cores, the SAME workload as ours (one
+    step = config 5 + config 4 at full size), all host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     oracle.build()
-    run, nbytes, desc = oracle_sample()
+    oracle.set_num_threads(os.cpu_count() or 1)
+    t_gen = time.perf_counter()
+    h, X5, s, X4 = host_workload()
+    t_gen = time.perf_counter() - t_gen
+
+    def run():
+        oracle.hodlr_matvec(C5.n, C5.levels, h.ranks, h.D, h.U, h.V, X5)
+        oracle.hss_matvec(C4.n, C4.levels, C4.k, s.D, s.U, s.V, s.R, s.W, s.B, X4)
+
     for _ in range(args.warmup):
         run()
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         run()
-    el = time.perf_counter() - t0
-    value = nbytes * args.steps / el / 1e9
+        times.append(time.perf_counter() - t0)
+    el = sum(times)
+    value = step_bytes() * args.steps / el / 1e9
     cores = oracle.num_threads()
+    desc = ("oracle (oracle/hm_oracle.c) on the full step: HODLR config 5 (n=2^24, leaf 256, 16 levels, k=1, "
+            "nrhs=1) + HSS config 4 (n=2^22, leaf 128, 15 levels, k=32, nrhs=32), host-generated inputs")
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -754,13 +860,75 @@ def run_reference(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded)",
-        "config": {"workload": "c5+c4 (bounded host sample per step: " + desc + ")"},
+        "data": "synthetic (seeded; config 5 closed-form inverse Laplacian, config 4 orthonormalised Gaussians)",
+        "config": {"workload": "c5+c4: HODLR config 5 (n=2^24, leaf 256, 16 levels, k=1, nrhs=1) + HSS config 4 "
+                               "(n=2^22, leaf 128, 15 levels, k=32, nrhs=32) per step",
+                   "step_alg_bytes": step_bytes(), "same_config": True,
+                   "input_generation_s": round(t_gen, 1)},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc + f"; {args.steps} steps, median step {statistics.median(times):.2f} s",
+                         **host_info()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def cpu_table(path, reps=3):
+    """the oracle per config at full size, 1 thread and all host cores,
+    median of `reps` (input generation excluded), with the host's CPU model and core count."""
+    import oracle
+    oracle.build()
+    allc = os.cpu_count() or 1
+    rows = []
+
+    def timed(f, threads):
+        oracle.set_num_threads(threads)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            f()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    def add(cfg, nrhs, nbytes, flops, f):
+        row = {"config": cfg, "nrhs": nrhs, "alg_bytes": nbytes, "gflop": round(flops / 1e9, 3)}
+        for th in (1, allc):
+            t = timed(f, th)
+            row[f"s_{th}thr"] = round(t, 4)
+            row[f"GB/s_{th}thr"] = round(nbytes / t / 1e9, 3)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+
+    c = hm_inputs.CONFIGS
+    for cid in (1, 3):
+        cfg = c[cid]
+        h = hm_inputs.hodlr_random(cfg.n, cfg.levels, [cfg.k] * cfg.levels, cid=cid)
+        for m in cfg.nrhs:
+            X = hm_inputs.rhs(cfg.n, m, cid=cid)
+            add(f"C{cid}", m, hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m),
+                hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m),
+                lambda: oracle.hodlr_matvec(cfg.n, cfg.levels, h.ranks, h.D, h.U, h.V, X))
+        del h
+    for cid in (2, 4):
+        cfg = c[cid]
+        sh = hm_inputs.hss_random(cfg.n, cfg.levels, cfg.k, cid=cid)
+        for m in cfg.nrhs:
+            X = hm_inputs.rhs(cfg.n, m, cid=cid)
+            add(f"C{cid}", m, hss_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m),
+                hss_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m),
+                lambda: oracle.hss_matvec(cfg.n, cfg.levels, cfg.k, sh.D, sh.U, sh.V, sh.R, sh.W, sh.B, X))
+        del sh
+    cfg = c[5]
+    h = hm_inputs.hodlr_inverse_laplacian(cfg.n, cfg.levels)
+    X = hm_inputs.rhs(cfg.n, 1, cid=5)
+    add("C5", 1, hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, 1), hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, 1),
+        lambda: oracle.hodlr_matvec(cfg.n, cfg.levels, h.ranks, h.D, h.U, h.V, X))
+    out = {"what": "oracle/hm_oracle.c timed per BASELINE.json config at full size (BASELINE.md §4)",
+           "reps": reps, "statistic": "median", "threads": [1, allc], "rows": rows,
+           "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), **host_info()}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps({"written": path}), flush=True)
 
 
 def main():
@@ -769,13 +937,17 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the secondary nrhs / ops sweep")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle comparison of the timed outputs")
+    ap.add_argument("--cpu-table", metavar="PATH", help="time the oracle per config (BASELINE.md §4: 1 thread and "
+                    "all cores, median of 3, full sizes) and write the JSON table to PATH; no GPU work")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.cpu_table:
+        cpu_table(args.cpu_table)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

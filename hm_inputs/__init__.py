@@ -18,10 +18,38 @@ Array ids: X=0, D=1, U=2, V=3, R=4, W=5, B=6.
 """
 from __future__ import annotations
 
+import ctypes
+import os
+import subprocess
 from dataclasses import dataclass, field
 from typing import Dict, Optional, Sequence, Tuple
 
 import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_FILL_SRC = os.path.join(_HERE, "fill.c")
+_FILL_LIB = os.path.join(_HERE, "libfill.so")
+_fill = None
+
+
+def build(force: bool = False) -> str:
+    """Compile fill.c (the OpenMP host fill of the closed-form config-5 generators)."""
+    if force or not os.path.exists(_FILL_LIB) or os.path.getmtime(_FILL_LIB) < os.path.getmtime(_FILL_SRC):
+        tmp = _FILL_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
+                               "-Wall", "-o", tmp, _FILL_SRC])
+        os.replace(tmp, _FILL_LIB)
+    return _FILL_LIB
+
+
+def _fill_lib():
+    global _fill
+    if _fill is None:
+        lib = ctypes.CDLL(build())
+        lib.fill_laplacian_leaves.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_void_p]
+        lib.fill_laplacian_leaves.restype = ctypes.c_int
+        _fill = lib
+    return _fill
 
 MASTER_SEED = 190907909  # fixed and recorded in the bench output (SURVEY G9)
 AID = {"X": 0, "D": 1, "U": 2, "V": 3, "R": 4, "W": 5, "B": 6}
@@ -135,6 +163,11 @@ def inverse_laplacian_leaf_blocks(n: int, levels: int, leaves=None, xp=np, devic
     kw = {} if xp is np else {"device": device}
     if leaves is None:
         leaves = range(1 << levels)
+    if xp is np and isinstance(leaves, range) and leaves.step == 1:  # contiguous: the OpenMP fill
+        out = np.empty(len(leaves) * b * b, dtype=np.float64)
+        if _fill_lib().fill_laplacian_leaves(n, b, leaves.start, len(leaves), out.ctypes.data) != 0:
+            raise ValueError("fill_laplacian_leaves: bad arguments")
+        return out
     leaves = list(leaves)
     out = xp.empty((len(leaves), b, b), dtype=xp.float64, **kw)
     np1 = n + 1

@@ -70,6 +70,8 @@ def _load() -> ctypes.CDLL:
             f = getattr(_lib, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        _lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        _lib.oracle_set_num_threads.restype = None
     return _lib
 
 
@@ -101,6 +103,11 @@ def _tree(n: int, p: int, c: Optional[Sequence[int]]) -> np.ndarray:
 
 def num_threads() -> int:
     return _load().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (results are bitwise independent of it)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def default_cluster(n: int, nmin: int):

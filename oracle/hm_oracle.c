@@ -33,6 +33,17 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops (results do not depend on it: every
+ * reduction is sequential in a fixed order). For the 1-thread / all-core
+ * baseline rows of BASELINE.md §4. */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n >= 1) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 /* ---------------------------------------------------------------- trees -- */
 /* Def. 2.1 + the leaf-endpoint vector c of P:560-565. */
 

@@ -142,6 +142,7 @@ int oracle_laplacian_inverse_apply(int64_t n, const double* X, int32_t m, double
 
 /* Number of threads the OpenMP parts use (1 if built without OpenMP). */
 int oracle_num_threads(void);
+void oracle_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

@@ -219,7 +219,7 @@ def test_hss_matvec_dist_nccl_p1(hm, comm, n, b, p, k, m):
     assert relerr(Yd.cpu().numpy(), Yr) <= TOL
     Y1 = hm.hss_matvec(n, p, b, k, g["D"], g["U"], g["V"], g["R"], g["W"], g["B"], Xd)
     torch.cuda.synchronize()
-    assert torch.equal(Yd, Y1)
+    assert relerr(Yd.cpu().numpy(), Y1.cpu().numpy()) <= 1e-14  # the single-GPU call may take hss_small
 
 
 def test_config5_dist_nccl_p1(hm, comm):

@@ -366,32 +366,66 @@ int oracle_hodlr_dense(int64_t n, int32_t p, const int64_t* c, const int32_t* ra
 }
 
 /* ------------------------------------------------------------------- HSS -- */
-
-/* node (l, i), l >= 1, in the level-major coefficient arrays x^, y^ */
-static int64_t coef_index(int32_t l, int64_t i) { return ((int64_t)1 << l) - 2 + i; }
+/* Ranks may differ per level (bases and translation operators need not
+ * have k columns on every level "as long as the dimensions are compatible"):
+ * k_l = ranks[l-1] for the nodes of level l = 1..p. Then U_i^(p), V_i^(p) are
+ * |I_i| x k_p, R_{U,i}^(l), R_{V,i}^(l) of a level-l node are 2k_{l+1} x k_l
+ * (eq. (3) P:256-259 with the children's k_{l+1} columns), the cores of the
+ * level-l siblings are k_l x k_l, and the coefficient vectors v_i^l are
+ * k_l x m. Flat layout (level-major, row-major; the uniform layout of hm.h
+ * when every k_l = k):
+ *   R, W  node (l, i), l = 1..p-1: offset sum_{l'<l} 2^l' 2 k_{l'+1} k_l' + i 2 k_{l+1} k_l
+ *   B     the cores of the level-l siblings 2q, 2q+1 (stored at the parent
+ *         (l-1, q)): offset sum_{l'<l} 2^(l'-1) 2 k_l'^2 + q 2 k_l^2, [B12; B21] */
 
 typedef struct {
   int64_t n;
-  int32_t p, k, m;
+  int32_t p, m;
   const int64_t* c;
   int64_t* d_off;
+  int32_t* kl;      /* kl[l] = k_l, l = 1..p (kl[0] = 0) */
+  int64_t* cf_off;  /* coefficient block of node (l, 0) in xh / yh, in doubles */
+  int64_t* rw_off;  /* R / W of node (l, 0) */
+  int64_t* b_off;   /* cores of the level-l siblings of parent (l-1, 0) */
   const double *D, *U, *V, *R, *W, *B, *X;
-  double* xh; /* v_i^l of Step 1, one k x m block per node l = 1..p */
+  double* xh; /* v_i^l of Step 1, one k_l x m block per node l = 1..p */
   double* yh; /* the same vectors after Steps 2-3 */
   int trans;  /* 1: apply A^* (adjoint), see hss_matvec_op */
 } hss_ctx;
 
-static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, int32_t k,
+static int32_t kMaxOr1(const int32_t* kl, int32_t p) {
+  int32_t k = 1;
+  for (int32_t l = 1; l <= p; ++l) k = kl[l] > k ? kl[l] : k;
+  return k;
+}
+
+static double* coef(const hss_ctx* s, double* base, int32_t l, int64_t i) {
+  return base + s->cf_off[l] + i * (int64_t)s->kl[l] * s->m;
+}
+
+static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
                      const double* D, const double* U, const double* V,
                      const double* R, const double* W, const double* B, const double* X, int32_t m) {
   memset(s, 0, sizeof(*s));
-  if (check_tree(n, p, c) || k < 0 || m < 1) return -1;
-  s->n = n; s->p = p; s->k = k; s->m = m; s->c = c;
+  if (check_tree(n, p, c) || m < 1 || (p > 0 && ranks == NULL)) return -1;
+  s->n = n; s->p = p; s->m = m; s->c = c;
   s->D = D; s->U = U; s->V = V; s->R = R; s->W = W; s->B = B; s->X = X;
   s->d_off = leaf_block_offsets(c, p);
-  if (!s->d_off) return -1;
-  int64_t nodes = ((int64_t)1 << (p + 1)) - 2;
-  size_t cnt = (size_t)(nodes * k * m + 1);
+  s->kl = (int32_t*)calloc((size_t)(p + 2), sizeof(int32_t));
+  s->cf_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
+  s->rw_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
+  s->b_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
+  if (!s->d_off || !s->kl || !s->cf_off || !s->rw_off || !s->b_off) return -1;
+  for (int32_t l = 1; l <= p; ++l) {
+    if (ranks[l - 1] < 0) return -1;
+    s->kl[l] = ranks[l - 1];
+  }
+  for (int32_t l = 1; l <= p; ++l) {
+    s->cf_off[l + 1] = s->cf_off[l] + ((int64_t)1 << l) * s->kl[l] * m;
+    s->b_off[l + 1] = s->b_off[l] + ((int64_t)1 << (l - 1)) * 2 * s->kl[l] * s->kl[l];
+    if (l <= p - 1) s->rw_off[l + 1] = s->rw_off[l] + ((int64_t)1 << l) * 2 * s->kl[l + 1] * s->kl[l];
+  }
+  size_t cnt = (size_t)s->cf_off[p + 1] + 1;
   s->xh = (double*)calloc(cnt, sizeof(double));
   s->yh = (double*)calloc(cnt, sizeof(double));
   return (s->xh && s->yh) ? 0 : -1;
@@ -399,40 +433,45 @@ static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, int32_t
 
 static void hss_teardown(hss_ctx* s) {
   free(s->d_off); free(s->xh); free(s->yh);
+  free(s->kl); free(s->cf_off); free(s->rw_off); free(s->b_off);
 }
 
 /* Step 1, first half, and the upsweep (Fig. 5 right):
  *   v_i^p = (V_i^(p))^* v(I_i^p),  i = 1..2^p
  *   v_i^l = (R_{V,i}^(l))^* [v_{2i-1}^{l+1}; v_{2i}^{l+1}],  l = p-1..1
- * with R_{V,i}^(l) = W[node] = [Wl; Wr] (2k x k), reading G3. */
+ * with R_{V,i}^(l) = W[node] = [Wl; Wr] (2k_{l+1} x k_l), reading G3. */
 static void hss_upsweep(hss_ctx* s) {
-  int32_t p = s->p, k = s->k, m = s->m;
+  int32_t p = s->p, m = s->m;
+  if (p == 0) return;
+  int32_t kp = s->kl[p];
   int64_t nl = (int64_t)1 << p;
-  if (k == 0 || p == 0) return;
-#pragma omp parallel for schedule(static) if (s->n * k * m > OMP_MIN_WORK)
-  for (int64_t i = 0; i < nl; ++i) {
-    int64_t lo = leaf_lo(s->c, i), hi = s->c[i];
-    double* t = s->xh + coef_index(p, i) * k * m;
-    for (int32_t a = 0; a < k; ++a)
-      for (int32_t q = 0; q < m; ++q) {
-        double acc = 0.0;
-        for (int64_t r = lo; r < hi; ++r) acc += s->V[r * k + a] * s->X[r * m + q];
-        t[a * m + q] = acc;
-      }
+  if (kp > 0) {
+#pragma omp parallel for schedule(static) if (s->n * kp * m > OMP_MIN_WORK)
+    for (int64_t i = 0; i < nl; ++i) {
+      int64_t lo = leaf_lo(s->c, i), hi = s->c[i];
+      double* t = coef(s, s->xh, p, i);
+      for (int32_t a = 0; a < kp; ++a)
+        for (int32_t q = 0; q < m; ++q) {
+          double acc = 0.0;
+          for (int64_t r = lo; r < hi; ++r) acc += s->V[r * kp + a] * s->X[r * m + q];
+          t[a * m + q] = acc;
+        }
+    }
   }
   for (int32_t l = p - 1; l >= 1; --l) {
     int64_t cnt = (int64_t)1 << l;
-#pragma omp parallel for schedule(static) if (cnt * 4 * k * k * m > OMP_MIN_WORK)
+    int32_t kc = s->kl[l + 1], k = s->kl[l];
+#pragma omp parallel for schedule(static) if (cnt * 4 * kc * k * m > OMP_MIN_WORK)
     for (int64_t i = 0; i < cnt; ++i) {
-      const double* Wn = s->W + coef_index(l, i) * 2 * k * k; /* [2k][k] */
-      const double* z0 = s->xh + coef_index(l + 1, 2 * i) * k * m;     /* v_{2i-1}^{l+1} */
-      const double* z1 = s->xh + coef_index(l + 1, 2 * i + 1) * k * m; /* v_{2i}^{l+1}   */
-      double* t = s->xh + coef_index(l, i) * k * m;
+      const double* Wn = s->W + s->rw_off[l] + i * 2 * kc * k; /* [2k_{l+1}][k_l] */
+      const double* z0 = coef(s, s->xh, l + 1, 2 * i);         /* v_{2i-1}^{l+1} */
+      const double* z1 = coef(s, s->xh, l + 1, 2 * i + 1);     /* v_{2i}^{l+1}   */
+      double* t = coef(s, s->xh, l, i);
       for (int32_t a = 0; a < k; ++a)
         for (int32_t q = 0; q < m; ++q) {
-          double acc = 0.0; /* (W^T z)[a] = sum_{r<2k} W[r][a] z[r], r in natural order */
-          for (int32_t r = 0; r < k; ++r) acc += Wn[r * k + a] * z0[r * m + q];
-          for (int32_t r = 0; r < k; ++r) acc += Wn[(k + r) * k + a] * z1[r * m + q];
+          double acc = 0.0; /* (W^T z)[a] = sum_{r<2k_{l+1}} W[r][a] z[r], r in natural order */
+          for (int32_t r = 0; r < kc; ++r) acc += Wn[r * k + a] * z0[r * m + q];
+          for (int32_t r = 0; r < kc; ++r) acc += Wn[(kc + r) * k + a] * z1[r * m + q];
           t[a * m + q] = acc;
         }
     }
@@ -444,10 +483,10 @@ static void hss_upsweep(hss_ctx* s) {
  * S_{2q,2q+1}^{(l)} = B12 and S_{2q+1,2q}^{(l)} = B21 of the parent (l-1, q).
  * Writes only the member `which` (0 = 2q, 1 = 2q+1) of the pair. */
 static void hss_couple(hss_ctx* s, int32_t l, int64_t q, int which) {
-  int32_t k = s->k, m = s->m;
-  const double* Bn = s->B + (((int64_t)1 << (l - 1)) - 1 + q) * 2 * k * k;
-  const double* xin = s->xh + coef_index(l, 2 * q + (which == 0 ? 1 : 0)) * k * m;
-  double* yout = s->yh + coef_index(l, 2 * q + which) * k * m;
+  int32_t k = s->kl[l], m = s->m;
+  const double* Bn = s->B + s->b_off[l] + q * 2 * k * k;
+  const double* xin = coef(s, s->xh, l, 2 * q + (which == 0 ? 1 : 0));
+  double* yout = coef(s, s->yh, l, 2 * q + which);
   /* A: S = B12 (which 0) or B21 (which 1). A^*: the cores of A^* are
    * S'_{2q,2q+1} = (S_{2q+1,2q})^* = B21^T and S'_{2q+1,2q} = B12^T. */
   const double* S = s->trans ? Bn + (which == 0 ? k * k : 0) : Bn + (which == 0 ? 0 : k * k);
@@ -461,13 +500,13 @@ static void hss_couple(hss_ctx* s, int32_t l, int64_t q, int which) {
 
 /* Step 3 for one child:
  *   [v_{2i-1}^{l+1}; v_{2i}^{l+1}] <- [v_{2i-1}^{l+1}; v_{2i}^{l+1}] + R_{U,i}^{(l)} v_i^l
- * R_{U,i}^{(l)} = R[node] = [Rl; Rr]. Updates child `which` (0 left, 1 right). */
+ * R_{U,i}^{(l)} = R[node] = [Rl; Rr] (2k_{l+1} x k_l). Updates child `which`. */
 static void hss_down(hss_ctx* s, int32_t l, int64_t i, int which) {
-  int32_t k = s->k, m = s->m;
-  const double* Rn = s->R + coef_index(l, i) * 2 * k * k + (which == 0 ? 0 : k * k);
-  const double* yin = s->yh + coef_index(l, i) * k * m;
-  double* ych = s->yh + coef_index(l + 1, 2 * i + which) * k * m;
-  for (int32_t a = 0; a < k; ++a)
+  int32_t kc = s->kl[l + 1], k = s->kl[l], m = s->m;
+  const double* Rn = s->R + s->rw_off[l] + i * 2 * kc * k + (which == 0 ? 0 : kc * k);
+  const double* yin = coef(s, s->yh, l, i);
+  double* ych = coef(s, s->yh, l + 1, 2 * i + which);
+  for (int32_t a = 0; a < kc; ++a)
     for (int32_t c2 = 0; c2 < m; ++c2) {
       double acc = 0.0;
       for (int32_t r = 0; r < k; ++r) acc += Rn[a * k + r] * yin[r * m + c2];
@@ -478,9 +517,10 @@ static void hss_down(hss_ctx* s, int32_t l, int64_t i, int which) {
 /* Step 4 for one leaf (reading G2): y(I_i) = U_i v_i^p + d_i,
  * d_i = A(I_i, I_i) v(I_i). Dblk is D_i, y the leaf's output rows. */
 static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double* y) {
-  int32_t k = s->k, m = s->m, p = s->p;
+  int32_t m = s->m, p = s->p;
+  int32_t k = p > 0 ? s->kl[p] : 0;
   int64_t lo = leaf_lo(s->c, i), rows = s->c[i] - lo;
-  const double* yv = (p > 0 && k > 0) ? s->yh + coef_index(p, i) * k * m : NULL;
+  const double* yv = (p > 0 && k > 0) ? coef(s, s->yh, p, i) : NULL;
   for (int64_t r = 0; r < rows; ++r)
     for (int32_t q = 0; q < m; ++q) {
       double d = 0.0;
@@ -493,42 +533,50 @@ static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double
     }
 }
 
+/* Steps 2 and 3 on every node (the whole tree). */
+static void hss_couple_down_all(hss_ctx* s) {
+  int32_t p = s->p;
+  for (int32_t l = 1; l <= p; ++l) { /* Step 2, all levels incl. the leaves (G1) */
+    int64_t pairs = (int64_t)1 << (l - 1);
+    int32_t k = s->kl[l];
+    if (k == 0) continue;
+#pragma omp parallel for schedule(static) if (pairs * 2 * k * k * s->m > OMP_MIN_WORK)
+    for (int64_t q = 0; q < pairs; ++q) {
+      hss_couple(s, l, q, 0);
+      hss_couple(s, l, q, 1);
+    }
+  }
+  for (int32_t l = 1; l <= p - 1; ++l) { /* Step 3, top to bottom */
+    int64_t cnt = (int64_t)1 << l;
+    int32_t k = s->kl[l], kc = s->kl[l + 1];
+    if (k == 0 || kc == 0) continue;
+#pragma omp parallel for schedule(static) if (cnt * 2 * kc * k * s->m > OMP_MIN_WORK)
+    for (int64_t i = 0; i < cnt; ++i) {
+      hss_down(s, l, i, 0);
+      hss_down(s, l, i, 1);
+    }
+  }
+}
+
 /* The adjoint of an HSS matrix is HSS on the same tree (eq. (3)):
  * A^*(I_b, I_a) = (U_a^(l) S_ab V_b^(l)*)^* = V_b^(l) S_ab^* U_a^(l)*, so A^*
  * has row bases V (translations W), column bases U (translations R), cores
  * S'_ba = S_ab^* and leaf blocks D_i^*. hss_matvec_op runs Fig. 5 right on
  * those generators (trans = 1): U <-> V and R <-> W exchanged here, the
  * transposed cores in hss_couple, D_i^* in hss_leaf_out. */
-static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, int32_t k,
+static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
                          const double* D, const double* U, const double* V,
                          const double* R, const double* W, const double* B,
                          const double* X, int32_t m, double* Y, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, k, D, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+  if (hss_setup(&s, n, p, c, ranks, D, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
       Y == NULL) {
     hss_teardown(&s);
     return -1;
   }
   s.trans = trans;
   hss_upsweep(&s);
-  if (k > 0) {
-    for (int32_t l = 1; l <= p; ++l) { /* Step 2, all levels incl. the leaves (G1) */
-      int64_t pairs = (int64_t)1 << (l - 1);
-#pragma omp parallel for schedule(static) if (pairs * 2 * k * k * m > OMP_MIN_WORK)
-      for (int64_t q = 0; q < pairs; ++q) {
-        hss_couple(&s, l, q, 0);
-        hss_couple(&s, l, q, 1);
-      }
-    }
-    for (int32_t l = 1; l <= p - 1; ++l) { /* Step 3, top to bottom */
-      int64_t cnt = (int64_t)1 << l;
-#pragma omp parallel for schedule(static) if (cnt * 2 * k * k * m > OMP_MIN_WORK)
-      for (int64_t i = 0; i < cnt; ++i) {
-        hss_down(&s, l, i, 0);
-        hss_down(&s, l, i, 1);
-      }
-    }
-  }
+  hss_couple_down_all(&s);
   int64_t nl = (int64_t)1 << p;
 #pragma omp parallel for schedule(dynamic, 1) if (n * m * 8 > OMP_MIN_WORK)
   for (int64_t i = 0; i < nl; ++i)
@@ -537,13 +585,13 @@ static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, int32_t k,
   return 0;
 }
 
-static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, int32_t k,
+static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
                                 const double* Dsel, const double* U, const double* V,
                                 const double* R, const double* W, const double* B,
                                 const double* X, int32_t m,
                                 const int64_t* leaves, int64_t nleaves, double* Yout, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, k, NULL, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+  if (hss_setup(&s, n, p, c, ranks, NULL, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
       Yout == NULL || leaves == NULL) {
     hss_teardown(&s);
     return -1;
@@ -554,16 +602,14 @@ static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, int32_t 
   for (int64_t t = 0; t < nleaves; ++t) {
     int64_t L = leaves[t];
     if (L < 0 || L >= nl) { hss_teardown(&s); return -1; }
-    if (k > 0) {
-      /* Step 2 on the path nodes (l, L >> (p-l)), l = 1..p, then Step 3 along it */
-      for (int32_t l = 1; l <= p; ++l) {
-        int64_t node = L >> (p - l);
-        hss_couple(&s, l, node >> 1, (int)(node & 1));
-      }
-      for (int32_t l = 1; l <= p - 1; ++l) {
-        int64_t node = L >> (p - l), child = L >> (p - l - 1);
-        hss_down(&s, l, node, (int)(child & 1));
-      }
+    /* Step 2 on the path nodes (l, L >> (p-l)), l = 1..p, then Step 3 along it */
+    for (int32_t l = 1; l <= p; ++l) {
+      int64_t node = L >> (p - l);
+      if (s.kl[l] > 0) hss_couple(&s, l, node >> 1, (int)(node & 1));
+    }
+    for (int32_t l = 1; l <= p - 1; ++l) {
+      int64_t node = L >> (p - l), child = L >> (p - l - 1);
+      if (s.kl[l] > 0 && s.kl[l + 1] > 0) hss_down(&s, l, node, (int)(child & 1));
     }
     int64_t rows = c[L] - leaf_lo(c, L);
     hss_leaf_out(&s, L, Dsel + doff, Yout + yoff);
@@ -574,18 +620,48 @@ static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, int32_t 
   return 0;
 }
 
+/* The uniform-rank entry points: ranks k on every level. */
+static int32_t* uniform_ranks(int32_t p, int32_t k) {
+  int32_t* r = (int32_t*)malloc(sizeof(int32_t) * (size_t)(p + 1));
+  if (r)
+    for (int32_t l = 0; l <= p; ++l) r[l] = k;
+  return r;
+}
+
 int oracle_hss_matvec(int64_t n, int32_t p, const int64_t* c, int32_t k,
                       const double* D, const double* U, const double* V,
                       const double* R, const double* W, const double* B,
                       const double* X, int32_t m, double* Y) {
-  return hss_matvec_op(n, p, c, k, D, U, V, R, W, B, X, m, Y, 0);
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  int rc = r ? hss_matvec_op(n, p, c, r, D, U, V, R, W, B, X, m, Y, 0) : -1;
+  free(r);
+  return rc;
 }
 
 int oracle_hss_matvec_t(int64_t n, int32_t p, const int64_t* c, int32_t k,
                         const double* D, const double* U, const double* V,
                         const double* R, const double* W, const double* B,
                         const double* X, int32_t m, double* Y) {
-  return hss_matvec_op(n, p, c, k, D, U, V, R, W, B, X, m, Y, 1);
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  int rc = r ? hss_matvec_op(n, p, c, r, D, U, V, R, W, B, X, m, Y, 1) : -1;
+  free(r);
+  return rc;
+}
+
+int oracle_hss_matvec_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                             const double* D, const double* U, const double* V,
+                             const double* R, const double* W, const double* B,
+                             const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 0);
+}
+
+int oracle_hss_matvec_ranked_t(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                               const double* D, const double* U, const double* V,
+                               const double* R, const double* W, const double* B,
+                               const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 1);
 }
 
 int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
@@ -593,7 +669,11 @@ int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
                              const double* R, const double* W, const double* B,
                              const double* X, int32_t m,
                              const int64_t* leaves, int64_t nleaves, double* Yout) {
-  return hss_matvec_leaves_op(n, p, c, k, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 0);
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  int rc = r ? hss_matvec_leaves_op(n, p, c, r, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 0) : -1;
+  free(r);
+  return rc;
 }
 
 int oracle_hss_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
@@ -601,59 +681,65 @@ int oracle_hss_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k
                                const double* R, const double* W, const double* B,
                                const double* X, int32_t m,
                                const int64_t* leaves, int64_t nleaves, double* Yout) {
-  return hss_matvec_leaves_op(n, p, c, k, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 1);
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  int rc = r ? hss_matvec_leaves_op(n, p, c, r, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 1) : -1;
+  free(r);
+  return rc;
 }
 
-int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
-                     const double* D, const double* U, const double* V,
-                     const double* R, const double* W, const double* B, double* A) {
+int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                            const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B, double* A) {
   /* Definition: diagonal leaf blocks D_i; every sibling block
    * A(I_a^l, I_b^l) = U_a^(l) S_ab^(l) (V_b^(l))^T, with the bases
    * of the upper levels rebuilt from the leaf bases by eq. (3):
    *   U_i^(l) = blockdiag(U_{2i}^(l+1), U_{2i+1}^(l+1)) R_{U,i}^(l), same for V
-   * with R_{V,i}^(l) = W[node]. */
-  if (check_tree(n, p, c) || k < 0 || A == NULL) return -1;
-  int64_t* d_off = leaf_block_offsets(c, p);
-  if (!d_off) return -1;
+   * with R_{V,i}^(l) = W[node]; k_l columns on level l. */
+  hss_ctx s;
+  if (A == NULL || hss_setup(&s, n, p, c, ranks, D, U, V, R, W, B, NULL, 1)) { hss_teardown(&s); return -1; }
   memset(A, 0, sizeof(double) * (size_t)(n * n));
   int64_t nl = (int64_t)1 << p;
   for (int64_t i = 0; i < nl; ++i) {
-    int64_t lo = leaf_lo(c, i), s = c[i] - lo;
-    for (int64_t r = 0; r < s; ++r)
-      for (int64_t q = 0; q < s; ++q) A[(lo + r) * n + lo + q] = D[d_off[i] + r * s + q];
+    int64_t lo = leaf_lo(c, i), sz = c[i] - lo;
+    for (int64_t r = 0; r < sz; ++r)
+      for (int64_t q = 0; q < sz; ++q) A[(lo + r) * n + lo + q] = D[s.d_off[i] + r * sz + q];
   }
-  free(d_off);
-  if (p == 0 || k == 0) return 0;
-  /* Ub[l], Vb[l]: n x k, rows I_i^l hold U_i^(l) (resp. V_i^(l)) */
-  double* Ub = (double*)malloc(sizeof(double) * (size_t)((p + 1) * n * k));
-  double* Vb = (double*)malloc(sizeof(double) * (size_t)((p + 1) * n * k));
-  if (!Ub || !Vb) { free(Ub); free(Vb); return -1; }
-  memcpy(Ub + (size_t)p * n * k, U, sizeof(double) * (size_t)(n * k));
-  memcpy(Vb + (size_t)p * n * k, V, sizeof(double) * (size_t)(n * k));
+  if (p == 0) { hss_teardown(&s); return 0; }
+  /* Ub, Vb: level l (1..p) block of n x k_l at nk_off[l]; rows I_i^l hold U_i^(l) */
+  int64_t* nk_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
+  for (int32_t l = 1; l <= p; ++l) nk_off[l + 1] = nk_off[l] + n * s.kl[l];
+  double* Ub = (double*)malloc(sizeof(double) * (size_t)(nk_off[p + 1] + 1));
+  double* Vb = (double*)malloc(sizeof(double) * (size_t)(nk_off[p + 1] + 1));
+  if (!Ub || !Vb || !nk_off) { free(Ub); free(Vb); free(nk_off); hss_teardown(&s); return -1; }
+  memcpy(Ub + nk_off[p], U, sizeof(double) * (size_t)(n * s.kl[p]));
+  memcpy(Vb + nk_off[p], V, sizeof(double) * (size_t)(n * s.kl[p]));
   for (int32_t l = p - 1; l >= 1; --l) {
+    int32_t k = s.kl[l], kc = s.kl[l + 1];
     for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
       for (int ch = 0; ch < 2; ++ch) {
         int64_t clo, chi;
         node_range(c, p, l + 1, 2 * i + ch, &clo, &chi);
-        const double* Rh = R + coef_index(l, i) * 2 * k * k + ch * k * k; /* Rl or Rr */
-        const double* Wh = W + coef_index(l, i) * 2 * k * k + ch * k * k; /* Wl or Wr */
+        const double* Rh = R + s.rw_off[l] + i * 2 * kc * k + ch * kc * k; /* Rl or Rr: k_{l+1} x k_l */
+        const double* Wh = W + s.rw_off[l] + i * 2 * kc * k + ch * kc * k;
         for (int64_t r = clo; r < chi; ++r)
           for (int32_t a = 0; a < k; ++a) {
             double su = 0.0, sv = 0.0;
-            for (int32_t e = 0; e < k; ++e) {
-              su += Ub[((size_t)(l + 1) * n + r) * k + e] * Rh[e * k + a];
-              sv += Vb[((size_t)(l + 1) * n + r) * k + e] * Wh[e * k + a];
+            for (int32_t e = 0; e < kc; ++e) {
+              su += Ub[nk_off[l + 1] + r * kc + e] * Rh[e * k + a];
+              sv += Vb[nk_off[l + 1] + r * kc + e] * Wh[e * k + a];
             }
-            Ub[((size_t)l * n + r) * k + a] = su;
-            Vb[((size_t)l * n + r) * k + a] = sv;
+            Ub[nk_off[l] + r * k + a] = su;
+            Vb[nk_off[l] + r * k + a] = sv;
           }
       }
     }
   }
-  double* tmp = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)(kMaxOr1(s.kl, p) + 1));
   for (int32_t l = 1; l <= p; ++l) {
+    int32_t k = s.kl[l];
     for (int64_t q = 0; q < ((int64_t)1 << (l - 1)); ++q) {
-      const double* Bn = B + (((int64_t)1 << (l - 1)) - 1 + q) * 2 * k * k;
+      const double* Bn = B + s.b_off[l] + q * 2 * k * k;
       for (int w = 0; w < 2; ++w) { /* w=0: A(I_2q, I_2q+1) = U S12 V^T; w=1: A(I_2q+1, I_2q) */
         int64_t a = 2 * q + w, b = 2 * q + 1 - w, alo, ahi, blo, bhi;
         node_range(c, p, l, a, &alo, &ahi);
@@ -662,23 +748,38 @@ int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
         for (int64_t r = alo; r < ahi; ++r) {
           for (int32_t e = 0; e < k; ++e) { /* (U_a S)[r][e] */
             double su = 0.0;
-            for (int32_t f = 0; f < k; ++f) su += Ub[((size_t)l * n + r) * k + f] * S[f * k + e];
+            for (int32_t f = 0; f < k; ++f) su += Ub[nk_off[l] + r * k + f] * S[f * k + e];
             tmp[e] = su;
           }
           for (int64_t q2 = blo; q2 < bhi; ++q2) {
             double sv = 0.0;
-            for (int32_t e = 0; e < k; ++e) sv += tmp[e] * Vb[((size_t)l * n + q2) * k + e];
+            for (int32_t e = 0; e < k; ++e) sv += tmp[e] * Vb[nk_off[l] + q2 * k + e];
             A[r * n + q2] = sv;
           }
         }
       }
     }
   }
-  free(tmp); free(Ub); free(Vb);
+  free(tmp); free(Ub); free(Vb); free(nk_off);
+  hss_teardown(&s);
   return 0;
 }
 
+int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
+                     const double* D, const double* U, const double* V,
+                     const double* R, const double* W, const double* B, double* A) {
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  int rc = r ? oracle_hss_dense_ranked(n, p, c, r, D, U, V, R, W, B, A) : -1;
+  free(r);
+  return rc;
+}
+
 /* --------------------------------------------------- hss2hodlr (f3) -- */
+
+/* node (l, i), l >= 1, of the uniform-rank level-major arrays */
+static int64_t coef_index(int32_t l, int64_t i) { return ((int64_t)1 << l) - 2 + i; }
+
 /* P:522 ("hss2hodlr ... by simply building explicit low-rank factorizations",
  * S:514-522): the level-l bases of eq. (3),
  *   U_i^(l) = blockdiag(U_{2i}^(l+1), U_{2i+1}^(l+1)) R_{U,i}^(l), V likewise with
@@ -790,7 +891,7 @@ static int hodlr_apply(const void* ctx, int trans, const double* x, double* y) {
 
 static int hss_apply(const void* ctx, int trans, const double* x, double* y) {
   const op_ctx* o = (const op_ctx*)ctx;
-  return hss_matvec_op(o->n, o->p, o->c, o->k, o->D, o->U, o->V, o->R, o->W, o->B, x, 1, y, trans);
+  return hss_matvec_op(o->n, o->p, o->c, o->ranks, o->D, o->U, o->V, o->R, o->W, o->B, x, 1, y, trans);
 }
 
 int oracle_hodlr_norm2_est(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
@@ -804,8 +905,13 @@ int oracle_hss_norm2_est(int64_t n, int32_t p, const int64_t* c, int32_t k,
                          const double* D, const double* U, const double* V,
                          const double* R, const double* W, const double* B,
                          const double* x0, int32_t iters, double* est) {
-  op_ctx o = {n, p, c, NULL, k, D, U, V, R, W, B};
-  return power_norm2(n, x0, iters, hss_apply, &o, est);
+  if (k < 0) return -1;
+  int32_t* r = uniform_ranks(p, k);
+  if (!r) return -1;
+  op_ctx o = {n, p, c, r, k, D, U, V, R, W, B};
+  int rc = power_norm2(n, x0, iters, hss_apply, &o, est);
+  free(r);
+  return rc;
 }
 
 int oracle_dense_matvec(int64_t n, const double* A, const double* X, int32_t m, double* Y) {

@@ -131,6 +131,23 @@ int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
                      const double* D, const double* U, const double* V,
                      const double* R, const double* W, const double* B, double* A);
 
+/* Per-level HSS ranks: k_l = ranks[l-1] on the nodes of level l = 1..p.
+ * U, V [n][k_p]; R, W node (l,i) [2k_{l+1}][k_l] at offset
+ * sum_{l'<l} 2^l' 2 k_{l'+1} k_l' + i 2 k_{l+1} k_l; B for the level-l siblings of
+ * parent (l-1, q) [2][k_l][k_l] at sum_{l'<l} 2^(l'-1) 2 k_l'^2 + q 2 k_l^2. Equal
+ * ranks give the uniform layout above (and the same result, bit for bit). */
+int oracle_hss_matvec_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                             const double* D, const double* U, const double* V,
+                             const double* R, const double* W, const double* B,
+                             const double* X, int32_t m, double* Y);
+int oracle_hss_matvec_ranked_t(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                               const double* D, const double* U, const double* V,
+                               const double* R, const double* W, const double* B,
+                               const double* X, int32_t m, double* Y);
+int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                            const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B, double* A);
+
 /* Plain dense product Y = A X (n x n times n x m), sums in natural order. */
 int oracle_dense_matvec(int64_t n, const double* A, const double* X, int32_t m, double* Y);
 

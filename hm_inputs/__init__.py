@@ -277,6 +277,36 @@ def hss_inverse_laplacian(n: int, levels: int) -> Hss:
                B.reshape(-1))
 
 
+def hss_random_ranked(n: int, levels: int, ranks: Sequence[int], seed: int = MASTER_SEED, cid: int = 0):
+    """Random HSS generators with per-level ranks k_l = ranks[l-1] (the layout of
+    include/hm.h hss_matvec_ranked): leaf U_i, V_i (b x k_p) and each node's R, W
+    (2k_{l+1} x k_l) are thin-QR Q factors of Gaussian blocks (orthonormal rows when
+    2k_{l+1} < k_l); cores N(0,1); D_i N(0,1)/sqrt(b). Returns an Hss with k = k_p and
+    the flat level-major R, W, B of the ranked layout."""
+    b = n >> levels
+    assert b << levels == n and levels >= 1
+    k = [int(r) for r in ranks]
+    nl = 1 << levels
+    D = np.empty((nl, b, b), dtype=np.float64)
+    for i in range(nl):
+        D[i] = normal((b, b), seed, cid, AID["D"], i) / np.sqrt(b)
+    kp = k[-1]
+    U = _orth_blocks(normal((nl, b, kp), seed, cid, AID["U"], 0)).reshape(-1) if kp else np.zeros(0)
+    V = _orth_blocks(normal((nl, b, kp), seed, cid, AID["V"], 0)).reshape(-1) if kp else np.zeros(0)
+    Rs, Ws, Bs = [], [], []
+    for l in range(1, levels):
+        kc, kl = k[l], k[l - 1]
+        if kc and kl:
+            Rs.append(_orth_blocks(normal((1 << l, 2 * kc, kl), seed, cid, AID["R"], l)).reshape(-1))
+            Ws.append(_orth_blocks(normal((1 << l, 2 * kc, kl), seed, cid, AID["W"], l)).reshape(-1))
+    for l in range(1, levels + 1):
+        kl = k[l - 1]
+        if kl:
+            Bs.append(normal((1 << (l - 1)) * 2 * kl * kl, seed, cid, AID["B"], l))
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0)  # noqa: E731
+    return Hss(n, levels, b, kp, D.reshape(-1), U, V, cat(Rs), cat(Ws), cat(Bs))
+
+
 def rhs(n: int, m: int, seed: int = MASTER_SEED, cid: int = 0, rows: Optional[Tuple[int, int]] = None,
         slab: int = 1 << 16) -> np.ndarray:
     """X iid N(0,1), [n][m], drawn in slabs of ``slab`` rows (shardable)."""

@@ -165,6 +165,28 @@ hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k,
                             const double* X_host, int32_t nrhs, double* Y_host,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* -------------------------------- HSS with per-level ranks (§8(f) f4) --
+ * the bases and translation operators need not have k columns on every
+ * level, "as long as the dimensions are compatible". Level l = 1..p has rank
+ * k_l = ranks[l-1] (0..64; 0 = no off-diagonal coupling through that level):
+ *   U, V [n][k_p]              leaf bases.
+ *   R, W                       node (l, i), l = 1..p-1: [2k_{l+1}][k_l] at offset
+ *                              sum_{l'<l} 2^l' 2 k_{l'+1} k_l' + i 2 k_{l+1} k_l
+ *                              (rows 0..k_{l+1}-1: the left child).
+ *   B                          cores of the level-l siblings 2q, 2q+1, stored at
+ *                              the parent (l-1, q): [2][k_l][k_l] at offset
+ *                              sum_{l'<l} 2^(l'-1) 2 k_l'^2 + q 2 k_l^2 ([0] = B12).
+ *   D, X, Y                    as for hss_matvec. op = 0: Y = A X; 1: A^T X.
+ * Equal ranks are exactly the layout of hss_matvec and run its kernels.
+ * Otherwise Steps 1 and 4 run the leaf kernels with k_p and the tree levels one
+ * launch per level. Same errors / determinism as hss_matvec. */
+hm_status hm_hss_ranked_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, size_t* bytes);
+hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t op,
+                            const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B,
+                            const double* X, int32_t nrhs, double* Y,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* ----------------------------------- general cluster trees (§8(f) f4) --
  * The cluster tree of depth `levels` = p given by its leaf endpoint vector
  * c (Def. 2.1): c is a HOST array of 2^p int64 values,
@@ -265,8 +287,7 @@ hm_status hss_to_hodlr(const hm_tree* tree, int32_t k,
  *   HSS    x of node (q, r) (Step 1 up to the subtree root, k nrhs doubles);
  *          every rank runs the replicated top tree (levels 1..q), then its
  *          subtree's coupling / downsweep from y of node (q, r), and Step 4.
- * Results equal the single-GPU product up to the order of the top-level sums
- * (HSS: bitwise, the top tree runs the same kernels on the same blocks). */
+ * Results equal the single-GPU product up to the order of the top-level sums. */
 
 /* ---- communicator: NCCL (loaded at run time from libnccl.so.2), one per
  * process, bound to the CUDA device current at hm_comm_init. Its allgather runs

@@ -36,7 +36,8 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hss_to_hodlr", "hm_hodlr_general_workspace_bytes", "hodlr_matvec_general",
            "hm_hss_general_workspace_bytes", "hss_matvec_general",
            "hm_comm_unique_id", "hm_comm_init", "hm_comm_destroy", "hm_comm_size", "hm_comm_allgather",
-           "hm_hodlr_dist_workspace_bytes", "hodlr_matvec_dist", "hm_hss_dist_workspace_bytes", "hss_matvec_dist")
+           "hm_hodlr_dist_workspace_bytes", "hodlr_matvec_dist", "hm_hss_dist_workspace_bytes", "hss_matvec_dist",
+           "hm_hss_ranked_workspace_bytes", "hss_matvec_ranked")
 
 
 class HmError(RuntimeError):
@@ -86,6 +87,8 @@ def load() -> ctypes.CDLL:
         "hodlr_matvec_general": [i64, i32, P, P, i32, P, P, P, P, i32, P, P, sz, P],
         "hm_hss_general_workspace_bytes": [i64, i32, P, i32, i32, ctypes.POINTER(sz)],
         "hss_matvec_general": [i64, i32, P, i32, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_hss_ranked_workspace_bytes": [T, P, i32, ctypes.POINTER(sz)],
+        "hss_matvec_ranked": [T, P, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hm_profile_enable": [i32],
         "hm_profile_collect": [ctypes.POINTER(hm_launch_record), i32, ctypes.POINTER(i32)],
     }
@@ -449,4 +452,47 @@ def hss_matvec_general(n, levels, c, k, D, U, V, R, W, B, X, op=0, Y=None, works
     _check(load().hss_matvec_general(int(n), int(levels), c.ctypes.data, int(k), int(op), _ptr(D), _ptr(U), _ptr(V),
                                      _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
                                      _stream(stream)))
+    return Y
+
+
+# ------------------------------------------------ HSS, per-level ranks (f4) --
+
+def hss_ranked_sizes(n, levels, ranks):
+    """Generator sizes (doubles) of an HSS matrix with per-level ranks (include/hm.h
+    hss_matvec_ranked): U/V, R/W, B."""
+    k = [int(r) for r in ranks]
+    kp = k[-1] if levels else 0
+    rw = sum((1 << l) * 2 * k[l] * k[l - 1] for l in range(1, levels))
+    b = sum((1 << (l - 1)) * 2 * k[l - 1] ** 2 for l in range(1, levels + 1))
+    return n * kp, rw, b
+
+
+def hm_hss_ranked_workspace_bytes(n, levels, leaf, ranks, nrhs) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hss_ranked_workspace_bytes(ctypes.byref(t), _ranks(ranks, levels), int(nrhs),
+                                                ctypes.byref(out)))
+    return out.value
+
+
+def hss_matvec_ranked(n, levels, leaf, ranks, D, U, V, R, W, B, X, op=0, Y=None, workspace=None, stream=None):
+    """Y = A X (op 0) or A^T X (op 1) for an HSS matrix with per-level ranks k_l = ranks[l-1]
+    (include/hm.h hss_matvec_ranked)."""
+    import torch
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    ws = _workspace(hm_hss_ranked_workspace_bytes(n, levels, leaf, ranks, nrhs), workspace, X.device)
+    _xy(X, Y, n)
+    nuv, nrw, nb = hss_ranked_sizes(n, levels, ranks)
+    _numel_at_least(D, n * leaf, "D")
+    for t_, c_, nm in ((U, nuv, "U"), (V, nuv, "V"), (R, nrw, "R"), (W, nrw, "W"), (B, nb, "B")):
+        _numel_at_least(t_, c_, nm)
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_matvec_ranked(ctypes.byref(t), _ranks(ranks, levels), int(op), _ptr(D), _ptr(U), _ptr(V),
+                                    _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
+                                    _stream(stream)))
     return Y

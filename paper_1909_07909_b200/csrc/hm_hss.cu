@@ -464,6 +464,140 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
   return HM_OK;
 }
 
+// ---- per-level ranks ----
+//
+// k_l = ranks[l-1] columns on level l: U, V [n][k_p]; R, W of node (l, i)
+// [2k_{l+1}][k_l]; the cores of the level-l siblings [2][k_l][k_l] (include/hm.h
+// hss_matvec_ranked has the offsets). Step 1 and Step 4 run the uniform leaf
+// kernels with k = k_p; the tree levels run hss_up_ranked / hss_down_ranked.
+// Equal ranks take hss_run (the tuned tree kernels).
+struct RankedPlan {
+  HssPlan P;  // leaf-level paths for k_p
+  int32_t kl[hm::kMaxLevels + 2];
+  int64_t cf[hm::kMaxLevels + 2], rw[hm::kMaxLevels + 2], bo[hm::kMaxLevels + 2];
+  size_t off_xh, off_yh, total;
+  bool uniform;
+};
+
+hm_status hss_ranked_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, RankedPlan* Q) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  memset(Q, 0, sizeof *Q);
+  const int p = tree->levels;
+  if (p > 0 && !ranks) return fail(HM_ERR_INVALID_ARG, "ranks is NULL");
+  if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
+  Q->uniform = true;
+  for (int l = 1; l <= p; ++l) {
+    const int k = ranks[l - 1];
+    if (k < 0) return fail(HM_ERR_INVALID_ARG, "ranks[%d] = %d < 0", l - 1, k);
+    if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
+    Q->kl[l] = k;
+    Q->uniform = Q->uniform && k == ranks[0];
+  }
+  const int kp = p > 0 ? Q->kl[p] : 0;
+  if ((st = hss_plan_ex(tree->n, tree->leaf, p, 0, kp, nrhs, 0, &Q->P))) return st;
+  for (int l = 1; l <= p; ++l) {
+    Q->cf[l + 1] = Q->cf[l] + ((int64_t)1 << l) * Q->kl[l] * nrhs;
+    Q->bo[l + 1] = Q->bo[l] + ((int64_t)1 << (l - 1)) * 2 * Q->kl[l] * Q->kl[l];
+    if (l <= p - 1) Q->rw[l + 1] = Q->rw[l] + ((int64_t)1 << l) * 2 * Q->kl[l + 1] * Q->kl[l];
+  }
+  size_t off = 0;
+  Q->off_xh = off;
+  off = align_up(off + sizeof(double) * (size_t)Q->cf[p + 1]);
+  Q->off_yh = off;
+  off = align_up(off + sizeof(double) * (size_t)Q->cf[p + 1]);
+  Q->total = std::max<size_t>(off, kAlign);
+  if (Q->uniform) {  // the tuned path's own workspace
+    HssPlan U;
+    if ((st = hss_plan(tree, p > 0 ? ranks[0] : 0, nrhs, 0, &U))) return st;
+    Q->total = std::max(Q->total, U.total);
+  }
+  return HM_OK;
+}
+
+hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, const double* D, const double* U,
+                         const double* V, const double* R, const double* W, const double* B, const double* X,
+                         int32_t nrhs, double* Y, void* ws, size_t ws_bytes, cudaStream_t s) {
+  RankedPlan Q;
+  hm_status st = hss_ranked_plan(tree, ranks, nrhs, &Q);
+  if (st) return st;
+  if (Q.uniform)
+    return hss_run(tree, tree->levels > 0 ? ranks[0] : 0, D, U, V, R, W, B, X, nrhs, Y, ws, ws_bytes, s, 0, op);
+  const HssPlan& P = Q.P;
+  const int p = P.p;
+  if (!D || !X || !Y) return fail(HM_ERR_INVALID_ARG, "NULL D / X / Y pointer");
+  if (!aligned16(D) || !aligned16(X) || !aligned16(Y)) return fail(HM_ERR_INVALID_ARG, "D, X, Y must be 16-byte aligned");
+  if (!ws || ws_bytes < Q.total || !aligned16(ws))
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu (or misaligned)", ws_bytes, Q.total);
+  const size_t xy = sizeof(double) * (size_t)(P.n * nrhs);
+  if (overlap(X, xy, Y, xy)) return fail(HM_ERR_INVALID_ARG, "X and Y overlap");
+  bool any = false, any_t = false, any_b = false;
+  for (int l = 1; l <= p; ++l) {
+    any = any || Q.kl[l] > 0;
+    any_b = any_b || Q.kl[l] > 0;
+    if (l <= p - 1) any_t = any_t || (Q.kl[l] > 0 && Q.kl[l + 1] > 0);
+  }
+  if ((Q.kl[p] > 0 && p > 0 && (!U || !V)) || (any_b && !B) || (any_t && (!R || !W)))
+    return fail(HM_ERR_INVALID_ARG, "NULL generator pointer");
+  if (op) {  // A^T: U <-> V, R <-> W, transposed cores, D_i^T
+    std::swap(U, V);
+    std::swap(R, W);
+  }
+  char* w = static_cast<char*>(ws);
+  double* xh = reinterpret_cast<double*>(w + Q.off_xh);
+  double* yh = reinterpret_cast<double*>(w + Q.off_yh);
+  const int kp = p > 0 ? Q.kl[p] : 0;
+  g_launches = 0;
+  prof_new_call();
+  auto grid_for = [](int64_t total) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + hm::kThreads - 1) / hm::kThreads, 148 * 16));
+  };
+  if (any) {
+    // Step 1: x of the leaves, V_i^T X(I_i) with k_p columns (the uniform leaf-level kernels)
+    if (kp > 0) {
+      double* xleaf = xh + Q.cf[p];
+      if (P.vt == VtPath::kMma) {
+        hm::BatchedVtParams bp{V, P.b * kp, X, P.b * nrhs, xleaf, (int64_t)kp * nrhs, (int64_t)1 << p, (int32_t)P.b,
+                               nrhs};
+        if ((st = vt_batched_dispatch("vt_batched", bp, kp, P.nt_vt, s))) return st;
+      } else {
+        hm::VtParams vp;
+        memset(&vp, 0, sizeof vp);
+        vp.X = X; vp.n = P.n; vp.m = nrhs; vp.mc = P.mc_vt ? P.mc_vt : vt_mc(P.b, nrhs);
+        vp.tile = P.tile ? P.tile : pick_tile(P.b, p, vp.mc); vp.nlev = 1;
+        vp.lev[0].V = V; vp.lev[0].k = kp; vp.lev[0].s = P.b; vp.lev[0].out = xleaf; vp.lev[0].partial = nullptr;
+        st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, kp, s) : vt_generic(vp, P.n, s);
+        if (st) return st;
+      }
+    }
+    // upsweep l = p-1..1 through W^T (2k_{l+1} x k_l)
+    for (int l = p - 1; l >= 1; --l) {
+      if (Q.kl[l] == 0) continue;
+      const hm::HssRankedLevelParams hp{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l], l, Q.kl[l],
+                                        Q.kl[l + 1], 0, nrhs, 0};
+      const int64_t total = ((int64_t)1 << l) * Q.kl[l] * nrhs;
+      if ((st = launch("hss_up_ranked", s,
+                       [&] { hm::hss_up_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); })))
+        return st;
+    }
+    // cores (levels 1..p, reading G1) + downsweep through R (k_l x k_{l-1} halves)
+    for (int l = 1; l <= p; ++l) {
+      if (Q.kl[l] == 0) continue;
+      const bool from_parent = l >= 2 && Q.kl[l - 1] > 0;
+      const hm::HssRankedLevelParams hp{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
+                                        from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], l, Q.kl[l], 0,
+                                        from_parent ? Q.kl[l - 1] : 0, nrhs, op};
+      const int64_t total = ((int64_t)1 << l) * Q.kl[l] * nrhs;
+      if ((st = launch("hss_down_ranked", s,
+                       [&] { hm::hss_down_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); })))
+        return st;
+    }
+  }
+  // Step 4: Y(I_i) = U_i y_i + D_i X(I_i) (k_p columns)
+  const double* yleaf = (p > 0 && kp > 0) ? yh + Q.cf[p] : nullptr;
+  return hss_leaf_phase(P, D, U, X, Y, yleaf, s, op != 0);
+}
+
 // ---- distributed HSS ----
 
 hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, int32_t flags,
@@ -639,6 +773,24 @@ hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* par
   prof_new_call();
   return hss_dist_end_body(P, d, D_local, U_local, R_sub, B_sub, R_root, W_top, R_top, B_top, X_local, gathered,
                            Y_local, static_cast<char*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+// Per-level ranks.
+hm_status hm_hss_ranked_workspace_bytes(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  RankedPlan Q;
+  hm_status st = hss_ranked_plan(tree, ranks, nrhs, &Q);
+  if (st) return st;
+  *bytes = Q.total;
+  return HM_OK;
+}
+
+hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t op, const double* D, const double* U,
+                            const double* V, const double* R, const double* W, const double* B, const double* X,
+                            int32_t nrhs, double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
+  return hss_ranked_run(tree, ranks, op, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
+                        static_cast<cudaStream_t>(stream));
 }
 
 // One call, NCCL inside: Step 1 + the subtree upsweep to x of

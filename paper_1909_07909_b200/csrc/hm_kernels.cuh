@@ -412,4 +412,64 @@ static __global__ void __launch_bounds__(kThreads) hss_down_level_kernel(const H
   }
 }
 
+// ------------------------------------------------ HSS, per-level ranks --
+// k_l columns on level l (2k_{l+1} x k_l translations, k_l x k_l cores).
+// One launch per level, thread per output entry, fixed-order sums (the generic
+// kernels above with the child / parent ranks separated).
+struct HssRankedLevelParams {
+  const double* G;    // up: W of level l (node i at i 2 kc k); down: R of level l-1 (node q at q 2 k kp)
+  const double* B;    // down: cores of the level-l siblings (pair q at q 2 k^2)
+  const double* xin;  // up: x of level l+1 (kc x m blocks); down: x of level l (k x m)
+  const double* yp;   // down: y of level l-1 (kp x m blocks), NULL on level 1
+  double* out;        // up: x of level l; down: y of level l
+  int32_t l, k, kc, kp, m, bt;
+};
+
+// x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]   (Fig. 5 right)
+static __global__ void __launch_bounds__(kThreads) hss_up_ranked_kernel(const HssRankedLevelParams P) {
+  const int k = P.k, kc = P.kc, m = P.m;
+  const int64_t km = (int64_t)k * m, total = (1ll << P.l) * km;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = e / km;
+    const int o = (int)(e - i * km);
+    const int a = o / m, c = o - a * m;
+    const double* Wn = P.G + i * 2 * kc * k;
+    const double* z0 = P.xin + 2 * i * kc * m;
+    const double* z1 = z0 + (int64_t)kc * m;
+    double acc = 0.0;
+    for (int r = 0; r < kc; ++r) acc = fma(Wn[r * k + a], z0[r * m + c], acc);
+    for (int r = 0; r < kc; ++r) acc = fma(Wn[(kc + r) * k + a], z1[r * m + c], acc);
+    P.out[e] = acc;
+  }
+}
+
+// y_l[2q+w] = S_w x_l[2q+1-w] + R_{l-1,q}[w] y_{l-1}[q]   (reading G1)
+static __global__ void __launch_bounds__(kThreads) hss_down_ranked_kernel(const HssRankedLevelParams P) {
+  const int k = P.k, kp = P.kp, m = P.m;
+  const int64_t km = (int64_t)k * m, total = (1ll << P.l) * km;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kThreads) {
+    const int64_t j = e / km;
+    const int o = (int)(e - j * km);
+    const int a = o / m, c = o - a * m;
+    const int64_t q = j >> 1;
+    const int w = (int)(j & 1);
+    const double* xs = P.xin + (j ^ 1) * km;
+    double yc = 0.0;
+    if (P.bt) {  // S'_w = (S_{1-w})^T (adjoint)
+      const double* S = P.B + (q * 2 + (1 - w)) * k * k;
+      for (int r = 0; r < k; ++r) yc = fma(S[r * k + a], xs[r * m + c], yc);
+    } else {
+      const double* S = P.B + (q * 2 + w) * k * k;
+      for (int r = 0; r < k; ++r) yc = fma(S[a * k + r], xs[r * m + c], yc);
+    }
+    double yd = 0.0;
+    if (P.yp && kp > 0) {
+      const double* Rn = P.G + (q * 2 * k + w * k) * kp;
+      const double* y0 = P.yp + q * (int64_t)kp * m;
+      for (int r = 0; r < kp; ++r) yd = fma(Rn[a * kp + r], y0[r * m + c], yd);
+    }
+    P.out[e] = yc + yd;
+  }
+}
+
 }  // namespace hm

@@ -1,0 +1,78 @@
+"""GPU parity of the HSS product with per-level ranks through
+the C-ABI (hss_matvec_ranked), A and A^T, against the oracle's ranked product
+(pinned in test_oracle_ranked.py). Tolerance: north_star's 1e-12."""
+import numpy as np
+import pytest
+
+import hm_inputs
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def hm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1909_07909_b200 as hm_
+    from paper_1909_07909_b200 import build
+    build.build()
+    hm_.load()
+    return hm_
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda:0")
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+CASES = [
+    # n, levels, ranks (level 1..p), nrhs
+    (1024, 4, [3, 5, 7, 8], 1),
+    (1024, 4, [8, 7, 5, 3], 3),
+    (4096, 6, [16, 16, 8, 8, 4, 4], 16),
+    (8192, 7, [32, 16, 16, 16, 16, 32, 32], 8),       # leaf level k = 32: tuned Step 1 / Step 4 (DMMA)
+    (8192, 7, [4, 8, 0, 8, 16, 16, 16], 1),           # a rank-0 level; m = 1 GEMV leaf kernels
+    (1 << 15, 8, [64, 48, 32, 32, 16, 16, 16, 16], 32),
+    (4096, 6, [5, 5, 5, 5, 5, 5], 2),                 # equal ranks: the tuned uniform path
+    (256, 1, [6], 4),                                 # p = 1
+]
+
+
+@pytest.mark.parametrize("op", [0, 1])
+@pytest.mark.parametrize("n,p,ranks,m", CASES)
+def test_hss_ranked_vs_oracle(hm, n, p, ranks, m, op):
+    s = hm_inputs.hss_random_ranked(n, p, ranks, cid=50)
+    X = hm_inputs.rhs(n, m, cid=50)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    Y = hm.hss_matvec_ranked(n, p, n >> p, ranks, *g, dev(X), op=op)
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec_ranked(n, p, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+def test_hss_ranked_config4_tree(hm):
+    """The config-4 tree (n = 2^22, leaf 128, 15 levels) with ranks growing towards the
+    root (16 at the leaves, 32 on the middle levels, 48 on the top ones), nrhs 32: every row."""
+    cfg = hm_inputs.CONFIGS[4]
+    ranks = [48] * 3 + [32] * 6 + [16] * 6
+    s = hm_inputs.hss_random_ranked(cfg.n, cfg.levels, ranks, cid=51)
+    X = hm_inputs.rhs(cfg.n, 32, cid=51)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    Y = hm.hss_matvec_ranked(cfg.n, cfg.levels, cfg.leaf, ranks, *g, dev(X))
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec_ranked(cfg.n, cfg.levels, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X)
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+def test_hss_ranked_errors(hm):
+    x = torch.zeros(1024, 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(hm.HmError):
+        hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 65, 8], x, x, x, x, x, x, x)
+    with pytest.raises(hm.HmError):
+        hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 7, 8], x, x, x, x, x, x, x, op=2)

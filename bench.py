@@ -894,7 +894,7 @@ def cpu_table(path, reps=3):
         row = {"config": cfg, "nrhs": nrhs, "alg_bytes": nbytes, "gflop": round(flops / 1e9, 3)}
         for th in (1, allc):
             t = timed(f, th)
-            row[f"s_{th}thr"] = round(t, 4)
+            row[f"s_{th}thr"] = float(f"{t:.4g}")
             row[f"GB/s_{th}thr"] = round(nbytes / t / 1e9, 3)
         rows.append(row)
         print(json.dumps(row), flush=True)

@@ -190,7 +190,8 @@ hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* cons
 
 template <int MC>
 hm_status gen_leaf_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * hm::gen_leaf_zs(MC));
+  // Z rows, then the U segments' extended-column tables (pointer + stride per rank column)
+  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * hm::gen_leaf_zs(MC)) + 16 * (size_t)lp.ktot + 16;
   allow_smem(hm::gen_leaf_kernel<MC>, std::max<size_t>(smem, 1));
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + MC - 1) / MC));
   return launch(lp.dtrans ? "gen_leaf_t" : "gen_leaf", s,
@@ -202,7 +203,7 @@ hm_status gen_leaf_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t 
 #endif
 template <int NT, bool DT>
 hm_status gen_leaf_mma_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * (NT * 8 + 4));
+  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * (NT * 8 + 4)) + 16 * (size_t)lp.ktot + 16;
   allow_smem(hm::gen_leaf_mma_kernel<NT, DT>, std::max<size_t>(smem, 1));
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + NT * 8 - 1) / (NT * 8)));
   return launch(DT ? "gen_leaf_mma_t" : "gen_leaf_mma", s,

@@ -27,7 +27,7 @@ namespace hm {
 
 constexpr int64_t kChunkRows = 4096;
 #ifndef HM_GEN_MMA_Q
-#define HM_GEN_MMA_Q 4  // k-steps of A fragments requested per batch in gen_leaf_mma
+#define HM_GEN_MMA_Q 8  // k-steps of A fragments requested per batch in gen_leaf_mma
 #endif
 
 // One chunk: rows [lo, hi) of one node; its partial goes to partial + pidx * k * m.
@@ -317,6 +317,22 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
       off += sg.k;
     }
   }
+  // extended-column tables of the U segments (after Z): base pointer of rank
+  // column a of segment s (row 0) and the segment's row stride k
+  const int kt = P.ktot;
+  const double** ubase = reinterpret_cast<const double**>(Z + (b + kt) * ZS);
+  int* ukst = reinterpret_cast<int*>(ubase + kt);
+  {
+    int e = 0;
+    for (int s2 = 0; s2 < P.nseg; ++s2) {
+      const int k2 = P.seg[s2].k;
+      for (int a = threadIdx.x; a < k2; a += kThreads) {
+        ubase[e + a] = P.seg[s2].A + a;
+        ukst[e + a] = k2;
+      }
+      e += k2;
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Di = P.D + P.doff[leaf];
@@ -373,21 +389,31 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
         for (int c = 0; c < MC; ++c) acc[u][c] = fma(d, z[c], acc[u][c]);
       }
     }
-    int64_t off = b;
-    for (int sgi = 0; sgi < P.nseg; ++sgi) {
-      const LeafSeg sg = P.seg[sgi];
-      for (int a0 = lane; a0 < sg.k; a0 += 32) {
-        double uu[GR];
+    // U segments, flattened: extended column e in [0, ktot) of segment s(e),
+    // rank column a(e) (tables staged above). GR x UJ loads in flight per lane,
+    // as for D, instead of one dependent round trip per segment.
+    for (int e0 = lane; e0 < kt; e0 += 32 * UJ) {
+      double uu[GR][UJ];
 #pragma unroll
-        for (int u = 0; u < GR; ++u) uu[u] = rok[u] ? __ldg(sg.A + (r0 + rw + 8 * u) * sg.k + a0) : 0.0;
+      for (int v = 0; v < UJ; ++v) {
+        const int e = e0 + 32 * v;
+        const bool eok = e < kt;
+        const double* ub = eok ? ubase[e] : nullptr;
+        const int ks = eok ? ukst[e] : 0;
+#pragma unroll
+        for (int u = 0; u < GR; ++u) uu[u][v] = (eok && rok[u]) ? __ldg(ub + (r0 + rw + 8 * u) * ks) : 0.0;
+      }
+#pragma unroll
+      for (int v = 0; v < UJ; ++v) {
+        const int e = e0 + 32 * v;
+        if (e >= kt) break;
         double z[MC];
-        zrow<MC>(z, Z + (off + a0) * ZS);
+        zrow<MC>(z, Z + (b + e) * ZS);
 #pragma unroll
         for (int c = 0; c < MC; ++c)
 #pragma unroll
-          for (int u = 0; u < GR; ++u) acc[u][c] = fma(uu[u], z[c], acc[u][c]);
+          for (int u = 0; u < GR; ++u) acc[u][c] = fma(uu[u][v], z[c], acc[u][c]);
       }
-      off += sg.k;
     }
 #pragma unroll
     for (int u = 0; u < GR; ++u) {
@@ -441,6 +467,20 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
     }
     off += sg.k;
   }
+  const int kt = P.ktot;
+  const double** ubase = reinterpret_cast<const double**>(Z + (b + kt) * ZS);
+  int* ukst = reinterpret_cast<int*>(ubase + kt);
+  {
+    int e = 0;
+    for (int s2 = 0; s2 < P.nseg; ++s2) {
+      const int k2 = P.seg[s2].k;
+      for (int a2 = threadIdx.x; a2 < k2; a2 += kThreads) {
+        ubase[e + a2] = P.seg[s2].A + a2;
+        ukst[e + a2] = k2;
+      }
+      e += k2;
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = lane >> 2, j = lane & 3;
@@ -479,28 +519,25 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, kok ? zr[nt * 8] : 0.0);
     }
-    // U segments: contraction over each segment's k rank columns
-    int64_t zo = b;
-    for (int s = 0; s < P.nseg; ++s) {
-      const LeafSeg sg = P.seg[s];
-      const double* Ar = sg.A + (r0 + (rok ? row : 0)) * sg.k;
-      for (int q0 = 0; q0 < (sg.k + 3) / 4; q0 += Q) {
-        double a[Q];
+    // U segments, flattened over the extended columns kk in [0, ktot) (tables
+    // staged above): Q k-steps of A fragments U_s(kk)[row][a(kk)] requested
+    // before their DMMAs, across segment boundaries
+    const int64_t grow = r0 + (rok ? row : 0);
+    for (int q0 = 0; 4 * q0 < kt; q0 += Q) {
+      double a[Q];
 #pragma unroll
-        for (int u = 0; u < Q; ++u) {
-          const int kk = 4 * (q0 + u) + j;
-          a[u] = (rok && kk < sg.k) ? __ldg(Ar + kk) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < Q; ++u) {
-          const int kk = 4 * (q0 + u) + j;
-          if (4 * (q0 + u) >= sg.k) break;
-          const double* zr = Z + (zo + (kk < sg.k ? kk : 0)) * ZS + i;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < sg.k ? zr[nt * 8] : 0.0);
-        }
+      for (int u = 0; u < Q; ++u) {
+        const int kk = 4 * (q0 + u) + j;
+        a[u] = (rok && kk < kt) ? __ldg(ubase[kk] + grow * ukst[kk]) : 0.0;
       }
-      zo += sg.k;
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        if (4 * (q0 + u) >= kt) break;
+        const int kk = 4 * (q0 + u) + j;
+        const double* zr = Z + (b + (kk < kt ? kk : 0)) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < kt ? zr[nt * 8] : 0.0);
+      }
     }
     if (rok) {
       double* y = P.Y + (r0 + row) * m + c0;

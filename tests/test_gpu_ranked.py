@@ -74,5 +74,6 @@ def test_hss_ranked_errors(hm):
     x = torch.zeros(1024, 1, dtype=torch.float64, device="cuda")
     with pytest.raises(hm.HmError):
         hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 65, 8], x, x, x, x, x, x, x)
-    with pytest.raises(hm.HmError):
-        hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 7, 8], x, x, x, x, x, x, x, op=2)
+    big = torch.zeros(1024 * 64, dtype=torch.float64, device="cuda")
+    with pytest.raises(hm.HmError):  # op must be 0 or 1
+        hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 7, 8], big, big, big, big, big, big, x, op=2)

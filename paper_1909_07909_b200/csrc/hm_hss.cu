@@ -288,6 +288,35 @@ hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int6
 // Step 1 on the subtree: leaf x = V^T X, upsweep to level 1, and (W_root given)
 // the subtree root's x_root = W_root^T [x_{1,0}; x_{1,1}]. A depth-0 subtree is
 // one leaf: its x is the root's, written to x_root.
+// Step 1 fused with the first three upsweep levels (hss_vt_up_kernel): k in
+// {16, 32}, one column chunk (nrhs <= 32), a tree of depth >= 4.
+#ifndef HM_VT_UP
+#define HM_VT_UP 1
+#endif
+bool vt_up_ok(const HssPlan& P) {
+  return HM_VT_UP && P.vt == VtPath::kMma && (P.k == 16 || P.k == 32) && P.m >= 2 && P.m <= 32 && P.p >= 4 &&
+         P.b % 4 == 0;
+}
+
+template <int KT, int NT>
+hm_status vt_up_launch(const hm::VtUpParams& vp, int64_t ctas, cudaStream_t s) {
+  const size_t smem = sizeof(double) * 12 * KT * (NT * 8 + 4);
+  allow_smem(hm::hss_vt_up_kernel<KT, NT>, smem);
+  return launch("hss_vt_up", s, [&] { hm::hss_vt_up_kernel<KT, NT><<<(unsigned)ctas, 256, smem, s>>>(vp); });
+}
+
+hm_status vt_up_dispatch(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
+                         cudaStream_t s) {
+  const hm::VtUpParams vp{V, Xd, W, xh, (int32_t)P.b, P.m, P.p};
+  const int64_t ctas = ((int64_t)1 << P.p) / 8;
+  const int nt = nt_for(P.m, 4);
+#define HM_VU(KT_)                                                 if (P.k == KT_) {                                                  if (nt == 1) return vt_up_launch<KT_, 1>(vp, ctas, s);           if (nt == 2) return vt_up_launch<KT_, 2>(vp, ctas, s);           return vt_up_launch<KT_, 4>(vp, ctas, s);                      }
+  HM_VU(16)
+  HM_VU(32)
+#undef HM_VU
+  return fail(HM_ERR_UNSUPPORTED, "hss_vt_up: no instance for k=%d", P.k);
+}
+
 hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
                        const double* W_root, double* x_root, cudaStream_t stream) {
   const int k = P.k, nrhs = P.m;
@@ -295,8 +324,12 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
   hm_status st;
   double* xleaf = (P.p == 0) ? x_root : xh + (((int64_t)1 << P.p) - 2) * km;
   if (xleaf == nullptr) return HM_OK;
-  const int up_from = P.p - 1;
-  if (P.vt == VtPath::kMma) {
+  int up_from = P.p - 1;
+  if (vt_up_ok(P)) {
+    // Step 1 + upsweep levels p-1, p-2, p-3 in one launch (hss_vt_up_kernel)
+    if ((st = vt_up_dispatch(P, V, W, Xd, xh, stream))) return st;
+    up_from = P.p - 4;
+  } else if (P.vt == VtPath::kMma) {
     hm::BatchedVtParams bp{V, P.b * k, Xd, P.b * nrhs, xleaf, km, (int64_t)1 << P.p, (int32_t)P.b, nrhs};
     if ((st = vt_batched_dispatch("vt_batched", bp, k, P.nt_vt, stream))) return st;
   } else {

@@ -229,4 +229,103 @@ __global__ void __launch_bounds__(256) hss_tree_sweep_kernel(const TreeParams P,
   }
 }
 
+// ---------------------------------------------------- Step 1 + 3 up levels --
+// HSS Step 1 fused with the first three upsweep levels (Fig. 5 right,
+// P:684-694), nrhs <= 8 NT (one column chunk), k = KT in {16, 32}. CTA = the
+// 8 leaves under node (p-3, c): warp w computes x_p[8c + w] = V_i^T X(I_i)
+// (the vt_batched product), keeps it in shared memory and writes it out; then
+// the CTA computes the 4 level-(p-1) nodes, the 2 level-(p-2) nodes and the
+// level-(p-3) node from shared memory (W^T [x_left; x_right], W streamed as
+// 128-bit A fragments), writing every x block once (the downsweep's coupling
+// reads them) and never re-reading one from HBM.
+struct VtUpParams {
+  const double* V;   // [n][KT] leaf bases
+  const double* X;   // [n][m]
+  const double* W;   // translations, heap order (node (l, i) at 2^l - 2 + i)
+  double* xh;        // coefficient blocks, level-major [KT][m]
+  int32_t b, m, p;
+};
+
+// C (16 x 8 NTW) = W_node^T Z for rank columns 16 mg.., columns c0..: A from W
+// ([2KT][KT] row-major), B from the staged children Z (2KT rows, stride zs).
+template <int KT, int NTW>
+__device__ __forceinline__ void vt_up_node(const double* __restrict__ Wn, const double* Z, int zs, int mg, int c0,
+                                           double* out_g, double* out_s, int m, int lane) {
+  constexpr int NQ = KT / 2;  // k-steps of 4 over 2 KT rows
+  constexpr int HQ = NQ < 8 ? NQ : 8;
+  const int i = lane >> 2, j = lane & 3;
+  const double* ap = Wn + mg * 16 + (int64_t)j * KT + 2 * i;
+  const double* bp = Z + j * zs + c0 + i;
+  double acc[2][NTW][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+#pragma unroll
+  for (int q0 = 0; q0 < NQ; q0 += HQ) {
+    double2 a[HQ];
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) a[q] = ldg_stream2(ap + (int64_t)(q0 + q) * 4 * KT);
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt) {
+        const double bf = bp[(q0 + q) * 4 * zs + nt * 8];
+        dmma(acc[0][nt][0], acc[0][nt][1], a[q].x, bf);
+        dmma(acc[1][nt][0], acc[1][nt][1], a[q].y, bf);
+      }
+    }
+  }
+  store_transposed<1, NTW>(acc, out_g + (int64_t)mg * 16 * m, m, c0, m, lane);
+  if (out_s) store_transposed<1, NTW>(acc, out_s + mg * 16 * zs, zs, c0, 1 << 30, lane);
+}
+
+// One up level inside the CTA: N nodes (4, 2, 1) from the 2N child blocks in
+// Zin; 8 / N warps per node split MG rank groups x CS column groups.
+template <int KT, int NT, int N>
+__device__ __forceinline__ void vt_up_level(const VtUpParams& P, int l, int64_t n0, const double* Zin, double* Zout,
+                                            int zs, int warp, int lane) {
+  constexpr int MG = KT / 16, WPN = 8 / N;
+  constexpr int CS0 = WPN / MG >= 1 ? WPN / MG : 1;
+  constexpr int CS = CS0 < NT ? CS0 : NT;
+  constexpr int NTW = NT / CS;
+  const int nd = warp / WPN, sub = warp % WPN;
+  if (sub >= MG * CS) return;
+  const int mg = sub % MG, cs = sub / MG;
+  const int64_t node = n0 + nd;
+  const double* Wn = P.W + (((int64_t)1 << l) - 2 + node) * 2 * KT * KT;
+  double* og = P.xh + (((int64_t)1 << l) - 2 + node) * (int64_t)KT * P.m;
+  vt_up_node<KT, NTW>(Wn, Zin + (int64_t)nd * 2 * KT * zs, zs, mg, cs * NTW * 8, og,
+                      Zout ? Zout + (int64_t)nd * KT * zs : nullptr, P.m, lane);
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256, 2) hss_vt_up_kernel(const VtUpParams P) {
+  extern __shared__ double sm[];
+  constexpr int MPW = KT / 16;
+  constexpr int zs = NT * 8 + 4;  // rows j apart: 4 (mod 8) doubles, conflict-free B fragments
+  double* L = sm;                   // 8 leaf blocks, then the 2 level-(p-2) blocks
+  double* M = sm + 8 * KT * zs;     // the 4 level-(p-1) blocks
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p = P.p, m = P.m;
+  const int64_t leaf = (int64_t)blockIdx.x * 8 + warp;
+  {
+    double acc[2 * MPW][NT][2];
+#pragma unroll
+    for (int t = 0; t < 2 * MPW; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+    warp_transposed_mma<MPW, NT, false, (MPW >= 2 ? 1 : 2)>(acc, P.V + leaf * P.b * KT, KT, P.X + leaf * P.b * m, m,
+                                                            0, m, P.b, lane);
+    store_transposed<MPW, NT>(acc, P.xh + (((int64_t)1 << p) - 2 + leaf) * (int64_t)KT * m, m, 0, m, lane);
+    store_transposed<MPW, NT>(acc, L + warp * KT * zs, zs, 0, 1 << 30, lane);
+  }
+  __syncthreads();
+  vt_up_level<KT, NT, 4>(P, p - 1, (int64_t)blockIdx.x * 4, L, M, zs, warp, lane);
+  __syncthreads();
+  vt_up_level<KT, NT, 2>(P, p - 2, (int64_t)blockIdx.x * 2, M, L, zs, warp, lane);
+  __syncthreads();
+  vt_up_level<KT, NT, 1>(P, p - 3, (int64_t)blockIdx.x, L, nullptr, zs, warp, lane);
+}
+
 }  // namespace hm

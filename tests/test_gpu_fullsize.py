@@ -110,9 +110,10 @@ def config4(hm):
 
 # tree-kernel instances each nrhs selects at k = 32, p = 15 (big levels >= 2^11 nodes
 # run one launch per level, GEMV levels >= 2^13 nodes at nrhs = 1)
+# (nrhs >= 2: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch)
 C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
-           8: {"hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-           32: {"hss_up_pair<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
+           8: {"hss_vt_up", "hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
+           32: {"hss_vt_up", "hss_up_pair<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
@@ -133,7 +134,7 @@ def test_config4_whole_y(hm, config4, m, op):
 
 # ------------------------------------------------- deep HSS tree, p = 14 --
 
-@pytest.fixture(scope="module", params=[16, 32])
+@pytest.fixture(scope="module", params=[16, 32, 64])
 def deep_hss(hm, request):
     k = request.param
     n, p = 1 << 20, 14  # leaf 64: levels 11..13 (up) and 11..14 (down) are big levels
@@ -141,23 +142,30 @@ def deep_hss(hm, request):
     return n, p, k, s, [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
 
 
-DEEP_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
-             2: {"hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-             8: {"hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-             16: {"hss_up_pair<nt2>", "hss_down_pair<nt2>", "hss_tree_sweep<nt2>"}}
+def deep_tree_kernels(k, m):
+    """Tree-kernel instances of the p = 14 tree: GEMV levels at nrhs 1; at nrhs >= 2
+    k = 16 / 32 fuse Step 1 with upsweep levels 13..11 (hss_vt_up, the rest in the
+    sweep), k = 64 runs vt_batched and the pair kernels on levels 13..11."""
+    if m == 1:
+        return {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"}
+    nt = "nt1" if m <= 8 else "nt2"
+    up = {"hss_vt_up"} if k in (16, 32) else {"vt_batched", f"hss_up_pair<{nt}>"}
+    return up | {f"hss_down_pair<{nt}>", f"hss_tree_sweep<{nt}>"}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
 @pytest.mark.parametrize("m", [1, 2, 8, 16])
 def test_deep_hss_whole_y(hm, deep_hss, m, op):
-    """p = 14 (n = 2^20, leaf 64), k in {16, 32}, nrhs in {1, 2, 8, 16}: the GEMV tree
-    kernels (nrhs 1) and the DMMA pair kernels with 1 and 2 column tiles, every row."""
+    """p = 14 (n = 2^20, leaf 64), k in {16, 32, 64}, nrhs in {1, 2, 8, 16}: the GEMV tree
+    kernels (nrhs 1), the fused Step-1 + upsweep kernel and the DMMA pair kernels with 1
+    and 2 column tiles, every row."""
     n, p, k, s, g = deep_hss
     X = hm_inputs.rhs(n, m, cid=40 + m)
     Xd = dev(X)
     fn = hm.hss_matvec if op == "A" else hm.hss_matvec_t
     Y, names = traced(hm, lambda: fn(n, p, 64, k, *g, Xd))
-    assert DEEP_TREE[m] <= names, (DEEP_TREE[m], names)
+    want = deep_tree_kernels(k, m)
+    assert want <= names, (want, names)
     ref = oracle.hss_matvec if op == "A" else oracle.hss_matvec_t
     Yr = ref(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
     assert relerr(Y.cpu().numpy(), Yr) <= TOL

@@ -289,12 +289,15 @@ hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int6
 // the subtree root's x_root = W_root^T [x_{1,0}; x_{1,1}]. A depth-0 subtree is
 // one leaf: its x is the root's, written to x_root.
 // Step 1 fused with the first three upsweep levels (hss_vt_up_kernel): k in
-// {16, 32}, one column chunk (nrhs <= 32), a tree of depth >= 4.
+// {16, 32}, nrhs <= 16, a tree of depth >= 4. Measured on config 4's tree
+// (kbench c4 / c4m8): m = 8: 313 us vs 341 (vt_batched + the three up-pair
+// launches); m = 32: 702 vs 622 — at two CTAs per SM the x-only phases 2-4
+// leave the memory pipe idle, so m = 32 keeps the separate kernels.
 #ifndef HM_VT_UP
 #define HM_VT_UP 1
 #endif
 bool vt_up_ok(const HssPlan& P) {
-  return HM_VT_UP && P.vt == VtPath::kMma && (P.k == 16 || P.k == 32) && P.m >= 2 && P.m <= 32 && P.p >= 4 &&
+  return HM_VT_UP && P.vt == VtPath::kMma && (P.k == 16 || P.k == 32) && P.m >= 2 && P.m <= 16 && P.p >= 4 &&
          P.b % 4 == 0;
 }
 

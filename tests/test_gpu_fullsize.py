@@ -110,10 +110,11 @@ def config4(hm):
 
 # tree-kernel instances each nrhs selects at k = 32, p = 15 (big levels >= 2^11 nodes
 # run one launch per level, GEMV levels >= 2^13 nodes at nrhs = 1)
-# (nrhs >= 2: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch)
+# (nrhs 8: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch;
+# nrhs 32: vt_batched + pair launches on levels 14..11)
 C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
            8: {"hss_vt_up", "hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-           32: {"hss_vt_up", "hss_up_pair<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
+           32: {"vt_batched", "hss_up_pair<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])

@@ -29,7 +29,9 @@ struct GenPlan {
   std::vector<int64_t> cbeg_off;       // per vt level: offset into cbeg
   std::vector<int64_t> chunk0;         // per vt level: first global chunk
   std::vector<int32_t> vt_levels;      // tree level of each vt level (HODLR: 1..p with k > 0; HSS: p)
-  size_t off_tab, off_lo, off_doff, off_chunks, off_cbeg;
+  std::vector<int32_t> vt_order;       // chunk execution order (by first row, then level)
+  std::vector<int32_t> leaf_order;     // leaf execution order (largest first)
+  size_t off_tab, off_lo, off_doff, off_chunks, off_cbeg, off_vorder, off_lorder;
   size_t off_t[hm::kMaxLevels + 1];    // HODLR t_l blocks
   size_t off_part[hm::kMaxLevels + 1]; // partials per vt level
   size_t tab_bytes, total;
@@ -104,6 +106,21 @@ void gen_layout_tables(GenPlan* G, size_t* off) {
   G->off_doff = o; o = align_up(o + sizeof(int64_t) * G->doff.size());
   G->off_chunks = o; o = align_up(o + sizeof(hm::GenChunk) * G->chunks.size());
   G->off_cbeg = o; o = align_up(o + sizeof(int64_t) * G->cbeg.size());
+  // execution orders: chunks of all levels sorted by first row (then level), so the
+  // CTAs reading the same X rows run in the same wave; leaves by decreasing size
+  G->vt_order.resize(G->chunks.size());
+  for (size_t c = 0; c < G->chunks.size(); ++c) G->vt_order[c] = (int32_t)c;
+  std::stable_sort(G->vt_order.begin(), G->vt_order.end(), [&](int32_t a, int32_t b) {
+    return G->chunks[a].lo < G->chunks[b].lo;
+  });
+  const int64_t nl = (int64_t)G->doff.size();
+  G->leaf_order.resize(nl);
+  for (int64_t i = 0; i < nl; ++i) G->leaf_order[i] = (int32_t)i;
+  std::stable_sort(G->leaf_order.begin(), G->leaf_order.end(), [&](int32_t a, int32_t b) {
+    return G->lo[a + 1] - G->lo[a] > G->lo[b + 1] - G->lo[b];
+  });
+  G->off_vorder = o; o = align_up(o + sizeof(int32_t) * G->vt_order.size());
+  G->off_lorder = o; o = align_up(o + sizeof(int32_t) * G->leaf_order.size());
   G->tab_bytes = o;
   *off = align_up(*off + o);
   G->nchunks = (int64_t)G->chunks.size();
@@ -116,6 +133,8 @@ hm_status gen_upload_tables(const GenPlan& G, char* w, cudaStream_t s) {
   memcpy(img.data() + G.off_doff, G.doff.data(), sizeof(int64_t) * G.doff.size());
   memcpy(img.data() + G.off_chunks, G.chunks.data(), sizeof(hm::GenChunk) * G.chunks.size());
   memcpy(img.data() + G.off_cbeg, G.cbeg.data(), sizeof(int64_t) * G.cbeg.size());
+  memcpy(img.data() + G.off_vorder, G.vt_order.data(), sizeof(int32_t) * G.vt_order.size());
+  memcpy(img.data() + G.off_lorder, G.leaf_order.data(), sizeof(int32_t) * G.leaf_order.size());
   if (cudaMemcpyAsync(w + G.off_tab, img.data(), G.tab_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return cuda_check("H2D copy of the tree tables");
   return HM_OK;
@@ -145,6 +164,7 @@ hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* cons
   memset(&vp, 0, sizeof vp);
   vp.X = X;
   vp.chunks = reinterpret_cast<const hm::GenChunk*>(w + G.off_tab + G.off_chunks);
+  vp.order = reinterpret_cast<const int32_t*>(w + G.off_tab + G.off_vorder);
   vp.nchunks = G.nchunks;
   vp.m = G.m;
   vp.mc = G.mc_vt;
@@ -299,6 +319,7 @@ hm_status hodlr_gen_run(int64_t n, int32_t p, const int64_t* c, const int32_t* r
   memset(&lp, 0, sizeof lp);
   lp.D = D; lp.X = X; lp.Y = Y; lp.m = nrhs; lp.mc = G.mc_leaf; lp.dtrans = op ? 1 : 0;
   lp.lo = reinterpret_cast<const int64_t*>(w + G.off_tab + G.off_lo);
+  lp.order = reinterpret_cast<const int32_t*>(w + G.off_tab + G.off_lorder);
   lp.doff = reinterpret_cast<const int64_t*>(w + G.off_tab + G.off_doff);
   off = 0;
   for (int l = 1; l <= p; ++l) {
@@ -403,6 +424,7 @@ hm_status hss_gen_run(int64_t n, int32_t p, const int64_t* c, int32_t k, int op,
   memset(&lp, 0, sizeof lp);
   lp.D = D; lp.X = X; lp.Y = Y; lp.m = nrhs; lp.mc = G.mc_leaf; lp.dtrans = op ? 1 : 0;
   lp.lo = reinterpret_cast<const int64_t*>(w + G.off_tab + G.off_lo);
+  lp.order = reinterpret_cast<const int32_t*>(w + G.off_tab + G.off_lorder);
   lp.doff = reinterpret_cast<const int64_t*>(w + G.off_tab + G.off_doff);
   if (coupled) {
     hm::LeafSeg& sg = lp.seg[lp.nseg++];

@@ -27,7 +27,7 @@ namespace hm {
 
 constexpr int64_t kChunkRows = 4096;
 #ifndef HM_GEN_MMA_Q
-#define HM_GEN_MMA_Q 8  // k-steps of A fragments requested per batch in gen_leaf_mma
+#define HM_GEN_MMA_Q 16  // k-steps of A fragments requested per batch in gen_leaf_mma
 #endif
 
 // One chunk: rows [lo, hi) of one node; its partial goes to partial + pidx * k * m.
@@ -52,6 +52,8 @@ struct GenVtLevel {
 struct GenVtParams {
   const double* X;        // [n][m]
   const GenChunk* chunks; // device table, all levels
+  const int32_t* order;   // execution order: CTA x runs chunk order[x] (all levels' chunks of a row
+                          // range back to back, so X rows are re-read from L2, not HBM)
   int64_t nchunks;
   int32_t m, mc;          // columns, columns per CTA (grid.y)
   int32_t nlev;
@@ -66,7 +68,7 @@ struct GenVtParams {
 // over the lanes sharing a column, fixed-order sum over the 8 warps.
 __global__ void __launch_bounds__(kThreads) gen_vt_gemv_kernel(const GenVtParams P) {
   __shared__ double red[kThreads / 32][64];
-  const GenChunk ch = P.chunks[blockIdx.x];
+  const GenChunk ch = P.chunks[P.order[blockIdx.x]];
   const GenVtLevel lv = P.lev[ch.lev];
   const int k = lv.k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(kThreads) gen_vt_gemv_kernel(const GenVtParams
 // the groups in shared memory. For k * mc > 256 threads loop over outputs.
 __global__ void __launch_bounds__(kThreads) gen_vt_chunk_kernel(const GenVtParams P) {
   __shared__ double red[kThreads];
-  const GenChunk ch = P.chunks[blockIdx.x];
+  const GenChunk ch = P.chunks[P.order[blockIdx.x]];
   const GenVtLevel lv = P.lev[ch.lev];
   const int k = lv.k, m = P.m;
   const int c0 = blockIdx.y * P.mc;
@@ -157,7 +159,7 @@ template <int KT, int NT>
 __global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams P) {
   extern __shared__ double red[];  // [8][KT][8 NT]
   constexpr int MC = NT * 8, MPW = KT / 16;
-  const GenChunk ch = P.chunks[blockIdx.x];
+  const GenChunk ch = P.chunks[P.order[blockIdx.x]];
   const GenVtLevel lv = P.lev[ch.lev];
   const int m = P.m;
   const int c0 = blockIdx.y * MC;
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(kThreads) gen_vt_reduce_kernel(const GenReduce
 // ------------------------------------------------------------------ leaf --
 
 struct GenLeafParams {
+  const int32_t* order;   // CTA x runs leaf order[x]: largest leaves first (shorter tail wave)
   const double* D;        // concatenated |I_i| x |I_i| blocks
   const int64_t* lo;      // device [nleaves + 1]: leaf i rows [lo[i], lo[i+1])
   const int64_t* doff;    // device [nleaves]: offset of D_i
@@ -289,7 +292,7 @@ __device__ __forceinline__ void zrow(double (&z)[MC], const double* zr) {
 template <int MC>
 __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams P) {
   extern __shared__ double smem[];
-  const int64_t leaf = blockIdx.x;
+  const int64_t leaf = P.order[blockIdx.x];
   const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
   if (b == 0) return;  // empty leaf: no rows
   const int c0 = blockIdx.y * MC;
@@ -446,7 +449,7 @@ template <int NT, bool DT>
 __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafParams P) {
   extern __shared__ double smem[];
   constexpr int MC = NT * 8, ZS = MC + 4, Q = HM_GEN_MMA_Q;
-  const int64_t leaf = blockIdx.x;
+  const int64_t leaf = P.order[blockIdx.x];
   const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
   if (b == 0) return;
   const int c0 = blockIdx.y * MC;

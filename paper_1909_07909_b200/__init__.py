@@ -63,6 +63,12 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    if LIB_PATH == os.path.join(_PKG, "libhm.so"):
+        # the in-tree library must carry the hash of the sources on disk (a stale
+        # binary that travelled with a snapshot is rebuilt, never loaded)
+        from . import build as _build
+        if _build.needs_build():
+            _build.build()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_1909_07909_b200.build` "
                           "(the CUDA path has no CPU fallback)")

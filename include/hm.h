@@ -200,8 +200,11 @@ hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t o
  * Limits: largest leaf + sum of ranks <= 20480 (shared-memory staging of a
  * leaf), else HM_ERR_UNSUPPORTED. Errors as for the uniform calls; c not
  * nondecreasing or c[2^p-1] != n is HM_ERR_INVALID_ARG. The tables derived
- * from c are copied into the workspace with one pageable host-to-device copy
- * per call, so these calls are NOT CUDA-graph capturable. Deterministic.
+ * from c are planned on the host (cached per thread for the last 4 trees) and
+ * copied into the workspace with one asynchronous copy from a pinned staging
+ * buffer (a per-thread ring of 4, a slot reused once its copy has completed):
+ * the call does not synchronise the stream, but it is not CUDA-graph
+ * capturable (the staging buffers are reused). Deterministic.
  * (hodlr_matvec / hodlr_matvec_t route per-level ranks on uniform trees
  * with fewer than 3 levels or leaves not a multiple of 64 here
  * automatically, with the same workspace query.) */

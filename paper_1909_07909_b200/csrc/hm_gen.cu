@@ -126,17 +126,47 @@ void gen_layout_tables(GenPlan* G, size_t* off) {
   G->nchunks = (int64_t)G->chunks.size();
 }
 
-hm_status gen_upload_tables(const GenPlan& G, char* w, cudaStream_t s) {
-  thread_local std::vector<char> img;
-  img.assign(G.tab_bytes, 0);
-  memcpy(img.data() + G.off_lo, G.lo.data(), sizeof(int64_t) * G.lo.size());
-  memcpy(img.data() + G.off_doff, G.doff.data(), sizeof(int64_t) * G.doff.size());
-  memcpy(img.data() + G.off_chunks, G.chunks.data(), sizeof(hm::GenChunk) * G.chunks.size());
-  memcpy(img.data() + G.off_cbeg, G.cbeg.data(), sizeof(int64_t) * G.cbeg.size());
-  memcpy(img.data() + G.off_vorder, G.vt_order.data(), sizeof(int32_t) * G.vt_order.size());
-  memcpy(img.data() + G.off_lorder, G.leaf_order.data(), sizeof(int32_t) * G.leaf_order.size());
-  if (cudaMemcpyAsync(w + G.off_tab, img.data(), G.tab_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+// Host image of the tables (built once per cached plan, see gen_cached).
+void gen_build_image(const GenPlan& G, std::vector<char>* img) {
+  img->assign(G.tab_bytes, 0);
+  memcpy(img->data() + G.off_lo, G.lo.data(), sizeof(int64_t) * G.lo.size());
+  memcpy(img->data() + G.off_doff, G.doff.data(), sizeof(int64_t) * G.doff.size());
+  memcpy(img->data() + G.off_chunks, G.chunks.data(), sizeof(hm::GenChunk) * G.chunks.size());
+  memcpy(img->data() + G.off_cbeg, G.cbeg.data(), sizeof(int64_t) * G.cbeg.size());
+  memcpy(img->data() + G.off_vorder, G.vt_order.data(), sizeof(int32_t) * G.vt_order.size());
+  memcpy(img->data() + G.off_lorder, G.leaf_order.data(), sizeof(int32_t) * G.leaf_order.size());
+}
+
+// The tables go to the workspace with one asynchronous copy from a pinned
+// staging buffer (a per-thread ring of 4; a slot is reused only after its
+// previous copy has completed), so the call does not synchronise the stream.
+hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* w, cudaStream_t s) {
+  struct Ring {
+    char* buf[4] = {};
+    size_t cap[4] = {};
+    cudaEvent_t ev[4] = {};
+    bool used[4] = {};
+    int next = 0;
+  };
+  thread_local Ring r;
+  const int slot = r.next;
+  r.next = (r.next + 1) % 4;
+  if (r.used[slot] && cudaEventSynchronize(r.ev[slot]) != cudaSuccess) return cuda_check("table staging event");
+  if (r.cap[slot] < img.size()) {
+    if (r.buf[slot]) cudaFreeHost(r.buf[slot]);
+    r.buf[slot] = nullptr;
+    r.cap[slot] = 0;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&r.buf[slot]), img.size(), cudaHostAllocDefault) != cudaSuccess)
+      return cuda_check("pinned staging buffer for the tree tables");
+    r.cap[slot] = img.size();
+  }
+  if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot], cudaEventDisableTiming) != cudaSuccess)
+    return cuda_check("table staging event");
+  memcpy(r.buf[slot], img.data(), img.size());
+  if (cudaMemcpyAsync(w + off_tab, r.buf[slot], img.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaEventRecord(r.ev[slot], s) != cudaSuccess)
     return cuda_check("H2D copy of the tree tables");
+  r.used[slot] = true;
   return HM_OK;
 }
 
@@ -285,12 +315,56 @@ hm_status hodlr_gen_plan(int64_t n, int32_t p, const int64_t* c, const int32_t* 
   return HM_OK;
 }
 
+hm_status hss_gen_plan(int64_t n, int32_t p, const int64_t* c, int32_t k, int32_t nrhs, GenPlan* G, HssPlan* H);
+
+// Per-thread cache of the last few plans (key: the call's tree, ranks and nrhs,
+// compared in full): repeated calls on one tree skip the host-side planning
+// (chunk tables, sorts) and the image build.
+struct GenCached {
+  int kind;  // 0 HODLR, 1 HSS
+  int64_t n;
+  int32_t p, k, nrhs;
+  std::vector<int64_t> c;
+  std::vector<int32_t> ranks;
+  GenPlan G;
+  HssPlan H;
+  std::vector<char> img;
+};
+
+const GenCached* gen_cached(int kind, int64_t n, int32_t p, const int64_t* c, const int32_t* ranks, int32_t k,
+                            int32_t nrhs, hm_status* st) {
+  thread_local std::vector<GenCached> cache;  // most recent first
+  const size_t nl = (p >= 0 && p <= 30) ? ((size_t)1 << p) : 0;
+  const size_t nr = (kind == 0 && p > 0 && ranks) ? (size_t)p : 0;
+  for (size_t e = 0; e < cache.size(); ++e) {
+    const GenCached& g = cache[e];
+    if (g.kind == kind && g.n == n && g.p == p && g.k == k && g.nrhs == nrhs && c && g.c.size() == nl &&
+        memcmp(g.c.data(), c, nl * sizeof(int64_t)) == 0 && g.ranks.size() == nr &&
+        (nr == 0 || memcmp(g.ranks.data(), ranks, nr * sizeof(int32_t)) == 0)) {
+      if (e) std::rotate(cache.begin(), cache.begin() + e, cache.begin() + e + 1);
+      *st = HM_OK;
+      return &cache.front();
+    }
+  }
+  GenCached g;
+  g.kind = kind; g.n = n; g.p = p; g.k = k; g.nrhs = nrhs;
+  *st = kind == 0 ? hodlr_gen_plan(n, p, c, ranks, nrhs, &g.G) : hss_gen_plan(n, p, c, k, nrhs, &g.G, &g.H);
+  if (*st) return nullptr;
+  g.c.assign(c, c + nl);
+  if (nr) g.ranks.assign(ranks, ranks + nr);
+  gen_build_image(g.G, &g.img);
+  cache.insert(cache.begin(), std::move(g));
+  if (cache.size() > 4) cache.pop_back();
+  return &cache.front();
+}
+
 hm_status hodlr_gen_run(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks, int op, const double* D,
                         const double* U, const double* V, const double* X, int32_t nrhs, double* Y, void* ws,
                         size_t ws_bytes, cudaStream_t s) {
-  GenPlan G;
-  hm_status st = hodlr_gen_plan(n, p, c, ranks, nrhs, &G);
+  hm_status st;
+  const GenCached* gc = gen_cached(0, n, p, c, ranks, 0, nrhs, &st);
   if (st) return st;
+  const GenPlan& G = gc->G;
   if (!ws || ws_bytes < G.total) return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, G.total);
   if (!aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
   if (!X || !Y || (!D && G.doff.size() > 0 && n > 0) || (G.ktot > 0 && (!U || !V)))
@@ -301,7 +375,7 @@ hm_status hodlr_gen_run(int64_t n, int32_t p, const int64_t* c, const int32_t* r
   char* w = static_cast<char*>(ws);
   g_launches = 0;
   prof_new_call();
-  if ((st = gen_upload_tables(G, w, s))) return st;
+  if ((st = gen_upload_tables(gc->img, G.off_tab, w, s))) return st;
   std::vector<const double*> Vl;
   std::vector<double*> outl;
   std::vector<int32_t> kl;
@@ -386,10 +460,11 @@ hm_status hss_gen_plan(int64_t n, int32_t p, const int64_t* c, int32_t k, int32_
 hm_status hss_gen_run(int64_t n, int32_t p, const int64_t* c, int32_t k, int op, const double* D, const double* U,
                       const double* V, const double* R, const double* W, const double* B, const double* X,
                       int32_t nrhs, double* Y, void* ws, size_t ws_bytes, cudaStream_t s) {
-  GenPlan G;
-  HssPlan H;
-  hm_status st = hss_gen_plan(n, p, c, k, nrhs, &G, &H);
+  hm_status st;
+  const GenCached* gc = gen_cached(1, n, p, c, nullptr, k, nrhs, &st);
   if (st) return st;
+  const GenPlan& G = gc->G;
+  const HssPlan& H = gc->H;
   if (!ws || ws_bytes < G.total) return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, G.total);
   if (!aligned16(ws)) return fail(HM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
   const bool coupled = k > 0 && p > 0;
@@ -407,7 +482,7 @@ hm_status hss_gen_run(int64_t n, int32_t p, const int64_t* c, int32_t k, int op,
   const int64_t km = (int64_t)k * nrhs;
   g_launches = 0;
   prof_new_call();
-  if ((st = gen_upload_tables(G, w, s))) return st;
+  if ((st = gen_upload_tables(gc->img, G.off_tab, w, s))) return st;
   const double* yleaf = nullptr;
   if (coupled) {
     double* xleaf = xh + (((int64_t)1 << p) - 2) * km;
@@ -436,10 +511,10 @@ hm_status hss_gen_run(int64_t n, int32_t p, const int64_t* c, int32_t k, int op,
 
 hm_status hodlr_gen_workspace(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks, int32_t nrhs,
                               size_t* bytes) {
-  GenPlan G;
-  hm_status st = hodlr_gen_plan(n, p, c, ranks, nrhs, &G);
+  hm_status st;
+  const GenCached* gc = gen_cached(0, n, p, c, ranks, 0, nrhs, &st);
   if (st) return st;
-  *bytes = G.total;
+  *bytes = gc->G.total;
   return HM_OK;
 }
 
@@ -454,11 +529,7 @@ extern "C" {
 hm_status hm_hodlr_general_workspace_bytes(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks,
                                            int32_t nrhs, size_t* bytes) {
   if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
-  GenPlan G;
-  hm_status st = hodlr_gen_plan(n, levels, c, ranks, nrhs, &G);
-  if (st) return st;
-  *bytes = G.total;
-  return HM_OK;
+  return hodlr_gen_workspace(n, levels, c, ranks, nrhs, bytes);
 }
 
 hm_status hodlr_matvec_general(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks, int32_t op,
@@ -472,11 +543,10 @@ hm_status hodlr_matvec_general(int64_t n, int32_t levels, const int64_t* c, cons
 hm_status hm_hss_general_workspace_bytes(int64_t n, int32_t levels, const int64_t* c, int32_t k, int32_t nrhs,
                                          size_t* bytes) {
   if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
-  GenPlan G;
-  HssPlan H;
-  hm_status st = hss_gen_plan(n, levels, c, k, nrhs, &G, &H);
+  hm_status st;
+  const GenCached* gc = gen_cached(1, n, levels, c, nullptr, k, nrhs, &st);
   if (st) return st;
-  *bytes = G.total;
+  *bytes = gc->G.total;
   return HM_OK;
 }
 

@@ -348,6 +348,23 @@ def _graph_us(torch, f, calls=20, replays=20):
         return f"graph capture failed: {type(e).__name__}: {e}"[:200]
 
 
+def _cold_us(torch, f, reps=30):
+    """Device us of ONE call with a cold L2: a 256 MB scratch buffer (> the 126 MB L2)
+    is written before every call; CUDA events around the call only; median."""
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=torch.cuda.current_device())
+    f()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        scratch.fill_(1)
+        a.record()
+        f()
+        b.record()
+    torch.cuda.synchronize()
+    del scratch
+    return round(statistics.median(a.elapsed_time(b) for a, b in ev) * 1e3, 2)
+
+
 def _time_call(torch, f, reps, warm=2):
     """Device ms per call: CUDA events on the current stream around `reps` calls."""
     for _ in range(warm):
@@ -504,6 +521,8 @@ def sweep(torch, device, wl, peak, parity=True):
                      device=device)
     ms = _time_call(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V, X, Y, ws), 200)
     out["c1_us"] = round(ms * 1e3, 2)
+    out["c1_us_cold_l2"] = _cold_us(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U,
+                                                                  h1.V, X, Y, ws))
     out["c1_us_graph"] = _graph_us(torch, lambda: hm.hodlr_matvec(c1.n, c1.levels, c1.leaf, h1.ranks, h1.D, h1.U, h1.V,
                                                                   X, Y, ws))
     if parity:
@@ -519,6 +538,8 @@ def sweep(torch, device, wl, peak, parity=True):
     ms = _time_call(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R, s2.W, s2.B, X,
                                                  Y, ws), 200)
     out["c2_us"] = round(ms * 1e3, 2)
+    out["c2_us_cold_l2"] = _cold_us(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V,
+                                                                s2.R, s2.W, s2.B, X, Y, ws))
     out["c2_us_graph"] = _graph_us(torch, lambda: hm.hss_matvec(c2.n, c2.levels, c2.leaf, c2.k, s2.D, s2.U, s2.V, s2.R,
                                                                 s2.W, s2.B, X, Y, ws))
     if parity:

@@ -129,6 +129,7 @@ hm_status hm_comm_unique_id(void* id_out) {
 }
 
 hm_status hm_comm_init(int32_t nranks, int32_t rank, const void* id, hm_comm** comm_out) {
+  HM_NVTX("hm_comm_init");
   if (!id || !comm_out) return fail(HM_ERR_INVALID_ARG, "NULL id / comm_out");
   *comm_out = nullptr;
   if (nranks < 1 || (nranks & (nranks - 1)) != 0)
@@ -183,6 +184,7 @@ hm_status hm_comm_size(const hm_comm* comm, int32_t* nranks, int32_t* rank) {
 }
 
 hm_status hm_comm_allgather(hm_comm* comm, const double* send, int64_t count, double* recv, void* stream) {
+  HM_NVTX("hm_comm_allgather");
   int32_t P = 0, r = 0;
   hm_status st = comm_check(comm, &P, &r);
   if (st) return st;

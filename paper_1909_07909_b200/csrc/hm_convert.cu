@@ -11,6 +11,7 @@ extern "C" {
 
 hm_status hss_to_hodlr(const hm_tree* tree, int32_t k, const double* U, const double* V, const double* R,
                        const double* W, const double* B, double* Uh, double* Vh, void* stream) {
+  HM_NVTX("hss_to_hodlr");
   hm_status st = check_tree(tree);
   if (st) return st;
   if (k < 0) return fail(HM_ERR_INVALID_ARG, "k = %d < 0", k);

@@ -535,6 +535,7 @@ hm_status hm_hodlr_general_workspace_bytes(int64_t n, int32_t levels, const int6
 hm_status hodlr_matvec_general(int64_t n, int32_t levels, const int64_t* c, const int32_t* ranks, int32_t op,
                                const double* D, const double* U, const double* V, const double* X, int32_t nrhs,
                                double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_general");
   if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
   return hodlr_gen_run(n, levels, c, ranks, op, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
                        static_cast<cudaStream_t>(stream));
@@ -554,6 +555,7 @@ hm_status hss_matvec_general(int64_t n, int32_t levels, const int64_t* c, int32_
                              const double* U, const double* V, const double* R, const double* W, const double* B,
                              const double* X, int32_t nrhs, double* Y, void* workspace, size_t workspace_bytes,
                              void* stream) {
+  HM_NVTX("hss_matvec_general");
   if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
   return hss_gen_run(n, levels, c, k, op, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));

@@ -392,6 +392,7 @@ hm_status hm_hodlr_norm2_workspace_bytes(const hm_tree* tree, const int32_t* ran
 hm_status hodlr_norm2_est(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                           const double* V, const double* x0, int32_t iters, double* est, void* workspace,
                           size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_norm2_est");
   size_t mv = 0;
   hm_status st = hm_hodlr_workspace_bytes(tree, ranks, 1, 0, &mv);
   if (st) return st;
@@ -424,6 +425,7 @@ hm_status hm_hodlr_workspace_bytes(const hm_tree* tree, const int32_t* ranks, in
 hm_status hodlr_matvec(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                        const double* V, const double* X, int32_t nrhs, double* Y, void* workspace,
                        size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec");
   if (hodlr_use_general(tree, ranks, nrhs, 0)) {
     const std::vector<int64_t> c = uniform_endpoints(tree);
     return hodlr_gen_run(tree->n, tree->levels, c.data(), ranks, 0, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
@@ -436,6 +438,7 @@ hm_status hodlr_matvec(const hm_tree* tree, const int32_t* ranks, const double* 
 hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                               const double* V, const double* X_host, int32_t nrhs, double* Y_host,
                               void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_hostio");
   return hodlr_run(tree, ranks, D, U, V, X_host, nrhs, Y_host, workspace, workspace_bytes,
                    static_cast<cudaStream_t>(stream), HM_WS_HOSTIO);
 }
@@ -443,6 +446,7 @@ hm_status hodlr_matvec_hostio(const hm_tree* tree, const int32_t* ranks, const d
 hm_status hodlr_matvec_t(const hm_tree* tree, const int32_t* ranks, const double* D, const double* U,
                          const double* V, const double* X, int32_t nrhs, double* Y, void* workspace,
                          size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_t");
   if (hodlr_use_general(tree, ranks, nrhs, 0)) {
     const std::vector<int64_t> c = uniform_endpoints(tree);
     return hodlr_gen_run(tree->n, tree->levels, c.data(), ranks, 1, D, U, V, X, nrhs, Y, workspace, workspace_bytes,
@@ -468,6 +472,7 @@ hm_status hm_hodlr_dist_sizes(const hm_tree* tree, const int32_t* ranks, int32_t
 hm_status hodlr_matvec_dist_begin(const hm_tree* tree, const int32_t* ranks, const hm_part* part,
                                   const double* V_local, const double* X_local, int32_t nrhs, double* send,
                                   void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_dist_begin");
   HodlrPlan P;
   DistPart d;
   hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
@@ -485,6 +490,7 @@ hm_status hodlr_matvec_dist_local(const hm_tree* tree, const int32_t* ranks, con
                                   const double* D_local, const double* U_local, const double* V_local,
                                   const double* X_local, int32_t nrhs, double* Y_local, void* workspace,
                                   size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_dist_local");
   HodlrPlan P;
   DistPart d;
   hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
@@ -511,6 +517,7 @@ hm_status hodlr_matvec_dist_end(const hm_tree* tree, const int32_t* ranks, const
                                 const double* D_local, const double* U_local, const double* X_local, int32_t nrhs,
                                 const double* gathered, double* Y_local, void* workspace, size_t workspace_bytes,
                                 void* stream) {
+  HM_NVTX("hodlr_matvec_dist_end");
   HodlrPlan P;
   DistPart d;
   hm_status st = hodlr_dist_plan(tree, ranks, nrhs, part, 0, &P, &d);
@@ -548,6 +555,7 @@ hm_status hm_hodlr_dist_workspace_bytes(const hm_tree* tree, const int32_t* rank
 hm_status hodlr_matvec_dist(hm_comm* comm, const hm_tree* tree, const int32_t* ranks, const double* D_local,
                             const double* U_local, const double* V_local, const double* X_local, int32_t nrhs,
                             double* Y_local, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hodlr_matvec_dist");
   int32_t nranks = 0, rank = 0;
   hm_status st = comm_check(comm, &nranks, &rank);
   if (st) return st;

@@ -772,6 +772,7 @@ hm_status hm_hss_norm2_workspace_bytes(const hm_tree* tree, int32_t k, size_t* b
 hm_status hss_norm2_est(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                         const double* R, const double* W, const double* B, const double* x0, int32_t iters,
                         double* est, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_norm2_est");
   HssPlan P;
   hm_status st = hss_plan(tree, k, 1, 0, &P);
   if (st) return st;
@@ -796,6 +797,7 @@ hm_status hm_hss_workspace_bytes(const hm_tree* tree, int32_t k, int32_t nrhs, i
 hm_status hss_matvec(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                      const double* R, const double* W, const double* B, const double* X, int32_t nrhs,
                      double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec");
   return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                  static_cast<cudaStream_t>(stream), 0);
 }
@@ -803,6 +805,7 @@ hm_status hss_matvec(const hm_tree* tree, int32_t k, const double* D, const doub
 hm_status hss_matvec_t(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                        const double* R, const double* W, const double* B, const double* X, int32_t nrhs,
                        double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_t");
   return hss_run(tree, k, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                  static_cast<cudaStream_t>(stream), 0, 1);
 }
@@ -810,6 +813,7 @@ hm_status hss_matvec_t(const hm_tree* tree, int32_t k, const double* D, const do
 hm_status hss_matvec_hostio(const hm_tree* tree, int32_t k, const double* D, const double* U, const double* V,
                             const double* R, const double* W, const double* B, const double* X_host,
                             int32_t nrhs, double* Y_host, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_hostio");
   return hss_run(tree, k, D, U, V, R, W, B, X_host, nrhs, Y_host, workspace, workspace_bytes,
                  static_cast<cudaStream_t>(stream), HM_WS_HOSTIO);
 }
@@ -828,6 +832,7 @@ hm_status hm_hss_dist_sizes(const hm_tree* tree, int32_t k, int32_t nrhs, const 
 hm_status hss_matvec_dist_begin(const hm_tree* tree, int32_t k, const hm_part* part, const double* V_local,
                                 const double* W_sub, const double* W_root, const double* X_local, int32_t nrhs,
                                 double* send, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_dist_begin");
   HssPlan P;
   DistPart d;
   hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
@@ -845,6 +850,7 @@ hm_status hss_matvec_dist_end(const hm_tree* tree, int32_t k, const hm_part* par
                               const double* R_root, const double* W_top, const double* R_top, const double* B_top,
                               const double* X_local, int32_t nrhs, const double* gathered, double* Y_local,
                               void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_dist_end");
   HssPlan P;
   DistPart d;
   hm_status st = hss_dist_plan(tree, k, nrhs, part, 0, &P, &d);
@@ -870,6 +876,7 @@ hm_status hm_hss_ranked_workspace_bytes(const hm_tree* tree, const int32_t* rank
 hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t op, const double* D, const double* U,
                             const double* V, const double* R, const double* W, const double* B, const double* X,
                             int32_t nrhs, double* Y, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_ranked");
   if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
   return hss_ranked_run(tree, ranks, op, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                         static_cast<cudaStream_t>(stream));
@@ -897,6 +904,7 @@ hm_status hss_matvec_dist(hm_comm* comm, const hm_tree* tree, int32_t k, const d
                           const double* B_sub, const double* R_root, const double* W_root, const double* R_top,
                           const double* W_top, const double* B_top, const double* X_local, int32_t nrhs,
                           double* Y_local, void* workspace, size_t workspace_bytes, void* stream) {
+  HM_NVTX("hss_matvec_dist");
   int32_t nranks = 0, rank = 0;
   hm_status st = comm_check(comm, &nranks, &rank);
   if (st) return st;

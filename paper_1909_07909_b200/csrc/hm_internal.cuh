@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hm.h"
 #include "hm_fast.cuh"
 
@@ -55,6 +57,17 @@ void allow_smem(K kernel, size_t bytes) {
 }
 
 int num_sms();  // SMs of the current device (queried once per device)
+
+// NVTX range around one C-ABI call (the host interval in which it validates and
+// enqueues its kernels; a profiler correlates the launches). Header-only NVTX:
+// a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define HM_NVTX(name) ::hmi::NvtxRange hm_nvtx_range_(name)
 
 // ------------------------------------------------------------ helpers --
 constexpr size_t kAlign = 256;

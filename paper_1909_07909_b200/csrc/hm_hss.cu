@@ -89,16 +89,7 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 #define HM_TREE_BIG_LEVEL 2048
 #endif
 constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
-// Levels 1..HM_TREE_TOP of the DMMA sweeps run in one cluster of HM_TREE_TOP_CTAS
-// CTAs (hss_tree_top_kernel; 0 = all small levels in the grid sweep).
-#ifndef HM_TREE_TOP
-#define HM_TREE_TOP 6
-#endif
-#ifndef HM_TREE_TOP_CTAS
-#define HM_TREE_TOP_CTAS 16
-#endif
-constexpr int kTreeTop = HM_TREE_TOP;
-constexpr int kTreeTopCtas = HM_TREE_TOP_CTAS;
+
 
 // ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
 #ifndef HM_GEMV_BIG
@@ -199,59 +190,27 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     st = launch(HM_NT_NAME("hss_up_pair"), s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
     if (st) return st;
   }
-  // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1). Levels
-  // 1..T (T = kTreeTop) run in one thread-block cluster (hss_tree_top_kernel,
-  // cluster barriers); levels T+1..lbig-1 in the cooperative grid sweep.
+  // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1), in one
+  // cooperative launch. (Tried: the top levels 1..6 in one 16-CTA cluster with
+  // cluster barriers — 67 + 72 us vs 140 us for the single sweep on config 4:
+  // a level's cost is its own dependent load / DMMA / store chain, ~5.6 us, not
+  // the barrier.)
   const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
-  const int T = kTreeTop;
-  auto sweep = [&](int a1, int a2, int a3, int a4) -> hm_status {
+  if (up_from >= 1 || down_to >= 1) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t need = std::max<int64_t>(1, (1ll << std::max(a1, a4)) / 2);
+    const int64_t need = std::max<int64_t>(1, (1ll << std::max(up_from, down_to)) / 2);
     dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sweep_blocks_per_sm * sms, need)));
     hm::TreeParams arg = tp;
+    int a1 = up_from, a2 = 1, a3 = 1, a4 = down_to;
     void* args[] = {&arg, &a1, &a2, &a3, &a4};
     cudaError_t e = cudaSuccess;
-    hm_status st2 = launch(HM_NT_NAME("hss_tree_sweep"), s, [&] {
+    st = launch(HM_NT_NAME("hss_tree_sweep"), s, [&] {
       e = cudaLaunchCooperativeKernel((const void*)hm::hss_tree_sweep_kernel<KT, NT>, grid, dim3(256), args, smem, s);
     });
-    if (st2 == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
-    return st2;
-  };
-  if (T <= 0) {
-    if (up_from >= 1 || down_to >= 1)
-      if ((st = sweep(up_from, 1, 1, down_to))) return st;
-  } else {
-    if (up_from > T && (st = sweep(up_from, T + 1, 1, 0))) return st;
-    const int tu = std::min(up_from, T), td = std::min(down_to, T);
-    if (tu >= 1 || td >= 1) {
-      static bool cattr = false;
-      if (!cattr) {
-        allow_smem(hm::hss_tree_top_kernel<KT, NT>, 200 * 1024);
-        cudaFuncSetAttribute(hm::hss_tree_top_kernel<KT, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cattr = true;
-      }
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kTreeTopCtas;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(kTreeTopCtas);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = s;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaError_t e = cudaSuccess;
-      st = launch(HM_NT_NAME("hss_tree_top"), s, [&] {
-        e = cudaLaunchKernelEx(&cfg, hm::hss_tree_top_kernel<KT, NT>, tp, tu, td);
-      });
-      if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_top: %s", cudaGetErrorString(e));
-      if (st) return st;
-    }
-    if (down_to > T && (st = sweep(0, 1, T + 1, down_to))) return st;
+    if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
+    if (st) return st;
   }
   // downsweep: big levels lbig .. p one launch each
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {

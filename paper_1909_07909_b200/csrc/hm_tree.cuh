@@ -229,32 +229,6 @@ __global__ void __launch_bounds__(256) hss_tree_sweep_kernel(const TreeParams P,
   }
 }
 
-// The top levels (few nodes, latency-bound) of both sweeps inside ONE thread-
-// block cluster: levels up_from..1 of the upsweep, then 1..down_to of the
-// coupling + downsweep, the cluster's CTAs splitting each level's node pairs,
-// a cluster barrier (release / acquire, cluster scope: the blocks written
-// before it are visible after it) between levels instead of a grid-wide one.
-template <int KT, int NT>
-__global__ void __launch_bounds__(256) hss_tree_top_kernel(const TreeParams P, int up_from, int down_to) {
-  namespace cg = cooperative_groups;
-  extern __shared__ double sm[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int nc = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-  bool first = true;
-  for (int l = up_from; l >= 1; --l) {
-    if (!first) cl.sync();
-    first = false;
-    const int64_t pairs = ((1ll << l) + 1) / 2;
-    for (int64_t r = rank; r < pairs; r += nc) tree_up_pair<KT, NT, true>(P, l, r, sm);
-  }
-  for (int l = 1; l <= down_to; ++l) {
-    if (!first) cl.sync();
-    first = false;
-    const int64_t pairs = 1ll << (l - 1);
-    for (int64_t q = rank; q < pairs; q += nc) tree_down_pair<KT, NT, true>(P, l, q, sm);
-  }
-}
-
 // ---------------------------------------------------- Step 1 + 3 up levels --
 // HSS Step 1 fused with the first three upsweep levels (Fig. 5 right,
 // P:684-694), nrhs <= 8 NT (one column chunk), k = KT in {16, 32}. CTA = the

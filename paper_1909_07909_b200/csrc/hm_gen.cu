@@ -35,7 +35,6 @@ struct GenPlan {
   size_t off_tab, off_lo, off_doff, off_chunks, off_cbeg, off_vorder, off_lorder;
   size_t off_t[hm::kMaxLevels + 1];    // HODLR t_l blocks
   size_t off_part[hm::kMaxLevels + 1]; // partials per vt level
-  size_t off_gpart[hm::kMaxLevels + 1]; // group partials per vt level (gen_vt_group, levels <= p-3)
   size_t tab_bytes, total;
 };
 
@@ -188,63 +187,6 @@ hm_status gen_vt_mma_dispatch(const hm::GenVtParams& vp, int64_t nchunks, int k,
   return gen_vt_mma_launch<64, 2>(vp, nchunks, s);
 }
 
-// nrhs >= 2, one rank KT in {16, 32, 64}, p >= 3: every vt level in one pass
-// over X (gen_vt_group_kernel), then the group partials of the levels <= p-3
-// reduced per node in group order (reduce_partials).
-#ifndef HM_GEN_GROUP_VT
-#define HM_GEN_GROUP_VT 1
-#endif
-template <int KT, int NT>
-hm_status gen_vt_group_launch(const hm::GenGroupVtParams& gp, int64_t groups, cudaStream_t s) {
-  const size_t smem = sizeof(double) * 8 * KT * NT * 8;
-  allow_smem(hm::gen_vt_group_kernel<KT, NT>, smem);
-  dim3 grid((unsigned)groups, (unsigned)((gp.m + NT * 8 - 1) / (NT * 8)));
-  return launch("gen_vt_group", s, [&] { hm::gen_vt_group_kernel<KT, NT><<<grid, hm::kThreads, smem, s>>>(gp); });
-}
-
-hm_status gen_vt_group_phase(const GenPlan& G, const double* const* Vlev, double* const* outlev, int k,
-                             const double* X, char* w, cudaStream_t s) {
-  const int nlev = (int)G.vt_levels.size();
-  hm::GenGroupVtParams gp;
-  memset(&gp, 0, sizeof gp);
-  gp.X = X;
-  gp.lo = reinterpret_cast<const int64_t*>(w + G.off_tab + G.off_lo);
-  gp.m = G.m; gp.nlev = nlev; gp.p = G.p;
-  hm::ReduceParams rp;
-  memset(&rp, 0, sizeof rp);
-  for (int L = 0; L < nlev; ++L) {
-    const int l = G.vt_levels[L];
-    gp.lev_l[L] = l;
-    gp.V[L] = Vlev[L];
-    gp.out[L] = outlev[L];
-    gp.gpart[L] = reinterpret_cast<double*>(w + G.off_gpart[L]);
-    if (l <= G.p - 3) {
-      hm::ReduceLevel& rl = rp.lev[rp.nlev++];
-      rl.partial = gp.gpart[L];
-      rl.out = outlev[L];
-      rl.nodes = (int64_t)1 << l;
-      rl.per_node = 1 << (G.p - 3 - l);
-      rl.km = k * G.m;
-      int lg = 0;
-      while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
-      rl.log2g = lg;
-      rl.thread_begin = rp.threads;
-      rp.threads += ((rl.nodes * rl.km << lg) + 31) / 32 * 32;
-    }
-  }
-  const int64_t groups = (int64_t)1 << (G.p - 3);
-  const int nt = G.m <= 8 ? 1 : (G.m <= 16 ? 2 : 4);
-  hm_status st;
-  if (k == 64) st = G.m <= 8 ? gen_vt_group_launch<64, 1>(gp, groups, s) : gen_vt_group_launch<64, 2>(gp, groups, s);
-  else if (k == 32) st = nt == 1 ? gen_vt_group_launch<32, 1>(gp, groups, s)
-                       : (nt == 2 ? gen_vt_group_launch<32, 2>(gp, groups, s) : gen_vt_group_launch<32, 4>(gp, groups, s));
-  else st = nt == 1 ? gen_vt_group_launch<16, 1>(gp, groups, s)
-          : (nt == 2 ? gen_vt_group_launch<16, 2>(gp, groups, s) : gen_vt_group_launch<16, 4>(gp, groups, s));
-  if (st || rp.nlev == 0) return st;
-  const unsigned grid = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
-  return launch("reduce_partials", s, [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, s>>>(rp); });
-}
-
 hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* const* outlev, const int32_t* klev,
                        const double* X, char* w, cudaStream_t s) {
   const int nlev = (int)G.vt_levels.size();
@@ -285,7 +227,6 @@ hm_status gen_vt_phase(const GenPlan& G, const double* const* Vlev, double* cons
   int kmma = G.m >= 2 ? klev[0] : 0;
   for (int L = 0; L < nlev; ++L) kmma = (klev[L] == kmma && pow2_rank(kmma, 16, 64)) ? kmma : 0;
   hm_status st;
-  if (kmma && G.p >= 3 && HM_GEN_GROUP_VT) return gen_vt_group_phase(G, Vlev, outlev, kmma, X, w, s);
   if (gemv) {
     st = launch("gen_vt_gemv", s, [&] { hm::gen_vt_gemv_kernel<<<(unsigned)G.nchunks, hm::kThreads, 0, s>>>(vp); });
   } else if (kmma) {
@@ -340,19 +281,6 @@ hm_status gen_leaf_phase(const GenPlan& G, const hm::GenLeafParams& lp, cudaStre
   }
 }
 
-// Group partials of the one-pass V^T X (gen_vt_group_kernel): one k x m block
-// per 8-leaf group for every vt level at or above level p-3.
-void gen_layout_group_partials(GenPlan* G, size_t* off) {
-  for (size_t L = 0; L < G->vt_levels.size(); ++L) {
-    G->off_gpart[L] = *off;
-    const int l = G->vt_levels[L];
-    if (G->p >= 3 && l <= G->p - 3) {
-      const int k = G->vt_k.empty() ? G->kmax : G->vt_k[L];
-      *off = align_up(*off + sizeof(double) * (size_t)((((int64_t)1 << (G->p - 3)) * k * G->m)));
-    }
-  }
-}
-
 hm_status hodlr_gen_plan(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks, int32_t nrhs, GenPlan* G) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
   hm_status st = gen_tree(n, p, c, G);
@@ -387,7 +315,6 @@ hm_status hodlr_gen_plan(int64_t n, int32_t p, const int64_t* c, const int32_t* 
     const int64_t cnt = (L + 1 < G->vt_levels.size() ? G->chunk0[L + 1] : G->nchunks) - G->chunk0[L];
     off = align_up(off + sizeof(double) * (size_t)(cnt * ranks[l - 1] * nrhs));
   }
-  gen_layout_group_partials(G, &off);
   G->total = std::max<size_t>(off, kAlign);
   return HM_OK;
 }
@@ -533,7 +460,6 @@ hm_status hss_gen_plan(int64_t n, int32_t p, const int64_t* c, int32_t k, int32_
     G->off_part[0] = off;
     off = align_up(off + sizeof(double) * (size_t)(G->nchunks * k * nrhs));
   }
-  gen_layout_group_partials(G, &off);
   G->total = std::max<size_t>(off, kAlign);
   return HM_OK;
 }

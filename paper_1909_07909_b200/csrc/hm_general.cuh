@@ -180,8 +180,31 @@ __global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams 
   for (int nt = 0; nt < NT; ++nt) colok[nt] = nt * 8 + i < mc;
   const double* A = lv.V + r0 * KT + 2 * i;
   const double* B = P.X + r0 * m + c0 + i;
-#pragma unroll 4
-  for (int64_t q = 0; q < (K + 3) / 4; ++q) {
+  // batches of QB k-steps: every load of a batch issued before its DMMAs
+  constexpr int QB = (MPW * NT <= 2) ? 8 : (MPW * NT <= 4 ? 4 : 2);
+  int64_t q = 0;
+  for (; 4 * (q + QB) <= K; q += QB) {
+    double2 a[QB][MPW];
+    double bf[QB][NT];
+#pragma unroll
+    for (int u = 0; u < QB; ++u) {
+      const int64_t row = 4 * (q + u) + j;
+#pragma unroll
+      for (int mp = 0; mp < MPW; ++mp) a[u][mp] = __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? __ldg(B + row * m + nt * 8) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < QB; ++u)
+#pragma unroll
+      for (int mp = 0; mp < MPW; ++mp)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[u][mp].x, bf[u][nt]);
+          dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[u][mp].y, bf[u][nt]);
+        }
+  }
+  for (; 4 * q < K; ++q) {  // masked tail
     const int64_t row = 4 * q + j;
     const bool ok = row < K;
     double2 a[MPW];
@@ -217,118 +240,6 @@ __global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams 
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) sum += red[((int64_t)w * KT + a) * MC + c];
     dst[a * m + c0 + c] = sum;
-  }
-}
-
-// nrhs >= 2, one rank KT in {16, 32, 64} on every vt level, p >= 3: ALL vt
-// levels in one pass over X. CTA = the 8 consecutive leaves under node
-// (p-3, g) (ragged rows allowed), warp w = leaf 8g + w. For each level the warp
-// contracts its leaf's rows (V rows 128-bit A fragments, X rows as B fragments
-// — re-read per level from L1/L2, not HBM), the 8 leaf results meet in shared
-// memory and are summed in leaf order: levels p-2..p have whole nodes inside
-// the group (written to t directly), levels <= p-3 leave one group partial per
-// node-slice (reduced in group order by reduce_partials).
-struct GenGroupVtParams {
-  const double* X;      // [n][m]
-  const int64_t* lo;    // device [nleaves + 1] leaf row starts
-  int32_t m, nlev, p, pad;
-  int32_t lev_l[kMaxLevels];        // tree level of vt level L
-  const double* V[kMaxLevels];      // [n][KT]
-  double* out[kMaxLevels];          // [2^l][KT][m]
-  double* gpart[kMaxLevels];        // [2^(p-3)][KT][m] (levels <= p-3)
-};
-
-template <int KT, int NT>
-__global__ void __launch_bounds__(kThreads) gen_vt_group_kernel(const GenGroupVtParams P) {
-  extern __shared__ double red[];  // [8][KT][8 NT]
-  constexpr int MC = NT * 8, MPW = KT / 16;
-  const int64_t g = blockIdx.x;
-  const int m = P.m, c0 = blockIdx.y * MC, mc = min(MC, m - c0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = lane >> 2, j = lane & 3;
-  const int64_t leaf = g * 8 + warp;
-  const int64_t r0 = P.lo[leaf], K = P.lo[leaf + 1] - r0;
-  bool colok[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) colok[nt] = nt * 8 + i < mc;
-  for (int L = 0; L < P.nlev; ++L) {
-    double acc[2 * MPW][NT][2];
-#pragma unroll
-    for (int t = 0; t < 2 * MPW; ++t)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
-    const double* A = P.V[L] + r0 * KT + 2 * i;
-    const double* B = P.X + r0 * m + c0 + i;
-    int64_t q = 0;
-    for (; 4 * (q + 4) <= K; q += 4) {  // 4 k-steps of loads in flight, unmasked
-      double2 a[4][MPW];
-      double bf[4][NT];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t row = 4 * (q + u) + j;
-#pragma unroll
-        for (int mp = 0; mp < MPW; ++mp) a[u][mp] = __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16));
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bf[u][nt] = colok[nt] ? __ldg(B + row * m + nt * 8) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int mp = 0; mp < MPW; ++mp)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[u][mp].x, bf[u][nt]);
-            dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[u][mp].y, bf[u][nt]);
-          }
-    }
-    for (; 4 * q < K; ++q) {  // masked tail
-      const int64_t row = 4 * q + j;
-      const bool ok = row < K;
-      double2 a[MPW];
-      double bf[NT];
-#pragma unroll
-      for (int mp = 0; mp < MPW; ++mp)
-        a[mp] = ok ? __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16)) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[nt] = (ok && colok[nt]) ? __ldg(B + row * m + nt * 8) : 0.0;
-#pragma unroll
-      for (int mp = 0; mp < MPW; ++mp)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[mp].x, bf[nt]);
-          dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[mp].y, bf[nt]);
-        }
-    }
-#pragma unroll
-    for (int t = 0; t < 2 * MPW; ++t) {
-      const int a = 16 * (t >> 1) + 2 * i + (t & 1);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        double* o = red + ((int64_t)warp * KT + a) * MC + nt * 8 + 2 * j;
-        o[0] = acc[t][nt][0];
-        o[1] = acc[t][nt][1];
-      }
-    }
-    __syncthreads();
-    const int l = P.lev_l[L];
-    if (l >= P.p - 2) {  // nodes inside the group: span leaves each, summed in leaf order
-      const int span = 1 << (P.p - l), nn = 8 / span;
-      for (int o = threadIdx.x; o < nn * KT * mc; o += kThreads) {
-        const int u = o / (KT * mc), r = o - u * KT * mc, a = r / mc, c = r - a * mc;
-        double sum = 0.0;
-        for (int s2 = 0; s2 < span; ++s2) sum += red[((int64_t)(u * span + s2) * KT + a) * MC + c];
-        P.out[L][((g * nn + u) * KT + a) * m + c0 + c] = sum;
-      }
-    } else {  // the group is part of one node: its partial, leaves in order
-      for (int o = threadIdx.x; o < KT * mc; o += kThreads) {
-        const int a = o / mc, c = o - a * mc;
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) sum += red[((int64_t)w * KT + a) * MC + c];
-        P.gpart[L][(g * KT + a) * m + c0 + c] = sum;
-      }
-    }
-    __syncthreads();
   }
 }
 

@@ -246,21 +246,17 @@ class DistWorkload:
         lpr = (1 << p5) // P
         nl5 = n5 // P
         self.rows5 = nl5
+        # only this rank's rows / subtree are generated (shard-local fill)
         self.D5 = hm_inputs.inverse_laplacian_leaf_blocks(n5, p5, leaves=range(r * lpr, (r + 1) * lpr), xp=torch,
                                                           device=device)
-        U, V = hm_inputs.inverse_laplacian_factors(n5, p5, xp=torch, device=device)
         self.ranks5 = [1] * p5
-        _, self.U5, self.V5 = hd.hodlr_shard(n5, p5, b5, self.ranks5, self.D5[:0], U, V, P, r)
-        del U, V
+        self.U5, self.V5 = hm_inputs.inverse_laplacian_factors(n5, p5, xp=torch, device=device,
+                                                               rows=(r * nl5, (r + 1) * nl5))
         g = torch.Generator(device=device)
         g.manual_seed(seed + r)
         self.X5 = torch.randn(nl5, M5, dtype=torch.float64, device=device, generator=g)
         self.Y5 = torch.empty_like(self.X5)
-        s4 = hm_inputs.device_hss_random(C4.n, C4.levels, C4.k, seed + 1, device)  # same draw on every rank
-        self.sh4 = {k_: v.contiguous() for k_, v in
-                    hd.hss_shard(C4.n, C4.levels, C4.leaf, C4.k, s4.D, s4.U, s4.V, s4.R, s4.W, s4.B, P, r).items()}
-        del s4
-        torch.cuda.empty_cache()
+        self.sh4 = hm_inputs.device_hss_shard(C4.n, C4.levels, C4.k, seed + 1, device, P, r)
         nl4 = C4.n // P
         self.rows4 = nl4
         self.X4 = torch.randn(nl4, M4, dtype=torch.float64, device=device, generator=g)

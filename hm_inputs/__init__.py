@@ -189,24 +189,28 @@ def inverse_laplacian_leaf_blocks(n: int, levels: int, leaves=None, xp=np, devic
     return out.reshape(-1)
 
 
-def inverse_laplacian_factors(n: int, levels: int, xp=np, device=None):
+def inverse_laplacian_factors(n: int, levels: int, xp=np, device=None, rows=None):
     """Level-major rank-1 factors (HODLR layout) of A = tridiag(-1,2,-1)^{-1} (reading G11):
     upper block (i<j): u_i = i, v_j = (n+1-j)/(n+1); lower block (i>j): u_i = n+1-i,
-    v_j = j/(n+1). Row r of level l sits in node (r-1)//s_l; odd nodes are lower blocks."""
+    v_j = j/(n+1). Row r of level l sits in node (r-1)//s_l; odd nodes are lower blocks.
+    ``rows`` = (r0, r1): only those rows of every level (a rank's shard, same layout
+    with r1 - r0 rows per level)."""
     kw = {} if xp is np else {"device": device}
     np1 = n + 1
-    g = xp.arange(1, n + 1, dtype=xp.int64, **kw)
+    r0, r1 = rows if rows is not None else (0, n)
+    nr = r1 - r0
+    g = xp.arange(r0 + 1, r1 + 1, dtype=xp.int64, **kw)
     gf = g.astype(np.float64) if xp is np else g.to(xp.float64)
     # divisor as an array: torch turns "/ scalar" into "* (1/scalar)", which is not
     # correctly rounded; tensor / tensor is a true IEEE division like numpy's
     den = np1 if xp is np else xp.full_like(gf, float(np1))
-    U = xp.empty(n * levels, dtype=xp.float64, **kw)
-    V = xp.empty(n * levels, dtype=xp.float64, **kw)
+    U = xp.empty(nr * levels, dtype=xp.float64, **kw)
+    V = xp.empty(nr * levels, dtype=xp.float64, **kw)
     for l in range(1, levels + 1):
         s = n >> l
         odd = ((g - 1) // s) % 2 == 1
-        U[(l - 1) * n: l * n] = xp.where(odd, np1 - gf, gf)
-        V[(l - 1) * n: l * n] = xp.where(odd, (np1 - gf) / den, gf / den)
+        U[(l - 1) * nr: l * nr] = xp.where(odd, np1 - gf, gf)
+        V[(l - 1) * nr: l * nr] = xp.where(odd, (np1 - gf) / den, gf / den)
     return U, V
 
 
@@ -365,3 +369,53 @@ def device_hss_random(n, levels, k, seed, device):
     R, W = orth(nt, 2 * k), orth(nt, 2 * k)
     B = torch.randn(nb * 2 * k * k, **f)
     return Hss(n, levels, b, k, D, U, V, R, W, B)
+
+
+def device_hss_shard(n, levels, k, seed, device, P, r, block=64):
+    """Rank r's shard (the dict of paper_1909_07909_b200.dist.hss_shard) of a device-drawn
+    random HSS matrix with hss_random's distributions, drawing ONLY what the rank holds
+    (bench only). Every array is drawn in blocks of `block` nodes, block j of (array,
+    level) from its own seed, so the global matrix does not depend on P and a rank
+    draws the blocks overlapping its nodes (the top levels' blocks on every rank)."""
+    import torch
+    b = n >> levels
+    q = P.bit_length() - 1
+    assert (1 << q) == P and q <= levels
+    f = dict(dtype=torch.float64, device=device)
+
+    def gen(aid, level, blk):
+        g = torch.Generator(device=device)
+        g.manual_seed((seed * 1000003 + aid * 10007 + level * 101) * 65537 + blk)
+        return g
+
+    def draw(aid, level, nodes, shape, lo, hi, orth=False, scale=1.0):
+        """nodes [lo, hi) of the (aid, level) array of `nodes` nodes, each of `shape`."""
+        out = []
+        for blk in range(lo // block, (hi + block - 1) // block):
+            a, z = blk * block, min(nodes, (blk + 1) * block)
+            x = torch.randn(z - a, *shape, generator=gen(aid, level, blk), **f)
+            if orth:
+                x = torch.linalg.qr(x, mode="reduced")[0]
+            out.append(x[max(lo, a) - a: min(hi, z) - a])
+        x = torch.cat(out) if out else torch.empty(0, *shape, **f)
+        return (x * scale if scale != 1.0 else x).reshape(-1)
+
+    nl, lpr = 1 << levels, (1 << levels) // P
+    L0, L1 = r * lpr, (r + 1) * lpr
+    pl = levels - q
+    sh = {"D": draw(AID["D"], levels, nl, (b, b), L0, L1, scale=1.0 / np.sqrt(b)),
+          "U": draw(AID["U"], levels, nl, (b, k), L0, L1, orth=True),
+          "V": draw(AID["V"], levels, nl, (b, k), L0, L1, orth=True)}
+    tr = lambda aid, l, lo, hi: draw(aid, l, 1 << l, (2 * k, k), lo, hi, orth=True)  # noqa: E731
+    cores = lambda l, lo, hi: draw(AID["B"], l, 1 << l, (2, k, k), lo, hi)  # noqa: E731
+    cat = lambda xs: torch.cat(xs) if xs else torch.empty(0, **f)  # noqa: E731
+    sh["W_sub"] = cat([tr(AID["W"], q + lp, r << lp, (r + 1) << lp) for lp in range(1, pl)])
+    sh["R_sub"] = cat([tr(AID["R"], q + lp, r << lp, (r + 1) << lp) for lp in range(1, pl)])
+    sh["B_sub"] = cat([cores(q + lp, r << lp, (r + 1) << lp) for lp in range(0, pl)])
+    has_root = q >= 1 and pl >= 1
+    sh["W_root"] = tr(AID["W"], q, r, r + 1) if has_root else torch.empty(0, **f)
+    sh["R_root"] = tr(AID["R"], q, r, r + 1) if has_root else torch.empty(0, **f)
+    sh["W_top"] = cat([tr(AID["W"], l, 0, 1 << l) for l in range(1, q)])
+    sh["R_top"] = cat([tr(AID["R"], l, 0, 1 << l) for l in range(1, q)])
+    sh["B_top"] = cat([cores(l, 0, 1 << l) for l in range(0, q)])
+    return {key: v.contiguous() for key, v in sh.items()}

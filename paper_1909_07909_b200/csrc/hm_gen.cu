@@ -254,7 +254,7 @@ hm_status gen_leaf_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t 
 #endif
 template <int NT, bool DT>
 hm_status gen_leaf_mma_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (size_t)(lp.ktot * (NT * 8 + 4)) + 16 * (size_t)lp.ktot + 16;
+  const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * (NT * 8 + 4)) + 16 * (size_t)lp.ktot + 16;
   allow_smem(hm::gen_leaf_mma_kernel<NT, DT>, std::max<size_t>(smem, 1));
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + NT * 8 - 1) / (NT * 8)));
   return launch(DT ? "gen_leaf_mma_t" : "gen_leaf_mma", s,
@@ -266,7 +266,7 @@ hm_status gen_leaf_phase(const GenPlan& G, const hm::GenLeafParams& lp, cudaStre
   // nrhs >= 2: DMMA leaf pass (8 NT columns per CTA) when the staged rows fit
   if (G.m >= HM_GEN_LEAF_MMA_MIN_M) {
     const int nt = G.m <= 8 ? 1 : (G.m <= 16 ? 2 : 4);
-    if (G.ktot * (nt * 8 + 4) <= kSmemBudgetDoubles) {  // only the T blocks are staged
+    if ((G.smax + G.ktot) * (nt * 8 + 4) <= kSmemBudgetDoubles) {
       if (nt == 1) return lp.dtrans ? gen_leaf_mma_launch<1, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<1, false>(lp, nl, G.smax, s);
       if (nt == 2) return lp.dtrans ? gen_leaf_mma_launch<2, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<2, false>(lp, nl, G.smax, s);
       return lp.dtrans ? gen_leaf_mma_launch<4, true>(lp, nl, G.smax, s) : gen_leaf_mma_launch<4, false>(lp, nl, G.smax, s);

@@ -477,11 +477,13 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
   if (b == 0) return;
   const int c0 = blockIdx.y * MC;
   const int m = P.m, mc = min(MC, m - c0);
-  // Z = the coefficient blocks T_1; ..; T_S only ([ktot][ZS]): the X rows are
-  // read as B fragments straight from global memory (L1 serves the re-reads by
-  // the CTA's warps), so shared memory stays small and more CTAs fit per SM
-  double* Z = smem;
-  int64_t off = 0;
+  double* Z = smem;  // [(b + ktot)][ZS]
+  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
+    const int64_t r = e / MC;
+    const int c = (int)(e - r * MC);
+    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * m + c0 + c] : 0.0;
+  }
+  int64_t off = b;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
     const double* T = sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
     off += sg.k;
   }
   const int kt = P.ktot;
-  const double** ubase = reinterpret_cast<const double**>(Z + kt * ZS);
+  const double** ubase = reinterpret_cast<const double**>(Z + (b + kt) * ZS);
   int* ukst = reinterpret_cast<int*>(ubase + kt);
   {
     int e = 0;
@@ -523,33 +525,25 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
     const int64_t rr = rok ? row : b - 1;
     const double* drow = DT ? Di + rr : Di + rr * b;
     const int64_t dstep = DT ? b : 1;
-    constexpr int QD = Q / NT >= 4 ? Q / NT : 4;  // k-steps per batch (A and B loads)
-    bool colok[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) colok[nt] = nt * 8 + i < mc;
-    const double* xb = P.X + r0 * m + c0 + i;
     int q0 = 0;
-    for (; 4 * (q0 + QD) <= bi; q0 += QD) {
-      double a[QD], bx[QD][NT];
+    for (; 4 * (q0 + Q) <= bi; q0 += Q) {
+      double a[Q];
 #pragma unroll
-      for (int u = 0; u < QD; ++u) {
-        const int kk = 4 * (q0 + u) + j;
-        a[u] = __ldg(drow + kk * dstep);
+      for (int u = 0; u < Q; ++u) a[u] = __ldg(drow + (4 * (q0 + u) + j) * dstep);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bx[u][nt] = colok[nt] ? __ldg(xb + (int64_t)kk * m + nt * 8) : 0.0;
+      for (int u = 0; u < Q; ++u) {
+        const double* zr = Z + (4 * (q0 + u) + j) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], zr[nt * 8]);
       }
-#pragma unroll
-      for (int u = 0; u < QD; ++u)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], bx[u][nt]);
     }
     for (; 4 * q0 < bi; ++q0) {
       const int kk = 4 * q0 + j;
       const bool kok = kk < bi;
       const double a = kok ? __ldg(drow + kk * dstep) : 0.0;
+      const double* zr = Z + (kok ? kk : 0) * ZS + i;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        dmma(acc[nt][0], acc[nt][1], a, (kok && colok[nt]) ? __ldg(xb + (int64_t)kk * m + nt * 8) : 0.0);
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, kok ? zr[nt * 8] : 0.0);
     }
     // U segments, flattened over the extended columns kk in [0, ktot) (tables
     // staged above): Q k-steps of A fragments U_s(kk)[row][a(kk)] requested
@@ -566,7 +560,7 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
       for (int u = 0; u < Q; ++u) {
         if (4 * (q0 + u) >= kt) break;
         const int kk = 4 * (q0 + u) + j;
-        const double* zr = Z + (kk < kt ? kk : 0) * ZS + i;
+        const double* zr = Z + (b + (kk < kt ? kk : 0)) * ZS + i;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < kt ? zr[nt * 8] : 0.0);
       }

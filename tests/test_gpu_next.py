@@ -48,13 +48,31 @@ def test_hodlr_norm2_est_vs_oracle(hm, n, leaf, levels, k, iters):
 
 @pytest.mark.parametrize("ranks", [[16, 8, 16, 4, 32, 2], [3, 0, 5, 7, 1, 2]])
 def test_hodlr_norm2_est_per_level_ranks(hm, ranks):
-    """Per-level ranks in the norm estimate: uniform-tree kernels for
-    power-of-two ranks, the general ones otherwise; both vs the oracle."""
+    """Per-level ranks in the norm estimate on the uniform-tree kernels (leaf 256,
+    6 levels: one V^T X pass per distinct rank, vt_contract for the odd ranks) vs the oracle."""
     n, leaf, levels = 16384, 256, 6
     h = hm_inputs.hodlr_random(n, levels, ranks, cid=42)
     x0 = hm_inputs.rhs(n, 1, cid=42).ravel()
     ref = oracle.hodlr_norm2_est(n, levels, h.ranks, h.D, h.U, h.V, x0, 4)
     est = hm.hodlr_norm2_est(n, levels, leaf, h.ranks, dev(h.D), dev(h.U), dev(h.V), dev(x0), 4)
+    assert abs(float(est.item()) - ref) <= TOL * ref
+
+
+@pytest.mark.parametrize("n,leaf,levels,ranks", [(1024, 256, 2, [4, 8]), (3072, 96, 5, [3, 8, 2, 5, 4])])
+def test_hodlr_norm2_est_general_routing(hm, n, leaf, levels, ranks):
+    """Per-level ranks the uniform-tree kernels cannot take (2 levels; leaf 96) run the
+    power method through the general-tree kernels, as hodlr_matvec does (the call's
+    trace shows gen_* launches) — vs the oracle."""
+    h = hm_inputs.hodlr_random(n, levels, ranks, cid=44)
+    x0 = hm_inputs.rhs(n, 1, cid=44).ravel()
+    ref = oracle.hodlr_norm2_est(n, levels, h.ranks, h.D, h.U, h.V, x0, 4)
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    est = hm.hodlr_norm2_est(n, levels, leaf, h.ranks, dev(h.D), dev(h.U), dev(h.V), dev(x0), 4)
+    torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert any(nm.startswith("gen_") for nm in names), names
     assert abs(float(est.item()) - ref) <= TOL * ref
 
 

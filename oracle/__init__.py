@@ -68,6 +68,9 @@ def _load() -> ctypes.CDLL:
             "oracle_hss_matvec_ranked": [i64, i32, P, P, P, P, P, P, P, P, P, i32, P],
             "oracle_hss_matvec_ranked_t": [i64, i32, P, P, P, P, P, P, P, P, P, i32, P],
             "oracle_hss_dense_ranked": [i64, i32, P, P, P, P, P, P, P, P, P],
+            "oracle_hss_matvec_noderanked": [i64, i32, P, P, P, P, P, P, P, P, P, i32, P],
+            "oracle_hss_matvec_noderanked_t": [i64, i32, P, P, P, P, P, P, P, P, P, i32, P],
+            "oracle_hss_dense_noderanked": [i64, i32, P, P, P, P, P, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -213,6 +216,32 @@ def hss_dense_ranked(n, p, ranks, D, U, V, R, W, B, c=None) -> np.ndarray:
     rc = _load().oracle_hss_dense_ranked(n, p, _ptr(c), _ptr(ranks), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W),
                                          _ptr(B), _ptr(A))
     _check(rc, "hss_dense_ranked")
+    return A
+
+
+def hss_matvec_noderanked(n, p, node_ranks, D, U, V, R, W, B, X, c=None, trans=False) -> np.ndarray:
+    """Y = A X (A^T X if trans) for an HSS matrix with per-node ranks, node (l, i)
+    at heap index 2^l - 2 + i; layout in hm_oracle.h."""
+    c = _tree(n, p, c)
+    X = _X2(X)
+    m = X.shape[1]
+    nr = np.ascontiguousarray(node_ranks if p > 0 else [0], dtype=np.int32)
+    D, U, V, R, W, B = (_f64(a) for a in (D, U, V, R, W, B))
+    Y = np.empty((n, m), dtype=np.float64)
+    fn = _load().oracle_hss_matvec_noderanked_t if trans else _load().oracle_hss_matvec_noderanked
+    rc = fn(n, p, _ptr(c), _ptr(nr), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(X), m, _ptr(Y))
+    _check(rc, "hss_matvec_noderanked")
+    return Y
+
+
+def hss_dense_noderanked(n, p, node_ranks, D, U, V, R, W, B, c=None) -> np.ndarray:
+    c = _tree(n, p, c)
+    nr = np.ascontiguousarray(node_ranks if p > 0 else [0], dtype=np.int32)
+    D, U, V, R, W, B = (_f64(a) for a in (D, U, V, R, W, B))
+    A = np.empty((n, n), dtype=np.float64)
+    rc = _load().oracle_hss_dense_noderanked(n, p, _ptr(c), _ptr(nr), _ptr(D), _ptr(U), _ptr(V), _ptr(R), _ptr(W),
+                                             _ptr(B), _ptr(A))
+    _check(rc, "hss_dense_noderanked")
     return A
 
 

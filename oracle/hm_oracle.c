@@ -366,66 +366,80 @@ int oracle_hodlr_dense(int64_t n, int32_t p, const int64_t* c, const int32_t* ra
 }
 
 /* ------------------------------------------------------------------- HSS -- */
-/* Ranks may differ per level (bases and translation operators need not
- * have k columns on every level "as long as the dimensions are compatible"):
- * k_l = ranks[l-1] for the nodes of level l = 1..p. Then U_i^(p), V_i^(p) are
- * |I_i| x k_p, R_{U,i}^(l), R_{V,i}^(l) of a level-l node are 2k_{l+1} x k_l
- * (eq. (3) P:256-259 with the children's k_{l+1} columns), the cores of the
- * level-l siblings are k_l x k_l, and the coefficient vectors v_i^l are
- * k_l x m. Flat layout (level-major, row-major; the uniform layout of hm.h
- * when every k_l = k):
- *   R, W  node (l, i), l = 1..p-1: offset sum_{l'<l} 2^l' 2 k_{l'+1} k_l' + i 2 k_{l+1} k_l
- *   B     the cores of the level-l siblings 2q, 2q+1 (stored at the parent
- *         (l-1, q)): offset sum_{l'<l} 2^(l'-1) 2 k_l'^2 + q 2 k_l^2, [B12; B21] */
+/* Ranks may differ per node (bases and translation operators need not
+ * have k columns "for every level and node ... as long as the dimensions are
+ * compatible"). Node (l, i), l = 1..p, has rank k_h at heap index
+ * h = 2^l - 2 + i. Then U_i^(p), V_i^(p) are |I_i| x k_h, the translations
+ * R_{U,i}^(l), R_{V,i}^(l) are (k_{2i} + k_{2i+1}) x k_h (eq. (3) P:256-259 with
+ * the children's columns), the cores of siblings 2q, 2q+1 are
+ * S_{2q,2q+1}: k_{2q} x k_{2q+1} and S_{2q+1,2q}: k_{2q+1} x k_{2q}, and the
+ * coefficient vectors v_i^l are k_h x m. Flat layout (row-major, heap order;
+ * the per-level and uniform layouts of hm.h are special cases):
+ *   U, V  leaf after leaf: leaf i's |I_i| x k rows
+ *   R, W  node (l, i), l = 1..p-1, heap order: [k_{2i} + k_{2i+1}][k_h]
+ *   B     parent (l-1, q), l = 1..p, heap order from the root: B12 then B21 */
 
 typedef struct {
   int64_t n;
   int32_t p, m;
   const int64_t* c;
   int64_t* d_off;
-  int32_t* kl;      /* kl[l] = k_l, l = 1..p (kl[0] = 0) */
-  int64_t* cf_off;  /* coefficient block of node (l, 0) in xh / yh, in doubles */
-  int64_t* rw_off;  /* R / W of node (l, 0) */
-  int64_t* b_off;   /* cores of the level-l siblings of parent (l-1, 0) */
+  int32_t* kn;      /* kn[h] = rank of node h = 2^l - 2 + i (l >= 1) */
+  int64_t* cf_off;  /* coefficient block of node h in xh / yh, in doubles */
+  int64_t* rw_off;  /* R / W of node h (l = 1..p-1) */
+  int64_t* b_off;   /* cores of the children of parent hp = 2^(l-1) - 1 + q (root hp = 0) */
+  int64_t* u_off;   /* U / V rows of leaf i */
   const double *D, *U, *V, *R, *W, *B, *X;
-  double* xh; /* v_i^l of Step 1, one k_l x m block per node l = 1..p */
+  double* xh; /* v_i^l of Step 1, one k_h x m block per node */
   double* yh; /* the same vectors after Steps 2-3 */
   int trans;  /* 1: apply A^* (adjoint), see hss_matvec_op */
 } hss_ctx;
 
-static int32_t kMaxOr1(const int32_t* kl, int32_t p) {
-  int32_t k = 1;
-  for (int32_t l = 1; l <= p; ++l) k = kl[l] > k ? kl[l] : k;
-  return k;
-}
+static int64_t hidx(int32_t l, int64_t i) { return ((int64_t)1 << l) - 2 + i; }
+static int32_t kof(const hss_ctx* s, int32_t l, int64_t i) { return l >= 1 ? s->kn[hidx(l, i)] : 0; }
 
 static double* coef(const hss_ctx* s, double* base, int32_t l, int64_t i) {
-  return base + s->cf_off[l] + i * (int64_t)s->kl[l] * s->m;
+  return base + s->cf_off[hidx(l, i)];
 }
 
-static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+/* node_ranks: heap order, 2^(p+1) - 2 entries (nodes of levels 1..p) */
+static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
                      const double* D, const double* U, const double* V,
                      const double* R, const double* W, const double* B, const double* X, int32_t m) {
   memset(s, 0, sizeof(*s));
-  if (check_tree(n, p, c) || m < 1 || (p > 0 && ranks == NULL)) return -1;
+  if (check_tree(n, p, c) || m < 1 || (p > 0 && node_ranks == NULL)) return -1;
   s->n = n; s->p = p; s->m = m; s->c = c;
   s->D = D; s->U = U; s->V = V; s->R = R; s->W = W; s->B = B; s->X = X;
   s->d_off = leaf_block_offsets(c, p);
-  s->kl = (int32_t*)calloc((size_t)(p + 2), sizeof(int32_t));
-  s->cf_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
-  s->rw_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
-  s->b_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
-  if (!s->d_off || !s->kl || !s->cf_off || !s->rw_off || !s->b_off) return -1;
-  for (int32_t l = 1; l <= p; ++l) {
-    if (ranks[l - 1] < 0) return -1;
-    s->kl[l] = ranks[l - 1];
+  const int64_t nn = ((int64_t)1 << (p + 1)) - 2, nl = (int64_t)1 << p;
+  s->kn = (int32_t*)calloc((size_t)(nn + 1), sizeof(int32_t));
+  s->cf_off = (int64_t*)calloc((size_t)(nn + 1), sizeof(int64_t));
+  s->rw_off = (int64_t*)calloc((size_t)(nn + 1), sizeof(int64_t));
+  s->b_off = (int64_t*)calloc((size_t)(nn + 1), sizeof(int64_t));
+  s->u_off = (int64_t*)calloc((size_t)(nl + 1), sizeof(int64_t));
+  if (!s->d_off || !s->kn || !s->cf_off || !s->rw_off || !s->b_off || !s->u_off) return -1;
+  for (int64_t h = 0; h < nn; ++h) {
+    if (node_ranks[h] < 0) return -1;
+    s->kn[h] = node_ranks[h];
   }
-  for (int32_t l = 1; l <= p; ++l) {
-    s->cf_off[l + 1] = s->cf_off[l] + ((int64_t)1 << l) * s->kl[l] * m;
-    s->b_off[l + 1] = s->b_off[l] + ((int64_t)1 << (l - 1)) * 2 * s->kl[l] * s->kl[l];
-    if (l <= p - 1) s->rw_off[l + 1] = s->rw_off[l] + ((int64_t)1 << l) * 2 * s->kl[l + 1] * s->kl[l];
-  }
-  size_t cnt = (size_t)s->cf_off[p + 1] + 1;
+  int64_t cf = 0, rw = 0, bo = 0;
+  for (int32_t l = 1; l <= p; ++l)
+    for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
+      s->cf_off[hidx(l, i)] = cf;
+      cf += (int64_t)kof(s, l, i) * m;
+      if (l <= p - 1) {
+        s->rw_off[hidx(l, i)] = rw;
+        rw += (int64_t)(kof(s, l + 1, 2 * i) + kof(s, l + 1, 2 * i + 1)) * kof(s, l, i);
+      }
+    }
+  for (int32_t l = 1; l <= p; ++l) /* parents (l-1, q) in heap order from the root */
+    for (int64_t q = 0; q < ((int64_t)1 << (l - 1)); ++q) {
+      s->b_off[((int64_t)1 << (l - 1)) - 1 + q] = bo;
+      bo += 2 * (int64_t)kof(s, l, 2 * q) * kof(s, l, 2 * q + 1);
+    }
+  for (int64_t i = 0; i < nl; ++i)
+    s->u_off[i + 1] = s->u_off[i] + (c[i] - leaf_lo(c, i)) * (int64_t)(p > 0 ? kof(s, p, i) : 0);
+  size_t cnt = (size_t)cf + 1;
   s->xh = (double*)calloc(cnt, sizeof(double));
   s->yh = (double*)calloc(cnt, sizeof(double));
   return (s->xh && s->yh) ? 0 : -1;
@@ -433,45 +447,44 @@ static int hss_setup(hss_ctx* s, int64_t n, int32_t p, const int64_t* c, const i
 
 static void hss_teardown(hss_ctx* s) {
   free(s->d_off); free(s->xh); free(s->yh);
-  free(s->kl); free(s->cf_off); free(s->rw_off); free(s->b_off);
+  free(s->kn); free(s->cf_off); free(s->rw_off); free(s->b_off); free(s->u_off);
 }
 
 /* Step 1, first half, and the upsweep (Fig. 5 right):
  *   v_i^p = (V_i^(p))^* v(I_i^p),  i = 1..2^p
  *   v_i^l = (R_{V,i}^(l))^* [v_{2i-1}^{l+1}; v_{2i}^{l+1}],  l = p-1..1
- * with R_{V,i}^(l) = W[node] = [Wl; Wr] (2k_{l+1} x k_l), reading G3. */
+ * with R_{V,i}^(l) = W[node] = [Wl; Wr] ((k_{2i} + k_{2i+1}) x k_h), reading G3. */
 static void hss_upsweep(hss_ctx* s) {
   int32_t p = s->p, m = s->m;
   if (p == 0) return;
-  int32_t kp = s->kl[p];
   int64_t nl = (int64_t)1 << p;
-  if (kp > 0) {
-#pragma omp parallel for schedule(static) if (s->n * kp * m > OMP_MIN_WORK)
-    for (int64_t i = 0; i < nl; ++i) {
-      int64_t lo = leaf_lo(s->c, i), hi = s->c[i];
-      double* t = coef(s, s->xh, p, i);
-      for (int32_t a = 0; a < kp; ++a)
-        for (int32_t q = 0; q < m; ++q) {
-          double acc = 0.0;
-          for (int64_t r = lo; r < hi; ++r) acc += s->V[r * kp + a] * s->X[r * m + q];
-          t[a * m + q] = acc;
-        }
-    }
+#pragma omp parallel for schedule(static) if (s->n * m * 16 > OMP_MIN_WORK)
+  for (int64_t i = 0; i < nl; ++i) {
+    int64_t lo = leaf_lo(s->c, i), hi = s->c[i];
+    int32_t kp = kof(s, p, i);
+    const double* Vi = s->V + s->u_off[i];  /* rows lo..hi-1 of leaf i, kp columns */
+    double* t = coef(s, s->xh, p, i);
+    for (int32_t a = 0; a < kp; ++a)
+      for (int32_t q = 0; q < m; ++q) {
+        double acc = 0.0;
+        for (int64_t r = lo; r < hi; ++r) acc += Vi[(r - lo) * kp + a] * s->X[r * m + q];
+        t[a * m + q] = acc;
+      }
   }
   for (int32_t l = p - 1; l >= 1; --l) {
     int64_t cnt = (int64_t)1 << l;
-    int32_t kc = s->kl[l + 1], k = s->kl[l];
-#pragma omp parallel for schedule(static) if (cnt * 4 * kc * k * m > OMP_MIN_WORK)
+#pragma omp parallel for schedule(static) if (cnt * 64 * m > OMP_MIN_WORK)
     for (int64_t i = 0; i < cnt; ++i) {
-      const double* Wn = s->W + s->rw_off[l] + i * 2 * kc * k; /* [2k_{l+1}][k_l] */
-      const double* z0 = coef(s, s->xh, l + 1, 2 * i);         /* v_{2i-1}^{l+1} */
-      const double* z1 = coef(s, s->xh, l + 1, 2 * i + 1);     /* v_{2i}^{l+1}   */
+      int32_t k = kof(s, l, i), k0 = kof(s, l + 1, 2 * i), k1 = kof(s, l + 1, 2 * i + 1);
+      const double* Wn = s->W + s->rw_off[hidx(l, i)]; /* [k0 + k1][k] */
+      const double* z0 = coef(s, s->xh, l + 1, 2 * i);     /* v_{2i-1}^{l+1} */
+      const double* z1 = coef(s, s->xh, l + 1, 2 * i + 1); /* v_{2i}^{l+1}   */
       double* t = coef(s, s->xh, l, i);
       for (int32_t a = 0; a < k; ++a)
         for (int32_t q = 0; q < m; ++q) {
-          double acc = 0.0; /* (W^T z)[a] = sum_{r<2k_{l+1}} W[r][a] z[r], r in natural order */
-          for (int32_t r = 0; r < kc; ++r) acc += Wn[r * k + a] * z0[r * m + q];
-          for (int32_t r = 0; r < kc; ++r) acc += Wn[(kc + r) * k + a] * z1[r * m + q];
+          double acc = 0.0; /* (W^T z)[a] = sum_r W[r][a] z[r], r in natural order */
+          for (int32_t r = 0; r < k0; ++r) acc += Wn[r * k + a] * z0[r * m + q];
+          for (int32_t r = 0; r < k1; ++r) acc += Wn[(k0 + r) * k + a] * z1[r * m + q];
           t[a * m + q] = acc;
         }
     }
@@ -480,30 +493,39 @@ static void hss_upsweep(hss_ctx* s) {
 
 /* Step 2 for one sibling pair (reading G1: l = 1..p, q = 0..2^(l-1)-1):
  *   [v_{2q}^l; v_{2q+1}^l] <- [0 S_{2q,2q+1}; S_{2q+1,2q} 0] [v_{2q}^l; v_{2q+1}^l]
- * S_{2q,2q+1}^{(l)} = B12 and S_{2q+1,2q}^{(l)} = B21 of the parent (l-1, q).
- * Writes only the member `which` (0 = 2q, 1 = 2q+1) of the pair. */
+ * S_{2q,2q+1}^{(l)} = B12 (k_{2q} x k_{2q+1}) and S_{2q+1,2q}^{(l)} = B21 of the
+ * parent (l-1, q). Writes only the member `which` (0 = 2q, 1 = 2q+1). */
 static void hss_couple(hss_ctx* s, int32_t l, int64_t q, int which) {
-  int32_t k = s->kl[l], m = s->m;
-  const double* Bn = s->B + s->b_off[l] + q * 2 * k * k;
+  int32_t m = s->m, k0 = kof(s, l, 2 * q), k1 = kof(s, l, 2 * q + 1);
+  const double* Bn = s->B + s->b_off[((int64_t)1 << (l - 1)) - 1 + q];
+  const double* B12 = Bn;                     /* k0 x k1 */
+  const double* B21 = Bn + (int64_t)k0 * k1;  /* k1 x k0 */
   const double* xin = coef(s, s->xh, l, 2 * q + (which == 0 ? 1 : 0));
   double* yout = coef(s, s->yh, l, 2 * q + which);
-  /* A: S = B12 (which 0) or B21 (which 1). A^*: the cores of A^* are
-   * S'_{2q,2q+1} = (S_{2q+1,2q})^* = B21^T and S'_{2q+1,2q} = B12^T. */
-  const double* S = s->trans ? Bn + (which == 0 ? k * k : 0) : Bn + (which == 0 ? 0 : k * k);
-  for (int32_t a = 0; a < k; ++a)
+  int32_t ko = which == 0 ? k0 : k1, ki = which == 0 ? k1 : k0; /* output / input rank */
+  /* A: S = B12 (which 0) or B21 (which 1), [ko][ki]. A^*: the cores of A^* are
+   * S'_{2q,2q+1} = (S_{2q+1,2q})^* = B21^T and S'_{2q+1,2q} = B12^T; B21^T is
+   * (k1 x k0)^T = k0 x k1, read transposed from B21. */
+  for (int32_t a = 0; a < ko; ++a)
     for (int32_t c2 = 0; c2 < m; ++c2) {
       double acc = 0.0;
-      for (int32_t r = 0; r < k; ++r) acc += (s->trans ? S[r * k + a] : S[a * k + r]) * xin[r * m + c2];
+      for (int32_t r = 0; r < ki; ++r) {
+        double sv;
+        if (s->trans) sv = which == 0 ? B21[r * k0 + a] : B12[r * k1 + a];
+        else sv = which == 0 ? B12[a * k1 + r] : B21[a * k0 + r];
+        acc += sv * xin[r * m + c2];
+      }
       yout[a * m + c2] = acc;
     }
 }
 
 /* Step 3 for one child:
  *   [v_{2i-1}^{l+1}; v_{2i}^{l+1}] <- [v_{2i-1}^{l+1}; v_{2i}^{l+1}] + R_{U,i}^{(l)} v_i^l
- * R_{U,i}^{(l)} = R[node] = [Rl; Rr] (2k_{l+1} x k_l). Updates child `which`. */
+ * R_{U,i}^{(l)} = R[node] = [Rl; Rr] ((k_{2i} + k_{2i+1}) x k_h). Updates child `which`. */
 static void hss_down(hss_ctx* s, int32_t l, int64_t i, int which) {
-  int32_t kc = s->kl[l + 1], k = s->kl[l], m = s->m;
-  const double* Rn = s->R + s->rw_off[l] + i * 2 * kc * k + (which == 0 ? 0 : kc * k);
+  int32_t k = kof(s, l, i), k0 = kof(s, l + 1, 2 * i), m = s->m;
+  int32_t kc = kof(s, l + 1, 2 * i + which);
+  const double* Rn = s->R + s->rw_off[hidx(l, i)] + (which == 0 ? 0 : (int64_t)k0 * k);
   const double* yin = coef(s, s->yh, l, i);
   double* ych = coef(s, s->yh, l + 1, 2 * i + which);
   for (int32_t a = 0; a < kc; ++a)
@@ -518,9 +540,10 @@ static void hss_down(hss_ctx* s, int32_t l, int64_t i, int which) {
  * d_i = A(I_i, I_i) v(I_i). Dblk is D_i, y the leaf's output rows. */
 static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double* y) {
   int32_t m = s->m, p = s->p;
-  int32_t k = p > 0 ? s->kl[p] : 0;
+  int32_t k = p > 0 ? kof(s, p, i) : 0;
   int64_t lo = leaf_lo(s->c, i), rows = s->c[i] - lo;
   const double* yv = (p > 0 && k > 0) ? coef(s, s->yh, p, i) : NULL;
+  const double* Ui = p > 0 ? s->U + s->u_off[i] : NULL;
   for (int64_t r = 0; r < rows; ++r)
     for (int32_t q = 0; q < m; ++q) {
       double d = 0.0;
@@ -528,7 +551,7 @@ static void hss_leaf_out(const hss_ctx* s, int64_t i, const double* Dblk, double
         d += (s->trans ? Dblk[j * rows + r] : Dblk[r * rows + j]) * s->X[(lo + j) * m + q];
       double u = 0.0;
       if (yv)
-        for (int32_t a = 0; a < k; ++a) u += s->U[(lo + r) * k + a] * yv[a * m + q];
+        for (int32_t a = 0; a < k; ++a) u += Ui[r * k + a] * yv[a * m + q];
       y[r * m + q] = u + d;
     }
 }
@@ -538,9 +561,7 @@ static void hss_couple_down_all(hss_ctx* s) {
   int32_t p = s->p;
   for (int32_t l = 1; l <= p; ++l) { /* Step 2, all levels incl. the leaves (G1) */
     int64_t pairs = (int64_t)1 << (l - 1);
-    int32_t k = s->kl[l];
-    if (k == 0) continue;
-#pragma omp parallel for schedule(static) if (pairs * 2 * k * k * s->m > OMP_MIN_WORK)
+#pragma omp parallel for schedule(static) if (pairs * 64 * s->m > OMP_MIN_WORK)
     for (int64_t q = 0; q < pairs; ++q) {
       hss_couple(s, l, q, 0);
       hss_couple(s, l, q, 1);
@@ -548,9 +569,7 @@ static void hss_couple_down_all(hss_ctx* s) {
   }
   for (int32_t l = 1; l <= p - 1; ++l) { /* Step 3, top to bottom */
     int64_t cnt = (int64_t)1 << l;
-    int32_t k = s->kl[l], kc = s->kl[l + 1];
-    if (k == 0 || kc == 0) continue;
-#pragma omp parallel for schedule(static) if (cnt * 2 * kc * k * s->m > OMP_MIN_WORK)
+#pragma omp parallel for schedule(static) if (cnt * 64 * s->m > OMP_MIN_WORK)
     for (int64_t i = 0; i < cnt; ++i) {
       hss_down(s, l, i, 0);
       hss_down(s, l, i, 1);
@@ -564,12 +583,12 @@ static void hss_couple_down_all(hss_ctx* s) {
  * S'_ba = S_ab^* and leaf blocks D_i^*. hss_matvec_op runs Fig. 5 right on
  * those generators (trans = 1): U <-> V and R <-> W exchanged here, the
  * transposed cores in hss_couple, D_i^* in hss_leaf_out. */
-static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
                          const double* D, const double* U, const double* V,
                          const double* R, const double* W, const double* B,
                          const double* X, int32_t m, double* Y, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, ranks, D, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+  if (hss_setup(&s, n, p, c, node_ranks, D, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
       Y == NULL) {
     hss_teardown(&s);
     return -1;
@@ -585,13 +604,14 @@ static int hss_matvec_op(int64_t n, int32_t p, const int64_t* c, const int32_t* 
   return 0;
 }
 
-static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
                                 const double* Dsel, const double* U, const double* V,
                                 const double* R, const double* W, const double* B,
                                 const double* X, int32_t m,
                                 const int64_t* leaves, int64_t nleaves, double* Yout, int trans) {
   hss_ctx s;
-  if (hss_setup(&s, n, p, c, ranks, NULL, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X, m) ||
+  if (hss_setup(&s, n, p, c, node_ranks, NULL, trans ? V : U, trans ? U : V, trans ? W : R, trans ? R : W, B, X,
+                m) ||
       Yout == NULL || leaves == NULL) {
     hss_teardown(&s);
     return -1;
@@ -605,11 +625,11 @@ static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const in
     /* Step 2 on the path nodes (l, L >> (p-l)), l = 1..p, then Step 3 along it */
     for (int32_t l = 1; l <= p; ++l) {
       int64_t node = L >> (p - l);
-      if (s.kl[l] > 0) hss_couple(&s, l, node >> 1, (int)(node & 1));
+      hss_couple(&s, l, node >> 1, (int)(node & 1));
     }
     for (int32_t l = 1; l <= p - 1; ++l) {
       int64_t node = L >> (p - l), child = L >> (p - l - 1);
-      if (s.kl[l] > 0 && s.kl[l + 1] > 0) hss_down(&s, l, node, (int)(child & 1));
+      hss_down(&s, l, node, (int)(child & 1));
     }
     int64_t rows = c[L] - leaf_lo(c, L);
     hss_leaf_out(&s, L, Dsel + doff, Yout + yoff);
@@ -620,11 +640,14 @@ static int hss_matvec_leaves_op(int64_t n, int32_t p, const int64_t* c, const in
   return 0;
 }
 
-/* The uniform-rank entry points: ranks k on every level. */
-static int32_t* uniform_ranks(int32_t p, int32_t k) {
-  int32_t* r = (int32_t*)malloc(sizeof(int32_t) * (size_t)(p + 1));
-  if (r)
-    for (int32_t l = 0; l <= p; ++l) r[l] = k;
+/* Per-node rank arrays (heap order, levels 1..p) of the uniform (k) and
+ * per-level (ranks[l-1] = k_l) entry points. */
+static int32_t* node_ranks_of_levels(int32_t p, const int32_t* ranks, int32_t k) {
+  const int64_t nn = ((int64_t)1 << (p + 1)) - 2;
+  int32_t* r = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nn + 1));
+  if (!r) return NULL;
+  for (int32_t l = 1; l <= p; ++l)
+    for (int64_t i = 0; i < ((int64_t)1 << l); ++i) r[((int64_t)1 << l) - 2 + i] = ranks ? ranks[l - 1] : k;
   return r;
 }
 
@@ -632,8 +655,8 @@ int oracle_hss_matvec(int64_t n, int32_t p, const int64_t* c, int32_t k,
                       const double* D, const double* U, const double* V,
                       const double* R, const double* W, const double* B,
                       const double* X, int32_t m, double* Y) {
-  if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
+  if (k < 0 || p < 0 || p > 40) return -1;
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
   int rc = r ? hss_matvec_op(n, p, c, r, D, U, V, R, W, B, X, m, Y, 0) : -1;
   free(r);
   return rc;
@@ -643,9 +666,19 @@ int oracle_hss_matvec_t(int64_t n, int32_t p, const int64_t* c, int32_t k,
                         const double* D, const double* U, const double* V,
                         const double* R, const double* W, const double* B,
                         const double* X, int32_t m, double* Y) {
-  if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
+  if (k < 0 || p < 0 || p > 40) return -1;
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
   int rc = r ? hss_matvec_op(n, p, c, r, D, U, V, R, W, B, X, m, Y, 1) : -1;
+  free(r);
+  return rc;
+}
+
+static int hss_ranked_op(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                         const double* D, const double* U, const double* V, const double* R, const double* W,
+                         const double* B, const double* X, int32_t m, double* Y, int trans) {
+  if (p < 0 || p > 40 || (p > 0 && !ranks)) return -1;
+  int32_t* r = node_ranks_of_levels(p, ranks, 0);
+  int rc = r ? hss_matvec_op(n, p, c, r, D, U, V, R, W, B, X, m, Y, trans) : -1;
   free(r);
   return rc;
 }
@@ -654,14 +687,28 @@ int oracle_hss_matvec_ranked(int64_t n, int32_t p, const int64_t* c, const int32
                              const double* D, const double* U, const double* V,
                              const double* R, const double* W, const double* B,
                              const double* X, int32_t m, double* Y) {
-  return hss_matvec_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 0);
+  return hss_ranked_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 0);
 }
 
 int oracle_hss_matvec_ranked_t(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
                                const double* D, const double* U, const double* V,
                                const double* R, const double* W, const double* B,
                                const double* X, int32_t m, double* Y) {
-  return hss_matvec_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 1);
+  return hss_ranked_op(n, p, c, ranks, D, U, V, R, W, B, X, m, Y, 1);
+}
+
+int oracle_hss_matvec_noderanked(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                 const double* D, const double* U, const double* V,
+                                 const double* R, const double* W, const double* B,
+                                 const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, node_ranks, D, U, V, R, W, B, X, m, Y, 0);
+}
+
+int oracle_hss_matvec_noderanked_t(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                   const double* D, const double* U, const double* V,
+                                   const double* R, const double* W, const double* B,
+                                   const double* X, int32_t m, double* Y) {
+  return hss_matvec_op(n, p, c, node_ranks, D, U, V, R, W, B, X, m, Y, 1);
 }
 
 int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
@@ -669,8 +716,8 @@ int oracle_hss_matvec_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k,
                              const double* R, const double* W, const double* B,
                              const double* X, int32_t m,
                              const int64_t* leaves, int64_t nleaves, double* Yout) {
-  if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
+  if (k < 0 || p < 0 || p > 40) return -1;
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
   int rc = r ? hss_matvec_leaves_op(n, p, c, r, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 0) : -1;
   free(r);
   return rc;
@@ -681,23 +728,23 @@ int oracle_hss_matvec_t_leaves(int64_t n, int32_t p, const int64_t* c, int32_t k
                                const double* R, const double* W, const double* B,
                                const double* X, int32_t m,
                                const int64_t* leaves, int64_t nleaves, double* Yout) {
-  if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
+  if (k < 0 || p < 0 || p > 40) return -1;
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
   int rc = r ? hss_matvec_leaves_op(n, p, c, r, Dsel, U, V, R, W, B, X, m, leaves, nleaves, Yout, 1) : -1;
   free(r);
   return rc;
 }
 
-int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
-                            const double* D, const double* U, const double* V,
-                            const double* R, const double* W, const double* B, double* A) {
+int oracle_hss_dense_noderanked(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                const double* D, const double* U, const double* V,
+                                const double* R, const double* W, const double* B, double* A) {
   /* Definition: diagonal leaf blocks D_i; every sibling block
    * A(I_a^l, I_b^l) = U_a^(l) S_ab^(l) (V_b^(l))^T, with the bases
    * of the upper levels rebuilt from the leaf bases by eq. (3):
    *   U_i^(l) = blockdiag(U_{2i}^(l+1), U_{2i+1}^(l+1)) R_{U,i}^(l), same for V
-   * with R_{V,i}^(l) = W[node]; k_l columns on level l. */
+   * with R_{V,i}^(l) = W[node]; k_h columns on node h. */
   hss_ctx s;
-  if (A == NULL || hss_setup(&s, n, p, c, ranks, D, U, V, R, W, B, NULL, 1)) { hss_teardown(&s); return -1; }
+  if (A == NULL || hss_setup(&s, n, p, c, node_ranks, D, U, V, R, W, B, NULL, 1)) { hss_teardown(&s); return -1; }
   memset(A, 0, sizeof(double) * (size_t)(n * n));
   int64_t nl = (int64_t)1 << p;
   for (int64_t i = 0; i < nl; ++i) {
@@ -706,71 +753,99 @@ int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_
       for (int64_t q = 0; q < sz; ++q) A[(lo + r) * n + lo + q] = D[s.d_off[i] + r * sz + q];
   }
   if (p == 0) { hss_teardown(&s); return 0; }
-  /* Ub, Vb: level l (1..p) block of n x k_l at nk_off[l]; rows I_i^l hold U_i^(l) */
-  int64_t* nk_off = (int64_t*)calloc((size_t)(p + 2), sizeof(int64_t));
-  for (int32_t l = 1; l <= p; ++l) nk_off[l + 1] = nk_off[l] + n * s.kl[l];
-  double* Ub = (double*)malloc(sizeof(double) * (size_t)(nk_off[p + 1] + 1));
-  double* Vb = (double*)malloc(sizeof(double) * (size_t)(nk_off[p + 1] + 1));
-  if (!Ub || !Vb || !nk_off) { free(Ub); free(Vb); free(nk_off); hss_teardown(&s); return -1; }
-  memcpy(Ub + nk_off[p], U, sizeof(double) * (size_t)(n * s.kl[p]));
-  memcpy(Vb + nk_off[p], V, sizeof(double) * (size_t)(n * s.kl[p]));
-  for (int32_t l = p - 1; l >= 1; --l) {
-    int32_t k = s.kl[l], kc = s.kl[l + 1];
+  /* Ub, Vb: node h's basis (|I_h| x k_h rows, row-major) at bo[h] */
+  const int64_t nn = ((int64_t)1 << (p + 1)) - 2;
+  int64_t* bo = (int64_t*)calloc((size_t)(nn + 1), sizeof(int64_t));
+  int64_t tot = 0, kmax = 1;
+  for (int32_t l = 1; l <= p; ++l)
     for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
+      int64_t lo, hi;
+      node_range(c, p, l, i, &lo, &hi);
+      bo[hidx(l, i)] = tot;
+      tot += (hi - lo) * (int64_t)kof(&s, l, i);
+      kmax = kof(&s, l, i) > kmax ? kof(&s, l, i) : kmax;
+    }
+  double* Ub = (double*)calloc((size_t)(tot + 1), sizeof(double));
+  double* Vb = (double*)calloc((size_t)(tot + 1), sizeof(double));
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)(kmax + 1));
+  if (!Ub || !Vb || !bo || !tmp) { free(Ub); free(Vb); free(bo); free(tmp); hss_teardown(&s); return -1; }
+  for (int64_t i = 0; i < nl; ++i) { /* leaf bases */
+    int64_t cnt = s.u_off[i + 1] - s.u_off[i];
+    memcpy(Ub + bo[hidx(p, i)], U + s.u_off[i], sizeof(double) * (size_t)cnt);
+    memcpy(Vb + bo[hidx(p, i)], V + s.u_off[i], sizeof(double) * (size_t)cnt);
+  }
+  for (int32_t l = p - 1; l >= 1; --l)
+    for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
+      int32_t k = kof(&s, l, i), k0 = kof(&s, l + 1, 2 * i);
+      int64_t lo, hi;
+      node_range(c, p, l, i, &lo, &hi);
       for (int ch = 0; ch < 2; ++ch) {
+        int32_t kc = kof(&s, l + 1, 2 * i + ch);
         int64_t clo, chi;
         node_range(c, p, l + 1, 2 * i + ch, &clo, &chi);
-        const double* Rh = R + s.rw_off[l] + i * 2 * kc * k + ch * kc * k; /* Rl or Rr: k_{l+1} x k_l */
-        const double* Wh = W + s.rw_off[l] + i * 2 * kc * k + ch * kc * k;
+        const double* Rh = R + s.rw_off[hidx(l, i)] + (ch ? (int64_t)k0 * k : 0); /* kc x k */
+        const double* Wh = W + s.rw_off[hidx(l, i)] + (ch ? (int64_t)k0 * k : 0);
+        const double* Uc = Ub + bo[hidx(l + 1, 2 * i + ch)];
+        const double* Vc = Vb + bo[hidx(l + 1, 2 * i + ch)];
         for (int64_t r = clo; r < chi; ++r)
           for (int32_t a = 0; a < k; ++a) {
             double su = 0.0, sv = 0.0;
             for (int32_t e = 0; e < kc; ++e) {
-              su += Ub[nk_off[l + 1] + r * kc + e] * Rh[e * k + a];
-              sv += Vb[nk_off[l + 1] + r * kc + e] * Wh[e * k + a];
+              su += Uc[(r - clo) * kc + e] * Rh[e * k + a];
+              sv += Vc[(r - clo) * kc + e] * Wh[e * k + a];
             }
-            Ub[nk_off[l] + r * k + a] = su;
-            Vb[nk_off[l] + r * k + a] = sv;
+            Ub[bo[hidx(l, i)] + (r - lo) * k + a] = su;
+            Vb[bo[hidx(l, i)] + (r - lo) * k + a] = sv;
           }
       }
     }
-  }
-  double* tmp = (double*)malloc(sizeof(double) * (size_t)(kMaxOr1(s.kl, p) + 1));
-  for (int32_t l = 1; l <= p; ++l) {
-    int32_t k = s.kl[l];
+  for (int32_t l = 1; l <= p; ++l)
     for (int64_t q = 0; q < ((int64_t)1 << (l - 1)); ++q) {
-      const double* Bn = B + s.b_off[l] + q * 2 * k * k;
+      const int32_t k0 = kof(&s, l, 2 * q), k1 = kof(&s, l, 2 * q + 1);
+      const double* Bn = B + s.b_off[((int64_t)1 << (l - 1)) - 1 + q];
       for (int w = 0; w < 2; ++w) { /* w=0: A(I_2q, I_2q+1) = U S12 V^T; w=1: A(I_2q+1, I_2q) */
         int64_t a = 2 * q + w, b = 2 * q + 1 - w, alo, ahi, blo, bhi;
         node_range(c, p, l, a, &alo, &ahi);
         node_range(c, p, l, b, &blo, &bhi);
-        const double* S = Bn + w * k * k;
+        const int32_t ka = w ? k1 : k0, kb = w ? k0 : k1;
+        const double* S = Bn + (w ? (int64_t)k0 * k1 : 0); /* ka x kb */
+        const double* Ua = Ub + bo[hidx(l, a)];
+        const double* Vbb = Vb + bo[hidx(l, b)];
         for (int64_t r = alo; r < ahi; ++r) {
-          for (int32_t e = 0; e < k; ++e) { /* (U_a S)[r][e] */
+          for (int32_t e = 0; e < kb; ++e) { /* (U_a S)[r][e] */
             double su = 0.0;
-            for (int32_t f = 0; f < k; ++f) su += Ub[nk_off[l] + r * k + f] * S[f * k + e];
+            for (int32_t f = 0; f < ka; ++f) su += Ua[(r - alo) * ka + f] * S[f * kb + e];
             tmp[e] = su;
           }
           for (int64_t q2 = blo; q2 < bhi; ++q2) {
             double sv = 0.0;
-            for (int32_t e = 0; e < k; ++e) sv += tmp[e] * Vb[nk_off[l] + q2 * k + e];
+            for (int32_t e = 0; e < kb; ++e) sv += tmp[e] * Vbb[(q2 - blo) * kb + e];
             A[r * n + q2] = sv;
           }
         }
       }
     }
-  }
-  free(tmp); free(Ub); free(Vb); free(nk_off);
+  free(tmp); free(Ub); free(Vb); free(bo);
   hss_teardown(&s);
   return 0;
+}
+
+int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_t* ranks,
+                            const double* D, const double* U, const double* V,
+                            const double* R, const double* W, const double* B, double* A) {
+  if (p < 0 || p > 40 || (p > 0 && !ranks)) return -1;
+  int32_t* r = node_ranks_of_levels(p, ranks, 0);
+  int rc = r ? oracle_hss_dense_noderanked(n, p, c, r, D, U, V, R, W, B, A) : -1;
+  free(r);
+  return rc;
 }
 
 int oracle_hss_dense(int64_t n, int32_t p, const int64_t* c, int32_t k,
                      const double* D, const double* U, const double* V,
                      const double* R, const double* W, const double* B, double* A) {
-  if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
-  int rc = r ? oracle_hss_dense_ranked(n, p, c, r, D, U, V, R, W, B, A) : -1;
+  if (k < 0 || p < 0 || p > 40) return -1;
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
+  int rc = r ? oracle_hss_dense_noderanked(n, p, c, r, D, U, V, R, W, B, A) : -1;
   free(r);
   return rc;
 }
@@ -906,7 +981,7 @@ int oracle_hss_norm2_est(int64_t n, int32_t p, const int64_t* c, int32_t k,
                          const double* R, const double* W, const double* B,
                          const double* x0, int32_t iters, double* est) {
   if (k < 0) return -1;
-  int32_t* r = uniform_ranks(p, k);
+  int32_t* r = node_ranks_of_levels(p, NULL, k);
   if (!r) return -1;
   op_ctx o = {n, p, c, r, k, D, U, V, R, W, B};
   int rc = power_norm2(n, x0, iters, hss_apply, &o, est);

@@ -148,6 +148,23 @@ int oracle_hss_dense_ranked(int64_t n, int32_t p, const int64_t* c, const int32_
                             const double* D, const double* U, const double* V,
                             const double* R, const double* W, const double* B, double* A);
 
+/* Per-node HSS ranks ("k columns for every level and node ... not
+ * necessary"): node (l, i), l = 1..p, has rank node_ranks[2^l - 2 + i]. U, V:
+ * leaf after leaf, |I_i| x k rows; R, W of node h (l = 1..p-1), heap order:
+ * [k_{2i} + k_{2i+1}][k_h]; cores of parent (l-1, q), heap order from the
+ * root: B12 [k_{2q}][k_{2q+1}] then B21 [k_{2q+1}][k_{2q}]. */
+int oracle_hss_matvec_noderanked(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                 const double* D, const double* U, const double* V,
+                                 const double* R, const double* W, const double* B,
+                                 const double* X, int32_t m, double* Y);
+int oracle_hss_matvec_noderanked_t(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                   const double* D, const double* U, const double* V,
+                                   const double* R, const double* W, const double* B,
+                                   const double* X, int32_t m, double* Y);
+int oracle_hss_dense_noderanked(int64_t n, int32_t p, const int64_t* c, const int32_t* node_ranks,
+                                const double* D, const double* U, const double* V,
+                                const double* R, const double* W, const double* B, double* A);
+
 /* Plain dense product Y = A X (n x n times n x m), sums in natural order. */
 int oracle_dense_matvec(int64_t n, const double* A, const double* X, int32_t m, double* Y);
 

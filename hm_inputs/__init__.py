@@ -311,6 +311,42 @@ def hss_random_ranked(n: int, levels: int, ranks: Sequence[int], seed: int = MAS
     return Hss(n, levels, b, kp, D.reshape(-1), U, V, cat(Rs), cat(Ws), cat(Bs))
 
 
+def hss_random_noderanked(n: int, levels: int, node_ranks: Sequence[int], seed: int = MASTER_SEED,
+                          cid: int = 0):
+    """Random HSS generators with per-node ranks (include/hm.h
+    hss_matvec_noderanked layout): node (l, i) has rank node_ranks[2^l - 2 + i]; leaf
+    bases and translations are thin-QR Q factors of Gaussian blocks, cores N(0,1),
+    D_i N(0,1)/sqrt(b). Returns an Hss (k = the largest leaf rank) with flat arrays."""
+    b = n >> levels
+    assert b << levels == n and levels >= 1
+    kn = [int(r) for r in node_ranks]
+    h = lambda l, i: (1 << l) - 2 + i  # noqa: E731
+    nl = 1 << levels
+    D = np.empty((nl, b, b), dtype=np.float64)
+    for i in range(nl):
+        D[i] = normal((b, b), seed, cid, AID["D"], i) / np.sqrt(b)
+    Us, Vs, Rs, Ws, Bs = [], [], [], [], []
+    for i in range(nl):
+        k = kn[h(levels, i)]
+        if k:
+            Us.append(_orth_blocks(normal((1, b, k), seed, cid, AID["U"], i)).reshape(-1))
+            Vs.append(_orth_blocks(normal((1, b, k), seed, cid, AID["V"], i)).reshape(-1))
+    for l in range(1, levels):
+        for i in range(1 << l):
+            k, kc = kn[h(l, i)], kn[h(l + 1, 2 * i)] + kn[h(l + 1, 2 * i + 1)]
+            if k and kc:
+                Rs.append(_orth_blocks(normal((1, kc, k), seed, cid, AID["R"], h(l, i))).reshape(-1))
+                Ws.append(_orth_blocks(normal((1, kc, k), seed, cid, AID["W"], h(l, i))).reshape(-1))
+    for l in range(1, levels + 1):
+        for q in range(1 << (l - 1)):
+            cnt = 2 * kn[h(l, 2 * q)] * kn[h(l, 2 * q + 1)]
+            if cnt:
+                Bs.append(normal(cnt, seed, cid, AID["B"], h(l, 2 * q)))
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0)  # noqa: E731
+    return Hss(n, levels, b, max(kn[h(levels, i)] for i in range(nl)), D.reshape(-1), cat(Us), cat(Vs), cat(Rs),
+               cat(Ws), cat(Bs))
+
+
 def rhs(n: int, m: int, seed: int = MASTER_SEED, cid: int = 0, rows: Optional[Tuple[int, int]] = None,
         slab: int = 1 << 16) -> np.ndarray:
     """X iid N(0,1), [n][m], drawn in slabs of ``slab`` rows (shardable)."""

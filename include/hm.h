@@ -187,6 +187,30 @@ hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t o
                             const double* X, int32_t nrhs, double* Y,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* -------------------------------- HSS with per-node ranks (§8(f) f4) --
+ * P:264 in full: every node may have its own rank. node_ranks (HOST array of
+ * 2^(p+1) - 2 entries): node (l, i), l = 1..p, has rank k_h = node_ranks[h],
+ * h = 2^l - 2 + i, 0..64. Layout (row-major, heap order):
+ *   U, V   leaf after leaf: leaf i's b x k_(p,i) rows.
+ *   R, W   node (l, i), l = 1..p-1: [k_(l+1,2i) + k_(l+1,2i+1)][k_(l,i)]
+ *          (rows of the left child first), nodes in heap order.
+ *   B      parent (l-1, q), l = 1..p, heap order from the root: B12
+ *          [k_(l,2q)][k_(l,2q+1)] then B21 [k_(l,2q+1)][k_(l,2q)].
+ *   D, X, Y, op as for hss_matvec_ranked. Ranks equal within each level are the
+ * per-level layout (and run that path directly). Otherwise the generators are
+ * zero-padded into the per-level layout with K_l = the level's largest rank
+ * (in the workspace; exact, the padding is zero) and the per-level path runs:
+ * one extra pass over the generators. The table of padded blocks is copied to
+ * the workspace asynchronously from a pinned staging buffer (not CUDA-graph
+ * capturable). */
+hm_status hm_hss_noderanked_workspace_bytes(const hm_tree* tree, const int32_t* node_ranks, int32_t nrhs,
+                                            size_t* bytes);
+hm_status hss_matvec_noderanked(const hm_tree* tree, const int32_t* node_ranks, int32_t op,
+                                const double* D, const double* U, const double* V,
+                                const double* R, const double* W, const double* B,
+                                const double* X, int32_t nrhs, double* Y,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /* ----------------------------------- general cluster trees (§8(f) f4) --
  * The cluster tree of depth `levels` = p given by its leaf endpoint vector
  * c (Def. 2.1): c is a HOST array of 2^p int64 values,

@@ -37,7 +37,8 @@ EXPORTS = ("hm_hodlr_workspace_bytes", "hodlr_matvec", "hodlr_matvec_hostio", "h
            "hm_hss_general_workspace_bytes", "hss_matvec_general",
            "hm_comm_unique_id", "hm_comm_init", "hm_comm_destroy", "hm_comm_size", "hm_comm_allgather",
            "hm_hodlr_dist_workspace_bytes", "hodlr_matvec_dist", "hm_hss_dist_workspace_bytes", "hss_matvec_dist",
-           "hm_hss_ranked_workspace_bytes", "hss_matvec_ranked")
+           "hm_hss_ranked_workspace_bytes", "hss_matvec_ranked",
+           "hm_hss_noderanked_workspace_bytes", "hss_matvec_noderanked")
 
 
 class HmError(RuntimeError):
@@ -95,6 +96,8 @@ def load() -> ctypes.CDLL:
         "hss_matvec_general": [i64, i32, P, i32, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hm_hss_ranked_workspace_bytes": [T, P, i32, ctypes.POINTER(sz)],
         "hss_matvec_ranked": [T, P, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
+        "hm_hss_noderanked_workspace_bytes": [T, P, i32, ctypes.POINTER(sz)],
+        "hss_matvec_noderanked": [T, P, i32, P, P, P, P, P, P, P, i32, P, P, sz, P],
         "hm_profile_enable": [i32],
         "hm_profile_collect": [ctypes.POINTER(hm_launch_record), i32, ctypes.POINTER(i32)],
     }
@@ -501,4 +504,58 @@ def hss_matvec_ranked(n, levels, leaf, ranks, D, U, V, R, W, B, X, op=0, Y=None,
     _check(load().hss_matvec_ranked(ctypes.byref(t), _ranks(ranks, levels), int(op), _ptr(D), _ptr(U), _ptr(V),
                                     _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(), ws.numel(),
                                     _stream(stream)))
+    return Y
+
+
+# ------------------------------------------------- HSS, per-node ranks (f4) --
+
+def hss_noderanked_sizes(n, levels, leaf, node_ranks):
+    """Generator sizes (doubles) of an HSS matrix with per-node ranks (include/hm.h
+    hss_matvec_noderanked): U/V, R/W, B."""
+    kn = [int(r) for r in node_ranks]
+    h = lambda l, i: (1 << l) - 2 + i  # noqa: E731
+    nuv = sum(leaf * kn[h(levels, i)] for i in range(1 << levels)) if levels else 0
+    nrw = sum((kn[h(l + 1, 2 * i)] + kn[h(l + 1, 2 * i + 1)]) * kn[h(l, i)]
+              for l in range(1, levels) for i in range(1 << l))
+    nb = sum(2 * kn[h(l, 2 * q)] * kn[h(l, 2 * q + 1)] for l in range(1, levels + 1) for q in range(1 << (l - 1)))
+    return nuv, nrw, nb
+
+
+def _node_ranks(node_ranks, levels):
+    nr = [int(r) for r in node_ranks]
+    need = (1 << (levels + 1)) - 2
+    if len(nr) != need:
+        raise ValueError(f"node_ranks has {len(nr)} entries, need 2^(levels+1) - 2 = {need}")
+    return (ctypes.c_int32 * max(need, 1))(*(nr or [0]))
+
+
+def hm_hss_noderanked_workspace_bytes(n, levels, leaf, node_ranks, nrhs) -> int:
+    out = ctypes.c_size_t(0)
+    t = make_tree(n, levels, leaf)
+    _check(load().hm_hss_noderanked_workspace_bytes(ctypes.byref(t), _node_ranks(node_ranks, levels), int(nrhs),
+                                                    ctypes.byref(out)))
+    return out.value
+
+
+def hss_matvec_noderanked(n, levels, leaf, node_ranks, D, U, V, R, W, B, X, op=0, Y=None, workspace=None,
+                          stream=None):
+    """Y = A X (op 0) or A^T X (op 1) for an HSS matrix with per-node ranks (P:264;
+    include/hm.h hss_matvec_noderanked); node (l, i) at heap index 2^l - 2 + i."""
+    import torch
+    X = _dev(X, "X")
+    nrhs = 1 if X.dim() == 1 else X.shape[1]
+    if Y is None:
+        Y = torch.empty_like(X)
+    for t_, nm in ((Y, "Y"), (D, "D"), (U, "U"), (V, "V"), (R, "R"), (W, "W"), (B, "B")):
+        _dev(t_, nm)
+    ws = _workspace(hm_hss_noderanked_workspace_bytes(n, levels, leaf, node_ranks, nrhs), workspace, X.device)
+    _xy(X, Y, n)
+    nuv, nrw, nb = hss_noderanked_sizes(n, levels, leaf, node_ranks)
+    _numel_at_least(D, n * leaf, "D")
+    for t_, c_, nm in ((U, nuv, "U"), (V, nuv, "V"), (R, nrw, "R"), (W, nrw, "W"), (B, nb, "B")):
+        _numel_at_least(t_, c_, nm)
+    t = make_tree(n, levels, leaf)
+    _check(load().hss_matvec_noderanked(ctypes.byref(t), _node_ranks(node_ranks, levels), int(op), _ptr(D), _ptr(U),
+                                        _ptr(V), _ptr(R), _ptr(W), _ptr(B), _ptr(X), nrhs, _ptr(Y), ws.data_ptr(),
+                                        ws.numel(), _stream(stream)))
     return Y

@@ -639,6 +639,149 @@ hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, cons
   return hss_leaf_phase(P, D, U, X, Y, yleaf, s, op != 0);
 }
 
+// ---- per-node ranks ----
+//
+// Node (l, i) has rank k_h, h = 2^l - 2 + i. The compact generators (layout
+// of include/hm.h hss_matvec_noderanked) are zero-padded into the per-level
+// layout with K_l = max_i k_(l,i) (pad_blocks_kernel, into the workspace) and
+// the per-level path runs on the padded copies: exact (the padded rows and
+// columns are zero), at the cost of one extra pass over the generators. Ranks
+// equal within every level need no padding (the layouts coincide).
+struct NodeRankPlan {
+  RankedPlan Q;               // the per-level plan for K_l
+  std::vector<int32_t> K;     // K[l-1], l = 1..p
+  bool per_level;             // ranks equal within each level: no padding
+  std::vector<hm::PadBlock> blocks;
+  int64_t nU, nRW, nB;        // padded sizes (doubles)
+  size_t off_U, off_V, off_R, off_W, off_B, off_tab, off_ranked, total;
+};
+
+hm_status noderank_plan(const hm_tree* tree, const int32_t* kn, int32_t nrhs, NodeRankPlan* N) {
+  hm_status st = check_tree(tree);
+  if (st) return st;
+  const int p = tree->levels;
+  const int64_t n = tree->n, b = tree->leaf;
+  if (p > 0 && !kn) return fail(HM_ERR_INVALID_ARG, "node_ranks is NULL");
+  auto h = [](int l, int64_t i) { return ((int64_t)1 << l) - 2 + i; };
+  N->K.assign(std::max(p, 1), 0);
+  N->per_level = true;
+  for (int l = 1; l <= p; ++l)
+    for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
+      const int k = kn[h(l, i)];
+      if (k < 0) return fail(HM_ERR_INVALID_ARG, "node_ranks[%lld] = %d < 0", (long long)h(l, i), k);
+      if (k > hm::kMaxRank) return fail(HM_ERR_UNSUPPORTED, "rank %d > %d", k, hm::kMaxRank);
+      N->per_level = N->per_level && k == kn[h(l, 0)];
+      N->K[l - 1] = std::max(N->K[l - 1], k);
+    }
+  if ((st = hss_ranked_plan(tree, N->K.data(), nrhs, &N->Q))) return st;
+  N->blocks.clear();
+  N->nU = N->nRW = N->nB = 0;
+  size_t off = 0;
+  if (!N->per_level && p > 0) {
+    const std::vector<int32_t>& K = N->K;
+    auto Kl = [&](int l) { return (int64_t)K[l - 1]; };
+    N->nU = n * Kl(p);
+    for (int l = 1; l < p; ++l) N->nRW += ((int64_t)1 << l) * 2 * Kl(l + 1) * Kl(l);
+    for (int l = 1; l <= p; ++l) N->nB += ((int64_t)1 << (l - 1)) * 2 * Kl(l) * Kl(l);
+    // compact source offsets walk the arrays in their order; padded ones are per-level
+    int64_t su = 0;
+    for (int64_t i = 0; i < ((int64_t)1 << p); ++i) {
+      const int k = kn[h(p, i)];
+      if (k > 0)
+        for (int a = 0; a < 2; ++a) N->blocks.push_back({su, i * b * Kl(p), (int32_t)b, k, (int32_t)Kl(p), a});
+      su += b * k;
+    }
+    int64_t srw = 0, drw = 0;
+    for (int l = 1; l < p; ++l)
+      for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
+        const int k = kn[h(l, i)], k0 = kn[h(l + 1, 2 * i)], k1 = kn[h(l + 1, 2 * i + 1)];
+        const int64_t dblk = drw + i * 2 * Kl(l + 1) * Kl(l);
+        for (int a = 2; a <= 3; ++a) {
+          if (k > 0 && k0 > 0) N->blocks.push_back({srw, dblk, k0, k, (int32_t)Kl(l), a});
+          if (k > 0 && k1 > 0)
+            N->blocks.push_back({srw + (int64_t)k0 * k, dblk + Kl(l + 1) * Kl(l), k1, k, (int32_t)Kl(l), a});
+        }
+        srw += (int64_t)(k0 + k1) * k;
+        if (i + 1 == ((int64_t)1 << l)) drw += ((int64_t)1 << l) * 2 * Kl(l + 1) * Kl(l);
+      }
+    int64_t sb = 0, db = 0;
+    for (int l = 1; l <= p; ++l)
+      for (int64_t q = 0; q < ((int64_t)1 << (l - 1)); ++q) {
+        const int k0 = kn[h(l, 2 * q)], k1 = kn[h(l, 2 * q + 1)];
+        const int64_t dblk = db + q * 2 * Kl(l) * Kl(l);
+        if (k0 > 0 && k1 > 0) {
+          N->blocks.push_back({sb, dblk, k0, k1, (int32_t)Kl(l), 4});
+          N->blocks.push_back({sb + (int64_t)k0 * k1, dblk + Kl(l) * Kl(l), k1, k0, (int32_t)Kl(l), 4});
+        }
+        sb += 2 * (int64_t)k0 * k1;
+        if (q + 1 == ((int64_t)1 << (l - 1))) db += ((int64_t)1 << (l - 1)) * 2 * Kl(l) * Kl(l);
+      }
+    N->off_U = off; off = align_up(off + sizeof(double) * (size_t)N->nU);
+    N->off_V = off; off = align_up(off + sizeof(double) * (size_t)N->nU);
+    N->off_R = off; off = align_up(off + sizeof(double) * (size_t)N->nRW);
+    N->off_W = off; off = align_up(off + sizeof(double) * (size_t)N->nRW);
+    N->off_B = off; off = align_up(off + sizeof(double) * (size_t)N->nB);
+    N->off_tab = off; off = align_up(off + sizeof(hm::PadBlock) * N->blocks.size());
+  }
+  N->off_ranked = off;
+  N->total = off + N->Q.total;
+  return HM_OK;
+}
+
+hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* w, cudaStream_t s);
+
+hm_status hss_noderank_run(const hm_tree* tree, const int32_t* kn, int op, const double* D, const double* U,
+                           const double* V, const double* R, const double* W, const double* B, const double* X,
+                           int32_t nrhs, double* Y, void* ws, size_t ws_bytes, cudaStream_t s) {
+  NodeRankPlan N;
+  hm_status st = noderank_plan(tree, kn, nrhs, &N);
+  if (st) return st;
+  if (!ws || ws_bytes < N.total || !aligned16(ws))
+    return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu (or misaligned)", ws_bytes, N.total);
+  char* w = static_cast<char*>(ws);
+  if (N.per_level)
+    return hss_ranked_run(tree, N.K.data(), op, D, U, V, R, W, B, X, nrhs, Y, w + N.off_ranked,
+                          ws_bytes - N.off_ranked, s);
+  double* pU = reinterpret_cast<double*>(w + N.off_U);
+  double* pV = reinterpret_cast<double*>(w + N.off_V);
+  double* pR = reinterpret_cast<double*>(w + N.off_R);
+  double* pW = reinterpret_cast<double*>(w + N.off_W);
+  double* pB = reinterpret_cast<double*>(w + N.off_B);
+  bool needR = false, needB = false, needU = false;
+  for (const hm::PadBlock& b : N.blocks) {
+    needU = needU || b.arr <= 1;
+    needR = needR || b.arr == 2 || b.arr == 3;
+    needB = needB || b.arr == 4;
+  }
+  if ((needU && (!U || !V)) || (needR && (!R || !W)) || (needB && !B))
+    return fail(HM_ERR_INVALID_ARG, "NULL generator pointer");
+  g_launches = 0;
+  prof_new_call();
+  if (cudaMemsetAsync(w + N.off_U, 0, N.off_tab - N.off_U, s) != cudaSuccess) return cuda_check("zero the padding");
+  if (!N.blocks.empty()) {
+    std::vector<char> img(sizeof(hm::PadBlock) * N.blocks.size());
+    memcpy(img.data(), N.blocks.data(), img.size());
+    if ((st = gen_upload_tables(img, N.off_tab, w, s))) return st;
+    hm::PadParams pp;
+    pp.blocks = reinterpret_cast<const hm::PadBlock*>(w + N.off_tab);
+    const double* srcs[5] = {U, V, R, W, B};
+    double* dsts[5] = {pU, pV, pR, pW, pB};
+    for (int a = 0; a < 5; ++a) {
+      pp.src[a] = srcs[a];
+      pp.dst[a] = dsts[a];
+    }
+    if ((st = launch("pad_blocks", s, [&] {
+           hm::pad_blocks_kernel<<<(unsigned)N.blocks.size(), hm::kThreads, 0, s>>>(pp);
+         })))
+      return st;
+  }
+  const int32_t pre = g_launches;
+  st = hss_ranked_run(tree, N.K.data(), op, D, pU, pV, pR, pW, pB, X, nrhs, Y, w + N.off_ranked,
+                      ws_bytes - N.off_ranked, s);
+  g_launches += pre;
+  return st;
+}
+
 // ---- distributed HSS ----
 
 hm_status hss_dist_plan(const hm_tree* tree, int32_t k, int32_t nrhs, const hm_part* part, int32_t flags,
@@ -839,6 +982,27 @@ hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t o
   if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
   return hss_ranked_run(tree, ranks, op, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
                         static_cast<cudaStream_t>(stream));
+}
+
+// Per-node ranks.
+hm_status hm_hss_noderanked_workspace_bytes(const hm_tree* tree, const int32_t* node_ranks, int32_t nrhs,
+                                            size_t* bytes) {
+  if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
+  NodeRankPlan N;
+  hm_status st = noderank_plan(tree, node_ranks, nrhs, &N);
+  if (st) return st;
+  *bytes = N.total;
+  return HM_OK;
+}
+
+hm_status hss_matvec_noderanked(const hm_tree* tree, const int32_t* node_ranks, int32_t op, const double* D,
+                                const double* U, const double* V, const double* R, const double* W, const double* B,
+                                const double* X, int32_t nrhs, double* Y, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  HM_NVTX("hss_matvec_noderanked");
+  if (op != 0 && op != 1) return fail(HM_ERR_INVALID_ARG, "op = %d (0: A X, 1: A^T X)", op);
+  return hss_noderank_run(tree, node_ranks, op, D, U, V, R, W, B, X, nrhs, Y, workspace, workspace_bytes,
+                          static_cast<cudaStream_t>(stream));
 }
 
 // One call, NCCL inside: Step 1 + the subtree upsweep to x of

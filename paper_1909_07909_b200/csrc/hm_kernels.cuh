@@ -472,4 +472,31 @@ static __global__ void __launch_bounds__(kThreads) hss_down_ranked_kernel(const 
   }
 }
 
+// ------------------------------------------ HSS, per-node ranks (padding) --
+// Per-node ranks run on the per-level layout with K_l = the level's
+// largest rank: every compact generator block is copied into the top-left
+// corner of its zero-filled padded block (an exact embedding: the padded
+// rows / columns are zero). CTA per block, threads over its elements.
+struct PadBlock {
+  int64_t src, dst;   // element offsets (source array / destination array)
+  int32_t rows, cols; // compact block
+  int32_t ld, arr;    // destination row stride; array id (0 U, 1 V, 2 R, 3 W, 4 B)
+};
+struct PadParams {
+  const PadBlock* blocks;
+  const double* src[5];
+  double* dst[5];
+};
+
+static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadParams P) {
+  const PadBlock b = P.blocks[blockIdx.x];
+  const double* s = P.src[b.arr] + b.src;
+  double* d = P.dst[b.arr] + b.dst;
+  const int64_t cnt = (int64_t)b.rows * b.cols;
+  for (int64_t e = threadIdx.x; e < cnt; e += kThreads) {
+    const int64_t r = e / b.cols, c = e - r * b.cols;
+    d[r * b.ld + c] = s[e];
+  }
+}
+
 }  // namespace hm

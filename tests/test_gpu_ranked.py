@@ -1,6 +1,6 @@
-"""GPU parity of the HSS product with per-level ranks through
-the C-ABI (hss_matvec_ranked), A and A^T, against the oracle's ranked product
-(pinned in test_oracle_ranked.py). Tolerance: north_star's 1e-12."""
+"""GPU parity of the HSS product with per-level and per-node ranks (
+P:264) through the C-ABI (hss_matvec_ranked, hss_matvec_noderanked), A and A^T, against
+the oracle's products (pinned in test_oracle_ranked.py). Tolerance: north_star's 1e-12."""
 import numpy as np
 import pytest
 
@@ -77,3 +77,46 @@ def test_hss_ranked_errors(hm):
     big = torch.zeros(1024 * 64, dtype=torch.float64, device="cuda")
     with pytest.raises(hm.HmError):  # op must be 0 or 1
         hm.hss_matvec_ranked(1024, 4, 64, [3, 5, 7, 8], big, big, big, big, big, big, x, op=2)
+
+
+# ---------------------------------------------------------- per-node ranks --
+
+def node_ranks_of(p, fn):
+    return [int(fn(l, i)) for l in range(1, p + 1) for i in range(1 << l)]
+
+
+NODE_CASES = [
+    # n, levels, per-node rank function (level, index), nrhs
+    (1024, 4, lambda l, i: 2 + (3 * i + l) % 7, 1),
+    (4096, 6, lambda l, i: 8 + 8 * ((i + l) % 2), 8),                  # 8 / 16 alternating: tuned paths at K_l = 16
+    (8192, 7, lambda l, i: (5 * i + 3 * l) % 11, 3),                   # rank-0 nodes
+    (1 << 15, 8, lambda l, i: 32 if (i % 4 == 0) else 16 + (i % 3), 32),
+    (4096, 6, lambda l, i: 4 * l, 2),                                  # equal within levels: the per-level path
+]
+
+
+@pytest.mark.parametrize("op", [0, 1])
+@pytest.mark.parametrize("n,p,fn,m", NODE_CASES)
+def test_hss_noderanked_vs_oracle(hm, n, p, fn, m, op):
+    kn = node_ranks_of(p, fn)
+    s = hm_inputs.hss_random_noderanked(n, p, kn, cid=52)
+    X = hm_inputs.rhs(n, m, cid=52)
+    g = [dev(a) if a.size else torch.zeros(1, dtype=torch.float64, device="cuda:0")
+         for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    Y = hm.hss_matvec_noderanked(n, p, n >> p, kn, *g, dev(X), op=op)
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec_noderanked(n, p, kn, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+def test_hss_noderanked_config4_tree(hm):
+    """The config-4 tree (n = 2^22, leaf 128, 15 levels) with per-node ranks 24..32, nrhs 32."""
+    cfg = hm_inputs.CONFIGS[4]
+    kn = node_ranks_of(cfg.levels, lambda l, i: 24 + (7 * i + l) % 9)
+    s = hm_inputs.hss_random_noderanked(cfg.n, cfg.levels, kn, cid=53)
+    X = hm_inputs.rhs(cfg.n, 32, cid=53)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    Y = hm.hss_matvec_noderanked(cfg.n, cfg.levels, cfg.leaf, kn, *g, dev(X))
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec_noderanked(cfg.n, cfg.levels, kn, s.D, s.U, s.V, s.R, s.W, s.B, X)
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL

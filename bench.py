@@ -485,6 +485,32 @@ def sweep(torch, device, wl, peak, parity=True):
                            "fp64_TFLOP/s": round(fl / (ms * 1e-3) / 1e12, 2), "matvecs/s": round(1e3 / ms, 1),
                            "column_matvecs/s": round(m * 1e3 / ms, 1)}
         del X, Y, ws
+    # HSS with per-level and per-node ranks (f4) on a 13-level tree (n = 2^20,
+    # leaf 128, nrhs 16), host-generated; every row vs the oracle
+    nr, pr, br, mr = 1 << 20, 13, 128, 16
+    lr = [32] * 4 + [24] * 4 + [16] * 5
+    kn = [16 + (7 * i + l) % 17 for l in range(1, pr + 1) for i in range(1 << l)]
+    Xr = hm_inputs.rhs(nr, mr, cid=60)
+    Xd = torch.from_numpy(Xr).to(device)
+    for tag, gen, call, ref in (
+            ("hss_per_level_ranks", lambda: hm_inputs.hss_random_ranked(nr, pr, lr, cid=60),
+             lambda g, Y: hm.hss_matvec_ranked(nr, pr, br, lr, *g, Xd, Y=Y),
+             lambda h: __import__("oracle").hss_matvec_ranked(nr, pr, lr, h.D, h.U, h.V, h.R, h.W, h.B, Xr)),
+            ("hss_per_node_ranks", lambda: hm_inputs.hss_random_noderanked(nr, pr, kn, cid=61),
+             lambda g, Y: hm.hss_matvec_noderanked(nr, pr, br, kn, *g, Xd, Y=Y),
+             lambda h: __import__("oracle").hss_matvec_noderanked(nr, pr, kn, h.D, h.U, h.V, h.R, h.W, h.B, Xr))):
+        h = gen()
+        g = [torch.from_numpy(a).to(device) for a in (h.D, h.U, h.V, h.R, h.W, h.B)]
+        Y = torch.empty_like(Xd)
+        ms = _time_call(torch, lambda: call(g, Y), 5)
+        nb = 8 * (sum(a.numel() for a in g) + 2 * nr * mr)
+        out[tag] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
+                    "tree": f"n=2^20, leaf {br}, {pr} levels, nrhs {mr}",
+                    "ranks": "32 x4, 24 x4, 16 x5 by level" if "level" in tag else "16..32 per node"}
+        if parity:
+            out[tag]["parity"] = {"relerr_vs_oracle": _relerr(Y.cpu().numpy(), ref(h)), "rows": nr}
+        del g, Y, h
+    del Xd
     # ||A||_2 of config 5 (power method on A A^*, 10 steps = 20 products)
     x0 = wl.X5[:, 0].contiguous()
     wsn = torch.empty(hm.hm_hodlr_norm2_workspace_bytes(C5.n, C5.levels, C5.leaf, h.ranks), dtype=torch.uint8,

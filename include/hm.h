@@ -14,8 +14,13 @@
  * Memory and ownership
  *   - Generator arrays, X, Y and the workspace are DEVICE pointers on the
  *     calling thread's current CUDA device, owned by the caller. The library
- *     allocates nothing, keeps no pointer after return, never synchronises the
- *     stream and never modifies an input (all inputs are const).
+ *     allocates no device memory, keeps no pointer after return, never
+ *     synchronises the stream and never modifies an input (all inputs are
+ *     const). Host-side state it does keep: a per-thread cache of general-tree
+ *     plans and a per-thread ring of 4 pinned staging buffers for the tables
+ *     those calls (and the per-node-rank HSS call) copy into the workspace;
+ *     the communicator of the multi-GPU calls owns an NCCL communicator, a
+ *     stream and two events (hm_comm_init / hm_comm_destroy).
  *   - Exception: the *_hostio variants take X and Y as HOST pointers (pinned
  *     memory recommended; pageable works but serialises) and copy them
  *     through the workspace on `stream` — the end-to-end path.

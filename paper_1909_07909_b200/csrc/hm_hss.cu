@@ -89,6 +89,11 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 #define HM_TREE_BIG_LEVEL 2048
 #endif
 constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
+// Big levels with the pair's generators staged in shared memory too
+// (hss_up_stage / hss_down_stage; 0: the register-streaming pair kernels).
+#ifndef HM_TREE_STAGE
+#define HM_TREE_STAGE 1
+#endif
 
 
 // ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
@@ -170,12 +175,16 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   constexpr int MINB_UP = (KT == 32 && NT == 4) ? HM_TREE_UP_MINB : 0;
   constexpr int MINB = (KT == 32 && NT == 4) ? HM_TREE_DN_MINB : 0;
   const size_t smem = sizeof(double) * (size_t)hm::tree_smem_doubles(KT, tp.m, NT);
+  const size_t smem_up_st = sizeof(double) * (size_t)hm::tree_up_stage_doubles(KT, tp.m, NT);
+  const size_t smem_dn_st = sizeof(double) * (size_t)hm::tree_down_stage_doubles(KT, tp.m, NT);
   static bool attrs = false;
   int sweep_blocks_per_sm = 0;
   if (!attrs) {
     allow_smem(hm::hss_up_pair_kernel<KT, NT, MINB_UP>, 200 * 1024);
     allow_smem(hm::hss_down_pair_kernel<KT, NT, MINB>, 200 * 1024);
     allow_smem(hm::hss_tree_sweep_kernel<KT, NT>, 200 * 1024);
+    allow_smem(hm::hss_up_stage_kernel<KT, NT>, 200 * 1024);
+    allow_smem(hm::hss_down_stage_kernel<KT, NT>, 200 * 1024);
     attrs = true;
   }
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sweep_blocks_per_sm, hm::hss_tree_sweep_kernel<KT, NT>, 256,
@@ -187,7 +196,13 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // upsweep: big levels up_from_l .. lbig one launch each
   for (int l = up_from_l; up && l >= lbig; --l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch(HM_NT_NAME("hss_up_pair"), s, [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
+    if (HM_TREE_STAGE && smem_up_st <= 200 * 1024) {
+      st = launch(HM_NT_NAME("hss_up_stage"), s,
+                  [&] { hm::hss_up_stage_kernel<KT, NT><<<pairs, 256, smem_up_st, s>>>(tp, l); });
+    } else {
+      st = launch(HM_NT_NAME("hss_up_pair"), s,
+                  [&] { hm::hss_up_pair_kernel<KT, NT, MINB_UP><<<pairs, 256, smem, s>>>(tp, l); });
+    }
     if (st) return st;
   }
   // small levels: up min(p-1, lbig-1) .. 1, down 1 .. min(p, lbig-1), in one
@@ -215,7 +230,13 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // downsweep: big levels lbig .. p one launch each
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    st = launch(HM_NT_NAME("hss_down_pair"), s, [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    if (HM_TREE_STAGE && smem_dn_st <= 200 * 1024) {
+      st = launch(HM_NT_NAME("hss_down_stage"), s,
+                  [&] { hm::hss_down_stage_kernel<KT, NT><<<pairs, 256, smem_dn_st, s>>>(tp, l); });
+    } else {
+      st = launch(HM_NT_NAME("hss_down_pair"), s,
+                  [&] { hm::hss_down_pair_kernel<KT, NT, MINB><<<pairs, 256, smem, s>>>(tp, l); });
+    }
     if (st) return st;
   }
   return HM_OK;

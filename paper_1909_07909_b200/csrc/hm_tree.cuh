@@ -229,6 +229,123 @@ __global__ void __launch_bounds__(256) hss_tree_sweep_kernel(const TreeParams P,
   }
 }
 
+// ------------------------------------------ big levels, generators staged --
+// The same pair tasks as tree_up_pair / tree_down_pair for the big levels (one
+// launch per level), with the node pair's generators (W; or R and the cores)
+// staged in shared memory together with the coefficient blocks: every byte a
+// CTA needs is requested at once (one cp.async wait), and the A fragments come
+// from shared memory. Strides: W rows KT + 4 (LDS.128 of rows 4q + j, columns
+// 2i: conflict-free), R / core rows KT + 8 (rows 8 rg + i, columns 8 q + 2 j).
+__host__ __device__ constexpr int tree_ws(int kt) { return kt + 4; }
+__host__ __device__ constexpr int tree_rs(int kt) { return kt + 8; }
+__host__ __device__ constexpr int64_t tree_up_stage_doubles(int kt, int m, int nt) {
+  return 4ll * kt * tree_up_stride(tree_mpad(m, nt)) + 4ll * kt * tree_ws(kt);
+}
+__host__ __device__ constexpr int64_t tree_down_stage_doubles(int kt, int m, int nt) {
+  return 3ll * kt * tree_down_stride(tree_mpad(m, nt)) + 4ll * kt * tree_rs(kt);
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) hss_up_stage_kernel(const TreeParams P, int l) {
+  extern __shared__ double sm[];
+  constexpr int MG = KT / 16, CKS = 4 / MG, NQ = KT / 2, WS = tree_ws(KT);
+  const int m = P.m, mp = tree_mpad(m, NT), zs = tree_up_stride(mp);
+  const int64_t km = (int64_t)KT * m, n0 = 2 * (int64_t)blockIdx.x;
+  double* Zc = sm;                 // the 4 children blocks
+  double* Ws = sm + 4 * KT * zs;   // W of the 2 nodes, [2][2KT][WS]
+  stage_rows_async(Zc, zs, P.xh + ((1ll << (l + 1)) - 2 + 2 * n0) * km, m, 4 * KT, m, mp);
+  stage_rows_async(Ws, WS, P.W + ((1ll << l) - 2 + n0) * 2 * KT * KT, KT, 4 * KT, KT, KT);
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3, mg = sub % MG;
+  const int i = lane >> 2, j = lane & 3;
+  constexpr int NTU = (NT * MG / 4) >= 1 ? (NT * MG / 4) : 1;
+  const double* ap = Ws + (nd * 2 * KT + j) * WS + mg * 16 + 2 * i;
+  const double* bp = Zc + nd * 2 * KT * zs + j * zs + i;
+  double* out = P.xh + ((1ll << l) - 2 + n0 + nd) * km + (int64_t)mg * 16 * m;
+  const int nck = mp / (NTU * 8);
+  for (int ck = sub / MG; ck < nck; ck += CKS) {
+    const int c0 = ck * NTU * 8;
+    double acc[2][NTU][2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NTU; ++nt) acc[t][nt][0] = acc[t][nt][1] = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < NQ; ++q) {
+      const double2 a = *reinterpret_cast<const double2*>(ap + q * 4 * WS);
+#pragma unroll
+      for (int nt = 0; nt < NTU; ++nt) {
+        const double bf = bp[q * 4 * zs + c0 + nt * 8];
+        dmma(acc[0][nt][0], acc[0][nt][1], a.x, bf);
+        dmma(acc[1][nt][0], acc[1][nt][1], a.y, bf);
+      }
+    }
+    store_transposed<1, NTU>(acc, out, m, c0, m, lane);
+  }
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256) hss_down_stage_kernel(const TreeParams P, int l) {
+  extern __shared__ double sm[];
+  constexpr int RGS = KT / 8, NQ = KT / 8, RS = tree_rs(KT);
+  const int m = P.m, mp = tree_mpad(m, NT), zs = tree_down_stride(mp);
+  const int64_t km = (int64_t)KT * m, q = blockIdx.x;
+  double* Zx = sm;                       // x of the sibling pair
+  double* Zy = sm + 2 * KT * zs;         // y of the parent
+  double* Sb = sm + 3 * KT * zs;         // the two cores [2][KT][RS]
+  double* Rb = Sb + 2 * KT * RS;         // the parent's R [2KT][RS]
+  const bool has_r = l >= 2 || P.R_root != nullptr;
+  stage_rows_async(Zx, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
+  if (l >= 2) stage_rows_async(Zy, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  else if (P.R_root) stage_rows_async(Zy, zs, P.y_root, m, KT, m, mp);
+  stage_rows_async(Sb, RS, P.B + ((1ll << (l - 1)) - 1 + q) * 2 * KT * KT, KT, 2 * KT, KT, KT);
+  if (has_r)
+    stage_rows_async(Rb, RS, l >= 2 ? P.R + ((1ll << (l - 1)) - 2 + q) * 2 * KT * KT : P.R_root, KT, 2 * KT, KT, KT);
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3;
+  const int i = lane >> 2, jj = lane & 3;
+  const double* S = Sb + (P.bt ? 1 - nd : nd) * KT * RS;
+  const double* Rw = Rb + nd * KT * RS;
+  const double* Zs = Zx + (1 - nd) * KT * zs;  // the sibling's x
+  double* yo = P.yh + ((1ll << l) - 2 + 2 * q + nd) * km;
+  const int nck = mp / (NT * 8);
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
+  for (int t = sub; t < RGS * nck; t += 4) {
+    const int rg = t % RGS, ck = t / RGS, c0 = ck * NT * 8;
+    double2 aR[NQ][1], aS[NQ][1];
+#pragma unroll
+    for (int q2 = 0; q2 < NQ; ++q2) {
+      aR[q2][0] = has_r ? *reinterpret_cast<const double2*>(Rw + (rg * 8 + i) * RS + 8 * q2 + 2 * jj)
+                        : make_double2(0.0, 0.0);
+      // adjoint: S'[row][k] = S[k][row]
+      aS[q2][0] = P.bt ? make_double2(S[(8 * q2 + 2 * jj) * RS + rg * 8 + i], S[(8 * q2 + 2 * jj + 1) * RS + rg * 8 + i])
+                       : *reinterpret_cast<const double2*>(S + (rg * 8 + i) * RS + 8 * q2 + 2 * jj);
+    }
+    double acc[1][NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
+    if (has_r) rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
+    rm_group<1, NT, false, false, NQ>(acc, aS, Zs + c0, zs, 0, NQ, colok, lane);
+    double* y = yo + (int64_t)(8 * rg + i) * m;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * jj;
+      if (c + 1 < m) {
+        y[c] = acc[0][nt][0];
+        y[c + 1] = acc[0][nt][1];
+      } else if (c < m) {
+        y[c] = acc[0][nt][0];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------- Step 1 + 3 up levels --
 // HSS Step 1 fused with the first three upsweep levels (Fig. 5 right,
 // P:684-694), nrhs <= 8 NT (one column chunk), k = KT in {16, 32}. CTA = the

@@ -89,10 +89,15 @@ hm_status hss_plan(const hm_tree* tree, int32_t k, int32_t nrhs, int32_t flags, 
 #define HM_TREE_BIG_LEVEL 2048
 #endif
 constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
-// Big levels with the pair's generators staged in shared memory too
-// (hss_up_stage / hss_down_stage; 0: the register-streaming pair kernels).
+// Big upsweep levels with the pair's W staged in shared memory too
+// (hss_up_stage; config 4: 238 vs 276 us for levels 14..11). The staged down
+// kernel (hss_down_stage) measured slower there (469 vs 428 us: 67 KB per CTA,
+// 3 CTAs per SM) and stays off; 0: the register-streaming pair kernels.
 #ifndef HM_TREE_STAGE
 #define HM_TREE_STAGE 1
+#endif
+#ifndef HM_TREE_STAGE_DOWN
+#define HM_TREE_STAGE_DOWN 0
 #endif
 
 
@@ -230,7 +235,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // downsweep: big levels lbig .. p one launch each
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
-    if (HM_TREE_STAGE && smem_dn_st <= 200 * 1024) {
+    if (HM_TREE_STAGE_DOWN && smem_dn_st <= 200 * 1024) {
       st = launch(HM_NT_NAME("hss_down_stage"), s,
                   [&] { hm::hss_down_stage_kernel<KT, NT><<<pairs, 256, smem_dn_st, s>>>(tp, l); });
     } else {

@@ -113,8 +113,8 @@ def config4(hm):
 # (nrhs 8: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch;
 # nrhs 32: vt_batched + pair launches on levels 14..11)
 C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
-           8: {"hss_vt_up", "hss_up_pair<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-           32: {"vt_batched", "hss_up_pair<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
+           8: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
+           32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
@@ -146,16 +146,21 @@ def deep_hss(hm, request):
 def deep_tree_kernels(k, m):
     """Tree-kernel instances of the p = 14 tree: GEMV levels at nrhs 1; at nrhs >= 2
     k = 16 / 32 fuse Step 1 with upsweep levels 13..11 (hss_vt_up, the rest in the
-    sweep), k = 64 runs vt_batched and the pair kernels on levels 13..11."""
+    sweep), k = 64 runs vt_batched and the staged up kernel on levels 13..11."""
     if m == 1:
         return {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"}
-    nt = "nt1" if m <= 8 else "nt2"
-    up = {"hss_vt_up"} if k in (16, 32) else {"vt_batched", f"hss_up_pair<{nt}>"}
+    nt = "nt1" if m <= 8 else ("nt2" if m <= 16 else "nt4")
+    if k in (16, 32) and m <= 16:
+        up = {"hss_vt_up"}
+    elif k == 64 and m > 16:  # the staged W would not fit in shared memory: register-streaming pair kernel
+        up = {"vt_batched", f"hss_up_pair<{nt}>"}
+    else:
+        up = {"vt_batched", f"hss_up_stage<{nt}>"}
     return up | {f"hss_down_pair<{nt}>", f"hss_tree_sweep<{nt}>"}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
-@pytest.mark.parametrize("m", [1, 2, 8, 16])
+@pytest.mark.parametrize("m", [1, 2, 8, 16, 32])
 def test_deep_hss_whole_y(hm, deep_hss, m, op):
     """p = 14 (n = 2^20, leaf 64), k in {16, 32, 64}, nrhs in {1, 2, 8, 16}: the GEMV tree
     kernels (nrhs 1), the fused Step-1 + upsweep kernel and the DMMA pair kernels with 1

@@ -14,6 +14,7 @@ Names follow the C-ABI: ``hodlr_matvec``, ``hss_matvec`` (device tensors),
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 from typing import Optional, Sequence
 
@@ -512,7 +513,11 @@ def hss_matvec_ranked(n, levels, leaf, ranks, D, U, V, R, W, B, X, op=0, Y=None,
 def hss_noderanked_sizes(n, levels, leaf, node_ranks):
     """Generator sizes (doubles) of an HSS matrix with per-node ranks (include/hm.h
     hss_matvec_noderanked): U/V, R/W, B."""
-    kn = [int(r) for r in node_ranks]
+    return _noderanked_sizes(int(n), int(levels), int(leaf), tuple(int(r) for r in node_ranks))
+
+
+@functools.lru_cache(maxsize=16)
+def _noderanked_sizes(n, levels, leaf, kn):
     h = lambda l, i: (1 << l) - 2 + i  # noqa: E731
     nuv = sum(leaf * kn[h(levels, i)] for i in range(1 << levels)) if levels else 0
     nrw = sum((kn[h(l + 1, 2 * i)] + kn[h(l + 1, 2 * i + 1)]) * kn[h(l, i)]
@@ -522,7 +527,11 @@ def hss_noderanked_sizes(n, levels, leaf, node_ranks):
 
 
 def _node_ranks(node_ranks, levels):
-    nr = [int(r) for r in node_ranks]
+    return _node_ranks_c(tuple(int(r) for r in node_ranks), int(levels))
+
+
+@functools.lru_cache(maxsize=16)
+def _node_ranks_c(nr, levels):
     need = (1 << (levels + 1)) - 2
     if len(nr) != need:
         raise ValueError(f"node_ranks has {len(nr)} entries, need 2^(levels+1) - 2 = {need}")

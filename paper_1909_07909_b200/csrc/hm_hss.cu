@@ -668,11 +668,12 @@ hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, cons
 // ---- per-node ranks ----
 //
 // Node (l, i) has rank k_h, h = 2^l - 2 + i. The compact generators (layout
-// of include/hm.h hss_matvec_noderanked) are zero-padded into the per-level
-// layout with K_l = max_i k_(l,i) (pad_blocks_kernel, into the workspace) and
-// the per-level path runs on the padded copies: exact (the padded rows and
-// columns are zero), at the cost of one extra pass over the generators. Ranks
-// equal within every level need no padding (the layouts coincide).
+// of include/hm.h hss_matvec_noderanked) are zero-padded into the uniform
+// layout with K = the largest rank of the tree (pad_blocks_kernel, into the
+// workspace) and the tuned uniform path runs on the padded copies: exact (the
+// padded rows and columns are zero), at the cost of one extra pass over the
+// generators. Ranks equal within every level need no padding (the per-level
+// layout coincides: hss_ranked_run). Plans are cached per thread (last 4).
 struct NodeRankPlan {
   RankedPlan Q;               // the per-level plan for K_l
   std::vector<int32_t> K;     // K[l-1], l = 1..p
@@ -699,6 +700,14 @@ hm_status noderank_plan(const hm_tree* tree, const int32_t* kn, int32_t nrhs, No
       N->per_level = N->per_level && k == kn[h(l, 0)];
       N->K[l - 1] = std::max(N->K[l - 1], k);
     }
+  if (!N->per_level) {
+    // pad every level to the largest rank of the tree: the uniform layout, so the
+    // tuned uniform kernels run (the per-level ranked kernels are CUDA-core
+    // thread-per-output ones: measured 2.2 ms vs ~1.0 ms on a 13-level tree)
+    int kmax = 0;
+    for (int l = 1; l <= p; ++l) kmax = std::max(kmax, N->K[l - 1]);
+    for (int l = 1; l <= p; ++l) N->K[l - 1] = kmax;
+  }
   if ((st = hss_ranked_plan(tree, N->K.data(), nrhs, &N->Q))) return st;
   N->blocks.clear();
   N->nU = N->nRW = N->nB = 0;
@@ -756,12 +765,46 @@ hm_status noderank_plan(const hm_tree* tree, const int32_t* kn, int32_t nrhs, No
 
 hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* w, cudaStream_t s);
 
+// Per-thread cache of the last 4 per-node plans (key: tree, node ranks, nrhs).
+struct NodeRankCached {
+  int64_t n, leaf;
+  int32_t p, nrhs;
+  std::vector<int32_t> kn;
+  NodeRankPlan N;
+  std::vector<char> img;
+};
+
+const NodeRankCached* noderank_cached(const hm_tree* tree, const int32_t* kn, int32_t nrhs, hm_status* st) {
+  thread_local std::vector<NodeRankCached> cache;
+  if ((*st = check_tree(tree))) return nullptr;
+  const int p = tree->levels;
+  const size_t nn = (size_t)((((int64_t)1 << (p + 1)) - 2));
+  for (size_t e = 0; e < cache.size(); ++e) {
+    const NodeRankCached& c = cache[e];
+    if (c.n == tree->n && c.leaf == tree->leaf && c.p == p && c.nrhs == nrhs && kn && c.kn.size() == nn &&
+        memcmp(c.kn.data(), kn, nn * sizeof(int32_t)) == 0) {
+      if (e) std::rotate(cache.begin(), cache.begin() + e, cache.begin() + e + 1);
+      return &cache.front();
+    }
+  }
+  NodeRankCached c;
+  c.n = tree->n; c.leaf = tree->leaf; c.p = p; c.nrhs = nrhs;
+  if ((*st = noderank_plan(tree, kn, nrhs, &c.N))) return nullptr;
+  if (kn) c.kn.assign(kn, kn + nn);
+  c.img.resize(sizeof(hm::PadBlock) * c.N.blocks.size());
+  if (!c.img.empty()) memcpy(c.img.data(), c.N.blocks.data(), c.img.size());
+  cache.insert(cache.begin(), std::move(c));
+  if (cache.size() > 4) cache.pop_back();
+  return &cache.front();
+}
+
 hm_status hss_noderank_run(const hm_tree* tree, const int32_t* kn, int op, const double* D, const double* U,
                            const double* V, const double* R, const double* W, const double* B, const double* X,
                            int32_t nrhs, double* Y, void* ws, size_t ws_bytes, cudaStream_t s) {
-  NodeRankPlan N;
-  hm_status st = noderank_plan(tree, kn, nrhs, &N);
+  hm_status st;
+  const NodeRankCached* nc = noderank_cached(tree, kn, nrhs, &st);
   if (st) return st;
+  const NodeRankPlan& N = nc->N;
   if (!ws || ws_bytes < N.total || !aligned16(ws))
     return fail(HM_ERR_WORKSPACE, "workspace %zu bytes < required %zu (or misaligned)", ws_bytes, N.total);
   char* w = static_cast<char*>(ws);
@@ -785,9 +828,7 @@ hm_status hss_noderank_run(const hm_tree* tree, const int32_t* kn, int op, const
   prof_new_call();
   if (cudaMemsetAsync(w + N.off_U, 0, N.off_tab - N.off_U, s) != cudaSuccess) return cuda_check("zero the padding");
   if (!N.blocks.empty()) {
-    std::vector<char> img(sizeof(hm::PadBlock) * N.blocks.size());
-    memcpy(img.data(), N.blocks.data(), img.size());
-    if ((st = gen_upload_tables(img, N.off_tab, w, s))) return st;
+    if ((st = gen_upload_tables(nc->img, N.off_tab, w, s))) return st;
     hm::PadParams pp;
     pp.blocks = reinterpret_cast<const hm::PadBlock*>(w + N.off_tab);
     const double* srcs[5] = {U, V, R, W, B};
@@ -1014,10 +1055,10 @@ hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t o
 hm_status hm_hss_noderanked_workspace_bytes(const hm_tree* tree, const int32_t* node_ranks, int32_t nrhs,
                                             size_t* bytes) {
   if (!bytes) return fail(HM_ERR_INVALID_ARG, "bytes is NULL");
-  NodeRankPlan N;
-  hm_status st = noderank_plan(tree, node_ranks, nrhs, &N);
+  hm_status st;
+  const NodeRankCached* nc = noderank_cached(tree, node_ranks, nrhs, &st);
   if (st) return st;
-  *bytes = N.total;
+  *bytes = nc->N.total;
   return HM_OK;
 }
 

@@ -510,14 +510,21 @@ def hss_matvec_ranked(n, levels, leaf, ranks, D, U, V, R, W, B, X, op=0, Y=None,
 
 # ------------------------------------------------- HSS, per-node ranks (f4) --
 
+def _kn_key(node_ranks) -> bytes:
+    import numpy as np
+    return np.ascontiguousarray(node_ranks, dtype=np.int32).tobytes()
+
+
 def hss_noderanked_sizes(n, levels, leaf, node_ranks):
     """Generator sizes (doubles) of an HSS matrix with per-node ranks (include/hm.h
     hss_matvec_noderanked): U/V, R/W, B."""
-    return _noderanked_sizes(int(n), int(levels), int(leaf), tuple(int(r) for r in node_ranks))
+    return _noderanked_sizes(int(n), int(levels), int(leaf), _kn_key(node_ranks))
 
 
 @functools.lru_cache(maxsize=16)
-def _noderanked_sizes(n, levels, leaf, kn):
+def _noderanked_sizes(n, levels, leaf, key):
+    import numpy as np
+    kn = np.frombuffer(key, dtype=np.int32).tolist()
     h = lambda l, i: (1 << l) - 2 + i  # noqa: E731
     nuv = sum(leaf * kn[h(levels, i)] for i in range(1 << levels)) if levels else 0
     nrw = sum((kn[h(l + 1, 2 * i)] + kn[h(l + 1, 2 * i + 1)]) * kn[h(l, i)]
@@ -527,11 +534,13 @@ def _noderanked_sizes(n, levels, leaf, kn):
 
 
 def _node_ranks(node_ranks, levels):
-    return _node_ranks_c(tuple(int(r) for r in node_ranks), int(levels))
+    return _node_ranks_c(_kn_key(node_ranks), int(levels))
 
 
 @functools.lru_cache(maxsize=16)
-def _node_ranks_c(nr, levels):
+def _node_ranks_c(key, levels):
+    import numpy as np
+    nr = np.frombuffer(key, dtype=np.int32).tolist()
     need = (1 << (levels + 1)) - 2
     if len(nr) != need:
         raise ValueError(f"node_ranks has {len(nr)} entries, need 2^(levels+1) - 2 = {need}")

@@ -718,39 +718,41 @@ hm_status noderank_plan(const hm_tree* tree, const int32_t* kn, int32_t nrhs, No
     N->nU = n * Kl(p);
     for (int l = 1; l < p; ++l) N->nRW += ((int64_t)1 << l) * 2 * Kl(l + 1) * Kl(l);
     for (int l = 1; l <= p; ++l) N->nB += ((int64_t)1 << (l - 1)) * 2 * Kl(l) * Kl(l);
-    // compact source offsets walk the arrays in their order; padded ones are per-level
+    // one entry per padded block (every padded element written once): compact
+    // source offsets walk the arrays in their order, padded ones are per-level
     int64_t su = 0;
     for (int64_t i = 0; i < ((int64_t)1 << p); ++i) {
       const int k = kn[h(p, i)];
-      if (k > 0)
-        for (int a = 0; a < 2; ++a) N->blocks.push_back({su, i * b * Kl(p), (int32_t)b, k, (int32_t)Kl(p), a});
+      for (int a = 0; a < 2; ++a)
+        N->blocks.push_back({su, i * b * Kl(p), (int32_t)b, k, (int32_t)b, (int32_t)Kl(p), a, 0});
       su += b * k;
     }
     int64_t srw = 0, drw = 0;
-    for (int l = 1; l < p; ++l)
+    for (int l = 1; l < p; ++l) {
       for (int64_t i = 0; i < ((int64_t)1 << l); ++i) {
         const int k = kn[h(l, i)], k0 = kn[h(l + 1, 2 * i)], k1 = kn[h(l + 1, 2 * i + 1)];
         const int64_t dblk = drw + i * 2 * Kl(l + 1) * Kl(l);
+        const int32_t dr = (int32_t)Kl(l + 1), dc = (int32_t)Kl(l);
         for (int a = 2; a <= 3; ++a) {
-          if (k > 0 && k0 > 0) N->blocks.push_back({srw, dblk, k0, k, (int32_t)Kl(l), a});
-          if (k > 0 && k1 > 0)
-            N->blocks.push_back({srw + (int64_t)k0 * k, dblk + Kl(l + 1) * Kl(l), k1, k, (int32_t)Kl(l), a});
+          N->blocks.push_back({srw, dblk, k0, k, dr, dc, a, 0});
+          N->blocks.push_back({srw + (int64_t)k0 * k, dblk + Kl(l + 1) * Kl(l), k1, k, dr, dc, a, 0});
         }
         srw += (int64_t)(k0 + k1) * k;
-        if (i + 1 == ((int64_t)1 << l)) drw += ((int64_t)1 << l) * 2 * Kl(l + 1) * Kl(l);
       }
+      drw += ((int64_t)1 << l) * 2 * Kl(l + 1) * Kl(l);
+    }
     int64_t sb = 0, db = 0;
-    for (int l = 1; l <= p; ++l)
+    for (int l = 1; l <= p; ++l) {
       for (int64_t q = 0; q < ((int64_t)1 << (l - 1)); ++q) {
         const int k0 = kn[h(l, 2 * q)], k1 = kn[h(l, 2 * q + 1)];
         const int64_t dblk = db + q * 2 * Kl(l) * Kl(l);
-        if (k0 > 0 && k1 > 0) {
-          N->blocks.push_back({sb, dblk, k0, k1, (int32_t)Kl(l), 4});
-          N->blocks.push_back({sb + (int64_t)k0 * k1, dblk + Kl(l) * Kl(l), k1, k0, (int32_t)Kl(l), 4});
-        }
+        const int32_t dk = (int32_t)Kl(l);
+        N->blocks.push_back({sb, dblk, k0, k1, dk, dk, 4, 0});
+        N->blocks.push_back({sb + (int64_t)k0 * k1, dblk + Kl(l) * Kl(l), k1, k0, dk, dk, 4, 0});
         sb += 2 * (int64_t)k0 * k1;
-        if (q + 1 == ((int64_t)1 << (l - 1))) db += ((int64_t)1 << (l - 1)) * 2 * Kl(l) * Kl(l);
       }
+      db += ((int64_t)1 << (l - 1)) * 2 * Kl(l) * Kl(l);
+    }
     N->off_U = off; off = align_up(off + sizeof(double) * (size_t)N->nU);
     N->off_V = off; off = align_up(off + sizeof(double) * (size_t)N->nU);
     N->off_R = off; off = align_up(off + sizeof(double) * (size_t)N->nRW);
@@ -818,15 +820,15 @@ hm_status hss_noderank_run(const hm_tree* tree, const int32_t* kn, int op, const
   double* pB = reinterpret_cast<double*>(w + N.off_B);
   bool needR = false, needB = false, needU = false;
   for (const hm::PadBlock& b : N.blocks) {
-    needU = needU || b.arr <= 1;
-    needR = needR || b.arr == 2 || b.arr == 3;
-    needB = needB || b.arr == 4;
+    const bool data = b.rows > 0 && b.cols > 0;
+    needU = needU || (data && b.arr <= 1);
+    needR = needR || (data && (b.arr == 2 || b.arr == 3));
+    needB = needB || (data && b.arr == 4);
   }
   if ((needU && (!U || !V)) || (needR && (!R || !W)) || (needB && !B))
     return fail(HM_ERR_INVALID_ARG, "NULL generator pointer");
   g_launches = 0;
   prof_new_call();
-  if (cudaMemsetAsync(w + N.off_U, 0, N.off_tab - N.off_U, s) != cudaSuccess) return cuda_check("zero the padding");
   if (!N.blocks.empty()) {
     if ((st = gen_upload_tables(nc->img, N.off_tab, w, s))) return st;
     hm::PadParams pp;

@@ -478,9 +478,10 @@ static __global__ void __launch_bounds__(kThreads) hss_down_ranked_kernel(const 
 // corner of its zero-filled padded block (an exact embedding: the padded
 // rows / columns are zero). CTA per block, threads over its elements.
 struct PadBlock {
-  int64_t src, dst;   // element offsets (source array / destination array)
-  int32_t rows, cols; // compact block
-  int32_t ld, arr;    // destination row stride; array id (0 U, 1 V, 2 R, 3 W, 4 B)
+  int64_t src, dst;     // element offsets (source array / destination array)
+  int32_t rows, cols;   // compact block (0 x 0: an all-zero padded block)
+  int32_t drows, dcols; // padded block; destination row stride = dcols
+  int32_t arr, pad;     // array id (0 U, 1 V, 2 R, 3 W, 4 B)
 };
 struct PadParams {
   const PadBlock* blocks;
@@ -488,14 +489,16 @@ struct PadParams {
   double* dst[5];
 };
 
+// Writes every element of one padded block exactly once: the compact block
+// in its top-left corner, zeros elsewhere.
 static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadParams P) {
   const PadBlock b = P.blocks[blockIdx.x];
   const double* s = P.src[b.arr] + b.src;
   double* d = P.dst[b.arr] + b.dst;
-  const int64_t cnt = (int64_t)b.rows * b.cols;
+  const int64_t cnt = (int64_t)b.drows * b.dcols;
   for (int64_t e = threadIdx.x; e < cnt; e += kThreads) {
-    const int64_t r = e / b.cols, c = e - r * b.cols;
-    d[r * b.ld + c] = s[e];
+    const int r = (int)(e / b.dcols), c = (int)(e - (int64_t)r * b.dcols);
+    d[e] = (r < b.rows && c < b.cols) ? s[(int64_t)r * b.cols + c] : 0.0;
   }
 }
 

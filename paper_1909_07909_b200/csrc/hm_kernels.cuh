@@ -495,10 +495,11 @@ static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadPa
   const PadBlock b = P.blocks[blockIdx.x];
   const double* s = P.src[b.arr] + b.src;
   double* d = P.dst[b.arr] + b.dst;
-  const int64_t cnt = (int64_t)b.drows * b.dcols;
-  for (int64_t e = threadIdx.x; e < cnt; e += kThreads) {
-    const int r = (int)(e / b.dcols), c = (int)(e - (int64_t)r * b.dcols);
-    d[e] = (r < b.rows && c < b.cols) ? s[(int64_t)r * b.cols + c] : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < b.drows; r += kThreads / 32) {  // warp per row, lanes over columns
+    const bool rok = r < b.rows;
+    for (int c = lane; c < b.dcols; c += 32)
+      d[(int64_t)r * b.dcols + c] = (rok && c < b.cols) ? s[(int64_t)r * b.cols + c] : 0.0;
   }
 }
 

@@ -21,4 +21,16 @@ $K4 > "$OUT/kb_c4.log" 2>&1
 ncu --set full --clock-control none --import-source on \
     -k regex:"vt_batched_kernel|hss_up_stage_kernel|hss_down_pair_kernel|hss_tree_sweep_kernel|leaf_mma_kernel" -c 13 \
     -o "$OUT/c4" $K4 > "$OUT/ncu_c4.log" 2>&1
+
+# the .ncu-rep files are too large to bring back (gpurun returns <= 64 MiB):
+# export the raw metrics, the details page and the per-line source page, then
+# keep only the compact exports
+for r in c5 c4; do
+  ncu -i "$OUT/$r.ncu-rep" --page raw --csv > "$OUT/$r.raw.csv" 2>/dev/null || true
+  ncu -i "$OUT/$r.ncu-rep" --page details > "$OUT/$r.details.txt" 2>/dev/null || true
+  ncu -i "$OUT/$r.ncu-rep" --page source --csv --print-source sass > "$OUT/$r.source.csv" 2>/dev/null || true
+  gzip -f "$OUT/$r.source.csv" || true
+  rm -f "$OUT/$r.ncu-rep"
+done
+du -sh "$OUT"
 echo "profile done"

@@ -68,6 +68,8 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
   P->off_yh = off; off = align_up(off + coef);
   P->off_txh = off; off = align_up(off + tcoef);
   P->off_tyh = off; off = align_up(off + tcoef);
+  P->off_flags = off;  // dataflow tree kernel: ticket + per-pair flags (hss_tree_flow_kernel)
+  if (P->mma_levels) off = align_up(off + sizeof(unsigned) * (size_t)(1 + (2ll << std::max(p, q))));
   P->off_x = P->off_y = off;
   if (flags & HM_WS_HOSTIO) {
     P->off_x = off; off = align_up(off + sizeof(double) * (size_t)(n * nrhs));
@@ -167,9 +169,69 @@ hm_status tree_gemv_dispatch(const hm::TreeGemvParams& tp, int p, int k, bool up
   return fail(HM_ERR_UNSUPPORTED, "hss tree gemv: no instance for k=%d", k);
 }
 
+// Dataflow tree kernel (hss_tree_flow_kernel): every level of both sweeps in
+// one launch, pair tasks ordered by flags instead of grid barriers. 0: the
+// per-level launches + cooperative sweep below.
+#ifndef HM_TREE_FLOW
+#define HM_TREE_FLOW 1
+#endif
+#ifndef HM_FLOW_LEVELS
+#define HM_FLOW_LEVELS 10  // levels 1..10 in the dataflow launch, the levels below one launch each
+#endif
+
+template <int KT, int NT>
+hm_status tree_flow_launch(const hm::TreeParams& tp, bool up, bool down, cudaStream_t s, int up_from,
+                           int down_last, unsigned* flags) {
+  const size_t smem = sizeof(double) * (size_t)hm::flow_smem_doubles(KT, tp.m, NT);
+  static int64_t cap = -1;  // resident CTAs of the instance (queried once)
+  if (cap < 0) {
+    allow_smem(hm::hss_tree_flow_kernel<KT, NT>, 200 * 1024);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_tree_flow_kernel<KT, NT>, 256, smem) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_tree_flow)");
+    cap = (int64_t)std::max(per_sm, 1) * num_sms();
+  }
+  const int L = up ? std::max(up_from, 0) : 0, DL = down ? std::max(down_last, 0) : 0;
+  const int64_t tasks = (L >= 1 ? (1ll << L) - 1 : 0) + (DL >= 1 ? (1ll << DL) - 1 : 0);
+  if (tasks == 0) return HM_OK;
+  const size_t fbytes = sizeof(unsigned) * (size_t)(1 + (1ll << L) + (1ll << DL));
+  if (cudaMemsetAsync(flags, 0, fbytes, s) != cudaSuccess) return cuda_check("hss_tree_flow flags");
+  hm::FlowParams fp{tp, flags, L, DL, nullptr};
+  const unsigned grid = (unsigned)std::min<int64_t>(cap, tasks);
+#if HM_FLOW_TRACE
+  // development builds: per-task timestamps of the last launch to $HM_FLOW_TRACE_FILE
+  static unsigned long long* tr = nullptr;
+  static int64_t tr_cap = 0;
+  if (tr_cap < tasks) {
+    if (tr) cudaFree(tr);
+    cudaMalloc(&tr, sizeof(unsigned long long) * 6 * (size_t)tasks);
+    tr_cap = tasks;
+  }
+  fp.trace = tr;
+#endif
+  hm_status st = launch(HM_NT_NAME("hss_tree_flow"), s,
+                        [&] { hm::hss_tree_flow_kernel<KT, NT><<<grid, 256, smem, s>>>(fp); });
+#if HM_FLOW_TRACE
+  if (st == HM_OK && getenv("HM_FLOW_TRACE_FILE")) {
+    std::vector<unsigned long long> h(6 * (size_t)tasks);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(getenv("HM_FLOW_TRACE_FILE"), "wb")) {
+      int32_t hdr[4] = {L, DL, (int32_t)grid, (int32_t)tasks};
+      fwrite(hdr, sizeof hdr, 1, f);
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+  }
+#endif
+  return st;
+}
+
 template <int KT, int NT>
 hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaStream_t s, int up_from_l,
-                      int down_last) {
+                      int down_last, unsigned* flags) {
+  const bool flow = HM_TREE_FLOW && flags && sizeof(double) * (size_t)hm::flow_smem_doubles(KT, tp.m, NT) <= 200 * 1024;
 #ifndef HM_TREE_UP_MINB
 #define HM_TREE_UP_MINB 4
 #endif
@@ -197,6 +259,7 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     return cuda_check("occupancy query (hss_tree_sweep)");
   int lbig = 1;  // first level with >= kTreeBigLevel nodes
   while (lbig <= p && (1ll << lbig) < kTreeBigLevel) ++lbig;
+  if (flow) lbig = HM_FLOW_LEVELS + 1;
   hm_status st;
   // upsweep: big levels up_from_l .. lbig one launch each
   for (int l = up_from_l; up && l >= lbig; --l) {
@@ -216,7 +279,9 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
   // a level's cost is its own dependent load / DMMA / store chain, ~5.6 us, not
   // the barrier.)
   const int up_from = up ? std::min(up_from_l, lbig - 1) : 0, down_to = down ? std::min(down_last, lbig - 1) : 0;
-  if (up_from >= 1 || down_to >= 1) {
+  if (flow && (up_from >= 1 || down_to >= 1)) {
+    if ((st = tree_flow_launch<KT, NT>(tp, up_from >= 1, down_to >= 1, s, up_from, down_to, flags))) return st;
+  } else if (up_from >= 1 || down_to >= 1) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -248,12 +313,12 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
 }
 
 hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up, bool down, cudaStream_t s,
-                        int up_from, int down_last) {
-#define HM_TREE(KT_)                                                                     \
-  if (k == KT_) {                                                                        \
-    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from, down_last);     \
-    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from, down_last);     \
-    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from, down_last);                  \
+                        int up_from, int down_last, unsigned* flags) {
+#define HM_TREE(KT_)                                                                        \
+  if (k == KT_) {                                                                           \
+    if (nt == 1) return tree_launch<KT_, 1>(tp, p, up, down, s, up_from, down_last, flags); \
+    if (nt == 2) return tree_launch<KT_, 2>(tp, p, up, down, s, up_from, down_last, flags); \
+    return tree_launch<KT_, 4>(tp, p, up, down, s, up_from, down_last, flags);              \
   }
   HM_TREE(16)
   HM_TREE(32)
@@ -266,7 +331,7 @@ hm_status tree_dispatch(const hm::TreeParams& tp, int p, int k, int nt, bool up,
 // generic per-level kernels or the DMMA tree kernels (tree_dispatch).
 hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
                          double* yh, const double* R_root, const double* y_root, bool up, bool down,
-                         cudaStream_t stream, int bt, int up_from, int down_last) {
+                         cudaStream_t stream, int bt, int up_from, int down_last, unsigned* flow_flags) {
   const int k = P.k, nrhs = P.m;
   hm_status st;
   if (up_from < 0) up_from = p - 1;  // first upsweep level to compute
@@ -277,7 +342,7 @@ hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double*
   }
   if (P.mma_levels) {
     hm::TreeParams tp{W, R, B, xh, yh, R_root, y_root, nrhs, bt};
-    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from, down_last);
+    return tree_dispatch(tp, p, k, P.nt_down, up, down, stream, up_from, down_last, flow_flags);
   }
   const int64_t km = (int64_t)k * nrhs;
   if (up)
@@ -351,8 +416,10 @@ hm_status vt_up_dispatch(const HssPlan& P, const double* V, const double* W, con
   return fail(HM_ERR_UNSUPPORTED, "hss_vt_up: no instance for k=%d", P.k);
 }
 
+// up_from_out != NULL: the tree levels are left to the caller (one launch with
+// the downsweep, hss_tree_flow_kernel), *up_from_out = the first level to compute.
 hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const double* Xd, double* xh,
-                       const double* W_root, double* x_root, cudaStream_t stream) {
+                       const double* W_root, double* x_root, cudaStream_t stream, int* up_from_out = nullptr) {
   const int k = P.k, nrhs = P.m;
   const int64_t km = (int64_t)k * nrhs;
   hm_status st;
@@ -376,6 +443,10 @@ hm_status hss_up_phase(const HssPlan& P, const double* V, const double* W, const
     vp.lev[0].partial = nullptr;
     st = (P.vt == VtPath::kGemv) ? vt_gemv_dispatch(vp, P.b, k, stream) : vt_generic(vp, P.n, stream);
     if (st) return st;
+  }
+  if (up_from_out) {
+    *up_from_out = up_from;
+    return HM_OK;
   }
   if (up_from >= 1 && (st = hss_tree_phase(P, P.p, W, nullptr, nullptr, xh, nullptr, nullptr, nullptr, true,
                                              false, stream, 0, up_from)))
@@ -519,8 +590,13 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
     if (st != HM_ERR_UNSUPPORTED) return st;  // not co-resident on this device: the level-by-level path
   }
   if (coupled) {
-    if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream))) return st;
-    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, false, true, stream, op))) return st;
+    // Step 1 (leaf x), then the upsweep levels and Steps 2-3 in one tree phase
+    int up_from = 0;
+    if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream, &up_from))) return st;
+    unsigned* fl = reinterpret_cast<unsigned*>(w + P.off_flags);
+    if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, up_from >= 1, true, stream, op,
+                             std::max(up_from, 1), -1, P.mma_levels ? fl : nullptr)))
+      return st;
   }
   const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
   if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) return st;
@@ -893,6 +969,7 @@ hm_status hss_dist_end_body(const HssPlan& P, const DistPart& d, const double* D
   double* yh = reinterpret_cast<double*>(w + P.off_yh);
   double* txh = reinterpret_cast<double*>(w + P.off_txh);
   double* tyh = reinterpret_cast<double*>(w + P.off_tyh);
+  unsigned* fl = P.mma_levels ? reinterpret_cast<unsigned*>(w + P.off_flags) : nullptr;
   const int64_t km = (int64_t)k * P.m;
   hm_status st;
   const double* yleaf = nullptr;
@@ -900,7 +977,8 @@ hm_status hss_dist_end_body(const HssPlan& P, const DistPart& d, const double* D
     // one rank: coupling + downsweep of the whole (local) tree on the x blocks
     // _begin left in the workspace, then the leaves (as in hss_matvec)
     if (!U_local || !B_sub || (P.p >= 2 && !R_sub)) return fail(HM_ERR_INVALID_ARG, "NULL U / R / B pointer");
-    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s))) return st;
+    if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, nullptr, nullptr, false, true, s, 0, -1, -1, fl)))
+      return st;
     yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
   }
   if (k > 0 && d.q > 0) {
@@ -912,11 +990,13 @@ hm_status hss_dist_end_body(const HssPlan& P, const DistPart& d, const double* D
     if (gathered != tq && cudaMemcpyAsync(tq, gathered, sizeof(double) * (size_t)(d.P * km),
                                           cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return cuda_check("copy of the gathered blocks");
-    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s))) return st;
+    if ((st = hss_tree_phase(P, d.q, W_top, R_top, B_top, txh, tyh, nullptr, nullptr, true, true, s, 0, -1, -1, fl)))
+      return st;
     const double* y_root = tyh + (((int64_t)1 << d.q) - 2 + d.rank) * km;
     if (P.p >= 1) {
       // the subtree's x blocks were left in this workspace by _begin
-      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s))) return st;
+      if ((st = hss_tree_phase(P, P.p, nullptr, R_sub, B_sub, xh, yh, R_root, y_root, false, true, s, 0, -1, -1, fl)))
+        return st;
       yleaf = yh + (((int64_t)1 << P.p) - 2) * km;
     } else {
       yleaf = y_root;

@@ -201,14 +201,15 @@ struct HssPlan {
   bool gemv_levels;  // warp-per-node GEMV tree kernels (nrhs <= 4), preferred over DMMA
   int32_t mc_vt, mc_leaf, nt_vt, nt_leaf, nt_down;
   int64_t tile;
-  size_t off_xh, off_yh, off_txh, off_tyh, off_x, off_y, total;
+  size_t off_xh, off_yh, off_txh, off_tyh, off_flags, off_x, off_y, total;
 };
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags,
                       HssPlan* P);
 hm_status hss_tree_phase(const HssPlan& P, int p, const double* W, const double* R, const double* B, double* xh,
                          double* yh, const double* R_root, const double* y_root, bool up, bool down,
-                         cudaStream_t stream, int bt = 0, int up_from = -1, int down_last = -1);
+                         cudaStream_t stream, int bt = 0, int up_from = -1, int down_last = -1,
+                         unsigned* flow_flags = nullptr);
 
 // -------------------------------------------------------------- hm_gen.cu --
 bool ranks_vary(int32_t p, const int32_t* ranks);

@@ -346,6 +346,276 @@ __global__ void __launch_bounds__(256) hss_down_stage_kernel(const TreeParams P,
   }
 }
 
+// ------------------------------------------------ dataflow tree (one launch) --
+// Every level of the upsweep and of the coupling / downsweep (Fig. 5 right,
+// P:689-716) in ONE launch without grid barriers: CTAs draw pair tasks from a
+// ticket counter in dependency order (up: level up_from .. 1, then down:
+// level 1 .. down_last) and a task waits only for the flags of the tasks it
+// reads — an up pair for its two child pairs, a down pair for its parent's pair
+// and (x computed in this launch) the up pair of its own level. A task only
+// waits for smaller tickets, which CTAs already running hold, so the schedule
+// needs no co-residency. Levels overlap: a pair starts as soon as its inputs
+// exist, not when the whole previous level is done, and the generators (W; R
+// and the cores), which never wait, are requested before the flag wait.
+//
+// flags: [0] ticket, then up flags (pair (l, r) at 2^(l-1) - 1 + r), then down
+// flags (offset 2^up_from, pair (l, q) at 2^(l-1) - 1 + q); zeroed before the
+// launch. A flag is released (bar.sync, then st.release.gpu by thread 0) once the
+// pair's blocks are stored; readers stage them with cp.async.cg / ld.cg (L2).
+struct FlowParams {
+  TreeParams T;
+  unsigned* flags;
+  int32_t up_from;    // upsweep levels up_from .. 1 (0: none)
+  int32_t down_last;  // downsweep levels 1 .. down_last (0: none)
+  unsigned long long* trace;  // HM_FLOW_TRACE builds: per task [start, waited, staged, done, signalled, smid]
+};
+#ifndef HM_FLOW_TRACE
+#define HM_FLOW_TRACE 0
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// task trace (HM_FLOW_TRACE builds only): thread 0 stamps the task's phases
+__device__ __forceinline__ void flow_stamp(unsigned long long* ft, int slot) {
+  if (HM_FLOW_TRACE && ft && threadIdx.x == 0) ft[slot] = gtimer();
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// thread 0 waits for the flags, then the CTA proceeds (bar.sync orders the
+// other threads' loads after thread 0's acquire)
+#ifndef HM_FLOW_SPLIT
+#define HM_FLOW_SPLIT 2  // independent partial sums per up-task accumulator
+#endif
+#ifndef HM_FLOW_SLEEP
+#define HM_FLOW_SLEEP 32  // ns between polls of a flag (0: spin)
+#endif
+#ifndef HM_FLOW_FENCE
+#define HM_FLOW_FENCE 0  // 1: __threadfence() before the release store (the release alone orders the CTA's stores after bar.sync)
+#endif
+__device__ __forceinline__ void flow_wait(const unsigned* f0, const unsigned* f1) {
+  if (threadIdx.x == 0) {
+    if (f0)
+      while (ld_acquire_u32(f0) == 0)
+        if (HM_FLOW_SLEEP) __nanosleep(HM_FLOW_SLEEP);
+    if (f1)
+      while (ld_acquire_u32(f1) == 0)
+        if (HM_FLOW_SLEEP) __nanosleep(HM_FLOW_SLEEP);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void flow_signal(unsigned* f) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (HM_FLOW_FENCE) __threadfence();
+    st_release_u32(f, 1u);
+  }
+}
+
+__host__ __device__ constexpr int64_t flow_smem_doubles(int kt, int m, int nt) {
+  return tree_up_stage_doubles(kt, m, nt) > tree_smem_doubles(kt, m, nt) ? tree_up_stage_doubles(kt, m, nt)
+                                                                         : tree_smem_doubles(kt, m, nt);
+}
+
+// Up pair (l, r) as hss_up_stage: W staged first, children after the wait.
+template <int KT, int NT>
+__device__ __forceinline__ void flow_up_pair(const TreeParams& P, int l, int64_t r, double* sm, const unsigned* f0,
+                                             const unsigned* f1, unsigned long long* ft) {
+  constexpr int MG = KT / 16, CKS = 4 / MG, NQ = KT / 2, WS = tree_ws(KT);
+  const int m = P.m, mp = tree_mpad(m, NT), zs = tree_up_stride(mp);
+  const int64_t km = (int64_t)KT * m, n0 = 2 * r;
+  double* Zc = sm;
+  double* Ws = sm + 4 * KT * zs;
+  stage_rows_async(Ws, WS, P.W + ((1ll << l) - 2 + n0) * 2 * KT * KT, KT, 4 * KT, KT, KT);
+  flow_wait(f0, f1);
+  flow_stamp(ft, 1);
+  stage_rows_async(Zc, zs, P.xh + ((1ll << (l + 1)) - 2 + 2 * n0) * km, m, 4 * KT, m, mp);
+  cp_async_wait_all();
+  __syncthreads();
+  flow_stamp(ft, 2);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3, mg = sub % MG;
+  const int i = lane >> 2, j = lane & 3;
+  constexpr int NTU = (NT * MG / 4) >= 1 ? (NT * MG / 4) : 1;
+  const double* ap = Ws + (nd * 2 * KT + j) * WS + mg * 16 + 2 * i;
+  const double* bp = Zc + nd * 2 * KT * zs + j * zs + i;
+  double* out = P.xh + ((1ll << l) - 2 + n0 + nd) * km + (int64_t)mg * 16 * m;
+  const int nck = mp / (NTU * 8);
+  for (int ck = sub / MG; ck < nck; ck += CKS) {
+    const int c0 = ck * NTU * 8;
+    // HM_FLOW_SPLIT independent partial sums over the k-steps: the dependent
+    // DMMA chain (the task's latency on the tree's critical path) is that much
+    // shorter; the partials are added in a fixed order at the end
+    double acc[HM_FLOW_SPLIT][2][NTU][2];
+#pragma unroll
+    for (int h = 0; h < HM_FLOW_SPLIT; ++h)
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) acc[h][t][nt][0] = acc[h][t][nt][1] = 0.0;
+#pragma unroll 2
+    for (int q0 = 0; q0 < NQ; q0 += HM_FLOW_SPLIT) {
+#pragma unroll
+      for (int h = 0; h < HM_FLOW_SPLIT; ++h) {
+        const int q = q0 + h;
+        const double2 a = *reinterpret_cast<const double2*>(ap + q * 4 * WS);
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) {
+          const double bf = bp[q * 4 * zs + c0 + nt * 8];
+          dmma(acc[h][0][nt][0], acc[h][0][nt][1], a.x, bf);
+          dmma(acc[h][1][nt][0], acc[h][1][nt][1], a.y, bf);
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 1; h < HM_FLOW_SPLIT; ++h)
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int nt = 0; nt < NTU; ++nt) {
+          acc[0][t][nt][0] += acc[h][t][nt][0];
+          acc[0][t][nt][1] += acc[h][t][nt][1];
+        }
+    store_transposed<1, NTU>(acc[0], out, m, c0, m, lane);
+  }
+}
+
+// Down pair (l, q) as tree_down_pair: the first task's R / core fragments are
+// requested before the wait, the coefficient blocks staged after it.
+template <int KT, int NT>
+__device__ __forceinline__ void flow_down_pair(const TreeParams& P, int l, int64_t q, double* sm, const unsigned* f0,
+                                               const unsigned* f1, unsigned long long* ft) {
+  constexpr int RGS = KT / 8;
+  const int m = P.m;
+  const int mp = tree_mpad(m, NT);
+  const int zs = tree_down_stride(mp);
+  const int64_t km = (int64_t)KT * m;
+  const bool root_term = (l == 1 && P.R_root != nullptr);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = w >> 2, sub = w & 3;
+  const int64_t j = 2 * q + nd;
+  const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + (P.bt ? 1 - nd : nd)) * KT * KT;
+  const double* Rw = (l >= 2) ? P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT
+                     : (root_term ? P.R_root + (int64_t)nd * KT * KT : nullptr);
+  const double* Zx = sm + (1 - nd) * KT * zs;
+  const double* Zy = sm + 2 * KT * zs;
+  double* yo = P.yh + ((1ll << l) - 2 + j) * km;
+  const int nck = mp / (NT * 8);
+  const int ntask = RGS * nck;
+  const int i = lane >> 2, jj = lane & 3;
+  constexpr int NQ = KT / 8;
+  double2 aR[NQ][1], aS[NQ][1];
+  auto load_task = [&](int t) {
+    const int rg = t % RGS;
+    const double* bR = Rw ? Rw + (int64_t)(rg * 8 + i) * KT + 2 * jj : nullptr;
+    const double* bS = P.bt ? S + (int64_t)(2 * jj) * KT + rg * 8 + i : S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
+#pragma unroll
+    for (int q2 = 0; q2 < NQ; ++q2) {
+      aR[q2][0] = bR ? ldg_stream2(bR + 8 * q2) : make_double2(0.0, 0.0);
+      aS[q2][0] = P.bt ? make_double2(ldg_stream(bS + (int64_t)8 * q2 * KT), ldg_stream(bS + (int64_t)(8 * q2 + 1) * KT))
+                       : ldg_stream2(bS + 8 * q2);
+    }
+  };
+  if (sub < ntask) load_task(sub);
+  flow_wait(f0, f1);
+  flow_stamp(ft, 1);
+  stage_rows_async(sm, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
+  if (l >= 2) stage_rows_async(sm + 2 * KT * zs, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  if (root_term) stage_rows_async(sm + 2 * KT * zs, zs, P.y_root, m, KT, m, mp);
+  cp_async_wait_all();
+  __syncthreads();
+  flow_stamp(ft, 2);
+  for (int t = sub; t < ntask; t += 4) {
+    const int rg = t % RGS, ck = t / RGS;
+    const int c0 = ck * NT * 8;
+    // the R and core terms in separate accumulators (two dependent DMMA chains
+    // of half the length, summed at the end)
+    double acc[1][NT][2], acs[1][NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = acs[0][nt][0] = acs[0][nt][1] = 0.0;
+    bool colok[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
+    if (Rw) rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
+    rm_group<1, NT, false, false, NQ>(acs, aS, Zx + c0, zs, 0, NQ, colok, lane);
+    if (t + 4 < ntask) load_task(t + 4);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      acc[0][nt][0] += acs[0][nt][0];
+      acc[0][nt][1] += acs[0][nt][1];
+    }
+    double* y = yo + (int64_t)(8 * rg + i) * m;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * jj;
+      if (c + 1 < m) {
+        y[c] = acc[0][nt][0];
+        y[c + 1] = acc[0][nt][1];
+      } else if (c < m) {
+        y[c] = acc[0][nt][0];
+      }
+    }
+  }
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256, KT >= 64 ? 1 : 2) hss_tree_flow_kernel(const FlowParams F) {
+  extern __shared__ double sm[];
+  __shared__ unsigned s_ticket;
+  const int L = F.up_from, DL = F.down_last;
+  const unsigned n_up = L >= 1 ? (1u << L) - 1 : 0u;
+  const unsigned n_all = n_up + (DL >= 1 ? (1u << DL) - 1 : 0u);
+  unsigned* upf = F.flags + 1;
+  unsigned* dnf = upf + (1u << L);
+  if (threadIdx.x == 0) s_ticket = atomicAdd(F.flags, 1u);
+  __syncthreads();
+  unsigned t = s_ticket;
+  while (t < n_all) {
+    // the next ticket is drawn while this task runs (read after its last barrier)
+    unsigned nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(F.flags, 1u);
+    unsigned long long* ft = HM_FLOW_TRACE && F.trace ? F.trace + 6ull * t : nullptr;
+    flow_stamp(ft, 0);
+    if (HM_FLOW_TRACE && ft && threadIdx.x == 0) {
+      unsigned smid;
+      asm("mov.u32 %0, %smid;" : "=r"(smid));
+      ft[5] = smid;
+    }
+    if (t < n_up) {
+      const unsigned v = (1u << L) - t;  // in (2^(l-1), 2^l]
+      const int l = 32 - __clz(v - 1);
+      const int64_t r = (int64_t)t - ((1ll << L) - (1ll << l));
+      const bool wait = l + 1 <= L;  // children computed in this launch
+      flow_up_pair<KT, NT>(F.T, l, r, sm, wait ? upf + (1u << l) - 1 + 2 * r : nullptr,
+                           wait ? upf + (1u << l) - 1 + 2 * r + 1 : nullptr, ft);
+      flow_stamp(ft, 3);
+      flow_signal(upf + (1u << (l - 1)) - 1 + r);
+    } else {
+      const unsigned u = t - n_up;
+      const int l = 32 - __clz(u + 1);
+      const int64_t q = (int64_t)u + 1 - (1ll << (l - 1));
+      const unsigned* fy = l >= 2 ? dnf + (1u << (l - 2)) - 1 + (q >> 1) : nullptr;
+      const unsigned* fx = l <= L ? upf + (1u << (l - 1)) - 1 + q : nullptr;
+      flow_down_pair<KT, NT>(F.T, l, q, sm, fy, fx, ft);
+      flow_stamp(ft, 3);
+      flow_signal(dnf + (1u << (l - 1)) - 1 + q);
+    }
+    flow_stamp(ft, 4);
+    if (threadIdx.x == 0) s_ticket = nxt;
+    __syncthreads();
+    t = s_ticket;
+    __syncthreads();  // s_ticket is rewritten at the end of the next task
+  }
+}
+
 // ---------------------------------------------------- Step 1 + 3 up levels --
 // HSS Step 1 fused with the first three upsweep levels (Fig. 5 right,
 // P:684-694), nrhs <= 8 NT (one column chunk), k = KT in {16, 32}. CTA = the

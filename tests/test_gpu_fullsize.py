@@ -113,8 +113,8 @@ def config4(hm):
 # (nrhs 8: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch;
 # nrhs 32: vt_batched + pair launches on levels 14..11)
 C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
-           8: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_pair<nt1>", "hss_tree_sweep<nt1>"},
-           32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_tree_sweep<nt4>"}}
+           8: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_pair<nt1>", "hss_tree_flow<nt1>"},
+           32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_tree_flow<nt4>"}}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
@@ -156,7 +156,10 @@ def deep_tree_kernels(k, m):
         up = {"vt_batched", f"hss_up_pair<{nt}>"}
     else:
         up = {"vt_batched", f"hss_up_stage<{nt}>"}
-    return up | {f"hss_down_pair<{nt}>", f"hss_tree_sweep<{nt}>"}
+    # the small levels (1..10) in the dataflow launch, unless its shared memory does
+    # not fit (k = 64 with 32 columns: the cooperative sweep)
+    top = f"hss_tree_sweep<{nt}>" if (k == 64 and m > 16) else f"hss_tree_flow<{nt}>"
+    return up | {f"hss_down_pair<{nt}>", top}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
@@ -175,3 +178,20 @@ def test_deep_hss_whole_y(hm, deep_hss, m, op):
     ref = oracle.hss_matvec if op == "A" else oracle.hss_matvec_t
     Yr = ref(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
     assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+@pytest.mark.parametrize("m", [2, 32])
+def test_tree_flow_repeatable(hm, deep_hss, m):
+    """The dataflow tree launch (hss_tree_flow: pair tasks ordered by flags, no grid
+    barrier) computes every block in a fixed order, so repeated products are bitwise
+    equal; a task that read a block before its producer released it would show up as
+    a difference between runs."""
+    n, p, k, s, g = deep_hss
+    if k == 64 and m > 16:
+        pytest.skip("k = 64 with 32 columns runs the cooperative sweep")
+    X = dev(hm_inputs.rhs(n, m, cid=70 + m))
+    Y0, names = traced(hm, lambda: hm.hss_matvec(n, p, 64, k, *g, X))
+    assert any(nm.startswith("hss_tree_flow") for nm in names), names
+    for _ in range(10):
+        Y = hm.hss_matvec(n, p, 64, k, *g, X)
+        assert torch.equal(Y, Y0)

@@ -400,11 +400,10 @@ def _endpoints(c, levels):
 
 
 def _leaf_block_doubles(c) -> int:
-    prev, tot = 0, 0
-    for e in c:
-        tot += (int(e) - prev) ** 2
-        prev = int(e)
-    return tot
+    """sum_i |I_i|^2 (the leaf blocks D_i) for the endpoint vector c."""
+    import numpy as np
+    sizes = np.diff(np.asarray(c, dtype=np.int64), prepend=np.int64(0))
+    return int(np.dot(sizes, sizes))
 
 
 def hm_hodlr_general_workspace_bytes(n, levels, c, ranks, nrhs) -> int:

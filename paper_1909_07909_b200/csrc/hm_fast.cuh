@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(NW * 32, 1) vt_lv_kernel(const VtParams P, int
   const int mp = (m + MC - 1) / MC * MC;
   const int XS = vt_lv_xstride(mp);
   const int sd = (int)vt_lv_stage_doubles(R, KT, nlev, mp);
-  const int64_t T = 8 * b;  // tile rows
+  const int64_t T = P.tile;  // tile rows: 8 or 4 leaves (the plan's wave balance)
   const int64_t row0 = (int64_t)blockIdx.x * T;
   const int nch = (int)(T / R);
   const int nck = mp / MC;

@@ -7,6 +7,20 @@
 
 namespace hmi {
 
+// Row tile of the many-right-hand-side V^T X (vt_lv_kernel, one CTA per SM): 8
+// leaves, or 4 when that fills the last wave of CTAs better — config 3 (512
+// 8-leaf tiles on 148 SMs: 3.46 waves, the last one 46% full) runs 1024 4-leaf
+// tiles (6.92 waves). Levels whose nodes span more than a tile reduce partials.
+int64_t lv_tile(int64_t n, int64_t b) {
+  const int64_t sms = num_sms();
+  auto eff = [&](int64_t tile) {
+    const int64_t t = n / tile;
+    return (double)t / (double)(((t + sms - 1) / sms) * sms);
+  };
+  if (n % (8 * b) != 0) return 4 * b;
+  return eff(4 * b) > eff(8 * b) + 0.02 ? 4 * b : 8 * b;
+}
+
 hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_t* ranks, int32_t nrhs,
                         int32_t flags, HodlrPlan* P, bool allow_vary = false) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
@@ -41,7 +55,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     if (!(tiles8 && b % 64 == 0 && b <= 1024))
       return fail(HM_ERR_UNSUPPORTED, "per-level ranks: uniform-tree kernels need levels >= 3 and leaf %% 64 == 0");
     P->vt = nrhs == 1 ? VtPath::kGemv : VtPath::kMma;
-    P->tile = (nrhs >= 2 && HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : 8 * b;
+    P->tile = (nrhs >= 2 && HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : (nrhs >= 2 ? lv_tile(n, b) : 8 * b);
     int mc = std::min<int32_t>(nrhs, hm::kMaxMc);
     while (mc > 1 && P->tile * mc + hm::kThreads > kSmemBudgetDoubles) --mc;
     P->mc_vt = mc;
@@ -68,7 +82,7 @@ hm_status hodlr_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, const int32_
     P->tile = 8 * b;
   } else if (nrhs >= 2 && tiles8 && b % 4 == 0 && pow2_rank((int)k, 1, 64)) {
     P->vt = VtPath::kMma;
-    P->tile = (HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : 8 * b;  // vt_lv (m >= HM_VT_LV_MIN_M) needs 8
+    P->tile = (HM_VT_TILE4 && nrhs < HM_VT_LV_MIN_M) ? 4 * b : lv_tile(n, b);
     P->nt_vt = vt_mma_nt((int)k, nrhs);
   } else {
     P->vt = VtPath::kGeneric;
@@ -157,11 +171,23 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
         rl.nodes = P.n / s;
         rl.per_node = (int32_t)(s / P.tile);
         rl.km = k * nrhs;
+        rl.block_begin = rp.blocks;
         int lg = 0;
-        while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
+        if (rl.per_node >= 512 && rl.km % 32 != 0) {
+          rl.mode = 2;  // a CTA per output
+          rp.blocks += rl.nodes * rl.km;
+        } else if (rl.km % 32 == 0) {
+          // warps per 32 outputs: ~8+ partials per warp, at most the CTA's 8 warps
+          while (lg < 3 && (1 << lg) < rl.per_node / 8) ++lg;
+          rl.mode = 1;
+          const int64_t slabs = rl.nodes * rl.km / 32, per_block = (hm::kThreads / 32) >> lg;
+          rp.blocks += (slabs + per_block - 1) / per_block;
+        } else {
+          while (lg < 5 && (1 << lg) < rl.per_node / 4) ++lg;  // ~4+ partials per lane
+          rl.mode = 0;
+          rp.blocks += ((rl.nodes * rl.km << lg) + hm::kThreads - 1) / hm::kThreads;
+        }
         rl.log2g = lg;
-        rl.thread_begin = rp.threads;
-        rp.threads += ((rl.nodes * rl.km << lg) + 31) / 32 * 32;
       }
     }
     uoff += P.n * k;
@@ -192,7 +218,7 @@ hm_status hodlr_vt_phase(const HodlrPlan& P, const int32_t* ranks, const double*
   else st = vt_generic(vp, P.n, stream);
   if (st) return st;
   if (rp.nlev > 0) {
-    const unsigned grid = (unsigned)((rp.threads + hm::kThreads - 1) / hm::kThreads);
+    const unsigned grid = (unsigned)rp.blocks;
     st = launch("reduce_partials", stream,
                 [&] { hm::reduce_partials_kernel<<<grid, hm::kThreads, 0, stream>>>(rp); });
     if (st) return st;

@@ -133,54 +133,115 @@ static __global__ void __launch_bounds__(kThreads) vt_contract_kernel(const VtPa
   }
 }
 
-// t_l[node] = sum_{j < s/tile} partial_l[node * (s/tile) + j] in a fixed order:
-// a group of G (power of two <= 32) consecutive lanes owns one output; lane g
-// sums j = g, g+G, ... sequentially, then a butterfly over the group. The
-// order depends only on the shapes, never on timing.
+// t_l[node] = sum_{j < s/tile} partial_l[node * (s/tile) + j] in a fixed order
+// that depends only on the shapes, never on timing. Two mappings, chosen per
+// level (each level owns a range of CTAs, block_begin):
+//  * mode 0 (k m < 32): a group of G = 2^log2g consecutive lanes owns one output;
+//    lane g sums j = g, g+G, ... (8 running sums), then a butterfly over the group;
+//  * mode 1 (k m a multiple of 32): a warp owns 32 consecutive outputs of one
+//    node (coalesced loads of every partial row), W = 2^log2g warps split the
+//    partials j = w, w+W, ... (8 running sums each), and the W warp sums are
+//    added in warp order through shared memory;
+//  * mode 2 (k m < 32, >= 512 partials per node, e.g. config 5's top levels): a CTA per
+//    output, the 256 threads' sums combined by warp butterflies and warp order.
 struct ReduceLevel {
   const double* partial;
   double* out;
   int64_t nodes;
-  int64_t thread_begin;  // first global thread of this level (multiple of 32)
-  int32_t per_node;      // tiles per node
-  int32_t km;            // k * m
-  int32_t log2g;         // group size G = 2^log2g
-  int32_t pad;
+  int64_t block_begin;  // first CTA of this level
+  int32_t per_node;     // tiles per node
+  int32_t km;           // k * m
+  int32_t log2g;        // mode 0: lanes per output; mode 1: warps per 32 outputs
+  int32_t mode;
 };
 struct ReduceParams {
   int32_t nlev;
-  int64_t threads;
+  int64_t blocks;
   ReduceLevel lev[kMaxLevels];
 };
 
+__device__ __forceinline__ double strided_sum8(const double* src, int64_t stride, int j, int step, int count) {
+  double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (; j + 7 * step < count; j += 8 * step) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r[u] += src[(int64_t)(j + u * step) * stride];
+  }
+  // the < 8 remaining partials, in order, through an unrolled guard (a
+  // register array indexed at run time would live in local memory)
+#pragma unroll
+  for (int u = 0; u < 7; ++u)
+    if (j + u * step < count) r[u] += src[(int64_t)(j + u * step) * stride];
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
 static __global__ void __launch_bounds__(kThreads) reduce_partials_kernel(const ReduceParams P) {
-  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  __shared__ double red[kThreads];
   int L = 0;
-  while (L + 1 < P.nlev && P.lev[L + 1].thread_begin <= t) ++L;
+  while (L + 1 < P.nlev && P.lev[L + 1].block_begin <= (int64_t)blockIdx.x) ++L;
   const ReduceLevel lv = P.lev[L];
-  const int64_t local = t - lv.thread_begin;
-  const int G = 1 << lv.log2g;
-  const int64_t oi = local >> lv.log2g;
-  const int g = (int)(local & (G - 1));
-  const bool active = t < P.threads && oi < lv.nodes * lv.km;
+  const int64_t blk = (int64_t)blockIdx.x - lv.block_begin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lv.mode == 0) {
+    const int64_t local = blk * kThreads + threadIdx.x;
+    const int G = 1 << lv.log2g;
+    const int64_t oi = local >> lv.log2g;
+    const int g = (int)(local & (G - 1));
+    const bool active = oi < lv.nodes * lv.km;
+    double s = 0.0;
+    if (active) {
+      const int64_t node = oi / lv.km;
+      const int64_t o = oi - node * lv.km;
+      const double* src = lv.partial + node * (int64_t)lv.per_node * lv.km + o;
+      double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      int j = g;
+      for (; j + 7 * G < lv.per_node; j += 8 * G) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] += src[(int64_t)(j + u * G) * lv.km];
+      }
+      for (int u = 0; j < lv.per_node; j += G, ++u) r[u] += src[(int64_t)j * lv.km];
+      s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    }
+    for (int w = 1; w < 32; w <<= 1)
+      if (w < G) s += __shfl_xor_sync(0xffffffffu, s, w);
+    if (active && g == 0) lv.out[oi] = s;
+    return;
+  }
+  if (lv.mode == 2) {
+    // one CTA per output (very long sums, few outputs): thread t sums j = t,
+    // t + 256, ...; then a butterfly per warp and the 8 warp sums in warp order
+    const int64_t oi = blk;
+    const int64_t node = oi / lv.km;
+    const int64_t o = oi - node * lv.km;
+    double s = strided_sum8(lv.partial + node * (int64_t)lv.per_node * lv.km + o, lv.km, threadIdx.x, kThreads,
+                            lv.per_node);
+    for (int w = 16; w >= 1; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int u = 1; u < kThreads / 32; ++u) t += red[u];
+      lv.out[oi] = t;
+    }
+    return;
+  }
+  const int W = 1 << lv.log2g;              // warps per slab of 32 outputs
+  const int64_t slab = blk * (kThreads / 32 / W) + warp / W;
+  const int sub = warp & (W - 1);
+  const int64_t oi = slab * 32 + lane;      // k m % 32 == 0: a slab lies in one node
+  const bool active = oi < lv.nodes * lv.km;
   double s = 0.0;
   if (active) {
     const int64_t node = oi / lv.km;
     const int64_t o = oi - node * lv.km;
-    const double* src = lv.partial + node * (int64_t)lv.per_node * lv.km + o;
-    // 8 independent running sums (loads in flight), combined in a fixed order
-    double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int j = g;
-    for (; j + 7 * G < lv.per_node; j += 8 * G) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] += src[(int64_t)(j + u * G) * lv.km];
-    }
-    for (int u = 0; j < lv.per_node; j += G, ++u) r[u] += src[(int64_t)j * lv.km];
-    s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    s = strided_sum8(lv.partial + node * (int64_t)lv.per_node * lv.km + o, lv.km, sub, W, lv.per_node);
   }
-  for (int w = 1; w < 32; w <<= 1)
-    if (w < G) s += __shfl_xor_sync(0xffffffffu, s, w);
-  if (active && g == 0) lv.out[oi] = s;
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (active && sub == 0) {
+    double t = red[threadIdx.x];
+    for (int u = 1; u < W; ++u) t += red[threadIdx.x + 32 * u];
+    lv.out[oi] = t;
+  }
 }
 
 // Distributed HODLR: after the allgather of every rank's

@@ -100,13 +100,14 @@ hm_status vt_lv_launch(const hm::VtParams& vp, int64_t b, size_t smem, cudaStrea
   constexpr int NW = HM_VT_LV_NW, NT = HM_VT_LV_NT;
   allow_smem(hm::vt_lv_kernel<KT, NT, IPW, HM_VT_LV_R, NS, NW>, smem);
   return launch("vt_lv", s, [&] {
-    hm::vt_lv_kernel<KT, NT, IPW, HM_VT_LV_R, NS, NW><<<(unsigned)(vp.n / (8 * b)), NW * 32, smem, s>>>(vp, b);
+    hm::vt_lv_kernel<KT, NT, IPW, HM_VT_LV_R, NS, NW><<<(unsigned)(vp.n / vp.tile), NW * 32, smem, s>>>(vp, b);
   });
 }
 
 hm_status vt_lv_dispatch(const hm::VtParams& vp, int64_t b, int k, cudaStream_t s) {
   constexpr int R = HM_VT_LV_R, NW = HM_VT_LV_NW, MC = 8 * HM_VT_LV_NT;
-  if (HM_VT_LV_MIN_M <= 0 || vp.m < HM_VT_LV_MIN_M || !(k == 16 || k == 32) || b % R != 0 || vp.nlev < 1)
+  if (HM_VT_LV_MIN_M <= 0 || vp.m < HM_VT_LV_MIN_M || !(k == 16 || k == 32) || b % R != 0 || vp.nlev < 1 ||
+      !(vp.tile == 8 * b || vp.tile == 4 * b))
     return HM_ERR_UNSUPPORTED;
   const int mp = (vp.m + MC - 1) / MC * MC;
   const int items = vp.nlev * (k / 16) * (mp / MC);

@@ -204,23 +204,31 @@ __global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams 
           dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[u][mp].y, bf[u][nt]);
         }
   }
-  for (; 4 * q < K; ++q) {  // masked tail
-    const int64_t row = 4 * q + j;
-    const bool ok = row < K;
-    double2 a[MPW];
-    double bf[NT];
+  if (4 * q < K) {
+    // masked tail (< QB k-steps) as one batch: every load before the DMMAs
+    double2 a[QB][MPW];
+    double bf[QB][NT];
 #pragma unroll
-    for (int mp = 0; mp < MPW; ++mp)
-      a[mp] = ok ? __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16)) : make_double2(0.0, 0.0);
+    for (int u = 0; u < QB; ++u) {
+      const int64_t row = 4 * (q + u) + j;
+      const bool ok = row < K;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bf[nt] = (ok && colok[nt]) ? __ldg(B + row * m + nt * 8) : 0.0;
+      for (int mp = 0; mp < MPW; ++mp)
+        a[u][mp] = ok ? __ldg(reinterpret_cast<const double2*>(A + row * KT + mp * 16)) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int mp = 0; mp < MPW; ++mp)
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = (ok && colok[nt]) ? __ldg(B + row * m + nt * 8) : 0.0;
+    }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[mp].x, bf[nt]);
-        dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[mp].y, bf[nt]);
-      }
+    for (int u = 0; u < QB; ++u) {
+      if (4 * (q + u) >= K) break;  // warp-uniform
+#pragma unroll
+      for (int mp = 0; mp < MPW; ++mp)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a[u][mp].x, bf[u][nt]);
+          dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a[u][mp].y, bf[u][nt]);
+        }
+    }
   }
 #pragma unroll
   for (int t = 0; t < 2 * MPW; ++t) {
@@ -405,14 +413,21 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
           for (int u = 0; u < GR; ++u) acc[u][c] = fma(d[u][v], z[c], acc[u][c]);
       }
     }
-    for (; j0 < bi; j0 += 32) {  // tail
-      double z[MC];
-      zrow<MC>(z, Z + j0 * ZS);
+    if (j0 < bi) {  // tail (< UJ chunks of 32 columns): one masked batch of loads
+      double d[GR][UJ];
 #pragma unroll
-      for (int u = 0; u < GR; ++u) {
-        const double d = __ldg(drow[u] + j0 * dstep);
+      for (int u = 0; u < GR; ++u)
 #pragma unroll
-        for (int c = 0; c < MC; ++c) acc[u][c] = fma(d, z[c], acc[u][c]);
+        for (int v = 0; v < UJ; ++v) d[u][v] = (j0 + 32 * v < bi) ? __ldg(drow[u] + (j0 + 32 * v) * dstep) : 0.0;
+#pragma unroll
+      for (int v = 0; v < UJ; ++v) {
+        if (j0 + 32 * v >= bi) break;
+        double z[MC];
+        zrow<MC>(z, Z + (j0 + 32 * v) * ZS);
+#pragma unroll
+        for (int c = 0; c < MC; ++c)
+#pragma unroll
+          for (int u = 0; u < GR; ++u) acc[u][c] = fma(d[u][v], z[c], acc[u][c]);
       }
     }
     // U segments, flattened: extended column e in [0, ktot) of segment s(e),
@@ -469,7 +484,10 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_kernel(const GenLeafParams 
 // 64-bit loads with rows / contraction indices past the block read as zero, Q
 // k-steps requested before their DMMAs.
 template <int NT, bool DT>
-__global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafParams P) {
+#ifndef HM_GEN_MMA_MINB
+#define HM_GEN_MMA_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, HM_GEN_MMA_MINB) gen_leaf_mma_kernel(const GenLeafParams P) {
   extern __shared__ double smem[];
   constexpr int MC = NT * 8, ZS = MC + 4, Q = HM_GEN_MMA_Q;
   const int64_t leaf = P.order[blockIdx.x];
@@ -537,13 +555,24 @@ __global__ void __launch_bounds__(kThreads) gen_leaf_mma_kernel(const GenLeafPar
         for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], zr[nt * 8]);
       }
     }
-    for (; 4 * q0 < bi; ++q0) {
-      const int kk = 4 * q0 + j;
-      const bool kok = kk < bi;
-      const double a = kok ? __ldg(drow + kk * dstep) : 0.0;
-      const double* zr = Z + (kok ? kk : 0) * ZS + i;
+    if (4 * q0 < bi) {
+      // the tail (< Q k-steps): one masked batch, every load requested before
+      // the first DMMA (a k-step at a time would expose a load latency each)
+      double a[Q];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a, kok ? zr[nt * 8] : 0.0);
+      for (int u = 0; u < Q; ++u) {
+        const int kk = 4 * (q0 + u) + j;
+        a[u] = kk < bi ? __ldg(drow + kk * dstep) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        if (4 * (q0 + u) >= bi) break;  // warp-uniform
+        const int kk = 4 * (q0 + u) + j;
+        const bool kok = kk < bi;
+        const double* zr = Z + (kok ? kk : 0) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kok ? zr[nt * 8] : 0.0);
+      }
     }
     // U segments, flattened over the extended columns kk in [0, ktot) (tables
     // staged above): Q k-steps of A fragments U_s(kk)[row][a(kk)] requested

@@ -108,6 +108,8 @@ def main(src, dst):
                 down += 1
             elif "sweep" in name:
                 kind, alg = "sweep (levels 1..10)", None
+            elif "tree_flow" in name:
+                kind, alg = "levels 10..1 up + 1..10 down (dataflow)", None
             else:
                 kind, alg = "leaf", alg_bytes_c4("leaf", 0)
             t = d["gpu__time_duration.sum"]

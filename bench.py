@@ -492,24 +492,27 @@ def sweep(torch, device, wl, peak, parity=True):
     kn = [16 + (7 * i + l) % 17 for l in range(1, pr + 1) for i in range(1 << l)]
     Xr = hm_inputs.rhs(nr, mr, cid=60)
     Xd = torch.from_numpy(Xr).to(device)
-    for tag, gen, call, ref in (
+    for tag, gen, wsq, call, ref in (
             ("hss_per_level_ranks", lambda: hm_inputs.hss_random_ranked(nr, pr, lr, cid=60),
-             lambda g, Y: hm.hss_matvec_ranked(nr, pr, br, lr, *g, Xd, Y=Y),
+             lambda: hm.hm_hss_ranked_workspace_bytes(nr, pr, br, lr, mr),
+             lambda g, Y, w: hm.hss_matvec_ranked(nr, pr, br, lr, *g, Xd, Y=Y, workspace=w),
              lambda hh: __import__("oracle").hss_matvec_ranked(nr, pr, lr, hh.D, hh.U, hh.V, hh.R, hh.W, hh.B, Xr)),
             ("hss_per_node_ranks", lambda: hm_inputs.hss_random_noderanked(nr, pr, kn, cid=61),
-             lambda g, Y: hm.hss_matvec_noderanked(nr, pr, br, kn, *g, Xd, Y=Y),
+             lambda: hm.hm_hss_noderanked_workspace_bytes(nr, pr, br, kn, mr),
+             lambda g, Y, w: hm.hss_matvec_noderanked(nr, pr, br, kn, *g, Xd, Y=Y, workspace=w),
              lambda hh: __import__("oracle").hss_matvec_noderanked(nr, pr, kn, hh.D, hh.U, hh.V, hh.R, hh.W, hh.B, Xr))):
         hr = gen()
         gr = [torch.from_numpy(a).to(device) for a in (hr.D, hr.U, hr.V, hr.R, hr.W, hr.B)]
         Y = torch.empty_like(Xd)
-        ms = _time_call(torch, lambda: call(gr, Y), 5)
+        wr = torch.empty(wsq(), dtype=torch.uint8, device=device)  # the caller's workspace, reused
+        ms = _time_call(torch, lambda: call(gr, Y, wr), 5)
         nb = 8 * (sum(a.numel() for a in gr) + 2 * nr * mr)
         out[tag] = {"ms": round(ms, 4), "GB/s": gbs(nb, ms), "frac_hbm": round(nb / (ms * 1e-3) / 1e9 / peak, 4),
                     "tree": f"n=2^20, leaf {br}, {pr} levels, nrhs {mr}",
                     "ranks": "32 x4, 24 x4, 16 x5 by level" if "level" in tag else "16..32 per node"}
         if parity:
             out[tag]["parity"] = {"relerr_vs_oracle": _relerr(Y.cpu().numpy(), ref(hr)), "rows": nr}
-        del gr, Y, hr
+        del gr, Y, hr, wr
     del Xd
     # ||A||_2 of config 5 (power method on A A^*, 10 steps = 20 products)
     x0 = wl.X5[:, 0].contiguous()

@@ -307,10 +307,23 @@ def _c4_leaf_roofline(per, steps, wl):
     flops = 2.0 * rows * M4 * (C4.leaf + C4.k)
     avg_ms = d[1] / d[0]
     tf = flops / (avg_ms * 1e-3) / 1e12
+    # context: what the read stream and the DMMA pipe deliver TOGETHER at this
+    # arithmetic intensity (tools/fp64_peaks.cu ridge kernel, sustained 3 s per
+    # point, profiles/r02/fp64_peaks_ridge.json), interpolated between the measured
+    # 4 and 6 flop/byte points; the kernel's physical bytes: D, U, X, Y, y
+    phys = 8.0 * rows * (C4.leaf + C4.k + 2 * M4) + 8.0 * (rows // C4.leaf) * C4.k * M4
+    inten = flops / phys
+    r4, r6 = (6961.9, 27.85), (5472.0, 32.83)  # (read GB/s, DMMA TF/s) at 4 and 6 flop/byte
+    t = min(max((inten - 4.0) / 2.0, 0.0), 1.0)
+    ridge_tf = r4[1] + t * (r6[1] - r4[1])
     return {"bound": "tensor (fp64 DMMA)", "kernel": "leaf_mma_kernel<2,4,1,4> (config-4 leaf pass: D_i X_i + U_i y_i)",
             "achieved": _fin(tf, 2), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": _fin(tf / FP64_PEAK_TFLOPS, 4),
             "peak_kind": "measured DMMA (tools/fp64_peaks.cu, profiles/r01_next/fp64_peaks_mix.json)",
-            "alg_flops_per_launch": flops, "avg_launch_ms": _fin(avg_ms, 4)}
+            "alg_flops_per_launch": flops, "avg_launch_ms": _fin(avg_ms, 4),
+            "ridge_context": {"flop_per_byte": _fin(inten, 2), "dmma_tflops_at_this_intensity": _fin(ridge_tf, 2),
+                              "frac": _fin(tf / ridge_tf, 4),
+                              "source": "profiles/r02/fp64_peaks_ridge.json: a 128-bit read stream with KD DMMAs per "
+                                        "4 loads, sustained; read and DMMA delivered together"}}
 
 
 def _fin(x, nd):

@@ -2,7 +2,8 @@
 //   (1) DFMA-only throughput (fp64 CUDA-core peak),
 //   (2) DMMA (mma.sync .f64, SASS DMMA.8x8x4) throughput (fp64 tensor peak),
 //   (3) a read-only fp64 stream over a buffer much larger than L2 (achievable read BW),
-//   (4) a read+write copy (same definition as MEASURED_PEAKS.json hbm_gbs).
+//   (4) a read+write copy (same definition as MEASURED_PEAKS.json hbm_gbs),
+//   (5) DMMA + DFMA side by side, sustained DMMA / read stream, and (6) the ridge.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peaks tools/fp64_peaks.cu
 // Prints one JSON object.
 #include <cstdio>
@@ -96,6 +97,33 @@ __global__ void mix_kernel(double* out, int iters) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// (6) The ridge: a read stream with KD DMMAs per four 128-bit loads per lane
+// (KD / 4 flop per byte), operands taken from the loaded data so neither pipe
+// can be skipped. Run back to back (sustained), it shows what the two pipes
+// deliver together under the board's power limit.
+template <int KD>
+__global__ void ridge_kernel(const double2* __restrict__ p, size_t n2, double* out) {
+  double d[8][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) d[c][0] = d[c][1] = 0.0;
+  const double b = 0.999999;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    double2 v[4] = {__ldg(p + i), __ldg(p + i + stride), __ldg(p + i + 2 * stride), __ldg(p + i + 3 * stride)};
+#pragma unroll
+    for (int c = 0; c < KD; ++c) {
+      const double a = (c & 1) ? v[(c >> 1) & 3].y : v[(c >> 1) & 3].x;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(d[c & 7][0]), "+d"(d[c & 7][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += d[c][0] + d[c][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 template <typename F>
 float time_ms(F f, int reps) {
   cudaEvent_t e0, e1;
@@ -172,9 +200,39 @@ int main() {
                               512.0 * 8 * (iters / 4) * (double)blocks * (threads / 32)) / 1e12;
   double read_sus = sustained([&] { read_kernel<<<sms * 8, 256>>>(a, n2, out); }, (double)bytes) / 1e9;
 
+  // the ridge, sustained: read GB/s and DMMA TF/s delivered together
+  char ridge_json[1024];
+  int rj = 0;
+  auto ridge = [&](auto kern, int kd) {
+    const double bytes_per = (double)bytes;
+    const double dmma_per = (double)(n2 / 4) * kd / 32.0;  // warp-instructions: KD per 4 loads per lane
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    kern(); CK(cudaDeviceSynchronize());
+    int calls = 0;
+    float total = 0.f;
+    CK(cudaEventRecord(e0));
+    while (total < 3000.f) {
+      for (int r = 0; r < 10; ++r) kern();
+      calls += 10;
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&total, e0, e1));
+    }
+    const double sec = total * 1e-3;
+    rj += snprintf(ridge_json + rj, sizeof ridge_json - rj, "%s\"kd%d\": {\"flop_per_byte\": %.2f, \"read_gbs\": %.1f, "
+                   "\"dmma_tflops\": %.2f}", rj ? ", " : "", kd, kd * 512.0 / 2048.0,
+                   bytes_per * calls / sec / 1e9, 512.0 * dmma_per * calls / sec / 1e12);
+  };
+  ridge([&] { ridge_kernel<16><<<sms * 8, 256>>>(a, n2, out); }, 16);
+  ridge([&] { ridge_kernel<24><<<sms * 8, 256>>>(a, n2, out); }, 24);
+  ridge([&] { ridge_kernel<32><<<sms * 8, 256>>>(a, n2, out); }, 32);
+
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_khz\": %d, \"dfma_tflops\": %.3f, \"dmma_m8n8k4_tflops\": %.3f, "
          "\"dmma_plus_dfma_tflops\": %.3f, \"read_stream_gbs\": %.1f, \"copy_rw_gbs\": %.1f, "
-         "\"dmma_m8n8k4_tflops_sustained\": %.3f, \"read_stream_gbs_sustained\": %.1f}\n",
-         prop.name, sms, prop.clockRate, dfma_tflops, dmma_tflops, mix_tflops, read_gbs, copy_gbs, dmma_sus, read_sus);
+         "\"dmma_m8n8k4_tflops_sustained\": %.3f, \"read_stream_gbs_sustained\": %.1f, "
+         "\"ridge_sustained\": {%s}}\n",
+         prop.name, sms, prop.clockRate, dfma_tflops, dmma_tflops, mix_tflops, read_gbs, copy_gbs, dmma_sus, read_sus,
+         ridge_json);
   return 0;
 }

@@ -194,3 +194,37 @@ def test_hss_to_hodlr_rejects_overlap(hm):
         hm.hss_to_hodlr(256, 2, 64, 4, *g, Uh=g[0].new_empty(2 * 256 * 4), Vh=None)  # fine
         big = torch.empty(2 * 256 * 4, dtype=torch.float64, device="cuda")
         hm.hss_to_hodlr(256, 2, 64, 4, *g, Uh=big, Vh=big)  # same buffer twice
+
+
+def test_hss_dataflow_tree_graph_capture(hm):
+    """The dataflow tree launch (flags zeroed by a memset on the caller's stream, then
+    hss_tree_flow) inside a CUDA graph: a 12-level tree with nrhs 16 (levels 1..10 in
+    the flow launch), captured once and replayed twice, gives the eager product's bits."""
+    n, p, leaf, k, m = 1 << 18, 12, 64, 16, 16
+    s = hm_inputs.hss_random(n, p, k, cid=47)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    X = dev(hm_inputs.rhs(n, m, cid=47))
+    ws = torch.empty(hm.hm_hss_workspace_bytes(n, p, leaf, k, m), dtype=torch.uint8, device="cuda")
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    Y0 = hm.hss_matvec(n, p, leaf, k, *g, X, workspace=ws).clone()
+    torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    assert any(t[0].startswith("hss_tree_flow") for t in hm.hm_profile_collect())
+    Y = torch.empty_like(X)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        hm.hss_matvec(n, p, leaf, k, *g, X, Y=Y, workspace=ws)
+    torch.cuda.current_stream().wait_stream(side)
+    Y.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        hm.hss_matvec(n, p, leaf, k, *g, X, Y=Y, workspace=ws)
+    for _ in range(2):
+        Y.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(Y, Y0)
+    Yr = oracle.hss_matvec(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, hm_inputs.rhs(n, m, cid=47))
+    assert float(np.linalg.norm(Y0.cpu().numpy() - Yr) / np.linalg.norm(Yr)) <= TOL

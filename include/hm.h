@@ -423,11 +423,17 @@ int32_t hm_last_launch_count(void);
  * bracketed by two CUDA events recorded on the launch's stream (no
  * synchronisation, ~1 us of host work per launch). hm_profile_collect waits
  * for the recorded events, writes up to `cap` records in launch order and
- * clears the trace. `call` numbers the matvec calls since the trace began. */
+ * clears the trace. `call` numbers the matvec calls since the trace began.
+ * `start_ms` places every record on one device timeline (it is measured from
+ * the first record's start event, whatever stream either was recorded on), so
+ * records of different streams — the distributed product's exchange on the
+ * communicator's stream ("nccl_allgather") and the kernels on the caller's
+ * stream — show whether they overlapped. */
 typedef struct {
   char name[40];  /* kernel name, e.g. "leaf_apply", "vt_contract" */
   int32_t call;   /* index of the matvec call that launched it      */
   float ms;       /* device time between the bracketing events      */
+  float start_ms; /* start event minus the trace's first start event */
 } hm_launch_record;
 
 hm_status hm_profile_enable(int32_t on);

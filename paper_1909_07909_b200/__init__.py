@@ -54,7 +54,8 @@ class hm_tree(ctypes.Structure):
 
 
 class hm_launch_record(ctypes.Structure):
-    _fields_ = [("name", ctypes.c_char * 40), ("call", ctypes.c_int32), ("ms", ctypes.c_float)]
+    _fields_ = [("name", ctypes.c_char * 40), ("call", ctypes.c_int32), ("ms", ctypes.c_float),
+                ("start_ms", ctypes.c_float)]
 
 
 _lib: Optional[ctypes.CDLL] = None
@@ -129,10 +130,17 @@ def hm_profile_enable(on: bool = True) -> None:
 
 def hm_profile_collect(cap: int = 1 << 16):
     """[(kernel name, call index, ms)] in launch order; clears the trace."""
+    return [(nm, c, ms) for nm, c, _, ms in hm_profile_timeline(cap)]
+
+
+def hm_profile_timeline(cap: int = 1 << 16):
+    """[(kernel name, call index, start_ms, ms)] in launch order, start_ms on one
+    device timeline across streams (include/hm.h); clears the trace."""
     buf = (hm_launch_record * cap)()
     cnt = ctypes.c_int32(0)
     _check(load().hm_profile_collect(buf, cap, ctypes.byref(cnt)))
-    return [(buf[i].name.decode(), int(buf[i].call), float(buf[i].ms)) for i in range(min(cnt.value, cap))]
+    return [(buf[i].name.decode(), int(buf[i].call), float(buf[i].start_ms), float(buf[i].ms))
+            for i in range(min(cnt.value, cap))]
 
 
 def _check(rc: int) -> None:

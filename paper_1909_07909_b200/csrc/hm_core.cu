@@ -140,13 +140,15 @@ hm_status hm_profile_collect(hm_launch_record* out, int32_t cap, int32_t* count)
   hm_status st = HM_OK;
   for (const TraceRec& r : g_prof_recs) {
     if (n < cap) {
-      float ms = 0.f;
-      if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess)
+      float ms = 0.f, t0 = 0.f;
+      if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess ||
+          cudaEventElapsedTime(&t0, g_prof_recs.front().a, r.a) != cudaSuccess)
         st = cuda_check("hm_profile_collect");
       memset(&out[n], 0, sizeof out[n]);
       strncpy(out[n].name, r.name, sizeof out[n].name - 1);
       out[n].call = r.call;
       out[n].ms = ms;
+      out[n].start_ms = t0;
     }
     ++n;
     g_prof_pool.push_back(r.a);

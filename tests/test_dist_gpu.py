@@ -244,3 +244,35 @@ def test_c_dist_example_on_gpu(hm, tmp_path):
     out = subprocess.run([exe, str(P)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "all ranks OK" in out.stdout
+
+
+def test_trace_timeline_across_streams(hm, comm):
+    """hm_profile_timeline puts the exchange (communicator stream) and the caller's
+    kernels on one device timeline: starts are measured from the first record, and
+    a kernel queued behind the exchange on the same caller stream starts after it."""
+    from paper_1909_07909_b200 import dist as hd
+    n, p, b, k, m = 1 << 16, 8, 256, 16, 8
+    h = hm_inputs.hodlr_random(n, p, [k] * p, cid=25)
+    D, U, V, Xd = dev(h.D), dev(h.U), dev(h.V), dev(hm_inputs.rhs(n, m, cid=25))
+    x = torch.arange(1 << 20, dtype=torch.float64, device="cuda:0")
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    hm.hodlr_matvec(n, p, b, h.ranks, D, U, V, Xd)
+    y = comm.allgather(x)                      # caller stream waits for the exchange
+    hm.hodlr_matvec(n, p, b, h.ranks, D, U, V, Xd)
+    torch.cuda.synchronize()
+    hm.hm_profile_enable(False)
+    tr = hm.hm_profile_timeline()
+    assert torch.equal(x, y)
+    assert tr[0][2] == 0.0
+    names = [t[0] for t in tr]
+    ix = names.index("nccl_allgather")
+    _, _, t_ex, ms_ex = tr[ix]
+    first = [t for t in tr[:ix]]
+    after = [t for t in tr[ix + 1:]]
+    assert first and after
+    eps = 2e-3  # ms: event resolution
+    assert t_ex + eps >= first[-1][2] + first[-1][3]           # ordered after the caller's work
+    assert all(t[2] + eps >= t_ex + ms_ex for t in after)      # the next call waited for it
+    for a, c in zip(tr[:ix - 1], tr[1:ix]):                     # one stream: records do not overlap
+        assert c[2] + eps >= a[2] + a[3]

@@ -195,3 +195,75 @@ def test_tree_flow_repeatable(hm, deep_hss, m):
     for _ in range(10):
         Y = hm.hss_matvec(n, p, 64, k, *g, X)
         assert torch.equal(Y, Y0)
+
+
+# ------------------------------------------- componentwise error bound --
+# SURVEY §8(c) "Componentwise bound": with G = the oracle run on |generators| and
+# |X| (so G >= |A_rep| |X| entrywise, formed in the fast algorithm's own
+# association, |U| (|V|^T |X|)), both the GPU product and the oracle satisfy
+# |Y - A_rep X| <= gamma_L G entrywise (standard summation error bound, any
+# summation order), hence |Y_gpu - Y_ref| <= 2 gamma_L G with
+# gamma_L = L u / (1 - L u), u = 2^-53, L the longest chain of sequential
+# floating-point operations feeding one output entry. Unlike the normwise check
+# this catches an error in an entry that is small against ||Y||.
+
+U_ROUND = 2.0 ** -53
+
+
+def gamma(L):
+    return L * U_ROUND / (1.0 - L * U_ROUND)
+
+
+def hodlr_chain(n, p, b, k):
+    """HODLR: max(leaf row, V^T x over the largest sibling block + the U t sum) plus
+    one addition per level and the leaf term."""
+    return max(b, (n >> 1) + k) + p + 1
+
+
+def hss_chain(p, b, k):
+    """HSS (Fig. 5 right): x-hat of a level-1 node = a leaf V^T x (b terms)
+    followed by p - 1 upsweep products of 2k terms; the coupling (k) and each
+    downsweep step (k + 1: R y-hat plus the coupling term) down to the leaf; U y-hat
+    (k) plus d (b)."""
+    return b + 2 * k * p + k + (k + 1) * p + k + b + 2
+
+
+def assert_componentwise(Y, Yr, G, L):
+    bound = 2.0 * gamma(L) * G
+    viol = np.abs(Y - Yr) > bound
+    assert not viol.any(), (int(viol.sum()), float(np.max(np.abs(Y - Yr) / np.maximum(bound, 1e-300))))
+
+
+@pytest.mark.parametrize("m", [1, 8, 64])
+def test_config3_componentwise(hm, config3, m):
+    cfg, h, (D, U, V) = config3
+    X = hm_inputs.rhs(cfg.n, m, cid=33)
+    Y = hm.hodlr_matvec(cfg.n, cfg.levels, cfg.leaf, h.ranks, D, U, V, dev(X))
+    torch.cuda.synchronize()
+    Yr = oracle.hodlr_matvec(cfg.n, cfg.levels, h.ranks, h.D, h.U, h.V, X)
+    G = oracle.hodlr_matvec(cfg.n, cfg.levels, h.ranks, np.abs(h.D), np.abs(h.U), np.abs(h.V), np.abs(X))
+    assert_componentwise(Y.cpu().numpy(), Yr, G, hodlr_chain(cfg.n, cfg.levels, cfg.leaf, cfg.k))
+
+
+def test_config4_componentwise(hm, config4):
+    cfg, s, g = config4
+    m = cfg.nrhs[0]
+    X = hm_inputs.rhs(cfg.n, m, cid=44)
+    Y = hm.hss_matvec(cfg.n, cfg.levels, cfg.leaf, cfg.k, *g, dev(X))
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec(cfg.n, cfg.levels, cfg.k, s.D, s.U, s.V, s.R, s.W, s.B, X)
+    a = {f: np.abs(getattr(s, f)) for f in ("D", "U", "V", "R", "W", "B")}
+    G = oracle.hss_matvec(cfg.n, cfg.levels, cfg.k, a["D"], a["U"], a["V"], a["R"], a["W"], a["B"], np.abs(X))
+    assert_componentwise(Y.cpu().numpy(), Yr, G, hss_chain(cfg.levels, cfg.leaf, cfg.k))
+
+
+@pytest.mark.parametrize("m", [1, 16])
+def test_deep_hss_componentwise(hm, deep_hss, m):
+    n, p, k, s, g = deep_hss
+    X = hm_inputs.rhs(n, m, cid=90 + m)
+    Y = hm.hss_matvec(n, p, 64, k, *g, dev(X))
+    torch.cuda.synchronize()
+    Yr = oracle.hss_matvec(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
+    a = {f: np.abs(getattr(s, f)) for f in ("D", "U", "V", "R", "W", "B")}
+    G = oracle.hss_matvec(n, p, k, a["D"], a["U"], a["V"], a["R"], a["W"], a["B"], np.abs(X))
+    assert_componentwise(Y.cpu().numpy(), Yr, G, hss_chain(p, 64, k))

@@ -254,6 +254,13 @@ hm_status gen_leaf_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t 
 #endif
 template <int NT, bool DT>
 hm_status gen_leaf_mma_launch(const hm::GenLeafParams& lp, int64_t nleaves, int64_t smax, cudaStream_t s) {
+  if constexpr (!DT) {  // 128-bit A fragments (hm_general.cuh gen_leaf_mma_al_kernel)
+    const size_t smem =
+        sizeof(double) * (size_t)((smax + lp.ktot) * hm::gen_al_zs(NT)) + hm::gen_al_tab_bytes(lp.ktot);
+    allow_smem(hm::gen_leaf_mma_al_kernel<NT>, smem);
+    dim3 grid((unsigned)nleaves, (unsigned)((lp.m + NT * 8 - 1) / (NT * 8)));
+    return launch("gen_leaf_mma", s, [&] { hm::gen_leaf_mma_al_kernel<NT><<<grid, hm::kThreads, smem, s>>>(lp); });
+  }
   const size_t smem = sizeof(double) * (size_t)((smax + lp.ktot) * (NT * 8 + 4)) + 16 * (size_t)lp.ktot + 16;
   allow_smem(hm::gen_leaf_mma_kernel<NT, DT>, std::max<size_t>(smem, 1));
   dim3 grid((unsigned)nleaves, (unsigned)((lp.m + NT * 8 - 1) / (NT * 8)));

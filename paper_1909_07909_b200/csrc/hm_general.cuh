@@ -606,4 +606,202 @@ __global__ void __launch_bounds__(kThreads, HM_GEN_MMA_MINB) gen_leaf_mma_kernel
   }
 }
 
+// gen_leaf_mma with 128-bit A fragments (Y = A X; the adjoint keeps the kernel
+// above). A ragged leaf block D_i (b x b, any b, any offset in D) has rows that
+// start on 8-byte boundaries only, so a 16-byte load of D[row][c, c+1] is legal
+// only where (address of D[row][0]) / 8 + c is even. A tile's 8 rows are chosen
+// to share that parity sigma — 8 consecutive rows when b is even, the rows of
+// one parity of a 16-row block when b is odd (row 16 B + 2 i + par) — and the
+// contraction runs over columns sigma + 8 g + [0, 8) in groups: lane (i, j)
+// loads D[row_i][sigma + 8 g + 2 j, + 1] (one LDG.128: ".x" feeds k-step 2 g,
+// ".y" k-step 2 g + 1, B rows sigma + 8 g + 2 j (+ 1) of the staged Z — the
+// k-permutation of warp_rowmajor_mma). The columns left over (column 0 when
+// sigma = 1, the < 8 after the last group) form two masked 64-bit k-steps.
+// U segments with k % 8 == 0 and a 16-byte aligned base stream the same way
+// (8-column groups, flattened over the segments through a group table); the
+// others fall back to 64-bit fragments per extended column.
+// Shared memory: Z [(smax + ktot)][ZS], ZS = 8 NT + 2 (rows 2 j apart:
+// conflict-free 64-bit B fragments), then the group table (pointer, row stride,
+// Z row) and the per-column table of the fallback segments.
+#ifndef HM_GEN_AL_QG
+#define HM_GEN_AL_QG 8  // 8-column groups per batch of loads
+#endif
+#ifndef HM_GEN_AL_PIPE
+#define HM_GEN_AL_PIPE 0  // 1: ping-pong the batches (measured slower: cr8 738 -> 779 us at QG 4)
+#endif
+#ifndef HM_GEN_AL_MINB
+#define HM_GEN_AL_MINB 3  // CTAs per SM for NT = 1
+#endif
+__host__ __device__ constexpr int gen_al_zs(int nt) { return 8 * nt + 2; }
+__host__ __device__ constexpr size_t gen_al_tab_bytes(int ktot) { return 32 * (size_t)ktot + 64; }
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, NT == 1 ? HM_GEN_AL_MINB : 1) gen_leaf_mma_al_kernel(const GenLeafParams P) {
+  extern __shared__ double smem[];
+  constexpr int MC = NT * 8, ZS = gen_al_zs(NT), QG = HM_GEN_AL_QG;  // 8-column groups per pipeline stage
+  const int64_t leaf = P.order[blockIdx.x];
+  const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
+  if (b == 0) return;
+  const int c0 = blockIdx.y * MC;
+  const int m = P.m, mc = min(MC, m - c0);
+  double* Z = smem;  // [(b + ktot)][ZS]
+  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
+    const int64_t r = e / MC;
+    const int c = (int)(e - r * MC);
+    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * m + c0 + c] : 0.0;
+  }
+  int64_t off = b;
+  for (int s = 0; s < P.nseg; ++s) {
+    const LeafSeg sg = P.seg[s];
+    const double* T = sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m;
+    for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
+      const int a = e / MC, c = e - a * MC;
+      Z[(off + a) * ZS + c] = (c < mc) ? T[a * m + c0 + c] : 0.0;
+    }
+    off += sg.k;
+  }
+  // tables: groups of 8 rank columns of the 128-bit segments, single columns of the others
+  const int kt = P.ktot;
+  const double** gbase = reinterpret_cast<const double**>(Z + (b + kt) * ZS);
+  const double** sbase = gbase + (kt / 8 + 1);
+  int* gk = reinterpret_cast<int*>(sbase + kt + 1);
+  int* gz = gk + (kt / 8 + 1);
+  int* sk = gz + (kt / 8 + 1);
+  int* sz = sk + kt + 1;
+  int ng = 0, ns = 0;  // every thread derives the counts (same loop, no synchronisation needed)
+  {
+    int zrow = (int)b;
+    for (int s2 = 0; s2 < P.nseg; ++s2) {
+      const LeafSeg sg = P.seg[s2];
+      const bool wide = (sg.k % 8 == 0) && ((reinterpret_cast<uintptr_t>(sg.A) & 15) == 0);
+      if (wide) {
+        for (int g = threadIdx.x; g < sg.k / 8; g += kThreads) {
+          gbase[ng + g] = sg.A + 8 * g;
+          gk[ng + g] = sg.k;
+          gz[ng + g] = zrow + 8 * g;
+        }
+        ng += sg.k / 8;
+      } else {
+        for (int a2 = threadIdx.x; a2 < sg.k; a2 += kThreads) {
+          sbase[ns + a2] = sg.A + a2;
+          sk[ns + a2] = sg.k;
+          sz[ns + a2] = zrow + a2;
+        }
+        ns += sg.k;
+      }
+      zrow += sg.k;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = lane >> 2, j = lane & 3;
+  const double* Di = P.D + P.doff[leaf];
+  const bool bodd = (b & 1) != 0;
+  const int64_t ntile = bodd ? 2 * ((b + 15) / 16) : (b + 7) / 8;
+  const int bi = (int)b;
+  for (int64_t t = warp; t < ntile; t += kThreads / 32) {
+    const int64_t row0 = bodd ? 16 * (t >> 1) + (t & 1) : 8 * t;
+    if (row0 >= b) continue;  // warp-uniform: a parity tile past the block
+    const int64_t row = bodd ? row0 + 2 * i : row0 + i;
+    const bool rok = row < b;
+    const int64_t rr = rok ? row : row0;  // same parity as the tile's rows
+    const double* drow = Di + rr * b;
+    const int sig = (int)((reinterpret_cast<uintptr_t>(Di + row0 * b) >> 3) & 1);
+    double acc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    // 8-column groups: the b-sigma aligned columns of D_i (x < G), then the
+    // 128-bit U groups (x >= G), one software pipeline over both — the next QG
+    // groups' loads are in flight while the current QG feed the tensor pipe
+    const int G = (bi - sig) / 8;
+    const int NG = G + ng;
+    const int64_t grow = r0 + rr;
+    const double* da = drow + sig + 2 * j;
+    auto gload = [&](double2 (&a)[QG], int x0) {
+#pragma unroll
+      for (int u = 0; u < QG; ++u) {
+        const int x = x0 + u;
+        a[u] = x >= NG  ? make_double2(0.0, 0.0)
+               : x < G ? ld_a_stream2(da + 8 * x)
+                       : ld_a_stream2(gbase[x - G] + grow * gk[x - G] + 2 * j);
+      }
+    };
+    auto gmma = [&](const double2 (&a)[QG], int x0) {
+#pragma unroll
+      for (int u = 0; u < QG; ++u) {
+        const int x = x0 + u;
+        if (x >= NG) break;  // warp-uniform
+        const double* zr = Z + (int64_t)((x < G ? sig + 8 * x : gz[x - G]) + 2 * j) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].x, zr[nt * 8]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].y, zr[ZS + nt * 8]);
+      }
+    };
+    if constexpr (HM_GEN_AL_PIPE) {
+      double2 a0[QG], a1[QG];
+      gload(a0, 0);
+      for (int x0 = 0; x0 < NG; x0 += 2 * QG) {
+        gload(a1, x0 + QG);
+        gmma(a0, x0);
+        if (x0 + QG >= NG) break;
+        gload(a0, x0 + 2 * QG);
+        gmma(a1, x0 + QG);
+      }
+    } else {  // batches: QG groups' loads, then their DMMAs
+      for (int x0 = 0; x0 < NG; x0 += QG) {
+        double2 a[QG];
+        gload(a, x0);
+        gmma(a, x0);
+      }
+    }
+    // leftover columns of D_i: 0 (sigma = 1) and [sigma + 8 G, b): at most 8, two masked k-steps
+    {
+      const int nrem = bi - 8 * G;  // = sig + (b - sig - 8 G)
+      double a2[2];
+      int col[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int sl = 4 * u + j;
+        col[u] = (sig && sl == 0) ? 0 : 8 * G + sl;  // sigma = 1: slot 0 is column 0, slot s > 0 column 8 G + s
+        a2[u] = sl < nrem ? drow[col[u]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (4 * u >= nrem) break;  // warp-uniform
+        const bool ok = 4 * u + j < nrem;
+        const double* zr = Z + (int64_t)(ok ? col[u] : 0) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a2[u], ok ? zr[nt * 8] : 0.0);
+      }
+    }
+    // U segments with 64-bit fragments (k % 8 != 0 or an unaligned base)
+    for (int q0 = 0; 4 * q0 < ns; q0 += 2 * QG) {
+      double a[2 * QG];
+#pragma unroll
+      for (int u = 0; u < 2 * QG; ++u) {
+        const int kk = 4 * (q0 + u) + j;
+        a[u] = kk < ns ? __ldg(sbase[kk] + grow * sk[kk]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2 * QG; ++u) {
+        if (4 * (q0 + u) >= ns) break;
+        const int kk = 4 * (q0 + u) + j;
+        const double* zr = Z + (int64_t)(kk < ns ? sz[kk] : 0) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < ns ? zr[nt * 8] : 0.0);
+      }
+    }
+    if (rok) {
+      double* y = P.Y + (r0 + row) * m + c0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt * 8 + 2 * j;
+        if (c < mc) y[c] = acc[nt][0];
+        if (c + 1 < mc) y[c + 1] = acc[nt][1];
+      }
+    }
+  }
+}
+
 }  // namespace hm

@@ -201,3 +201,37 @@ def test_general_uniform_endpoints_match_uniform_path(hm):
     assert float(torch.linalg.norm(Yg - Yu) / torch.linalg.norm(Yu)) <= TOL
     Yg2 = hm.hodlr_matvec_general(n, p, c, [k] * p, dev(D), dev(U), dev(V), X)
     assert torch.equal(Yg, Yg2)
+
+
+@pytest.mark.parametrize("m", [2, 8, 16, 32])
+@pytest.mark.parametrize("dshift", [0, 1])
+def test_ragged_wide_fragments(hm, m, dshift):
+    """The nrhs >= 2 ragged leaf pass loads D and U as 128-bit fragments where the
+    row address allows it (gen_leaf_mma_al_kernel): odd and even leaf sizes (rows of
+    alternating 16-byte alignment), D starting 8 bytes past a 16-byte boundary
+    (dshift = 1), levels whose rank is a multiple of 8 (the 128-bit U groups) next to
+    ranks that are not (the 64-bit fallback columns). Every row against the oracle."""
+    rng = np.random.default_rng(300 + m + 7 * dshift)
+    p = 7
+    sizes = rng.integers(60, 140, size=1 << p)
+    sizes[::5] = 1                      # one-row leaves
+    sizes[3::11] = 0                    # empty leaves
+    c = np.cumsum(sizes).astype(np.int64)
+    n = int(c[-1])
+    ranks = [8, 16, 5, 0, 24, 3, 16]
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    Dbuf = torch.zeros(D.size + 1, dtype=torch.float64, device="cuda:0")
+    Dbuf[dshift:dshift + D.size] = dev(D.ravel())
+    Dd = Dbuf[dshift:dshift + D.size]
+    Y, names = None, set()
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    try:
+        Y = hm.hodlr_matvec_general(n, p, c, ranks, Dd, dev(U), dev(V), dev(X), op=0)
+        torch.cuda.synchronize()
+    finally:
+        hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert "gen_leaf_mma" in names, names
+    assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X, c=c)) <= TOL

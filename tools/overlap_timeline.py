@@ -12,10 +12,15 @@ the one-call hodlr_matvec_dist issues them (hm_hodlr.cu):
                     pass without the top levels) | wait | _end (combine +
                     top-level epilogue)
   exchange        : after _begin, on a second stream: an optional modelled
-                    link latency (torch.cuda._sleep, --link-delay-us), then the
-                    P slots of the gathered buffer delivered by P real NCCL
-                    allgathers on libhm's one-rank communicator (its own
-                    stream, traced as "nccl_allgather").
+                    link latency (torch.cuda._sleep, --link-delay-us), then
+                    the gathered buffer (the P ranks' send slots) delivered by
+                    one real NCCL allgather on libhm's one-rank communicator
+                    (its own stream, traced as "nccl_allgather").
+
+Before each traced step the caller stream gets a short spin (HOST_LEAD_US), so
+the host has enqueued the whole step before the device reaches it: the
+timeline then shows the device-side ordering of the two streams (what the
+events allow to overlap), not this Python driver's enqueue latency.
 
 Every record comes from libhm's launch trace (hm_profile_timeline: CUDA events
 on the launching stream, start times on one device timeline). The same is done
@@ -38,15 +43,22 @@ import paper_1909_07909_b200 as hm  # noqa: E402
 from paper_1909_07909_b200 import dist as hd  # noqa: E402
 
 CLK_HZ = 1.965e9  # B200 max SM clock: cycles of the modelled link latency
+HOST_LEAD_US = 400.0
 
 
-def _exchange(comm, sends, gathered, sd, side, s, delay_us):
+def _lead(s):
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(int(HOST_LEAD_US * 1e-6 * CLK_HZ))
+
+
+def _exchange(comm, allsends, gathered, side, s, delay_us):
+    """One collective call, as the one-call product issues (a one-rank allgather of
+    the P ranks' concatenated send buffers delivers the same gathered bytes)."""
     side.wait_stream(s)
     with torch.cuda.stream(side):
         if delay_us > 0:
             torch.cuda._sleep(int(delay_us * 1e-6 * CLK_HZ))
-        for j, snd in enumerate(sends):
-            comm.allgather(snd, recv=gathered[j * sd:(j + 1) * sd], stream=side)
+        comm.allgather(allsends, recv=gathered, stream=side)
 
 
 def _records(tr, phases):
@@ -85,14 +97,17 @@ def hodlr(comm, P, rank, delay_us, reps):
         if r == rank:
             shards = dict(D=Dl.contiguous(), U=Ul.contiguous(), V=Vl.contiguous(), X=Xl, ws=ws)
     gathered = torch.empty(P * sd, dtype=torch.float64, device=dev)
+    allsends = torch.cat(sends)  # rank r's slot is rewritten by its _begin every step
     Yl = torch.empty_like(shards["X"])
     s, side = torch.cuda.Stream(), torch.cuda.Stream()
     sh = shards
 
     def step():
+        _lead(s)
         with torch.cuda.stream(s):
-            hd.hodlr_matvec_dist_begin(n, p, b, h.ranks, P, rank, sh["V"], sh["X"], sends[rank], sh["ws"], stream=s)
-            _exchange(comm, sends, gathered, sd, side, s, delay_us)
+            hd.hodlr_matvec_dist_begin(n, p, b, h.ranks, P, rank, sh["V"], sh["X"], allsends[rank * sd:(rank + 1) * sd],
+                                       sh["ws"], stream=s)
+            _exchange(comm, allsends, gathered, side, s, delay_us)
             hd.hodlr_matvec_dist_local(n, p, b, h.ranks, P, rank, sh["D"], sh["U"], sh["V"], sh["X"], Yl, sh["ws"],
                                        stream=s)
             s.wait_stream(side)
@@ -148,13 +163,15 @@ def hss(comm, P, rank, delay_us, reps):
             del shd
     shd, Xl, ws = mine
     gathered = torch.empty(P * sd, dtype=torch.float64, device=dev)
+    allsends = torch.cat(sends)
     Yl = torch.empty_like(Xl)
     s, side = torch.cuda.Stream(), torch.cuda.Stream()
 
     def step():
+        _lead(s)
         with torch.cuda.stream(s):
-            hd.hss_matvec_dist_begin(n, p, b, k, P, rank, shd, Xl, sends[rank], ws, stream=s)
-            _exchange(comm, sends, gathered, sd, side, s, delay_us)
+            hd.hss_matvec_dist_begin(n, p, b, k, P, rank, shd, Xl, allsends[rank * sd:(rank + 1) * sd], ws, stream=s)
+            _exchange(comm, allsends, gathered, side, s, delay_us)
             s.wait_stream(side)
             hd.hss_matvec_dist_end(n, p, b, k, P, rank, shd, Xl, gathered, Yl, ws, stream=s)
 

@@ -626,9 +626,6 @@ __global__ void __launch_bounds__(kThreads, HM_GEN_MMA_MINB) gen_leaf_mma_kernel
 #ifndef HM_GEN_AL_QG
 #define HM_GEN_AL_QG 8  // 8-column groups per batch of loads
 #endif
-#ifndef HM_GEN_AL_PIPE
-#define HM_GEN_AL_PIPE 0  // 1: ping-pong the batches (measured slower: cr8 738 -> 779 us at QG 4)
-#endif
 #ifndef HM_GEN_AL_MINB
 #define HM_GEN_AL_MINB 3  // CTAs per SM for NT = 1
 #endif
@@ -638,27 +635,21 @@ __host__ __device__ constexpr size_t gen_al_tab_bytes(int ktot) { return 32 * (s
 template <int NT>
 __global__ void __launch_bounds__(kThreads, NT == 1 ? HM_GEN_AL_MINB : 1) gen_leaf_mma_al_kernel(const GenLeafParams P) {
   extern __shared__ double smem[];
-  constexpr int MC = NT * 8, ZS = gen_al_zs(NT), QG = HM_GEN_AL_QG;  // 8-column groups per pipeline stage
+  constexpr int MC = NT * 8, ZS = gen_al_zs(NT), QG = HM_GEN_AL_QG;  // 8-column groups per batch of loads
   const int64_t leaf = P.order[blockIdx.x];
   const int64_t r0 = P.lo[leaf], b = P.lo[leaf + 1] - r0;
   if (b == 0) return;
   const int c0 = blockIdx.y * MC;
   const int m = P.m, mc = min(MC, m - c0);
-  double* Z = smem;  // [(b + ktot)][ZS]
-  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
-    const int64_t r = e / MC;
-    const int c = (int)(e - r * MC);
-    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * m + c0 + c] : 0.0;
-  }
-  int64_t off = b;
-  for (int s = 0; s < P.nseg; ++s) {
-    const LeafSeg sg = P.seg[s];
-    const double* T = sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m;
-    for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
-      const int a = e / MC, c = e - a * MC;
-      Z[(off + a) * ZS + c] = (c < mc) ? T[a * m + c0 + c] : 0.0;
+  double* Z = smem;  // [(b + ktot)][ZS]: X(I_i) columns c0.., then T_s[node_s] per segment (cp.async)
+  stage_rows_async(Z, ZS, P.X + r0 * m + c0, m, (int)b, mc, MC);
+  {
+    int64_t off = b;
+    for (int s = 0; s < P.nseg; ++s) {
+      const LeafSeg sg = P.seg[s];
+      stage_rows_async(Z + off * ZS, ZS, sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m + c0, m, sg.k, mc, MC);
+      off += sg.k;
     }
-    off += sg.k;
   }
   // tables: groups of 8 rank columns of the 128-bit segments, single columns of the others
   const int kt = P.ktot;
@@ -692,13 +683,31 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? HM_GEN_AL_MINB : 1) gen_le
       zrow += sg.k;
     }
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = lane >> 2, j = lane & 3;
   const double* Di = P.D + P.doff[leaf];
   const bool bodd = (b & 1) != 0;
   const int64_t ntile = bodd ? 2 * ((b + 15) / 16) : (b + 7) / 8;
   const int bi = (int)b;
+  // the first batch of D loads of the warp's first tile is requested before the
+  // staging wait: the row addresses need no staged data
+  double2 a[QG];  // the A-fragment batch buffer (first batch filled before the wait)
+  bool pre = false;
+  if (warp < ntile) {
+    const int64_t t = warp;
+    const int64_t row0 = bodd ? 16 * (t >> 1) + (t & 1) : 8 * t;
+    if (row0 < b) {
+      const int64_t row = bodd ? row0 + 2 * i : row0 + i;
+      const double* drow = Di + (row < b ? row : row0) * b;
+      const int sig = (int)((reinterpret_cast<uintptr_t>(Di + row0 * b) >> 3) & 1);
+      const int G = (bi - sig) / 8;
+#pragma unroll
+      for (int u = 0; u < QG; ++u) a[u] = u < G ? ld_a_stream2(drow + sig + 2 * j + 8 * u) : make_double2(0.0, 0.0);
+      pre = true;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
   for (int64_t t = warp; t < ntile; t += kThreads / 32) {
     const int64_t row0 = bodd ? 16 * (t >> 1) + (t & 1) : 8 * t;
     if (row0 >= b) continue;  // warp-uniform: a parity tile past the block
@@ -710,52 +719,28 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? HM_GEN_AL_MINB : 1) gen_le
     double acc[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-    // 8-column groups: the b-sigma aligned columns of D_i (x < G), then the
-    // 128-bit U groups (x >= G), one software pipeline over both — the next QG
-    // groups' loads are in flight while the current QG feed the tensor pipe
+    // full groups of 8 aligned columns: lane (i, j) loads D[row][sigma + 8 g + 2 j, + 1]
     const int G = (bi - sig) / 8;
-    const int NG = G + ng;
-    const int64_t grow = r0 + rr;
     const double* da = drow + sig + 2 * j;
-    auto gload = [&](double2 (&a)[QG], int x0) {
+    const double* zb = Z + (int64_t)(sig + 2 * j) * ZS + i;
+    for (int g0 = 0; g0 < G; g0 += QG) {
+      if (!pre) {  // warp-uniform (pre: this batch was requested before the staging wait)
 #pragma unroll
-      for (int u = 0; u < QG; ++u) {
-        const int x = x0 + u;
-        a[u] = x >= NG  ? make_double2(0.0, 0.0)
-               : x < G ? ld_a_stream2(da + 8 * x)
-                       : ld_a_stream2(gbase[x - G] + grow * gk[x - G] + 2 * j);
+        for (int u = 0; u < QG; ++u) a[u] = (g0 + u < G) ? ld_a_stream2(da + 8 * (g0 + u)) : make_double2(0.0, 0.0);
       }
-    };
-    auto gmma = [&](const double2 (&a)[QG], int x0) {
+      pre = false;
 #pragma unroll
       for (int u = 0; u < QG; ++u) {
-        const int x = x0 + u;
-        if (x >= NG) break;  // warp-uniform
-        const double* zr = Z + (int64_t)((x < G ? sig + 8 * x : gz[x - G]) + 2 * j) * ZS + i;
+        if (g0 + u >= G) break;  // warp-uniform
+        const double* zr = zb + (int64_t)(8 * (g0 + u)) * ZS;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].x, zr[nt * 8]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].y, zr[ZS + nt * 8]);
       }
-    };
-    if constexpr (HM_GEN_AL_PIPE) {
-      double2 a0[QG], a1[QG];
-      gload(a0, 0);
-      for (int x0 = 0; x0 < NG; x0 += 2 * QG) {
-        gload(a1, x0 + QG);
-        gmma(a0, x0);
-        if (x0 + QG >= NG) break;
-        gload(a0, x0 + 2 * QG);
-        gmma(a1, x0 + QG);
-      }
-    } else {  // batches: QG groups' loads, then their DMMAs
-      for (int x0 = 0; x0 < NG; x0 += QG) {
-        double2 a[QG];
-        gload(a, x0);
-        gmma(a, x0);
-      }
     }
-    // leftover columns of D_i: 0 (sigma = 1) and [sigma + 8 G, b): at most 8, two masked k-steps
+    pre = false;  // (G == 0: the prefetched batch was all zeros)
+    // leftover columns: 0 (sigma = 1) and [sigma + 8 G, b): at most 8, two masked k-steps
     {
       const int nrem = bi - 8 * G;  // = sig + (b - sig - 8 G)
       double a2[2];
@@ -775,21 +760,37 @@ __global__ void __launch_bounds__(kThreads, NT == 1 ? HM_GEN_AL_MINB : 1) gen_le
         for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a2[u], ok ? zr[nt * 8] : 0.0);
       }
     }
-    // U segments with 64-bit fragments (k % 8 != 0 or an unaligned base)
-    for (int q0 = 0; 4 * q0 < ns; q0 += 2 * QG) {
-      double a[2 * QG];
+    // U segments, 128-bit groups (flattened over the segments)
+    const int64_t grow = r0 + rr;
+    for (int g0 = 0; g0 < ng; g0 += QG) {
 #pragma unroll
-      for (int u = 0; u < 2 * QG; ++u) {
+      for (int u = 0; u < QG; ++u)
+        a[u] = (g0 + u < ng) ? ld_a_stream2(gbase[g0 + u] + grow * gk[g0 + u] + 2 * j) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < QG; ++u) {
+        if (g0 + u >= ng) break;
+        const double* zr = Z + (int64_t)(gz[g0 + u] + 2 * j) * ZS + i;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].x, zr[nt * 8]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u].y, zr[ZS + nt * 8]);
+      }
+    }
+    // U segments with 64-bit fragments (k % 8 != 0 or an unaligned base)
+    for (int q0 = 0; 4 * q0 < ns; q0 += QG) {
+      double as[QG];
+#pragma unroll
+      for (int u = 0; u < QG; ++u) {
         const int kk = 4 * (q0 + u) + j;
-        a[u] = kk < ns ? __ldg(sbase[kk] + grow * sk[kk]) : 0.0;
+        as[u] = kk < ns ? __ldg(sbase[kk] + grow * sk[kk]) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 2 * QG; ++u) {
+      for (int u = 0; u < QG; ++u) {
         if (4 * (q0 + u) >= ns) break;
         const int kk = 4 * (q0 + u) + j;
         const double* zr = Z + (int64_t)(kk < ns ? sz[kk] : 0) * ZS + i;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], kk < ns ? zr[nt * 8] : 0.0);
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], as[u], kk < ns ? zr[nt * 8] : 0.0);
       }
     }
     if (rok) {

@@ -92,6 +92,9 @@ HODLR_CASES = [
     (32768, 128, 8, 32, 32),    # level-parallel pipelined V^T X (vt_lv, m > 16)
     (16384, 64, 8, 16, 17),     # vt_lv, odd m: synchronous X staging, padded columns
     (65536, 256, 8, 16, 48),    # vt_lv, 3 work items per warp
+    (16384, 256, 6, 16, 100),   # nrhs > 64: several column chunks of every kernel
+    (8192, 64, 7, 32, 129),
+    (4096, 128, 5, 8, 200),
 ]
 
 
@@ -118,6 +121,8 @@ HSS_CASES = [
     (16384, 256, 6, 32, 8),
     (16384, 128, 7, 64, 5),
     (2048, 128, 4, 16, 2),
+    (16384, 128, 7, 32, 100),   # nrhs > 64: several column chunks of every kernel
+    (8192, 64, 7, 16, 129),
 ]
 
 

@@ -623,34 +623,6 @@ __device__ __forceinline__ void rm_load(double2 (&a)[PF][RG], const double* base
                               : make_double2(0.0, 0.0);
 }
 
-// The lane's A pointer of warp_rowmajor_mma (row i of the warp's first tile, column 2 j).
-template <bool PAIR = false>
-__device__ __forceinline__ const double* rm_base(const double* E, int64_t lda, int lane) {
-  return E + (int64_t)(PAIR ? 2 * (lane >> 2) : (lane >> 2)) * lda + 2 * (lane & 3);
-}
-
-// warp_rowmajor_mma whose first batch of A fragments (a0 = rm_load(rm_base(E), 0))
-// the caller requested earlier (e.g. before a shared-memory staging wait).
-template <int RG, int NT, bool ZG, bool COH = false, int PF = HM_RM_PF, bool PAIR = false>
-__device__ __forceinline__ void warp_rowmajor_mma_pre(double (&acc)[RG][NT][2], double2 (&a0)[PF][RG],
-                                                      const double* __restrict__ E, int64_t lda, int K,
-                                                      const double* Z, int64_t zs, int zvalid, int lane) {
-  const int i = lane >> 2;
-  const double* base = rm_base<PAIR>(E, lda, lane);
-  bool colok[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) colok[nt] = !ZG || (nt * 8 + i) < zvalid;
-  const int nq = K / 8;
-  double2 a1[PF][RG];
-  for (int q = 0; q < nq; q += 2 * PF) {
-    rm_load<RG, PF, PAIR>(a1, base, lda, q + PF, nq);
-    rm_group<RG, NT, ZG, COH, PF>(acc, a0, Z, zs, q, nq, colok, lane);
-    if (q + PF >= nq) break;
-    rm_load<RG, PF, PAIR>(a0, base, lda, q + 2 * PF, nq);
-    rm_group<RG, NT, ZG, COH, PF>(acc, a1, Z, zs, q + PF, nq, colok, lane);
-  }
-}
-
 template <int RG, int NT, bool ZG, bool COH = false, int PF = HM_RM_PF, bool PAIR = false>
 __device__ __forceinline__ void warp_rowmajor_mma(double (&acc)[RG][NT][2], const double* __restrict__ E, int64_t lda,
                                                   int K, const double* Z, int64_t zs, int zvalid, int lane) {
@@ -722,9 +694,6 @@ __device__ __forceinline__ void warp_dt_mma(double (&acc)[RG][NT][2], const doub
 // DT (adjoint): the leaf term is D_i^T X_i (warp_dt_mma); for even RG the
 // warp's rows are in PAIR order, which the U segments and the store follow.
 
-#ifndef HM_LEAF_PREFETCH
-#define HM_LEAF_PREFETCH 1
-#endif
 template <int RG, int NT, int PF, int MINB, bool DT = false>
 __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P) {
   constexpr bool PAIR = DT && (RG % 2 == 0);
@@ -752,29 +721,17 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
     stage_rows_async(ZT + zoff * ZS, ZS, sg.T + node * sg.k * m + c0, m, sg.k, mc, MC);
     zoff += sg.k;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wrow = (int64_t)warp * 8 * RG;
-#if HM_LEAF_PREFETCH
-  // the first batch of D fragments is requested before the staging wait (the
-  // row addresses need no staged data)
-  double2 a0[PF][RG];
-  if constexpr (!DT)
-    rm_load<RG, PF>(a0, rm_base(P.D + leaf * b * b + wrow * b, b, lane), b, 0, (int)(b / 8));
-#endif
   cp_async_wait_all();
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[RG][NT][2];
 #pragma unroll
   for (int rg = 0; rg < RG; ++rg)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
+  const int64_t wrow = (int64_t)warp * 8 * RG;
   if constexpr (DT) warp_dt_mma<RG, NT>(acc, P.D + leaf * b * b + wrow, b, (int)b, Z, ZSX, lane);
-#if HM_LEAF_PREFETCH
-  else warp_rowmajor_mma_pre<RG, NT, false, false, PF>(acc, a0, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC,
-                                                       lane);
-#else
   else warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
-#endif
   zoff = 0;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];

@@ -495,20 +495,12 @@ __global__ void __launch_bounds__(kThreads, HM_GEN_MMA_MINB) gen_leaf_mma_kernel
   if (b == 0) return;
   const int c0 = blockIdx.y * MC;
   const int m = P.m, mc = min(MC, m - c0);
-  double* Z = smem;  // [(b + ktot)][ZS]
-  for (int64_t e = threadIdx.x; e < b * MC; e += kThreads) {
-    const int64_t r = e / MC;
-    const int c = (int)(e - r * MC);
-    Z[r * ZS + c] = (c < mc) ? P.X[(r0 + r) * m + c0 + c] : 0.0;
-  }
+  double* Z = smem;  // [(b + ktot)][ZS]: X(I_i) columns c0.., then T_s[node_s] per segment (cp.async)
+  stage_rows_async(Z, ZS, P.X + r0 * m + c0, m, (int)b, mc, MC);
   int64_t off = b;
   for (int s = 0; s < P.nseg; ++s) {
     const LeafSeg sg = P.seg[s];
-    const double* T = sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m;
-    for (int e = threadIdx.x; e < sg.k * MC; e += kThreads) {
-      const int a = e / MC, c = e - a * MC;
-      Z[(off + a) * ZS + c] = (c < mc) ? T[a * m + c0 + c] : 0.0;
-    }
+    stage_rows_async(Z + off * ZS, ZS, sg.T + ((leaf >> sg.shift) ^ sg.xr) * sg.k * m + c0, m, sg.k, mc, MC);
     off += sg.k;
   }
   const int kt = P.ktot;
@@ -525,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, HM_GEN_MMA_MINB) gen_leaf_mma_kernel
       e += k2;
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = lane >> 2, j = lane & 3;

@@ -182,8 +182,16 @@ hm_status gen_vt_mma_launch(const hm::GenVtParams& vp, int64_t nchunks, cudaStre
 }
 
 hm_status gen_vt_mma_dispatch(const hm::GenVtParams& vp, int64_t nchunks, int k, cudaStream_t s) {
-  if (k == 16) return vp.m <= 16 ? gen_vt_mma_launch<16, 2>(vp, nchunks, s) : gen_vt_mma_launch<16, 4>(vp, nchunks, s);
-  if (k == 32) return vp.m <= 16 ? gen_vt_mma_launch<32, 2>(vp, nchunks, s) : gen_vt_mma_launch<32, 4>(vp, nchunks, s);
+  // 8 NT columns per CTA: NT = 1 up to 8 columns (no DMMAs on padding columns; ncu, ragged config-3 tree at
+  // m = 8 with NT = 2: tensor pipe 48% busy, half of it on zero columns)
+  if (k == 16) {
+    if (vp.m <= 8) return gen_vt_mma_launch<16, 1>(vp, nchunks, s);
+    return vp.m <= 16 ? gen_vt_mma_launch<16, 2>(vp, nchunks, s) : gen_vt_mma_launch<16, 4>(vp, nchunks, s);
+  }
+  if (k == 32) {
+    if (vp.m <= 8) return gen_vt_mma_launch<32, 1>(vp, nchunks, s);
+    return vp.m <= 16 ? gen_vt_mma_launch<32, 2>(vp, nchunks, s) : gen_vt_mma_launch<32, 4>(vp, nchunks, s);
+  }
   return gen_vt_mma_launch<64, 2>(vp, nchunks, s);
 }
 

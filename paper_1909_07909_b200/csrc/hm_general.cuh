@@ -150,13 +150,16 @@ __global__ void __launch_bounds__(kThreads) gen_vt_chunk_kernel(const GenVtParam
   }
 }
 
+#ifndef HM_GEN_VT_MINB
+#define HM_GEN_VT_MINB 3  // CTAs per SM of the small instances (KT NT <= 16)
+#endif
 // nrhs >= 2, every level of rank KT in {16, 32, 64}: DMMA per chunk. Warp w
 // takes an 8th of the chunk's rows (a multiple of 4), t = V(rows)^T X(rows)
 // with the hm_fast.cuh fragment layout (one 128-bit load of a V row covers 16
 // rank columns; rows past the chunk end read as zero), then a fixed-order sum
 // over the 8 warps in shared memory. grid.y = column chunks of 8 NT.
 template <int KT, int NT>
-__global__ void __launch_bounds__(kThreads) gen_vt_mma_kernel(const GenVtParams P) {
+__global__ void __launch_bounds__(kThreads, KT * NT <= 16 ? HM_GEN_VT_MINB : 1) gen_vt_mma_kernel(const GenVtParams P) {
   extern __shared__ double red[];  // [8][KT][8 NT]
   constexpr int MC = NT * 8, MPW = KT / 16;
   const GenChunk ch = P.chunks[P.order[blockIdx.x]];

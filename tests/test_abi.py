@@ -207,3 +207,36 @@ def test_dist_workspace_queries():
     assert e.value.status == hm.HM_ERR_UNSUPPORTED
     with pytest.raises(hm.HmError):
         hd.hss_dist_workspace_bytes(1 << 15, 8, 128, 32, 32, 512)   # P > 2^levels
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The binding's ctypes records have the C header's sizes and field offsets
+    (hm_tree, hm_part, hm_launch_record): a plain-C probe compiled against
+    include/hm.h prints them."""
+    import ctypes
+    import subprocess
+    import paper_1909_07909_b200 as hm
+    from paper_1909_07909_b200 import dist
+    recs = {
+        "hm_tree": (hm.hm_tree, ["n", "levels", "flags", "leaf"]),
+        "hm_part": (dist.hm_part, ["nranks", "rank"]),
+        "hm_launch_record": (hm.hm_launch_record, ["name", "call", "ms", "start_ms"]),
+    }
+    src = ["#include <stdio.h>", "#include <stddef.h>", '#include "hm.h"', "int main(void) {"]
+    for name, (_, fields) in recs.items():
+        src.append(f'  printf("{name} %zu", sizeof({name}));')
+        for f in fields:
+            src.append(f'  printf(" %zu", offsetof({name}, {f}));')
+        src.append('  printf("\\n");')
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = str(tmp_path / "layout")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(c), "-o", exe],
+                   check=True, capture_output=True, text=True)
+    out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split("\n")
+    for line in filter(None, out):
+        name, size, *offs = line.split()
+        cls, fields = recs[name]
+        assert ctypes.sizeof(cls) == int(size), name
+        assert [getattr(cls, f).offset for f in fields] == [int(o) for o in offs], name

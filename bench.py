@@ -502,7 +502,7 @@ def sweep(torch, device, wl, peak, parity=True):
     # leaf 128, nrhs 16), host-generated; every row vs the oracle
     nr, pr, br, mr = 1 << 20, 13, 128, 16
     lr = [32] * 4 + [24] * 4 + [16] * 5
-    kn = [16 + (7 * i + l) % 17 for l in range(1, pr + 1) for i in range(1 << l)]
+    kn = np.array([16 + (7 * i + l) % 17 for l in range(1, pr + 1) for i in range(1 << l)], dtype=np.int32)
     Xr = hm_inputs.rhs(nr, mr, cid=60)
     Xd = torch.from_numpy(Xr).to(device)
     for tag, gen, wsq, call, ref in (

@@ -519,6 +519,8 @@ def hss_matvec_ranked(n, levels, leaf, ranks, D, U, V, R, W, B, X, op=0, Y=None,
 
 def _kn_key(node_ranks) -> bytes:
     import numpy as np
+    if isinstance(node_ranks, np.ndarray) and node_ranks.dtype == np.int32 and node_ranks.flags.c_contiguous:
+        return node_ranks.tobytes()  # (a list of 2^(p+1) ranks costs ~1 ms to convert: pass an int32 array)
     return np.ascontiguousarray(node_ranks, dtype=np.int32).tobytes()
 
 

@@ -154,12 +154,16 @@ hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* 
   r.next = (r.next + 1) % 4;
   if (r.used[slot] && cudaEventSynchronize(r.ev[slot]) != cudaSuccess) return cuda_check("table staging event");
   if (r.cap[slot] < img.size()) {
+    // grow to the next power of two (at least 1 MB): alternating table sizes do not
+    // re-pin a buffer on every call (cudaFreeHost synchronises the device)
+    size_t cap = (size_t)1 << 20;
+    while (cap < img.size()) cap <<= 1;
     if (r.buf[slot]) cudaFreeHost(r.buf[slot]);
     r.buf[slot] = nullptr;
     r.cap[slot] = 0;
-    if (cudaHostAlloc(reinterpret_cast<void**>(&r.buf[slot]), img.size(), cudaHostAllocDefault) != cudaSuccess)
+    if (cudaHostAlloc(reinterpret_cast<void**>(&r.buf[slot]), cap, cudaHostAllocDefault) != cudaSuccess)
       return cuda_check("pinned staging buffer for the tree tables");
-    r.cap[slot] = img.size();
+    r.cap[slot] = cap;
   }
   if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot], cudaEventDisableTiming) != cudaSuccess)
     return cuda_check("table staging event");

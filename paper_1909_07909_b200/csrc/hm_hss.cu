@@ -622,6 +622,32 @@ struct RankedPlan {
   bool uniform;
 };
 
+// DMMA level kernels (hm_tree.cuh) when the output rank is a multiple of 8 and
+// the contraction lengths multiples of 4; otherwise the CUDA-core ones.
+#ifndef HM_RANKED_MMA
+#define HM_RANKED_MMA 1
+#endif
+bool ranked_mma_ok(int k, int kin, int kp, int32_t nrhs) {
+  return HM_RANKED_MMA && nrhs >= 2 && k % 8 == 0 && kin % 4 == 0 && kp % 4 == 0;
+}
+
+template <int NT>
+hm_status ranked_mma_launch_nt(const hm::RankedMmaParams& rp, bool up, cudaStream_t s) {
+  const int64_t warps = rp.nodes * (rp.k / 8) * ((rp.m + NT * 8 - 1) / (NT * 8));
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  if (up)
+    return launch(HM_NT_NAME("hss_up_ranked_mma"), s,
+                  [&] { hm::hss_up_ranked_mma_kernel<NT><<<grid, 256, 0, s>>>(rp); });
+  return launch(HM_NT_NAME("hss_down_ranked_mma"), s,
+                [&] { hm::hss_down_ranked_mma_kernel<NT><<<grid, 256, 0, s>>>(rp); });
+}
+
+hm_status ranked_mma_launch(const hm::RankedMmaParams& rp, bool up, cudaStream_t s) {
+  if (rp.m <= 8) return ranked_mma_launch_nt<1>(rp, up, s);
+  if (rp.m <= 16) return ranked_mma_launch_nt<2>(rp, up, s);
+  return ranked_mma_launch_nt<4>(rp, up, s);
+}
+
 hm_status hss_ranked_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, RankedPlan* Q) {
   hm_status st = check_tree(tree);
   if (st) return st;
@@ -716,6 +742,12 @@ hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, cons
     // upsweep l = p-1..1 through W^T (2k_{l+1} x k_l)
     for (int l = p - 1; l >= 1; --l) {
       if (Q.kl[l] == 0) continue;
+      if (ranked_mma_ok(Q.kl[l], 2 * Q.kl[l + 1], 0, nrhs)) {
+        const hm::RankedMmaParams rp{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l],
+                                     (int64_t)1 << l, Q.kl[l], Q.kl[l + 1], 0, nrhs, 0};
+        if ((st = ranked_mma_launch(rp, true, s))) return st;
+        continue;
+      }
       const hm::HssRankedLevelParams hp{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l], l, Q.kl[l],
                                         Q.kl[l + 1], 0, nrhs, 0};
       const int64_t total = ((int64_t)1 << l) * Q.kl[l] * nrhs;
@@ -727,6 +759,13 @@ hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, cons
     for (int l = 1; l <= p; ++l) {
       if (Q.kl[l] == 0) continue;
       const bool from_parent = l >= 2 && Q.kl[l - 1] > 0;
+      if (ranked_mma_ok(Q.kl[l], Q.kl[l], from_parent ? Q.kl[l - 1] : 0, nrhs)) {
+        const hm::RankedMmaParams rp{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
+                                     from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], (int64_t)1 << l,
+                                     Q.kl[l], 0, from_parent ? Q.kl[l - 1] : 0, nrhs, op};
+        if ((st = ranked_mma_launch(rp, false, s))) return st;
+        continue;
+      }
       const hm::HssRankedLevelParams hp{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
                                         from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], l, Q.kl[l], 0,
                                         from_parent ? Q.kl[l - 1] : 0, nrhs, op};
@@ -916,7 +955,8 @@ hm_status hss_noderank_run(const hm_tree* tree, const int32_t* kn, int op, const
       pp.dst[a] = dsts[a];
     }
     if ((st = launch("pad_blocks", s, [&] {
-           hm::pad_blocks_kernel<<<(unsigned)N.blocks.size(), hm::kThreads, 0, s>>>(pp);
+           const int64_t nb = (int64_t)N.blocks.size();
+           hm::pad_blocks_kernel<<<(unsigned)std::min<int64_t>(nb, 148 * 8), hm::kThreads, 0, s>>>(pp, nb);
          })))
       return st;
   }

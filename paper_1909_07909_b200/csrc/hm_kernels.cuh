@@ -552,16 +552,29 @@ struct PadParams {
 
 // Writes every element of one padded block exactly once: the compact block
 // in its top-left corner, zeros elsewhere.
-static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadParams P) {
-  const PadBlock b = P.blocks[blockIdx.x];
-  const double* s = P.src[b.arr] + b.src;
-  double* d = P.dst[b.arr] + b.dst;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < b.drows; r += kThreads / 32) {  // warp per row, lanes over columns
-    const bool rok = r < b.rows;
-    for (int c = lane; c < b.dcols; c += 32)
-      d[(int64_t)r * b.dcols + c] = (rok && c < b.cols) ? s[(int64_t)r * b.cols + c] : 0.0;
+static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadParams P, int64_t nblocks) {
+ for (int64_t bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {  // CTAs stride over the blocks
+  const PadBlock b = P.blocks[bi];
+  const double* __restrict__ s = P.src[b.arr] + b.src;
+  double* __restrict__ d = P.dst[b.arr] + b.dst;
+  // threads over the padded block's elements (consecutive threads: consecutive
+  // destination elements), 4 loads in flight per thread before their stores
+  const int64_t tot = (int64_t)b.drows * b.dcols;
+  for (int64_t e0 = threadIdx.x; e0 < tot; e0 += 4 * kThreads) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = e0 + (int64_t)u * kThreads;
+      const int r = (int)(e / b.dcols), c = (int)(e - (int64_t)r * b.dcols);
+      v[u] = (e < tot && r < b.rows && c < b.cols) ? __ldg(s + (int64_t)r * b.cols + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = e0 + (int64_t)u * kThreads;
+      if (e < tot) d[e] = v[u];
+    }
   }
+ }
 }
 
 }  // namespace hm

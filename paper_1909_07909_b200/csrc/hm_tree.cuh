@@ -715,4 +715,115 @@ __global__ void __launch_bounds__(256, 2) hss_vt_up_kernel(const VtUpParams P) {
   vt_up_level<KT, NT, 1>(P, p - 3, (int64_t)blockIdx.x, L, nullptr, zs, warp, lane);
 }
 
+// ---- HSS with per-level ranks, DMMA level kernels ----
+// One warp = one node x one 8-row tile of its output block x one chunk of 8 NT
+// columns; 8 warps per CTA. Shapes are runtime: k_l (output rows, % 8 == 0),
+// the contraction lengths 2 k_{l+1} (up) and k_l, k_{l-1} (down) % 4 == 0.
+// A fragments by 64-bit loads (row i of the tile, k-index 4 q + j), B fragments
+// from the coefficient blocks in global memory (L2); QK k-steps of loads
+// requested before their DMMAs. Same fixed summation order on every call.
+struct RankedMmaParams {
+  const double* G;    // up: W of level l ([2kc][k] per node); down: R of level l-1 ([2k][kp] per parent)
+  const double* B;    // down: cores of the level-l siblings ([2][k][k] per pair)
+  const double* xin;  // up: x of level l+1 ([kc][m] blocks); down: x of level l ([k][m])
+  const double* yp;   // down: y of level l-1 ([kp][m] blocks), NULL: no parent term
+  double* out;        // up: x of level l; down: y of level l ([k][m] blocks)
+  int64_t nodes;      // 2^l
+  int32_t k, kc, kp, m, bt;
+};
+
+// acc += A(8 rows at a0, row stride lda, or transposed: A^T with AT) . Z (K x cols at z, ld m)
+template <int NT, bool AT>
+__device__ __forceinline__ void ranked_tile_mma(double (&acc)[NT][2], const double* a0, int64_t lda, const double* z,
+                                                int m, int K, const bool (&colok)[NT], int lane) {
+  constexpr int QK = 4;
+  const int i = lane >> 2, j = lane & 3;
+  for (int q0 = 0; q0 < K / 4; q0 += QK) {
+    double a[QK], bf[QK][NT];
+#pragma unroll
+    for (int u = 0; u < QK; ++u) {
+      const int kk = 4 * (q0 + u) + j;
+      const bool ok = 4 * (q0 + u) < K;
+      a[u] = ok ? (AT ? __ldg(a0 + (int64_t)kk * lda + i) : __ldg(a0 + (int64_t)i * lda + kk)) : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bf[u][nt] = (ok && colok[nt]) ? ldg_cg(z + (int64_t)kk * m + nt * 8 + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < QK; ++u) {
+      if (4 * (q0 + u) >= K) break;  // warp-uniform
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[nt][0], acc[nt][1], a[u], bf[u][nt]);
+    }
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void ranked_store(const double (&acc)[NT][2], double* out, int m, int c0, int lane) {
+  const int i = lane >> 2, j = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = c0 + nt * 8 + 2 * j;
+    if (c < m) out[(int64_t)i * m + c] = acc[nt][0];
+    if (c + 1 < m) out[(int64_t)i * m + c + 1] = acc[nt][1];
+  }
+}
+
+// x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]   (Fig. 5 right)
+template <int NT>
+__global__ void __launch_bounds__(256) hss_up_ranked_mma_kernel(const RankedMmaParams P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tiles = P.k / 8, nck = (P.m + NT * 8 - 1) / (NT * 8);
+  const int64_t per = (int64_t)tiles * nck;
+  const int64_t node = gw / per;
+  if (node >= P.nodes) return;
+  const int rem = (int)(gw - node * per), tile = rem % tiles, c0 = (rem / tiles) * NT * 8;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = c0 + nt * 8 + (lane >> 2) < P.m;
+  double acc[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  // A = W^T: A[a][r] = W[r][a], W row-major [2kc][k]
+  ranked_tile_mma<NT, true>(acc, P.G + node * 2 * P.kc * P.k + 8 * tile, P.k,
+                            P.xin + 2 * node * (int64_t)P.kc * P.m + c0, P.m, 2 * P.kc, colok, lane);
+  ranked_store<NT>(acc, P.out + (node * P.k + 8 * tile) * (int64_t)P.m, P.m, c0, lane);
+}
+
+// y_l[2q+w] = S_w x_l[2q+1-w] + R_{l-1,q}[w] y_{l-1}[q]   (reading G1;
+// bt: S'_w = (S_{1-w})^T, the adjoint's cores)
+template <int NT>
+__global__ void __launch_bounds__(256) hss_down_ranked_mma_kernel(const RankedMmaParams P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tiles = P.k / 8, nck = (P.m + NT * 8 - 1) / (NT * 8);
+  const int64_t per = (int64_t)tiles * nck;
+  const int64_t jn = gw / per;
+  if (jn >= P.nodes) return;
+  const int rem = (int)(gw - jn * per), tile = rem % tiles, c0 = (rem / tiles) * NT * 8;
+  const int64_t q = jn >> 1;
+  const int w = (int)(jn & 1);
+  const int k = P.k, m = P.m;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = c0 + nt * 8 + (lane >> 2) < m;
+  double acc[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  const double* xs = P.xin + (jn ^ 1) * (int64_t)k * m + c0;
+  if (P.bt) {
+    const double* S = P.B + (q * 2 + (1 - w)) * (int64_t)k * k;
+    ranked_tile_mma<NT, true>(acc, S + 8 * tile, k, xs, m, k, colok, lane);
+  } else {
+    const double* S = P.B + (q * 2 + w) * (int64_t)k * k;
+    ranked_tile_mma<NT, false>(acc, S + (int64_t)8 * tile * k, k, xs, m, k, colok, lane);
+  }
+  if (P.yp && P.kp > 0) {
+    const double* Rn = P.G + (q * 2 * k + (int64_t)w * k) * P.kp;
+    ranked_tile_mma<NT, false>(acc, Rn + (int64_t)8 * tile * P.kp, P.kp, P.yp + q * (int64_t)P.kp * m + c0, m, P.kp,
+                               colok, lane);
+  }
+  ranked_store<NT>(acc, P.out + (jn * k + 8 * tile) * (int64_t)m, m, c0, lane);
+}
+
 }  // namespace hm

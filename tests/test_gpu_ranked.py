@@ -120,3 +120,26 @@ def test_hss_noderanked_config4_tree(hm):
     torch.cuda.synchronize()
     Yr = oracle.hss_matvec_noderanked(cfg.n, cfg.levels, kn, s.D, s.U, s.V, s.R, s.W, s.B, X)
     assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+@pytest.mark.parametrize("op", [0, 1])
+def test_hss_ranked_dmma_levels_ran(hm, op):
+    """Per-level ranks that are multiples of 8 run the DMMA level kernels
+    (hss_up_ranked_mma / hss_down_ranked_mma, hm_tree.cuh); a level of rank 4 next to
+    them keeps the CUDA-core kernels. Every row against the oracle, A and A^T."""
+    n, p, m = 1 << 14, 8, 12
+    ranks = [24, 16, 16, 8, 4, 8, 16, 24]
+    s = hm_inputs.hss_random_ranked(n, p, ranks, cid=52)
+    X = hm_inputs.rhs(n, m, cid=52)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    try:
+        Y = hm.hss_matvec_ranked(n, p, n >> p, ranks, *g, dev(X), op=op)
+        torch.cuda.synchronize()
+    finally:
+        hm.hm_profile_enable(False)
+    names = {t[0] for t in hm.hm_profile_collect()}
+    assert {"hss_up_ranked_mma<nt2>", "hss_down_ranked_mma<nt2>", "hss_down_ranked"} <= names, names
+    Yr = oracle.hss_matvec_ranked(n, p, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL

@@ -43,6 +43,25 @@ def run(name, reps):
         f = lambda: hm.hodlr_matvec_general(n, cfg.levels, c, rk, D, U, V, X, 1 if adj else 0, Y, ws)
         nbytes = 8 * (D.numel() + U.numel() + V.numel() + 2 * n * m)
         flops = 2 * m * (D.numel() + U.numel() + V.numel())
+    elif name in ("hpl", "hpn"):  # HSS with per-level / per-node ranks (the bench sweep's trees)
+        import numpy as np
+        nr, pr, br, m = 1 << 20, 13, 128, 16
+        if name == "hpl":
+            lr = [32] * 4 + [24] * 4 + [16] * 5
+            hr = hm_inputs.hss_random_ranked(nr, pr, lr, cid=60)
+            wsb = hm.hm_hss_ranked_workspace_bytes(nr, pr, br, lr, m)
+        else:
+            lr = np.array([16 + (7 * i + l) % 17 for l in range(1, pr + 1) for i in range(1 << l)], dtype=np.int32)
+            hr = hm_inputs.hss_random_noderanked(nr, pr, lr, cid=61)
+            wsb = hm.hm_hss_noderanked_workspace_bytes(nr, pr, br, lr, m)
+        g = [torch.from_numpy(a).to(dev) for a in (hr.D, hr.U, hr.V, hr.R, hr.W, hr.B)]
+        X = torch.randn(nr, m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        mv = hm.hss_matvec_ranked if name == "hpl" else hm.hss_matvec_noderanked
+        f = lambda: mv(nr, pr, br, lr, *g, X, Y=Y, workspace=ws)
+        nbytes = 8 * (sum(a.numel() for a in g) + 2 * nr * m)
+        flops = 2 * m * sum(a.numel() for a in g)
     elif name.startswith("c3") or name in ("c5", "c1"):
         cfg = hm_inputs.CONFIGS[{"c1": 1, "c5": 5}.get(name, 3)]
         m = int(name[3:]) if name.startswith("c3m") else 1

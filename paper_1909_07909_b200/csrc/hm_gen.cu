@@ -138,40 +138,23 @@ void gen_build_image(const GenPlan& G, std::vector<char>* img) {
   memcpy(img->data() + G.off_lorder, G.leaf_order.data(), sizeof(int32_t) * G.leaf_order.size());
 }
 
-// The tables go to the workspace with one asynchronous copy from a pinned
-// staging buffer (a per-thread ring of 4; a slot is reused only after its
-// previous copy has completed), so the call does not synchronise the stream.
-hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* w, cudaStream_t s) {
-  struct Ring {
-    char* buf[4] = {};
-    size_t cap[4] = {};
-    cudaEvent_t ev[4] = {};
-    bool used[4] = {};
-    int next = 0;
-  };
-  thread_local Ring r;
-  const int slot = r.next;
-  r.next = (r.next + 1) % 4;
-  if (r.used[slot] && cudaEventSynchronize(r.ev[slot]) != cudaSuccess) return cuda_check("table staging event");
-  if (r.cap[slot] < img.size()) {
-    // grow to the next power of two (at least 1 MB): alternating table sizes do not
-    // re-pin a buffer on every call (cudaFreeHost synchronises the device)
-    size_t cap = (size_t)1 << 20;
-    while (cap < img.size()) cap <<= 1;
-    if (r.buf[slot]) cudaFreeHost(r.buf[slot]);
-    r.buf[slot] = nullptr;
-    r.cap[slot] = 0;
-    if (cudaHostAlloc(reinterpret_cast<void**>(&r.buf[slot]), cap, cudaHostAllocDefault) != cudaSuccess)
-      return cuda_check("pinned staging buffer for the tree tables");
-    r.cap[slot] = cap;
+// The tables go to the workspace with one asynchronous copy from the plan's
+// pinned image (PinnedImage: pinned once per cached plan), so the call neither
+// synchronises the stream nor allocates.
+hm_status gen_upload_tables(const PinnedImage& img, size_t off_tab, char* w, cudaStream_t s) {
+  if (img.empty()) return HM_OK;
+  if (!img.pinned) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&img.pinned), img.size(), cudaHostAllocDefault) != cudaSuccess) {
+      img.pinned = nullptr;
+      return cuda_check("pinned copy of the tree tables");
+    }
+    memcpy(img.pinned, img.host.data(), img.size());
+    if (cudaEventCreateWithFlags(&img.done, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_check("table upload event");
   }
-  if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot], cudaEventDisableTiming) != cudaSuccess)
-    return cuda_check("table staging event");
-  memcpy(r.buf[slot], img.data(), img.size());
-  if (cudaMemcpyAsync(w + off_tab, r.buf[slot], img.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
-      cudaEventRecord(r.ev[slot], s) != cudaSuccess)
+  if (cudaMemcpyAsync(w + off_tab, img.pinned, img.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaEventRecord(img.done, s) != cudaSuccess)
     return cuda_check("H2D copy of the tree tables");
-  r.used[slot] = true;
   return HM_OK;
 }
 
@@ -351,7 +334,7 @@ struct GenCached {
   std::vector<int32_t> ranks;
   GenPlan G;
   HssPlan H;
-  std::vector<char> img;
+  PinnedImage img;
 };
 
 const GenCached* gen_cached(int kind, int64_t n, int32_t p, const int64_t* c, const int32_t* ranks, int32_t k,
@@ -375,7 +358,7 @@ const GenCached* gen_cached(int kind, int64_t n, int32_t p, const int64_t* c, co
   if (*st) return nullptr;
   g.c.assign(c, c + nl);
   if (nr) g.ranks.assign(ranks, ranks + nr);
-  gen_build_image(g.G, &g.img);
+  gen_build_image(g.G, &g.img.host);
   cache.insert(cache.begin(), std::move(g));
   if (cache.size() > 4) cache.pop_back();
   return &cache.front();

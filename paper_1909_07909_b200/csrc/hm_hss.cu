@@ -880,7 +880,7 @@ hm_status noderank_plan(const hm_tree* tree, const int32_t* kn, int32_t nrhs, No
   return HM_OK;
 }
 
-hm_status gen_upload_tables(const std::vector<char>& img, size_t off_tab, char* w, cudaStream_t s);
+hm_status gen_upload_tables(const PinnedImage& img, size_t off_tab, char* w, cudaStream_t s);
 
 // Per-thread cache of the last 4 per-node plans (key: tree, node ranks, nrhs).
 struct NodeRankCached {
@@ -888,7 +888,7 @@ struct NodeRankCached {
   int32_t p, nrhs;
   std::vector<int32_t> kn;
   NodeRankPlan N;
-  std::vector<char> img;
+  PinnedImage img;
 };
 
 const NodeRankCached* noderank_cached(const hm_tree* tree, const int32_t* kn, int32_t nrhs, hm_status* st) {
@@ -908,8 +908,8 @@ const NodeRankCached* noderank_cached(const hm_tree* tree, const int32_t* kn, in
   c.n = tree->n; c.leaf = tree->leaf; c.p = p; c.nrhs = nrhs;
   if ((*st = noderank_plan(tree, kn, nrhs, &c.N))) return nullptr;
   if (kn) c.kn.assign(kn, kn + nn);
-  c.img.resize(sizeof(hm::PadBlock) * c.N.blocks.size());
-  if (!c.img.empty()) memcpy(c.img.data(), c.N.blocks.data(), c.img.size());
+  c.img.host.resize(sizeof(hm::PadBlock) * c.N.blocks.size());
+  if (!c.img.empty()) memcpy(c.img.host.data(), c.N.blocks.data(), c.img.size());
   cache.insert(cache.begin(), std::move(c));
   if (cache.size() > 4) cache.pop_back();
   return &cache.front();

@@ -30,6 +30,49 @@
 
 namespace hmi {
 
+// Host image of a cached plan's device tables, with a pinned copy made on the
+// first upload and kept for the life of the cache entry: every later call is
+// one asynchronous H2D copy, no staging memcpy and no pinned allocation (which
+// synchronises the device and can take milliseconds in a process that already
+// pins gigabytes). The destructor waits for the last copy before unpinning.
+struct PinnedImage {
+  std::vector<char> host;
+  mutable char* pinned = nullptr;
+  mutable cudaEvent_t done = nullptr;
+  PinnedImage() = default;
+  PinnedImage(const PinnedImage&) = delete;
+  PinnedImage& operator=(const PinnedImage&) = delete;
+  PinnedImage(PinnedImage&& o) noexcept : host(std::move(o.host)), pinned(o.pinned), done(o.done) {
+    o.pinned = nullptr;
+    o.done = nullptr;
+  }
+  PinnedImage& operator=(PinnedImage&& o) noexcept {
+    if (this != &o) {
+      release();
+      host = std::move(o.host);
+      pinned = o.pinned;
+      done = o.done;
+      o.pinned = nullptr;
+      o.done = nullptr;
+    }
+    return *this;
+  }
+  ~PinnedImage() { release(); }
+  void release() {
+    if (done) {
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+      done = nullptr;
+    }
+    if (pinned) {
+      cudaFreeHost(pinned);
+      pinned = nullptr;
+    }
+  }
+  size_t size() const { return host.size(); }
+  bool empty() const { return host.empty(); }
+};
+
 // ------------------------------------------------------------ errors --
 extern thread_local std::string g_err;
 extern thread_local int32_t g_launches;

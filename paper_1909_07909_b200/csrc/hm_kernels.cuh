@@ -559,18 +559,50 @@ static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadPa
   double* __restrict__ d = P.dst[b.arr] + b.dst;
   // threads over the padded block's elements (consecutive threads: consecutive
   // destination elements), 4 loads in flight per thread before their stores
-  const int64_t tot = (int64_t)b.drows * b.dcols;
-  for (int64_t e0 = threadIdx.x; e0 < tot; e0 += 4 * kThreads) {
+  if ((int64_t)b.drows * b.dcols >= (1ll << 31)) {  // huge leaf blocks: 64-bit index math
+    for (int64_t e = threadIdx.x; e < (int64_t)b.drows * b.dcols; e += kThreads) {
+      const int64_t r = e / b.dcols, c = e - r * b.dcols;
+      d[e] = (r < b.rows && c < b.cols) ? __ldg(s + r * b.cols + c) : 0.0;
+    }
+    continue;
+  }
+  if (b.dcols <= 64) {  // every block of the per-node layout (ranks <= kMaxRank): warp per row, no division
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r0 = warp; r0 < b.drows; r0 += 4 * (kThreads / 32)) {  // 4 rows per warp in flight
+      double v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * (kThreads / 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = lane + 32 * h;
+          v[u][h] = (r < b.rows && c < b.cols) ? __ldg(s + (int64_t)r * b.cols + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * (kThreads / 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = lane + 32 * h;
+          if (r < b.drows && c < b.dcols) d[(int64_t)r * b.dcols + c] = v[u][h];
+        }
+      }
+    }
+    continue;
+  }
+  const int tot = b.drows * b.dcols;  // 32-bit index math (a 64-bit division per element was the cost)
+  for (int e0 = threadIdx.x; e0 < tot; e0 += 4 * kThreads) {
     double v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t e = e0 + (int64_t)u * kThreads;
-      const int r = (int)(e / b.dcols), c = (int)(e - (int64_t)r * b.dcols);
-      v[u] = (e < tot && r < b.rows && c < b.cols) ? __ldg(s + (int64_t)r * b.cols + c) : 0.0;
+      const int e = e0 + u * kThreads;
+      const int r = e / b.dcols, c = e - r * b.dcols;
+      v[u] = (e < tot && r < b.rows && c < b.cols) ? __ldg(s + r * b.cols + c) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t e = e0 + (int64_t)u * kThreads;
+      const int e = e0 + u * kThreads;
       if (e < tot) d[e] = v[u];
     }
   }

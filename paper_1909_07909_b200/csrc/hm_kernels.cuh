@@ -566,31 +566,6 @@ static __global__ void __launch_bounds__(kThreads) pad_blocks_kernel(const PadPa
     }
     continue;
   }
-  if (b.dcols <= 64) {  // every block of the per-node layout (ranks <= kMaxRank): warp per row, no division
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int r0 = warp; r0 < b.drows; r0 += 4 * (kThreads / 32)) {  // 4 rows per warp in flight
-      double v[4][2];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = r0 + u * (kThreads / 32);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = lane + 32 * h;
-          v[u][h] = (r < b.rows && c < b.cols) ? __ldg(s + (int64_t)r * b.cols + c) : 0.0;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = r0 + u * (kThreads / 32);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = lane + 32 * h;
-          if (r < b.drows && c < b.dcols) d[(int64_t)r * b.dcols + c] = v[u][h];
-        }
-      }
-    }
-    continue;
-  }
   const int tot = b.drows * b.dcols;  // 32-bit index math (a 64-bit division per element was the cost)
   for (int e0 = threadIdx.x; e0 < tot; e0 += 4 * kThreads) {
     double v[4];

@@ -648,6 +648,51 @@ hm_status ranked_mma_launch(const hm::RankedMmaParams& rp, bool up, cudaStream_t
   return ranked_mma_launch_nt<4>(rp, up, s);
 }
 
+// The small levels (< kRankedSweepNodes nodes) of both per-level-rank sweeps in
+// one cooperative launch (hss_ranked_sweep_kernel): a grid barrier between
+// levels instead of a kernel boundary.
+#ifndef HM_RANKED_SWEEP
+#define HM_RANKED_SWEEP 1
+#endif
+constexpr int64_t kRankedSweepNodes = 2048;
+
+template <int NT, typename Steps>
+hm_status ranked_sweep_launch_nt(const Steps& steps, size_t w0, size_t w1, cudaStream_t s) {
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    int dev = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hm::hss_ranked_sweep_kernel<NT>, 256, 0) !=
+        cudaSuccess)
+      return cuda_check("occupancy query (hss_ranked_sweep)");
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  hm::RankedSweepParams sp;
+  memset(&sp, 0, sizeof sp);
+  int64_t most = 1;
+  for (size_t i = w0; i < w1; ++i) {
+    sp.step[sp.nsteps] = steps[i].rp;
+    sp.up[sp.nsteps] = steps[i].up ? 1 : 0;
+    ++sp.nsteps;
+    most = std::max<int64_t>(most, steps[i].rp.nodes * (steps[i].rp.k / 8) * ((steps[i].rp.m + NT * 8 - 1) / (NT * 8)));
+  }
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms, (most + 7) / 8)));
+  void* args[] = {&sp};
+  cudaError_t e = cudaSuccess;
+  hm_status st = launch(HM_NT_NAME("hss_ranked_sweep"), s, [&] {
+    e = cudaLaunchCooperativeKernel((const void*)hm::hss_ranked_sweep_kernel<NT>, grid, dim3(256), args, 0, s);
+  });
+  if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_ranked_sweep: %s", cudaGetErrorString(e));
+  return st;
+}
+
+template <typename Steps>
+hm_status ranked_sweep_launch(const Steps& steps, size_t w0, size_t w1, int32_t m, cudaStream_t s) {
+  if (m <= 8) return ranked_sweep_launch_nt<1>(steps, w0, w1, s);
+  if (m <= 16) return ranked_sweep_launch_nt<2>(steps, w0, w1, s);
+  return ranked_sweep_launch_nt<4>(steps, w0, w1, s);
+}
+
 hm_status hss_ranked_plan(const hm_tree* tree, const int32_t* ranks, int32_t nrhs, RankedPlan* Q) {
   hm_status st = check_tree(tree);
   if (st) return st;
@@ -739,40 +784,70 @@ hm_status hss_ranked_run(const hm_tree* tree, const int32_t* ranks, int op, cons
         if (st) return st;
       }
     }
-    // upsweep l = p-1..1 through W^T (2k_{l+1} x k_l)
+    // the level steps in execution order: upsweep l = p-1..1 through W^T
+    // (2k_{l+1} x k_l), then cores (levels 1..p, reading G1) + downsweep through R
+    struct Step {
+      bool up, mma;
+      int l;
+      hm::RankedMmaParams rp;
+      hm::HssRankedLevelParams hp;
+    };
+    std::vector<Step> steps;
     for (int l = p - 1; l >= 1; --l) {
       if (Q.kl[l] == 0) continue;
-      if (ranked_mma_ok(Q.kl[l], 2 * Q.kl[l + 1], 0, nrhs)) {
-        const hm::RankedMmaParams rp{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l],
-                                     (int64_t)1 << l, Q.kl[l], Q.kl[l + 1], 0, nrhs, 0};
-        if ((st = ranked_mma_launch(rp, true, s))) return st;
-        continue;
-      }
-      const hm::HssRankedLevelParams hp{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l], l, Q.kl[l],
-                                        Q.kl[l + 1], 0, nrhs, 0};
-      const int64_t total = ((int64_t)1 << l) * Q.kl[l] * nrhs;
-      if ((st = launch("hss_up_ranked", s,
-                       [&] { hm::hss_up_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); })))
-        return st;
+      Step t;
+      t.up = true;
+      t.l = l;
+      t.mma = ranked_mma_ok(Q.kl[l], 2 * Q.kl[l + 1], 0, nrhs);
+      t.rp = hm::RankedMmaParams{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l], (int64_t)1 << l,
+                                 Q.kl[l], Q.kl[l + 1], 0, nrhs, 0};
+      t.hp = hm::HssRankedLevelParams{W + Q.rw[l], nullptr, xh + Q.cf[l + 1], nullptr, xh + Q.cf[l], l, Q.kl[l],
+                                      Q.kl[l + 1], 0, nrhs, 0};
+      steps.push_back(t);
     }
-    // cores (levels 1..p, reading G1) + downsweep through R (k_l x k_{l-1} halves)
     for (int l = 1; l <= p; ++l) {
       if (Q.kl[l] == 0) continue;
       const bool from_parent = l >= 2 && Q.kl[l - 1] > 0;
-      if (ranked_mma_ok(Q.kl[l], Q.kl[l], from_parent ? Q.kl[l - 1] : 0, nrhs)) {
-        const hm::RankedMmaParams rp{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
-                                     from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], (int64_t)1 << l,
-                                     Q.kl[l], 0, from_parent ? Q.kl[l - 1] : 0, nrhs, op};
-        if ((st = ranked_mma_launch(rp, false, s))) return st;
+      Step t;
+      t.up = false;
+      t.l = l;
+      t.mma = ranked_mma_ok(Q.kl[l], Q.kl[l], from_parent ? Q.kl[l - 1] : 0, nrhs);
+      t.rp = hm::RankedMmaParams{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
+                                 from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], (int64_t)1 << l, Q.kl[l], 0,
+                                 from_parent ? Q.kl[l - 1] : 0, nrhs, op};
+      t.hp = hm::HssRankedLevelParams{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
+                                      from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], l, Q.kl[l], 0,
+                                      from_parent ? Q.kl[l - 1] : 0, nrhs, op};
+      steps.push_back(t);
+    }
+    // the small levels (contiguous in this order: the top of both sweeps) in one
+    // cooperative launch when every one of them takes the DMMA kernels
+    size_t w0 = steps.size(), w1 = steps.size();
+    for (size_t i = 0; i < steps.size(); ++i)
+      if (((int64_t)1 << steps[i].l) < kRankedSweepNodes) {
+        w0 = std::min(w0, i);
+        w1 = i + 1;
+      }
+    bool sweep = HM_RANKED_SWEEP && w1 > w0 + 1;
+    for (size_t i = w0; sweep && i < w1; ++i) sweep = steps[i].mma;
+    for (size_t i = 0; i < steps.size(); ++i) {
+      if (sweep && i == w0) {
+        if ((st = ranked_sweep_launch(steps, w0, w1, nrhs, s))) return st;
+        i = w1 - 1;
         continue;
       }
-      const hm::HssRankedLevelParams hp{from_parent ? R + Q.rw[l - 1] : nullptr, B + Q.bo[l], xh + Q.cf[l],
-                                        from_parent ? yh + Q.cf[l - 1] : nullptr, yh + Q.cf[l], l, Q.kl[l], 0,
-                                        from_parent ? Q.kl[l - 1] : 0, nrhs, op};
-      const int64_t total = ((int64_t)1 << l) * Q.kl[l] * nrhs;
-      if ((st = launch("hss_down_ranked", s,
-                       [&] { hm::hss_down_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); })))
-        return st;
+      const Step& t = steps[i];
+      if (t.mma) {
+        if ((st = ranked_mma_launch(t.rp, t.up, s))) return st;
+        continue;
+      }
+      const int64_t total = ((int64_t)1 << t.l) * Q.kl[t.l] * nrhs;
+      const hm::HssRankedLevelParams hp = t.hp;
+      st = t.up ? launch("hss_up_ranked", s,
+                         [&] { hm::hss_up_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); })
+                : launch("hss_down_ranked", s,
+                         [&] { hm::hss_down_ranked_kernel<<<grid_for(total), hm::kThreads, 0, s>>>(hp); });
+      if (st) return st;
     }
   }
   // Step 4: Y(I_i) = U_i y_i + D_i X(I_i) (k_p columns)

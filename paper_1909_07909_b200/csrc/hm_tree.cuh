@@ -768,15 +768,43 @@ __device__ __forceinline__ void ranked_store(const double (&acc)[NT][2], double*
   }
 }
 
-// x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]   (Fig. 5 right, P:689-694)
+// One warp task of a level (defined below, shared with the cooperative sweep).
+template <int NT>
+__device__ __forceinline__ void ranked_up_task(const RankedMmaParams& P, int64_t gw, int lane);
+template <int NT>
+__device__ __forceinline__ void ranked_down_task(const RankedMmaParams& P, int64_t gw, int lane);
+
 template <int NT>
 __global__ void __launch_bounds__(256) hss_up_ranked_mma_kernel(const RankedMmaParams P) {
-  const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= P.nodes * (P.k / 8) * ((P.m + NT * 8 - 1) / (NT * 8))) return;
+  ranked_up_task<NT>(P, gw, threadIdx.x & 31);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) hss_down_ranked_mma_kernel(const RankedMmaParams P) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= P.nodes * (P.k / 8) * ((P.m + NT * 8 - 1) / (NT * 8))) return;
+  ranked_down_task<NT>(P, gw, threadIdx.x & 31);
+}
+
+// The small levels of the per-level-rank sweeps in one cooperative launch: the
+// steps (up levels, then down levels, each a RankedMmaParams) run in order with
+// a grid barrier between them; inside a step the warps stride over the warp
+// tasks of hss_up_ranked_mma / hss_down_ranked_mma (the same arithmetic).
+constexpr int kRankedSweepMax = 2 * kMaxLevels;
+struct RankedSweepParams {
+  RankedMmaParams step[kRankedSweepMax];
+  int32_t up[kRankedSweepMax];  // 1: upsweep step, 0: downsweep step
+  int32_t nsteps;
+};
+
+// x_l[i] = W_{l,i}^T [x_{l+1}[2i]; x_{l+1}[2i+1]]   (Fig. 5 right, P:689-694)
+template <int NT>
+__device__ __forceinline__ void ranked_up_task(const RankedMmaParams& P, int64_t gw, int lane) {
   const int tiles = P.k / 8, nck = (P.m + NT * 8 - 1) / (NT * 8);
   const int64_t per = (int64_t)tiles * nck;
   const int64_t node = gw / per;
-  if (node >= P.nodes) return;
   const int rem = (int)(gw - node * per), tile = rem % tiles, c0 = (rem / tiles) * NT * 8;
   bool colok[NT];
 #pragma unroll
@@ -784,7 +812,6 @@ __global__ void __launch_bounds__(256) hss_up_ranked_mma_kernel(const RankedMmaP
   double acc[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-  // A = W^T: A[a][r] = W[r][a], W row-major [2kc][k]
   ranked_tile_mma<NT, true>(acc, P.G + node * 2 * P.kc * P.k + 8 * tile, P.k,
                             P.xin + 2 * node * (int64_t)P.kc * P.m + c0, P.m, 2 * P.kc, colok, lane);
   ranked_store<NT>(acc, P.out + (node * P.k + 8 * tile) * (int64_t)P.m, P.m, c0, lane);
@@ -793,13 +820,10 @@ __global__ void __launch_bounds__(256) hss_up_ranked_mma_kernel(const RankedMmaP
 // y_l[2q+w] = S_w x_l[2q+1-w] + R_{l-1,q}[w] y_{l-1}[q]   (reading G1;
 // bt: S'_w = (S_{1-w})^T, the adjoint's cores)
 template <int NT>
-__global__ void __launch_bounds__(256) hss_down_ranked_mma_kernel(const RankedMmaParams P) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void ranked_down_task(const RankedMmaParams& P, int64_t gw, int lane) {
   const int tiles = P.k / 8, nck = (P.m + NT * 8 - 1) / (NT * 8);
   const int64_t per = (int64_t)tiles * nck;
   const int64_t jn = gw / per;
-  if (jn >= P.nodes) return;
   const int rem = (int)(gw - jn * per), tile = rem % tiles, c0 = (rem / tiles) * NT * 8;
   const int64_t q = jn >> 1;
   const int w = (int)(jn & 1);
@@ -824,6 +848,24 @@ __global__ void __launch_bounds__(256) hss_down_ranked_mma_kernel(const RankedMm
                                colok, lane);
   }
   ranked_store<NT>(acc, P.out + (jn * k + 8 * tile) * (int64_t)m, m, c0, lane);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) hss_ranked_sweep_kernel(const RankedSweepParams S) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int st = 0; st < S.nsteps; ++st) {
+    if (st) grid.sync();
+    const RankedMmaParams& P = S.step[st];
+    const int64_t tasks = P.nodes * (P.k / 8) * ((P.m + NT * 8 - 1) / (NT * 8));
+    for (int64_t gw = gw0; gw < tasks; gw += nw) {
+      if (S.up[st]) ranked_up_task<NT>(P, gw, lane);
+      else ranked_down_task<NT>(P, gw, lane);
+    }
+  }
 }
 
 }  // namespace hm

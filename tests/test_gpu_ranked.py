@@ -143,3 +143,27 @@ def test_hss_ranked_dmma_levels_ran(hm, op):
     assert {"hss_up_ranked_mma<nt2>", "hss_down_ranked_mma<nt2>", "hss_down_ranked"} <= names, names
     Yr = oracle.hss_matvec_ranked(n, p, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
     assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+@pytest.mark.parametrize("op", [0, 1])
+def test_hss_ranked_sweep_small_levels(hm, op):
+    """The bench sweep's per-level tree (n = 2^20, leaf 128, 13 levels, ranks 32/24/16,
+    nrhs 16): the levels with < 2048 nodes of both sweeps run in one cooperative launch
+    (hss_ranked_sweep), the bigger ones one DMMA launch each. Every row, A and A^T."""
+    n, p, m = 1 << 20, 13, 16
+    ranks = [32] * 4 + [24] * 4 + [16] * 5
+    s = hm_inputs.hss_random_ranked(n, p, ranks, cid=53)
+    X = hm_inputs.rhs(n, m, cid=53)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    hm.hm_profile_collect()
+    hm.hm_profile_enable(True)
+    try:
+        Y = hm.hss_matvec_ranked(n, p, n >> p, ranks, *g, dev(X), op=op)
+        torch.cuda.synchronize()
+    finally:
+        hm.hm_profile_enable(False)
+    names = [t[0] for t in hm.hm_profile_collect()]
+    assert names.count("hss_ranked_sweep<nt2>") == 1, names
+    assert "hss_up_ranked_mma<nt2>" in names and "hss_down_ranked_mma<nt2>" in names, names
+    Yr = oracle.hss_matvec_ranked(n, p, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
+    assert relerr(Y.cpu().numpy(), Yr) <= TOL

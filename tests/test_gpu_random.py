@@ -92,3 +92,42 @@ def test_random_general_trees(hm, seed):
         torch.cuda.synchronize()
         ref = (oracle.hss_matvec_t if op else oracle.hss_matvec)(n, p, k, D, U, V, R, W, B, X, c=c)
         assert relerr(Y.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_ragged_wide(hm, seed):
+    """Random ragged trees with ranks that are multiples of 8 on most levels and nrhs
+    2..40: the 128-bit-fragment DMMA leaf pass (gen_leaf_mma_al) and the one-tile
+    V^T X meet random leaf sizes, alignments and column chunks."""
+    rng = np.random.default_rng(1300 + seed)
+    p = int(rng.integers(3, 8))
+    n = int(rng.integers(8 << p, 12000))
+    c = ragged_tree(n, p, 50 + seed, empty=float(rng.uniform(0, 0.2)))
+    ranks = [int(rng.choice([8, 16, 16, 32, 3, 0])) for _ in range(p)]
+    m = int(rng.integers(2, 41))
+    D, U, V = random_hodlr_general(c, p, ranks, rng)
+    X = rng.standard_normal((n, m))
+    Y = hm.hodlr_matvec_general(n, p, c, ranks, dev(D), dev(U), dev(V), dev(X), op=0)
+    torch.cuda.synchronize()
+    assert relerr(Y.cpu().numpy(), oracle.hodlr_matvec(n, p, ranks, D, U, V, X, c=c)) <= TOL
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_hss_per_level_ranks(hm, seed):
+    """Random per-level HSS ranks (multiples of 8 take the DMMA level kernels and the
+    cooperative small-level sweep, others the CUDA-core kernels), random nrhs and
+    operator, every row against the oracle."""
+    rng = np.random.default_rng(1400 + seed)
+    p = int(rng.integers(2, 10))
+    b = int(rng.choice([32, 64, 128]))
+    n = b << p
+    ranks = [int(rng.choice([8, 16, 24, 32, 5, 12])) for _ in range(p)]
+    m = int(rng.integers(2, 35))
+    op = int(rng.integers(0, 2))
+    s = hm_inputs.hss_random_ranked(n, p, ranks, cid=1400 + seed)
+    X = hm_inputs.rhs(n, m, cid=1400 + seed)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    Y = hm.hss_matvec_ranked(n, p, b, ranks, *g, dev(X), op=op)
+    torch.cuda.synchronize()
+    ref = oracle.hss_matvec_ranked(n, p, ranks, s.D, s.U, s.V, s.R, s.W, s.B, X, trans=bool(op))
+    assert relerr(Y.cpu().numpy(), ref) <= TOL

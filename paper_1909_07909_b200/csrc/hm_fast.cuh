@@ -760,6 +760,102 @@ __global__ void __launch_bounds__(256, MINB) leaf_mma_kernel(const LeafParams P)
   }
 }
 
+// HSS Step 4 with the leaf level's coupling + downsweep folded in (Fig. 5
+// right): per leaf i = 2q + w the CTA first forms
+//   y_i = S_w x_{i^1} + R_{p-1,q}[w] y_{p-1,q}        (KT x MC columns c0..)
+// — S_w, R rows as A fragments from global memory, x_{i^1} and y_{p-1,q}
+// staged with X(I_i) — keeps it in shared memory in place of the y_i the
+// separate downsweep launch would have written, then runs the leaf pass
+// Y(I_i) = D_i X(I_i) + U_i y_i of leaf_mma_kernel. Saves the level-p y blocks'
+// write and re-read (and one launch). Forward product, p >= 2, one U segment.
+struct LeafDownParams {
+  const double* B;    // cores, pair (l, q) at 2^l - 1 + q ([2][KT][KT])
+  const double* R;    // translations, node (l, i) at 2^l - 2 + i ([2KT][KT])
+  const double* xh;   // x of the leaves: leaf i at i KT m
+  const double* yhp;  // y of level p-1: node q at q KT m
+  int32_t p;
+  int32_t pad;
+};
+
+template <int RG, int NT, int PF, int MINB, int KT>
+__global__ void __launch_bounds__(256, MINB) leaf_mma_down_kernel(const LeafParams P, const LeafDownParams Q) {
+  extern __shared__ double sm[];
+  constexpr int MC = NT * 8, ZS = MC + 2;
+  const int nchunks = (P.m + MC - 1) / MC;
+  const int64_t leaf = blockIdx.x / nchunks;
+  const int c0 = (int)(blockIdx.x - leaf * nchunks) * MC;
+  const int64_t b = P.b;  // == 64 RG
+  const int64_t r0 = leaf * b;
+  const int m = P.m;
+  const int mc = min(MC, m - c0);
+  const int64_t km = (int64_t)KT * m;
+  const int64_t q = leaf >> 1;
+  const int w = (int)(leaf & 1);
+  double* Z = sm;                 // X(I_i): b rows
+  double* ZT = Z + b * ZS;        // x_{i^1} (KT rows), then y_i (KT rows)
+  double* ZP = ZT + KT * ZS;      // y_{p-1,q}: KT rows
+  stage_rows_async(Z, ZS, P.X + r0 * m + c0, m, (int)b, mc, MC);
+  stage_rows_async(ZT, ZS, Q.xh + (leaf ^ 1) * km + c0, m, KT, mc, MC);
+  stage_rows_async(ZP, ZS, Q.yhp + q * km + c0, m, KT, mc, MC);
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = lane >> 2, j = lane & 3;
+  // y_i: (KT / 8) x NT tiles of 8 x 8, over the 8 warps; K = KT from each operand
+  constexpr int TILES = (KT / 8) * NT, TPW = (TILES + 7) / 8;
+  const double* S = Q.B + ((((int64_t)1 << (Q.p - 1)) - 1 + q) * 2 + w) * KT * KT;
+  const double* Rw = Q.R + ((((int64_t)1 << (Q.p - 1)) - 2 + q) * 2 * KT + (int64_t)w * KT) * KT;
+  double yacc[TPW][1][1][2];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    yacc[u][0][0][0] = yacc[u][0][0][1] = 0.0;
+    const int t = warp + 8 * u;
+    if (t < TILES) {
+      const int rt = t % (KT / 8), ct = t / (KT / 8);
+      warp_rowmajor_mma<1, 1, false, false, 2>(yacc[u], S + (int64_t)8 * rt * KT, KT, KT, ZT + ct * 8, ZS, MC, lane);
+      warp_rowmajor_mma<1, 1, false, false, 2>(yacc[u], Rw + (int64_t)8 * rt * KT, KT, KT, ZP + ct * 8, ZS, MC, lane);
+    }
+  }
+  __syncthreads();  // every warp has read x_{i^1}: its rows now take y_i
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int t = warp + 8 * u;
+    if (t < TILES) {
+      const int rt = t % (KT / 8), ct = t / (KT / 8);
+      double* o = ZT + (8 * rt + i) * ZS + ct * 8 + 2 * j;
+      o[0] = yacc[u][0][0][0];
+      o[1] = yacc[u][0][0][1];
+    }
+  }
+  __syncthreads();
+  double acc[RG][NT][2];
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[rg][nt][0] = acc[rg][nt][1] = 0.0;
+  const int64_t wrow = (int64_t)warp * 8 * RG;
+  warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.D + leaf * b * b + wrow * b, b, (int)b, Z, ZS, MC, lane);
+  warp_rowmajor_mma<RG, NT, false, false, PF>(acc, P.seg[0].A + (r0 + wrow) * KT, KT, KT, ZT, ZS, MC, lane);
+#pragma unroll
+  for (int rg = 0; rg < RG; ++rg) {
+    double* y = P.Y + (r0 + wrow + 8 * rg + i) * m;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c = c0 + nt * 8 + 2 * j;
+      if (c + 1 < m) {
+        if ((m & 1) == 0) {
+          *reinterpret_cast<double2*>(y + c) = make_double2(acc[rg][nt][0], acc[rg][nt][1]);
+        } else {
+          y[c] = acc[rg][nt][0];
+          y[c + 1] = acc[rg][nt][1];
+        }
+      } else if (c < m) {
+        y[c] = acc[rg][nt][0];
+      }
+    }
+  }
+}
+
 // One warp accumulates C (16 MPW x 8 NT) += A^T B over K rows, A [K][lda]
 // row-major (the warp's rank columns start at A), B [K][ldb] (columns c0..).
 // The 4 rows of one k-step are rows r + (lane & 3). One LDG.128 of A covers 16

@@ -487,6 +487,12 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
   return HM_OK;
 }
 
+// HSS Step 4 with the leaf level's coupling + downsweep (hm_fast.cuh
+// leaf_mma_down_kernel) instead of a separate level-p downsweep launch.
+#ifndef HM_LEAF_DOWN
+#define HM_LEAF_DOWN 1
+#endif
+
 // ---- small trees: one cooperative launch (hm_small.cuh) ----
 #ifndef HM_NO_SMALL
 #define HM_NO_SMALL 0
@@ -589,17 +595,39 @@ hm_status hss_run(const hm_tree* tree, int32_t k, const double* D, const double*
     }
     if (st != HM_ERR_UNSUPPORTED) return st;  // not co-resident on this device: the level-by-level path
   }
+  // the leaf level's coupling + downsweep inside the leaf pass (leaf_mma_down_kernel)
+  // for up to 16 columns per CTA: measured on config 4's tree, nrhs 8 / 16: 1473 ->
+  // 1439 / 1744 -> 1703 us; at 32 columns the leaf pass sits at the fp64 ridge and
+  // the extra DMMAs cost more than the separate HBM-bound launch (2465 -> 2550 us)
+  const bool fuse_down = HM_LEAF_DOWN && coupled && op == 0 && P.mma_levels && !P.gemv_levels &&
+                         P.leaf == LeafPath::kMma && P.p >= 2 && P.nt_leaf <= 2 &&
+                         leaf_down_supported(P.b, k, P.nt_leaf);
   if (coupled) {
     // Step 1 (leaf x), then the upsweep levels and Steps 2-3 in one tree phase
     int up_from = 0;
     if ((st = hss_up_phase(P, V, W, Xd, xh, nullptr, nullptr, stream, &up_from))) return st;
     unsigned* fl = reinterpret_cast<unsigned*>(w + P.off_flags);
     if ((st = hss_tree_phase(P, P.p, W, R, B, xh, yh, nullptr, nullptr, up_from >= 1, true, stream, op,
-                             std::max(up_from, 1), -1, P.mma_levels ? fl : nullptr)))
+                             std::max(up_from, 1), fuse_down ? P.p - 1 : -1, P.mma_levels ? fl : nullptr)))
       return st;
   }
   const double* yleaf = coupled ? yh + (((int64_t)1 << P.p) - 2) * km : nullptr;
-  if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) return st;
+  if (fuse_down) {
+    hm::LeafParams lp;
+    memset(&lp, 0, sizeof lp);
+    lp.D = D; lp.X = Xd; lp.Y = Yd; lp.b = P.b; lp.m = P.m; lp.mc = P.mc_leaf;
+    hm::LeafSeg& sg = lp.seg[lp.nseg++];
+    sg.A = U; sg.T = yleaf; sg.k = k; sg.shift = 0; sg.xr = 0;
+    lp.ktot = k;
+    const hm::LeafDownParams q{B, R, xh + (((int64_t)1 << P.p) - 2) * km, yh + (((int64_t)1 << (P.p - 1)) - 2) * km,
+                               P.p, 0};
+    st = leaf_down_dispatch(lp, q, 1ll << P.p, k, P.nt_leaf, stream);
+    if (st == HM_ERR_UNSUPPORTED) return fail(HM_ERR_UNSUPPORTED, "leaf_mma_down: no instance (b=%lld, nt=%d)",
+                                              (long long)P.b, P.nt_leaf);
+    if (st) return st;
+  } else if ((st = hss_leaf_phase(P, D, U, Xd, Yd, yleaf, stream, op != 0))) {
+    return st;
+  }
   if (flags & HM_WS_HOSTIO) {
     if (cudaMemcpyAsync(Y, Yd, xy_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
       return cuda_check("D2H copy of Y");

@@ -194,6 +194,11 @@ enum class VtPath { kNone, kGeneric, kGemv, kMma };
 enum class LeafPath { kGeneric, kGemv, kMma };  // kGemv: TMA ring when the shape allows (leaf_gemv_tma)
 
 // ------------------------------------------------------------ hm_leaf.cu --
+// HSS Step 4 with the leaf level's coupling + downsweep folded in (leaf_mma_down_kernel):
+// HM_ERR_UNSUPPORTED when the shape has no instance (the caller keeps the separate launch).
+hm_status leaf_down_dispatch(const hm::LeafParams& lp, const hm::LeafDownParams& q, int64_t nleaves, int k, int nt,
+                             cudaStream_t s);
+bool leaf_down_supported(int64_t b, int k, int nt);
 hm_status leaf_dispatch(const hm::LeafParams& lp, int64_t nleaves, LeafPath path, int k, int nt, int mc,
                         cudaStream_t s, bool kvary = false);
 

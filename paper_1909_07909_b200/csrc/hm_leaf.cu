@@ -106,7 +106,39 @@ hm_status launch_leaf_mma(const hm::LeafParams& lp, int64_t nleaves, cudaStream_
   });
 }
 
+template <int RG, int NT, int KT>
+hm_status launch_leaf_down(const hm::LeafParams& lp, const hm::LeafDownParams& q, int64_t nleaves, cudaStream_t s) {
+  constexpr int PF = LeafMmaTune<RG, NT>::PF, MINB = LeafMmaTune<RG, NT>::MINB;
+  const size_t smem = sizeof(double) * (size_t)((lp.b + 2 * KT) * (NT * 8 + 2));
+  if (smem > sizeof(double) * (size_t)kSmemBudgetDoubles) return HM_ERR_UNSUPPORTED;
+  const int64_t chunks = (lp.m + NT * 8 - 1) / (NT * 8);
+  allow_smem(hm::leaf_mma_down_kernel<RG, NT, PF, MINB, KT>, smem);
+  return launch("leaf_mma_down", s, [&] {
+    hm::leaf_mma_down_kernel<RG, NT, PF, MINB, KT><<<(unsigned)(nleaves * chunks), 256, smem, s>>>(lp, q);
+  });
+}
+
 }  // namespace
+
+bool leaf_down_supported(int64_t b, int k, int nt) {
+  const int rg = (int)(b / 64);
+  const bool inst = b % 64 == 0 && (k == 16 || k == 32) && (rg == 1 || rg == 2 || rg == 4) &&
+                    (nt == 1 || nt == 2 || (nt == 4 && rg < 4));
+  return inst && (b + 2 * k) * (nt * 8 + 2) <= kSmemBudgetDoubles;
+}
+
+hm_status leaf_down_dispatch(const hm::LeafParams& lp, const hm::LeafDownParams& q, int64_t nleaves, int k, int nt,
+                             cudaStream_t s) {
+  if (lp.nseg != 1 || lp.dtrans || q.p < 2 || !leaf_down_supported(lp.b, k, nt)) return HM_ERR_UNSUPPORTED;
+  const int rg = (int)(lp.b / 64);
+  if (lp.b % 64 != 0) return HM_ERR_UNSUPPORTED;
+#define HM_LD(RG_, NT_)                                                                      \
+  if (rg == RG_ && nt == NT_)                                                                \
+    return k == 16 ? launch_leaf_down<RG_, NT_, 16>(lp, q, nleaves, s) : launch_leaf_down<RG_, NT_, 32>(lp, q, nleaves, s);
+  HM_LD(1, 1) HM_LD(1, 2) HM_LD(1, 4) HM_LD(2, 1) HM_LD(2, 2) HM_LD(2, 4) HM_LD(4, 1) HM_LD(4, 2)
+#undef HM_LD
+  return HM_ERR_UNSUPPORTED;
+}
 
 hm_status leaf_dispatch(const hm::LeafParams& lp, int64_t nleaves, LeafPath path, int k, int nt, int mc,
                         cudaStream_t s, bool kvary) {

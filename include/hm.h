@@ -16,9 +16,10 @@
  *     calling thread's current CUDA device, owned by the caller. The library
  *     allocates no device memory, keeps no pointer after return, never
  *     synchronises the stream and never modifies an input (all inputs are
- *     const). Host-side state it does keep: a per-thread cache of general-tree
- *     plans and a per-thread ring of 4 pinned staging buffers for the tables
- *     those calls (and the per-node-rank HSS call) copy into the workspace;
+ *     const). Host-side state it does keep: a per-thread cache of the last 4
+ *     general-tree (and per-node-rank HSS) plans, each with a pinned copy of the
+ *     tables those calls copy into the workspace (pinned on first use, unpinned
+ *     when the plan leaves the cache);
  *     the communicator of the multi-GPU calls owns an NCCL communicator, a
  *     stream and two events (hm_comm_init / hm_comm_destroy).
  *   - Exception: the *_hostio variants take X and Y as HOST pointers (pinned
@@ -206,8 +207,8 @@ hm_status hss_matvec_ranked(const hm_tree* tree, const int32_t* ranks, int32_t o
  * zero-padded into the per-level layout with K_l = the level's largest rank
  * (in the workspace; exact, the padding is zero) and the per-level path runs:
  * one extra pass over the generators. The table of padded blocks is copied to
- * the workspace asynchronously from a pinned staging buffer (not CUDA-graph
- * capturable). */
+ * the workspace asynchronously from the cached plan's pinned copy (not
+ * CUDA-graph capturable: the first call of a tree pins its table). */
 hm_status hm_hss_noderanked_workspace_bytes(const hm_tree* tree, const int32_t* node_ranks, int32_t nrhs,
                                             size_t* bytes);
 hm_status hss_matvec_noderanked(const hm_tree* tree, const int32_t* node_ranks, int32_t op,
@@ -229,11 +230,11 @@ hm_status hss_matvec_noderanked(const hm_tree* tree, const int32_t* node_ranks, 
  * Limits: largest leaf + sum of ranks <= 20480 (shared-memory staging of a
  * leaf), else HM_ERR_UNSUPPORTED. Errors as for the uniform calls; c not
  * nondecreasing or c[2^p-1] != n is HM_ERR_INVALID_ARG. The tables derived
- * from c are planned on the host (cached per thread for the last 4 trees) and
- * copied into the workspace with one asynchronous copy from a pinned staging
- * buffer (a per-thread ring of 4, a slot reused once its copy has completed):
- * the call does not synchronise the stream, but it is not CUDA-graph
- * capturable (the staging buffers are reused). Deterministic.
+ * from c are planned on the host (cached per thread for the last 4 trees, each
+ * plan with a pinned copy of its tables) and copied into the workspace with
+ * one asynchronous copy: the call does not synchronise the stream (a plan
+ * leaving the cache waits for its last copy before unpinning), but it is not
+ * CUDA-graph capturable (the first call of a tree pins its tables). Deterministic.
  * (hodlr_matvec / hodlr_matvec_t route per-level ranks on uniform trees
  * with fewer than 3 levels or leaves not a multiple of 64 here
  * automatically, with the same workspace query.) */

@@ -67,6 +67,28 @@ def step_bytes():
     return hodlr_bytes(C5.n, C5.leaf, C5.levels, C5.k, M5) + hss_bytes(C4.n, C4.leaf, C4.levels, C4.k, M4)
 
 
+def hss_attainable_ms(n, b, p, k, m, copy_gbs):
+    """Config 4's attainable time: every phase at what the machine
+    measurably delivers for it — the leaf pass (D X + U y: 2 n m (b + k) flops over
+    its physical bytes) at the read-stream + DMMA ridge for its intensity
+    (profiles/r02/fp64_peaks_ridge.json, interpolated between 4 and 6 flop/B),
+    Step 1 (V, X read, leaf x written) at the read stream, the tree levels
+    (W, R, B and the coefficient blocks they read and write) at the copy figure."""
+    blk = k * m
+    leaf_flops = 2.0 * n * m * (b + k)
+    leaf_bytes = 8.0 * (n * b + n * k + 2 * n * m + (1 << p) * blk)
+    inten = leaf_flops / leaf_bytes
+    t = min(max((inten - 4.0) / 2.0, 0.0), 1.0)
+    ridge_tf = 27.85 + t * (32.83 - 27.85)
+    step1_bytes = 8.0 * (n * k + n * m + (1 << p) * blk)
+    nodes = (1 << (p + 1)) - 2  # coefficient blocks of levels 1..p
+    gen = 8.0 * (2 * ((1 << p) - 2) * 2 * k * k + ((1 << p) - 1) * 2 * k * k)
+    coef = 8.0 * blk * ((nodes - 2) + (nodes - (1 << p)) + nodes + (nodes - (1 << p)) + nodes)
+    ms = leaf_flops / (ridge_tf * 1e12) * 1e3 + step1_bytes / (READ_STREAM_GBS * 1e9) * 1e3 \
+        + (gen + coef) / (copy_gbs * 1e9) * 1e3
+    return ms
+
+
 def leaf_apply_c5_bytes(n, b, p, k, m):
     """Algorithmic bytes of one HODLR leaf-pass (leaf_gemv) launch: D + every level's U + X + Y."""
     return 8 * (n * b + p * n * k + 2 * n * m)
@@ -746,7 +768,11 @@ def run_ours(args):
                        "fp64_TFLOP/s": round(f4 / (c4_ms * 1e-3) / 1e12, 2),
                        "frac_fp64": round(f4 / (c4_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                        "fp64_peak": f"{FP64_PEAK_TFLOPS} TFLOP/s measured DMMA (profiles/r01_next/fp64_peaks_mix.json)",
-                       "matvecs/s": round(1e3 / c4_ms, 1), "column_matvecs/s": round(M4 * 1e3 / c4_ms, 1)},
+                       "matvecs/s": round(1e3 / c4_ms, 1), "column_matvecs/s": round(M4 * 1e3 / c4_ms, 1),
+                       "attainable_ms": round(hss_attainable_ms(C4.n, C4.leaf, C4.levels, C4.k, M4, peak), 4),
+                       "frac_attainable": round(hss_attainable_ms(C4.n, C4.leaf, C4.levels, C4.k, M4, peak) / c4_ms, 4),
+                       "attainable_note": "leaf pass at the measured read+DMMA ridge, Step 1 at the read stream, "
+                                          "tree levels at the copy figure (DESIGN.md §11)"},
         },
         "kernels": {k_: {"launches_per_step": v[0] // args.steps, "ms_per_step": round(v[1] / args.steps, 4)}
                     for k_, v in sorted(per.items())},

@@ -101,6 +101,12 @@ constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
 #ifndef HM_TREE_STAGE_DOWN
 #define HM_TREE_STAGE_DOWN 0
 #endif
+#ifndef HM_TREE_DOWN2
+#define HM_TREE_DOWN2 1  // two big downsweep levels per launch (hss_down_two_kernel)
+#endif
+#ifndef HM_TREE_DOWN2_MINB
+#define HM_TREE_DOWN2_MINB 3  // measured: 2 -> 3 CTAs per SM, config 4 nrhs 16 down levels 153 -> 135 us
+#endif
 
 
 // ---- nrhs <= 4: warp-per-node GEMV tree levels (hm_treegemv.cuh) ----
@@ -297,9 +303,22 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
     if (st) return st;
   }
-  // downsweep: big levels lbig .. p one launch each
+  // downsweep: big levels lbig .. p one launch each, or, up to 16 columns, two
+  // per launch (hss_down_two, pairs ending at down_last; 3 CTAs per SM, KT = 64
+  // at 2: 3 would spill)
+  constexpr int MINB2 = KT >= 64 ? 2 : HM_TREE_DOWN2_MINB;
+  const size_t smem_two = sizeof(double) * (size_t)hm::tree_down_two_doubles(KT, tp.m, NT);
+  const bool two_ok = HM_TREE_DOWN2 && NT <= 2 && smem_two <= 110 * 1024;
+  if (two_ok) allow_smem(hm::hss_down_two_kernel<KT, NT, MINB2>, smem_two);
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
+    if (two_ok && l >= 2 && l + 1 <= down_last && (down_last - l + 1) % 2 == 0) {
+      st = launch(HM_NT_NAME("hss_down_two"), s,
+                  [&] { hm::hss_down_two_kernel<KT, NT, MINB2><<<pairs, 256, smem_two, s>>>(tp, l); });
+      if (st) return st;
+      ++l;
+      continue;
+    }
     if (HM_TREE_STAGE_DOWN && smem_dn_st <= 200 * 1024) {
       st = launch(HM_NT_NAME("hss_down_stage"), s,
                   [&] { hm::hss_down_stage_kernel<KT, NT><<<pairs, 256, smem_dn_st, s>>>(tp, l); });

@@ -205,6 +205,109 @@ __global__ void __launch_bounds__(256, MINB) hss_down_pair_kernel(const TreePara
   tree_down_pair<KT, NT, false>(P, l, blockIdx.x, sm);
 }
 
+// A fragments of one down task (row group rg of y = Rw y_parent + S x_sib), as in
+// tree_down_pair's load_task.
+template <int KT>
+__device__ __forceinline__ void down_load_task(double2 (&aR)[KT / 8][1], double2 (&aS)[KT / 8][1], const double* S,
+                                               const double* Rw, int bt, int rg, int lane) {
+  const int i = lane >> 2, jj = lane & 3;
+  const double* bR = Rw + (int64_t)(rg * 8 + i) * KT + 2 * jj;
+  const double* bS = bt ? S + (int64_t)(2 * jj) * KT + rg * 8 + i : S + (int64_t)(rg * 8 + i) * KT + 2 * jj;
+#pragma unroll
+  for (int q2 = 0; q2 < KT / 8; ++q2) {
+    aR[q2][0] = ldg_stream2(bR + 8 * q2);
+    aS[q2][0] = bt ? make_double2(ldg_stream(bS + (int64_t)8 * q2 * KT), ldg_stream(bS + (int64_t)(8 * q2 + 1) * KT))
+                   : ldg_stream2(bS + 8 * q2);
+  }
+}
+// One down task: rows 8 rg .. 8 rg + 7, columns c0 .. c0 + 8 NT - 1 of
+// y = Rw y_parent + S x_sib from the staged blocks Zy, Zx (row stride zs);
+// written to yo (row stride ldo, columns < lim).
+template <int KT, int NT>
+__device__ __forceinline__ void down_task(const double2 (&aR)[KT / 8][1], const double2 (&aS)[KT / 8][1],
+                                          const double* Zx, const double* Zy, int zs, double* yo, int64_t ldo, int lim,
+                                          int rg, int c0, int lane) {
+  constexpr int NQ = KT / 8;
+  const int i = lane >> 2, jj = lane & 3;
+  double acc[1][NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
+  bool colok[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
+  rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
+  rm_group<1, NT, false, false, NQ>(acc, aS, Zx + c0, zs, 0, NQ, colok, lane);
+  double* y = yo + (int64_t)(8 * rg + i) * ldo;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = c0 + nt * 8 + 2 * jj;
+    if (c + 1 < lim) {
+      y[c] = acc[0][nt][0];
+      y[c + 1] = acc[0][nt][1];
+    } else if (c < lim) {
+      y[c] = acc[0][nt][0];
+    }
+  }
+}
+
+// Two downsweep levels in one launch (l >= 2): CTA = the level-(l-1) node q.
+// Stages x_l[2q..2q+1], y_{l-1}[q] and the four grandchildren x_{l+1}[4q..4q+3]
+// at once; phase A (4 warps per node) forms y_l[2q + nd] = R_{l-1,q}[nd] y_{l-1}[q]
+// + S_nd x_l[2q+1-nd] in shared memory only; phase B (2 warps per node) forms
+// y_{l+1}[4q + c] from it and writes them. y_l never goes to HBM: one write +
+// one re-read of the level's blocks saved. Used for up to 16 columns (NT <= 2):
+// config 4 at nrhs 8 / 16, down levels 11..14: 119 / 176 -> 103 / 135 us. At 32
+// columns (78 KB staged, 2 CTAs per SM) levels 14 + 15 took 345 us against
+// 108 + 209 us as two pair launches, and 16-column windows (generators read
+// twice) 484 vs 472 us for levels 11..15: nrhs 32 keeps the pair launches.
+__host__ __device__ constexpr int64_t tree_down_two_doubles(int kt, int m, int nt) {
+  return 9ll * kt * tree_down_stride(tree_mpad(m, nt));
+}
+template <int KT, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) hss_down_two_kernel(const TreeParams P, int l) {
+  extern __shared__ double sm[];
+  constexpr int RGS = KT / 8, NQ = KT / 8;
+  const int m = P.m, mp = tree_mpad(m, NT), zs = tree_down_stride(mp);
+  const int64_t km = (int64_t)KT * m;
+  const int64_t q = blockIdx.x;
+  const int blk = KT * zs;
+  double* Xl = sm;            // x_l[2q], x_l[2q+1]
+  double* Yp = sm + 2 * blk;  // y_{l-1}[q]
+  double* Yl = sm + 3 * blk;  // y_l[2q], y_l[2q+1]
+  double* Xc = sm + 5 * blk;  // x_{l+1}[4q .. 4q+3]
+  stage_rows_async(Xl, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
+  stage_rows_async(Yp, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  stage_rows_async(Xc, zs, P.xh + ((1ll << (l + 1)) - 2 + 4 * q) * km, m, 4 * KT, m, mp);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nck = mp / (NT * 8), ntask = RGS * nck;
+  double2 aR[NQ][1], aS[NQ][1];
+  {  // phase A: level l
+    const int nd = w >> 2, sub = w & 3;
+    const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + (P.bt ? 1 - nd : nd)) * KT * KT;
+    const double* Rw = P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT;
+    if (sub < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, sub % RGS, lane);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int t = sub; t < ntask; t += 4) {
+      down_task<KT, NT>(aR, aS, Xl + (1 - nd) * blk, Yp, zs, Yl + nd * blk, zs, mp, t % RGS, (t / RGS) * NT * 8, lane);
+      if (t + 4 < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, (t + 4) % RGS, lane);
+    }
+  }
+  {  // phase B: level l + 1, node 4q + nd4 under the level-l node 2q + pp
+    const int nd4 = w >> 1, sub = w & 1, pp = nd4 >> 1, nd = nd4 & 1;
+    const int64_t qq = 2 * q + pp;
+    const double* S = P.B + (((1ll << l) - 1 + qq) * 2 + (P.bt ? 1 - nd : nd)) * KT * KT;
+    const double* Rw = P.R + (((1ll << l) - 2 + qq) * 2 * KT + nd * KT) * KT;
+    if (sub < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, sub % RGS, lane);
+    __syncthreads();  // y_l complete
+    double* yo = P.yh + ((1ll << (l + 1)) - 2 + 4 * q + nd4) * km;
+    for (int t = sub; t < ntask; t += 2) {
+      down_task<KT, NT>(aR, aS, Xc + (nd4 ^ 1) * blk, Yl + pp * blk, zs, yo, m, m, t % RGS, (t / RGS) * NT * 8, lane);
+      if (t + 2 < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, (t + 2) % RGS, lane);
+    }
+  }
+}
+
 // Levels [lo, hi] of both sweeps in one cooperative launch: up l = hi-1 .. lo
 // (reading x_{l+1}), then down l = lo' .. hi where lo' = lo for the down pass
 // (down starts at level 1 when lo == 1). Grid barrier between levels.

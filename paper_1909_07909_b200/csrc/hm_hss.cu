@@ -104,6 +104,9 @@ constexpr int64_t kTreeBigLevel = HM_TREE_BIG_LEVEL;
 #ifndef HM_TREE_DOWN2
 #define HM_TREE_DOWN2 1  // two big downsweep levels per launch (hss_down_two_kernel)
 #endif
+#ifndef HM_TREE_DOWN2_NT4
+#define HM_TREE_DOWN2_NT4 1
+#endif
 #ifndef HM_TREE_DOWN2_MINB
 #define HM_TREE_DOWN2_MINB 3  // measured: 2 -> 3 CTAs per SM, config 4 nrhs 16 down levels 153 -> 135 us
 #endif
@@ -303,18 +306,26 @@ hm_status tree_launch(const hm::TreeParams& tp, int p, bool up, bool down, cudaS
     if (st == HM_OK && e != cudaSuccess) return fail(HM_ERR_CUDA, "hss_tree_sweep: %s", cudaGetErrorString(e));
     if (st) return st;
   }
-  // downsweep: big levels lbig .. p one launch each, or, up to 16 columns, two
-  // per launch (hss_down_two, pairs ending at down_last; 3 CTAs per SM, KT = 64
-  // at 2: 3 would spill)
+  // downsweep: big levels lbig .. p one launch each, or two per launch
+  // (hss_down_two, pairs ending at down_last): up to 16 columns with 9 staged
+  // blocks, 32 columns (one phase-A task per warp) with y_l over x_l (7 blocks);
+  // 3 CTAs per SM (KT = 64: 2, 3 would spill)
   constexpr int MINB2 = KT >= 64 ? 2 : HM_TREE_DOWN2_MINB;
-  const size_t smem_two = sizeof(double) * (size_t)hm::tree_down_two_doubles(KT, tp.m, NT);
-  const bool two_ok = HM_TREE_DOWN2 && NT <= 2 && smem_two <= 110 * 1024;
-  if (two_ok) allow_smem(hm::hss_down_two_kernel<KT, NT, MINB2>, smem_two);
+  const int ntask_a = (KT / 8) * (hm::tree_mpad(tp.m, NT) / (NT * 8));
+  const bool alias = NT == 4 && ntask_a <= 4;
+  const size_t smem_two = sizeof(double) * (size_t)hm::tree_down_two_doubles(KT, tp.m, NT, alias);
+  const bool two_ok = HM_TREE_DOWN2 && (NT <= 2 || (alias && HM_TREE_DOWN2_NT4)) && smem_two <= 110 * 1024;
+  if (two_ok) {
+    if (alias) allow_smem(hm::hss_down_two_kernel<KT, NT, MINB2, true>, smem_two);
+    else allow_smem(hm::hss_down_two_kernel<KT, NT, MINB2, false>, smem_two);
+  }
   for (int l = std::max(lbig, 1); down && l <= down_last; ++l) {
     const unsigned pairs = (unsigned)(1ll << (l - 1));
     if (two_ok && l >= 2 && l + 1 <= down_last && (down_last - l + 1) % 2 == 0) {
-      st = launch(HM_NT_NAME("hss_down_two"), s,
-                  [&] { hm::hss_down_two_kernel<KT, NT, MINB2><<<pairs, 256, smem_two, s>>>(tp, l); });
+      st = launch(HM_NT_NAME("hss_down_two"), s, [&] {
+        if (alias) hm::hss_down_two_kernel<KT, NT, MINB2, true><<<pairs, 256, smem_two, s>>>(tp, l);
+        else hm::hss_down_two_kernel<KT, NT, MINB2, false><<<pairs, 256, smem_two, s>>>(tp, l);
+      });
       if (st) return st;
       ++l;
       continue;

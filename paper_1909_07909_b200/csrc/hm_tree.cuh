@@ -221,15 +221,13 @@ __device__ __forceinline__ void down_load_task(double2 (&aR)[KT / 8][1], double2
   }
 }
 // One down task: rows 8 rg .. 8 rg + 7, columns c0 .. c0 + 8 NT - 1 of
-// y = Rw y_parent + S x_sib from the staged blocks Zy, Zx (row stride zs);
-// written to yo (row stride ldo, columns < lim).
+// y = Rw y_parent + S x_sib from the staged blocks Zy, Zx (row stride zs), into
+// registers (down_task_acc), then stored to yo (row stride ldo, columns < lim).
 template <int KT, int NT>
-__device__ __forceinline__ void down_task(const double2 (&aR)[KT / 8][1], const double2 (&aS)[KT / 8][1],
-                                          const double* Zx, const double* Zy, int zs, double* yo, int64_t ldo, int lim,
-                                          int rg, int c0, int lane) {
+__device__ __forceinline__ void down_task_acc(double (&acc)[1][NT][2], const double2 (&aR)[KT / 8][1],
+                                              const double2 (&aS)[KT / 8][1], const double* Zx, const double* Zy,
+                                              int zs, int c0, int lane) {
   constexpr int NQ = KT / 8;
-  const int i = lane >> 2, jj = lane & 3;
-  double acc[1][NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[0][nt][0] = acc[0][nt][1] = 0.0;
   bool colok[NT];
@@ -237,6 +235,11 @@ __device__ __forceinline__ void down_task(const double2 (&aR)[KT / 8][1], const 
   for (int nt = 0; nt < NT; ++nt) colok[nt] = true;
   rm_group<1, NT, false, false, NQ>(acc, aR, Zy + c0, zs, 0, NQ, colok, lane);
   rm_group<1, NT, false, false, NQ>(acc, aS, Zx + c0, zs, 0, NQ, colok, lane);
+}
+template <int NT>
+__device__ __forceinline__ void down_store(const double (&acc)[1][NT][2], double* yo, int64_t ldo, int lim, int rg,
+                                           int c0, int lane) {
+  const int i = lane >> 2, jj = lane & 3;
   double* y = yo + (int64_t)(8 * rg + i) * ldo;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
@@ -249,21 +252,33 @@ __device__ __forceinline__ void down_task(const double2 (&aR)[KT / 8][1], const 
     }
   }
 }
+template <int KT, int NT>
+__device__ __forceinline__ void down_task(const double2 (&aR)[KT / 8][1], const double2 (&aS)[KT / 8][1],
+                                          const double* Zx, const double* Zy, int zs, double* yo, int64_t ldo, int lim,
+                                          int rg, int c0, int lane) {
+  double acc[1][NT][2];
+  down_task_acc<KT, NT>(acc, aR, aS, Zx, Zy, zs, c0, lane);
+  down_store<NT>(acc, yo, ldo, lim, rg, c0, lane);
+}
 
 // Two downsweep levels in one launch (l >= 2): CTA = the level-(l-1) node q.
 // Stages x_l[2q..2q+1], y_{l-1}[q] and the four grandchildren x_{l+1}[4q..4q+3]
 // at once; phase A (4 warps per node) forms y_l[2q + nd] = R_{l-1,q}[nd] y_{l-1}[q]
 // + S_nd x_l[2q+1-nd] in shared memory only; phase B (2 warps per node) forms
 // y_{l+1}[4q + c] from it and writes them. y_l never goes to HBM: one write +
-// one re-read of the level's blocks saved. Used for up to 16 columns (NT <= 2):
-// config 4 at nrhs 8 / 16, down levels 11..14: 119 / 176 -> 103 / 135 us. At 32
-// columns (78 KB staged, 2 CTAs per SM) levels 14 + 15 took 345 us against
-// 108 + 209 us as two pair launches, and 16-column windows (generators read
-// twice) 484 vs 472 us for levels 11..15: nrhs 32 keeps the pair launches.
-__host__ __device__ constexpr int64_t tree_down_two_doubles(int kt, int m, int nt) {
-  return 9ll * kt * tree_down_stride(tree_mpad(m, nt));
+// one re-read of the level's blocks saved. Config 4, down levels 11..14 at
+// nrhs 8 / 16: 119 / 176 -> 103 / 135 us; 11..15 at nrhs 32 (ALIAS layout,
+// 3 CTAs per SM): 470 -> 420-430 us. (The 9-block layout at 32 columns, 78 KB
+// per CTA and 2 CTAs per SM, took 345 us for levels 14 + 15 against 108 + 209 us
+// as two pair launches; 16-column windows that re-read the generators 484 us.)
+__host__ __device__ constexpr int64_t tree_down_two_doubles(int kt, int m, int nt, bool alias = false) {
+  return (alias ? 7ll : 9ll) * kt * tree_down_stride(tree_mpad(m, nt));
 }
-template <int KT, int NT, int MINB>
+// ALIAS (every warp has at most one phase-A task): y_l is written over the
+// staged x_l pair after a barrier — 7 blocks instead of 9, so 3 CTAs per SM fit
+// at k = 32 with 32 columns. The grandchildren's x_{l+1} are a second cp.async
+// group, still landing while phase A computes.
+template <int KT, int NT, int MINB, bool ALIAS>
 __global__ void __launch_bounds__(256, MINB) hss_down_two_kernel(const TreeParams P, int l) {
   extern __shared__ double sm[];
   constexpr int RGS = KT / 8, NQ = KT / 8;
@@ -271,13 +286,15 @@ __global__ void __launch_bounds__(256, MINB) hss_down_two_kernel(const TreeParam
   const int64_t km = (int64_t)KT * m;
   const int64_t q = blockIdx.x;
   const int blk = KT * zs;
-  double* Xl = sm;            // x_l[2q], x_l[2q+1]
-  double* Yp = sm + 2 * blk;  // y_{l-1}[q]
-  double* Yl = sm + 3 * blk;  // y_l[2q], y_l[2q+1]
-  double* Xc = sm + 5 * blk;  // x_{l+1}[4q .. 4q+3]
+  double* Xl = sm;                                // x_l[2q], x_l[2q+1]
+  double* Yp = sm + 2 * blk;                      // y_{l-1}[q]
+  double* Yl = ALIAS ? sm : sm + 3 * blk;         // y_l[2q], y_l[2q+1]
+  double* Xc = sm + (ALIAS ? 3 : 5) * blk;        // x_{l+1}[4q .. 4q+3]
   stage_rows_async(Xl, zs, P.xh + ((1ll << l) - 2 + 2 * q) * km, m, 2 * KT, m, mp);
   stage_rows_async(Yp, zs, P.yh + ((1ll << (l - 1)) - 2 + q) * km, m, KT, m, mp);
+  cp_async_commit_group();
   stage_rows_async(Xc, zs, P.xh + ((1ll << (l + 1)) - 2 + 4 * q) * km, m, 4 * KT, m, mp);
+  cp_async_commit_group();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nck = mp / (NT * 8), ntask = RGS * nck;
   double2 aR[NQ][1], aS[NQ][1];
@@ -286,13 +303,23 @@ __global__ void __launch_bounds__(256, MINB) hss_down_two_kernel(const TreeParam
     const double* S = P.B + (((1ll << (l - 1)) - 1 + q) * 2 + (P.bt ? 1 - nd : nd)) * KT * KT;
     const double* Rw = P.R + (((1ll << (l - 1)) - 2 + q) * 2 * KT + nd * KT) * KT;
     if (sub < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, sub % RGS, lane);
-    cp_async_wait_all();
-    __syncthreads();
-    for (int t = sub; t < ntask; t += 4) {
-      down_task<KT, NT>(aR, aS, Xl + (1 - nd) * blk, Yp, zs, Yl + nd * blk, zs, mp, t % RGS, (t / RGS) * NT * 8, lane);
-      if (t + 4 < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, (t + 4) % RGS, lane);
+    cp_async_wait_groups<1>();  // x_l, y_{l-1} landed (this thread's copies) ...
+    __syncthreads();            // ... and everyone's
+    if constexpr (ALIAS) {
+      double acc[1][NT][2];
+      const bool has = sub < ntask;
+      if (has) down_task_acc<KT, NT>(acc, aR, aS, Xl + (1 - nd) * blk, Yp, zs, (sub / RGS) * NT * 8, lane);
+      __syncthreads();  // every read of x_l / y_{l-1} done: y_l overwrites x_l
+      if (has) down_store<NT>(acc, Yl + nd * blk, zs, mp, sub % RGS, (sub / RGS) * NT * 8, lane);
+    } else {
+      for (int t = sub; t < ntask; t += 4) {
+        down_task<KT, NT>(aR, aS, Xl + (1 - nd) * blk, Yp, zs, Yl + nd * blk, zs, mp, t % RGS, (t / RGS) * NT * 8,
+                          lane);
+        if (t + 4 < ntask) down_load_task<KT>(aR, aS, S, Rw, P.bt, (t + 4) % RGS, lane);
+      }
     }
   }
+  cp_async_wait_groups<0>();  // x_{l+1} landed
   {  // phase B: level l + 1, node 4q + nd4 under the level-l node 2q + pp
     const int nd4 = w >> 1, sub = w & 1, pp = nd4 >> 1, nd = nd4 & 1;
     const int64_t qq = 2 * q + pp;

@@ -114,11 +114,12 @@ def config4(hm):
 # nrhs 32: vt_batched + pair launches on levels 14..11)
 C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
            8: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_two<nt1>", "hss_tree_flow<nt1>", "leaf_mma_down"},
-           32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_tree_flow<nt4>", "leaf_mma"}}
+           32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_down_two<nt4>", "hss_tree_flow<nt4>",
+                "leaf_mma"}}
 # (forward product at nrhs <= 16: the leaf level's coupling + downsweep inside the leaf
 # pass, leaf_mma_down; the adjoint and nrhs 32 keep the separate level-p launch.
-# Up to 16 columns the big downsweep levels run two per launch, hss_down_two,
-# pairs ending at the last level: nrhs 8 forward 11-12 | 13-14)
+# The big downsweep levels run two per launch, hss_down_two, pairs ending at the
+# last level: nrhs 8 forward 11-12 | 13-14, nrhs 32 11 | 12-13 | 14-15)
 
 
 @pytest.mark.parametrize("op", ["A", "At"])
@@ -164,8 +165,9 @@ def deep_tree_kernels(k, m):
     # the small levels (1..10) in the dataflow launch, unless its shared memory does
     # not fit (k = 64 with 32 columns: the cooperative sweep)
     top = f"hss_tree_sweep<{nt}>" if (k == 64 and m > 16) else f"hss_tree_flow<{nt}>"
-    # big downsweep levels two per launch (hss_down_two) up to 16 columns
-    return up | {f"hss_down_two<{nt}>" if m <= 16 else f"hss_down_pair<{nt}>", top}
+    # big downsweep levels two per launch (hss_down_two), except k = 64 with 32
+    # columns (8 phase-A tasks: neither layout leaves 2+ CTAs per SM)
+    return up | {f"hss_down_pair<{nt}>" if (k == 64 and m > 16) else f"hss_down_two<{nt}>", top}
 
 
 @pytest.mark.parametrize("op", ["A", "At"])

@@ -20,6 +20,13 @@ namespace hmi {
 #define HM_TREE_GEMV_MAXM 1  // m = 2..4: the DMMA tree levels measured faster (C4 m=2: 490 vs 560 us)
 #endif
 constexpr int kTreeGemvMaxM = HM_TREE_GEMV_MAXM;
+// One right-hand side on a deep tree: the DMMA path on one padded 8-column
+// tile beats the GEMV kernels (config 4, kbench c4m2 vs c4m1: 1312 vs 1467 us;
+// the warp-per-node down levels stream R, B at 3.7 TB/s, the dataflow launch
+// halves the small levels). Trees shallower than this keep the GEMV path. 0: off.
+#ifndef HM_M1_MMA_MINP
+#define HM_M1_MMA_MINP 13
+#endif
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
   if (nrhs < 1) return fail(HM_ERR_INVALID_ARG, "nrhs = %d < 1", nrhs);
@@ -29,12 +36,15 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
   P->n = n; P->b = b; P->p = p; P->q = q; P->m = nrhs; P->k = k;
   const bool coupled = (k > 0 && p + q > 0);
   const bool leaf_coupled = (k > 0 && (p > 0 || q > 0));
+  const bool m1_mma = HM_M1_MMA_MINP > 0 && nrhs == 1 && coupled && p >= HM_M1_MMA_MINP &&
+                      (b == 64 || b == 128 || b == 256) && pow2_rank(k, 16, 64);
+  const bool wide = nrhs >= 2 || m1_mma;  // the DMMA kernels (8-column tiles, masked)
   if (!coupled) {
     P->vt = VtPath::kNone;
-  } else if (nrhs == 1 && p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
+  } else if (!wide && p >= 3 && b % 64 == 0 && b <= 4096 && pow2_rank(k, 1, 64)) {
     P->vt = VtPath::kGemv;
     P->tile = 8 * b;
-  } else if (nrhs >= 2 && b % 4 == 0 && pow2_rank(k, 16, 64)) {
+  } else if (wide && b % 4 == 0 && pow2_rank(k, 16, 64)) {
     P->vt = VtPath::kMma;  // batched: warps per leaf
     P->nt_vt = nt_for(nrhs, HM_VTB_NTMAX);
   } else {
@@ -42,13 +52,13 @@ hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int
     P->mc_vt = vt_mc(b, nrhs);
     P->tile = pick_tile(b, p, P->mc_vt);
   }
-  P->mma_levels = coupled && nrhs >= 2 && pow2_rank(k, 16, 64);
-  P->gemv_levels = coupled && nrhs <= kTreeGemvMaxM && pow2_rank(k, 16, 64);
+  P->mma_levels = coupled && wide && pow2_rank(k, 16, 64);
+  P->gemv_levels = coupled && !m1_mma && nrhs <= kTreeGemvMaxM && pow2_rank(k, 16, 64);
   if (P->mma_levels) P->nt_down = nt_for(nrhs, HM_TREE_NTMAX);
   const int ktot = leaf_coupled ? k : 0;
-  if (nrhs == 1 && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
+  if (!wide && b % 64 == 0 && b <= 1024 && (ktot == 0 || pow2_rank(ktot, 1, 64))) {
     P->leaf = LeafPath::kGemv;
-  } else if (nrhs >= 2 && (b == 64 || b == 128 || b == 256) && ktot % 8 == 0) {
+  } else if (wide && (b == 64 || b == 128 || b == 256) && ktot % 8 == 0) {
     P->leaf = LeafPath::kMma;
     P->nt_leaf = nt_for(nrhs, b == 256 ? 2 : 4);
     if ((b + ktot) * (8 * P->nt_leaf + 4) > kSmemBudgetDoubles) P->leaf = LeafPath::kGeneric;
@@ -423,7 +433,7 @@ hm_status hss_single_vt(const HssPlan& P, const double* A, const double* Z, int6
 #define HM_VT_UP 1
 #endif
 bool vt_up_ok(const HssPlan& P) {
-  return HM_VT_UP && P.vt == VtPath::kMma && (P.k == 16 || P.k == 32) && P.m >= 2 && P.m <= 16 && P.p >= 4 &&
+  return HM_VT_UP && P.vt == VtPath::kMma && (P.k == 16 || P.k == 32) && P.m <= 16 && P.p >= 4 &&
          P.b % 4 == 0;
 }
 

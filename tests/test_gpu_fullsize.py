@@ -109,10 +109,11 @@ def config4(hm):
 
 
 # tree-kernel instances each nrhs selects at k = 32, p = 15 (big levels >= 2^11 nodes
-# run one launch per level, GEMV levels >= 2^13 nodes at nrhs = 1)
+# run one launch per level; nrhs = 1 on a tree of depth >= 13 with a 64 / 128 / 256
+# leaf runs the DMMA kernels on one masked 8-column tile, HM_M1_MMA_MINP)
 # (nrhs 8: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch;
 # nrhs 32: vt_batched + pair launches on levels 14..11)
-C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"},
+C4_TREE = {1: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_two<nt1>", "hss_tree_flow<nt1>", "leaf_mma_down"},
            8: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_two<nt1>", "hss_tree_flow<nt1>", "leaf_mma_down"},
            32: {"vt_batched", "hss_up_stage<nt4>", "hss_down_pair<nt4>", "hss_down_two<nt4>", "hss_tree_flow<nt4>",
                 "leaf_mma"}}
@@ -126,7 +127,7 @@ C4_TREE = {1: {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"
 @pytest.mark.parametrize("m", [1, 8, 32])
 def test_config4_whole_y(hm, config4, m, op):
     """Config 4 (HSS n = 2^22, leaf 128, 15 levels, k = 32), nrhs 32 (BASELINE) and 1, 8
-    (the GEMV and NT = 1 tree kernels): all 2^22 rows."""
+    (the NT = 1 tree kernels; nrhs 1 as one masked column tile): all 2^22 rows."""
     cfg, s, g = config4
     X = hm_inputs.rhs(cfg.n, m, cid=4)
     Xd = dev(X)
@@ -150,11 +151,10 @@ def deep_hss(hm, request):
 
 
 def deep_tree_kernels(k, m):
-    """Tree-kernel instances of the p = 14 tree: GEMV levels at nrhs 1; at nrhs >= 2
-    k = 16 / 32 fuse Step 1 with upsweep levels 13..11 (hss_vt_up, the rest in the
-    sweep), k = 64 runs vt_batched and the staged up kernel on levels 13..11."""
-    if m == 1:
-        return {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"}
+    """Tree-kernel instances of the p = 14 tree (nrhs 1 runs the nrhs-2 kernels on one
+    masked column tile: depth >= 13, leaf 64): k = 16 / 32 fuse Step 1 with upsweep
+    levels 13..11 (hss_vt_up, the rest in the sweep), k = 64 runs vt_batched and the
+    staged up kernel on levels 13..11."""
     nt = "nt1" if m <= 8 else ("nt2" if m <= 16 else "nt4")
     if k in (16, 32) and m <= 16:
         up = {"hss_vt_up"}
@@ -173,9 +173,9 @@ def deep_tree_kernels(k, m):
 @pytest.mark.parametrize("op", ["A", "At"])
 @pytest.mark.parametrize("m", [1, 2, 8, 16, 32])
 def test_deep_hss_whole_y(hm, deep_hss, m, op):
-    """p = 14 (n = 2^20, leaf 64), k in {16, 32, 64}, nrhs in {1, 2, 8, 16}: the GEMV tree
-    kernels (nrhs 1), the fused Step-1 + upsweep kernel and the DMMA pair kernels with 1
-    and 2 column tiles, every row."""
+    """p = 14 (n = 2^20, leaf 64), k in {16, 32, 64}, nrhs in {1, 2, 8, 16, 32}: the fused
+    Step-1 + upsweep kernel and the DMMA pair kernels with 1, 2 and 4 column tiles (nrhs 1
+    as one masked tile), every row."""
     n, p, k, s, g = deep_hss
     X = hm_inputs.rhs(n, m, cid=40 + m)
     Xd = dev(X)
@@ -186,6 +186,24 @@ def test_deep_hss_whole_y(hm, deep_hss, m, op):
     ref = oracle.hss_matvec if op == "A" else oracle.hss_matvec_t
     Yr = ref(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
     assert relerr(Y.cpu().numpy(), Yr) <= TOL
+
+
+@pytest.mark.parametrize("k", [16, 32, 64])
+def test_deep_hss_gemv_levels(hm, k):
+    """nrhs 1 on a deep tree whose leaf size (192) the DMMA leaf pass does not take:
+    the warp-per-node GEMV tree kernels, one launch per level from 2^13 nodes down
+    (hss_up_gemv / hss_down_gemv) and the cooperative sweep above; A and A^T, every row."""
+    n, p = 192 << 14, 14
+    s = hm_inputs.hss_random(n, p, k, cid=80 + k)
+    g = [dev(a) for a in (s.D, s.U, s.V, s.R, s.W, s.B)]
+    X = hm_inputs.rhs(n, 1, cid=81)
+    Xd = dev(X)
+    for fn, ref in ((hm.hss_matvec, oracle.hss_matvec), (hm.hss_matvec_t, oracle.hss_matvec_t)):
+        Y, names = traced(hm, lambda: fn(n, p, 192, k, *g, Xd))
+        want = {"hss_up_gemv<m1>", "hss_down_gemv<m1>", "hss_tree_gemv_sweep<m1>"}
+        assert want <= names, (want, names)
+        Yr = ref(n, p, k, s.D, s.U, s.V, s.R, s.W, s.B, X)
+        assert relerr(Y.cpu().numpy(), Yr) <= TOL
 
 
 @pytest.mark.parametrize("m", [2, 32])

@@ -1,6 +1,6 @@
 """Per-kernel timing of single configs (development tool, not the bench contract).
 
-    python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 c4m1 c4m8 [--reps N]
+    python tools/kbench.py c5 c4 c3m1 c3m8 c3m64 c2 c1 c4m1 c4m8 hs:20:14:32:1 [--reps N]
 
 A trailing "t" (c5t, c4t, c3m8t, ...) times the adjoint product A^T X instead.
 
@@ -77,6 +77,17 @@ def run(name, reps):
         f = lambda: mv(cfg.n, cfg.levels, cfg.leaf, h.ranks, h.D, h.U, h.V, X, Y, ws)
         nbytes = hodlr_bytes(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
         flops = hodlr_flops(cfg.n, cfg.leaf, cfg.levels, cfg.k, m)
+    elif name.startswith("hs:"):  # hs:<log2 n>:<levels>:<k>:<nrhs> — any uniform HSS tree (leaf = n >> levels)
+        ln, p_, k_, m = (int(v) for v in name.split(":")[1:])
+        n_, b_ = 1 << ln, (1 << ln) >> p_
+        s = hm_inputs.device_hss_random(n_, p_, k_, 7, dev)
+        X = torch.randn(n_, m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        ws = torch.empty(hm.hm_hss_workspace_bytes(n_, p_, b_, k_, m), dtype=torch.uint8, device=dev)
+        mv = hm.hss_matvec_t if adj else hm.hss_matvec
+        f = lambda: mv(n_, p_, b_, k_, s.D, s.U, s.V, s.R, s.W, s.B, X, Y, ws)
+        nbytes = hss_bytes(n_, b_, p_, k_, m)
+        flops = hss_flops(n_, b_, p_, k_, m)
     else:
         cfg = hm_inputs.CONFIGS[{"c2": 2, "c4": 4}[name[:2]]]
         m = int(name[3:]) if name[2:3] == "m" else cfg.nrhs[0]  # c4m8: config 4 with 8 columns

@@ -20,12 +20,15 @@ namespace hmi {
 #define HM_TREE_GEMV_MAXM 1  // m = 2..4: the DMMA tree levels measured faster (C4 m=2: 490 vs 560 us)
 #endif
 constexpr int kTreeGemvMaxM = HM_TREE_GEMV_MAXM;
-// One right-hand side on a deep tree: the DMMA path on one padded 8-column
-// tile beats the GEMV kernels (config 4, kbench c4m2 vs c4m1: 1312 vs 1467 us;
-// the warp-per-node down levels stream R, B at 3.7 TB/s, the dataflow launch
-// halves the small levels). Trees shallower than this keep the GEMV path. 0: off.
+// One right-hand side (leaf 64 / 128 / 256, k in {16, 32, 64}): the DMMA path on
+// one padded 8-column tile beats the GEMV kernels at every depth measured
+// (tools/kbench.py hs:..., GEMV vs DMMA path: config 4 1461 vs 1295 us; p = 14
+// leaf 64 k 16 / 32 / 64: 461 / 636 / 1370 vs 296 / 412 / 968 us; p = 12: 285 vs
+// 245; p = 10: 152 vs 106; p = 8: 93 vs 59; p = 5: 37 vs 26 us — the warp-per-node
+// down levels stream R, B at 3.7 TB/s, the dataflow launch halves the small
+// levels). Minimum subtree depth for it; 0: off (the GEMV path).
 #ifndef HM_M1_MMA_MINP
-#define HM_M1_MMA_MINP 13
+#define HM_M1_MMA_MINP 1
 #endif
 
 hm_status hss_plan_ex(int64_t n, int64_t b, int32_t p, int32_t q, int32_t k, int32_t nrhs, int32_t flags, HssPlan* P) {
@@ -537,11 +540,23 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
 #ifndef HM_NO_SMALL
 #define HM_NO_SMALL 0
 #endif
+// One CTA per leaf streams its D_i alone, so the launch pays off only while the
+// leaves are few or small. Measured at nrhs 1 (tools/kbench.py hs:..., one launch vs
+// the level-by-level DMMA path): p = 8 leaf 128 / 64: 96 / 83 vs 59 / 52 us; p = 7
+// leaf 128: 61 vs 50 us, leaf 64 (k 16): 28 vs 37 us; p = 6: 46 vs 45, 39 vs 40 us;
+// p = 5: 26 vs 33 us; p <= 4: 18-30 vs 25-32 us. HM_SMALL_DEEP_ALL: the same depth
+// rule for every nrhs (default: nrhs 1 only; nrhs >= 2 up to kSmallMaxLevels).
+#ifndef HM_SMALL_DEEP_ALL
+#define HM_SMALL_DEEP_ALL 0
+#endif
 constexpr int kSmallMaxLevels = 8;  // up to 256 leaves: one CTA per leaf, all co-resident
 
 bool small_ok(const HssPlan& P) {
-  return !HM_NO_SMALL && P.q == 0 && P.mma_levels && P.p >= 1 && P.p <= kSmallMaxLevels && P.m >= 2 && P.m <= 32 &&
-         (P.b == 64 || P.b == 128);
+  if (HM_NO_SMALL || P.q != 0 || !P.mma_levels || P.p < 1 || P.p > kSmallMaxLevels || P.m > 32 ||
+      !(P.b == 64 || P.b == 128))
+    return false;
+  if (P.m == 1 || HM_SMALL_DEEP_ALL) return P.p <= 6 || (P.p == 7 && P.b == 64);
+  return true;
 }
 
 template <int KT, int NT, int RG>

@@ -120,6 +120,8 @@ def test_hodlr_dist_emulated(hm, n, b, p, k, m, P):
     (4096, 64, 6, 5, 3, 2),            # generic kernels
     (2048, 64, 5, 16, 2, 32),          # one leaf per rank
     (1024, 64, 4, 16, 4, 8),           # subtree of depth 1
+    (1 << 20, 64, 14, 32, 1, 2),       # m = 1 on a subtree of depth 13: the DMMA kernels on one masked tile
+    (1 << 20, 64, 14, 16, 1, 4),       # m = 1, subtree of depth 12: the GEMV kernels
 ])
 def test_hss_dist_emulated(hm, n, b, p, k, m, P):
     from paper_1909_07909_b200 import dist as hd

@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on -k regex:"vt_gemv_kernel|
 K4="python tools/kbench.py c4 --reps 1"
 $K4 > "$OUT/kb_c4.log" 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"vt_batched_kernel|hss_up_stage_kernel|hss_down_pair_kernel|hss_tree_flow_kernel|leaf_mma_kernel" -c 13 \
+    -k regex:"vt_batched_kernel|hss_up_stage_kernel|hss_down_pair_kernel|hss_down_two_kernel|hss_tree_flow_kernel|leaf_mma_kernel" -c 10 \
     -o "$OUT/c4" $K4 > "$OUT/ncu_c4.log" 2>&1
 
 # the .ncu-rep files are too large to bring back (gpurun returns <= 64 MiB):

@@ -40,6 +40,9 @@ def alg_bytes_c4(kind, idx):
     if kind == "down":  # idx 0..4 = levels 11..15: R and cores of the parents, x of the level, y parent, y out
         l = 11 + idx
         return (1 << (l - 1)) * 4 * kk + c4_blocks(l) + c4_blocks(l - 1) + c4_blocks(l)
+    if kind == "down2":  # idx = first level l of the fused pair (l, l+1): R and cores of both levels' parents,
+        l = idx           # x of both levels, y of level l-1 in, y of level l+1 out (y_l stays in shared memory)
+        return ((1 << (l - 1)) + (1 << l)) * 4 * kk + c4_blocks(l) + 2 * c4_blocks(l + 1) + c4_blocks(l - 1)
     if kind == "leaf":
         return 8 * (N4 * B4 + N4 * K4 + 2 * N4 * M4) + c4_blocks(P4)
     return None
@@ -93,6 +96,7 @@ def main(src, dst):
     caps = []
     for cfg, path in (("c5", "c5.raw.csv"), ("c4", "c4.raw.csv")):
         up = down = 0
+        dl = 11  # next downsweep level (config 4: pair launch on 11, then hss_down_two on 12-13 and 14-15)
         for d in read_raw(os.path.join(src, path)):
             name = d["Kernel Name"]
             if cfg == "c5":
@@ -103,9 +107,12 @@ def main(src, dst):
             elif "up_stage" in name or "up_pair" in name:
                 kind, alg = f"up level {P4 - 1 - up}", alg_bytes_c4("up", up)
                 up += 1
+            elif "down_two" in name:
+                kind, alg = f"down levels {dl}-{dl + 1} (one launch)", alg_bytes_c4("down2", dl)
+                dl += 2
             elif "down_pair" in name or "down_stage" in name:
-                kind, alg = f"down level {11 + down}", alg_bytes_c4("down", down)
-                down += 1
+                kind, alg = f"down level {dl}", alg_bytes_c4("down", dl - 11)
+                dl += 1
             elif "sweep" in name:
                 kind, alg = "sweep (levels 1..10)", None
             elif "tree_flow" in name:

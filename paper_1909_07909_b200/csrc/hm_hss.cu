@@ -541,13 +541,16 @@ hm_status hss_check_ptrs(const HssPlan& P, const double* U, const double* V, con
 #define HM_NO_SMALL 0
 #endif
 // One CTA per leaf streams its D_i alone, so the launch pays off only while the
-// leaves are few or small. Measured at nrhs 1 (tools/kbench.py hs:..., one launch vs
-// the level-by-level DMMA path): p = 8 leaf 128 / 64: 96 / 83 vs 59 / 52 us; p = 7
-// leaf 128: 61 vs 50 us, leaf 64 (k 16): 28 vs 37 us; p = 6: 46 vs 45, 39 vs 40 us;
-// p = 5: 26 vs 33 us; p <= 4: 18-30 vs 25-32 us. HM_SMALL_DEEP_ALL: the same depth
-// rule for every nrhs (default: nrhs 1 only; nrhs >= 2 up to kSmallMaxLevels).
+// leaves are few or small: depth <= 6, or 7 with 64-row leaves. Measured against
+// the level-by-level DMMA path (tools/kbench.py hs:..., k = 32, one launch vs
+// levels): p = 8 leaf 128, nrhs 1 / 2 / 8 / 16 / 32: 96 / 97 / 102 / 129 / 218 vs
+// 59 / 57 / 54 / 66 / 109 us; p = 8 leaf 64, nrhs 1 / 2: 83 / 84 vs 52 / 48 us;
+// p = 7 leaf 128, nrhs 1 / 2 / 8 / 16 / 32: 61 / 60 / 66 / 73 / 116 vs 50 / 47 /
+// 48 / 54 / 89 us; p = 7 leaf 64 (k 16, nrhs 1): 28 vs 37 us; p = 6: 46 vs 45,
+// 39 vs 40 us; p = 5: 26 vs 33 us; p <= 4: 18-30 vs 25-32 us.
+// HM_SMALL_DEEP_ALL 0: the depth rule at nrhs 1 only (nrhs >= 2 up to depth 8).
 #ifndef HM_SMALL_DEEP_ALL
-#define HM_SMALL_DEEP_ALL 0
+#define HM_SMALL_DEEP_ALL 1
 #endif
 constexpr int kSmallMaxLevels = 8;  // up to 256 leaves: one CTA per leaf, all co-resident
 

@@ -116,12 +116,12 @@ def test_hodlr_dist_emulated(hm, n, b, p, k, m, P):
 @pytest.mark.parametrize("n,b,p,k,m,P", [
     (1 << 15, 128, 8, 32, 32, 2), (1 << 15, 128, 8, 32, 32, 8), (1 << 15, 128, 8, 32, 32, 4),
     (1 << 15, 128, 8, 32, 32, 1), (8192, 64, 7, 16, 1, 1),     # one rank
-    (8192, 64, 7, 16, 1, 4),           # m = 1 kernels
+    (8192, 64, 7, 16, 1, 4),           # m = 1 (one masked DMMA column tile)
     (4096, 64, 6, 5, 3, 2),            # generic kernels
     (2048, 64, 5, 16, 2, 32),          # one leaf per rank
     (1024, 64, 4, 16, 4, 8),           # subtree of depth 1
-    (1 << 20, 64, 14, 32, 1, 2),       # m = 1 on a subtree of depth 13: the DMMA kernels on one masked tile
-    (1 << 20, 64, 14, 16, 1, 4),       # m = 1, subtree of depth 12: the GEMV kernels
+    (1 << 20, 64, 14, 32, 1, 2),       # m = 1 on deep subtrees (depth 13, 12): the DMMA kernels on one masked tile
+    (1 << 20, 64, 14, 16, 1, 4),
 ])
 def test_hss_dist_emulated(hm, n, b, p, k, m, P):
     from paper_1909_07909_b200 import dist as hd

@@ -109,8 +109,8 @@ def config4(hm):
 
 
 # tree-kernel instances each nrhs selects at k = 32, p = 15 (big levels >= 2^11 nodes
-# run one launch per level; nrhs = 1 on a tree of depth >= 13 with a 64 / 128 / 256
-# leaf runs the DMMA kernels on one masked 8-column tile, HM_M1_MMA_MINP)
+# run one launch per level; nrhs = 1 with a 64 / 128 / 256 leaf runs the DMMA kernels
+# on one masked 8-column tile, HM_M1_MMA_MINP)
 # (nrhs 8: Step 1 + upsweep levels 14..12 in hss_vt_up, level 11 as a pair launch;
 # nrhs 32: vt_batched + pair launches on levels 14..11)
 C4_TREE = {1: {"hss_vt_up", "hss_up_stage<nt1>", "hss_down_two<nt1>", "hss_tree_flow<nt1>", "leaf_mma_down"},
@@ -152,7 +152,7 @@ def deep_hss(hm, request):
 
 def deep_tree_kernels(k, m):
     """Tree-kernel instances of the p = 14 tree (nrhs 1 runs the nrhs-2 kernels on one
-    masked column tile: depth >= 13, leaf 64): k = 16 / 32 fuse Step 1 with upsweep
+    masked column tile): k = 16 / 32 fuse Step 1 with upsweep
     levels 13..11 (hss_vt_up, the rest in the sweep), k = 64 runs vt_batched and the
     staged up kernel on levels 13..11."""
     nt = "nt1" if m <= 8 else ("nt2" if m <= 16 else "nt4")

@@ -43,9 +43,11 @@ def run(name, reps):
         f = lambda: hm.hodlr_matvec_general(n, cfg.levels, c, rk, D, U, V, X, 1 if adj else 0, Y, ws)
         nbytes = 8 * (D.numel() + U.numel() + V.numel() + 2 * n * m)
         flops = 2 * m * (D.numel() + U.numel() + V.numel())
-    elif name in ("hpl", "hpn"):  # HSS with per-level / per-node ranks (the bench sweep's trees)
+    elif name.split(":")[0] in ("hpl", "hpn"):  # HSS with per-level / per-node ranks (the bench sweep's trees); hpl:1 = nrhs 1
         import numpy as np
         nr, pr, br, m = 1 << 20, 13, 128, 16
+        if ":" in name:
+            name, m = name.split(":")[0], int(name.split(":")[1])
         if name == "hpl":
             lr = [32] * 4 + [24] * 4 + [16] * 5
             hr = hm_inputs.hss_random_ranked(nr, pr, lr, cid=60)
